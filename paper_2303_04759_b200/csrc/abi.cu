@@ -1,0 +1,246 @@
+// abi.cu -- the extern "C" surface of libtcb200.so (include/tcb200.h).
+//
+// tcb_plan_create is the "compile" half of KernelCache::get (backends.hpp:340-354):
+// it validates shapes/dtypes/attrs for one dialect op and freezes a launch
+// closure; tcb_launch is Kernel::exec (backends.hpp:328-331) but asynchronous on
+// a CUDA stream.  Unknown ops / unsupported dtype combinations return
+// TCB_ERR_UNIMPLEMENTED: there is no CPU fallback anywhere in this library.
+#include <mutex>
+#include <sstream>
+
+#include "common.cuh"
+
+namespace tcb {
+
+static std::map<std::string, Builder>& builders() {
+  static std::map<std::string, Builder> m;
+  return m;
+}
+void register_builder(const char* op, Builder b) { builders()[op] = b; }
+
+static thread_local std::string g_last_error;
+
+static int set_err(int code, const std::string& m) {
+  g_last_error = m;
+  return code;
+}
+
+static Spec to_spec(const tcb_tensor& t) {
+  Spec s;
+  s.dtype = t.dtype;
+  s.rank = t.rank;
+  if (t.rank < 0 || t.rank > TCB_MAX_RANK) fail(TCB_ERR_ARG, "bad rank");
+  for (int i = 0; i < t.rank; ++i) {
+    if (t.shape[i] < 1) fail(TCB_ERR_TYPE, "tensor dimension must be >= 1");
+    s.shape[i] = t.shape[i];
+  }
+  for (int i = 0; i < t.rank; ++i)
+    if (t.stride[i] != 0) fail(TCB_ERR_UNIMPLEMENTED, "strided tensors are not supported");
+  return s;
+}
+
+static std::string spec_str(const Spec& s) {
+  std::string r = dtype_name(s.dtype);
+  r += '[';
+  for (int i = 0; i < s.rank; ++i) {
+    if (i) r += ',';
+    r += std::to_string(s.shape[i]);
+  }
+  return r + ']';
+}
+
+}  // namespace tcb
+
+struct tcb_plan_ {
+  tcb::Plan p;
+};
+
+using namespace tcb;
+
+#define TCB_TRY(body)                                   \
+  try {                                                 \
+    body;                                               \
+    return TCB_OK;                                      \
+  } catch (const tcb::Status& s) {                      \
+    return set_err(s.code, s.what());                   \
+  } catch (const std::exception& e) {                   \
+    return set_err(TCB_ERR_ARG, e.what());              \
+  }
+
+extern "C" {
+
+const char* tcb_last_error(void) { return g_last_error.c_str(); }
+
+int tcb_last_error_set(int code, const char* m) { return set_err(code, m ? m : ""); }
+
+int tcb_init(int device, uint64_t arena_bytes, void** arena_base) {
+  TCB_TRY({
+    TCB_CUDA(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    TCB_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10)
+      fail(TCB_ERR_UNIMPLEMENTED, std::string("libtcb200 targets sm_100a; device is ") + prop.name);
+    if (arena_bytes && arena_base) TCB_CUDA(cudaMalloc(arena_base, arena_bytes));
+  });
+}
+
+int tcb_free_arena(void* arena_base) { TCB_TRY(TCB_CUDA(cudaFree(arena_base))); }
+
+int tcb_plan_create(const char* dialect_op, const tcb_tensor* in, int nin, const tcb_tensor* out,
+                    int nout, const tcb_attr* attrs, int nattr, const char* closure_hash,
+                    tcb_plan* plan) {
+  TCB_TRY({
+    std::string name = dialect_op ? dialect_op : "";
+    std::string base = name;
+    if (name.rfind("b200.", 0) == 0) base = name.substr(5);
+    else if (name.find('.') != std::string::npos)
+      fail(TCB_ERR_UNIMPLEMENTED, "libtcb200 only implements the b200 dialect, got " + name);
+    auto it = builders().find(base);
+    if (it == builders().end())
+      fail(TCB_ERR_UNIMPLEMENTED, "no b200 kernel for op " + base);
+    auto* pl = new tcb_plan_();
+    Plan& p = pl->p;
+    p.op = base;
+    try {
+      for (int i = 0; i < nin; ++i) p.in.push_back(to_spec(in[i]));
+      for (int i = 0; i < nout; ++i) p.out.push_back(to_spec(out[i]));
+      std::ostringstream key;
+      key << "b200." << base << "|";
+      for (auto& s : p.in) key << spec_str(s) << ",";
+      key << "->";
+      for (auto& s : p.out) key << spec_str(s) << ",";
+      key << "|";
+      for (int i = 0; i < nattr; ++i) {
+        tcb_attr a = attrs[i];
+        p.attrs.strs.push_back(a.key ? a.key : "");
+        if (a.kind == TCB_ATTR_STR) p.attrs.strs.push_back(a.s ? a.s : "");
+      }
+      // second pass: point keys/strings at owned storage (strs no longer grows)
+      size_t si = 0;
+      for (int i = 0; i < nattr; ++i) {
+        tcb_attr a = attrs[i];
+        a.key = p.attrs.strs[si++].c_str();
+        if (a.kind == TCB_ATTR_STR) a.s = p.attrs.strs[si++].c_str();
+        p.attrs.m[a.key] = a;
+      }
+      for (auto& [k, a] : p.attrs.m) {
+        key << k << "=";
+        if (a.kind == TCB_ATTR_INT) key << a.i;
+        else if (a.kind == TCB_ATTR_FLOAT) key << a.d;
+        else key << a.s;
+        key << ";";
+      }
+      if (closure_hash) key << "|" << closure_hash;
+      p.key = key.str();
+      it->second(p);
+      if (!p.run) fail(TCB_ERR_UNIMPLEMENTED, "b200." + base + ": no kernel for this configuration");
+    } catch (...) {
+      delete pl;
+      throw;
+    }
+    *plan = pl;
+  });
+}
+
+int tcb_launch(tcb_plan plan, const tcb_tensor* in, int nin, tcb_tensor* out, int nout,
+               void* stream) {
+  TCB_TRY({
+    if (!plan) fail(TCB_ERR_ARG, "null plan");
+    Plan& p = plan->p;
+    if (nin != int(p.in.size()) || nout != int(p.out.size()))
+      fail(TCB_ERR_ARG, "b200." + p.op + ": launch arity differs from plan");
+    p.run(in, out, static_cast<cudaStream_t>(stream));
+    TCB_CUDA(cudaGetLastError());
+  });
+}
+
+void tcb_plan_destroy(tcb_plan plan) { delete plan; }
+
+int tcb_plan_num_kernels(tcb_plan plan) { return plan ? plan->p.nkernels : 0; }
+
+const char* tcb_plan_key(tcb_plan plan) { return plan ? plan->p.key.c_str() : ""; }
+
+const char* tcb_supported_ops(void) {
+  static std::string s;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    for (auto& [k, v] : builders()) {
+      if (!s.empty()) s += ' ';
+      s += k;
+    }
+  });
+  return s.c_str();
+}
+
+// ---- graphs -----------------------------------------------------------------
+int tcb_graph_capture_begin(void* stream) {
+  TCB_TRY(TCB_CUDA(
+      cudaStreamBeginCapture(static_cast<cudaStream_t>(stream), cudaStreamCaptureModeThreadLocal)));
+}
+int tcb_graph_capture_end(void* stream, void** graph_exec) {
+  TCB_TRY({
+    cudaGraph_t g;
+    TCB_CUDA(cudaStreamEndCapture(static_cast<cudaStream_t>(stream), &g));
+    cudaGraphExec_t ge;
+    TCB_CUDA(cudaGraphInstantiate(&ge, g, 0));
+    TCB_CUDA(cudaGraphDestroy(g));
+    *graph_exec = ge;
+  });
+}
+int tcb_graph_launch(void* graph_exec, void* stream) {
+  TCB_TRY(TCB_CUDA(cudaGraphLaunch(static_cast<cudaGraphExec_t>(graph_exec),
+                                   static_cast<cudaStream_t>(stream))));
+}
+int tcb_graph_destroy(void* graph_exec) {
+  TCB_TRY(TCB_CUDA(cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(graph_exec))));
+}
+
+// ---- helpers ----------------------------------------------------------------
+int tcb_memcpy(void* dst, const void* src, uint64_t bytes, int kind, void* stream) {
+  TCB_TRY({
+    cudaMemcpyKind k = kind == 0   ? cudaMemcpyHostToDevice
+                       : kind == 1 ? cudaMemcpyDeviceToHost
+                                   : cudaMemcpyDeviceToDevice;
+    TCB_CUDA(cudaMemcpyAsync(dst, src, bytes, k, static_cast<cudaStream_t>(stream)));
+  });
+}
+int tcb_memset(void* dst, int value, uint64_t bytes, void* stream) {
+  TCB_TRY(TCB_CUDA(cudaMemsetAsync(dst, value, bytes, static_cast<cudaStream_t>(stream))));
+}
+int tcb_stream_create(void** stream) {
+  TCB_TRY({
+    cudaStream_t s;
+    TCB_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    *stream = s;
+  });
+}
+int tcb_stream_destroy(void* stream) {
+  TCB_TRY(TCB_CUDA(cudaStreamDestroy(static_cast<cudaStream_t>(stream))));
+}
+int tcb_stream_sync(void* stream) {
+  TCB_TRY(TCB_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream))));
+}
+int tcb_event_create(void** ev) {
+  TCB_TRY({
+    cudaEvent_t e;
+    TCB_CUDA(cudaEventCreate(&e));
+    *ev = e;
+  });
+}
+int tcb_event_record(void* ev, void* stream) {
+  TCB_TRY(TCB_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(ev), static_cast<cudaStream_t>(stream))));
+}
+int tcb_stream_wait_event(void* stream, void* ev) {
+  TCB_TRY(TCB_CUDA(
+      cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), static_cast<cudaEvent_t>(ev), 0)));
+}
+int tcb_event_elapsed_ms(void* start, void* stop, float* ms) {
+  TCB_TRY(TCB_CUDA(
+      cudaEventElapsedTime(ms, static_cast<cudaEvent_t>(start), static_cast<cudaEvent_t>(stop))));
+}
+int tcb_event_destroy(void* ev) { TCB_TRY(TCB_CUDA(cudaEventDestroy(static_cast<cudaEvent_t>(ev)))); }
+int tcb_host_alloc(void** p, uint64_t bytes) { TCB_TRY(TCB_CUDA(cudaMallocHost(p, bytes))); }
+int tcb_host_free(void* p) { TCB_TRY(TCB_CUDA(cudaFreeHost(p))); }
+int tcb_device_sync(void) { TCB_TRY(TCB_CUDA(cudaDeviceSynchronize())); }
+
+}  // extern "C"

@@ -1,0 +1,252 @@
+// common.cuh -- shared plumbing of libtcb200 (the b200 dialect kernels).
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstring>
+#include <functional>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <cmath>
+#include <type_traits>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/tcb200.h"
+
+namespace tcb {
+
+constexpr int kNumSMs = 148;
+
+// ------------------------------------------------------------------ errors
+struct Status : std::runtime_error {
+  int code;
+  Status(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+[[noreturn]] inline void fail(int code, const std::string& m) { throw Status(code, m); }
+inline void require(bool c, const std::string& m) {
+  if (!c) fail(TCB_ERR_TYPE, m);
+}
+#define TCB_CUDA(x)                                                                   \
+  do {                                                                                \
+    cudaError_t e_ = (x);                                                             \
+    if (e_ != cudaSuccess)                                                            \
+      ::tcb::fail(TCB_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_));    \
+  } while (0)
+
+// ------------------------------------------------------------------ tensors
+struct Spec {
+  int dtype = TCB_F32;
+  int rank = 0;
+  int64_t shape[TCB_MAX_RANK] = {0};
+  int64_t numel() const {
+    int64_t n = 1;
+    for (int i = 0; i < rank; ++i) n *= shape[i];
+    return n;
+  }
+  int64_t dim(int i) const { return shape[i < 0 ? rank + i : i]; }
+};
+
+inline int dtype_bytes(int d) { return d == TCB_F32 || d == TCB_I32 ? 4 : d == TCB_U8 ? 1 : 2; }
+inline const char* dtype_name(int d) {
+  switch (d) {
+    case TCB_F32: return "f32";
+    case TCB_F16: return "f16";
+    case TCB_BF16: return "bf16";
+    case TCB_I32: return "i32";
+    case TCB_U8: return "u8";
+  }
+  return "?";
+}
+inline bool is_float(int d) { return d == TCB_F32 || d == TCB_F16 || d == TCB_BF16; }
+
+// ------------------------------------------------------------------ attrs
+struct Attrs {
+  std::map<std::string, tcb_attr> m;
+  std::vector<std::string> strs;  // storage
+  double f(const char* k, double d) const {
+    auto it = m.find(k);
+    if (it == m.end()) return d;
+    return it->second.kind == TCB_ATTR_FLOAT ? it->second.d
+           : it->second.kind == TCB_ATTR_INT ? double(it->second.i)
+                                             : d;
+  }
+  int64_t i(const char* k, int64_t d) const {
+    auto it = m.find(k);
+    if (it == m.end()) return d;
+    return it->second.kind == TCB_ATTR_INT ? it->second.i
+           : it->second.kind == TCB_ATTR_FLOAT ? int64_t(it->second.d)
+                                               : d;
+  }
+  std::string s(const char* k, const std::string& d) const {
+    auto it = m.find(k);
+    if (it == m.end() || it->second.kind != TCB_ATTR_STR || !it->second.s) return d;
+    return it->second.s;
+  }
+};
+
+// --------------------------------------------------------------- device math
+__device__ __forceinline__ float ld_f(const float* p, int64_t i) { return p[i]; }
+__device__ __forceinline__ float ld_f(const __half* p, int64_t i) { return __half2float(p[i]); }
+__device__ __forceinline__ float ld_f(const __nv_bfloat16* p, int64_t i) {
+  return __bfloat162float(p[i]);
+}
+__device__ __forceinline__ void st_f(float* p, int64_t i, float v) { p[i] = v; }
+__device__ __forceinline__ void st_f(__half* p, int64_t i, float v) { p[i] = __float2half_rn(v); }
+__device__ __forceinline__ void st_f(__nv_bfloat16* p, int64_t i, float v) {
+  p[i] = __float2bfloat16_rn(v);
+}
+template <typename T>
+__device__ __forceinline__ T from_f(float v);
+template <>
+__device__ __forceinline__ float from_f<float>(float v) { return v; }
+template <>
+__device__ __forceinline__ __half from_f<__half>(float v) { return __float2half_rn(v); }
+template <>
+__device__ __forceinline__ __nv_bfloat16 from_f<__nv_bfloat16>(float v) {
+  return __float2bfloat16_rn(v);
+}
+__device__ __forceinline__ float to_f(float v) { return v; }
+__device__ __forceinline__ float to_f(__half v) { return __half2float(v); }
+__device__ __forceinline__ float to_f(__nv_bfloat16 v) { return __bfloat162float(v); }
+
+// erf-based GELU and its derivative (match oracle.c gelu_f / gelu_grad_f)
+__device__ __forceinline__ float gelu_f(float x) {
+  return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f));
+}
+__device__ __forceinline__ float gelu_grad_f(float x) {
+  float cdf = 0.5f * (1.0f + erff(x * 0.70710678118654752f));
+  float pdf = expf(-0.5f * x * x) * 0.39894228040143268f;
+  return __fadd_rn(cdf, __fmul_rn(x, pdf));
+}
+
+enum Act { ACT_NONE = 0, ACT_RELU = 1, ACT_TANH = 2, ACT_GELU = 3 };
+inline int parse_act(const std::string& s) {
+  if (s.empty() || s == "none") return ACT_NONE;
+  if (s == "relu") return ACT_RELU;
+  if (s == "tanh") return ACT_TANH;
+  if (s == "gelu") return ACT_GELU;
+  fail(TCB_ERR_TYPE, "unknown activation '" + s + "'");
+}
+__device__ __forceinline__ float act_f(int act, float v) {
+  switch (act) {
+    case ACT_RELU: return v > 0.0f ? v : 0.0f;
+    case ACT_TANH: return tanhf(v);
+    case ACT_GELU: return gelu_f(v);
+    default: return v;
+  }
+}
+__device__ __forceinline__ float dact_f(int act, float aux) {
+  switch (act) {
+    case ACT_RELU: return aux > 0.0f ? 1.0f : 0.0f;
+    case ACT_TANH: return __fsub_rn(1.0f, __fmul_rn(aux, aux));
+    case ACT_GELU: return gelu_grad_f(aux);
+    default: return 1.0f;
+  }
+}
+
+// Philox4x32-10 keep decision, identical to oracle.c orc_dropout_keep.
+__device__ __forceinline__ void philox4x32_10(uint32_t c[4], uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    uint32_t lo0 = 0xD2511F53u * c[0];
+    uint32_t hi0 = __umulhi(0xD2511F53u, c[0]);
+    uint32_t lo1 = 0xCD9E8D57u * c[2];
+    uint32_t hi1 = __umulhi(0xCD9E8D57u, c[2]);
+    uint32_t n0 = hi1 ^ c[1] ^ k0;
+    uint32_t n2 = hi0 ^ c[3] ^ k1;
+    c[0] = n0;
+    c[1] = lo1;
+    c[2] = n2;
+    c[3] = lo0;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+}
+struct DropCfg {
+  float p = 0.0f, scale = 1.0f;
+  uint64_t seed = 0, salt = 0;
+};
+// 4 keep bits for indices (q*4 .. q*4+3)
+__device__ __forceinline__ uint32_t dropout_bits4(const DropCfg& d, uint64_t q) {
+  uint32_t c[4] = {uint32_t(q), uint32_t(d.salt), uint32_t(d.salt >> 32), 0u};
+  philox4x32_10(c, uint32_t(d.seed), uint32_t(d.seed >> 32));
+  uint32_t bits = 0;
+#pragma unroll
+  for (int w = 0; w < 4; ++w) {
+    float u = float(c[w] >> 8) * (1.0f / 16777216.0f);
+    bits |= (u >= d.p ? 1u : 0u) << w;
+  }
+  return bits;
+}
+__device__ __forceinline__ bool dropout_keep(const DropCfg& d, uint64_t idx) {
+  if (d.p <= 0.0f) return true;
+  return (dropout_bits4(d, idx >> 2) >> (idx & 3)) & 1u;
+}
+inline DropCfg drop_cfg(const Attrs& a) {
+  DropCfg d;
+  d.p = float(a.f("p", 0.0));
+  d.scale = d.p > 0.0f ? 1.0f / (1.0f - d.p) : 1.0f;
+  d.seed = uint64_t(a.i("seed", 0));
+  d.salt = uint64_t(a.i("salt", 0));
+  return d;
+}
+
+inline int grid_for(int64_t n, int block, int max_blocks = kNumSMs * 8) {
+  int64_t g = (n + block - 1) / block;
+  if (g > max_blocks) g = max_blocks;
+  if (g < 1) g = 1;
+  return int(g);
+}
+
+// dtype dispatch helper: calls f((T*)nullptr) with the storage type
+template <typename Fn>
+void dispatch_float(int dtype, Fn&& f) {
+  switch (dtype) {
+    case TCB_F32: f((float*)nullptr); return;
+    case TCB_F16: f((__half*)nullptr); return;
+    case TCB_BF16: f((__nv_bfloat16*)nullptr); return;
+  }
+  fail(TCB_ERR_TYPE, std::string("unsupported dtype ") + dtype_name(dtype));
+}
+
+// ------------------------------------------------------------------ plans
+using RunFn = std::function<void(const tcb_tensor* in, tcb_tensor* out, cudaStream_t s)>;
+
+struct Plan {
+  std::string op;  // base op
+  std::string key;
+  std::vector<Spec> in, out;
+  Attrs attrs;
+  RunFn run;
+  int nkernels = 1;
+};
+
+using Builder = void (*)(Plan&);
+void register_builder(const char* op, Builder b);
+struct AutoReg {
+  AutoReg(const char* op, Builder b) { register_builder(op, b); }
+};
+#define TCB_CAT2(a, b) a##b
+#define TCB_CAT(a, b) TCB_CAT2(a, b)
+#define TCB_REGISTER(op, fn) static ::tcb::AutoReg TCB_CAT(_tcb_reg_, __COUNTER__)(op, fn)
+
+inline void check_arity(const Plan& p, int nin_min, int nin_max, int nout_min, int nout_max) {
+  int ni = int(p.in.size()), no = int(p.out.size());
+  if (ni < nin_min || ni > nin_max || no < nout_min || no > nout_max)
+    fail(TCB_ERR_TYPE, "b200." + p.op + ": wrong number of inputs/outputs (" + std::to_string(ni) +
+                           ", " + std::to_string(no) + ")");
+}
+inline bool same_shape(const Spec& a, const Spec& b) {
+  if (a.rank != b.rank) return false;
+  for (int i = 0; i < a.rank; ++i)
+    if (a.shape[i] != b.shape[i]) return false;
+  return true;
+}
+
+}  // namespace tcb

@@ -1,0 +1,55 @@
+// gemm.cuh -- the GEMM problem description shared by the exact SIMT kernel
+// (k_gemm_exact.cu) and the tcgen05 tensor-core kernel (k_gemm_tc.cu).
+//
+// C[z](m,n) = epi( alpha * sum_k A[z](m,k) * B[z](k,n) )
+//   A[z](m,k) = ta ? A[off_a(z) + k*lda + m] : A[off_a(z) + m*lda + k]
+//   B[z](k,n) = tb ? B[off_b(z) + n*ldb + k] : B[off_b(z) + k*ldb + n]
+//   off_x(z) = (z / Z2) * x_s1 + (z % Z2) * x_s2      (two-level batch: (b, head))
+// epilogue (in this order, f32):
+//   v = alpha*acc; v += bias[n]; v *= act'(aux(m,n)); aux_out(m,n) = v; v = act(v)
+// then one round-to-nearest-even store into C's dtype.  This covers matmul
+// (backends.hpp:143-155), matmul_add_act (backends.hpp:311-324) and the
+// extension GEMMs (linear, matmul_t, matmul_dact, batch_matmul, attention).
+#pragma once
+#include "common.cuh"
+
+namespace tcb {
+
+struct GemmOperand {
+  const void* ptr = nullptr;
+  int64_t ld = 0, s1 = 0, s2 = 0;
+  int dtype = TCB_F32;
+};
+
+struct GemmArgs {
+  int64_t M = 0, N = 0, K = 0;
+  int64_t Z = 1, Z2 = 1;
+  int ta = 0, tb = 0;
+  GemmOperand a, b;
+  void* c = nullptr;
+  int64_t ldc = 0, c_s1 = 0, c_s2 = 0;
+  int c_dtype = TCB_F32;
+  float alpha = 1.0f;
+  const void* bias = nullptr;  // [N], dtype bias_dtype
+  int bias_dtype = TCB_F32;
+  int act = ACT_NONE;          // forward activation
+  int dact = ACT_NONE;         // multiply by act'(aux)
+  const void* aux = nullptr;   // same layout as C (ldc, batch strides), aux_dtype
+  int aux_dtype = TCB_F32;
+  void* aux_out = nullptr;     // pre-activation store, same layout/dtype as C
+};
+
+// Launch helpers (defined in the .cu files)
+void launch_gemm_exact(const GemmArgs& g, cudaStream_t s);
+// returns false when the tensor-core path cannot take this problem
+bool gemm_tc_supported(const GemmArgs& g, std::string* why);
+void launch_gemm_tc(const GemmArgs& g, cudaStream_t s);
+
+// Picks the kernel: tcgen05 for f16/bf16 operands unless exact is requested or
+// the shape is unsupported (then the exact SIMT kernel; never a CPU path).
+inline void launch_gemm(const GemmArgs& g, bool exact, cudaStream_t s) {
+  if (!exact && gemm_tc_supported(g, nullptr)) launch_gemm_tc(g, s);
+  else launch_gemm_exact(g, s);
+}
+
+}  // namespace tcb

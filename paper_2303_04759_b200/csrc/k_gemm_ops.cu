@@ -1,0 +1,147 @@
+// k_gemm_ops.cu -- plan builders for the GEMM-shaped ops of the b200 dialect:
+//   matmul        A[M,K].B[K,N]                        backends.hpp:143-155,215
+//   matmul_t      alpha * op(A).op(B), out dtype attr   (absorbs `transpose` and
+//                 `cast` into operand major-ness / epilogue)
+//   linear        act(x.W + bias) [, pre-activation]    matmul_add_act, backends.hpp:311-324
+//   matmul_dact   (op(A).op(B)) * act'(aux)             backward GEMM, fused dact
+//   batch_matmul  rank-3 batched matmul_t
+// f16/bf16 operands run on the tcgen05 kernel; f32 (or attr exact=1) runs the
+// exact SIMT kernel, bit-identical to the reference.
+#include "gemm.cuh"
+
+namespace tcb {
+
+static bool want_exact(const Plan& p) {
+  return p.in[0].dtype == TCB_F32 || p.attrs.i("exact", 0) != 0;
+}
+
+// Fill the static part of a 2-D GEMM: A, B are rank-2 dense row-major.
+static GemmArgs gemm2d(const Spec& A, const Spec& B, int ta, int tb, const Spec& C,
+                       const std::string& op) {
+  require(A.rank == 2 && B.rank == 2, op + ": rank-2 inputs required");
+  GemmArgs g;
+  g.ta = ta;
+  g.tb = tb;
+  g.M = ta ? A.shape[1] : A.shape[0];
+  g.K = ta ? A.shape[0] : A.shape[1];
+  int64_t kb = tb ? B.shape[1] : B.shape[0];
+  g.N = tb ? B.shape[0] : B.shape[1];
+  if (g.K != kb)
+    fail(TCB_ERR_TYPE, op + ": inner dimensions disagree");
+  require(A.dtype == B.dtype, op + ": dtype mismatch without explicit cast");
+  require(is_float(A.dtype), op + ": float operands only");
+  require(C.rank == 2 && C.shape[0] == g.M && C.shape[1] == g.N, op + ": output shape mismatch");
+  g.a.ld = A.shape[1];
+  g.b.ld = B.shape[1];
+  g.a.dtype = A.dtype;
+  g.b.dtype = B.dtype;
+  g.ldc = g.N;
+  g.c_dtype = C.dtype;
+  return g;
+}
+
+static void b_matmul(Plan& p) {
+  check_arity(p, 2, 2, 1, 1);
+  GemmArgs g = gemm2d(p.in[0], p.in[1], 0, 0, p.out[0], "matmul");
+  require(p.out[0].dtype == p.in[0].dtype, "matmul: output dtype must equal input dtype");
+  const bool exact = want_exact(p);
+  p.run = [g, exact](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) mutable {
+    g.a.ptr = in[0].ptr;
+    g.b.ptr = in[1].ptr;
+    g.c = out[0].ptr;
+    launch_gemm(g, exact, s);
+  };
+}
+TCB_REGISTER("matmul", b_matmul);
+
+static void b_matmul_t(Plan& p) {
+  check_arity(p, 2, 2, 1, 1);
+  GemmArgs g = gemm2d(p.in[0], p.in[1], int(p.attrs.i("ta", 0)), int(p.attrs.i("tb", 0)), p.out[0],
+                      "matmul_t");
+  g.alpha = float(p.attrs.f("alpha", 1.0));
+  const bool exact = want_exact(p);
+  p.run = [g, exact](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) mutable {
+    g.a.ptr = in[0].ptr;
+    g.b.ptr = in[1].ptr;
+    g.c = out[0].ptr;
+    launch_gemm(g, exact, s);
+  };
+}
+TCB_REGISTER("matmul_t", b_matmul_t);
+
+static void b_linear(Plan& p) {
+  check_arity(p, 3, 3, 1, 2);
+  GemmArgs g = gemm2d(p.in[0], p.in[1], 0, int(p.attrs.i("tw", 0)), p.out[0], "linear");
+  require(p.in[2].numel() == g.N, "linear: bias must have N elements");
+  g.bias_dtype = p.in[2].dtype;
+  g.act = parse_act(p.attrs.s("act", "none"));
+  if (p.out.size() > 1) require(same_shape(p.out[1], p.out[0]) && p.out[1].dtype == p.out[0].dtype,
+                                "linear: pre-activation output must match y");
+  const bool exact = want_exact(p);
+  const bool save = p.out.size() > 1;
+  p.run = [g, exact, save](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) mutable {
+    g.a.ptr = in[0].ptr;
+    g.b.ptr = in[1].ptr;
+    g.bias = in[2].ptr;
+    g.c = out[0].ptr;
+    g.aux_out = save ? out[1].ptr : nullptr;
+    launch_gemm(g, exact, s);
+  };
+}
+TCB_REGISTER("linear", b_linear);
+
+static void b_matmul_dact(Plan& p) {
+  check_arity(p, 3, 3, 1, 1);
+  GemmArgs g = gemm2d(p.in[0], p.in[1], int(p.attrs.i("ta", 0)), int(p.attrs.i("tb", 0)), p.out[0],
+                      "matmul_dact");
+  g.dact = parse_act(p.attrs.s("act", "none"));
+  require(same_shape(p.in[2], p.out[0]), "matmul_dact: aux must have the output's shape");
+  g.aux_dtype = p.in[2].dtype;
+  const bool exact = want_exact(p);
+  p.run = [g, exact](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) mutable {
+    g.a.ptr = in[0].ptr;
+    g.b.ptr = in[1].ptr;
+    g.aux = in[2].ptr;
+    g.c = out[0].ptr;
+    launch_gemm(g, exact, s);
+  };
+}
+TCB_REGISTER("matmul_dact", b_matmul_dact);
+
+static void b_batch_matmul(Plan& p) {
+  check_arity(p, 2, 2, 1, 1);
+  const Spec &A = p.in[0], &B = p.in[1], &C = p.out[0];
+  require(A.rank == 3 && B.rank == 3 && C.rank == 3, "batch_matmul: rank-3 inputs required");
+  require(A.shape[0] == B.shape[0] && C.shape[0] == A.shape[0], "batch_matmul: batch mismatch");
+  GemmArgs g;
+  g.ta = int(p.attrs.i("ta", 0));
+  g.tb = int(p.attrs.i("tb", 0));
+  g.M = g.ta ? A.shape[2] : A.shape[1];
+  g.K = g.ta ? A.shape[1] : A.shape[2];
+  g.N = g.tb ? B.shape[1] : B.shape[2];
+  require((g.tb ? B.shape[2] : B.shape[1]) == g.K, "batch_matmul: inner dimensions disagree");
+  require(C.shape[1] == g.M && C.shape[2] == g.N, "batch_matmul: output shape mismatch");
+  require(A.dtype == B.dtype, "batch_matmul: dtype mismatch");
+  g.Z = A.shape[0];
+  g.Z2 = 1;
+  g.a.ld = A.shape[2];
+  g.b.ld = B.shape[2];
+  g.a.s2 = A.shape[1] * A.shape[2];
+  g.b.s2 = B.shape[1] * B.shape[2];
+  g.c_s2 = g.M * g.N;
+  g.a.dtype = A.dtype;
+  g.b.dtype = B.dtype;
+  g.ldc = g.N;
+  g.c_dtype = C.dtype;
+  g.alpha = float(p.attrs.f("alpha", 1.0));
+  const bool exact = want_exact(p);
+  p.run = [g, exact](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) mutable {
+    g.a.ptr = in[0].ptr;
+    g.b.ptr = in[1].ptr;
+    g.c = out[0].ptr;
+    launch_gemm(g, exact, s);
+  };
+}
+TCB_REGISTER("batch_matmul", b_batch_matmul);
+
+}  // namespace tcb

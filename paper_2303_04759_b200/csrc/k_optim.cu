@@ -1,0 +1,130 @@
+// k_optim.cu -- fused optimizer updates over flat parameter buffers.
+//
+//  sgd_update      backends.hpp:216-221  p - lr*g (float lr, no FMA): bit-exact.
+//  adam_update     backends.hpp:222-243  per-element double math with bias
+//                  corrections 1 - beta^t (t read from the step tensor):
+//                  B200's FP64 rate makes this free next to the 28 B/param of
+//                  HBM traffic, so the update is bit-exact up to the ulp of the
+//                  device pow() in the bias corrections.
+//  adam_update_ex  the same + grad_scale (the ZeRO 1/N mean fold)
+//                  + the bf16/f16 copy of the new parameter as a 4th output
+//                  (AutoCast's param cast fused into the producer).
+// The VM lays all parameters (and grads, m, v) out as single flat segments, so
+// one launch updates the whole model -- horizontal fusion of the per-param
+// updates, i.e. a multi-tensor optimizer.
+// Updates may be in place (out ptr == in ptr): each element is read before it is
+// written by the same thread.
+#include "common.cuh"
+
+namespace tcb {
+
+__global__ void k_sgd(const float* __restrict__ p, const float* __restrict__ g, float* pn, int64_t n,
+                      float lr) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    pn[i] = __fsub_rn(p[i], __fmul_rn(lr, g[i]));
+}
+
+static void b_sgd(Plan& p) {
+  check_arity(p, 2, 2, 1, 1);
+  require(p.in[0].dtype == TCB_F32 && p.in[1].dtype == TCB_F32,
+          "sgd_update: master params/grads must be f32");
+  require(same_shape(p.in[0], p.in[1]), "sgd_update: param/grad shape mismatch");
+  const int64_t n = p.in[0].numel();
+  const float lr = float(p.attrs.f("lr", 0.0));
+  p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
+    k_sgd<<<grid_for(n, 256), 256, 0, s>>>((const float*)in[0].ptr, (const float*)in[1].ptr,
+                                            (float*)out[0].ptr, n, lr);
+  };
+}
+TCB_REGISTER("sgd_update", b_sgd);
+
+struct AdamCfg {
+  double lr, b1, b2, eps, gs;
+};
+
+template <typename TH>
+__device__ __forceinline__ void adam_elem(const AdamCfg& c, double bc1, double bc2, float p, float g,
+                                          float m, float v, float& po, float& mo, float& vo, TH* half,
+                                          int64_t i) {
+  double gd = g;
+  if (c.gs != 1.0) gd = __dmul_rn(gd, c.gs);
+  double mi = __dadd_rn(__dmul_rn(c.b1, double(m)), __dmul_rn(__dsub_rn(1.0, c.b1), gd));
+  double vi = __dadd_rn(__dmul_rn(c.b2, double(v)), __dmul_rn(__dmul_rn(__dsub_rn(1.0, c.b2), gd), gd));
+  double mhat = __ddiv_rn(mi, bc1);
+  double vhat = __ddiv_rn(vi, bc2);
+  double upd = __ddiv_rn(__dmul_rn(c.lr, mhat), __dadd_rn(__dsqrt_rn(vhat), c.eps));
+  float pn = float(__dsub_rn(double(p), upd));
+  po = pn;
+  mo = float(mi);
+  vo = float(vi);
+  if (half) half[i] = from_f<TH>(pn);
+}
+
+template <typename TH>
+__global__ void __launch_bounds__(256) k_adam(const float* __restrict__ p, const float* __restrict__ g,
+                                              const float* __restrict__ m, const float* __restrict__ v,
+                                              const float* __restrict__ step, float* po, float* mo,
+                                              float* vo, TH* half, int64_t n, AdamCfg c) {
+  const double t = double(step[0]);
+  const double bc1 = __dsub_rn(1.0, pow(c.b1, t));
+  const double bc2 = __dsub_rn(1.0, pow(c.b2, t));
+  const int64_t nv = n / 4;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < nv; q += stride) {
+    float4 P = reinterpret_cast<const float4*>(p)[q];
+    float4 G = reinterpret_cast<const float4*>(g)[q];
+    float4 M = reinterpret_cast<const float4*>(m)[q];
+    float4 V = reinterpret_cast<const float4*>(v)[q];
+    float4 PO, MO, VO;
+    adam_elem(c, bc1, bc2, P.x, G.x, M.x, V.x, PO.x, MO.x, VO.x, half, q * 4 + 0);
+    adam_elem(c, bc1, bc2, P.y, G.y, M.y, V.y, PO.y, MO.y, VO.y, half, q * 4 + 1);
+    adam_elem(c, bc1, bc2, P.z, G.z, M.z, V.z, PO.z, MO.z, VO.z, half, q * 4 + 2);
+    adam_elem(c, bc1, bc2, P.w, G.w, M.w, V.w, PO.w, MO.w, VO.w, half, q * 4 + 3);
+    reinterpret_cast<float4*>(po)[q] = PO;
+    reinterpret_cast<float4*>(mo)[q] = MO;
+    reinterpret_cast<float4*>(vo)[q] = VO;
+  }
+  for (int64_t i = nv * 4 + blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += stride)
+    adam_elem(c, bc1, bc2, p[i], g[i], m[i], v[i], po[i], mo[i], vo[i], half, i);
+}
+
+static void b_adam(Plan& p) {
+  check_arity(p, 5, 5, 3, 4);
+  for (int i = 0; i < 4; ++i) {
+    require(p.in[i].dtype == TCB_F32, "adam_update: master params/states must be f32");
+    require(same_shape(p.in[i], p.in[0]), "adam_update: shape mismatch");
+  }
+  require(p.in[4].numel() == 1 && p.in[4].dtype == TCB_F32, "adam_update: step must be an f32 scalar");
+  AdamCfg c{p.attrs.f("lr", 1e-3), p.attrs.f("beta1", 0.9), p.attrs.f("beta2", 0.999),
+            p.attrs.f("eps", 1e-8), p.attrs.f("grad_scale", 1.0)};
+  const int64_t n = p.in[0].numel();
+  const int hd = p.out.size() > 3 ? p.out[3].dtype : -1;
+  if (hd >= 0) require(hd == TCB_BF16 || hd == TCB_F16, "adam_update_ex: 4th output must be bf16/f16");
+  p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
+    for (int i = 0; i < 4; ++i)
+      if (reinterpret_cast<uintptr_t>(in[i].ptr) % 16 || (i < 3 && reinterpret_cast<uintptr_t>(out[i].ptr) % 16))
+        fail(TCB_ERR_ARG, "adam_update: buffers must be 16-byte aligned");
+    const int grid = grid_for((n + 3) / 4, 256, kNumSMs * 4);
+    if (hd == TCB_BF16)
+      k_adam<__nv_bfloat16><<<grid, 256, 0, s>>>(
+          (const float*)in[0].ptr, (const float*)in[1].ptr, (const float*)in[2].ptr,
+          (const float*)in[3].ptr, (const float*)in[4].ptr, (float*)out[0].ptr, (float*)out[1].ptr,
+          (float*)out[2].ptr, (__nv_bfloat16*)out[3].ptr, n, c);
+    else if (hd == TCB_F16)
+      k_adam<__half><<<grid, 256, 0, s>>>((const float*)in[0].ptr, (const float*)in[1].ptr,
+                                          (const float*)in[2].ptr, (const float*)in[3].ptr,
+                                          (const float*)in[4].ptr, (float*)out[0].ptr,
+                                          (float*)out[1].ptr, (float*)out[2].ptr,
+                                          (__half*)out[3].ptr, n, c);
+    else
+      k_adam<float><<<grid, 256, 0, s>>>((const float*)in[0].ptr, (const float*)in[1].ptr,
+                                         (const float*)in[2].ptr, (const float*)in[3].ptr,
+                                         (const float*)in[4].ptr, (float*)out[0].ptr,
+                                         (float*)out[1].ptr, (float*)out[2].ptr, nullptr, n, c);
+  };
+}
+TCB_REGISTER("adam_update", b_adam);
+TCB_REGISTER("adam_update_ex", b_adam);
+
+}  // namespace tcb

@@ -1,0 +1,217 @@
+// k_reduce.cu -- b200 kernels for sum / mean (backends.hpp:95-141) and mse
+// (backends.hpp:205-214).
+//
+// Two strategies:
+//  * exact: one thread per output slot accumulates its reduced elements in
+//    row-major order -- the same order as the reference's flat scan, so f32/f16
+//    results are bit-identical to exec_base.  Used for the reference dtypes.
+//  * fast: warp-per-column-tile tree reduction for bf16 activations (the AMP
+//    extension; bias gradients of [T, N] GEMM outputs), deterministic but in a
+//    different association order (tolerance-checked).
+#include "common.cuh"
+
+namespace tcb {
+
+struct RedGeom {
+  int rank;
+  int64_t shape[TCB_MAX_RANK];
+  int reduced[TCB_MAX_RANK];
+  int64_t count;  // elements per slot
+};
+
+static RedGeom red_geom(const Spec& x, const std::string& axes_s) {
+  RedGeom g{};
+  g.rank = x.rank;
+  for (int i = 0; i < x.rank; ++i) g.shape[i] = x.shape[i];
+  if (axes_s.empty()) {
+    for (int i = 0; i < x.rank; ++i) g.reduced[i] = 1;
+  } else {
+    size_t pos = 0;
+    while (pos < axes_s.size()) {
+      size_t c = axes_s.find(',', pos);
+      if (c == std::string::npos) c = axes_s.size();
+      int a = std::stoi(axes_s.substr(pos, c - pos));
+      if (a < 0 || a >= x.rank) fail(TCB_ERR_TYPE, "reduction axis out of range: " + axes_s);
+      g.reduced[a] = 1;
+      pos = c + 1;
+    }
+  }
+  g.count = 1;
+  for (int i = 0; i < x.rank; ++i)
+    if (g.reduced[i]) g.count *= x.shape[i];
+  return g;
+}
+
+// exact: thread per output slot; walk reduced coordinates in row-major order
+template <typename T, typename TO>
+__global__ void k_reduce_exact(const T* __restrict__ x, TO* __restrict__ o, int64_t nslots, RedGeom g,
+                               int mean) {
+  int64_t slot = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (slot >= nslots) return;
+  // base offset of this slot (kept dims), strides of all dims
+  int64_t stride[TCB_MAX_RANK];
+  int64_t s = 1;
+  for (int d = g.rank - 1; d >= 0; --d) {
+    stride[d] = s;
+    s *= g.shape[d];
+  }
+  int64_t base = 0, rem = slot;
+  for (int d = g.rank - 1; d >= 0; --d) {
+    if (g.reduced[d]) continue;
+    int64_t q = rem / g.shape[d];
+    base += (rem - q * g.shape[d]) * stride[d];
+    rem = q;
+  }
+  float acc = 0.0f;
+  for (int64_t r = 0; r < g.count; ++r) {
+    int64_t off = 0, rr = r;
+    for (int d = g.rank - 1; d >= 0; --d) {
+      if (!g.reduced[d]) continue;
+      int64_t q = rr / g.shape[d];
+      off += (rr - q * g.shape[d]) * stride[d];
+      rr = q;
+    }
+    acc = __fadd_rn(acc, to_f(x[base + off]));
+  }
+  if (mean) acc = __fmul_rn(acc, 1.0f / float(g.count));
+  o[slot] = from_f<TO>(acc);
+}
+
+// fast: x viewed as [outer, red, inner]; block = 32 inner columns x 8 warps
+template <typename T, typename TO>
+__global__ void k_reduce_cols(const T* __restrict__ x, TO* __restrict__ o, int64_t outer, int64_t red,
+                              int64_t inner, float scale) {
+  __shared__ float part[8][33];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t tiles_per_outer = (inner + 31) / 32;
+  const int64_t ob = blockIdx.x / tiles_per_outer;
+  const int64_t col = (blockIdx.x % tiles_per_outer) * 32 + lane;
+  float acc = 0.0f;
+  if (col < inner) {
+    const T* px = x + ob * red * inner + col;
+    for (int64_t r = warp; r < red; r += 8) acc += to_f(px[r * inner]);
+  }
+  part[warp][lane] = acc;
+  __syncthreads();
+  if (warp == 0 && col < inner) {
+    float t = 0.0f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) t += part[w][lane];
+    o[ob * inner + col] = from_f<TO>(t * scale);
+  }
+}
+
+// fast: inner == 1, one warp per row
+template <typename T, typename TO>
+__global__ void k_reduce_rows(const T* __restrict__ x, TO* __restrict__ o, int64_t rows, int64_t red,
+                              float scale) {
+  const int64_t row = blockIdx.x * int64_t(blockDim.x / 32) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  float acc = 0.0f;
+  for (int64_t j = lane; j < red; j += 32) acc += to_f(x[row * red + j]);
+#pragma unroll
+  for (int m = 16; m; m >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, m);
+  if (lane == 0) o[row] = from_f<TO>(acc * scale);
+}
+
+static void build_reduce(Plan& p, int mean) {
+  check_arity(p, 1, 1, 1, 1);
+  const Spec& X = p.in[0];
+  require(is_float(X.dtype), p.op + ": float dtypes only");
+  RedGeom g = red_geom(X, p.attrs.s("axes", ""));
+  const int64_t nslots = p.out[0].numel();
+  require(nslots * g.count == X.numel(), p.op + ": output shape mismatch");
+  // contiguous reduced block?
+  int first = -1, last = -1;
+  for (int i = 0; i < X.rank; ++i)
+    if (g.reduced[i]) {
+      if (first < 0) first = i;
+      last = i;
+    }
+  bool contiguous = first >= 0;
+  for (int i = first; contiguous && i <= last; ++i) contiguous = g.reduced[i];
+  const bool exact = X.dtype != TCB_BF16 || p.attrs.i("exact", 0) != 0 || !contiguous;
+  const int dto = p.out[0].dtype;
+  dispatch_float(X.dtype, [&](auto* tp) {
+    using T = std::remove_pointer_t<decltype(tp)>;
+    dispatch_float(dto, [&](auto* op_) {
+      using TO = std::remove_pointer_t<decltype(op_)>;
+      if (exact) {
+        p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
+          k_reduce_exact<T, TO><<<unsigned((nslots + 127) / 128), 128, 0, s>>>(
+              (const T*)in[0].ptr, (TO*)out[0].ptr, nslots, g, mean);
+        };
+        return;
+      }
+      int64_t outer = 1, red = 1, inner = 1;
+      for (int i = 0; i < first; ++i) outer *= X.shape[i];
+      for (int i = first; i <= last; ++i) red *= X.shape[i];
+      for (int i = last + 1; i < X.rank; ++i) inner *= X.shape[i];
+      const float scale = mean ? 1.0f / float(red) : 1.0f;
+      if (inner == 1) {
+        p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
+          k_reduce_rows<T, TO><<<unsigned((outer + 7) / 8), 256, 0, s>>>((const T*)in[0].ptr,
+                                                                          (TO*)out[0].ptr, outer, red, scale);
+        };
+      } else {
+        const int64_t blocks = outer * ((inner + 31) / 32);
+        p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
+          k_reduce_cols<T, TO><<<unsigned(blocks), 256, 0, s>>>((const T*)in[0].ptr, (TO*)out[0].ptr,
+                                                                  outer, red, inner, scale);
+        };
+      }
+    });
+  });
+}
+static void b_sum(Plan& p) { build_reduce(p, 0); }
+static void b_mean(Plan& p) { build_reduce(p, 1); }
+TCB_REGISTER("sum", b_sum);
+TCB_REGISTER("mean", b_mean);
+
+// mse: sequential f32 sum of squared differences, then acc / numel (a divide)
+template <typename T>
+__global__ void k_mse_exact(const T* __restrict__ a, const T* __restrict__ b, float* o, int64_t n) {
+  float acc = 0.0f;
+  for (int64_t i = 0; i < n; ++i) {
+    float d = __fsub_rn(to_f(a[i]), to_f(b[i]));
+    acc = __fadd_rn(acc, __fmul_rn(d, d));
+  }
+  o[0] = __fdiv_rn(acc, float(n));
+}
+template <typename T>
+__global__ void k_mse_block(const T* __restrict__ a, const T* __restrict__ b, float* o, int64_t n) {
+  __shared__ float part[32];
+  float acc = 0.0f;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    float d = to_f(a[i]) - to_f(b[i]);
+    acc += d * d;
+  }
+  for (int m = 16; m; m >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, m);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = 0.0f;
+    for (int w = 0; w < int(blockDim.x / 32); ++w) t += part[w];
+    o[0] = t / float(n);
+  }
+}
+static void b_mse(Plan& p) {
+  check_arity(p, 2, 2, 1, 1);
+  require(same_shape(p.in[0], p.in[1]), "mse: prediction/label shape mismatch");
+  require(p.in[0].dtype == p.in[1].dtype, "mse: dtype mismatch without explicit cast");
+  require(p.out[0].dtype == TCB_F32 && p.out[0].numel() == 1, "mse: output is f32[1]");
+  const int64_t n = p.in[0].numel();
+  dispatch_float(p.in[0].dtype, [&](auto* tp) {
+    using T = std::remove_pointer_t<decltype(tp)>;
+    p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
+      if (n <= (1 << 16))
+        k_mse_exact<T><<<1, 1, 0, s>>>((const T*)in[0].ptr, (const T*)in[1].ptr, (float*)out[0].ptr, n);
+      else
+        k_mse_block<T><<<1, 1024, 0, s>>>((const T*)in[0].ptr, (const T*)in[1].ptr, (float*)out[0].ptr, n);
+    };
+  });
+}
+TCB_REGISTER("mse", b_mse);
+
+}  // namespace tcb

@@ -1,0 +1,924 @@
+// k_transformer.cu -- the memory-bound transformer ops the reference lacks
+// (SURVEY.md §2.4 / §8a A15): layer_norm (+ fused dropout-residual),
+// layer_norm_dx, softmax / softmax_dx, the attention fwd/bwd closures (tcgen05
+// GEMMs on strided head views + row softmax), embedding gather / deterministic
+// scatter-add, and the fused cross-entropy loss + gradient.
+//
+// Row kernels use one warp per row with 16-byte vector loads when the row length
+// allows, f32 statistics and warp-shuffle reductions; the oracle (oracle.c) has
+// the same formulas with sequential sums (tolerance-checked, not bit-exact).
+#include "gemm.cuh"
+
+namespace tcb {
+
+// ---------------------------------------------------------------- utilities
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int m = 16; m; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int m = 16; m; m >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, m));
+  return v;
+}
+
+// Plan-owned device scratch (allocated once at plan creation, freed with the
+// plan). Launches of one plan are stream-ordered, so reuse is race-free.
+struct Scratch {
+  void* p = nullptr;
+  explicit Scratch(size_t bytes) { TCB_CUDA(cudaMalloc(&p, bytes ? bytes : 16)); }
+  ~Scratch() {
+    if (p) cudaFree(p);
+  }
+};
+
+// 8 consecutive elements <-> floats
+template <typename T>
+struct Vec8;
+template <>
+struct Vec8<__nv_bfloat16> {
+  static __device__ __forceinline__ void load(const __nv_bfloat16* p, float* f) {
+    uint4 q = *reinterpret_cast<const uint4*>(p);
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&q);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      float2 t = __bfloat1622float2(h[i]);
+      f[2 * i] = t.x;
+      f[2 * i + 1] = t.y;
+    }
+  }
+  static __device__ __forceinline__ void store(__nv_bfloat16* p, const float* f) {
+    uint4 q;
+    __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&q);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
+    *reinterpret_cast<uint4*>(p) = q;
+  }
+};
+template <>
+struct Vec8<__half> {
+  static __device__ __forceinline__ void load(const __half* p, float* f) {
+    uint4 q = *reinterpret_cast<const uint4*>(p);
+    const __half2* h = reinterpret_cast<const __half2*>(&q);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      float2 t = __half22float2(h[i]);
+      f[2 * i] = t.x;
+      f[2 * i + 1] = t.y;
+    }
+  }
+  static __device__ __forceinline__ void store(__half* p, const float* f) {
+    uint4 q;
+    __half2* h = reinterpret_cast<__half2*>(&q);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) h[i] = __floats2half2_rn(f[2 * i], f[2 * i + 1]);
+    *reinterpret_cast<uint4*>(p) = q;
+  }
+};
+template <>
+struct Vec8<float> {
+  static __device__ __forceinline__ void load(const float* p, float* f) {
+    float4 a = *reinterpret_cast<const float4*>(p), b = *reinterpret_cast<const float4*>(p + 4);
+    f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w;
+    f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
+  }
+  static __device__ __forceinline__ void store(float* p, const float* f) {
+    *reinterpret_cast<float4*>(p) = make_float4(f[0], f[1], f[2], f[3]);
+    *reinterpret_cast<float4*>(p + 4) = make_float4(f[4], f[5], f[6], f[7]);
+  }
+};
+
+// load/store 8 elements starting at i (vector path when aligned, else scalar)
+template <typename T>
+__device__ __forceinline__ void ld8(const T* p, int64_t i, int64_t n, bool vec, float* f) {
+  if (vec) {
+    Vec8<T>::load(p + i, f);
+  } else {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) f[k] = i + k < n ? to_f(p[i + k]) : 0.0f;
+  }
+}
+template <typename T>
+__device__ __forceinline__ void st8(T* p, int64_t i, int64_t n, bool vec, const float* f) {
+  if (vec) {
+    Vec8<T>::store(p + i, f);
+  } else {
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (i + k < n) p[i + k] = from_f<T>(f[k]);
+  }
+}
+
+constexpr int LN_MAXC = 8;  // up to 8 chunks of 8 per lane: H <= 2048
+
+// keep bits for elements i .. i+7 (two Philox calls when i is 4-aligned)
+__device__ __forceinline__ uint32_t drop_bits8(const DropCfg& d, uint64_t i) {
+  if (d.p <= 0.0f) return 0xFFu;
+  if ((i & 3) == 0) return dropout_bits4(d, i >> 2) | (dropout_bits4(d, (i >> 2) + 1) << 4);
+  uint32_t b = 0;
+  for (int k = 0; k < 8; ++k) b |= uint32_t(dropout_keep(d, i + k)) << k;
+  return b;
+}
+
+// ------------------------------------------------------------ layer norm fwd
+// y = LN(s) where s = x (layer_norm) or s = round(dropout(x) + r) (add_layer_norm)
+template <typename T>
+__global__ void __launch_bounds__(256) k_ln_fwd(const T* __restrict__ x, const T* __restrict__ r,
+                                                const float* __restrict__ gamma_f,
+                                                const T* __restrict__ gamma_t, const float* __restrict__ beta_f,
+                                                const T* __restrict__ beta_t, T* __restrict__ y,
+                                                T* __restrict__ s_out, float* __restrict__ mean_o,
+                                                float* __restrict__ rstd_o, int64_t rows, int H, float eps,
+                                                DropCfg d, bool vec) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = blockIdx.x * int64_t(blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  const int nch = (H + 7) / 8;
+  float v[LN_MAXC][8];
+  float sum = 0.0f;
+#pragma unroll
+  for (int c = 0; c < LN_MAXC; ++c) {
+    const int ch = lane + c * 32;
+    if (ch < nch) {
+      const int64_t i = row * H + ch * 8;
+      ld8(x, i, (row + 1) * int64_t(H), vec, v[c]);
+      if (r) {
+        float rr[8];
+        ld8(r, i, (row + 1) * int64_t(H), vec, rr);
+        const uint32_t bits = drop_bits8(d, uint64_t(i));
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          float xv = ((bits >> k) & 1u) ? __fmul_rn(v[c][k], d.scale) : 0.0f;
+          v[c][k] = to_f(from_f<T>(__fadd_rn(xv, rr[k])));  // s is rounded to the storage dtype
+        }
+        st8(s_out, i, (row + 1) * int64_t(H), vec, v[c]);
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (ch * 8 + k < H) sum += v[c][k];
+    }
+  }
+  const float inv = 1.0f / float(H);
+  const float mean = warp_sum(sum) * inv;
+  float sq = 0.0f;
+#pragma unroll
+  for (int c = 0; c < LN_MAXC; ++c) {
+    const int ch = lane + c * 32;
+    if (ch < nch) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (ch * 8 + k < H) {
+          float dd = v[c][k] - mean;
+          sq += dd * dd;
+        }
+    }
+  }
+  const float rstd = 1.0f / sqrtf(warp_sum(sq) * inv + eps);
+  if (lane == 0) {
+    mean_o[row] = mean;
+    rstd_o[row] = rstd;
+  }
+#pragma unroll
+  for (int c = 0; c < LN_MAXC; ++c) {
+    const int ch = lane + c * 32;
+    if (ch < nch) {
+      float o[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int j = ch * 8 + k;
+        if (j < H) {
+          float g = gamma_f ? gamma_f[j] : to_f(gamma_t[j]);
+          float b = beta_f ? beta_f[j] : to_f(beta_t[j]);
+          o[k] = (v[c][k] - mean) * rstd * g + b;
+        } else {
+          o[k] = 0.0f;
+        }
+      }
+      st8(y, row * H + ch * 8, (row + 1) * int64_t(H), vec, o);
+    }
+  }
+}
+
+static void build_ln_fwd(Plan& p, bool residual) {
+  if (residual) check_arity(p, 4, 4, 4, 4);
+  else check_arity(p, 3, 3, 3, 3);
+  const Spec& X = p.in[0];
+  const int H = int(X.dim(-1));
+  const int64_t rows = X.numel() / H;
+  require(H <= LN_MAXC * 8 * 32, p.op + ": hidden size > 2048 unsupported");
+  const Spec& G = p.in[residual ? 2 : 1];
+  require(G.numel() == H, p.op + ": gamma must have H elements");
+  require(G.dtype == TCB_F32 || G.dtype == X.dtype, p.op + ": gamma dtype");
+  const bool gf = G.dtype == TCB_F32;
+  const float eps = float(p.attrs.f("eps", 1e-12));
+  const DropCfg d = drop_cfg(p.attrs);
+  dispatch_float(X.dtype, [&](auto* tp) {
+    using T = std::remove_pointer_t<decltype(tp)>;
+    p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
+      const int gi = residual ? 2 : 1;
+      bool vec = (H % 8 == 0);
+      for (int i = 0; i < (residual ? 2 : 1); ++i) vec = vec && reinterpret_cast<uintptr_t>(in[i].ptr) % 16 == 0;
+      vec = vec && reinterpret_cast<uintptr_t>(out[0].ptr) % 16 == 0;
+      if (residual) vec = vec && reinterpret_cast<uintptr_t>(out[1].ptr) % 16 == 0;
+      k_ln_fwd<T><<<unsigned((rows + 7) / 8), 256, 0, s>>>(
+          (const T*)in[0].ptr, residual ? (const T*)in[1].ptr : nullptr,
+          gf ? (const float*)in[gi].ptr : nullptr, gf ? nullptr : (const T*)in[gi].ptr,
+          gf ? (const float*)in[gi + 1].ptr : nullptr, gf ? nullptr : (const T*)in[gi + 1].ptr,
+          (T*)out[0].ptr, residual ? (T*)out[1].ptr : nullptr, (float*)out[residual ? 2 : 1].ptr,
+          (float*)out[residual ? 3 : 2].ptr, rows, H, eps, d, vec);
+    };
+  });
+}
+static void b_layer_norm(Plan& p) { build_ln_fwd(p, false); }
+static void b_add_layer_norm(Plan& p) { build_ln_fwd(p, true); }
+TCB_REGISTER("layer_norm", b_layer_norm);
+TCB_REGISTER("add_layer_norm", b_add_layer_norm);
+
+// ------------------------------------------------------------ layer norm bwd
+// ds = rstd*(g - mean(g) - xh*mean(g*xh)) [+ dres]; dx = dropout(ds);
+// per-CTA partial column sums of dy*xh and dy -> ws, then k_colsum finalises.
+constexpr int LNB_ROWS = 32;  // rows per CTA (8 warps x 4 rows)
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_ln_bwd(const T* __restrict__ sx, const float* __restrict__ gamma_f,
+                                                const T* __restrict__ gamma_t, const float* __restrict__ mean,
+                                                const float* __restrict__ rstd, const T* __restrict__ dy,
+                                                const T* __restrict__ dres, T* __restrict__ ds_o,
+                                                T* __restrict__ dx_o, float* __restrict__ ws, int64_t rows,
+                                                int H, DropCfg d, bool vec) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nch = (H + 7) / 8;
+  float pg[LN_MAXC][8], pb[LN_MAXC][8];
+#pragma unroll
+  for (int c = 0; c < LN_MAXC; ++c)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) pg[c][k] = pb[c][k] = 0.0f;
+  const float inv = 1.0f / float(H);
+  for (int rr = 0; rr < LNB_ROWS / 8; ++rr) {
+    const int64_t row = int64_t(blockIdx.x) * LNB_ROWS + warp * (LNB_ROWS / 8) + rr;
+    if (row >= rows) break;
+    const float mu = mean[row], rs = rstd[row];
+    float xh[LN_MAXC][8], g[LN_MAXC][8];
+    float c1 = 0.0f, c2 = 0.0f;
+#pragma unroll
+    for (int c = 0; c < LN_MAXC; ++c) {
+      const int ch = lane + c * 32;
+      if (ch < nch) {
+        const int64_t i = row * H + ch * 8;
+        float sv[8], dv[8];
+        ld8(sx, i, (row + 1) * int64_t(H), vec, sv);
+        ld8(dy, i, (row + 1) * int64_t(H), vec, dv);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int j = ch * 8 + k;
+          if (j < H) {
+            float gm = gamma_f ? gamma_f[j] : to_f(gamma_t[j]);
+            xh[c][k] = (sv[k] - mu) * rs;
+            g[c][k] = dv[k] * gm;
+            c1 += g[c][k] * xh[c][k];
+            c2 += g[c][k];
+            pg[c][k] += dv[k] * xh[c][k];
+            pb[c][k] += dv[k];
+          } else {
+            xh[c][k] = g[c][k] = 0.0f;
+          }
+        }
+      }
+    }
+    c1 = warp_sum(c1) * inv;
+    c2 = warp_sum(c2) * inv;
+#pragma unroll
+    for (int c = 0; c < LN_MAXC; ++c) {
+      const int ch = lane + c * 32;
+      if (ch < nch) {
+        const int64_t i = row * H + ch * 8;
+        float o[8], res[8];
+        if (dres) ld8(dres, i, (row + 1) * int64_t(H), vec, res);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          o[k] = rs * (g[c][k] - c2 - xh[c][k] * c1);
+          if (dres) o[k] += res[k];
+        }
+        st8(ds_o, i, (row + 1) * int64_t(H), vec, o);
+        if (dx_o) {
+          const uint32_t bits = drop_bits8(d, uint64_t(i));
+#pragma unroll
+          for (int k = 0; k < 8; ++k) o[k] = ((bits >> k) & 1u) ? o[k] * d.scale : 0.0f;
+          st8(dx_o, i, (row + 1) * int64_t(H), vec, o);
+        }
+      }
+    }
+  }
+  // CTA partials: smem reduce over the 8 warps, then one row of ws per CTA
+  extern __shared__ float red[];  // [8][2][H]
+#pragma unroll
+  for (int c = 0; c < LN_MAXC; ++c) {
+    const int ch = lane + c * 32;
+    if (ch < nch) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int j = ch * 8 + k;
+        if (j < H) {
+          red[(warp * 2 + 0) * H + j] = pg[c][k];
+          red[(warp * 2 + 1) * H + j] = pb[c][k];
+        }
+      }
+    }
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < H; j += blockDim.x) {
+    float a = 0.0f, b = 0.0f;
+    for (int w = 0; w < 8; ++w) {
+      a += red[(w * 2 + 0) * H + j];
+      b += red[(w * 2 + 1) * H + j];
+    }
+    ws[(int64_t(blockIdx.x) * 2 + 0) * H + j] = a;
+    ws[(int64_t(blockIdx.x) * 2 + 1) * H + j] = b;
+  }
+}
+
+// sum the per-CTA partials in fixed order -> dgamma, dbeta (f32)
+__global__ void k_ln_colsum(const float* __restrict__ ws, float* __restrict__ dg, float* __restrict__ db,
+                            int nblk, int H) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= H) return;
+  float a = 0.0f, b = 0.0f;
+  for (int k = 0; k < nblk; ++k) {
+    a += ws[(int64_t(k) * 2 + 0) * H + j];
+    b += ws[(int64_t(k) * 2 + 1) * H + j];
+  }
+  dg[j] = a;
+  db[j] = b;
+}
+
+static void b_layer_norm_dx(Plan& p) {
+  check_arity(p, 5, 6, 3, 4);
+  const Spec& S = p.in[0];
+  const int H = int(S.dim(-1));
+  const int64_t rows = S.numel() / H;
+  require(H <= LN_MAXC * 8 * 32, "layer_norm_dx: hidden size > 2048 unsupported");
+  require(p.out[1].dtype == TCB_F32 && p.out[2].dtype == TCB_F32, "layer_norm_dx: dgamma/dbeta are f32");
+  const bool gf = p.in[1].dtype == TCB_F32;
+  const bool has_res = p.in.size() > 5, has_dx = p.out.size() > 3;
+  const DropCfg d = drop_cfg(p.attrs);
+  const int nblk = int((rows + LNB_ROWS - 1) / LNB_ROWS);
+  auto ws = std::make_shared<Scratch>(size_t(nblk) * 2 * H * sizeof(float));
+  const size_t smem = size_t(16) * H * sizeof(float);
+  p.nkernels = 2;
+  dispatch_float(S.dtype, [&](auto* tp) {
+    using T = std::remove_pointer_t<decltype(tp)>;
+    static std::once_flag once;
+    std::call_once(once, [] {
+      TCB_CUDA(cudaFuncSetAttribute(k_ln_bwd<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * 2048 * 4));
+    });
+    p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
+      bool vec = H % 8 == 0;
+      for (int i : {0, 4}) vec = vec && reinterpret_cast<uintptr_t>(in[i].ptr) % 16 == 0;
+      if (has_res) vec = vec && reinterpret_cast<uintptr_t>(in[5].ptr) % 16 == 0;
+      vec = vec && reinterpret_cast<uintptr_t>(out[0].ptr) % 16 == 0;
+      if (has_dx) vec = vec && reinterpret_cast<uintptr_t>(out[3].ptr) % 16 == 0;
+      k_ln_bwd<T><<<nblk, 256, smem, s>>>(
+          (const T*)in[0].ptr, gf ? (const float*)in[1].ptr : nullptr, gf ? nullptr : (const T*)in[1].ptr,
+          (const float*)in[2].ptr, (const float*)in[3].ptr, (const T*)in[4].ptr,
+          has_res ? (const T*)in[5].ptr : nullptr, (T*)out[0].ptr, has_dx ? (T*)out[3].ptr : nullptr,
+          (float*)ws->p, rows, H, d, vec);
+      k_ln_colsum<<<(H + 127) / 128, 128, 0, s>>>((const float*)ws->p, (float*)out[1].ptr,
+                                                  (float*)out[2].ptr, nblk, H);
+    };
+  });
+}
+TCB_REGISTER("layer_norm_dx", b_layer_norm_dx);
+
+// ------------------------------------------------------------------ softmax
+// rows of length C; v = x*scale (causal: -inf for col > row % Sq); P = softmax;
+// optional Pd = dropout(P) (index = row*C + col).  One warp per row.
+constexpr int SM_MAXV = 32;  // up to 32 values per lane: C <= 1024
+
+template <typename TI, typename TO>
+__global__ void __launch_bounds__(256) k_softmax(const TI* __restrict__ x, TO* __restrict__ P,
+                                                 TO* __restrict__ Pd, int64_t rows, int C, int Sq,
+                                                 float scale, int causal, DropCfg d) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = blockIdx.x * int64_t(blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  const int qi = int(row % Sq);
+  float v[SM_MAXV];
+  float m = -INFINITY;
+#pragma unroll
+  for (int c = 0; c < SM_MAXV; ++c) {
+    const int j = lane + c * 32;
+    float t = -INFINITY;
+    if (j < C) {
+      t = to_f(x[row * C + j]) * scale;
+      if (causal && j > qi) t = -INFINITY;
+    }
+    v[c] = t;
+    m = fmaxf(m, t);
+  }
+  m = warp_max(m);
+  float sum = 0.0f;
+#pragma unroll
+  for (int c = 0; c < SM_MAXV; ++c) {
+    const int j = lane + c * 32;
+    v[c] = j < C ? expf(v[c] - m) : 0.0f;
+    sum += v[c];
+  }
+  sum = warp_sum(sum);
+#pragma unroll
+  for (int c = 0; c < SM_MAXV; ++c) {
+    const int j = lane + c * 32;
+    if (j < C) {
+      TO pv = from_f<TO>(v[c] / sum);
+      P[row * C + j] = pv;
+      if (Pd) {
+        const uint64_t idx = uint64_t(row) * C + j;
+        Pd[row * C + j] = from_f<TO>(dropout_keep(d, idx) ? to_f(pv) * d.scale : 0.0f);
+      }
+    }
+  }
+}
+
+// dS = P * (dP - rowdot(P, dP)) * scale with dP = dropout(dPd); optional Pd out
+template <typename TP, typename TG, typename TO>
+__global__ void __launch_bounds__(256) k_softmax_bwd(const TP* __restrict__ P, const TG* __restrict__ dPd,
+                                                     TO* __restrict__ dS, TO* __restrict__ Pd_o, int64_t rows,
+                                                     int C, float scale, DropCfg d) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = blockIdx.x * int64_t(blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  float pv[SM_MAXV], dp[SM_MAXV];
+  float dot = 0.0f;
+#pragma unroll
+  for (int c = 0; c < SM_MAXV; ++c) {
+    const int j = lane + c * 32;
+    pv[c] = dp[c] = 0.0f;
+    if (j < C) {
+      const uint64_t idx = uint64_t(row) * C + j;
+      const bool keep = dropout_keep(d, idx);
+      pv[c] = to_f(P[row * C + j]);
+      dp[c] = keep ? to_f(dPd[row * C + j]) * d.scale : 0.0f;
+      if (Pd_o) Pd_o[row * C + j] = from_f<TO>(keep ? pv[c] * d.scale : 0.0f);
+      dot += pv[c] * dp[c];
+    }
+  }
+  dot = warp_sum(dot);
+#pragma unroll
+  for (int c = 0; c < SM_MAXV; ++c) {
+    const int j = lane + c * 32;
+    if (j < C) dS[row * C + j] = from_f<TO>(pv[c] * (dp[c] - dot) * scale);
+  }
+}
+
+template <typename Fn>
+static void dispatch2(int a, int b, Fn&& f) {
+  dispatch_float(a, [&](auto* pa) { dispatch_float(b, [&](auto* pb) { f(pa, pb); }); });
+}
+
+static void b_softmax(Plan& p) {
+  check_arity(p, 1, 1, 1, 2);
+  const Spec& X = p.in[0];
+  const int C = int(X.dim(-1));
+  require(C <= SM_MAXV * 32, "softmax: row length > 1024 unsupported");
+  const int64_t rows = X.numel() / C;
+  const int Sq = X.rank >= 2 ? int(X.dim(-2)) : 1;
+  const float scale = float(p.attrs.f("scale", 1.0));
+  const int causal = int(p.attrs.i("causal", 0));
+  const DropCfg d = drop_cfg(p.attrs);
+  dispatch2(X.dtype, p.out[0].dtype, [&](auto* pa, auto* pb) {
+    using TI = std::remove_pointer_t<decltype(pa)>;
+    using TO = std::remove_pointer_t<decltype(pb)>;
+    const bool pd = p.out.size() > 1;
+    p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
+      k_softmax<TI, TO><<<unsigned((rows + 7) / 8), 256, 0, s>>>(
+          (const TI*)in[0].ptr, (TO*)out[0].ptr, pd ? (TO*)out[1].ptr : nullptr, rows, C, Sq, scale, causal, d);
+    };
+  });
+}
+TCB_REGISTER("softmax", b_softmax);
+
+static void b_softmax_dx(Plan& p) {
+  check_arity(p, 2, 2, 1, 1);
+  const Spec& Y = p.in[0];
+  const int C = int(Y.dim(-1));
+  require(C <= SM_MAXV * 32, "softmax_dx: row length > 1024 unsupported");
+  const int64_t rows = Y.numel() / C;
+  const float scale = float(p.attrs.f("scale", 1.0));
+  DropCfg d;  // no dropout on the standalone op
+  const int dg = p.in[1].dtype;
+  dispatch2(Y.dtype, p.out[0].dtype, [&](auto* pa, auto* pb) {
+    using TP = std::remove_pointer_t<decltype(pa)>;
+    using TO = std::remove_pointer_t<decltype(pb)>;
+    dispatch_float(dg, [&](auto* pg) {
+      using TG = std::remove_pointer_t<decltype(pg)>;
+      p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
+        k_softmax_bwd<TP, TG, TO><<<unsigned((rows + 7) / 8), 256, 0, s>>>(
+            (const TP*)in[0].ptr, (const TG*)in[1].ptr, (TO*)out[0].ptr, nullptr, rows, C, scale, d);
+      };
+    });
+  });
+}
+TCB_REGISTER("softmax_dx", b_softmax_dx);
+
+// ---------------------------------------------------------------- attention
+// qkv [T, 3H] with T = B*S; heads A, dh = H/A.  Head (b, h) of Q/K/V is a
+// strided [S, dh] view (row stride 3H) -- consumed directly by the GEMM tensor
+// maps, no head split/merge copies.
+struct AttnGeom {
+  int64_t B, S, A, H, dh, Z;
+  float scale;
+  int causal;
+  DropCfg d;
+  int dt;
+  bool exact;
+};
+
+static AttnGeom attn_geom(const Plan& p) {
+  const Spec& X = p.in[0];
+  require(X.rank == 2 && X.shape[1] % 3 == 0, p.op + ": qkv must be [T, 3H]");
+  AttnGeom g;
+  g.H = X.shape[1] / 3;
+  g.A = p.attrs.i("heads", 1);
+  g.S = p.attrs.i("seq", X.shape[0]);
+  require(g.A >= 1 && g.H % g.A == 0, p.op + ": heads must divide H");
+  require(g.S >= 1 && X.shape[0] % g.S == 0, p.op + ": seq must divide T");
+  require(g.S <= SM_MAXV * 32, p.op + ": seq > 1024 unsupported");
+  g.B = X.shape[0] / g.S;
+  g.dh = g.H / g.A;
+  g.Z = g.B * g.A;
+  g.scale = float(p.attrs.f("scale", 1.0 / std::sqrt(double(g.dh))));
+  g.causal = int(p.attrs.i("causal", 0));
+  g.d = drop_cfg(p.attrs);
+  g.dt = X.dtype;
+  g.exact = X.dtype == TCB_F32 || p.attrs.i("exact", 0) != 0;
+  return g;
+}
+
+// operand view of part `part` (0 q, 1 k, 2 v) of qkv for batch z = (b, h)
+static GemmOperand qkv_view(const AttnGeom& g, const void* qkv, int part) {
+  GemmOperand o;
+  o.ptr = static_cast<const char*>(qkv) + size_t(part) * g.H * dtype_bytes(g.dt);
+  o.ld = 3 * g.H;
+  o.s1 = g.S * 3 * g.H;
+  o.s2 = g.dh;
+  o.dtype = g.dt;
+  return o;
+}
+static GemmOperand sq_view(const AttnGeom& g, const void* p, int dt) {  // [Z, S, S]
+  GemmOperand o;
+  o.ptr = p;
+  o.ld = g.S;
+  o.s1 = g.A * g.S * g.S;
+  o.s2 = g.S * g.S;
+  o.dtype = dt;
+  return o;
+}
+static GemmOperand ctx_view(const AttnGeom& g, const void* p) {  // [T, H] head views
+  GemmOperand o;
+  o.ptr = p;
+  o.ld = g.H;
+  o.s1 = g.S * g.H;
+  o.s2 = g.dh;
+  o.dtype = g.dt;
+  return o;
+}
+static GemmArgs attn_gemm(const AttnGeom& g, int64_t M, int64_t N, int64_t K, GemmOperand a, int ta,
+                          GemmOperand b, int tb) {
+  GemmArgs r;
+  r.M = M;
+  r.N = N;
+  r.K = K;
+  r.Z = g.Z;
+  r.Z2 = g.A;
+  r.a = a;
+  r.b = b;
+  r.ta = ta;
+  r.tb = tb;
+  return r;
+}
+static void set_c(GemmArgs& r, void* c, int64_t ld, int64_t s1, int64_t s2, int dt) {
+  r.c = c;
+  r.ldc = ld;
+  r.c_s1 = s1;
+  r.c_s2 = s2;
+  r.c_dtype = dt;
+}
+
+// attention(qkv) -> (ctx [T,H], probs [Z*S, S])
+static void b_attention(Plan& p) {
+  check_arity(p, 1, 1, 2, 2);
+  const AttnGeom g = attn_geom(p);
+  require(p.out[0].numel() == g.B * g.S * g.H, "attention: ctx must be [T, H]");
+  require(p.out[1].numel() == g.Z * g.S * g.S, "attention: probs must be [B*A*S, S]");
+  const size_t nsq = size_t(g.Z) * g.S * g.S;
+  auto scores = std::make_shared<Scratch>(nsq * 4);
+  auto pd = std::make_shared<Scratch>(g.d.p > 0.0f ? nsq * dtype_bytes(g.dt) : 0);
+  p.nkernels = 3;
+  dispatch_float(g.dt, [&](auto* tp) {
+    using T = std::remove_pointer_t<decltype(tp)>;
+    p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
+      // 1. scores = scale * Q K^T (f32)
+      GemmArgs q = attn_gemm(g, g.S, g.S, g.dh, qkv_view(g, in[0].ptr, 0), 0, qkv_view(g, in[0].ptr, 1), 1);
+      q.alpha = g.scale;
+      set_c(q, scores->p, g.S, g.A * g.S * g.S, g.S * g.S, TCB_F32);
+      launch_gemm(q, g.exact, s);
+      // 2. P = softmax(scores) (+ dropout copy)
+      const int64_t rows = g.Z * g.S;
+      T* Pd = g.d.p > 0.0f ? (T*)pd->p : nullptr;
+      k_softmax<float, T><<<unsigned((rows + 7) / 8), 256, 0, s>>>(
+          (const float*)scores->p, (T*)out[1].ptr, Pd, rows, int(g.S), int(g.S), 1.0f, g.causal, g.d);
+      // 3. ctx = Pd V
+      GemmArgs c = attn_gemm(g, g.S, g.dh, g.S, sq_view(g, Pd ? (const void*)Pd : out[1].ptr, g.dt), 0,
+                             qkv_view(g, in[0].ptr, 2), 0);
+      set_c(c, out[0].ptr, g.H, g.S * g.H, g.dh, g.dt);
+      launch_gemm(c, g.exact, s);
+    };
+  });
+}
+TCB_REGISTER("attention", b_attention);
+
+// attention_dx(qkv, probs, dctx) -> dqkv [T, 3H]
+static void b_attention_dx(Plan& p) {
+  check_arity(p, 3, 3, 1, 1);
+  const AttnGeom g = attn_geom(p);
+  require(p.out[0].numel() == p.in[0].numel(), "attention_dx: dqkv must be [T, 3H]");
+  const size_t nsq = size_t(g.Z) * g.S * g.S;
+  auto dpd = std::make_shared<Scratch>(nsq * 4);
+  auto ds = std::make_shared<Scratch>(nsq * dtype_bytes(g.dt));
+  auto pd = std::make_shared<Scratch>(g.d.p > 0.0f ? nsq * dtype_bytes(g.dt) : 0);
+  p.nkernels = 5;
+  dispatch_float(g.dt, [&](auto* tp) {
+    using T = std::remove_pointer_t<decltype(tp)>;
+    p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
+      const void* qkv = in[0].ptr;
+      // 1. dPd = dctx V^T (f32)
+      GemmArgs a = attn_gemm(g, g.S, g.S, g.dh, ctx_view(g, in[2].ptr), 0, qkv_view(g, qkv, 2), 1);
+      set_c(a, dpd->p, g.S, g.A * g.S * g.S, g.S * g.S, TCB_F32);
+      launch_gemm(a, g.exact, s);
+      // 2. dS = P (dP - rowdot) * scale ; Pd
+      const int64_t rows = g.Z * g.S;
+      T* Pd = g.d.p > 0.0f ? (T*)pd->p : nullptr;
+      k_softmax_bwd<T, float, T><<<unsigned((rows + 7) / 8), 256, 0, s>>>(
+          (const T*)in[1].ptr, (const float*)dpd->p, (T*)ds->p, Pd, rows, int(g.S), g.scale, g.d);
+      char* dq = static_cast<char*>(out[0].ptr);
+      const size_t part = size_t(g.H) * dtype_bytes(g.dt);
+      // 3. dQ = dS K
+      GemmArgs b = attn_gemm(g, g.S, g.dh, g.S, sq_view(g, ds->p, g.dt), 0, qkv_view(g, qkv, 1), 0);
+      set_c(b, dq, 3 * g.H, g.S * 3 * g.H, g.dh, g.dt);
+      launch_gemm(b, g.exact, s);
+      // 4. dK = dS^T Q
+      GemmArgs c = attn_gemm(g, g.S, g.dh, g.S, sq_view(g, ds->p, g.dt), 1, qkv_view(g, qkv, 0), 0);
+      set_c(c, dq + part, 3 * g.H, g.S * 3 * g.H, g.dh, g.dt);
+      launch_gemm(c, g.exact, s);
+      // 5. dV = Pd^T dctx
+      GemmArgs v = attn_gemm(g, g.S, g.dh, g.S, sq_view(g, Pd ? (const void*)Pd : in[1].ptr, g.dt), 1,
+                             ctx_view(g, in[2].ptr), 0);
+      set_c(v, dq + 2 * part, 3 * g.H, g.S * 3 * g.H, g.dh, g.dt);
+      launch_gemm(v, g.exact, s);
+    };
+  });
+}
+TCB_REGISTER("attention_dx", b_attention_dx);
+
+// ---------------------------------------------------------------- embedding
+template <typename TT, typename TO>
+__global__ void k_embed(const int32_t* __restrict__ ids, const TT* __restrict__ table, TO* __restrict__ out,
+                        int64_t T, int64_t H, int64_t V, int* __restrict__ err) {
+  const int64_t t = blockIdx.x * int64_t(blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (t >= T) return;
+  const int32_t id = ids[t];
+  if (id < 0 || id >= V) {
+    if (lane == 0) atomicExch(err, 1);
+    return;
+  }
+  for (int64_t j = lane; j < H; j += 32) out[t * H + j] = from_f<TO>(to_f(table[int64_t(id) * H + j]));
+}
+
+static void b_embedding(Plan& p) {
+  check_arity(p, 2, 2, 1, 1);
+  require(p.in[0].dtype == TCB_I32, "embedding: ids must be i32");
+  require(p.in[1].rank == 2, "embedding: table must be rank 2");
+  const int64_t T = p.in[0].numel(), V = p.in[1].shape[0], H = p.in[1].shape[1];
+  require(p.out[0].numel() == T * H, "embedding: output must be [T, H]");
+  auto err = std::make_shared<Scratch>(4);
+  TCB_CUDA(cudaMemset(err->p, 0, 4));
+  dispatch2(p.in[1].dtype, p.out[0].dtype, [&](auto* pa, auto* pb) {
+    using TT = std::remove_pointer_t<decltype(pa)>;
+    using TO = std::remove_pointer_t<decltype(pb)>;
+    p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
+      k_embed<TT, TO><<<unsigned((T + 7) / 8), 256, 0, s>>>((const int32_t*)in[0].ptr, (const TT*)in[1].ptr,
+                                                             (TO*)out[0].ptr, T, H, V, (int*)err->p);
+    };
+  });
+}
+TCB_REGISTER("embedding", b_embedding);
+
+// Deterministic scatter-add: stable rank of (id, t) pairs, then one warp per
+// distinct id accumulates its rows in ascending t onto base -- the oracle's
+// order exactly, so f32 results are bit-identical.
+__global__ void k_embed_rank(const int32_t* __restrict__ ids, int32_t* __restrict__ sorted, int64_t T) {
+  const int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (t >= T) return;
+  const int32_t my = ids[t];
+  int64_t rank = 0;
+  for (int64_t u = 0; u < T; ++u) {
+    const int32_t o = ids[u];
+    rank += (o < my) || (o == my && u < t);
+  }
+  sorted[rank] = int32_t(t);
+}
+
+template <typename TD>
+__global__ void k_embed_accum(const int32_t* __restrict__ ids, const int32_t* __restrict__ sorted,
+                              const TD* __restrict__ dy, float* __restrict__ out, int64_t T, int64_t H) {
+  const int64_t pos = blockIdx.x * int64_t(blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (pos >= T) return;
+  const int32_t id = ids[sorted[pos]];
+  if (pos > 0 && ids[sorted[pos - 1]] == id) return;  // not a segment head
+  int64_t end = pos + 1;
+  while (end < T && ids[sorted[end]] == id) ++end;
+  for (int64_t j = lane; j < H; j += 32) {
+    float acc = out[int64_t(id) * H + j];
+    for (int64_t q = pos; q < end; ++q) acc = __fadd_rn(acc, to_f(dy[int64_t(sorted[q]) * H + j]));
+    out[int64_t(id) * H + j] = acc;
+  }
+}
+
+static void b_embedding_dx(Plan& p) {
+  check_arity(p, 2, 3, 1, 1);
+  require(p.in[0].dtype == TCB_I32, "embedding_dx: ids must be i32");
+  require(p.out[0].dtype == TCB_F32 && p.out[0].rank == 2, "embedding_dx: output is f32 [V, H]");
+  const int64_t T = p.in[0].numel(), V = p.out[0].shape[0], H = p.out[0].shape[1];
+  require(p.in[1].numel() == T * H, "embedding_dx: dy must be [T, H]");
+  const bool has_base = p.in.size() > 2;
+  if (has_base) require(p.in[2].dtype == TCB_F32 && p.in[2].numel() == V * H, "embedding_dx: base is f32 [V,H]");
+  auto sorted = std::make_shared<Scratch>(size_t(T) * 4);
+  p.nkernels = 3;
+  dispatch_float(p.in[1].dtype, [&](auto* tp) {
+    using TD = std::remove_pointer_t<decltype(tp)>;
+    p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
+      const size_t nb = size_t(V) * H * 4;
+      if (has_base) {
+        if (in[2].ptr != out[0].ptr) TCB_CUDA(cudaMemcpyAsync(out[0].ptr, in[2].ptr, nb, cudaMemcpyDeviceToDevice, s));
+      } else {
+        TCB_CUDA(cudaMemsetAsync(out[0].ptr, 0, nb, s));
+      }
+      k_embed_rank<<<unsigned((T + 255) / 256), 256, 0, s>>>((const int32_t*)in[0].ptr, (int32_t*)sorted->p, T);
+      k_embed_accum<TD><<<unsigned((T + 7) / 8), 256, 0, s>>>((const int32_t*)in[0].ptr, (const int32_t*)sorted->p,
+                                                              (const TD*)in[1].ptr, (float*)out[0].ptr, T, H);
+    };
+  });
+}
+TCB_REGISTER("embedding_dx", b_embedding_dx);
+
+// ------------------------------------------------------------ cross entropy
+// (logits [T, Vp], labels [T]) -> (loss f32[1], dlogits [T, Vp])
+__global__ void k_ce_count(const int32_t* __restrict__ labels, int64_t T, int64_t ign, float* __restrict__ inv_n) {
+  __shared__ int part[32];
+  int c = 0;
+  for (int64_t t = threadIdx.x; t < T; t += blockDim.x) c += labels[t] != ign;
+  for (int m = 16; m; m >>= 1) c += __shfl_xor_sync(0xffffffffu, c, m);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int n = 0;
+    for (int w = 0; w < int(blockDim.x >> 5); ++w) n += part[w];
+    inv_n[0] = n ? 1.0f / float(n) : 0.0f;
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(512) k_ce_row(const T* __restrict__ x, const int32_t* __restrict__ labels,
+                                                T* __restrict__ dx, float* __restrict__ row_loss,
+                                                const float* __restrict__ inv_n_p, int64_t Vp, int64_t V,
+                                                int64_t ign, float gscale, int* __restrict__ err, bool vec) {
+  __shared__ float sm[32], ss[32];
+  const int64_t t = blockIdx.x;
+  const int32_t lab = labels[t];
+  const T* xr = x + t * Vp;
+  T* dr = dx ? dx + t * Vp : nullptr;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if (lab == ign) {
+    if (dr)
+      for (int64_t j = threadIdx.x; j < Vp; j += blockDim.x) dr[j] = from_f<T>(0.0f);
+    if (threadIdx.x == 0) row_loss[t] = 0.0f;
+    return;
+  }
+  if (lab < 0 || lab >= V) {
+    if (threadIdx.x == 0) atomicExch(err, 1);
+    return;
+  }
+  // pass 1: online max / sum
+  float m = -INFINITY, s = 0.0f;
+  const int64_t nch = V / 8;
+  for (int64_t c = threadIdx.x; c < (vec ? nch : 0); c += blockDim.x) {
+    float f[8];
+    Vec8<T>::load(xr + c * 8, f);
+    float lm = f[0];
+#pragma unroll
+    for (int k = 1; k < 8; ++k) lm = fmaxf(lm, f[k]);
+    if (lm > m) {
+      s *= expf(m - lm);
+      m = lm;
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += expf(f[k] - m);
+  }
+  for (int64_t j = (vec ? nch * 8 : 0) + threadIdx.x; j < V; j += blockDim.x) {
+    float f = to_f(xr[j]);
+    if (f > m) {
+      s *= expf(m - f);
+      m = f;
+    }
+    s += expf(f - m);
+  }
+  // combine (m, s) across the block
+  float wm = warp_max(m);
+  s = s * (m == -INFINITY ? 0.0f : expf(m - wm));
+  s = warp_sum(s);
+  if (lane == 0) {
+    sm[warp] = wm;
+    ss[warp] = s;
+  }
+  __syncthreads();
+  float M = -INFINITY;
+  for (int w = 0; w < nw; ++w) M = fmaxf(M, sm[w]);
+  float S = 0.0f;
+  for (int w = 0; w < nw; ++w) S += ss[w] * expf(sm[w] - M);
+  const float lse = M + logf(S);
+  if (threadIdx.x == 0) row_loss[t] = lse - to_f(xr[lab]);
+  if (!dr) return;
+  // pass 2: gradient
+  const float inv_s = 1.0f / S;
+  const float k = gscale * inv_n_p[0];
+  for (int64_t c = threadIdx.x; c < (vec ? Vp / 8 : 0); c += blockDim.x) {
+    float f[8];
+    Vec8<T>::load(xr + c * 8, f);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int64_t j = c * 8 + q;
+      float v = j < V ? expf(f[q] - M) * inv_s : 0.0f;
+      if (j == lab) v -= 1.0f;
+      f[q] = v * k;
+    }
+    Vec8<T>::store(dr + c * 8, f);
+  }
+  for (int64_t j = (vec ? (Vp / 8) * 8 : 0) + threadIdx.x; j < Vp; j += blockDim.x) {
+    float v = j < V ? expf(to_f(xr[j]) - M) * inv_s : 0.0f;
+    if (j == lab) v -= 1.0f;
+    dr[j] = from_f<T>(v * k);
+  }
+}
+
+__global__ void k_ce_final(const float* __restrict__ row_loss, const float* __restrict__ inv_n, int64_t T,
+                           float* __restrict__ loss) {
+  __shared__ float part[32];
+  float a = 0.0f;
+  for (int64_t t = threadIdx.x; t < T; t += blockDim.x) a += row_loss[t];
+  a = warp_sum(a);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = a;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float s = 0.0f;
+    for (int w = 0; w < int(blockDim.x >> 5); ++w) s += part[w];
+    loss[0] = s * inv_n[0];
+  }
+}
+
+static void b_cross_entropy(Plan& p) {
+  check_arity(p, 2, 2, 1, 2);
+  const Spec& X = p.in[0];
+  require(X.rank == 2, "cross_entropy: logits must be [T, V]");
+  require(p.in[1].dtype == TCB_I32 && p.in[1].numel() == X.shape[0], "cross_entropy: labels must be i32 [T]");
+  require(p.out[0].dtype == TCB_F32 && p.out[0].numel() == 1, "cross_entropy: loss is f32[1]");
+  const int64_t T = X.shape[0], Vp = X.shape[1];
+  const int64_t V = p.attrs.i("classes", Vp);
+  require(V >= 1 && V <= Vp, "cross_entropy: classes must be in [1, Vp]");
+  const int64_t ign = p.attrs.i("ignore_index", -100);
+  const float gscale = float(p.attrs.f("grad_scale", 1.0));
+  const bool grad = p.out.size() > 1;
+  if (grad) require(same_shape(p.out[1], X) && p.out[1].dtype == X.dtype, "cross_entropy: dlogits like logits");
+  auto ws = std::make_shared<Scratch>(size_t(T + 4) * 4);
+  auto err = std::make_shared<Scratch>(4);
+  TCB_CUDA(cudaMemset(err->p, 0, 4));
+  p.nkernels = 3;
+  dispatch_float(X.dtype, [&](auto* tp) {
+    using T_ = std::remove_pointer_t<decltype(tp)>;
+    p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
+      float* inv_n = (float*)ws->p;
+      float* rows = inv_n + 4;
+      const bool vec = Vp % 8 == 0 && reinterpret_cast<uintptr_t>(in[0].ptr) % 16 == 0 &&
+                       (!grad || reinterpret_cast<uintptr_t>(out[1].ptr) % 16 == 0);
+      k_ce_count<<<1, 1024, 0, s>>>((const int32_t*)in[1].ptr, T, ign, inv_n);
+      k_ce_row<T_><<<unsigned(T), 512, 0, s>>>((const T_*)in[0].ptr, (const int32_t*)in[1].ptr,
+                                                grad ? (T_*)out[1].ptr : nullptr, rows, inv_n, Vp, V, ign,
+                                                gscale, (int*)err->p, vec);
+      k_ce_final<<<1, 1024, 0, s>>>(rows, inv_n, T, (float*)out[0].ptr);
+    };
+  });
+}
+TCB_REGISTER("cross_entropy", b_cross_entropy);
+
+}  // namespace tcb

@@ -1,0 +1,313 @@
+"""Per-kernel parity of libtcb200 (b200 dialect, cuda:0) against the CPU oracle.
+
+Bar (BASELINE.json north_star): integer / index / layout work and
+every reference op whose ref kernel has a fixed f32 order is BIT-EXACT; floating
+point with a different association order (tensor-core GEMMs, parallel row
+reductions) is checked with the tolerance written in each test.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from gpu_util import bits_equal, max_ulp_bf16, quantize, rel_err, run_both  # noqa: E402
+from paper_2303_04759_b200.abi import BF16, F16, F32, I32  # noqa: E402
+
+RNG = np.random.default_rng(1234)
+
+
+def rn(*shape, lo=-1.0, hi=1.0):
+    return RNG.uniform(lo, hi, size=shape).astype(np.float32)
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2303_04759_b200.runtime import lib
+    lib()  # fail loudly if the extension is missing
+
+
+# ---------------------------------------------------------------- elementwise
+
+@pytest.mark.parametrize("dt", [F32, F16, BF16])
+@pytest.mark.parametrize("op", ["add", "sub", "mul", "div", "tanh_dx"])
+def test_binary_bit_exact(op, dt):
+    a, b = rn(37, 53), rn(37, 53, lo=0.5, hi=2.0)
+    for bshape in [(37, 53), (53,), (1,), (37, 1)]:
+        bb = rn(*bshape, lo=0.5, hi=2.0)
+        g, o = run_both(op, [(a, dt), (bb, dt)], [((37, 53), dt)])
+        assert bits_equal(g[0], o[0]), (op, dt, bshape)
+    g, o = run_both(op, [(rn(4, 1, 6), dt), (rn(3, 1, lo=0.5), dt)], [((4, 3, 6), dt)])
+    assert bits_equal(g[0], o[0])
+
+
+@pytest.mark.parametrize("dt", [F32, BF16])
+@pytest.mark.parametrize("op", ["neg", "relu", "gtz"])
+def test_unary_bit_exact(op, dt):
+    g, o = run_both(op, [(rn(1000, lo=-3, hi=3), dt)], [((1000,), dt)])
+    assert bits_equal(g[0], o[0])
+
+
+@pytest.mark.parametrize("op", ["tanh", "gelu"])
+def test_transcendental_unary(op):
+    # device tanhf/erff vs glibc: a few f32 ulps
+    g, o = run_both(op, [(rn(4096, lo=-4, hi=4), F32)], [((4096,), F32)])
+    assert np.max(np.abs(g[0] - o[0])) <= 4e-7 * np.maximum(1, np.abs(o[0])).max()
+    g, o = run_both(op, [(rn(4096, lo=-4, hi=4), BF16)], [((4096,), BF16)])
+    assert max_ulp_bf16(g[0], o[0]) <= 1
+
+
+def test_gelu_dx():
+    g, o = run_both("gelu_dx", [(rn(2048, lo=-4, hi=4), F32), (rn(2048), F32)], [((2048,), F32)])
+    assert rel_err(g[0], o[0]) < 1e-6
+
+
+def test_layout_ops_bit_exact():
+    x = rn(33, 65, lo=-100, hi=100)
+    for to, dt in [("f16", F16), ("bf16", BF16), ("f32", F32)]:
+        op = "cast" if to != "bf16" else "convert"
+        g, o = run_both(op, [(x, F32)], [((33, 65), dt)], {"to": to})
+        assert bits_equal(g[0], o[0])
+    g, o = run_both("bcast", [(rn(65), F32)], [((3, 33, 65), F32)], {"shape": "3,33,65"})
+    assert bits_equal(g[0], o[0])
+    for dt in (F32, BF16):
+        g, o = run_both("transpose", [(x, dt)], [((65, 33), dt)])
+        assert bits_equal(g[0], o[0])
+    g, o = run_both("reshape", [(x, F32)], [((65, 33), F32)], {"shape": "65,33"})
+    assert bits_equal(g[0], o[0])
+    g, o = run_both("view", [(x, F32)], [((7, 10), F32)], {"offset": 100, "shape": "7,10"})
+    assert bits_equal(g[0], o[0])
+
+
+def test_dropout_mask_bit_exact():
+    x = rn(10007)
+    for p in (0.0, 0.1, 0.5):
+        attrs = {"p": p, "seed": 7, "salt": 3}
+        g, o = run_both("dropout", [(x, F32)], [((10007,), F32)], attrs)
+        assert bits_equal(g[0], o[0]), p
+        g, o = run_both("dropout", [(x, BF16)], [((10007,), BF16)], attrs)
+        assert bits_equal(g[0], o[0]), p
+
+
+# ------------------------------------------------------------------ reductions
+
+@pytest.mark.parametrize("op", ["sum", "mean"])
+def test_reductions_exact(op):
+    x = rn(6, 50, 7)
+    for axes, shape in [("", (1,)), ("0", (50, 7)), ("1", (6, 7)), ("2", (6, 50)), ("0,2", (50,))]:
+        g, o = run_both(op, [(x, F32)], [(shape, F32)], {"axes": axes})
+        assert bits_equal(g[0], o[0]), axes
+    g, o = run_both(op, [(rn(300, 96), F16)], [((96,), F16)], {"axes": "0"})
+    assert bits_equal(g[0], o[0])
+
+
+def test_reduction_bf16_fast_path():
+    x = rn(4096, 768)
+    g, o = run_both("sum", [(x, BF16)], [((768,), F32)], {"axes": "0"})
+    assert rel_err(g[0], o[0]) < 1e-5
+    g, o = run_both("mean", [(x, BF16)], [((4096,), F32)], {"axes": "1"})
+    assert rel_err(g[0], o[0]) < 1e-5
+
+
+def test_mse_exact():
+    g, o = run_both("mse", [(rn(64, 10), F32), (rn(64, 10), F32)], [((1,), F32)])
+    assert bits_equal(g[0], o[0])
+
+
+# ------------------------------------------------------------------------ gemm
+
+@pytest.mark.parametrize("mnk", [(2, 4, 3), (33, 47, 65), (128, 96, 64)])
+@pytest.mark.parametrize("dt", [F32, F16])
+def test_matmul_exact_kernel_bit_exact(mnk, dt):
+    m, n, k = mnk
+    g, o = run_both("matmul", [(rn(m, k), dt), (rn(k, n), dt)], [((m, n), dt)])
+    assert bits_equal(g[0], o[0])
+
+
+@pytest.mark.parametrize("ta,tb", [(0, 0), (0, 1), (1, 0), (1, 1)])
+@pytest.mark.parametrize("mnk", [(128, 128, 64), (300, 200, 136), (256, 512, 1024), (1000, 768, 320)])
+def test_matmul_t_tcgen05(mnk, ta, tb):
+    """bf16 tcgen05 GEMM, f32 output: only the fp32 summation order differs from
+    the oracle's k-ascending loop -> norm-wise rel err < 1e-5."""
+    m, n, k = mnk
+    a = rn(k, m) if ta else rn(m, k)
+    b = rn(n, k) if tb else rn(k, n)
+    attrs = {"ta": ta, "tb": tb, "alpha": 0.5}
+    g, o = run_both("matmul_t", [(a, BF16), (b, BF16)], [((m, n), F32)], attrs)
+    assert rel_err(g[0], o[0]) < 1e-5, rel_err(g[0], o[0])
+    g, o = run_both("matmul_t", [(a, BF16), (b, BF16)], [((m, n), BF16)], attrs)
+    assert max_ulp_bf16(g[0], o[0]) <= 1
+
+
+def test_matmul_t_exact_flag_bit_exact():
+    a, b = rn(70, 40), rn(40, 50)
+    g, o = run_both("matmul_t", [(a, BF16), (b, BF16)], [((70, 50), BF16)], {"exact": 1})
+    assert bits_equal(g[0], o[0])
+
+
+@pytest.mark.parametrize("act", ["none", "relu", "tanh", "gelu"])
+def test_linear_tcgen05(act):
+    m, k, n = 512, 256, 384
+    x, w, b = rn(m, k), rn(k, n, lo=-0.1, hi=0.1), rn(n)
+    g, o = run_both("linear", [(x, BF16), (w, BF16), (b, F32)], [((m, n), BF16), ((m, n), BF16)],
+                    {"act": act})
+    assert max_ulp_bf16(g[0], o[0]) <= 2 and max_ulp_bf16(g[1], o[1]) <= 1
+
+
+@pytest.mark.parametrize("act", ["none", "relu", "tanh"])
+def test_linear_f32_matches_matmul_add_act(act):
+    """fp32 linear = opt-dialect matmul_add_act (bit-exact for none/relu)."""
+    m, k, n = 64, 48, 80
+    g, o = run_both("linear", [(rn(m, k), F32), (rn(k, n), F32), (rn(n), F32)], [((m, n), F32)],
+                    {"act": act})
+    if act == "tanh":
+        assert rel_err(g[0], o[0]) < 1e-6
+    else:
+        assert bits_equal(g[0], o[0])
+
+
+def test_matmul_dact_gelu():
+    m, k, n = 256, 384, 192
+    dy, w, u = rn(m, k), rn(n, k), rn(m, n, lo=-3, hi=3)
+    g, o = run_both("matmul_dact", [(dy, BF16), (w, BF16), (u, BF16)], [((m, n), BF16)],
+                    {"tb": 1, "act": "gelu"})
+    assert max_ulp_bf16(g[0], o[0]) <= 2
+
+
+def test_batch_matmul():
+    a, b = rn(6, 128, 64), rn(6, 128, 64)
+    g, o = run_both("batch_matmul", [(a, BF16), (b, BF16)], [((6, 128, 128), F32)], {"tb": 1})
+    assert rel_err(g[0], o[0]) < 1e-5
+    g, o = run_both("batch_matmul", [(a, F32), (b, F32)], [((6, 128, 128), F32)], {"tb": 1})
+    assert bits_equal(g[0], o[0])
+
+
+# ------------------------------------------------------------------ optimizer
+
+def test_sgd_bit_exact():
+    g, o = run_both("sgd_update", [(rn(10001), F32), (rn(10001), F32)], [((10001,), F32)], {"lr": 0.01})
+    assert bits_equal(g[0], o[0])
+
+
+def test_adam_double_math():
+    n = 100003
+    p, gr, m, v = rn(n), rn(n), rn(n, lo=-0.1, hi=0.1), rn(n, lo=0, hi=0.01)
+    attrs = {"lr": 1e-3, "beta1": 0.9, "beta2": 0.999, "eps": 1e-6}
+    step = np.array([3.0], np.float32)
+    g, o = run_both("adam_update", [(p, F32), (gr, F32), (m, F32), (v, F32), (step, F32)],
+                    [((n,), F32)] * 3, attrs)
+    for x, y in zip(g, o):
+        # double math on both sides; only the device pow() ulp in 1-beta^t differs
+        assert np.max(np.abs(x - y) / np.maximum(np.abs(y), 1e-30)) < 2e-7
+    g, o = run_both("adam_update_ex", [(p, F32), (gr, F32), (m, F32), (v, F32), (step, F32)],
+                    [((n,), F32)] * 3 + [((n,), BF16)], dict(attrs, grad_scale=0.25))
+    assert max_ulp_bf16(g[3], o[3]) <= 1 and rel_err(g[0], o[0]) < 1e-7
+
+
+# ------------------------------------------------------------ transformer ops
+
+@pytest.mark.parametrize("dt,H", [(F32, 128), (BF16, 768), (BF16, 1000)])
+def test_layer_norm(dt, H):
+    T = 257
+    x, gm, bt = rn(T, H, lo=-2, hi=2), rn(H, lo=0.5, hi=1.5), rn(H, lo=-0.1, hi=0.1)
+    g, o = run_both("layer_norm", [(x, dt), (gm, F32), (bt, F32)], [((T, H), dt), ((T,), F32), ((T,), F32)],
+                    {"eps": 1e-12})
+    assert rel_err(g[1], o[1]) < 1e-5 and rel_err(g[2], o[2]) < 1e-5
+    if dt == F32:
+        assert rel_err(g[0], o[0]) < 1e-5
+    else:
+        assert max_ulp_bf16(g[0], o[0]) <= 1
+
+
+@pytest.mark.parametrize("p", [0.0, 0.1])
+def test_add_layer_norm_and_backward(p):
+    T, H = 300, 768
+    x, r = rn(T, H), rn(T, H)
+    gm, bt = rn(H, lo=0.5, hi=1.5), rn(H, lo=-0.1, hi=0.1)
+    attrs = {"eps": 1e-12, "p": p, "seed": 11, "salt": 5}
+    g, o = run_both("add_layer_norm", [(x, BF16), (r, BF16), (gm, F32), (bt, F32)],
+                    [((T, H), BF16), ((T, H), BF16), ((T,), F32), ((T,), F32)], attrs)
+    assert bits_equal(g[1], o[1])  # s = round(dropout(x) + r): bit-exact incl. the Philox mask
+    assert max_ulp_bf16(g[0], o[0]) <= 1
+    s, mean, rstd = o[1], o[2], o[3]
+    dy, dres = rn(T, H), rn(T, H)
+    g, o = run_both("layer_norm_dx", [(s, BF16), (gm, F32), (mean, F32), (rstd, F32), (dy, BF16), (dres, BF16)],
+                    [((T, H), BF16), ((H,), F32), ((H,), F32), ((T, H), BF16)], attrs)
+    assert rel_err(g[0], o[0]) < 5e-3 and rel_err(g[3], o[3]) < 5e-3
+    assert rel_err(g[1], o[1]) < 1e-5 and rel_err(g[2], o[2]) < 1e-5
+
+
+def test_layer_norm_dx_f32():
+    T, H = 64, 128
+    s, gm = rn(T, H), rn(H, lo=0.5, hi=1.5)
+    mean = s.mean(1).astype(np.float32)
+    rstd = (1 / np.sqrt(s.var(1) + 1e-12)).astype(np.float32)
+    g, o = run_both("layer_norm_dx", [(s, F32), (gm, F32), (mean, F32), (rstd, F32), (rn(T, H), F32)],
+                    [((T, H), F32), ((H,), F32), ((H,), F32)])
+    for a, b in zip(g, o):
+        assert rel_err(a, b) < 1e-5
+
+
+@pytest.mark.parametrize("causal", [0, 1])
+def test_softmax_and_dx(causal):
+    x = rn(4, 128, 128, lo=-5, hi=5)
+    g, o = run_both("softmax", [(x, F32)], [((4, 128, 128), F32)], {"scale": 0.125, "causal": causal})
+    assert rel_err(g[0], o[0]) < 1e-6
+    y, dy = o[0], rn(4, 128, 128)
+    g, o = run_both("softmax_dx", [(y, F32), (dy, F32)], [((4, 128, 128), F32)], {"scale": 0.125})
+    assert rel_err(g[0], o[0]) < 1e-5
+
+
+@pytest.mark.parametrize("dt", [F32, BF16])
+@pytest.mark.parametrize("p,causal", [(0.0, 0), (0.1, 0), (0.0, 1)])
+def test_attention_fwd_bwd(dt, p, causal):
+    B, S, A, dh = 2, 128, 4, 64
+    H = A * dh
+    T = B * S
+    qkv = rn(T, 3 * H)
+    attrs = {"heads": A, "seq": S, "p": p, "seed": 3, "salt": 9, "causal": causal}
+    g, o = run_both("attention", [(qkv, dt)], [((T, H), dt), ((B * A * S, S), dt)], attrs)
+    tol = 1e-5 if dt == F32 else 2e-2
+    assert rel_err(g[0], o[0]) < tol and rel_err(g[1], o[1]) < tol, (rel_err(g[0], o[0]), rel_err(g[1], o[1]))
+    probs, dctx = o[1], rn(T, H)
+    g, o = run_both("attention_dx", [(qkv, dt), (probs, dt), (dctx, dt)], [((T, 3 * H), dt)], attrs)
+    assert rel_err(g[0], o[0]) < (1e-5 if dt == F32 else 3e-2), rel_err(g[0], o[0])
+
+
+def test_embedding_bit_exact():
+    V, H, T = 1000, 96, 513
+    ids = RNG.integers(0, V, size=T).astype(np.int32)
+    ids[:40] = 7  # collisions
+    table = rn(V, H)
+    for dt in (F32, BF16):
+        g, o = run_both("embedding", [(ids, I32), (table, dt)], [((T, H), dt)])
+        assert bits_equal(g[0], o[0])
+    dy = rn(T, H)
+    g, o = run_both("embedding_dx", [(ids, I32), (dy, F32)], [((V, H), F32)])
+    assert bits_equal(g[0], o[0])  # deterministic ordered scatter-add == oracle order
+    base = rn(V, H)
+    g, o = run_both("embedding_dx", [(ids, I32), (dy, BF16), (base, F32)], [((V, H), F32)])
+    assert bits_equal(g[0], o[0])
+
+
+@pytest.mark.parametrize("dt", [F32, BF16])
+def test_cross_entropy(dt):
+    T, V, Vp = 300, 1000, 1024
+    x = rn(T, Vp, lo=-4, hi=4)
+    lab = RNG.integers(0, V, size=T).astype(np.int32)
+    lab[::7] = -100
+    attrs = {"classes": V, "ignore_index": -100}
+    g, o = run_both("cross_entropy", [(x, dt), (lab, I32)], [((1,), F32), ((T, Vp), dt)], attrs)
+    assert abs(g[0][0] - o[0][0]) <= 1e-5 * abs(o[0][0])
+    assert rel_err(g[1], o[1]) < (1e-5 if dt == F32 else 5e-3)
+    assert np.all(g[1][:, V:] == 0) and np.all(g[1][::7] == 0)
+
+
+def test_unimplemented_is_loud():
+    from paper_2303_04759_b200.runtime import Plan, UnimplementedOp
+    with pytest.raises(UnimplementedOp):
+        Plan("b200.no_such_op", [((4,), F32)], [((4,), F32)])
+    with pytest.raises(UnimplementedOp):
+        Plan("ref.add", [((4,), F32), ((4,), F32)], [((4,), F32)])
