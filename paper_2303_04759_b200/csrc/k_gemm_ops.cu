@@ -11,8 +11,10 @@
 
 namespace tcb {
 
+// The reference dtypes (f32, emulated f16) keep the bit-exact contract of
+// matmul_ref; bf16 (the AutoCast extension) runs on the tensor cores.
 static bool want_exact(const Plan& p) {
-  return p.in[0].dtype == TCB_F32 || p.attrs.i("exact", 0) != 0;
+  return p.in[0].dtype != TCB_BF16 || p.attrs.i("exact", 0) != 0;
 }
 
 // Fill the static part of a 2-D GEMM: A, B are rank-2 dense row-major.
@@ -126,9 +128,9 @@ static void b_batch_matmul(Plan& p) {
   g.Z2 = 1;
   g.a.ld = A.shape[2];
   g.b.ld = B.shape[2];
-  g.a.s2 = A.shape[1] * A.shape[2];
-  g.b.s2 = B.shape[1] * B.shape[2];
-  g.c_s2 = g.M * g.N;
+  g.a.s1 = A.shape[1] * A.shape[2];  // z1 = z when Z2 == 1
+  g.b.s1 = B.shape[1] * B.shape[2];
+  g.c_s1 = g.M * g.N;
   g.a.dtype = A.dtype;
   g.b.dtype = B.dtype;
   g.ldc = g.N;
