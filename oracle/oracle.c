@@ -608,11 +608,13 @@ static int layer_norm_fwd(const orc_tensor* x, const orc_tensor* r, const orc_te
   return 0;
 }
 
-/* layer_norm_dx(s, gamma, mean, rstd, dy [, dres]) -> (ds, dgamma, dbeta [, dx]) */
+/* layer_norm_dx(s, gamma, mean, rstd, dy [, dy2]) -> (ds, dgamma, dbeta [, dx]).
+ * dy2 is a second incoming gradient summed into dy first (fan-out accumulation
+ * of the residual stream fused into the backward). */
 static int layer_norm_bwd(const orc_tensor* const* in, int nin, orc_tensor* out, int nout,
                           const orc_attr* a, int na) {
   const orc_tensor *s = in[0], *g = in[1], *mean_t = in[2], *rstd_t = in[3], *dy = in[4];
-  const orc_tensor* dres = nin > 5 ? in[5] : NULL;
+  const orc_tensor* dy2 = nin > 5 ? in[5] : NULL;
   const int64_t H = s->shape[s->rank - 1];
   const int64_t T = numel(s) / H;
   const float p = (float)adbl(a, na, "p", 0.0);
@@ -627,7 +629,9 @@ static int layer_norm_bwd(const orc_tensor* const* in, int nin, orc_tensor* out,
     float c1 = 0.0f, c2 = 0.0f;
     for (int64_t j = 0; j < H; ++j) {
       float xh = (F(s)[t * H + j] - mean) * rstd;
-      float gg = F(dy)[t * H + j] * F(g)[j];
+      float dyv = F(dy)[t * H + j];
+      if (dy2) dyv += F(dy2)[t * H + j];
+      float gg = dyv * F(g)[j];
       c1 += gg * xh;
       c2 += gg;
     }
@@ -636,9 +640,9 @@ static int layer_norm_bwd(const orc_tensor* const* in, int nin, orc_tensor* out,
     for (int64_t j = 0; j < H; ++j) {
       float xh = (F(s)[t * H + j] - mean) * rstd;
       float dyv = F(dy)[t * H + j];
+      if (dy2) dyv += F(dy2)[t * H + j];
       float gg = dyv * F(g)[j];
       float dsv = rstd * (gg - c2 - xh * c1);
-      if (dres) dsv += F(dres)[t * H + j];
       F(&out[0])[t * H + j] = rnd(out[0].dtype, dsv);
       if (nout > 3) {
         uint64_t idx = (uint64_t)(t * H + j);
@@ -806,6 +810,28 @@ int orc_exec(const char* op, const orc_tensor* in, int nin, orc_tensor* out, int
   }
   if (!strcmp(op, "sum")) { NEED(1, 1); return reduce_op(&in[0], &out[0], astr(A, na, "axes", ""), 0); }
   if (!strcmp(op, "mean")) { NEED(1, 1); return reduce_op(&in[0], &out[0], astr(A, na, "axes", ""), 1); }
+  if (!strcmp(op, "add_scalar")) { /* x + value, one rounding */
+    NEED(1, 1);
+    float v = (float)adbl(A, na, "value", 0.0);
+    int64_t n = numel(&out[0]);
+    for (int64_t i = 0; i < n; ++i) F(&out[0])[i] = rnd(out[0].dtype, F(&in[0])[i] + v);
+    return 0;
+  }
+  if (!strcmp(op, "fill")) {
+    if (nout < 1) return fail("fill: one output");
+    float v = (float)adbl(A, na, "value", 0.0);
+    int64_t n = numel(&out[0]);
+    for (int64_t i = 0; i < n; ++i) F(&out[0])[i] = rnd(out[0].dtype, v);
+    return 0;
+  }
+  if (!strcmp(op, "colsum")) { /* bias gradient: f32 column sums over all leading dims, rows ascending */
+    NEED(1, 1);
+    int64_t C = in[0].shape[in[0].rank - 1], R = numel(&in[0]) / C;
+    for (int64_t j = 0; j < C; ++j) F(&out[0])[j] = 0.0f;
+    for (int64_t r = 0; r < R; ++r)
+      for (int64_t j = 0; j < C; ++j) F(&out[0])[j] += F(&in[0])[r * C + j];
+    return 0;
+  }
   if (!strcmp(op, "mse")) { /* backends.hpp:205-214: sequential acc, then a divide */
     NEED(2, 1);
     float acc = 0.0f;

@@ -360,4 +360,43 @@ static void b_dropout(Plan& p) {
 }
 TCB_REGISTER("dropout", b_dropout);
 
+// --------------------------------------------------------- add_scalar / fill
+template <typename T>
+__global__ void k_add_scalar(const T* __restrict__ x, T* __restrict__ y, int64_t n, float v) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    y[i] = from_f<T>(__fadd_rn(to_f(x[i]), v));
+}
+static void b_add_scalar(Plan& p) {
+  check_arity(p, 1, 1, 1, 1);
+  require(p.in[0].dtype == p.out[0].dtype && same_shape(p.in[0], p.out[0]), "add_scalar: shape/dtype");
+  const int64_t n = p.out[0].numel();
+  const float v = float(p.attrs.f("value", 0.0));
+  dispatch_float(p.out[0].dtype, [&](auto* tp) {
+    using T = std::remove_pointer_t<decltype(tp)>;
+    p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
+      k_add_scalar<T><<<grid_for(n, 256), 256, 0, s>>>((const T*)in[0].ptr, (T*)out[0].ptr, n, v);
+    };
+  });
+}
+TCB_REGISTER("add_scalar", b_add_scalar);
+
+template <typename T>
+__global__ void k_fill(T* __restrict__ y, int64_t n, float v) {
+  const T t = from_f<T>(v);
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    y[i] = t;
+}
+static void b_fill(Plan& p) {
+  check_arity(p, 0, 0, 1, 1);
+  const int64_t n = p.out[0].numel();
+  const float v = float(p.attrs.f("value", 0.0));
+  dispatch_float(p.out[0].dtype, [&](auto* tp) {
+    using T = std::remove_pointer_t<decltype(tp)>;
+    p.run = [=](const tcb_tensor*, tcb_tensor* out, cudaStream_t s) {
+      k_fill<T><<<grid_for(n, 256), 256, 0, s>>>((T*)out[0].ptr, n, v);
+    };
+  });
+}
+TCB_REGISTER("fill", b_fill);
+
 }  // namespace tcb

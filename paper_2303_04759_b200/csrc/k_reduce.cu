@@ -169,6 +169,39 @@ static void b_mean(Plan& p) { build_reduce(p, 1); }
 TCB_REGISTER("sum", b_sum);
 TCB_REGISTER("mean", b_mean);
 
+// colsum: f32 column sums over all leading dims (bias gradients of [T, N]
+// GEMM outputs); exact row order for f32 input, split-row tree otherwise.
+static void b_colsum(Plan& p) {
+  check_arity(p, 1, 1, 1, 1);
+  const Spec& X = p.in[0];
+  require(is_float(X.dtype), "colsum: float input");
+  require(p.out[0].dtype == TCB_F32, "colsum: output is f32");
+  const int64_t C = X.dim(-1), R = X.numel() / C;
+  require(p.out[0].numel() == C, "colsum: output must have the last dim's size");
+  RedGeom g{};
+  g.rank = 2;
+  g.shape[0] = R;
+  g.shape[1] = C;
+  g.reduced[0] = 1;
+  g.count = R;
+  const bool exact = X.dtype == TCB_F32 || p.attrs.i("exact", 0) != 0;
+  dispatch_float(X.dtype, [&](auto* tp) {
+    using T = std::remove_pointer_t<decltype(tp)>;
+    if (exact) {
+      p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
+        k_reduce_exact<T, float><<<unsigned((C + 127) / 128), 128, 0, s>>>((const T*)in[0].ptr,
+                                                                           (float*)out[0].ptr, C, g, 0);
+      };
+    } else {
+      p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
+        k_reduce_cols<T, float><<<unsigned((C + 31) / 32), 256, 0, s>>>((const T*)in[0].ptr,
+                                                                        (float*)out[0].ptr, 1, R, C, 1.0f);
+      };
+    }
+  });
+}
+TCB_REGISTER("colsum", b_colsum);
+
 // mse: sequential f32 sum of squared differences, then acc / numel (a divide)
 template <typename T>
 __global__ void k_mse_exact(const T* __restrict__ a, const T* __restrict__ b, float* o, int64_t n) {

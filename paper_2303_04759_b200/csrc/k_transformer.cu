@@ -236,7 +236,8 @@ TCB_REGISTER("layer_norm", b_layer_norm);
 TCB_REGISTER("add_layer_norm", b_add_layer_norm);
 
 // ------------------------------------------------------------ layer norm bwd
-// ds = rstd*(g - mean(g) - xh*mean(g*xh)) [+ dres]; dx = dropout(ds);
+// dy += dy2 (fused fan-out accumulation); ds = rstd*(g - mean(g) - xh*mean(g*xh));
+// dx = dropout(ds);
 // per-CTA partial column sums of dy*xh and dy -> ws, then k_colsum finalises.
 constexpr int LNB_ROWS = 32;  // rows per CTA (8 warps x 4 rows)
 
@@ -244,7 +245,7 @@ template <typename T>
 __global__ void __launch_bounds__(256) k_ln_bwd(const T* __restrict__ sx, const float* __restrict__ gamma_f,
                                                 const T* __restrict__ gamma_t, const float* __restrict__ mean,
                                                 const float* __restrict__ rstd, const T* __restrict__ dy,
-                                                const T* __restrict__ dres, T* __restrict__ ds_o,
+                                                const T* __restrict__ dy2, T* __restrict__ ds_o,
                                                 T* __restrict__ dx_o, float* __restrict__ ws, int64_t rows,
                                                 int H, DropCfg d, bool vec) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -269,6 +270,12 @@ __global__ void __launch_bounds__(256) k_ln_bwd(const T* __restrict__ sx, const 
         float sv[8], dv[8];
         ld8(sx, i, (row + 1) * int64_t(H), vec, sv);
         ld8(dy, i, (row + 1) * int64_t(H), vec, dv);
+        if (dy2) {
+          float d2[8];
+          ld8(dy2, i, (row + 1) * int64_t(H), vec, d2);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) dv[k] = __fadd_rn(dv[k], d2[k]);
+        }
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
           const int j = ch * 8 + k;
@@ -293,13 +300,9 @@ __global__ void __launch_bounds__(256) k_ln_bwd(const T* __restrict__ sx, const 
       const int ch = lane + c * 32;
       if (ch < nch) {
         const int64_t i = row * H + ch * 8;
-        float o[8], res[8];
-        if (dres) ld8(dres, i, (row + 1) * int64_t(H), vec, res);
+        float o[8];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          o[k] = rs * (g[c][k] - c2 - xh[c][k] * c1);
-          if (dres) o[k] += res[k];
-        }
+        for (int k = 0; k < 8; ++k) o[k] = rs * (g[c][k] - c2 - xh[c][k] * c1);
         st8(ds_o, i, (row + 1) * int64_t(H), vec, o);
         if (dx_o) {
           const uint32_t bits = drop_bits8(d, uint64_t(i));

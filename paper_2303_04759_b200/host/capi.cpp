@@ -1,0 +1,349 @@
+// capi.cpp -- libtrainc_b200.so: the C entry points of the b200 training-step
+// runtime (graph build -> autodiff -> fusion -> memsched -> dispatch -> device
+// VM), used by bench.py / tests / __graft_entry__ through ctypes.  This is the
+// host side "above the C ABI": C++ over the reference's IR/registry, calling
+// libtcb200.so for every kernel.
+#include <chrono>
+#include <cstring>
+#include <memory>
+#include <sstream>
+
+#include "models.hpp"
+#include "vm.hpp"
+
+namespace tb {
+
+static thread_local std::string g_err;
+
+struct Session {
+  ModelCfg cfg;
+  TrainStep ts;
+  FunctionPtr fn;  // dispatched, scheduled (and rematerialised) step
+  DeviceVM vm;
+  void* stream = nullptr;
+  int device = 0;
+  int rank = 0;
+  int32_t* h_ids = nullptr;  // pinned staging
+  int32_t* h_labels = nullptr;
+  float* h_loss = nullptr;
+  RematPlan remat;
+  int64_t budget = 0;
+  double compile_ms = 0;
+  std::string text;
+};
+
+static std::string print_fn(const ir::FunctionIR& fn) {
+  std::ostringstream os;
+  os << "fn " << fn.name << "(";
+  for (size_t i = 0; i < fn.params.size(); ++i)
+    os << (i ? ", " : "") << "%" << fn.params[i]->id << ": " << type_str(fn.params[i]->ty);
+  os << ") {\n";
+  auto seq = ir::flatten(fn);
+  for (auto& b : seq.lets) {
+    os << "  let %" << b.var->id << " = ";
+    if (b.value->kind == ExprKind::TupleGet) {
+      os << "%" << b.value->args[0]->var->id << "." << b.value->index;
+    } else {
+      os << b.value->op << "(";
+      for (size_t i = 0; i < b.value->args.size(); ++i)
+        os << (i ? ", " : "") << "%" << b.value->args[i]->var->id;
+      os << ")";
+      if (!b.value->call_attrs.empty()) {
+        os << " @{";
+        bool first = true;
+        for (auto& [k, v] : b.value->call_attrs) {
+          os << (first ? "" : ", ") << k << "=";
+          first = false;
+          if (auto* i = std::get_if<std::int64_t>(&v)) os << *i;
+          else if (auto* d = std::get_if<double>(&v)) os << *d;
+          else os << std::get<std::string>(v);
+        }
+        os << "}";
+      }
+    }
+    os << " : " << type_str(b.var->ty) << ";\n";
+  }
+  os << "  (";
+  if (seq.ret)
+    for (size_t i = 0; i < seq.ret->args.size(); ++i) os << (i ? ", " : "") << "%" << seq.ret->args[i]->var->id;
+  os << ")\n}\n";
+  return os.str();
+}
+
+}  // namespace tb
+
+using namespace tb;
+
+#define TB_TRY(...)                          \
+  try {                                      \
+    __VA_ARGS__;                             \
+    return 0;                                \
+  } catch (const std::exception& e) {        \
+    g_err = e.what();                        \
+    return 1;                                \
+  }
+
+extern "C" {
+
+const char* tb_last_error(void) { return g_err.c_str(); }
+
+/// cfg: "kind=bert;L=12;H=768;..." plus optional runtime keys
+///   budget=<bytes>  rematerialise the step under this memory budget
+///   schedule=1      p-c list scheduling
+///   rank=<r>        ZeRO rank (with world=<n>)
+// graph pipeline shared by the device session and the CPU-only inspection
+// entry points: build -> autodiff/fusion -> [schedule] -> [remat] -> dispatch
+static void prepare(Session& s, const char* cfg_c) {
+  ensure_registered(split_ws(tcb_supported_ops()));
+  std::string model, all = cfg_c ? cfg_c : "";
+  std::istringstream is(all);
+  std::string kv;
+  int do_schedule = 0;
+  while (std::getline(is, kv, ';')) {
+    if (kv.rfind("budget=", 0) == 0) s.budget = std::stoll(kv.substr(7));
+    else if (kv.rfind("schedule=", 0) == 0) do_schedule = std::stoi(kv.substr(9));
+    else if (kv.rfind("rank=", 0) == 0) s.rank = std::stoi(kv.substr(5));
+    else if (!kv.empty()) model += kv + ";";
+  }
+  s.cfg = parse_cfg(model);
+  s.ts = build_train_step(s.cfg);
+  FunctionPtr fn = s.ts.fn;
+  if (do_schedule) fn = ir::make_fn(fn->name, fn->params, schedule(*fn, s.ts.state_binding));
+  if (s.budget > 0) {
+    auto [rf, plan] = rematerialize(*fn, s.budget, s.ts.state_binding);
+    fn = rf;
+    s.remat = plan;
+  }
+  // dispatch (opreg.hpp:740-766 semantics) to the b200 dialect on "cuda"
+  LetSeq seq = ir::flatten(*fn);
+  opreg::DispatchConfig dc;
+  dc.device = "cuda";
+  dc.enabled_dialects = {"b200"};
+  dispatch_anf(seq, dc);
+  s.fn = ir::make_fn(fn->name, fn->params, seq);
+}
+
+/// CPU-only: build the step graph and its memory plan without a device.
+/// out: P, P_pad, lets, planner_peak, arena_plan_bytes, state_bytes, fused_dact,
+/// fused_ln_dy2, fused_emb, dead, remat_replays, peak_before_remat, peak_after_remat
+int tb_graph_info(const char* cfg, int64_t* out, int n) {
+  TB_TRY({
+    Session s;
+    prepare(s, cfg);
+    Layout L = build_layout(*s.fn, s.ts.state_binding);
+    MemProfile mp = peak_memory(L);
+    ArenaPlan ap = plan_arena(L);
+    int64_t v[] = {s.ts.P, s.ts.P_pad, L.n, mp.peak, ap.size, mp.state_bytes, s.ts.fusion.dact, s.ts.fusion.ln_dy2,
+                   s.ts.fusion.emb_base, s.ts.fusion.dead, s.remat.replays, s.remat.peak_before, s.remat.peak_after};
+    for (int i = 0; i < n && i < int(sizeof v / sizeof v[0]); ++i) out[i] = v[i];
+  });
+}
+
+static thread_local std::string g_text;
+const char* tb_graph_text(const char* cfg, const char* what) {
+  try {
+    Session s;
+    prepare(s, cfg);
+    std::string w = what ? what : "";
+    if (w == "mem") {
+      auto mp = peak_memory(build_layout(*s.fn, s.ts.state_binding));
+      std::ostringstream os;
+      os << "index,live_bytes\n";
+      for (size_t i = 0; i < mp.curve.size(); ++i) os << i << "," << mp.curve[i] << "\n";
+      g_text = os.str();
+    } else {
+      g_text = print_fn(*s.fn);
+    }
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    g_text.clear();
+  }
+  return g_text.c_str();
+}
+
+void* tb_session_create(const char* cfg_c, int device) {
+  try {
+    auto t0 = std::chrono::steady_clock::now();
+    auto s = std::make_unique<Session>();
+    s->device = device;
+    prepare(*s, cfg_c);
+    s->vm.set_device(device);
+    s->vm.compile(s->fn, s->ts.state_binding);
+    tcb_check(tcb_stream_create(&s->stream), "stream");
+    const int64_t T = s->cfg.T();
+    tcb_check(tcb_host_alloc(reinterpret_cast<void**>(&s->h_ids), uint64_t(T) * 4), "pinned");
+    tcb_check(tcb_host_alloc(reinterpret_cast<void**>(&s->h_labels), uint64_t(T) * 4), "pinned");
+    tcb_check(tcb_host_alloc(reinterpret_cast<void**>(&s->h_loss), 64), "pinned");
+    // constant inputs: position ids (t mod S) and token types (0)
+    std::vector<int32_t> pos(static_cast<size_t>(T)), typ(static_cast<size_t>(T), 0);
+    for (int64_t t = 0; t < T; ++t) pos[size_t(t)] = int32_t(t % s->cfg.S);
+    tcb_check(tcb_memcpy(s->vm.param_ptr(s->ts.i_pos), pos.data(), uint64_t(T) * 4, 0, nullptr), "pos");
+    if (s->ts.i_type >= 0)
+      tcb_check(tcb_memcpy(s->vm.param_ptr(s->ts.i_type), typ.data(), uint64_t(T) * 4, 0, nullptr), "type");
+    tcb_check(tcb_device_sync(), "sync");
+    s->compile_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    return s.release();
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
+
+void tb_session_destroy(void* h) {
+  auto* s = static_cast<Session*>(h);
+  if (!s) return;
+  if (s->stream) tcb_stream_destroy(s->stream);
+  if (s->h_ids) tcb_host_free(s->h_ids);
+  if (s->h_labels) tcb_host_free(s->h_labels);
+  if (s->h_loss) tcb_host_free(s->h_loss);
+  delete s;
+}
+
+/// out[0..]: P, P_pad, T, arena_bytes, state_bytes, planner_peak, instructions,
+/// kernels_per_step, lets, fused_dact, fused_ln_dy2, fused_emb, dead, remat_replays,
+/// peak_before_remat, compile_us, shard
+int tb_session_info(void* h, int64_t* out, int n) {
+  TB_TRY({
+    auto* s = static_cast<Session*>(h);
+    const auto& st = s->vm.stats();
+    int64_t v[] = {s->ts.P, s->ts.P_pad, s->cfg.T(), st.arena_bytes, st.state_bytes, st.planner_peak,
+                   st.instructions, st.kernels, st.lets, s->ts.fusion.dact, s->ts.fusion.ln_dy2,
+                   s->ts.fusion.emb_base, s->ts.fusion.dead, s->remat.replays, s->remat.peak_before,
+                   int64_t(s->compile_ms * 1000), s->ts.shard()};
+    for (int i = 0; i < n && i < int(sizeof v / sizeof v[0]); ++i) out[i] = v[i];
+  });
+}
+
+int tb_session_init_params(void* h) {
+  TB_TRY({
+    auto* s = static_cast<Session*>(h);
+    std::vector<float> p = init_params(s->ts);
+    const int64_t sh = s->cfg.world > 1 ? s->ts.shard() : s->ts.P_pad;
+    const float* mine = p.data() + size_t(s->cfg.world > 1 ? s->rank * sh : 0);
+    tcb_check(tcb_memcpy(s->vm.param_ptr(s->ts.i_params), mine, uint64_t(sh) * 4, 0, nullptr), "params");
+    if (s->ts.i_p16 >= 0) {
+      std::vector<uint16_t> h16(p.size());
+      for (size_t i = 0; i < p.size(); ++i) h16[i] = bf16_bits(p[i]);
+      tcb_check(tcb_memcpy(s->vm.param_ptr(s->ts.i_p16), h16.data(), uint64_t(h16.size()) * 2, 0, nullptr), "p16");
+    }
+    if (s->ts.i_m >= 0) {
+      tcb_check(tcb_memset(s->vm.param_ptr(s->ts.i_m), 0, uint64_t(sh) * 4, nullptr), "m");
+      tcb_check(tcb_memset(s->vm.param_ptr(s->ts.i_v), 0, uint64_t(sh) * 4, nullptr), "v");
+      tcb_check(tcb_memset(s->vm.param_ptr(s->ts.i_step), 0, 4, nullptr), "step");
+    }
+    tcb_check(tcb_device_sync(), "sync");
+  });
+}
+
+/// Synthetic MLM batch: ids = Rng(seed).below(V); 15% of the
+/// positions (Rng.below(100) < 15) carry their id as label, the rest -100.
+int tb_synthetic_batch(int64_t T, int64_t V, int64_t seed, int32_t* ids, int32_t* labels, int causal_lm) {
+  TB_TRY({
+    Rng r(static_cast<uint64_t>(seed));
+    for (int64_t t = 0; t < T; ++t) ids[t] = int32_t(r.below(uint32_t(V)));
+    for (int64_t t = 0; t < T; ++t) {
+      if (causal_lm) labels[t] = (t + 1 < T) ? ids[t + 1] : -100;
+      else labels[t] = r.below(100) < 15 ? ids[t] : -100;
+    }
+  });
+}
+
+/// Copy a batch from host memory into the step's input buffers (H2D on the
+/// session stream, through the pinned staging buffers).
+int tb_session_set_batch(void* h, const int32_t* ids, const int32_t* labels) {
+  TB_TRY({
+    auto* s = static_cast<Session*>(h);
+    const int64_t T = s->cfg.T();
+    if (ids != s->h_ids) std::memcpy(s->h_ids, ids, size_t(T) * 4);
+    if (labels != s->h_labels) std::memcpy(s->h_labels, labels, size_t(T) * 4);
+    tcb_check(tcb_memcpy(s->vm.param_ptr(s->ts.i_ids), s->h_ids, uint64_t(T) * 4, 0, s->stream), "ids");
+    tcb_check(tcb_memcpy(s->vm.param_ptr(s->ts.i_labels), s->h_labels, uint64_t(T) * 4, 0, s->stream), "labels");
+  });
+}
+
+/// pinned staging pointers (so callers can fill them without an extra copy)
+int32_t* tb_session_ids_buffer(void* h) { return static_cast<Session*>(h)->h_ids; }
+int32_t* tb_session_labels_buffer(void* h) { return static_cast<Session*>(h)->h_labels; }
+
+int tb_session_step(void* h, int use_graph) {
+  TB_TRY({
+    auto* s = static_cast<Session*>(h);
+    s->vm.run(s->stream, use_graph != 0);
+  });
+}
+
+/// enqueue the D2H read of the loss; *out valid after tb_session_sync
+int tb_session_fetch_loss(void* h) {
+  TB_TRY({
+    auto* s = static_cast<Session*>(h);
+    auto seq = ir::flatten(s->vm.fn());
+    const ir::Var* lv = seq.ret->args.at(0)->var.get();
+    tcb_check(tcb_memcpy(s->h_loss, s->vm.ptr_of(lv), 4, 1, s->stream), "loss");
+  });
+}
+float tb_session_loss_value(void* h) { return static_cast<Session*>(h)->h_loss[0]; }
+
+int tb_session_sync(void* h) { TB_TRY(tcb_check(tcb_stream_sync(static_cast<Session*>(h)->stream), "sync")); }
+
+void* tb_session_stream(void* h) { return static_cast<Session*>(h)->stream; }
+
+/// device pointer / byte size of function parameter `name` (ids, labels,
+/// params, p16, m, v, step, ...)
+int tb_session_param(void* h, const char* name, void** ptr, int64_t* bytes) {
+  TB_TRY({
+    auto* s = static_cast<Session*>(h);
+    const auto& ps = s->vm.fn().params;
+    for (size_t i = 0; i < ps.size(); ++i)
+      if (ps[i]->id == name) {
+        *ptr = s->vm.param_ptr(int(i));
+        *bytes = nbytes(ps[i]->ty);
+        return 0;
+      }
+    throw Error(std::string("no parameter ") + name);
+  });
+}
+
+/// offsets/shapes of the flat parameter segments: "name offset numel\n"
+const char* tb_session_segments(void* h) {
+  auto* s = static_cast<Session*>(h);
+  std::ostringstream os;
+  for (auto& g : s->ts.segs) os << g.name << " " << g.offset << " " << g.numel << "\n";
+  s->text = os.str();
+  return s->text.c_str();
+}
+
+/// "ir": the dispatched step function; "bytecode": VM disassembly;
+/// "mem": liveness/peak CSV (index,live_bytes,op) as `trainc inspect --mem`
+const char* tb_session_text(void* h, const char* what) {
+  auto* s = static_cast<Session*>(h);
+  std::string w = what ? what : "";
+  if (w == "ir") s->text = print_fn(s->vm.fn());
+  else if (w == "bytecode") s->text = s->vm.disasm();
+  else if (w == "mem") {
+    auto mp = peak_memory(s->vm.layout());
+    auto seq = ir::flatten(s->vm.fn());
+    std::ostringstream os;
+    os << "index,live_bytes,op\n";
+    for (size_t i = 0; i < mp.curve.size() && i < seq.lets.size(); ++i)
+      os << i << "," << mp.curve[i] << ","
+         << (seq.lets[i].value->kind == ExprKind::Call ? seq.lets[i].value->op : "tuple_get") << "\n";
+    s->text = os.str();
+  } else s->text = "";
+  return s->text.c_str();
+}
+
+int tb_session_set_comm(void* h, void* comm) {
+  TB_TRY(static_cast<Session*>(h)->vm.set_comm(comm));
+}
+
+/// KernelCache counters (backends.hpp:363-368): compiles, hits, size
+int tb_cache_stats(int64_t* out3) {
+  TB_TRY({
+    auto& c = backends::KernelCache::global();
+    out3[0] = int64_t(c.compiles());
+    out3[1] = int64_t(c.hits());
+    out3[2] = int64_t(c.size());
+  });
+}
+
+}  // extern "C"

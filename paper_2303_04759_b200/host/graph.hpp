@@ -1,0 +1,509 @@
+// graph.hpp -- typed ANF construction, reverse-mode autodiff and the peephole
+// fusion pass, all over the reference IR (ir.hpp) and registry (opreg.hpp).
+//
+//  Graph      incremental ANF emitter on top of ir::AnfBuilder (ir.hpp:265-313)
+//             that runs each op's type relation as it is emitted, so every Var
+//             carries its TensorType/TupleType immediately.
+//  autodiff   SPEC.md:217-279: reverse traversal of the let sequence, one
+//             adjoint rule per base op, fan-out accumulation as an explicit
+//             `add` chain in deterministic reverse-traversal order.  Leaves are
+//             `view`s of a flat parameter buffer; their gradients are emitted as
+//             one flat `concat` in offset order (the buffer the optimizer and the
+//             ZeRO reduce-scatter consume as a single segment).
+//  fuse       SPEC.md:346-422 restricted to the patterns the b200 kernels
+//             implement: dact into the producing dgrad GEMM epilogue, residual
+//             gradient sums into layer_norm_dx, tied-embedding accumulation into
+//             embedding_dx; then dead-let elimination.
+#pragma once
+
+#include <algorithm>
+#include <functional>
+#include <map>
+#include <set>
+#include <unordered_map>
+
+#include "ext_ops.hpp"
+
+namespace tb {
+
+using ir::ExprKind;
+using ir::ExprPtr;
+using ir::FunctionPtr;
+using ir::LetBinding;
+using ir::LetSeq;
+using ir::VarPtr;
+
+inline AttrMap attrs_merge(AttrMap a, const AttrMap& b) {
+  for (auto& [k, v] : b) a[k] = v;
+  return a;
+}
+
+class Graph {
+ public:
+  explicit Graph(std::string name = "train_step") : name_(std::move(name)), ab_("t") {}
+
+  VarPtr param(const std::string& id, TensorType ty, AttrMap attrs = {}) {
+    auto v = ir::make_var(id, Type(ty), std::move(attrs));
+    ab_.reserve(id);
+    params_.push_back(v);
+    return v;
+  }
+
+  /// Emit `op(args...)` as a let; the type relation runs now.
+  VarPtr op(const std::string& name, const std::vector<VarPtr>& args, AttrMap attrs = {},
+            const std::string& hint = "") {
+    std::vector<ExprPtr> xs;
+    std::vector<Type> tys;
+    for (auto& a : args) {
+      if (!a) throw Error("internal: null argument to " + name);
+      xs.push_back(ir::var_ref(a));
+      tys.push_back(a->ty);
+    }
+    const auto& base = opreg::registry().base_of(name);
+    if (base.arity >= 0 && int(args.size()) != base.arity)
+      throw TypeError(name + ": expects " + std::to_string(base.arity) + " args, got " +
+                      std::to_string(args.size()));
+    Type out = opreg::registry().type_rel_of(name)(tys, attrs);
+    auto call = ir::call(name, std::move(xs), std::move(attrs));
+    call->ty = out;
+    auto v = ab_.emit(call, hint.empty() ? "t" : hint);
+    v->ty = out;
+    return v;
+  }
+
+  VarPtr get(const VarPtr& tup, int i, const std::string& hint = "") {
+    if (!tup->ty.is_tuple()) throw TypeError("tuple_get on non-tuple %" + tup->id);
+    auto e = ir::tuple_get(ir::var_ref(tup), i);
+    Type t = tup->ty.tuple().fields.at(i);
+    e->ty = t;
+    auto v = ab_.emit(e, hint.empty() ? "t" : hint);
+    v->ty = t;
+    return v;
+  }
+
+  LetSeq& seq() { return ab_.seq(); }
+  const std::vector<VarPtr>& params() const { return params_; }
+
+  FunctionPtr finish(const std::vector<VarPtr>& rets) {
+    LetSeq s = ab_.seq();
+    std::vector<ExprPtr> xs;
+    TupleType tt;
+    for (auto& r : rets) {
+      xs.push_back(ir::var_ref(r));
+      tt.fields.push_back(r->ty.tensor());
+    }
+    s.ret = ir::tuple(xs);
+    s.ret->ty = tt;
+    return ir::make_fn(name_, params_, s);
+  }
+
+ private:
+  std::string name_;
+  ir::AnfBuilder ab_;
+  std::vector<VarPtr> params_;
+};
+
+inline const std::string& call_op(const LetBinding& b) { return b.value->op; }
+inline VarPtr arg_var(const ExprPtr& call, size_t i) {
+  const auto& a = call->args.at(i);
+  return a->kind == ExprKind::VarRef ? a->var : nullptr;
+}
+
+// ------------------------------------------------------------------ autodiff
+
+/// A differentiable leaf: a `view` of a flat parameter buffer, with the offset
+/// of its master (f32) segment in the gradient buffer.
+struct Leaf {
+  VarPtr view;
+  int64_t offset;  // element offset in the flat master buffer
+  int64_t numel;
+};
+
+struct AdjointCtx {
+  Graph& g;
+  const LetBinding& let;
+  std::vector<VarPtr> dout;  // per output field (tensor ops: size 1); null = no grad
+};
+using Adjoint = std::function<std::vector<VarPtr>(AdjointCtx&)>;  // grad per input (null = none)
+
+inline std::map<std::string, Adjoint>& adjoints() {
+  static std::map<std::string, Adjoint> m;
+  return m;
+}
+
+inline AttrMap pick(const AttrMap& a, std::initializer_list<const char*> keys) {
+  AttrMap r;
+  for (auto* k : keys)
+    if (a.count(k)) r[k] = a.at(k);
+  return r;
+}
+
+/// Gradient of an elementwise input whose shape may be broadcast (trailing
+/// dims, opreg.hpp:75-87): reduce over the broadcast dims.
+inline VarPtr unbroadcast(Graph& g, const VarPtr& grad, const TensorType& target) {
+  const auto& gt = grad->ty.tensor();
+  if (gt.shape == target.shape) return grad;
+  // only the bias-style case [.., N] -> [N] is needed by the models
+  if (target.rank() == 1 && target.shape[0] == gt.shape.back()) {
+    VarPtr s = g.op("colsum", {grad});
+    if (target.dtype != kF32) s = g.op("convert", {s}, {{"to", std::string(dtype_str(target.dtype))}});
+    return s;
+  }
+  if (numel(target) == numel(gt))
+    return g.op("reshape", {grad}, {{"shape", opreg::shape_attr(target.shape)}});
+  throw NonDifferentiable("unbroadcast from " + type_str(gt) + " to " + type_str(target));
+}
+
+inline void register_default_adjoints() {
+  auto& A = adjoints();
+  if (!A.empty()) return;
+  // --- reference base ops ---
+  A["add"] = [](AdjointCtx& c) -> std::vector<VarPtr> {
+    auto a = arg_var(c.let.value, 0), b = arg_var(c.let.value, 1);
+    return {a ? unbroadcast(c.g, c.dout[0], a->ty.tensor()) : nullptr,
+            b ? unbroadcast(c.g, c.dout[0], b->ty.tensor()) : nullptr};
+  };
+  A["sub"] = [](AdjointCtx& c) -> std::vector<VarPtr> {
+    auto b = arg_var(c.let.value, 1);
+    return {c.dout[0], b ? c.g.op("neg", {unbroadcast(c.g, c.dout[0], b->ty.tensor())}) : nullptr};
+  };
+  A["mul"] = [](AdjointCtx& c) -> std::vector<VarPtr> {
+    auto a = arg_var(c.let.value, 0), b = arg_var(c.let.value, 1);
+    return {b ? unbroadcast(c.g, c.g.op("mul", {c.dout[0], b}), a->ty.tensor()) : nullptr,
+            a ? unbroadcast(c.g, c.g.op("mul", {c.dout[0], a}), b->ty.tensor()) : nullptr};
+  };
+  A["neg"] = [](AdjointCtx& c) -> std::vector<VarPtr> { return {c.g.op("neg", {c.dout[0]})}; };
+  // tanh: NeedsY, dx = tanh_dx(y, dy) = dy * (1 - y^2) -- not the paper's 1-2y
+  A["tanh"] = [](AdjointCtx& c) -> std::vector<VarPtr> { return {c.g.op("tanh_dx", {c.let.var, c.dout[0]})}; };
+  // relu: NeedsX, subgradient 0 at the kink via gtz
+  A["relu"] = [](AdjointCtx& c) -> std::vector<VarPtr> {
+    return {c.g.op("mul", {c.dout[0], c.g.op("gtz", {arg_var(c.let.value, 0)})})};
+  };
+  A["gelu"] = [](AdjointCtx& c) -> std::vector<VarPtr> {
+    return {c.g.op("gelu_dx", {arg_var(c.let.value, 0), c.dout[0]})};
+  };
+  // matmul: dA = dY B^T, dB = A^T dY with the transposes absorbed
+  A["matmul"] = [](AdjointCtx& c) -> std::vector<VarPtr> {
+    auto a = arg_var(c.let.value, 0), b = arg_var(c.let.value, 1);
+    return {c.g.op("matmul_t", {c.dout[0], b}, {{"tb", std::int64_t(1)}}),
+            c.g.op("matmul_t", {a, c.dout[0]}, {{"ta", std::int64_t(1)}})};
+  };
+  A["convert"] = [](AdjointCtx& c) -> std::vector<VarPtr> {
+    auto a = arg_var(c.let.value, 0);
+    return {c.g.op("convert", {c.dout[0]}, {{"to", std::string(dtype_str(a->ty.tensor().dtype))}})};
+  };
+  A["reshape"] = [](AdjointCtx& c) -> std::vector<VarPtr> {
+    auto a = arg_var(c.let.value, 0);
+    return {c.g.op("reshape", {c.dout[0]}, {{"shape", opreg::shape_attr(a->ty.tensor().shape)}})};
+  };
+  A["dropout"] = [](AdjointCtx& c) -> std::vector<VarPtr> {
+    return {c.g.op("dropout", {c.dout[0]}, pick(c.let.value->call_attrs, {"p", "seed", "salt"}))};
+  };
+  // --- extension ops ---
+  // linear: du = dy * act'(u); dx = du W^T; dW = x^T du (f32, the master grad);
+  // db = colsum(du).  Needs u (save_preact) for relu/gelu, y for tanh.
+  A["linear"] = [](AdjointCtx& c) -> std::vector<VarPtr> {
+    const auto& at = c.let.value->call_attrs;
+    const std::string act = ir::attr_string(at, "act", "none");
+    const int tw = int(ir::attr_int(at, "tw", 0));
+    auto x = arg_var(c.let.value, 0), w = arg_var(c.let.value, 1);
+    VarPtr dy = c.dout[0];
+    if (!dy) return {nullptr, nullptr, nullptr};
+    VarPtr du = dy;
+    if (act != "none") {
+      if (act == "tanh") {
+        VarPtr y = c.let.var->ty.is_tuple() ? c.g.get(c.let.var, 0) : c.let.var;
+        du = c.g.op("tanh_dx", {y, dy});
+      } else {
+        if (!c.let.var->ty.is_tuple()) throw NonDifferentiable("linear(act=" + act + ") needs save_preact=1");
+        VarPtr u = c.g.get(c.let.var, 1);
+        du = act == "gelu" ? c.g.op("gelu_dx", {u, dy}) : c.g.op("mul", {dy, c.g.op("gtz", {u})});
+      }
+    }
+    VarPtr dx = c.g.op("matmul_t", {du, w}, {{"tb", std::int64_t(tw ? 0 : 1)}});
+    VarPtr dw = tw ? c.g.op("matmul_t", {du, x}, {{"ta", std::int64_t(1)}, {"out", std::string("f32")}})
+                   : c.g.op("matmul_t", {x, du}, {{"ta", std::int64_t(1)}, {"out", std::string("f32")}});
+    VarPtr db = c.g.op("colsum", {du});
+    return {dx, dw, db};
+  };
+  A["attention"] = [](AdjointCtx& c) -> std::vector<VarPtr> {
+    if (!c.dout[0]) return {nullptr};
+    auto qkv = arg_var(c.let.value, 0);
+    VarPtr probs = c.g.get(c.let.var, 1);
+    return {c.g.op("attention_dx", {qkv, probs, c.dout[0]}, c.let.value->call_attrs)};
+  };
+  A["layer_norm"] = [](AdjointCtx& c) -> std::vector<VarPtr> {
+    if (!c.dout[0]) return {nullptr, nullptr, nullptr};
+    auto x = arg_var(c.let.value, 0), gm = arg_var(c.let.value, 1);
+    auto t = c.g.op("layer_norm_dx", {x, gm, c.g.get(c.let.var, 1), c.g.get(c.let.var, 2), c.dout[0]});
+    return {c.g.get(t, 0), c.g.get(t, 1), c.g.get(t, 2)};
+  };
+  A["add_layer_norm"] = [](AdjointCtx& c) -> std::vector<VarPtr> {
+    if (!c.dout[0]) return {nullptr, nullptr, nullptr, nullptr};
+    auto gm = arg_var(c.let.value, 2);
+    const auto& at = c.let.value->call_attrs;
+    auto t = c.g.op("layer_norm_dx", {c.g.get(c.let.var, 1), gm, c.g.get(c.let.var, 2), c.g.get(c.let.var, 3), c.dout[0]},
+                    pick(at, {"p", "seed", "salt"}));
+    VarPtr ds = c.g.get(t, 0);
+    VarPtr dx = ir::attr_double(at, "p", 0.0) > 0.0 ? c.g.get(t, 3) : ds;
+    return {dx, ds, c.g.get(t, 1), c.g.get(t, 2)};
+  };
+  A["embedding"] = [](AdjointCtx& c) -> std::vector<VarPtr> {
+    auto ids = arg_var(c.let.value, 0), tab = arg_var(c.let.value, 1);
+    return {nullptr, c.g.op("embedding_dx", {ids, c.dout[0]}, {{"rows", tab->ty.tensor().shape[0]}})};
+  };
+  // monolithic CE adjoint: dlogits is the op's second output; the
+  // loss is the function's final output so d loss = 1.
+  A["cross_entropy"] = [](AdjointCtx& c) -> std::vector<VarPtr> {
+    if (!c.let.var->ty.is_tuple()) throw NonDifferentiable("cross_entropy needs grad=1");
+    return {c.g.get(c.let.var, 1), nullptr};
+  };
+}
+
+struct GradResult {
+  VarPtr flat_grad;  // f32 [P] in leaf-offset order
+};
+
+/// Reverse-mode AD of `loss` w.r.t. the leaves (which must tile [0, P) of the
+/// flat master buffer).  Appends the backward lets to `g` and returns the flat
+/// gradient var.
+inline GradResult autodiff(Graph& g, const VarPtr& loss, std::vector<Leaf> leaves, int64_t P) {
+  register_default_adjoints();
+  LetSeq fwd = g.seq();  // snapshot of the forward lets
+  std::unordered_map<const ir::Var*, VarPtr> grad;
+  std::map<std::pair<const ir::Var*, int>, VarPtr> tgrad;
+  std::unordered_map<const ir::Var*, size_t> index;
+  for (size_t i = 0; i < fwd.lets.size(); ++i) index[fwd.lets[i].var.get()] = i;
+
+  auto accumulate = [&](const VarPtr& v, const VarPtr& d) {
+    if (!d) return;
+    auto it = grad.find(v.get());
+    if (it == grad.end()) {
+      grad[v.get()] = d;
+    } else {
+      VarPtr a = it->second, b = d;
+      if (a->ty.tensor().dtype != b->ty.tensor().dtype)
+        b = g.op("convert", {b}, {{"to", std::string(dtype_str(a->ty.tensor().dtype))}});
+      it->second = g.op("add", {a, b});
+    }
+  };
+
+  // seed: the loss must come from cross_entropy(grad=1) via tuple_get 0
+  {
+    auto it = index.find(loss.get());
+    if (it == index.end()) throw Error("autodiff: loss is not a let of this graph");
+    const auto& lb = fwd.lets[it->second];
+    if (lb.value->kind != ExprKind::TupleGet)
+      throw NonDifferentiable("autodiff: loss must be tuple_get(cross_entropy(..., grad=1), 0)");
+    auto src = lb.value->args[0]->var;
+    tgrad[{src.get(), 0}] = loss;  // placeholder: d loss = 1 (consumed by the CE adjoint)
+  }
+
+  for (size_t ii = fwd.lets.size(); ii-- > 0;) {
+    const LetBinding& lb = fwd.lets[ii];
+    const ExprPtr& e = lb.value;
+    if (e->kind == ExprKind::TupleGet) {
+      auto it = grad.find(lb.var.get());
+      if (it != grad.end()) {
+        auto key = std::make_pair(e->args[0]->var.get(), e->index);
+        auto jt = tgrad.find(key);
+        if (jt == tgrad.end()) tgrad[key] = it->second;
+        else jt->second = g.op("add", {jt->second, it->second});
+      }
+      continue;
+    }
+    if (e->kind != ExprKind::Call) continue;
+    if (e->op == "view") continue;  // leaves: handled below
+    std::vector<VarPtr> dout;
+    bool any = false;
+    if (lb.var->ty.is_tuple()) {
+      for (size_t k = 0; k < lb.var->ty.tuple().fields.size(); ++k) {
+        auto jt = tgrad.find({lb.var.get(), int(k)});
+        dout.push_back(jt == tgrad.end() ? nullptr : jt->second);
+        any = any || jt != tgrad.end();
+      }
+    } else {
+      auto it = grad.find(lb.var.get());
+      dout.push_back(it == grad.end() ? nullptr : it->second);
+      any = it != grad.end();
+    }
+    if (!any) continue;
+    auto rule = adjoints().find(e->op);
+    if (rule == adjoints().end()) throw NonDifferentiable("no adjoint registered for op " + e->op);
+    AdjointCtx ctx{g, lb, dout};
+    auto dins = rule->second(ctx);
+    for (size_t j = 0; j < dins.size() && j < e->args.size(); ++j) {
+      auto av = arg_var(e, j);
+      if (av && dins[j]) accumulate(av, dins[j]);
+    }
+  }
+
+  // leaf gradients -> one flat f32 buffer in offset order
+  std::sort(leaves.begin(), leaves.end(), [](const Leaf& a, const Leaf& b) { return a.offset < b.offset; });
+  std::vector<VarPtr> parts;
+  int64_t pos = 0;
+  auto zeros = [&](int64_t n) {
+    return g.op("fill", {}, {{"shape", std::to_string(n)}, {"dtype", std::string("f32")}, {"value", 0.0}});
+  };
+  for (auto& lf : leaves) {
+    if (lf.offset < pos) throw Error("autodiff: parameter leaves overlap");
+    if (lf.offset > pos) parts.push_back(zeros(lf.offset - pos));  // alignment gap
+    auto it = grad.find(lf.view.get());
+    if (it == grad.end()) throw NonDifferentiable("no gradient reaches parameter %" + lf.view->id);
+    VarPtr d = it->second;
+    if (d->ty.tensor().dtype != kF32) d = g.op("convert", {d}, {{"to", std::string("f32")}});
+    parts.push_back(d);
+    pos += lf.numel;
+  }
+  if (pos > P) throw Error("autodiff: leaves exceed the flat buffer");
+  if (pos < P) parts.push_back(zeros(P - pos));
+  return {g.op("concat", parts, {}, "grad")};
+}
+
+// -------------------------------------------------------------------- fusion
+
+struct UseInfo {
+  std::unordered_map<const ir::Var*, int> count;
+  std::set<const ir::Var*> returned;
+};
+
+inline UseInfo count_uses(const LetSeq& s) {
+  UseInfo u;
+  for (auto& b : s.lets)
+    for (auto& a : b.value->args)
+      if (a->kind == ExprKind::VarRef) u.count[a->var.get()]++;
+  if (s.ret)
+    for (auto& a : s.ret->args)
+      if (a->kind == ExprKind::VarRef) {
+        u.count[a->var.get()]++;
+        u.returned.insert(a->var.get());
+      }
+  return u;
+}
+
+struct FusionStats {
+  int dact = 0, ln_dy2 = 0, emb_base = 0, dead = 0;
+};
+
+/// Pattern fusion + dead-let elimination.  Each rewrite needs the absorbed
+/// producer to have exactly one use (SPEC.md:381-388 materialization rule).
+inline FusionStats fuse(LetSeq& s, bool patterns = true) {
+  FusionStats st;
+  UseInfo u = count_uses(s);
+  std::unordered_map<const ir::Var*, size_t> def;
+  for (size_t i = 0; i < s.lets.size(); ++i) def[s.lets[i].var.get()] = i;
+  std::set<size_t> removed;
+  auto producer = [&](const VarPtr& v) -> LetBinding* {
+    if (!v) return nullptr;
+    auto it = def.find(v.get());
+    if (it == def.end() || removed.count(it->second)) return nullptr;
+    auto& b = s.lets[it->second];
+    return b.value->kind == ExprKind::Call ? &b : nullptr;
+  };
+  auto single = [&](const VarPtr& v) { return u.count[v.get()] == 1 && !u.returned.count(v.get()); };
+
+  for (size_t i = 0; patterns && i < s.lets.size(); ++i) {
+    auto& b = s.lets[i];
+    if (b.value->kind != ExprKind::Call) continue;
+    const std::string op = b.value->op;
+    // 1. gelu_dx(u, matmul_t(a, b)) -> matmul_dact(a, b, u)   (dact in the dgrad epilogue)
+    if (op == "gelu_dx") {
+      auto src = arg_var(b.value, 1);
+      auto* p = producer(src);
+      if (p && p->value->op == "matmul_t" && single(src) && ir::attr_double(p->value->call_attrs, "alpha", 1.0) == 1.0 &&
+          !p->value->call_attrs.count("out")) {
+        AttrMap at = pick(p->value->call_attrs, {"ta", "tb"});
+        at["act"] = std::string("gelu");
+        auto call = ir::call("matmul_dact", {p->value->args[0], p->value->args[1], b.value->args[0]}, at);
+        call->ty = b.value->ty;
+        b.value = call;
+        removed.insert(def[src.get()]);
+        ++st.dact;
+        continue;
+      }
+    }
+    // 2. layer_norm_dx(s, g, m, r, add(a, b)) -> layer_norm_dx(s, g, m, r, a, b)
+    if (op == "layer_norm_dx" && b.value->args.size() == 5) {
+      auto src = arg_var(b.value, 4);
+      auto* p = producer(src);
+      if (p && p->value->op == "add" && single(src)) {
+        auto a = arg_var(p->value, 0), c = arg_var(p->value, 1);
+        if (a && c && a->ty == src->ty && c->ty == src->ty) {
+          auto call = ir::call("layer_norm_dx",
+                               {b.value->args[0], b.value->args[1], b.value->args[2], b.value->args[3],
+                                p->value->args[0], p->value->args[1]},
+                               b.value->call_attrs);
+          call->ty = b.value->ty;
+          b.value = call;
+          removed.insert(def[src.get()]);
+          ++st.ln_dy2;
+          continue;
+        }
+      }
+    }
+    // 3. add(embedding_dx(ids, dy), X) -> embedding_dx(ids, dy, X)  (tied embeddings)
+    if (op == "add") {
+      for (int side = 0; side < 2; ++side) {
+        auto src = arg_var(b.value, side), other = arg_var(b.value, 1 - side);
+        auto* p = producer(src);
+        if (p && other && p->value->op == "embedding_dx" && p->value->args.size() == 2 && single(src) &&
+            other->ty == src->ty) {
+          auto call = ir::call("embedding_dx", {p->value->args[0], p->value->args[1], b.value->args[1 - side]},
+                               p->value->call_attrs);
+          call->ty = b.value->ty;
+          b.value = call;
+          removed.insert(def[src.get()]);
+          ++st.emb_base;
+          break;
+        }
+      }
+    }
+  }
+  LetSeq out;
+  for (size_t i = 0; i < s.lets.size(); ++i)
+    if (!removed.count(i)) out.lets.push_back(s.lets[i]);
+  out.ret = s.ret;
+  // dead-let elimination (everything here is pure except collectives/shard)
+  bool changed = true;
+  while (changed) {
+    changed = false;
+    UseInfo uu = count_uses(out);
+    LetSeq keep;
+    keep.ret = out.ret;
+    for (auto& b : out.lets) {
+      bool pure = b.value->kind != ExprKind::Call || opreg::registry().base_of(b.value->op).pure;
+      if (pure && uu.count[b.var.get()] == 0) {
+        ++st.dead;
+        changed = true;
+        continue;
+      }
+      keep.lets.push_back(b);
+    }
+    out = std::move(keep);
+  }
+  s = std::move(out);
+  return st;
+}
+
+/// dispatch_pass (opreg.hpp:740-766) works on Dataflow form; this applies the
+/// same OpRegistry::resolve decision in place on ANF so the execution order
+/// chosen by memsched is untouched.
+inline void dispatch_anf(LetSeq& s, const opreg::DispatchConfig& cfg) {
+  for (auto& b : s.lets) {
+    if (b.value->kind != ExprKind::Call || b.value->op.find('.') != std::string::npos) continue;
+    try {
+      b.value->op = opreg::registry().resolve(b.value->op, cfg).full_name();
+    } catch (const UnimplementedOp& e) {
+      std::string shapes;
+      for (auto& a : b.value->args) shapes += (shapes.empty() ? "" : ", ") + (a->var ? type_str(a->var->ty) : "?");
+      throw UnimplementedOp(std::string(e.what()) + " (inputs: " + shapes + ")");
+    }
+  }
+}
+
+inline std::string base_name(const std::string& op) {
+  auto d = op.find('.');
+  return d == std::string::npos ? op : op.substr(d + 1);
+}
+
+}  // namespace tb

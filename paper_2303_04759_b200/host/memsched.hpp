@@ -1,0 +1,568 @@
+// memsched.hpp -- execution-order optimisation on ANF:
+// exact liveness over storage units, the peak-memory curve, the p-c greedy
+// list scheduler and budgeted rematerialisation by liveness splitting.
+//
+// Storage model (shared with the device VM, so the planner's numbers are the
+// VM's numbers): every tensor-valued let owns a storage unit, except
+//   view / reshape / tuple_get   aliases of their source (0 bytes),
+//   concat                       its inputs are placed inside its output
+//                                ("concat elision"), so the output unit is live
+//                                from the first input's definition,
+//   state-bound outputs          written in place into the state parameter they
+//                                update (optimizer p/m/v, step, half copy).
+// A unit is live on [def, last use]; parameters are live throughout.  The op at
+// index i needs its inputs and outputs live at i.
+#pragma once
+
+#include <algorithm>
+#include <limits>
+#include <map>
+#include <numeric>
+#include <unordered_map>
+
+#include "graph.hpp"
+
+namespace tb {
+
+struct Unit {
+  int64_t bytes = 0;
+  int def = 0, last = 0;
+  int parent = -1;        // concat elision: placed inside parent at sub_off
+  int64_t sub_off = 0;
+  int param = -1;         // >= 0: a function parameter (persistent state / input)
+  int producer = -1;      // let index that writes it (-1 for params)
+};
+
+struct Ref {
+  int unit = -1;
+  int64_t off = 0;   // byte offset inside the unit
+  int64_t bytes = 0;
+};
+
+struct Layout {
+  std::vector<Unit> units;
+  std::unordered_map<const ir::Var*, std::vector<Ref>> refs;  // per tensor field
+  std::vector<int> concat_copy;  // lets whose concat could not be fully elided
+  int n = 0;                     // number of lets
+  // root unit of u (following concat parents) and the byte offset inside it
+  std::pair<int, int64_t> root(int u) const {
+    int64_t off = 0;
+    while (units[u].parent >= 0) {
+      off += units[u].sub_off;
+      u = units[u].parent;
+    }
+    return {u, off};
+  }
+};
+
+inline bool inplace_safe(const std::string& base, int in_idx, int out_idx) {
+  if (base == "adam_update" || base == "adam_update_ex")
+    return (out_idx == 0 && in_idx == 0) || (out_idx == 1 && in_idx == 2) || (out_idx == 2 && in_idx == 3);
+  if (base == "sgd_update") return in_idx == 0 && out_idx == 0;
+  if (base == "add_scalar") return in_idx == 0 && out_idx == 0;
+  return false;
+}
+
+/// state_binding: (ret index, param index) pairs; params listed are written in
+/// place when liveness allows (otherwise the VM copies back after the step).
+inline Layout build_layout(const ir::FunctionIR& fn, const std::vector<std::pair<int, int>>& state_binding,
+                           bool elide_concat = true) {
+  Layout L;
+  auto seq = ir::flatten(fn);
+  L.n = int(seq.lets.size());
+  auto new_unit = [&](int64_t bytes, int def, int producer, int param = -1) {
+    Unit u;
+    u.bytes = bytes;
+    u.def = def;
+    u.last = def;
+    u.producer = producer;
+    u.param = param;
+    L.units.push_back(u);
+    return int(L.units.size()) - 1;
+  };
+  for (size_t p = 0; p < fn.params.size(); ++p) {
+    int u = new_unit(nbytes(fn.params[p]->ty), -1, -1, int(p));
+    L.units[u].last = L.n;
+    L.refs[fn.params[p].get()] = {Ref{u, 0, L.units[u].bytes}};
+  }
+  // returned var -> param it must be written into
+  std::unordered_map<const ir::Var*, int> bind;
+  std::unordered_map<const ir::Var*, int> ret_index;
+  if (seq.ret && seq.ret->kind == ExprKind::Tuple) {
+    for (size_t j = 0; j < seq.ret->args.size(); ++j) {
+      auto& a = seq.ret->args[j];
+      if (a->kind == ExprKind::VarRef) ret_index[a->var.get()] = int(j);
+    }
+    for (auto& [rj, pi] : state_binding)
+      if (rj < int(seq.ret->args.size()) && seq.ret->args[rj]->kind == ExprKind::VarRef)
+        bind[seq.ret->args[rj]->var.get()] = pi;
+  }
+  // last use of every var; for params the alias-aware last use (views of a
+  // param are reads of it) comes from an unbound dry run of this function
+  std::unordered_map<const ir::Var*, int> last_use;
+  for (int i = 0; i < L.n; ++i)
+    for (auto& a : seq.lets[i].value->args)
+      if (a->kind == ExprKind::VarRef) last_use[a->var.get()] = i;
+  if (!state_binding.empty()) {
+    Layout dry = build_layout(fn, {}, elide_concat);
+    for (auto& u : dry.units)
+      if (u.param >= 0) {
+        int l = -1;
+        for (int i = 0; i < dry.n; ++i)
+          for (auto& a : seq.lets[i].value->args)
+            if (a->kind == ExprKind::VarRef)
+              for (auto& r : dry.refs.at(a->var.get()))
+                if (dry.root(r.unit).first == int(&u - dry.units.data())) l = i;
+        last_use[fn.params[u.param].get()] = l;
+      }
+  }
+  // a field var (tuple_get) that is returned/bound: find it through tuple_gets
+  std::unordered_map<const ir::Var*, std::map<int, const ir::Var*>> tuple_fields;
+  for (auto& b : seq.lets)
+    if (b.value->kind == ExprKind::TupleGet)
+      tuple_fields[b.value->args[0]->var.get()][b.value->index] = b.var.get();
+
+  auto try_bind = [&](const ir::Var* out_var, int let_i, const ir::ExprPtr& call, int out_idx) -> int {
+    auto it = bind.find(out_var);
+    if (it == bind.end()) return -1;
+    int pi = it->second;
+    const ir::Var* pv = fn.params[pi].get();
+    auto lu = last_use.find(pv);
+    int lastp = lu == last_use.end() ? -1 : lu->second;
+    if (lastp > let_i) return -1;
+    if (lastp == let_i) {
+      bool ok = false;
+      for (size_t k = 0; k < call->args.size(); ++k)
+        if (call->args[k]->kind == ExprKind::VarRef && call->args[k]->var.get() == pv)
+          ok = inplace_safe(base_name(call->op), int(k), out_idx);
+      if (!ok) return -1;
+    }
+    return L.refs[pv][0].unit;
+  };
+
+  for (int i = 0; i < L.n; ++i) {
+    const auto& b = seq.lets[i];
+    const auto& e = b.value;
+    auto arg_refs = [&](size_t k) -> const std::vector<Ref>& { return L.refs.at(e->args[k]->var.get()); };
+    if (e->kind == ExprKind::TupleGet) {
+      L.refs[b.var.get()] = {L.refs.at(e->args[0]->var.get()).at(e->index)};
+      continue;
+    }
+    if (e->kind != ExprKind::Call) throw Error("memsched: unsupported let kind");
+    const std::string base = base_name(e->op);
+    if (base == "view") {
+      Ref r = arg_refs(0)[0];
+      const auto& src = e->args[0]->var->ty.tensor();
+      r.off += ir::attr_int(e->call_attrs, "offset", 0) * dtype_bytes(src.dtype);
+      r.bytes = nbytes(b.var->ty);
+      L.refs[b.var.get()] = {r};
+      continue;
+    }
+    if (base == "reshape") {
+      L.refs[b.var.get()] = {arg_refs(0)[0]};
+      continue;
+    }
+    if (base == "concat") {
+      int u = new_unit(nbytes(b.var->ty), i, i);
+      int64_t off = 0;
+      bool all = true;
+      for (size_t k = 0; k < e->args.size(); ++k) {
+        const Ref& r = arg_refs(k)[0];
+        Unit& cu = L.units[r.unit];
+        bool ok = elide_concat && r.off == 0 && r.bytes == cu.bytes && cu.param < 0 && cu.parent < 0 &&
+                  cu.producer >= 0 && last_use[e->args[k]->var.get()] == i;
+        // the producer must produce exactly this unit (not a tuple field shared elsewhere)
+        if (ok) {
+          cu.parent = u;
+          cu.sub_off = off;
+          L.units[u].def = std::min(L.units[u].def, cu.def);
+        } else {
+          all = false;
+        }
+        off += r.bytes;
+      }
+      if (!all) L.concat_copy.push_back(i);
+      L.refs[b.var.get()] = {Ref{u, 0, L.units[u].bytes}};
+      continue;
+    }
+    // ordinary op: one unit per output field, or in place into a bound param
+    std::vector<Ref> outs;
+    if (b.var->ty.is_tuple()) {
+      const auto& fields = b.var->ty.tuple().fields;
+      auto tf = tuple_fields.find(b.var.get());
+      for (size_t k = 0; k < fields.size(); ++k) {
+        int pu = -1;
+        if (tf != tuple_fields.end() && tf->second.count(int(k)))
+          pu = try_bind(tf->second.at(int(k)), i, e, int(k));
+        if (pu >= 0) outs.push_back(Ref{pu, 0, nbytes(fields[k])});
+        else {
+          int u = new_unit(nbytes(fields[k]), i, i);
+          outs.push_back(Ref{u, 0, L.units[u].bytes});
+        }
+      }
+    } else {
+      int pu = try_bind(b.var.get(), i, e, 0);
+      if (pu >= 0) outs.push_back(Ref{pu, 0, nbytes(b.var->ty)});
+      else {
+        int u = new_unit(nbytes(b.var->ty), i, i);
+        outs.push_back(Ref{u, 0, L.units[u].bytes});
+      }
+    }
+    L.refs[b.var.get()] = outs;
+  }
+  // uses extend lifetimes
+  for (int i = 0; i < L.n; ++i)
+    for (auto& a : seq.lets[i].value->args)
+      if (a->kind == ExprKind::VarRef)
+        for (auto& r : L.refs.at(a->var.get())) L.units[r.unit].last = std::max(L.units[r.unit].last, i);
+  if (seq.ret)
+    for (auto& a : seq.ret->args)
+      if (a->kind == ExprKind::VarRef)
+        for (auto& r : L.refs.at(a->var.get())) L.units[r.unit].last = L.n;
+  // concat children: the parent covers them
+  for (size_t u = 0; u < L.units.size(); ++u) {
+    if (L.units[u].parent < 0) continue;
+    auto [root, off] = L.root(int(u));
+    (void)off;
+    L.units[root].def = std::min(L.units[root].def, L.units[u].def);
+    L.units[root].last = std::max(L.units[root].last, L.units[u].last);
+  }
+  return L;
+}
+
+// ------------------------------------------------------------ peak memory
+struct MemProfile {
+  std::vector<int64_t> curve;  // bytes live at each let index
+  int64_t peak = 0;
+  int peak_index = -1;
+  int64_t state_bytes = 0;     // parameters (live throughout)
+};
+
+/// a tensor occupies its bytes from its producing op through
+/// its last use; op i needs inputs + outputs live at i.
+inline MemProfile peak_memory(const Layout& L) {
+  MemProfile m;
+  m.curve.assign(std::max(L.n, 1), 0);
+  for (size_t u = 0; u < L.units.size(); ++u) {
+    const Unit& x = L.units[u];
+    if (x.parent >= 0) continue;
+    if (x.param >= 0) {
+      m.state_bytes += x.bytes;
+      for (auto& c : m.curve) c += x.bytes;
+      continue;
+    }
+    for (int i = std::max(0, x.def); i <= std::min(x.last, L.n - 1); ++i) m.curve[i] += x.bytes;
+  }
+  for (int i = 0; i < int(m.curve.size()); ++i)
+    if (m.curve[i] > m.peak) {
+      m.peak = m.curve[i];
+      m.peak_index = i;
+    }
+  return m;
+}
+
+inline MemProfile peak_memory(const ir::FunctionIR& fn, const std::vector<std::pair<int, int>>& sb = {}) {
+  return peak_memory(build_layout(fn, sb));
+}
+
+// ----------------------------------------------------------- arena plan
+struct ArenaPlan {
+  std::vector<int64_t> offset;  // per unit (-1: not in the arena)
+  int64_t size = 0;             // high-water mark
+};
+
+/// Static offsets for every non-parameter root unit: walk the let order, free
+/// units after their last use, place new units best-fit into freed gaps
+/// (address-ordered free list), else at the top.  Deterministic.
+inline ArenaPlan plan_arena(const Layout& L, int64_t align = 256) {
+  ArenaPlan P;
+  P.offset.assign(L.units.size(), -1);
+  std::vector<std::vector<int>> starts(L.n + 1), ends(L.n + 2);
+  for (size_t u = 0; u < L.units.size(); ++u) {
+    const Unit& x = L.units[u];
+    if (x.parent >= 0 || x.param >= 0 || x.bytes == 0) continue;
+    starts[std::max(0, x.def)].push_back(int(u));
+    ends[std::min(x.last, L.n) + 1].push_back(int(u));
+  }
+  std::map<int64_t, int64_t> free_;  // offset -> size
+  int64_t top = 0;
+  auto rnd = [&](int64_t b) { return (b + align - 1) / align * align; };
+  auto release = [&](int u) {
+    int64_t off = P.offset[u], sz = rnd(L.units[u].bytes);
+    auto it = free_.emplace(off, sz).first;
+    auto nx = std::next(it);
+    if (nx != free_.end() && it->first + it->second == nx->first) {
+      it->second += nx->second;
+      free_.erase(nx);
+    }
+    if (it != free_.begin()) {
+      auto pv = std::prev(it);
+      if (pv->first + pv->second == it->first) {
+        pv->second += it->second;
+        free_.erase(it);
+        it = pv;
+      }
+    }
+    if (it->first + it->second == top) {
+      top = it->first;
+      free_.erase(it);
+    }
+  };
+  for (int i = 0; i <= L.n; ++i) {
+    for (int u : ends[i]) release(u);
+    auto& st = starts[std::min(i, L.n)];
+    if (i < L.n) {
+      std::vector<int> us = st;
+      std::sort(us.begin(), us.end(), [&](int a, int b) {
+        return L.units[a].bytes != L.units[b].bytes ? L.units[a].bytes > L.units[b].bytes : a < b;
+      });
+      for (int u : us) {
+        int64_t sz = rnd(L.units[u].bytes);
+        auto best = free_.end();
+        for (auto it = free_.begin(); it != free_.end(); ++it)
+          if (it->second >= sz && (best == free_.end() || it->second < best->second)) best = it;
+        if (best != free_.end()) {
+          P.offset[u] = best->first;
+          int64_t rem = best->second - sz, noff = best->first + sz;
+          free_.erase(best);
+          if (rem > 0) free_.emplace(noff, rem);
+        } else {
+          P.offset[u] = top;
+          top += sz;
+        }
+        P.size = std::max(P.size, top);
+      }
+    }
+  }
+  return P;
+}
+
+// ---------------------------------------------------------------- cost model
+/// Per-op cost for scheduling / remat scores: GEMM-shaped ops
+/// m*n*k, attention its two batched products, everything else the element
+/// count of its largest operand -- CostModel::op_cost (opreg.hpp:536-559)
+/// extended to the closure-like extension ops it would throw on.
+inline double op_cost(const ir::ExprPtr& call) {
+  const std::string base = base_name(call->op);
+  auto T = [&](size_t i) { return call->args.at(i)->var->ty.tensor(); };
+  if (base == "matmul") return double(T(0).shape[0]) * T(0).shape[1] * T(1).shape[1];
+  if (base == "linear" || base == "matmul_t" || base == "matmul_dact") {
+    const auto& a = T(0);
+    double k = a.shape[ir::attr_int(call->call_attrs, "ta", 0) ? 0 : 1];
+    return double(numel(a)) / k * k * double(numel(T(1))) / k;
+  }
+  if (base == "attention" || base == "attention_dx") {
+    const auto& q = T(0);
+    double S = double(ir::attr_int(call->call_attrs, "seq", q.shape[0]));
+    return 2.0 * double(q.shape[0]) * S * double(q.shape[1] / 3);
+  }
+  double n = 1;
+  for (auto& a : call->args)
+    if (a->kind == ExprKind::VarRef && a->var->ty.is_tensor()) n = std::max(n, double(numel(a->var->ty.tensor())));
+  if (call->ty.is_tensor()) n = std::max(n, double(numel(call->ty.tensor())));
+  return n;
+}
+
+// ------------------------------------------------------------------ schedule
+/// p - c greedy list scheduling: among ready lets pick the
+/// one with minimum (bytes produced - bytes freed), ties by original order.
+inline LetSeq schedule(const ir::FunctionIR& fn, const std::vector<std::pair<int, int>>& sb = {}) {
+  Layout L = build_layout(fn, sb);
+  LetSeq seq = ir::flatten(fn);
+  const int n = int(seq.lets.size());
+  std::unordered_map<const ir::Var*, int> def;
+  for (int i = 0; i < n; ++i) def[seq.lets[i].var.get()] = i;
+  std::vector<std::vector<int>> deps(n), users(n);
+  for (int i = 0; i < n; ++i)
+    for (auto& a : seq.lets[i].value->args)
+      if (a->kind == ExprKind::VarRef && def.count(a->var.get())) {
+        int d = def[a->var.get()];
+        deps[i].push_back(d);
+        users[d].push_back(i);
+      }
+  // remaining uses per root unit
+  auto roots_of = [&](const ir::Var* v) {
+    std::vector<int> r;
+    for (auto& ref : L.refs.at(v)) r.push_back(L.root(ref.unit).first);
+    return r;
+  };
+  std::vector<int> remaining(L.units.size(), 0);
+  for (int i = 0; i < n; ++i)
+    for (auto& a : seq.lets[i].value->args)
+      if (a->kind == ExprKind::VarRef)
+        for (int u : roots_of(a->var.get())) remaining[u]++;
+  std::vector<char> pinned(L.units.size(), 0);
+  for (size_t u = 0; u < L.units.size(); ++u)
+    if (L.units[u].param >= 0 || L.units[u].last >= n) pinned[u] = 1;
+  std::vector<int> indeg(n);
+  for (int i = 0; i < n; ++i) indeg[i] = int(deps[i].size());
+  std::vector<int> ready;
+  for (int i = 0; i < n; ++i)
+    if (!indeg[i]) ready.push_back(i);
+  std::vector<char> produced(L.units.size(), 0);
+  LetSeq out;
+  out.ret = seq.ret;
+  while (!ready.empty()) {
+    int best = -1;
+    double best_score = 0;
+    for (int i : ready) {
+      const auto& b = seq.lets[i];
+      double p = 0, c = 0;
+      for (auto& r : L.refs.at(b.var.get())) {
+        int u = L.root(r.unit).first;
+        if (!produced[u] && L.units[u].param < 0) p += double(L.units[u].bytes);
+      }
+      std::unordered_map<int, int> cnt;
+      for (auto& a : b.value->args)
+        if (a->kind == ExprKind::VarRef)
+          for (int u : roots_of(a->var.get())) cnt[u]++;
+      for (auto& [u, k] : cnt)
+        if (!pinned[u] && remaining[u] == k) c += double(L.units[u].bytes);
+      double sc = p - c;
+      if (best < 0 || sc < best_score || (sc == best_score && i < best)) {
+        best = i;
+        best_score = sc;
+      }
+    }
+    ready.erase(std::find(ready.begin(), ready.end(), best));
+    const auto& b = seq.lets[best];
+    for (auto& r : L.refs.at(b.var.get())) produced[L.root(r.unit).first] = 1;
+    for (auto& a : b.value->args)
+      if (a->kind == ExprKind::VarRef)
+        for (int u : roots_of(a->var.get())) remaining[u]--;
+    out.lets.push_back(b);
+    for (int j : users[best])
+      if (--indeg[j] == 0) ready.push_back(j);
+  }
+  if (int(out.lets.size()) != n) throw Error("schedule: cycle detected");
+  return out;
+}
+
+// -------------------------------------------------------------- rematerialize
+struct RematSplit {
+  std::string victim;  // var id evicted
+  int evict_index;     // evicted after this position (in the output order)
+  int replay_before;   // position of the first use it was replayed for
+};
+struct RematPlan {
+  std::vector<RematSplit> splits;
+  int replays = 0;     // replayed ops ("overhead")
+  int64_t peak_before = 0, peak_after = 0;
+};
+
+inline bool replayable(const ir::ExprPtr& e) {
+  if (e->kind != ExprKind::Call) return false;
+  const std::string base = base_name(e->op);
+  if (is_alias_op(base) || base == "fill") return false;
+  const auto& bop = opreg::registry().base_of(e->op);
+  return bop.pure && !bop.collective;
+}
+
+/// Budgeted rematerialisation: simulate the live set in
+/// order; wherever the projected bytes (live + this op's new outputs) exceed
+/// the budget, evict the live, not-currently-needed, replayable tensor with the
+/// minimum score cost(producer) * remaining_uses / bytes (ties: larger, then
+/// earlier), and replay its producer right before its next use (liveness
+/// split).  Replay inputs must be live there; depth-1 victims only (the spec
+/// allows <= 3; deeper chains are not evicted).  Throws BudgetInfeasible when
+/// the floor (state + max single-op working set) exceeds the budget.
+inline std::pair<FunctionPtr, RematPlan> rematerialize(const ir::FunctionIR& fn, int64_t budget,
+                                                        const std::vector<std::pair<int, int>>& sb = {}) {
+  RematPlan plan;
+  auto cur = std::make_shared<ir::FunctionIR>(fn);
+  for (int iter = 0; iter < 100000; ++iter) {
+    Layout L = build_layout(*cur, sb);
+    MemProfile mp = peak_memory(L);
+    if (iter == 0) plan.peak_before = mp.peak;
+    plan.peak_after = mp.peak;
+    if (mp.peak <= budget) return {cur, plan};
+    LetSeq seq = ir::flatten(*cur);
+    const int n = int(seq.lets.size());
+    const int i = mp.peak_index;
+    // floor: state + inputs/outputs of op i
+    int64_t floor_i = mp.state_bytes;
+    std::set<int> needed;
+    for (auto& r : L.refs.at(seq.lets[i].var.get())) needed.insert(L.root(r.unit).first);
+    for (auto& a : seq.lets[i].value->args)
+      if (a->kind == ExprKind::VarRef)
+        for (auto& r : L.refs.at(a->var.get())) needed.insert(L.root(r.unit).first);
+    for (int u : needed)
+      if (L.units[u].param < 0) floor_i += L.units[u].bytes;
+    // candidates: units live across i, not used at i, produced by a replayable
+    // single-output op whose inputs are params or still live at the next use
+    std::unordered_map<const ir::Var*, int> def;
+    for (int k = 0; k < n; ++k) def[seq.lets[k].var.get()] = k;
+    int best_u = -1, best_next = -1;
+    double best_score = std::numeric_limits<double>::infinity();
+    for (size_t u = 0; u < L.units.size(); ++u) {
+      const Unit& x = L.units[u];
+      if (x.param >= 0 || x.parent >= 0 || x.producer < 0 || x.def >= i || x.last <= i || x.last >= n) continue;
+      if (needed.count(int(u))) continue;
+      const auto& pe = seq.lets[x.producer].value;
+      if (!replayable(pe) || seq.lets[x.producer].var->ty.is_tuple()) continue;
+      // next use after i
+      int next = -1, uses_after = 0;
+      for (int k = i + 1; k < n; ++k)
+        for (auto& a : seq.lets[k].value->args)
+          if (a->kind == ExprKind::VarRef)
+            for (auto& r : L.refs.at(a->var.get()))
+              if (L.root(r.unit).first == int(u)) {
+                if (next < 0) next = k;
+                ++uses_after;
+              }
+      if (next < 0) continue;
+      // replay inputs must be live at `next` (params, or units whose last >= next)
+      bool ok = true;
+      for (auto& a : pe->args) {
+        if (a->kind != ExprKind::VarRef) continue;
+        for (auto& r : L.refs.at(a->var.get())) {
+          const Unit& iu = L.units[L.root(r.unit).first];
+          if (iu.param < 0 && iu.last < next) ok = false;
+        }
+      }
+      if (!ok) continue;
+      double score = op_cost(pe) * uses_after / double(std::max<int64_t>(1, x.bytes));
+      if (score < best_score) {
+        best_score = score;
+        best_u = int(u);
+        best_next = next;
+      }
+    }
+    if (best_u < 0) {
+      if (floor_i > budget)
+        throw BudgetInfeasible("remat: floor " + std::to_string(floor_i) + " B exceeds budget " + std::to_string(budget));
+      throw BudgetInfeasible("remat: no evictable tensor at index " + std::to_string(i));
+    }
+    // liveness split: clone the producer right before best_next, rename uses >= best_next
+    const int prod = L.units[best_u].producer;
+    const auto& pb = seq.lets[prod];
+    auto nv = ir::make_var(pb.var->id + "_r" + std::to_string(plan.replays), pb.var->ty, pb.var->attrs);
+    auto ne = std::make_shared<ir::Expr>(*pb.value);
+    ne->serial = ir::detail::next_serial();
+    const ir::Var* old = pb.var.get();
+    LetSeq out;
+    out.ret = seq.ret;
+    for (int k = 0; k < n; ++k) {
+      if (k == best_next) out.lets.push_back({nv, ne});
+      auto b = seq.lets[k];
+      if (k >= best_next) {
+        bool touched = false;
+        auto e2 = std::make_shared<ir::Expr>(*b.value);
+        for (auto& a : e2->args)
+          if (a->kind == ExprKind::VarRef && a->var.get() == old) {
+            a = ir::var_ref(nv);
+            touched = true;
+          }
+        if (touched) b.value = e2;
+      }
+      out.lets.push_back(b);
+    }
+    // returned vars are never victims (last < n), so ret is unchanged
+    plan.splits.push_back({pb.var->id, i, best_next});
+    plan.replays++;
+    cur = ir::make_fn(cur->name, cur->params, out);
+  }
+  throw BudgetInfeasible("remat: iteration limit");
+}
+
+}  // namespace tb

@@ -1,0 +1,363 @@
+// models.hpp -- builders of the all-in-one training-step function
+// for the BASELINE.json configs: a BERT MLM encoder (C1 tiny fp32 / C2 base /
+// C4 large) and a GPT-2 causal LM (C3 medium / C5 XL).  Pure graph
+// construction over the reference IR: forward ops are emitted with
+// tb::Graph, the backward by tb::autodiff, then the fusion pass and the
+// optimizer (SGD, or Adam with the fused bf16 param copy), optionally ZeRO-1
+// partitioned (reduce_scatter -> sharded update -> all_gather).
+//
+// Parameters live in ONE flat f32 master buffer (and, under AutoCast, one flat
+// bf16 copy); every weight is a `view` of it.  That single segment is what makes
+// the optimizer one multi-tensor launch and the ZeRO collectives one bucket each.
+#pragma once
+
+#include <cmath>
+#include <sstream>
+
+#include "graph.hpp"
+
+namespace tb {
+
+struct ModelCfg {
+  std::string kind = "bert";  // bert | gpt2
+  int64_t L = 2, H = 128, A = 2, F = 512, V = 1024, S = 128, B = 8;
+  int64_t max_pos = 0;      // 0 -> bert: 512, gpt2: S
+  std::string dtype = "f32";  // activation / compute dtype: f32 | bf16
+  double p = 0.0;           // dropout
+  std::string opt = "sgd";  // sgd | adam
+  double lr = 0.01, beta1 = 0.9, beta2 = 0.999, eps = 1e-6;
+  int64_t seed_w = 42, seed_d = 1234, seed_drop = 7;
+  int64_t world = 1;        // ZeRO-1 data-parallel ranks
+  double ln_eps = 1e-12;
+  int fuse = 1;             // run the fusion pass
+  int64_t vocab_pad() const { return ((V + 63) / 64) * 64; }
+  int64_t T() const { return B * S; }
+  int64_t positions() const { return max_pos ? max_pos : (kind == "bert" ? std::max<int64_t>(512, S) : S); }
+};
+
+inline ModelCfg parse_cfg(const std::string& s) {
+  ModelCfg c;
+  std::istringstream is(s);
+  std::string kv;
+  while (std::getline(is, kv, ';')) {
+    auto eq = kv.find('=');
+    if (eq == std::string::npos) continue;
+    std::string k = kv.substr(0, eq), v = kv.substr(eq + 1);
+    auto I = [&] { return std::stoll(v); };
+    auto D = [&] { return std::stod(v); };
+    if (k == "kind") c.kind = v;
+    else if (k == "L") c.L = I();
+    else if (k == "H") c.H = I();
+    else if (k == "A") c.A = I();
+    else if (k == "F") c.F = I();
+    else if (k == "V") c.V = I();
+    else if (k == "S") c.S = I();
+    else if (k == "B") c.B = I();
+    else if (k == "max_pos") c.max_pos = I();
+    else if (k == "dtype") c.dtype = v;
+    else if (k == "p") c.p = D();
+    else if (k == "opt") c.opt = v;
+    else if (k == "lr") c.lr = D();
+    else if (k == "beta1") c.beta1 = D();
+    else if (k == "beta2") c.beta2 = D();
+    else if (k == "eps") c.eps = D();
+    else if (k == "seed_w") c.seed_w = I();
+    else if (k == "seed_d") c.seed_d = I();
+    else if (k == "seed_drop") c.seed_drop = I();
+    else if (k == "world") c.world = I();
+    else if (k == "ln_eps") c.ln_eps = D();
+    else if (k == "fuse") c.fuse = int(I());
+    else throw Error("unknown model config key '" + k + "'");
+  }
+  if (c.H % c.A) throw TypeError("H must be divisible by A");
+  return c;
+}
+
+enum class Init { Uniform, Ones, Zeros };
+struct ParamSeg {
+  std::string name;
+  std::vector<int64_t> shape;
+  int64_t offset, numel;
+  Init init;
+};
+
+struct TrainStep {
+  ModelCfg cfg;
+  FunctionPtr fn;
+  int64_t P = 0;      // real parameter count
+  int64_t P_pad = 0;  // padded to a multiple of world (ZeRO shards)
+  std::vector<ParamSeg> segs;
+  // function parameter roles (indices into fn->params)
+  int i_ids = -1, i_labels = -1, i_pos = -1, i_type = -1, i_params = -1, i_p16 = -1, i_m = -1, i_v = -1,
+      i_step = -1;
+  std::vector<std::pair<int, int>> state_binding;  // (ret index, param index): in-place state update
+  FusionStats fusion;
+  int64_t shard() const { return P_pad / cfg.world; }
+};
+
+class ParamTable {
+ public:
+  // every segment starts on a 64-element (128 B for bf16) boundary so each
+  // weight view is a legal TMA base for the tcgen05 GEMM
+  void add(const std::string& name, std::vector<int64_t> shape, Init init) {
+    int64_t n = 1;
+    for (auto d : shape) n *= d;
+    total_ = (total_ + 63) / 64 * 64;
+    segs_.push_back({name, shape, total_, n, init});
+    total_ += n;
+  }
+  const std::vector<ParamSeg>& segs() const { return segs_; }
+  int64_t total() const { return total_; }
+  const ParamSeg& get(const std::string& n) const {
+    for (auto& s : segs_)
+      if (s.name == n) return s;
+    throw Error("no parameter " + n);
+  }
+
+ private:
+  std::vector<ParamSeg> segs_;
+  int64_t total_ = 0;
+};
+
+inline ParamTable param_table(const ModelCfg& c) {
+  ParamTable t;
+  const int64_t H = c.H, F = c.F, Vp = c.vocab_pad();
+  const auto U = Init::Uniform, O = Init::Ones, Z = Init::Zeros;
+  t.add("word_emb", {Vp, H}, U);
+  t.add("pos_emb", {c.positions(), H}, U);
+  if (c.kind == "bert") {
+    t.add("type_emb", {2, H}, U);
+    t.add("emb_ln.g", {H}, O);
+    t.add("emb_ln.b", {H}, Z);
+  }
+  for (int64_t l = 0; l < c.L; ++l) {
+    const std::string p = "layer" + std::to_string(l) + ".";
+    if (c.kind == "gpt2") {
+      t.add(p + "ln1.g", {H}, O);
+      t.add(p + "ln1.b", {H}, Z);
+    }
+    t.add(p + "qkv.w", {H, 3 * H}, U);
+    t.add(p + "qkv.b", {3 * H}, Z);
+    t.add(p + "proj.w", {H, H}, U);
+    t.add(p + "proj.b", {H}, Z);
+    if (c.kind == "bert") {
+      t.add(p + "ln1.g", {H}, O);
+      t.add(p + "ln1.b", {H}, Z);
+    } else {
+      t.add(p + "ln2.g", {H}, O);
+      t.add(p + "ln2.b", {H}, Z);
+    }
+    t.add(p + "ffn1.w", {H, F}, U);
+    t.add(p + "ffn1.b", {F}, Z);
+    t.add(p + "ffn2.w", {F, H}, U);
+    t.add(p + "ffn2.b", {H}, Z);
+    if (c.kind == "bert") {
+      t.add(p + "ln2.g", {H}, O);
+      t.add(p + "ln2.b", {H}, Z);
+    }
+  }
+  if (c.kind == "bert") {
+    t.add("mlm.dense.w", {H, H}, U);
+    t.add("mlm.dense.b", {H}, Z);
+    t.add("mlm.ln.g", {H}, O);
+    t.add("mlm.ln.b", {H}, Z);
+    t.add("mlm.dec.b", {Vp}, Z);
+  } else {
+    t.add("lnf.g", {H}, O);
+    t.add("lnf.b", {H}, Z);
+  }
+  return t;
+}
+
+/// Build the training step.  Inputs: ids, labels, pos_ids (+ type_ids for
+/// BERT), params (f32 master, sharded under ZeRO), [p16 (half copy, full)],
+/// [m, v (sharded), step].  Outputs: (loss, new states...) with in-place
+/// bindings back onto the state inputs.
+inline TrainStep build_train_step(const ModelCfg& c) {
+  TrainStep ts;
+  ts.cfg = c;
+  ParamTable tab = param_table(c);
+  ts.segs = tab.segs();
+  ts.P = tab.total();
+  ts.P_pad = ((ts.P + 64 * c.world - 1) / (64 * c.world)) * (64 * c.world);  // 128 B-aligned shards
+  const bool amp = c.dtype != "f32";
+  const DType act = dtype_from(c.dtype);
+  const int64_t T = c.T(), H = c.H, Vp = c.vocab_pad();
+  const bool adam = c.opt == "adam";
+  if (c.world > 1 && !adam) throw Error("ZeRO partitioning is implemented for Adam");
+  if (c.world > 1 && !amp) throw Error("ZeRO path expects the AutoCast (half param copy) graph");
+
+  Graph g;
+  auto P = [&](const std::string& n, TensorType t) {
+    auto v = g.param(n, t);
+    return int(g.params().size() - 1);
+  };
+  ts.i_ids = P("ids", {kI32, {T}});
+  ts.i_labels = P("labels", {kI32, {T}});
+  ts.i_pos = P("pos_ids", {kI32, {T}});
+  if (c.kind == "bert") ts.i_type = P("type_ids", {kI32, {T}});
+  const int64_t pstate = c.world > 1 ? ts.shard() : ts.P_pad;
+  ts.i_params = P("params", {kF32, {pstate}});
+  if (amp) ts.i_p16 = P("p16", {act, {ts.P_pad}});
+  if (adam) {
+    ts.i_m = P("m", {kF32, {pstate}});
+    ts.i_v = P("v", {kF32, {pstate}});
+    ts.i_step = P("step", {kF32, {1}});
+  }
+  auto par = [&](int i) { return g.params()[i]; };
+  VarPtr ids = par(ts.i_ids), labels = par(ts.i_labels), pos_ids = par(ts.i_pos);
+  VarPtr wsrc = amp ? par(ts.i_p16) : par(ts.i_params);
+
+  std::vector<Leaf> leaves;
+  std::map<std::string, VarPtr> W;
+  for (auto& s : ts.segs) {
+    auto v = g.op("view", {wsrc}, {{"offset", s.offset}, {"shape", opreg::shape_attr(s.shape)}}, "w");
+    W[s.name] = v;
+    leaves.push_back({v, s.offset, s.numel});
+  }
+  int64_t salt = 1;
+  auto drop_attrs = [&](AttrMap a = {}) {
+    a["p"] = c.p;
+    a["seed"] = c.seed_drop;
+    a["salt"] = salt++;
+    return a;
+  };
+  auto linear = [&](VarPtr x, const std::string& w, const std::string& b, const std::string& actf = "none",
+                    int tw = 0) {
+    AttrMap a{{"act", actf}};
+    if (tw) a["tw"] = std::int64_t(1);
+    if (actf == "gelu" || actf == "relu") a["save_preact"] = std::int64_t(1);
+    VarPtr y = g.op("linear", {x, W[w], W[b]}, a);
+    return y->ty.is_tuple() ? g.get(y, 0) : y;
+  };
+  AttrMap attn_attrs{{"heads", c.A}, {"seq", c.S}, {"causal", std::int64_t(c.kind == "gpt2")}};
+
+  // ---- embeddings
+  VarPtr h;
+  if (c.kind == "bert") {
+    VarPtr type_ids = par(ts.i_type);
+    VarPtr e = g.op("add", {g.op("embedding", {ids, W["word_emb"]}), g.op("embedding", {pos_ids, W["pos_emb"]})});
+    e = g.op("add", {e, g.op("embedding", {type_ids, W["type_emb"]})});
+    VarPtr ln = g.op("layer_norm", {e, W["emb_ln.g"], W["emb_ln.b"]}, {{"eps", c.ln_eps}});
+    h = g.get(ln, 0);
+    if (c.p > 0) h = g.op("dropout", {h}, drop_attrs());
+  } else {
+    h = g.op("add", {g.op("embedding", {ids, W["word_emb"]}), g.op("embedding", {pos_ids, W["pos_emb"]})});
+    if (c.p > 0) h = g.op("dropout", {h}, drop_attrs());
+  }
+  // ---- encoder / decoder blocks
+  for (int64_t l = 0; l < c.L; ++l) {
+    const std::string p = "layer" + std::to_string(l) + ".";
+    if (c.kind == "bert") {  // post-LN
+      VarPtr qkv = linear(h, p + "qkv.w", p + "qkv.b");
+      VarPtr at = g.op("attention", {qkv}, drop_attrs(attn_attrs));
+      VarPtr ao = linear(g.get(at, 0), p + "proj.w", p + "proj.b");
+      VarPtr l1 = g.op("add_layer_norm", {ao, h, W[p + "ln1.g"], W[p + "ln1.b"]}, drop_attrs({{"eps", c.ln_eps}}));
+      VarPtr h1 = g.get(l1, 0);
+      VarPtr f = linear(h1, p + "ffn1.w", p + "ffn1.b", "gelu");
+      VarPtr f2 = linear(f, p + "ffn2.w", p + "ffn2.b");
+      VarPtr l2 = g.op("add_layer_norm", {f2, h1, W[p + "ln2.g"], W[p + "ln2.b"]}, drop_attrs({{"eps", c.ln_eps}}));
+      h = g.get(l2, 0);
+    } else {  // GPT-2 pre-LN: h = h + drop(attn(ln1(h))); h = h + drop(mlp(ln2(h)))
+      VarPtr x1 = g.get(g.op("layer_norm", {h, W[p + "ln1.g"], W[p + "ln1.b"]}, {{"eps", 1e-5}}), 0);
+      VarPtr qkv = linear(x1, p + "qkv.w", p + "qkv.b");
+      VarPtr at = g.op("attention", {qkv}, drop_attrs(attn_attrs));
+      VarPtr ao = linear(g.get(at, 0), p + "proj.w", p + "proj.b");
+      if (c.p > 0) ao = g.op("dropout", {ao}, drop_attrs());
+      h = g.op("add", {ao, h});
+      VarPtr x2 = g.get(g.op("layer_norm", {h, W[p + "ln2.g"], W[p + "ln2.b"]}, {{"eps", 1e-5}}), 0);
+      VarPtr f = linear(x2, p + "ffn1.w", p + "ffn1.b", "gelu");
+      VarPtr f2 = linear(f, p + "ffn2.w", p + "ffn2.b");
+      if (c.p > 0) f2 = g.op("dropout", {f2}, drop_attrs());
+      h = g.op("add", {f2, h});
+    }
+  }
+  // ---- LM head (tied decoder: logits = x . word_emb^T, all positions as HF computes)
+  VarPtr x;
+  if (c.kind == "bert") {
+    VarPtr t = linear(h, "mlm.dense.w", "mlm.dense.b", "gelu");
+    x = g.get(g.op("layer_norm", {t, W["mlm.ln.g"], W["mlm.ln.b"]}, {{"eps", c.ln_eps}}), 0);
+  } else {
+    x = g.get(g.op("layer_norm", {h, W["lnf.g"], W["lnf.b"]}, {{"eps", 1e-5}}), 0);
+  }
+  VarPtr logits;
+  if (c.kind == "bert") {
+    logits = linear(x, "word_emb", "mlm.dec.b", "none", /*tw=*/1);
+  } else {
+    logits = g.op("matmul_t", {x, W["word_emb"]}, {{"tb", std::int64_t(1)}});
+  }
+  VarPtr ce = g.op("cross_entropy", {logits, labels},
+                   {{"classes", c.V}, {"ignore_index", std::int64_t(-100)}, {"grad", std::int64_t(1)}});
+  VarPtr loss = g.get(ce, 0, "loss");
+
+  // ---- backward (autodiff) -> flat f32 gradient [P]
+  // gaps between aligned segments and the tail up to P_pad get zero gradients
+  // (SPEC.md:513,566 zero-padded shards)
+  GradResult gr = autodiff(g, loss, leaves, ts.P_pad);
+  VarPtr grad = gr.flat_grad;
+
+  // ---- optimizer (+ ZeRO-1)
+  std::vector<VarPtr> rets{loss};
+  if (!adam) {
+    VarPtr np = g.op("sgd_update", {par(ts.i_params), grad}, {{"lr", c.lr}});
+    rets.push_back(np);
+    ts.state_binding.push_back({1, ts.i_params});
+  } else {
+    VarPtr gsh = grad;
+    if (c.world > 1)
+      gsh = g.op("reduce_scatter", {grad}, {{"world", c.world}});
+    VarPtr step = par(ts.i_step);
+    VarPtr step1 = g.op("add_scalar", {step}, {{"value", 1.0}});
+    AttrMap aa{{"lr", c.lr}, {"beta1", c.beta1}, {"beta2", c.beta2}, {"eps", c.eps},
+               {"grad_scale", 1.0 / double(c.world)}, {"half", c.dtype == "f32" ? std::string("bf16") : c.dtype}};
+    VarPtr up = g.op("adam_update_ex", {par(ts.i_params), gsh, par(ts.i_m), par(ts.i_v), step1}, aa);
+    VarPtr np = g.get(up, 0), nm = g.get(up, 1), nv = g.get(up, 2), nh = g.get(up, 3);
+    if (c.world > 1)
+      nh = g.op("all_gather", {nh}, {{"world", c.world}, {"shape", std::to_string(ts.P_pad)}});
+    rets.insert(rets.end(), {np, nm, nv, step1});
+    ts.state_binding.push_back({1, ts.i_params});
+    ts.state_binding.push_back({2, ts.i_m});
+    ts.state_binding.push_back({3, ts.i_v});
+    ts.state_binding.push_back({4, ts.i_step});
+    if (amp) {
+      rets.push_back(nh);
+      ts.state_binding.push_back({5, ts.i_p16});
+    }
+  }
+  FunctionPtr raw = g.finish(rets);
+  LetSeq seq = ir::flatten(*raw);
+  ts.fusion = fuse(seq, c.fuse != 0);
+  ts.fn = ir::make_fn(raw->name, raw->params, seq);
+  return ts;
+}
+
+/// trainc::Rng (tensor.hpp:145-176) init: weights uniform(-0.02, 0.02) in
+/// segment order from seed_w; LayerNorm gamma 1, biases/beta 0.
+inline std::vector<float> init_params(const TrainStep& ts) {
+  std::vector<float> p(size_t(ts.P_pad), 0.0f);
+  Rng rng(static_cast<uint64_t>(ts.cfg.seed_w));
+  for (auto& s : ts.segs) {
+    for (int64_t i = 0; i < s.numel; ++i) {
+      float v = 0.0f;
+      if (s.init == Init::Uniform) v = rng.uniform(-0.02f, 0.02f);
+      else if (s.init == Init::Ones) v = 1.0f;
+      p[size_t(s.offset + i)] = v;
+    }
+  }
+  // vocabulary padding rows of the word embedding stay zero (never indexed)
+  for (auto& s : ts.segs)
+    if (s.name == "word_emb")
+      for (int64_t r = ts.cfg.V; r < ts.cfg.vocab_pad(); ++r)
+        for (int64_t j = 0; j < ts.cfg.H; ++j) p[size_t(s.offset + r * ts.cfg.H + j)] = 0.0f;
+  return p;
+}
+
+inline uint16_t bf16_bits(float f) {
+  uint32_t x;
+  std::memcpy(&x, &f, 4);
+  if ((x & 0x7fffffffu) > 0x7f800000u) return uint16_t((x >> 16) | 0x40u);
+  x += 0x7fffu + ((x >> 16) & 1u);
+  return uint16_t(x >> 16);
+}
+
+}  // namespace tb

@@ -1,0 +1,271 @@
+"""Python binding of libtrainc_b200.so -- the b200 training-step runtime.
+
+    s = Session(ModelConfig.bert_base(B=32))   # graph -> autodiff -> fusion -> VM
+    s.init_params()
+    ids, labels = synthetic_batch(s.cfg)
+    s.set_batch(ids, labels); s.step(); loss = s.loss()
+
+Every kernel the step launches is a libtcb200 sm_100a kernel; there is no CPU
+path here (creating a session on a machine without a B200 raises).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass, field, fields
+
+import numpy as np
+
+from . import runtime
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+HOST_LIB = os.path.join(PKG, "lib", "libtrainc_b200.so")
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        runtime.lib()  # libtcb200 first (dependency, rpath $ORIGIN)
+        if not os.path.exists(HOST_LIB):
+            raise RuntimeError(f"{HOST_LIB} not built; run __graft_entry__.build()")
+        L = ctypes.CDLL(HOST_LIB)
+        L.tb_last_error.restype = ctypes.c_char_p
+        L.tb_session_create.restype = ctypes.c_void_p
+        L.tb_session_create.argtypes = [ctypes.c_char_p, ctypes.c_int]
+        for f in ("tb_session_destroy", "tb_session_init_params", "tb_session_sync",
+                  "tb_session_fetch_loss"):
+            getattr(L, f).argtypes = [ctypes.c_void_p]
+        L.tb_session_step.argtypes = [ctypes.c_void_p, ctypes.c_int]
+        L.tb_session_info.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64), ctypes.c_int]
+        L.tb_session_set_batch.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+        L.tb_session_loss_value.restype = ctypes.c_float
+        L.tb_session_loss_value.argtypes = [ctypes.c_void_p]
+        L.tb_session_stream.restype = ctypes.c_void_p
+        L.tb_session_stream.argtypes = [ctypes.c_void_p]
+        L.tb_session_param.argtypes = [ctypes.c_void_p, ctypes.c_char_p, ctypes.POINTER(ctypes.c_void_p),
+                                       ctypes.POINTER(ctypes.c_int64)]
+        L.tb_session_ids_buffer.restype = ctypes.c_void_p
+        L.tb_session_ids_buffer.argtypes = [ctypes.c_void_p]
+        L.tb_session_labels_buffer.restype = ctypes.c_void_p
+        L.tb_session_labels_buffer.argtypes = [ctypes.c_void_p]
+        L.tb_session_text.restype = ctypes.c_char_p
+        L.tb_session_text.argtypes = [ctypes.c_void_p, ctypes.c_char_p]
+        L.tb_session_segments.restype = ctypes.c_char_p
+        L.tb_session_segments.argtypes = [ctypes.c_void_p]
+        L.tb_session_set_comm.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
+        L.tb_graph_info.argtypes = [ctypes.c_char_p, ctypes.POINTER(ctypes.c_int64), ctypes.c_int]
+        L.tb_graph_text.restype = ctypes.c_char_p
+        L.tb_graph_text.argtypes = [ctypes.c_char_p, ctypes.c_char_p]
+        L.tb_synthetic_batch.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p,
+                                         ctypes.c_void_p, ctypes.c_int]
+        L.tb_cache_stats.argtypes = [ctypes.POINTER(ctypes.c_int64)]
+        _lib = L
+    return _lib
+
+
+def _check(rc):
+    if rc != 0:
+        raise RuntimeError(lib().tb_last_error().decode())
+
+
+@dataclass
+class ModelConfig:
+    """Mirrors tb::ModelCfg (host/models.hpp)."""
+    kind: str = "bert"
+    L: int = 2
+    H: int = 128
+    A: int = 2
+    F: int = 512
+    V: int = 1024
+    S: int = 128
+    B: int = 8
+    dtype: str = "f32"
+    p: float = 0.0
+    opt: str = "sgd"
+    lr: float = 0.01
+    beta1: float = 0.9
+    beta2: float = 0.999
+    eps: float = 1e-6
+    seed_w: int = 42
+    seed_d: int = 1234
+    seed_drop: int = 7
+    world: int = 1
+    fuse: int = 1
+    extra: dict = field(default_factory=dict)  # runtime keys: budget, schedule, rank
+
+    def cfg_string(self, model_only: bool = False) -> str:
+        kv = [f"{f.name}={getattr(self, f.name)}" for f in fields(self) if f.name != "extra"]
+        if not model_only:
+            kv += [f"{k}={v}" for k, v in self.extra.items()]
+        return ";".join(kv)
+
+    @property
+    def T(self) -> int:
+        return self.B * self.S
+
+    # --- the BASELINE.json configs (SURVEY.md §8 notation) ---
+    @staticmethod
+    def tiny(**kw):  # C1: tiny BERT fp32 SGD (A=2, F=512, V=1024 assumed)
+        return ModelConfig(**{**dict(kind="bert", L=2, H=128, A=2, F=512, V=1024, S=128, B=8,
+                                     dtype="f32", opt="sgd", lr=0.01), **kw})
+
+    @staticmethod
+    def bert_base(**kw):  # C2: BERT-base MLM, bf16 AutoCast + Adam
+        return ModelConfig(**{**dict(kind="bert", L=12, H=768, A=12, F=3072, V=30522, S=128, B=32,
+                                     dtype="bf16", opt="adam", lr=1e-4, eps=1e-6, p=0.1), **kw})
+
+    @staticmethod
+    def bert_large(**kw):  # C4
+        return ModelConfig(**{**dict(kind="bert", L=24, H=1024, A=16, F=4096, V=30522, S=128, B=32,
+                                     dtype="bf16", opt="adam", lr=1e-4, eps=1e-6, p=0.1), **kw})
+
+    @staticmethod
+    def gpt2_medium(**kw):  # C3
+        return ModelConfig(**{**dict(kind="gpt2", L=24, H=1024, A=16, F=4096, V=50257, S=512, B=8,
+                                     dtype="bf16", opt="adam", lr=1e-4, eps=1e-6, p=0.1), **kw})
+
+    @staticmethod
+    def gpt2_xl(**kw):  # C5
+        return ModelConfig(**{**dict(kind="gpt2", L=48, H=1600, A=25, F=6400, V=50257, S=1024, B=8,
+                                     dtype="bf16", opt="adam", lr=1e-4, eps=1e-6, p=0.1), **kw})
+
+
+def synthetic_batch(cfg: ModelConfig, seed: int | None = None):
+    """SURVEY.md §8d synthetic data via trainc::Rng (MLM: 15% labelled;
+    causal LM: next-token labels)."""
+    T = cfg.T
+    ids = np.empty(T, np.int32)
+    labels = np.empty(T, np.int32)
+    _check(lib().tb_synthetic_batch(T, cfg.V, cfg.seed_d if seed is None else seed, ids.ctypes.data,
+                                    labels.ctypes.data, int(cfg.kind == "gpt2")))
+    return ids, labels
+
+
+INFO_FIELDS = ["P", "P_pad", "T", "arena_bytes", "state_bytes", "planner_peak", "instructions",
+               "kernels_per_step", "lets", "fused_dact", "fused_ln_dy2", "fused_emb", "dead",
+               "remat_replays", "peak_before_remat", "compile_us", "shard"]
+GRAPH_FIELDS = ["P", "P_pad", "lets", "planner_peak", "arena_plan_bytes", "state_bytes", "fused_dact",
+                "fused_ln_dy2", "fused_emb", "dead", "remat_replays", "peak_before_remat",
+                "peak_after_remat"]
+
+
+def graph_info(cfg: ModelConfig) -> dict:
+    """CPU-only: build + plan the step graph without a device."""
+    out = (ctypes.c_int64 * len(GRAPH_FIELDS))()
+    _check(lib().tb_graph_info(cfg.cfg_string().encode(), out, len(GRAPH_FIELDS)))
+    return dict(zip(GRAPH_FIELDS, list(out)))
+
+
+def graph_text(cfg: ModelConfig, what: str = "ir") -> str:
+    t = lib().tb_graph_text(cfg.cfg_string().encode(), what.encode()).decode()
+    if not t:
+        raise RuntimeError(lib().tb_last_error().decode())
+    return t
+
+
+class Session:
+    def __init__(self, cfg: ModelConfig, device: int = 0):
+        self.cfg = cfg
+        h = lib().tb_session_create(cfg.cfg_string().encode(), device)
+        if not h:
+            raise RuntimeError(lib().tb_last_error().decode())
+        self.h = h
+        self.T = cfg.T
+
+    def info(self) -> dict:
+        out = (ctypes.c_int64 * len(INFO_FIELDS))()
+        _check(lib().tb_session_info(self.h, out, len(INFO_FIELDS)))
+        return dict(zip(INFO_FIELDS, list(out)))
+
+    def init_params(self):
+        _check(lib().tb_session_init_params(self.h))
+
+    def set_batch(self, ids: np.ndarray, labels: np.ndarray):
+        ids = np.ascontiguousarray(ids, np.int32)
+        labels = np.ascontiguousarray(labels, np.int32)
+        _check(lib().tb_session_set_batch(self.h, ids.ctypes.data, labels.ctypes.data))
+
+    def staging(self):
+        """numpy views of the pinned host staging buffers (ids, labels)."""
+        L = lib()
+        T = self.T
+        ids = np.ctypeslib.as_array((ctypes.c_int32 * T).from_address(L.tb_session_ids_buffer(self.h)))
+        lab = np.ctypeslib.as_array((ctypes.c_int32 * T).from_address(L.tb_session_labels_buffer(self.h)))
+        return ids, lab
+
+    def set_batch_from_staging(self):
+        L = lib()
+        _check(L.tb_session_set_batch(self.h, L.tb_session_ids_buffer(self.h), L.tb_session_labels_buffer(self.h)))
+
+    def step(self, graph: bool = True):
+        _check(lib().tb_session_step(self.h, int(graph)))
+
+    def fetch_loss(self):
+        _check(lib().tb_session_fetch_loss(self.h))
+
+    def sync(self):
+        _check(lib().tb_session_sync(self.h))
+
+    def loss(self) -> float:
+        self.fetch_loss()
+        self.sync()
+        return float(lib().tb_session_loss_value(self.h))
+
+    @property
+    def stream(self) -> int:
+        return lib().tb_session_stream(self.h)
+
+    def param_ptr(self, name: str):
+        p = ctypes.c_void_p()
+        n = ctypes.c_int64()
+        _check(lib().tb_session_param(self.h, name.encode(), ctypes.byref(p), ctypes.byref(n)))
+        return p.value, n.value
+
+    def read(self, name: str, dtype=np.float32) -> np.ndarray:
+        ptr, nbytes = self.param_ptr(name)
+        out = np.empty(nbytes // np.dtype(dtype).itemsize, dtype)
+        self.sync()
+        runtime.check(runtime.lib().tcb_memcpy(ctypes.c_void_p(out.ctypes.data), ctypes.c_void_p(ptr),
+                                               ctypes.c_uint64(nbytes), 1, None))
+        runtime.check(runtime.lib().tcb_device_sync())
+        return out
+
+    def write(self, name: str, arr: np.ndarray):
+        ptr, nbytes = self.param_ptr(name)
+        arr = np.ascontiguousarray(arr)
+        assert arr.nbytes == nbytes, (arr.nbytes, nbytes)
+        runtime.check(runtime.lib().tcb_memcpy(ctypes.c_void_p(ptr), ctypes.c_void_p(arr.ctypes.data),
+                                               ctypes.c_uint64(nbytes), 0, None))
+        runtime.check(runtime.lib().tcb_device_sync())
+
+    def segments(self) -> list[tuple[str, int, int]]:
+        out = []
+        for line in lib().tb_session_segments(self.h).decode().splitlines():
+            n, o, k = line.split()
+            out.append((n, int(o), int(k)))
+        return out
+
+    def text(self, what: str) -> str:
+        return lib().tb_session_text(self.h, what.encode()).decode()
+
+    def set_comm(self, comm: int):
+        _check(lib().tb_session_set_comm(self.h, comm))
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().tb_session_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def cache_stats() -> dict:
+    out = (ctypes.c_int64 * 3)()
+    _check(lib().tb_cache_stats(out))
+    return {"compiles": out[0], "hits": out[1], "size": out[2]}

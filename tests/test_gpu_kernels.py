@@ -237,8 +237,8 @@ def test_add_layer_norm_and_backward(p):
     assert bits_equal(g[1], o[1])  # s = round(dropout(x) + r): bit-exact incl. the Philox mask
     assert rel_err(g[0], o[0]) < BF16_TOL
     s, mean, rstd = o[1], o[2], o[3]
-    dy, dres = rn(T, H), rn(T, H)
-    g, o = run_both("layer_norm_dx", [(s, BF16), (gm, F32), (mean, F32), (rstd, F32), (dy, BF16), (dres, BF16)],
+    dy, dy2 = rn(T, H), rn(T, H)
+    g, o = run_both("layer_norm_dx", [(s, BF16), (gm, F32), (mean, F32), (rstd, F32), (dy, BF16), (dy2, BF16)],
                     [((T, H), BF16), ((H,), F32), ((H,), F32), ((T, H), BF16)], attrs)
     assert rel_err(g[0], o[0]) < 5e-3 and rel_err(g[3], o[3]) < 5e-3
     assert rel_err(g[1], o[1]) < 1e-5 and rel_err(g[2], o[2]) < 1e-5
