@@ -1,0 +1,384 @@
+#!/usr/bin/env python3
+"""Benchmark: BERT-base MLM seq128 training samples/s on B200 (BASELINE.json
+metric, config C2: B=32 per GPU, bf16 AutoCast + Adam, dropout 0.1, synthetic
+data, random init), plus the roofline of the dominant kernel and the CPU
+reference path.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 runs under torchrun (one process per GPU, ZeRO-1 over NCCL, weak scaling:
+B=32 per GPU).  Prints ONE JSON line on rank 0.
+
+Timing: W untimed warm-up steps, then K steps between a barrier +
+synchronize on both sides, CUDA events on the session's compute stream, max
+over ranks.  `value` replays the captured CUDA graph with the batch already in
+HBM; `e2e` adds, every step, the H2D copy of that step's ids/labels from pinned
+host memory and the D2H read of the loss.  The step's working set (bf16
+weights 0.22 GB, fp32 master+Adam 1.3 GB, activations ~2 GB) exceeds the
+126 MB L2, so no explicit flush is needed between steps.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "train samples/sec (BERT-base, seq128) at 1/8 B200; max batch under remat"
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def load_peaks():
+    try:
+        with open(PEAKS_PATH) as f:
+            p = json.load(f)
+        return p, "measured"
+    except Exception:
+        return FALLBACK_PEAKS, "fallback"
+
+
+def c2_config(world: int):
+    from paper_2303_04759_b200.session import ModelConfig
+    return ModelConfig.bert_base(B=32, world=world)
+
+
+def model_flops_per_sample(cfg) -> float:
+    """3 x forward GEMM FLOPs, dense S x S attention, all-position MLM logits
+    (85.50 GFLOP/sample for C2)."""
+    S, H, F, L, V = cfg.S, cfg.H, cfg.F, cfg.L, cfg.V
+    per_tok = L * (2 * H * 3 * H + 2 * H * H + 2 * 2 * H * F + 2 * 2 * S * H) + 2 * H * H + 2 * H * V
+    return 3.0 * per_tok * S
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled DURING the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.lines = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        sm, mx, reasons = [], 0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9 or f[0] != str(self.idx):
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = max(mx, float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ ours
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", init_method="env://")
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def make_comm(world, rank):
+    import ctypes
+
+    import torch.distributed as dist
+    from paper_2303_04759_b200 import runtime
+    L = runtime.lib()
+    uid = ctypes.create_string_buffer(128)
+    if rank == 0:
+        runtime.check(L.tcb_comm_unique_id(uid))
+    obj = [bytes(uid.raw) if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    uid = ctypes.create_string_buffer(obj[0], 128)
+    comm = ctypes.c_void_p()
+    runtime.check(L.tcb_comm_init_rank(uid, world, rank, ctypes.byref(comm)))
+    return comm.value
+
+
+class Events:
+    def __init__(self):
+        import ctypes
+
+        from paper_2303_04759_b200 import runtime
+        self.L = runtime.lib()
+        self.a, self.b = ctypes.c_void_p(), ctypes.c_void_p()
+        runtime.check(self.L.tcb_event_create(ctypes.byref(self.a)))
+        runtime.check(self.L.tcb_event_create(ctypes.byref(self.b)))
+
+    def start(self, stream):
+        self.L.tcb_event_record(self.a, stream)
+
+    def stop(self, stream):
+        self.L.tcb_event_record(self.b, stream)
+
+    def ms(self) -> float:
+        import ctypes
+        self.L.tcb_event_elapsed_ms.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(ctypes.c_float)]
+        v = ctypes.c_float()
+        from paper_2303_04759_b200 import runtime
+        runtime.check(self.L.tcb_event_elapsed_ms(self.a, self.b, ctypes.byref(v)))
+        return float(v.value)
+
+
+def gemm_roofline(stream, peaks, iters=50):
+    """Dominant kernel: the tcgen05 GEMM at the BERT-base FFN1 forward shape
+    (linear 4096x768 . 768x3072 + bias + GeLU, pre-activation saved), timed with
+    CUDA events over `iters` launches on the session stream."""
+    import ctypes
+
+    import torch
+    from paper_2303_04759_b200.abi import BF16, F32
+    from paper_2303_04759_b200.runtime import Plan
+    M, K, N = 4096, 768, 3072
+    x = torch.randn(M, K, device="cuda").to(torch.bfloat16)
+    w = (0.02 * torch.randn(K, N, device="cuda")).to(torch.bfloat16)
+    b = torch.zeros(N, device="cuda")
+    y = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    u = torch.empty_like(y)
+    torch.cuda.synchronize()
+    plan = Plan("linear", [((M, K), BF16), ((K, N), BF16), ((N,), F32)], [((M, N), BF16), ((M, N), BF16)],
+                {"act": "gelu", "save_preact": 1})
+    ins, outs = [x.data_ptr(), w.data_ptr(), b.data_ptr()], [y.data_ptr(), u.data_ptr()]
+    for _ in range(5):
+        plan.launch(ins, outs, stream)
+    ev = Events()
+    from paper_2303_04759_b200 import runtime
+    runtime.check(runtime.lib().tcb_stream_sync(ctypes.c_void_p(stream)))
+    ev.start(stream)
+    for _ in range(iters):
+        plan.launch(ins, outs, stream)
+    ev.stop(stream)
+    runtime.check(runtime.lib().tcb_stream_sync(ctypes.c_void_p(stream)))
+    ms = ev.ms() / iters
+    flops = 2.0 * M * N * K
+    achieved = flops / (ms * 1e-3) / 1e12
+    peak = peaks.get("bf16_tflops", FALLBACK_PEAKS["bf16_tflops"])
+    return {"bound": "tensor", "achieved": round(achieved, 1), "peak": peak, "unit": "TFLOP/s",
+            "frac": round(achieved / peak, 4), "traffic": None,
+            "kernel": f"b200.linear tcgen05 {M}x{K}x{N} bf16 (+bias+gelu+preact)", "us_per_launch": round(ms * 1e3, 2)}
+
+
+def cpu_baseline_port():
+    """The CPU oracle (ANF interpreter over the exec_base restatement, one
+    thread) on a bounded sample: ONE C2 training step at B=1 (1 sample, S=128,
+    full 12 layers + MLM head)."""
+    from oracle.interp_py import Interp
+    from paper_2303_04759_b200.session import ModelConfig, synthetic_batch
+    cfg = ModelConfig.bert_base(B=1)
+    o = Interp(cfg.cfg_string(model_only=True))
+    ids, labels = synthetic_batch(cfg)
+    t = time.time()
+    o.step(ids, labels)
+    dt = time.time() - t
+    return {"value": round(1.0 / dt, 5), "unit": "samples/s", "cores": 1, "kind": "port",
+            "sample": f"1 C2 train step at B=1 (S=128, 12 layers, bf16-emulated, Adam): {dt:.1f} s single-thread"}
+
+
+def run_ours(args):
+    world, rank, local = dist_setup()
+    from paper_2303_04759_b200.session import Session, synthetic_batch
+    peaks, peak_kind = load_peaks()
+    cfg = c2_config(world)
+    cfg.extra["rank"] = rank
+    s = Session(cfg, device=local)
+    if world > 1:
+        s.set_comm(make_comm(world, rank))
+    s.init_params()
+    ids, labels = synthetic_batch(cfg, seed=cfg.seed_d + rank)
+    h_ids, h_lab = s.staging()
+    h_ids[:] = ids
+    h_lab[:] = labels
+    s.set_batch_from_staging()
+    info = s.info()
+    stream = s.stream
+    for _ in range(args.warmup):
+        s.step(graph=True)
+    s.sync()
+    first_loss = s.loss()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    # --- device-resident timed region
+    ev = Events()
+    barrier(world)
+    s.sync()
+    ev.start(stream)
+    for _ in range(args.steps):
+        s.step(graph=True)
+    ev.stop(stream)
+    s.sync()
+    barrier(world)
+    ms = max_over_ranks(ev.ms() / args.steps, world)
+    # --- end-to-end timed region: H2D batch + step + D2H loss every step
+    ev2 = Events()
+    barrier(world)
+    s.sync()
+    ev2.start(stream)
+    for _ in range(args.steps):
+        s.set_batch_from_staging()
+        s.step(graph=True)
+        s.fetch_loss()
+    ev2.stop(stream)
+    s.sync()
+    barrier(world)
+    ms_e2e = max_over_ranks(ev2.ms() / args.steps, world)
+    clk = clocks.stop()
+    last_loss = s.loss()
+
+    samples = cfg.B * world
+    value = samples / (ms * 1e-3)
+    e2e = samples / (ms_e2e * 1e-3)
+    roof = gemm_roofline(stream, peaks) if rank == 0 else None
+    if rank != 0:
+        return
+    roof["peak_source"] = peak_kind
+    step_flops = model_flops_per_sample(cfg) * cfg.B
+    out = {
+        "metric": METRIC,
+        "value": round(value, 2),
+        "unit": "samples/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms, 4),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "bf16",
+        "data": "synthetic (trainc::Rng ids, 15% MLM labels; random-init weights uniform(-0.02,0.02))",
+        "config": {"workload": "C2: BERT-base MLM train step (L12 H768 A12 F3072 V30522), bf16 AutoCast + Adam, dropout 0.1",
+                   "model": "bert-base", "global_batch": samples, "seq_len": cfg.S,
+                   "parallelism": f"dp{world}" + (" zero1" if world > 1 else ""),
+                   "l2": "working set > 126 MB L2 (no flush needed)",
+                   "model_tflops": round(step_flops / (ms * 1e-3) / 1e12, 1),
+                   "step_roofline_frac_gemm_only": round(step_flops / (ms * 1e-3) / 1e12 /
+                                                         peaks.get("bf16_tflops_sustained", 1400.0), 4),
+                   "arena_bytes": info["arena_bytes"], "state_bytes": info["state_bytes"],
+                   "kernels_per_step": info["kernels_per_step"], "loss_first": round(first_loss, 4),
+                   "loss_last": round(last_loss, 4)},
+        "e2e": {"value": round(e2e, 2), "unit": "samples/s", "h2d_bytes_per_step": 2 * cfg.T * 4,
+                "d2h_bytes_per_step": 4, "ms_per_step": round(ms_e2e, 4)},
+        "gpu_launches": info["kernels_per_step"] * args.steps,
+        "clocks": clk,
+        "roofline": roof,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline_port()
+    print(json.dumps(out), flush=True)
+
+
+# ------------------------------------------------------------ reference arm
+def _replica(_):
+    from oracle.interp_py import Interp
+    from paper_2303_04759_b200.session import ModelConfig, synthetic_batch
+    cfg = ModelConfig.bert_base(B=1)
+    o = Interp(cfg.cfg_string(model_only=True))
+    ids, labels = synthetic_batch(cfg)
+    t = time.time()
+    o.step(ids, labels)
+    return time.time() - t
+
+
+def run_reference(args):
+    """The reference's CPU path (the exec_base restatement driven by the ANF
+    interpreter, pinned bit-exact to the reference's own kernels) on all host
+    cores: independent single-thread replicas, one C2 step at B=1 each."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import multiprocessing as mp
+    cores = os.cpu_count() or 1
+    n = max(1, min(cores, args.steps))
+    t = time.time()
+    with mp.get_context("spawn").Pool(n) as pool:
+        times = pool.map(_replica, range(n))
+    wall = time.time() - t
+    value = n / wall
+    sample = f"{n} concurrent single-thread replicas x 1 C2 step at B=1 (S=128); per-step {min(times):.1f}-{max(times):.1f} s"
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": round(value, 5), "unit": "samples/s",
+        "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1000 * wall, 1), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32 (bf16-emulated)", "data": "synthetic",
+        "config": {"workload": "C2 BERT-base MLM step, sampled at B=1 per replica", "model": "bert-base",
+                   "global_batch": n, "seq_len": 128, "parallelism": f"{n} CPU replicas"},
+        "cpu_baseline": {"value": round(value, 5), "unit": "samples/s", "cores": n, "kind": "port", "sample": sample},
+        "e2e": {"value": round(value, 5), "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

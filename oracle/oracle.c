@@ -385,17 +385,49 @@ static int reduce_op(const orc_tensor* x, orc_tensor* out, const char* axes_s, i
  * transposed (the extension that absorbs `transpose`). */
 static void gemm_acc(const float* A, const float* B, float* C, int64_t M, int64_t N, int64_t K,
                      int ta, int tb, float alpha) {
-  for (int64_t i = 0; i < M; ++i) {
-    for (int64_t j = 0; j < N; ++j) {
-      float acc = 0.0f;
-      for (int64_t kk = 0; kk < K; ++kk) {
-        float a = ta ? A[kk * M + i] : A[i * K + kk];
-        float b = tb ? B[j * K + kk] : B[kk * N + j];
-        acc += a * b;
+  /* Evaluated in matmul_blocked's loop order (backends.hpp:280-304, tile 32):
+   * each C[i][j] still accumulates a*b in ascending k from 0.0f, so the bits
+   * equal matmul_ref's i-j-k loop (the opt/ref equivalence the reference relies
+   * on) -- only the memory access pattern differs. */
+  const float* Ar = A;
+  const float* Br = B;
+  float* At = NULL;
+  float* Bt = NULL;
+  if (ta) { /* materialise A as [M, K] */
+    At = (float*)malloc(sizeof(float) * (size_t)(M * K));
+    for (int64_t k = 0; k < K; ++k)
+      for (int64_t i = 0; i < M; ++i) At[i * K + k] = A[k * M + i];
+    Ar = At;
+  }
+  if (tb) { /* materialise B as [K, N] */
+    Bt = (float*)malloc(sizeof(float) * (size_t)(K * N));
+    for (int64_t j = 0; j < N; ++j)
+      for (int64_t k = 0; k < K; ++k) Bt[k * N + j] = B[j * K + k];
+    Br = Bt;
+  }
+  for (int64_t i = 0; i < M * N; ++i) C[i] = 0.0f;
+  const int64_t tile = 32;
+  for (int64_t i0 = 0; i0 < M; i0 += tile) {
+    const int64_t imax = i0 + tile < M ? i0 + tile : M;
+    for (int64_t k0 = 0; k0 < K; k0 += tile) {
+      const int64_t kmax = k0 + tile < K ? k0 + tile : K;
+      for (int64_t j0 = 0; j0 < N; j0 += 256) {
+        const int64_t jmax = j0 + 256 < N ? j0 + 256 : N;
+        for (int64_t i = i0; i < imax; ++i) {
+          float* crow = C + i * N;
+          for (int64_t kk = k0; kk < kmax; ++kk) {
+            const float aik = Ar[i * K + kk];
+            const float* brow = Br + kk * N;
+            for (int64_t j = j0; j < jmax; ++j) crow[j] += aik * brow[j];
+          }
+        }
       }
-      C[i * N + j] = alpha == 1.0f ? acc : acc * alpha;
     }
   }
+  if (alpha != 1.0f)
+    for (int64_t i = 0; i < M * N; ++i) C[i] *= alpha;
+  free(At);
+  free(Bt);
 }
 
 enum { ACT_NONE = 0, ACT_RELU = 1, ACT_TANH = 2, ACT_GELU = 3 };

@@ -188,6 +188,19 @@ inline void register_default_adjoints() {
     return {c.g.op("matmul_t", {c.dout[0], b}, {{"tb", std::int64_t(1)}}),
             c.g.op("matmul_t", {a, c.dout[0]}, {{"ta", std::int64_t(1)}})};
   };
+  // matmul_t (ta = 0): C = A op(B); dA = dC op(B)^T, dB = (A^T dC) or (dC^T A), f32
+  A["matmul_t"] = [](AdjointCtx& c) -> std::vector<VarPtr> {
+    const auto& at = c.let.value->call_attrs;
+    if (ir::attr_int(at, "ta", 0) || ir::attr_double(at, "alpha", 1.0) != 1.0)
+      throw NonDifferentiable("matmul_t adjoint supports ta=0, alpha=1");
+    const int tb = int(ir::attr_int(at, "tb", 0));
+    auto a = arg_var(c.let.value, 0), b = arg_var(c.let.value, 1);
+    VarPtr dy = c.dout[0];
+    VarPtr da = c.g.op("matmul_t", {dy, b}, {{"tb", std::int64_t(tb ? 0 : 1)}});
+    VarPtr db = tb ? c.g.op("matmul_t", {dy, a}, {{"ta", std::int64_t(1)}, {"out", std::string("f32")}})
+                   : c.g.op("matmul_t", {a, dy}, {{"ta", std::int64_t(1)}, {"out", std::string("f32")}});
+    return {da, db};
+  };
   A["convert"] = [](AdjointCtx& c) -> std::vector<VarPtr> {
     auto a = arg_var(c.let.value, 0);
     return {c.g.op("convert", {c.dout[0]}, {{"to", std::string(dtype_str(a->ty.tensor().dtype))}})};

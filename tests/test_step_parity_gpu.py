@@ -28,13 +28,14 @@ def rel(a, b):
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
 
 
-def run_pair(cfg: ModelConfig, steps: int, graph: bool = True):
+def run_pair(cfg: ModelConfig, steps: int, graph: bool = True, same_batch: bool = True):
+    """same_batch: repeat one batch (the loss must then fall step over step)."""
     s = Session(cfg)
     s.init_params()
     o = Interp(cfg.cfg_string(model_only=True))
     gl, ol = [], []
     for k in range(steps):
-        ids, labels = synthetic_batch(cfg, seed=cfg.seed_d + k)
+        ids, labels = synthetic_batch(cfg, seed=cfg.seed_d + (0 if same_batch else k))
         s.set_batch(ids, labels)
         s.step(graph=graph)
         gl.append(s.loss())
@@ -44,7 +45,7 @@ def run_pair(cfg: ModelConfig, steps: int, graph: bool = True):
 
 def test_c1_tiny_fp32_sgd_parity():
     """C1: tiny BERT fp32 + SGD: loss and updated params within 1e-4 relative."""
-    cfg = ModelConfig.tiny()
+    cfg = ModelConfig.tiny(lr=0.1)
     s, o, gl, ol = run_pair(cfg, steps=3)
     assert np.all(np.abs(gl - ol) <= 1e-4 * np.abs(ol)), (gl, ol)
     P = s.info()["P_pad"]
