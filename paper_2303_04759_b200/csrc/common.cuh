@@ -215,6 +215,16 @@ void dispatch_float(int dtype, Fn&& f) {
   fail(TCB_ERR_TYPE, std::string("unsupported dtype ") + dtype_name(dtype));
 }
 
+// Plan-owned device scratch (allocated once at plan creation, freed with the
+// plan).  Launches of one plan are stream-ordered, so reuse is race-free.
+struct Scratch {
+  void* p = nullptr;
+  explicit Scratch(size_t bytes) { TCB_CUDA(cudaMalloc(&p, bytes ? bytes : 16)); }
+  ~Scratch() {
+    if (p) cudaFree(p);
+  }
+};
+
 // ------------------------------------------------------------------ plans
 using RunFn = std::function<void(const tcb_tensor* in, tcb_tensor* out, cudaStream_t s)>;
 

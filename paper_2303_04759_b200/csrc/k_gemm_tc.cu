@@ -143,8 +143,52 @@ __device__ __forceinline__ void decode_tile(const TcParams& P, int64_t t, int& z
   nb = int(r - int64_t(mb) * P.n_blocks);
 }
 
+// Store 32 consecutive f32 values of one row into dst (dtype dt).  Every loop
+// is unrolled with compile-time indices so v[] stays in registers (a runtime
+// trip count here made ptxas spill the whole array to local memory).
+__device__ __forceinline__ void store_row32(void* dst, int dt, int64_t base, const float (&v)[32], bool vec,
+                                            int nvalid) {
+  if (dt == TCB_F32) {
+    float* o = static_cast<float*>(dst) + base;
+    if (vec) {
+#pragma unroll
+      for (int j = 0; j < 32; j += 4) *reinterpret_cast<float4*>(o + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (j < nvalid) o[j] = v[j];
+    }
+  } else if (dt == TCB_BF16) {
+    __nv_bfloat16* o = static_cast<__nv_bfloat16*>(dst) + base;
+    if (vec) {
+#pragma unroll
+      for (int j = 0; j < 32; j += 8) {
+        uint4 q;
+        __nv_bfloat162 h0 = __floats2bfloat162_rn(v[j], v[j + 1]);
+        __nv_bfloat162 h1 = __floats2bfloat162_rn(v[j + 2], v[j + 3]);
+        __nv_bfloat162 h2 = __floats2bfloat162_rn(v[j + 4], v[j + 5]);
+        __nv_bfloat162 h3 = __floats2bfloat162_rn(v[j + 6], v[j + 7]);
+        q.x = *reinterpret_cast<uint32_t*>(&h0);
+        q.y = *reinterpret_cast<uint32_t*>(&h1);
+        q.z = *reinterpret_cast<uint32_t*>(&h2);
+        q.w = *reinterpret_cast<uint32_t*>(&h3);
+        *reinterpret_cast<uint4*>(o + j) = q;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (j < nvalid) o[j] = __float2bfloat16_rn(v[j]);
+    }
+  } else {
+    __half* o = static_cast<__half*>(dst) + base;
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (j < nvalid) o[j] = __float2half_rn(v[j]);
+  }
+}
+
 // 32 consecutive output columns of one row: epilogue + store
-__device__ __forceinline__ void epi_store32(const TcParams& P, const uint32_t* r, int64_t m, int64_t n0,
+__device__ __forceinline__ void epi_store32(const TcParams& P, const uint32_t (&r)[32], int64_t m, int64_t n0,
                                             int64_t coff) {
   float v[32];
 #pragma unroll
@@ -152,9 +196,16 @@ __device__ __forceinline__ void epi_store32(const TcParams& P, const uint32_t* r
   const int64_t base = coff + m * P.ldc + n0;
   const int nvalid = int(P.N - n0 < 32 ? P.N - n0 : 32);
   if (P.bias) {
+    if (P.bias_dtype == TCB_F32) {
+      const float* b = static_cast<const float*>(P.bias) + n0;
 #pragma unroll
-    for (int j = 0; j < 32; ++j)
-      if (j < nvalid) v[j] += ld_e(P.bias, P.bias_dtype, n0 + j);
+      for (int j = 0; j < 32; ++j)
+        if (j < nvalid) v[j] += __ldg(b + j);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (j < nvalid) v[j] += ld_e(P.bias, P.bias_dtype, n0 + j);
+    }
   }
   if (P.dact != ACT_NONE) {
 #pragma unroll
@@ -162,48 +213,18 @@ __device__ __forceinline__ void epi_store32(const TcParams& P, const uint32_t* r
       if (j < nvalid) v[j] *= dact_f(P.dact, ld_e(P.aux, P.aux_dtype, base + j));
   }
   const bool vec = P.c_vec_ok && nvalid == 32;
-  for (int pass = 0; pass < (P.aux_out ? 2 : 1); ++pass) {
-    void* dst = pass == 0 && P.aux_out ? P.aux_out : P.c;
-    const bool final_pass = !(pass == 0 && P.aux_out);
-    float w[32];
+  if (P.aux_out) store_row32(P.aux_out, P.c_dtype, base, v, vec, nvalid);  // pre-activation u
+  if (P.act != ACT_NONE) {
 #pragma unroll
-    for (int j = 0; j < 32; ++j) w[j] = final_pass && P.act != ACT_NONE ? act_f(P.act, v[j]) : v[j];
-    if (P.c_dtype == TCB_F32) {
-      float* o = static_cast<float*>(dst) + base;
-      if (vec) {
-#pragma unroll
-        for (int j = 0; j < 32; j += 4) *reinterpret_cast<float4*>(o + j) = make_float4(w[j], w[j + 1], w[j + 2], w[j + 3]);
-      } else {
-        for (int j = 0; j < nvalid; ++j) o[j] = w[j];
-      }
-    } else if (P.c_dtype == TCB_BF16) {
-      __nv_bfloat16* o = static_cast<__nv_bfloat16*>(dst) + base;
-      if (vec) {
-#pragma unroll
-        for (int j = 0; j < 32; j += 8) {
-          uint4 q;
-          __nv_bfloat162 h0 = __floats2bfloat162_rn(w[j], w[j + 1]);
-          __nv_bfloat162 h1 = __floats2bfloat162_rn(w[j + 2], w[j + 3]);
-          __nv_bfloat162 h2 = __floats2bfloat162_rn(w[j + 4], w[j + 5]);
-          __nv_bfloat162 h3 = __floats2bfloat162_rn(w[j + 6], w[j + 7]);
-          q.x = *reinterpret_cast<uint32_t*>(&h0);
-          q.y = *reinterpret_cast<uint32_t*>(&h1);
-          q.z = *reinterpret_cast<uint32_t*>(&h2);
-          q.w = *reinterpret_cast<uint32_t*>(&h3);
-          *reinterpret_cast<uint4*>(o + j) = q;
-        }
-      } else {
-        for (int j = 0; j < nvalid; ++j) o[j] = __float2bfloat16_rn(w[j]);
-      }
-    } else {
-      __half* o = static_cast<__half*>(dst) + base;
-      for (int j = 0; j < nvalid; ++j) o[j] = __float2half_rn(w[j]);
-    }
+    for (int j = 0; j < 32; ++j) v[j] = act_f(P.act, v[j]);
   }
+  store_row32(P.c, P.c_dtype, base, v, vec, nvalid);
 }
 
+constexpr int TC_THREADS = 384;  // warps 0-3: TMA, MMA, TMEM alloc, spare; 4-11: epilogue
+
 template <int BN>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(TC_THREADS, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               const TcParams P) {
   using C = TcCfg<BN>;
@@ -231,7 +252,7 @@ __global__ void __launch_bounds__(256, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], 128);
+      mbar_init(&tempty[s], TC_THREADS - 128);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -324,8 +345,11 @@ __global__ void __launch_bounds__(256, 1)
       }
     }
   } else if (warp >= 4) {
-    // ===================== epilogue =====================
-    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    // ===================== epilogue (8 warps) =====================
+    // warp w may only touch TMEM lanes 32*(w%4)..+31; the two warps sharing a
+    // lane quarter split the tile's 32-column chunks between them
+    const int q = warp & 3;
+    const int half = (warp - 4) >> 2;
     const int row = q * 32 + lane;
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -337,7 +361,7 @@ __global__ void __launch_bounds__(256, 1)
       tc_fence_after();
       const int64_t m = int64_t(mb) * TC_BM + row;
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
+      for (int c = half; c < BN / 32; c += 2) {
         uint32_t r[32];
         const uint32_t taddr = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * BN + c * 32);
         TMEM_LD32(taddr, r);
@@ -471,7 +495,7 @@ static void launch_bn(const GemmArgs& g, cudaStream_t s) {
   CUtensorMap tb = g.tb ? make_map(g.b, g.b.dtype, g.K, g.N, g.Z2, Z1, BN)
                         : make_map(g.b, g.b.dtype, g.N, g.K, g.Z2, Z1, 64);
   const int grid = int(P.num_tiles < kNumSMs ? P.num_tiles : kNumSMs);
-  k_gemm_tc<BN><<<grid, 256, C::SMEM, s>>>(ta, tb, P);
+  k_gemm_tc<BN><<<grid, TC_THREADS, C::SMEM, s>>>(ta, tb, P);
 }
 
 void launch_gemm_tc(const GemmArgs& g, cudaStream_t s) {

@@ -169,6 +169,62 @@ static void b_mean(Plan& p) { build_reduce(p, 1); }
 TCB_REGISTER("sum", b_sum);
 TCB_REGISTER("mean", b_mean);
 
+// Split-row column sums of x [R, C] (C % 8 == 0, 16-byte rows): block (cx, cy)
+// covers 256 columns x CS_ROWS rows; each lane owns 8 adjacent columns (one
+// 16-byte load per row), the 8 warps interleave rows, smem folds the warps and
+// the block writes one partial row; k_colsum_final adds the partials in chunk
+// order.  Deterministic; fills the machine at any R.
+constexpr int CS_ROWS = 128;
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_colsum_partial(const T* __restrict__ x, float* __restrict__ part,
+                                                        int64_t R, int64_t C) {
+  __shared__ float red[8][256 + 4];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t c0 = int64_t(blockIdx.x) * 256 + lane * 8;
+  const int64_t r0 = int64_t(blockIdx.y) * CS_ROWS;
+  const int64_t r1 = r0 + CS_ROWS < R ? r0 + CS_ROWS : R;
+  float acc[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) acc[k] = 0.0f;
+  if (c0 < C) {
+    for (int64_t r = r0 + warp; r < r1; r += 8) {
+      float f[8];
+      if constexpr (sizeof(T) == 2) {
+        uint4 q = *reinterpret_cast<const uint4*>(x + r * C + c0);
+        const T* h = reinterpret_cast<const T*>(&q);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) f[k] = to_f(h[k]);
+      } else {
+        float4 a = *reinterpret_cast<const float4*>(x + r * C + c0);
+        float4 b = *reinterpret_cast<const float4*>(x + r * C + c0 + 4);
+        f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w; f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) acc[k] += f[k];
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 8; ++k) red[warp][lane * 8 + k] = acc[k];
+  __syncthreads();
+  const int64_t c = int64_t(blockIdx.x) * 256 + threadIdx.x;
+  if (c < C) {
+    float s = 0.0f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) s += red[w][threadIdx.x];
+    part[int64_t(blockIdx.y) * C + c] = s;
+  }
+}
+
+__global__ void k_colsum_final(const float* __restrict__ part, float* __restrict__ out, int64_t nchunk, int64_t C,
+                               float scale) {
+  const int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (c >= C) return;
+  float s = 0.0f;
+  for (int64_t k = 0; k < nchunk; ++k) s += part[k * C + c];
+  out[c] = s * scale;
+}
+
 // colsum: f32 column sums over all leading dims (bias gradients of [T, N]
 // GEMM outputs); exact row order for f32 input, split-row tree otherwise.
 static void b_colsum(Plan& p) {
@@ -191,6 +247,17 @@ static void b_colsum(Plan& p) {
       p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
         k_reduce_exact<T, float><<<unsigned((C + 127) / 128), 128, 0, s>>>((const T*)in[0].ptr,
                                                                            (float*)out[0].ptr, C, g, 0);
+      };
+    } else if (C % 8 == 0) {
+      const int64_t nchunk = (R + CS_ROWS - 1) / CS_ROWS;
+      auto ws = std::make_shared<Scratch>(size_t(nchunk) * C * 4);
+      p.nkernels = 2;
+      p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
+        if (reinterpret_cast<uintptr_t>(in[0].ptr) % 16) fail(TCB_ERR_ARG, "colsum: input not 16-byte aligned");
+        dim3 grid(unsigned((C + 255) / 256), unsigned(nchunk));
+        k_colsum_partial<T><<<grid, 256, 0, s>>>((const T*)in[0].ptr, (float*)ws->p, R, C);
+        k_colsum_final<<<unsigned((C + 255) / 256), 256, 0, s>>>((const float*)ws->p, (float*)out[0].ptr, nchunk, C,
+                                                                  1.0f);
       };
     } else {
       p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {

@@ -23,15 +23,6 @@ __device__ __forceinline__ float warp_max(float v) {
   return v;
 }
 
-// Plan-owned device scratch (allocated once at plan creation, freed with the
-// plan). Launches of one plan are stream-ordered, so reuse is race-free.
-struct Scratch {
-  void* p = nullptr;
-  explicit Scratch(size_t bytes) { TCB_CUDA(cudaMalloc(&p, bytes ? bytes : 16)); }
-  ~Scratch() {
-    if (p) cudaFree(p);
-  }
-};
 
 // 8 consecutive elements <-> floats
 template <typename T>
@@ -732,21 +723,33 @@ __global__ void k_embed_rank(const int32_t* __restrict__ ids, int32_t* __restric
   sorted[rank] = int32_t(t);
 }
 
+// block (pos, column tile): if sorted position `pos` starts a segment of equal
+// ids, each thread accumulates one column over the whole segment in ascending t
+// (loads batched 4 deep; the adds keep the oracle's order).  Column-parallel,
+// so one id covering every token (token-type ids) is 256x wider than a warp.
 template <typename TD>
-__global__ void k_embed_accum(const int32_t* __restrict__ ids, const int32_t* __restrict__ sorted,
-                              const TD* __restrict__ dy, float* __restrict__ out, int64_t T, int64_t H) {
-  const int64_t pos = blockIdx.x * int64_t(blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (pos >= T) return;
+__global__ void __launch_bounds__(256) k_embed_accum(const int32_t* __restrict__ ids,
+                                                     const int32_t* __restrict__ sorted,
+                                                     const TD* __restrict__ dy, float* __restrict__ out,
+                                                     int64_t T, int64_t H) {
+  const int64_t pos = blockIdx.x;
   const int32_t id = ids[sorted[pos]];
   if (pos > 0 && ids[sorted[pos - 1]] == id) return;  // not a segment head
   int64_t end = pos + 1;
   while (end < T && ids[sorted[end]] == id) ++end;
-  for (int64_t j = lane; j < H; j += 32) {
-    float acc = out[int64_t(id) * H + j];
-    for (int64_t q = pos; q < end; ++q) acc = __fadd_rn(acc, to_f(dy[int64_t(sorted[q]) * H + j]));
-    out[int64_t(id) * H + j] = acc;
+  const int64_t j = int64_t(blockIdx.y) * blockDim.x + threadIdx.x;
+  if (j >= H) return;
+  float acc = out[int64_t(id) * H + j];
+  int64_t q = pos;
+  for (; q + 4 <= end; q += 4) {
+    float v0 = to_f(dy[int64_t(sorted[q]) * H + j]);
+    float v1 = to_f(dy[int64_t(sorted[q + 1]) * H + j]);
+    float v2 = to_f(dy[int64_t(sorted[q + 2]) * H + j]);
+    float v3 = to_f(dy[int64_t(sorted[q + 3]) * H + j]);
+    acc = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(acc, v0), v1), v2), v3);
   }
+  for (; q < end; ++q) acc = __fadd_rn(acc, to_f(dy[int64_t(sorted[q]) * H + j]));
+  out[int64_t(id) * H + j] = acc;
 }
 
 static void b_embedding_dx(Plan& p) {
@@ -769,7 +772,7 @@ static void b_embedding_dx(Plan& p) {
         TCB_CUDA(cudaMemsetAsync(out[0].ptr, 0, nb, s));
       }
       k_embed_rank<<<unsigned((T + 255) / 256), 256, 0, s>>>((const int32_t*)in[0].ptr, (int32_t*)sorted->p, T);
-      k_embed_accum<TD><<<unsigned((T + 7) / 8), 256, 0, s>>>((const int32_t*)in[0].ptr, (const int32_t*)sorted->p,
+      k_embed_accum<TD><<<dim3(unsigned(T), unsigned((H + 255) / 256)), 256, 0, s>>>((const int32_t*)in[0].ptr, (const int32_t*)sorted->p,
                                                               (const TD*)in[1].ptr, (float*)out[0].ptr, T, H);
     };
   });

@@ -116,6 +116,24 @@ def test_reduction_bf16_fast_path():
     assert rel_err(g[0], o[0]) < 1e-5
 
 
+@pytest.mark.parametrize("shape", [(4096, 768), (300, 2304), (77, 40)])
+def test_colsum(shape):
+    x = rn(*shape)
+    g, o = run_both("colsum", [(x, BF16)], [((shape[1],), F32)])
+    assert rel_err(g[0], o[0]) < 1e-5
+    g, o = run_both("colsum", [(x, F32)], [((shape[1],), F32)])
+    assert bits_equal(g[0], o[0])  # f32: exact row order
+
+
+def test_embedding_dx_single_long_segment():
+    """token-type ids: every token hits row 0 (one 4096-long segment)"""
+    T, H = 4096, 768
+    ids = np.zeros(T, np.int32)
+    dy = rn(T, H)
+    g, o = run_both("embedding_dx", [(ids, I32), (dy, BF16)], [((2, H), F32)], {"rows": 2})
+    assert bits_equal(g[0], o[0])
+
+
 def test_mse_exact():
     g, o = run_both("mse", [(rn(64, 10), F32), (rn(64, 10), F32)], [((1,), F32)])
     assert bits_equal(g[0], o[0])

@@ -1,0 +1,63 @@
+#!/usr/bin/env python3
+"""Time the b200 GEMM (linear / matmul_t) at the BERT-base shapes with CUDA
+events; used for ncu captures (`ncu -k regex:k_gemm_tc ... python
+tools/probe_gemm.py --only N`)."""
+import argparse
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+from paper_2303_04759_b200.abi import BF16, F32  # noqa: E402
+from paper_2303_04759_b200.runtime import Plan  # noqa: E402
+
+T = 4096
+# (name, op, M, K, N, ta, tb, out)
+SHAPES = [
+    ("qkv_fwd", "matmul_t", T, 768, 2304, 0, 0, BF16),
+    ("proj_fwd", "matmul_t", T, 768, 768, 0, 0, BF16),
+    ("ffn1_fwd", "matmul_t", T, 768, 3072, 0, 0, BF16),
+    ("ffn2_fwd", "matmul_t", T, 3072, 768, 0, 0, BF16),
+    ("ffn1_dgrad", "matmul_t", T, 3072, 768, 0, 1, BF16),
+    ("ffn1_wgrad", "matmul_t", 768, T, 3072, 1, 0, F32),
+    ("decoder_fwd", "matmul_t", T, 768, 30528, 0, 1, BF16),
+    ("big_sq", "matmul_t", 8192, 8192, 8192, 0, 1, BF16),
+]
+
+
+def run(name, op, M, K, N, ta, tb, out, iters):
+    a = torch.randn(K, M, device="cuda") if ta else torch.randn(M, K, device="cuda")
+    b = torch.randn(N, K, device="cuda") if tb else torch.randn(K, N, device="cuda")
+    a, b = a.to(torch.bfloat16).contiguous(), b.to(torch.bfloat16).contiguous()
+    c = torch.empty(M, N, device="cuda", dtype=torch.float32 if out == F32 else torch.bfloat16)
+    plan = Plan(op, [(tuple(a.shape), BF16), (tuple(b.shape), BF16)], [((M, N), out)], {"ta": ta, "tb": tb})
+    s = torch.cuda.current_stream().cuda_stream
+    for _ in range(3):
+        plan.launch([a.data_ptr(), b.data_ptr()], [c.data_ptr()], s)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(iters):
+        plan.launch([a.data_ptr(), b.data_ptr()], [c.data_ptr()], s)
+    e1.record()
+    torch.cuda.synchronize()
+    us = e0.elapsed_time(e1) * 1000 / iters
+    tf = 2.0 * M * N * K / (us * 1e-6) / 1e12
+    return {"name": name, "M": M, "K": K, "N": N, "ta": ta, "tb": tb, "us": round(us, 2), "tflops": round(tf, 1)}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--only", type=int, default=-1)
+    ap.add_argument("--iters", type=int, default=20)
+    args = ap.parse_args()
+    shapes = SHAPES if args.only < 0 else [SHAPES[args.only]]
+    for sh in shapes:
+        print(json.dumps(run(*sh, iters=args.iters)), flush=True)
+
+
+if __name__ == "__main__":
+    main()
