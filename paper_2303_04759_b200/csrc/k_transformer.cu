@@ -103,6 +103,22 @@ __device__ __forceinline__ void st8(T* p, int64_t i, int64_t n, bool vec, const 
 
 constexpr int LN_MAXC = 8;  // up to 8 chunks of 8 per lane: H <= 2048
 
+// calls f(std::integral_constant<int, NC>) with NC = ceil(H / 256)
+template <typename Fn>
+static void dispatch_nc(int H, Fn&& f) {
+  switch ((H + 255) / 256) {
+    case 1: f(std::integral_constant<int, 1>{}); return;
+    case 2: f(std::integral_constant<int, 2>{}); return;
+    case 3: f(std::integral_constant<int, 3>{}); return;
+    case 4: f(std::integral_constant<int, 4>{}); return;
+    case 5: f(std::integral_constant<int, 5>{}); return;
+    case 6: f(std::integral_constant<int, 6>{}); return;
+    case 7: f(std::integral_constant<int, 7>{}); return;
+    case 8: f(std::integral_constant<int, 8>{}); return;
+  }
+  fail(TCB_ERR_UNIMPLEMENTED, "layer norm: hidden size > 2048 unsupported");
+}
+
 // keep bits for elements i .. i+7 (two Philox calls when i is 4-aligned)
 __device__ __forceinline__ uint32_t drop_bits8(const DropCfg& d, uint64_t i) {
   if (d.p <= 0.0f) return 0xFFu;
@@ -114,7 +130,9 @@ __device__ __forceinline__ uint32_t drop_bits8(const DropCfg& d, uint64_t i) {
 
 // ------------------------------------------------------------ layer norm fwd
 // y = LN(s) where s = x (layer_norm) or s = round(dropout(x) + r) (add_layer_norm)
-template <typename T>
+// NC: 8-element chunks per lane (H <= 256*NC), so the row stays in registers
+// with no dead predicated slots.
+template <typename T, int NC>
 __global__ void __launch_bounds__(256) k_ln_fwd(const T* __restrict__ x, const T* __restrict__ r,
                                                 const float* __restrict__ gamma_f,
                                                 const T* __restrict__ gamma_t, const float* __restrict__ beta_f,
@@ -126,10 +144,10 @@ __global__ void __launch_bounds__(256) k_ln_fwd(const T* __restrict__ x, const T
   const int64_t row = blockIdx.x * int64_t(blockDim.x >> 5) + (threadIdx.x >> 5);
   if (row >= rows) return;
   const int nch = (H + 7) / 8;
-  float v[LN_MAXC][8];
+  float v[NC][8];
   float sum = 0.0f;
 #pragma unroll
-  for (int c = 0; c < LN_MAXC; ++c) {
+  for (int c = 0; c < NC; ++c) {
     const int ch = lane + c * 32;
     if (ch < nch) {
       const int64_t i = row * H + ch * 8;
@@ -154,7 +172,7 @@ __global__ void __launch_bounds__(256) k_ln_fwd(const T* __restrict__ x, const T
   const float mean = warp_sum(sum) * inv;
   float sq = 0.0f;
 #pragma unroll
-  for (int c = 0; c < LN_MAXC; ++c) {
+  for (int c = 0; c < NC; ++c) {
     const int ch = lane + c * 32;
     if (ch < nch) {
 #pragma unroll
@@ -171,7 +189,7 @@ __global__ void __launch_bounds__(256) k_ln_fwd(const T* __restrict__ x, const T
     rstd_o[row] = rstd;
   }
 #pragma unroll
-  for (int c = 0; c < LN_MAXC; ++c) {
+  for (int c = 0; c < NC; ++c) {
     const int ch = lane + c * 32;
     if (ch < nch) {
       float o[8];
@@ -205,20 +223,23 @@ static void build_ln_fwd(Plan& p, bool residual) {
   const float eps = float(p.attrs.f("eps", 1e-12));
   const DropCfg d = drop_cfg(p.attrs);
   dispatch_float(X.dtype, [&](auto* tp) {
-    using T = std::remove_pointer_t<decltype(tp)>;
+   using T = std::remove_pointer_t<decltype(tp)>;
+   dispatch_nc(H, [&](auto nc) {
+    constexpr int NC = decltype(nc)::value;
     p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
       const int gi = residual ? 2 : 1;
       bool vec = (H % 8 == 0);
       for (int i = 0; i < (residual ? 2 : 1); ++i) vec = vec && reinterpret_cast<uintptr_t>(in[i].ptr) % 16 == 0;
       vec = vec && reinterpret_cast<uintptr_t>(out[0].ptr) % 16 == 0;
       if (residual) vec = vec && reinterpret_cast<uintptr_t>(out[1].ptr) % 16 == 0;
-      k_ln_fwd<T><<<unsigned((rows + 7) / 8), 256, 0, s>>>(
+      k_ln_fwd<T, NC><<<unsigned((rows + 7) / 8), 256, 0, s>>>(
           (const T*)in[0].ptr, residual ? (const T*)in[1].ptr : nullptr,
           gf ? (const float*)in[gi].ptr : nullptr, gf ? nullptr : (const T*)in[gi].ptr,
           gf ? (const float*)in[gi + 1].ptr : nullptr, gf ? nullptr : (const T*)in[gi + 1].ptr,
           (T*)out[0].ptr, residual ? (T*)out[1].ptr : nullptr, (float*)out[residual ? 2 : 1].ptr,
           (float*)out[residual ? 3 : 2].ptr, rows, H, eps, d, vec);
     };
+   });
   });
 }
 static void b_layer_norm(Plan& p) { build_ln_fwd(p, false); }
@@ -230,9 +251,9 @@ TCB_REGISTER("add_layer_norm", b_add_layer_norm);
 // dy += dy2 (fused fan-out accumulation); ds = rstd*(g - mean(g) - xh*mean(g*xh));
 // dx = dropout(ds);
 // per-CTA partial column sums of dy*xh and dy -> ws, then k_colsum finalises.
-constexpr int LNB_ROWS = 32;  // rows per CTA (8 warps x 4 rows)
+constexpr int LNB_ROWS = 16;  // rows per CTA (8 warps x 2 rows)
 
-template <typename T>
+template <typename T, int NC>
 __global__ void __launch_bounds__(256) k_ln_bwd(const T* __restrict__ sx, const float* __restrict__ gamma_f,
                                                 const T* __restrict__ gamma_t, const float* __restrict__ mean,
                                                 const float* __restrict__ rstd, const T* __restrict__ dy,
@@ -241,9 +262,9 @@ __global__ void __launch_bounds__(256) k_ln_bwd(const T* __restrict__ sx, const 
                                                 int H, DropCfg d, bool vec) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nch = (H + 7) / 8;
-  float pg[LN_MAXC][8], pb[LN_MAXC][8];
+  float pg[NC][8], pb[NC][8];
 #pragma unroll
-  for (int c = 0; c < LN_MAXC; ++c)
+  for (int c = 0; c < NC; ++c)
 #pragma unroll
     for (int k = 0; k < 8; ++k) pg[c][k] = pb[c][k] = 0.0f;
   const float inv = 1.0f / float(H);
@@ -251,10 +272,10 @@ __global__ void __launch_bounds__(256) k_ln_bwd(const T* __restrict__ sx, const 
     const int64_t row = int64_t(blockIdx.x) * LNB_ROWS + warp * (LNB_ROWS / 8) + rr;
     if (row >= rows) break;
     const float mu = mean[row], rs = rstd[row];
-    float xh[LN_MAXC][8], g[LN_MAXC][8];
+    float xh[NC][8], g[NC][8];
     float c1 = 0.0f, c2 = 0.0f;
 #pragma unroll
-    for (int c = 0; c < LN_MAXC; ++c) {
+    for (int c = 0; c < NC; ++c) {
       const int ch = lane + c * 32;
       if (ch < nch) {
         const int64_t i = row * H + ch * 8;
@@ -287,7 +308,7 @@ __global__ void __launch_bounds__(256) k_ln_bwd(const T* __restrict__ sx, const 
     c1 = warp_sum(c1) * inv;
     c2 = warp_sum(c2) * inv;
 #pragma unroll
-    for (int c = 0; c < LN_MAXC; ++c) {
+    for (int c = 0; c < NC; ++c) {
       const int ch = lane + c * 32;
       if (ch < nch) {
         const int64_t i = row * H + ch * 8;
@@ -307,7 +328,7 @@ __global__ void __launch_bounds__(256) k_ln_bwd(const T* __restrict__ sx, const 
   // CTA partials: smem reduce over the 8 warps, then one row of ws per CTA
   extern __shared__ float red[];  // [8][2][H]
 #pragma unroll
-  for (int c = 0; c < LN_MAXC; ++c) {
+  for (int c = 0; c < NC; ++c) {
     const int ch = lane + c * 32;
     if (ch < nch) {
 #pragma unroll
@@ -332,18 +353,34 @@ __global__ void __launch_bounds__(256) k_ln_bwd(const T* __restrict__ sx, const 
   }
 }
 
-// sum the per-CTA partials in fixed order -> dgamma, dbeta (f32)
-__global__ void k_ln_colsum(const float* __restrict__ ws, float* __restrict__ dg, float* __restrict__ db,
-                            int nblk, int H) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= H) return;
+// sum the per-CTA partials in fixed order -> dgamma, dbeta (f32): block = 32
+// columns x 8 warps; warp w folds partial rows w, w+8, ...; smem combines.
+__global__ void __launch_bounds__(256) k_ln_colsum(const float* __restrict__ ws, float* __restrict__ dg,
+                                                   float* __restrict__ db, int nblk, int H) {
+  __shared__ float ra[8][33], rb[8][33];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int j = blockIdx.x * 32 + lane;
   float a = 0.0f, b = 0.0f;
-  for (int k = 0; k < nblk; ++k) {
-    a += ws[(int64_t(k) * 2 + 0) * H + j];
-    b += ws[(int64_t(k) * 2 + 1) * H + j];
+  if (j < H) {
+#pragma unroll 4
+    for (int k = warp; k < nblk; k += 8) {
+      a += ws[(int64_t(k) * 2 + 0) * H + j];
+      b += ws[(int64_t(k) * 2 + 1) * H + j];
+    }
   }
-  dg[j] = a;
-  db[j] = b;
+  ra[warp][lane] = a;
+  rb[warp][lane] = b;
+  __syncthreads();
+  if (warp == 0 && j < H) {
+    float sa = 0.0f, sb = 0.0f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+      sa += ra[w][lane];
+      sb += rb[w][lane];
+    }
+    dg[j] = sa;
+    db[j] = sb;
+  }
 }
 
 static void b_layer_norm_dx(Plan& p) {
@@ -361,10 +398,12 @@ static void b_layer_norm_dx(Plan& p) {
   const size_t smem = size_t(16) * H * sizeof(float);
   p.nkernels = 2;
   dispatch_float(S.dtype, [&](auto* tp) {
-    using T = std::remove_pointer_t<decltype(tp)>;
+   using T = std::remove_pointer_t<decltype(tp)>;
+   dispatch_nc(H, [&](auto nc) {
+    constexpr int NC = decltype(nc)::value;
     static std::once_flag once;
     std::call_once(once, [] {
-      TCB_CUDA(cudaFuncSetAttribute(k_ln_bwd<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * 2048 * 4));
+      TCB_CUDA(cudaFuncSetAttribute(k_ln_bwd<T, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * 2048 * 4));
     });
     p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
       bool vec = H % 8 == 0;
@@ -372,14 +411,15 @@ static void b_layer_norm_dx(Plan& p) {
       if (has_res) vec = vec && reinterpret_cast<uintptr_t>(in[5].ptr) % 16 == 0;
       vec = vec && reinterpret_cast<uintptr_t>(out[0].ptr) % 16 == 0;
       if (has_dx) vec = vec && reinterpret_cast<uintptr_t>(out[3].ptr) % 16 == 0;
-      k_ln_bwd<T><<<nblk, 256, smem, s>>>(
+      k_ln_bwd<T, NC><<<nblk, 256, smem, s>>>(
           (const T*)in[0].ptr, gf ? (const float*)in[1].ptr : nullptr, gf ? nullptr : (const T*)in[1].ptr,
           (const float*)in[2].ptr, (const float*)in[3].ptr, (const T*)in[4].ptr,
           has_res ? (const T*)in[5].ptr : nullptr, (T*)out[0].ptr, has_dx ? (T*)out[3].ptr : nullptr,
           (float*)ws->p, rows, H, d, vec);
-      k_ln_colsum<<<(H + 127) / 128, 128, 0, s>>>((const float*)ws->p, (float*)out[1].ptr,
-                                                  (float*)out[2].ptr, nblk, H);
+      k_ln_colsum<<<(H + 31) / 32, 256, 0, s>>>((const float*)ws->p, (float*)out[1].ptr,
+                                                (float*)out[2].ptr, nblk, H);
     };
+   });
   });
 }
 TCB_REGISTER("layer_norm_dx", b_layer_norm_dx);
@@ -389,79 +429,155 @@ TCB_REGISTER("layer_norm_dx", b_layer_norm_dx);
 // optional Pd = dropout(P) (index = row*C + col).  One warp per row.
 constexpr int SM_MAXV = 32;  // up to 32 values per lane: C <= 1024
 
-template <typename TI, typename TO>
+// 4 consecutive elements (vector access when the row is 4-element aligned)
+template <typename T>
+__device__ __forceinline__ void ld4(const T* p, int64_t i, int64_t lim, bool vec, float* f) {
+  if (vec) {
+    if constexpr (sizeof(T) == 4) {
+      float4 a = *reinterpret_cast<const float4*>(p + i);
+      f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w;
+    } else {
+      uint2 q = *reinterpret_cast<const uint2*>(p + i);
+      const T* h = reinterpret_cast<const T*>(&q);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) f[k] = to_f(h[k]);
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) f[k] = i + k < lim ? to_f(p[i + k]) : 0.0f;
+  }
+}
+template <typename T>
+__device__ __forceinline__ void st4(T* p, int64_t i, int64_t lim, bool vec, const float* f) {
+  if (vec) {
+    if constexpr (sizeof(T) == 4) {
+      *reinterpret_cast<float4*>(p + i) = make_float4(f[0], f[1], f[2], f[3]);
+    } else {
+      uint2 q;
+      T* h = reinterpret_cast<T*>(&q);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) h[k] = from_f<T>(f[k]);
+      *reinterpret_cast<uint2*>(p + i) = q;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (i + k < lim) p[i + k] = from_f<T>(f[k]);
+  }
+}
+
+// One warp per row; lane owns NQ quads of 4 adjacent columns (C <= 128*NQ),
+// so the row lives in registers and one Philox call covers a quad's 4 keep bits.
+template <typename TI, typename TO, int NQ>
 __global__ void __launch_bounds__(256) k_softmax(const TI* __restrict__ x, TO* __restrict__ P,
                                                  TO* __restrict__ Pd, int64_t rows, int C, int Sq,
-                                                 float scale, int causal, DropCfg d) {
+                                                 float scale, int causal, DropCfg d, bool vec) {
   const int lane = threadIdx.x & 31;
   const int64_t row = blockIdx.x * int64_t(blockDim.x >> 5) + (threadIdx.x >> 5);
   if (row >= rows) return;
   const int qi = int(row % Sq);
-  float v[SM_MAXV];
+  const int64_t base = row * C, lim = base + C;
+  float v[NQ][4];
   float m = -INFINITY;
 #pragma unroll
-  for (int c = 0; c < SM_MAXV; ++c) {
-    const int j = lane + c * 32;
-    float t = -INFINITY;
-    if (j < C) {
-      t = to_f(x[row * C + j]) * scale;
+  for (int c = 0; c < NQ; ++c) {
+    const int j0 = (c * 32 + lane) * 4;
+    if (j0 < C) ld4(x, base + j0, lim, vec, v[c]);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int j = j0 + k;
+      float t = (j < C) ? v[c][k] * scale : -INFINITY;
       if (causal && j > qi) t = -INFINITY;
+      v[c][k] = t;
+      m = fmaxf(m, t);
     }
-    v[c] = t;
-    m = fmaxf(m, t);
   }
   m = warp_max(m);
   float sum = 0.0f;
 #pragma unroll
-  for (int c = 0; c < SM_MAXV; ++c) {
-    const int j = lane + c * 32;
-    v[c] = j < C ? expf(v[c] - m) : 0.0f;
-    sum += v[c];
-  }
+  for (int c = 0; c < NQ; ++c)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      v[c][k] = v[c][k] == -INFINITY ? 0.0f : expf(v[c][k] - m);
+      sum += v[c][k];
+    }
   sum = warp_sum(sum);
 #pragma unroll
-  for (int c = 0; c < SM_MAXV; ++c) {
-    const int j = lane + c * 32;
-    if (j < C) {
-      TO pv = from_f<TO>(v[c] / sum);
-      P[row * C + j] = pv;
-      if (Pd) {
-        const uint64_t idx = uint64_t(row) * C + j;
-        Pd[row * C + j] = from_f<TO>(dropout_keep(d, idx) ? to_f(pv) * d.scale : 0.0f);
-      }
+  for (int c = 0; c < NQ; ++c) {
+    const int j0 = (c * 32 + lane) * 4;
+    if (j0 >= C) continue;
+    float o[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) o[k] = to_f(from_f<TO>(v[c][k] / sum));
+    st4(P, base + j0, lim, vec, o);
+    if (Pd) {
+      const uint64_t i0 = uint64_t(base + j0);
+      const uint32_t bits = d.p <= 0.0f ? 0xFu
+                            : (i0 & 3) == 0 ? dropout_bits4(d, i0 >> 2)
+                                            : (uint32_t(dropout_keep(d, i0)) | uint32_t(dropout_keep(d, i0 + 1)) << 1 |
+                                               uint32_t(dropout_keep(d, i0 + 2)) << 2 | uint32_t(dropout_keep(d, i0 + 3)) << 3);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) o[k] = ((bits >> k) & 1u) ? o[k] * d.scale : 0.0f;
+      st4(Pd, base + j0, lim, vec, o);
     }
   }
 }
 
 // dS = P * (dP - rowdot(P, dP)) * scale with dP = dropout(dPd); optional Pd out
-template <typename TP, typename TG, typename TO>
+template <typename TP, typename TG, typename TO, int NQ>
 __global__ void __launch_bounds__(256) k_softmax_bwd(const TP* __restrict__ P, const TG* __restrict__ dPd,
                                                      TO* __restrict__ dS, TO* __restrict__ Pd_o, int64_t rows,
-                                                     int C, float scale, DropCfg d) {
+                                                     int C, float scale, DropCfg d, bool vec) {
   const int lane = threadIdx.x & 31;
   const int64_t row = blockIdx.x * int64_t(blockDim.x >> 5) + (threadIdx.x >> 5);
   if (row >= rows) return;
-  float pv[SM_MAXV], dp[SM_MAXV];
+  const int64_t base = row * C, lim = base + C;
+  float pv[NQ][4], dp[NQ][4];
   float dot = 0.0f;
 #pragma unroll
-  for (int c = 0; c < SM_MAXV; ++c) {
-    const int j = lane + c * 32;
-    pv[c] = dp[c] = 0.0f;
-    if (j < C) {
-      const uint64_t idx = uint64_t(row) * C + j;
-      const bool keep = dropout_keep(d, idx);
-      pv[c] = to_f(P[row * C + j]);
-      dp[c] = keep ? to_f(dPd[row * C + j]) * d.scale : 0.0f;
-      if (Pd_o) Pd_o[row * C + j] = from_f<TO>(keep ? pv[c] * d.scale : 0.0f);
-      dot += pv[c] * dp[c];
+  for (int c = 0; c < NQ; ++c) {
+    const int j0 = (c * 32 + lane) * 4;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) pv[c][k] = dp[c][k] = 0.0f;
+    if (j0 >= C) continue;
+    ld4(P, base + j0, lim, vec, pv[c]);
+    ld4(dPd, base + j0, lim, vec, dp[c]);
+    const uint64_t i0 = uint64_t(base + j0);
+    const uint32_t bits = d.p <= 0.0f ? 0xFu
+                          : (i0 & 3) == 0 ? dropout_bits4(d, i0 >> 2)
+                                          : (uint32_t(dropout_keep(d, i0)) | uint32_t(dropout_keep(d, i0 + 1)) << 1 |
+                                             uint32_t(dropout_keep(d, i0 + 2)) << 2 | uint32_t(dropout_keep(d, i0 + 3)) << 3);
+    float pdv[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const bool keep = (bits >> k) & 1u;
+      dp[c][k] = keep ? dp[c][k] * d.scale : 0.0f;
+      pdv[k] = keep ? pv[c][k] * d.scale : 0.0f;
+      dot += pv[c][k] * dp[c][k];
     }
+    if (Pd_o) st4(Pd_o, base + j0, lim, vec, pdv);
   }
   dot = warp_sum(dot);
 #pragma unroll
-  for (int c = 0; c < SM_MAXV; ++c) {
-    const int j = lane + c * 32;
-    if (j < C) dS[row * C + j] = from_f<TO>(pv[c] * (dp[c] - dot) * scale);
+  for (int c = 0; c < NQ; ++c) {
+    const int j0 = (c * 32 + lane) * 4;
+    if (j0 >= C) continue;
+    float o[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) o[k] = pv[c][k] * (dp[c][k] - dot) * scale;
+    st4(dS, base + j0, lim, vec, o);
   }
+}
+
+// NQ = ceil(C / 128) in {1, 2, 4, 8}
+template <typename Fn>
+static void dispatch_nq(int C, Fn&& f) {
+  const int nq = (C + 127) / 128;
+  if (nq <= 1) f(std::integral_constant<int, 1>{});
+  else if (nq <= 2) f(std::integral_constant<int, 2>{});
+  else if (nq <= 4) f(std::integral_constant<int, 4>{});
+  else if (nq <= 8) f(std::integral_constant<int, 8>{});
+  else fail(TCB_ERR_UNIMPLEMENTED, "softmax: row length > 1024 unsupported");
 }
 
 template <typename Fn>
@@ -480,13 +596,19 @@ static void b_softmax(Plan& p) {
   const int causal = int(p.attrs.i("causal", 0));
   const DropCfg d = drop_cfg(p.attrs);
   dispatch2(X.dtype, p.out[0].dtype, [&](auto* pa, auto* pb) {
-    using TI = std::remove_pointer_t<decltype(pa)>;
-    using TO = std::remove_pointer_t<decltype(pb)>;
+   using TI = std::remove_pointer_t<decltype(pa)>;
+   using TO = std::remove_pointer_t<decltype(pb)>;
+   dispatch_nq(C, [&](auto nq) {
+    constexpr int NQ = decltype(nq)::value;
     const bool pd = p.out.size() > 1;
     p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
-      k_softmax<TI, TO><<<unsigned((rows + 7) / 8), 256, 0, s>>>(
-          (const TI*)in[0].ptr, (TO*)out[0].ptr, pd ? (TO*)out[1].ptr : nullptr, rows, C, Sq, scale, causal, d);
+      const bool vec = C % 4 == 0 && reinterpret_cast<uintptr_t>(in[0].ptr) % 16 == 0 &&
+                       reinterpret_cast<uintptr_t>(out[0].ptr) % 16 == 0 &&
+                       (!pd || reinterpret_cast<uintptr_t>(out[1].ptr) % 16 == 0);
+      k_softmax<TI, TO, NQ><<<unsigned((rows + 7) / 8), 256, 0, s>>>(
+          (const TI*)in[0].ptr, (TO*)out[0].ptr, pd ? (TO*)out[1].ptr : nullptr, rows, C, Sq, scale, causal, d, vec);
     };
+   });
   });
 }
 TCB_REGISTER("softmax", b_softmax);
@@ -504,11 +626,17 @@ static void b_softmax_dx(Plan& p) {
     using TP = std::remove_pointer_t<decltype(pa)>;
     using TO = std::remove_pointer_t<decltype(pb)>;
     dispatch_float(dg, [&](auto* pg) {
-      using TG = std::remove_pointer_t<decltype(pg)>;
+     using TG = std::remove_pointer_t<decltype(pg)>;
+     dispatch_nq(C, [&](auto nq) {
+      constexpr int NQ = decltype(nq)::value;
       p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
-        k_softmax_bwd<TP, TG, TO><<<unsigned((rows + 7) / 8), 256, 0, s>>>(
-            (const TP*)in[0].ptr, (const TG*)in[1].ptr, (TO*)out[0].ptr, nullptr, rows, C, scale, d);
+        const bool vec = C % 4 == 0 && reinterpret_cast<uintptr_t>(in[0].ptr) % 16 == 0 &&
+                         reinterpret_cast<uintptr_t>(in[1].ptr) % 16 == 0 &&
+                         reinterpret_cast<uintptr_t>(out[0].ptr) % 16 == 0;
+        k_softmax_bwd<TP, TG, TO, NQ><<<unsigned((rows + 7) / 8), 256, 0, s>>>(
+            (const TP*)in[0].ptr, (const TG*)in[1].ptr, (TO*)out[0].ptr, nullptr, rows, C, scale, d, vec);
       };
+     });
     });
   });
 }
@@ -619,8 +747,11 @@ static void b_attention(Plan& p) {
       // 2. P = softmax(scores) (+ dropout copy)
       const int64_t rows = g.Z * g.S;
       T* Pd = g.d.p > 0.0f ? (T*)pd->p : nullptr;
-      k_softmax<float, T><<<unsigned((rows + 7) / 8), 256, 0, s>>>(
-          (const float*)scores->p, (T*)out[1].ptr, Pd, rows, int(g.S), int(g.S), 1.0f, g.causal, g.d);
+      dispatch_nq(int(g.S), [&](auto nq) {
+        k_softmax<float, T, decltype(nq)::value><<<unsigned((rows + 7) / 8), 256, 0, s>>>(
+            (const float*)scores->p, (T*)out[1].ptr, Pd, rows, int(g.S), int(g.S), 1.0f, g.causal, g.d,
+            g.S % 4 == 0 && reinterpret_cast<uintptr_t>(out[1].ptr) % 16 == 0);
+      });
       // 3. ctx = Pd V
       GemmArgs c = attn_gemm(g, g.S, g.dh, g.S, sq_view(g, Pd ? (const void*)Pd : out[1].ptr, g.dt), 0,
                              qkv_view(g, in[0].ptr, 2), 0);
@@ -652,8 +783,11 @@ static void b_attention_dx(Plan& p) {
       // 2. dS = P (dP - rowdot) * scale ; Pd
       const int64_t rows = g.Z * g.S;
       T* Pd = g.d.p > 0.0f ? (T*)pd->p : nullptr;
-      k_softmax_bwd<T, float, T><<<unsigned((rows + 7) / 8), 256, 0, s>>>(
-          (const T*)in[1].ptr, (const float*)dpd->p, (T*)ds->p, Pd, rows, int(g.S), g.scale, g.d);
+      dispatch_nq(int(g.S), [&](auto nq) {
+        k_softmax_bwd<T, float, T, decltype(nq)::value><<<unsigned((rows + 7) / 8), 256, 0, s>>>(
+            (const T*)in[1].ptr, (const float*)dpd->p, (T*)ds->p, Pd, rows, int(g.S), g.scale, g.d,
+            g.S % 4 == 0 && reinterpret_cast<uintptr_t>(in[1].ptr) % 16 == 0);
+      });
       char* dq = static_cast<char*>(out[0].ptr);
       const size_t part = size_t(g.H) * dtype_bytes(g.dt);
       // 3. dQ = dS K
@@ -711,16 +845,30 @@ TCB_REGISTER("embedding", b_embedding);
 // Deterministic scatter-add: stable rank of (id, t) pairs, then one warp per
 // distinct id accumulates its rows in ascending t onto base -- the oracle's
 // order exactly, so f32 results are bit-identical.
-__global__ void k_embed_rank(const int32_t* __restrict__ ids, int32_t* __restrict__ sorted, int64_t T) {
+// Stable counting rank of token t among all T ids (ids staged through smem in
+// tiles); the first occurrence of each id also records its segment length at
+// the segment's head position (seg_len is zeroed beforehand).
+__global__ void __launch_bounds__(64) k_embed_rank(const int32_t* __restrict__ ids, int32_t* __restrict__ sorted,
+                                                   int32_t* __restrict__ seg_len, int64_t T) {
+  __shared__ int32_t tile[2048];
   const int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-  if (t >= T) return;
-  const int32_t my = ids[t];
-  int64_t rank = 0;
-  for (int64_t u = 0; u < T; ++u) {
-    const int32_t o = ids[u];
-    rank += (o < my) || (o == my && u < t);
+  const int32_t my = t < T ? ids[t] : 0;
+  int64_t less = 0, eq_before = 0, eq = 0;
+  for (int64_t u0 = 0; u0 < T; u0 += 2048) {
+    const int64_t n = T - u0 < 2048 ? T - u0 : 2048;
+    __syncthreads();
+    for (int64_t k = threadIdx.x; k < n; k += blockDim.x) tile[k] = ids[u0 + k];
+    __syncthreads();
+    for (int64_t k = 0; k < n; ++k) {
+      const int32_t o = tile[k];
+      less += o < my;
+      eq += o == my;
+      eq_before += (o == my) & (u0 + k < t);
+    }
   }
-  sorted[rank] = int32_t(t);
+  if (t >= T) return;
+  sorted[less + eq_before] = int32_t(t);
+  if (eq_before == 0) seg_len[less] = int32_t(eq);
 }
 
 // block (pos, column tile): if sorted position `pos` starts a segment of equal
@@ -730,13 +878,14 @@ __global__ void k_embed_rank(const int32_t* __restrict__ ids, int32_t* __restric
 template <typename TD>
 __global__ void __launch_bounds__(256) k_embed_accum(const int32_t* __restrict__ ids,
                                                      const int32_t* __restrict__ sorted,
+                                                     const int32_t* __restrict__ seg_len,
                                                      const TD* __restrict__ dy, float* __restrict__ out,
                                                      int64_t T, int64_t H) {
   const int64_t pos = blockIdx.x;
+  const int32_t len = seg_len[pos];
+  if (len == 0) return;  // not a segment head
   const int32_t id = ids[sorted[pos]];
-  if (pos > 0 && ids[sorted[pos - 1]] == id) return;  // not a segment head
-  int64_t end = pos + 1;
-  while (end < T && ids[sorted[end]] == id) ++end;
+  const int64_t end = pos + len;
   const int64_t j = int64_t(blockIdx.y) * blockDim.x + threadIdx.x;
   if (j >= H) return;
   float acc = out[int64_t(id) * H + j];
@@ -760,7 +909,7 @@ static void b_embedding_dx(Plan& p) {
   require(p.in[1].numel() == T * H, "embedding_dx: dy must be [T, H]");
   const bool has_base = p.in.size() > 2;
   if (has_base) require(p.in[2].dtype == TCB_F32 && p.in[2].numel() == V * H, "embedding_dx: base is f32 [V,H]");
-  auto sorted = std::make_shared<Scratch>(size_t(T) * 4);
+  auto sorted = std::make_shared<Scratch>(size_t(T) * 8);  // sorted[T] ++ seg_len[T]
   p.nkernels = 3;
   dispatch_float(p.in[1].dtype, [&](auto* tp) {
     using TD = std::remove_pointer_t<decltype(tp)>;
@@ -771,9 +920,12 @@ static void b_embedding_dx(Plan& p) {
       } else {
         TCB_CUDA(cudaMemsetAsync(out[0].ptr, 0, nb, s));
       }
-      k_embed_rank<<<unsigned((T + 255) / 256), 256, 0, s>>>((const int32_t*)in[0].ptr, (int32_t*)sorted->p, T);
-      k_embed_accum<TD><<<dim3(unsigned(T), unsigned((H + 255) / 256)), 256, 0, s>>>((const int32_t*)in[0].ptr, (const int32_t*)sorted->p,
-                                                              (const TD*)in[1].ptr, (float*)out[0].ptr, T, H);
+      int32_t* srt = (int32_t*)sorted->p;
+      int32_t* seg = srt + T;
+      TCB_CUDA(cudaMemsetAsync(seg, 0, size_t(T) * 4, s));
+      k_embed_rank<<<unsigned((T + 63) / 64), 64, 0, s>>>((const int32_t*)in[0].ptr, srt, seg, T);
+      k_embed_accum<TD><<<dim3(unsigned(T), unsigned((H + 255) / 256)), 256, 0, s>>>(
+          (const int32_t*)in[0].ptr, srt, seg, (const TD*)in[1].ptr, (float*)out[0].ptr, T, H);
     };
   });
 }

@@ -60,6 +60,7 @@ inline bool inplace_safe(const std::string& base, int in_idx, int out_idx) {
     return (out_idx == 0 && in_idx == 0) || (out_idx == 1 && in_idx == 2) || (out_idx == 2 && in_idx == 3);
   if (base == "sgd_update") return in_idx == 0 && out_idx == 0;
   if (base == "add_scalar") return in_idx == 0 && out_idx == 0;
+  if (base == "embedding_dx") return in_idx == 2 && out_idx == 0;  // base + scatter
   return false;
 }
 
@@ -140,12 +141,20 @@ inline Layout build_layout(const ir::FunctionIR& fn, const std::vector<std::pair
     return L.refs[pv][0].unit;
   };
 
+  // number of vars referring to each unit (aliases block plain in-place reuse)
+  std::vector<int> unit_refs(L.units.size(), 1);
+  auto note = [&](int u) {
+    if (int(unit_refs.size()) <= u) unit_refs.resize(u + 1, 0);
+    unit_refs[u]++;
+  };
+
   for (int i = 0; i < L.n; ++i) {
     const auto& b = seq.lets[i];
     const auto& e = b.value;
     auto arg_refs = [&](size_t k) -> const std::vector<Ref>& { return L.refs.at(e->args[k]->var.get()); };
     if (e->kind == ExprKind::TupleGet) {
       L.refs[b.var.get()] = {L.refs.at(e->args[0]->var.get()).at(e->index)};
+      note(L.refs[b.var.get()][0].unit);
       continue;
     }
     if (e->kind != ExprKind::Call) throw Error("memsched: unsupported let kind");
@@ -156,10 +165,12 @@ inline Layout build_layout(const ir::FunctionIR& fn, const std::vector<std::pair
       r.off += ir::attr_int(e->call_attrs, "offset", 0) * dtype_bytes(src.dtype);
       r.bytes = nbytes(b.var->ty);
       L.refs[b.var.get()] = {r};
+      note(r.unit);
       continue;
     }
     if (base == "reshape") {
       L.refs[b.var.get()] = {arg_refs(0)[0]};
+      note(arg_refs(0)[0].unit);
       continue;
     }
     if (base == "concat") {
@@ -183,6 +194,7 @@ inline Layout build_layout(const ir::FunctionIR& fn, const std::vector<std::pair
       }
       if (!all) L.concat_copy.push_back(i);
       L.refs[b.var.get()] = {Ref{u, 0, L.units[u].bytes}};
+      note(u);
       continue;
     }
     // ordinary op: one unit per output field, or in place into a bound param
@@ -202,6 +214,21 @@ inline Layout build_layout(const ir::FunctionIR& fn, const std::vector<std::pair
       }
     } else {
       int pu = try_bind(b.var.get(), i, e, 0);
+      // plain in-place reuse: an in-place-safe input whose whole, unaliased
+      // activation unit dies at this op hands its storage to the output
+      if (pu < 0 && !bind.count(b.var.get())) {
+        for (size_t k = 0; k < e->args.size() && pu < 0; ++k) {
+          if (e->args[k]->kind != ExprKind::VarRef || !inplace_safe(base, int(k), 0)) continue;
+          const ir::Var* av = e->args[k]->var.get();
+          const auto& rs = L.refs.at(av);
+          if (rs.size() != 1) continue;
+          const Ref& r = rs[0];
+          const Unit& cu = L.units[r.unit];
+          if (cu.param < 0 && cu.parent < 0 && r.off == 0 && r.bytes == cu.bytes && cu.bytes == nbytes(b.var->ty) &&
+              unit_refs[r.unit] == 1 && last_use[av] == i && !ret_index.count(av))
+            pu = r.unit;
+        }
+      }
       if (pu >= 0) outs.push_back(Ref{pu, 0, nbytes(b.var->ty)});
       else {
         int u = new_unit(nbytes(b.var->ty), i, i);
@@ -209,6 +236,10 @@ inline Layout build_layout(const ir::FunctionIR& fn, const std::vector<std::pair
       }
     }
     L.refs[b.var.get()] = outs;
+    for (auto& r : outs) {
+      if (int(unit_refs.size()) <= r.unit) unit_refs.resize(r.unit + 1, 0);
+      unit_refs[r.unit]++;
+    }
   }
   // uses extend lifetimes
   for (int i = 0; i < L.n; ++i)
