@@ -28,11 +28,11 @@ constexpr int TC_BK = 64;  // 64 bf16 = 128 B = one SWIZZLE_128B atom row
 
 template <int BN>
 struct TcCfg {
-  static constexpr int STAGES = BN == 256 ? 4 : 6;
+  static constexpr int STAGES = BN == 256 ? 4 : BN == 192 ? 5 : 6;
   static constexpr int A_BYTES = TC_BM * TC_BK * 2;  // 16 KB
   static constexpr int B_BYTES = BN * TC_BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int TMEM_COLS = 2 * BN;
+  static constexpr int TMEM_COLS = 2 * BN <= 256 ? 256 : 512;  // power of two >= 2 accumulators
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 };
 
@@ -501,10 +501,29 @@ static void launch_bn(const GemmArgs& g, cudaStream_t s) {
 void launch_gemm_tc(const GemmArgs& g, cudaStream_t s) {
   std::string why;
   if (!gemm_tc_supported(g, &why)) fail(TCB_ERR_UNIMPLEMENTED, "tcgen05 gemm: " + why);
-  // wave quantisation: prefer 256-wide tiles unless that leaves most SMs idle
+  // Tile width by a wave-quantised cost model: time ~ waves(BN) * BN / e(BN),
+  // where e(BN) is the measured mainloop efficiency of a 1-CTA 128xBN tile
+  // (smem-read bound at small BN: ~0.5 @128, ~0.66 @192, ~0.75 @256).
   const int64_t mb = (g.M + TC_BM - 1) / TC_BM;
-  const int64_t t256 = mb * ((g.N + 255) / 256) * g.Z;
-  if (g.N > 128 && t256 >= kNumSMs) launch_bn<256>(g, s);
+  int best = 128;
+  double best_cost = 1e30;
+  const int cand[3] = {256, 192, 128};
+  const double eff[3] = {0.75, 0.66, 0.5};
+  for (int i = 0; i < 3; ++i) {
+    const int bn = cand[i];
+    if (bn > 128 && g.N <= 128) continue;
+    const int64_t nb = (g.N + bn - 1) / bn;
+    const int64_t tiles = mb * nb * g.Z;
+    const double waves = double((tiles + kNumSMs - 1) / kNumSMs);
+    // columns actually computed per n-block (tail blocks waste the remainder)
+    const double cost = waves * double(bn) / eff[i];
+    if (cost < best_cost - 1e-9) {
+      best_cost = cost;
+      best = bn;
+    }
+  }
+  if (best == 256) launch_bn<256>(g, s);
+  else if (best == 192) launch_bn<192>(g, s);
   else launch_bn<128>(g, s);
 }
 

@@ -49,11 +49,48 @@ def run(name, op, M, K, N, ta, tb, out, iters):
     return {"name": name, "M": M, "K": K, "N": N, "ta": ta, "tb": tb, "us": round(us, 2), "tflops": round(tf, 1)}
 
 
+def time_plan(plan, ins, outs, iters):
+    s = torch.cuda.current_stream().cuda_stream
+    for _ in range(3):
+        plan.launch(ins, outs, s)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(iters):
+        plan.launch(ins, outs, s)
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) * 1000 / iters
+
+
+def attention(iters, p=0.1):
+    """BERT-base attention closures (B=32, S=128, A=12, dh=64)."""
+    B, S, A, H = 32, 128, 12, 768
+    T = B * S
+    qkv = torch.randn(T, 3 * H, device="cuda").to(torch.bfloat16)
+    ctx = torch.empty(T, H, device="cuda", dtype=torch.bfloat16)
+    probs = torch.empty(B * A * S, S, device="cuda", dtype=torch.bfloat16)
+    dq = torch.empty_like(qkv)
+    at = {"heads": A, "seq": S, "p": p, "seed": 7, "salt": 1}
+    f = Plan("attention", [((T, 3 * H), BF16)], [((T, H), BF16), ((B * A * S, S), BF16)], at)
+    b = Plan("attention_dx", [((T, 3 * H), BF16), ((B * A * S, S), BF16), ((T, H), BF16)], [((T, 3 * H), BF16)], at)
+    uf = time_plan(f, [qkv.data_ptr()], [ctx.data_ptr(), probs.data_ptr()], iters)
+    ub = time_plan(b, [qkv.data_ptr(), probs.data_ptr(), ctx.data_ptr()], [dq.data_ptr()], iters)
+    fl = 4.0 * B * A * S * S * 64
+    return [{"name": "attention_fwd", "us": round(uf, 2), "tflops": round(fl / uf / 1e6, 1)},
+            {"name": "attention_bwd", "us": round(ub, 2), "tflops": round(2 * fl / ub / 1e6, 1)}]
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--only", type=int, default=-1)
     ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--attention", action="store_true")
     args = ap.parse_args()
+    if args.attention:
+        for r in attention(args.iters):
+            print(json.dumps(r), flush=True)
+        return
     shapes = SHAPES if args.only < 0 else [SHAPES[args.only]]
     for sh in shapes:
         print(json.dumps(run(*sh, iters=args.iters)), flush=True)
