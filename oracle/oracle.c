@@ -123,9 +123,11 @@ static void round_all(const orc_tensor* t, int64_t n) {
 
 /* ------------------------------------------------------------------ philox */
 /* Philox4x32-10 (Salmon et al., SC'11), the counter-based generator used by
- * every dropout site on both CPU and GPU.  Element i of
- * a site draws word (i & 3) of philox(counter = {i >> 2, salt_lo, salt_hi, 0},
- * key = {seed_lo, seed_hi}); keep iff (word >> 8) * 2^-24 >= p. */
+ * every dropout site on both CPU and GPU.  One call
+ * covers 8 elements: element i of a site draws 16-bit lane (i & 7) of
+ * philox(counter = {i >> 3, salt_lo, salt_hi, 0}, key = {seed_lo, seed_hi})
+ * (low half of word (i&7)>>1 for even i, high half for odd); keep iff
+ * h * 2^-16 >= p. */
 static void philox4x32_10(uint32_t c[4], uint32_t k0, uint32_t k1) {
   for (int r = 0; r < 10; ++r) {
     uint64_t p0 = (uint64_t)0xD2511F53u * c[0];
@@ -145,10 +147,11 @@ static void philox4x32_10(uint32_t c[4], uint32_t k0, uint32_t k1) {
 
 int orc_dropout_keep(uint64_t seed, uint64_t salt, uint64_t index, float p) {
   if (p <= 0.0f) return 1;
-  uint32_t c[4] = {(uint32_t)(index >> 2), (uint32_t)salt, (uint32_t)(salt >> 32), 0u};
+  uint32_t c[4] = {(uint32_t)(index >> 3), (uint32_t)salt, (uint32_t)(salt >> 32), 0u};
   philox4x32_10(c, (uint32_t)seed, (uint32_t)(seed >> 32));
-  uint32_t w = c[index & 3];
-  float u = (float)(w >> 8) * (1.0f / 16777216.0f);
+  uint32_t w = c[(index & 7) >> 1];
+  uint32_t h = (index & 1) ? (w >> 16) : (w & 0xFFFFu);
+  float u = (float)h * (1.0f / 65536.0f);
   return u >= p;
 }
 

@@ -172,21 +172,30 @@ struct DropCfg {
   float p = 0.0f, scale = 1.0f;
   uint64_t seed = 0, salt = 0;
 };
-// 4 keep bits for indices (q*4 .. q*4+3)
-__device__ __forceinline__ uint32_t dropout_bits4(const DropCfg& d, uint64_t q) {
+// 8 keep bits for indices (q*8 .. q*8+7): one Philox call, 16 bits per element
+// (identical to oracle.c orc_dropout_keep)
+__device__ __forceinline__ uint32_t dropout_bits8q(const DropCfg& d, uint64_t q) {
   uint32_t c[4] = {uint32_t(q), uint32_t(d.salt), uint32_t(d.salt >> 32), 0u};
   philox4x32_10(c, uint32_t(d.seed), uint32_t(d.seed >> 32));
   uint32_t bits = 0;
 #pragma unroll
-  for (int w = 0; w < 4; ++w) {
-    float u = float(c[w] >> 8) * (1.0f / 16777216.0f);
-    bits |= (u >= d.p ? 1u : 0u) << w;
+  for (int k = 0; k < 8; ++k) {
+    const uint32_t h = (k & 1) ? (c[k >> 1] >> 16) : (c[k >> 1] & 0xFFFFu);
+    bits |= (float(h) * (1.0f / 65536.0f) >= d.p ? 1u : 0u) << k;
   }
   return bits;
 }
 __device__ __forceinline__ bool dropout_keep(const DropCfg& d, uint64_t idx) {
   if (d.p <= 0.0f) return true;
-  return (dropout_bits4(d, idx >> 2) >> (idx & 3)) & 1u;
+  return (dropout_bits8q(d, idx >> 3) >> (idx & 7)) & 1u;
+}
+// keep bits of the 4 elements i0 .. i0+3 (one call when they share an 8-group)
+__device__ __forceinline__ uint32_t dropout_bits4(const DropCfg& d, uint64_t i0) {
+  if (d.p <= 0.0f) return 0xFu;
+  if ((i0 & 7) <= 4) return (dropout_bits8q(d, i0 >> 3) >> (i0 & 7)) & 0xFu;
+  uint32_t b = 0;
+  for (int k = 0; k < 4; ++k) b |= uint32_t(dropout_keep(d, i0 + k)) << k;
+  return b;
 }
 inline DropCfg drop_cfg(const Attrs& a) {
   DropCfg d;

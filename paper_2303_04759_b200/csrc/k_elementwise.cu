@@ -332,16 +332,16 @@ static void b_concat(Plan& p) {
 TCB_REGISTER("concat", b_concat);
 
 // ----------------------------------------------------------------- dropout
-// one Philox call yields the keep bits for 4 consecutive elements
+// one Philox call yields the keep bits for 8 consecutive elements
 template <typename T>
 __global__ void k_dropout(const T* __restrict__ x, T* __restrict__ y, int64_t n, DropCfg d) {
-  const int64_t nq = (n + 3) / 4;
+  const int64_t nq = (n + 7) / 8;
   for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < nq;
        q += int64_t(gridDim.x) * blockDim.x) {
-    uint32_t bits = d.p > 0.0f ? dropout_bits4(d, uint64_t(q)) : 0xFu;
+    uint32_t bits = d.p > 0.0f ? dropout_bits8q(d, uint64_t(q)) : 0xFFu;
 #pragma unroll
-    for (int w = 0; w < 4; ++w) {
-      int64_t i = q * 4 + w;
+    for (int w = 0; w < 8; ++w) {
+      int64_t i = q * 8 + w;
       if (i < n) y[i] = from_f<T>(((bits >> w) & 1u) ? __fmul_rn(to_f(x[i]), d.scale) : 0.0f);
     }
   }
@@ -354,7 +354,7 @@ static void b_dropout(Plan& p) {
   dispatch_float(p.out[0].dtype, [&](auto* tp) {
     using T = std::remove_pointer_t<decltype(tp)>;
     p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
-      k_dropout<T><<<grid_for((n + 3) / 4, 256), 256, 0, s>>>((const T*)in[0].ptr, (T*)out[0].ptr, n, d);
+      k_dropout<T><<<grid_for((n + 7) / 8, 256), 256, 0, s>>>((const T*)in[0].ptr, (T*)out[0].ptr, n, d);
     };
   });
 }

@@ -122,7 +122,7 @@ static void dispatch_nc(int H, Fn&& f) {
 // keep bits for elements i .. i+7 (two Philox calls when i is 4-aligned)
 __device__ __forceinline__ uint32_t drop_bits8(const DropCfg& d, uint64_t i) {
   if (d.p <= 0.0f) return 0xFFu;
-  if ((i & 3) == 0) return dropout_bits4(d, i >> 2) | (dropout_bits4(d, (i >> 2) + 1) << 4);
+  if ((i & 7) == 0) return dropout_bits8q(d, i >> 3);
   uint32_t b = 0;
   for (int k = 0; k < 8; ++k) b |= uint32_t(dropout_keep(d, i + k)) << k;
   return b;
@@ -140,71 +140,98 @@ __global__ void __launch_bounds__(256) k_ln_fwd(const T* __restrict__ x, const T
                                                 T* __restrict__ s_out, float* __restrict__ mean_o,
                                                 float* __restrict__ rstd_o, int64_t rows, int H, float eps,
                                                 DropCfg d, bool vec) {
+  // RW rows per warp, every global load of both rows issued before the first
+  // reduction so enough bytes are in flight to cover DRAM latency
+  constexpr int RW = NC <= 2 ? 2 : 1;
   const int lane = threadIdx.x & 31;
-  const int64_t row = blockIdx.x * int64_t(blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (row >= rows) return;
+  const int64_t row0 = (blockIdx.x * int64_t(blockDim.x >> 5) + (threadIdx.x >> 5)) * RW;
+  if (row0 >= rows) return;
   const int nch = (H + 7) / 8;
-  float v[NC][8];
-  float sum = 0.0f;
+  float v[RW][NC][8], rr[RW][NC][8];
 #pragma unroll
-  for (int c = 0; c < NC; ++c) {
-    const int ch = lane + c * 32;
-    if (ch < nch) {
-      const int64_t i = row * H + ch * 8;
-      ld8(x, i, (row + 1) * int64_t(H), vec, v[c]);
-      if (r) {
-        float rr[8];
-        ld8(r, i, (row + 1) * int64_t(H), vec, rr);
-        const uint32_t bits = drop_bits8(d, uint64_t(i));
+  for (int q = 0; q < RW; ++q)
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          float xv = ((bits >> k) & 1u) ? __fmul_rn(v[c][k], d.scale) : 0.0f;
-          v[c][k] = to_f(from_f<T>(__fadd_rn(xv, rr[k])));  // s is rounded to the storage dtype
-        }
-        st8(s_out, i, (row + 1) * int64_t(H), vec, v[c]);
+    for (int c = 0; c < NC; ++c) {
+      const int64_t row = row0 + q;
+      const int ch = lane + c * 32;
+      if (row < rows && ch < nch) {
+        const int64_t i = row * H + ch * 8;
+        ld8(x, i, (row + 1) * int64_t(H), vec, v[q][c]);
+        if (r) ld8(r, i, (row + 1) * int64_t(H), vec, rr[q][c]);
       }
+    }
+  float sum[RW];
 #pragma unroll
-      for (int k = 0; k < 8; ++k)
-        if (ch * 8 + k < H) sum += v[c][k];
+  for (int q = 0; q < RW; ++q) {
+    sum[q] = 0.0f;
+    const int64_t row = row0 + q;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const int ch = lane + c * 32;
+      if (row < rows && ch < nch) {
+        const int64_t i = row * H + ch * 8;
+        if (r) {
+          const uint32_t bits = drop_bits8(d, uint64_t(i));
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            float xv = ((bits >> k) & 1u) ? __fmul_rn(v[q][c][k], d.scale) : 0.0f;
+            v[q][c][k] = to_f(from_f<T>(__fadd_rn(xv, rr[q][c][k])));  // s rounded to storage dtype
+          }
+          st8(s_out, i, (row + 1) * int64_t(H), vec, v[q][c]);
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (ch * 8 + k < H) sum[q] += v[q][c][k];
+      }
     }
   }
   const float inv = 1.0f / float(H);
-  const float mean = warp_sum(sum) * inv;
-  float sq = 0.0f;
+  float mean[RW], sq[RW];
 #pragma unroll
-  for (int c = 0; c < NC; ++c) {
-    const int ch = lane + c * 32;
-    if (ch < nch) {
+  for (int q = 0; q < RW; ++q) mean[q] = warp_sum(sum[q]) * inv;
 #pragma unroll
-      for (int k = 0; k < 8; ++k)
-        if (ch * 8 + k < H) {
-          float dd = v[c][k] - mean;
-          sq += dd * dd;
-        }
+  for (int q = 0; q < RW; ++q) {
+    sq[q] = 0.0f;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const int ch = lane + c * 32;
+      if (ch < nch) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (ch * 8 + k < H) {
+            float dd = v[q][c][k] - mean[q];
+            sq[q] += dd * dd;
+          }
+      }
     }
   }
-  const float rstd = 1.0f / sqrtf(warp_sum(sq) * inv + eps);
-  if (lane == 0) {
-    mean_o[row] = mean;
-    rstd_o[row] = rstd;
-  }
 #pragma unroll
-  for (int c = 0; c < NC; ++c) {
-    const int ch = lane + c * 32;
-    if (ch < nch) {
-      float o[8];
+  for (int q = 0; q < RW; ++q) {
+    const int64_t row = row0 + q;
+    if (row >= rows) break;
+    const float rstd = 1.0f / sqrtf(warp_sum(sq[q]) * inv + eps);
+    if (lane == 0) {
+      mean_o[row] = mean[q];
+      rstd_o[row] = rstd;
+    }
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int j = ch * 8 + k;
-        if (j < H) {
-          float g = gamma_f ? gamma_f[j] : to_f(gamma_t[j]);
-          float b = beta_f ? beta_f[j] : to_f(beta_t[j]);
-          o[k] = (v[c][k] - mean) * rstd * g + b;
-        } else {
-          o[k] = 0.0f;
+    for (int c = 0; c < NC; ++c) {
+      const int ch = lane + c * 32;
+      if (ch < nch) {
+        float o[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int j = ch * 8 + k;
+          if (j < H) {
+            float g = gamma_f ? __ldg(gamma_f + j) : to_f(gamma_t[j]);
+            float b = beta_f ? __ldg(beta_f + j) : to_f(beta_t[j]);
+            o[k] = (v[q][c][k] - mean[q]) * rstd * g + b;
+          } else {
+            o[k] = 0.0f;
+          }
         }
+        st8(y, row * H + ch * 8, (row + 1) * int64_t(H), vec, o);
       }
-      st8(y, row * H + ch * 8, (row + 1) * int64_t(H), vec, o);
     }
   }
 }
@@ -232,7 +259,8 @@ static void build_ln_fwd(Plan& p, bool residual) {
       for (int i = 0; i < (residual ? 2 : 1); ++i) vec = vec && reinterpret_cast<uintptr_t>(in[i].ptr) % 16 == 0;
       vec = vec && reinterpret_cast<uintptr_t>(out[0].ptr) % 16 == 0;
       if (residual) vec = vec && reinterpret_cast<uintptr_t>(out[1].ptr) % 16 == 0;
-      k_ln_fwd<T, NC><<<unsigned((rows + 7) / 8), 256, 0, s>>>(
+      constexpr int RW = NC <= 2 ? 2 : 1;
+      k_ln_fwd<T, NC><<<unsigned((rows + 8 * RW - 1) / (8 * RW)), 256, 0, s>>>(
           (const T*)in[0].ptr, residual ? (const T*)in[1].ptr : nullptr,
           gf ? (const float*)in[gi].ptr : nullptr, gf ? nullptr : (const T*)in[gi].ptr,
           gf ? (const float*)in[gi + 1].ptr : nullptr, gf ? nullptr : (const T*)in[gi + 1].ptr,
@@ -262,11 +290,16 @@ __global__ void __launch_bounds__(256) k_ln_bwd(const T* __restrict__ sx, const 
                                                 int H, DropCfg d, bool vec) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nch = (H + 7) / 8;
-  float pg[NC][8], pb[NC][8];
+  // per-warp dgamma/dbeta partials live in smem (not registers), laid out
+  // [warp][2][k][chunk] so a warp's accesses are bank-conflict free
+  extern __shared__ float red[];
+  constexpr int CP = NC * 32;  // chunk pitch
+  float* pg = red + (warp * 2 + 0) * 8 * CP;
+  float* pb = red + (warp * 2 + 1) * 8 * CP;
 #pragma unroll
   for (int c = 0; c < NC; ++c)
 #pragma unroll
-    for (int k = 0; k < 8; ++k) pg[c][k] = pb[c][k] = 0.0f;
+    for (int k = 0; k < 8; ++k) pg[k * CP + c * 32 + lane] = pb[k * CP + c * 32 + lane] = 0.0f;
   const float inv = 1.0f / float(H);
   for (int rr = 0; rr < LNB_ROWS / 8; ++rr) {
     const int64_t row = int64_t(blockIdx.x) * LNB_ROWS + warp * (LNB_ROWS / 8) + rr;
@@ -297,8 +330,8 @@ __global__ void __launch_bounds__(256) k_ln_bwd(const T* __restrict__ sx, const 
             g[c][k] = dv[k] * gm;
             c1 += g[c][k] * xh[c][k];
             c2 += g[c][k];
-            pg[c][k] += dv[k] * xh[c][k];
-            pb[c][k] += dv[k];
+            pg[k * CP + c * 32 + lane] += dv[k] * xh[c][k];
+            pb[k * CP + c * 32 + lane] += dv[k];
           } else {
             xh[c][k] = g[c][k] = 0.0f;
           }
@@ -325,28 +358,14 @@ __global__ void __launch_bounds__(256) k_ln_bwd(const T* __restrict__ sx, const 
       }
     }
   }
-  // CTA partials: smem reduce over the 8 warps, then one row of ws per CTA
-  extern __shared__ float red[];  // [8][2][H]
-#pragma unroll
-  for (int c = 0; c < NC; ++c) {
-    const int ch = lane + c * 32;
-    if (ch < nch) {
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int j = ch * 8 + k;
-        if (j < H) {
-          red[(warp * 2 + 0) * H + j] = pg[c][k];
-          red[(warp * 2 + 1) * H + j] = pb[c][k];
-        }
-      }
-    }
-  }
+  // CTA partials: fold the 8 warps' smem rows, then one row of ws per CTA
   __syncthreads();
   for (int j = threadIdx.x; j < H; j += blockDim.x) {
+    const int off = (j & 7) * CP + (j >> 3);
     float a = 0.0f, b = 0.0f;
     for (int w = 0; w < 8; ++w) {
-      a += red[(w * 2 + 0) * H + j];
-      b += red[(w * 2 + 1) * H + j];
+      a += red[(w * 2 + 0) * 8 * CP + off];
+      b += red[(w * 2 + 1) * 8 * CP + off];
     }
     ws[(int64_t(blockIdx.x) * 2 + 0) * H + j] = a;
     ws[(int64_t(blockIdx.x) * 2 + 1) * H + j] = b;
@@ -395,7 +414,7 @@ static void b_layer_norm_dx(Plan& p) {
   const DropCfg d = drop_cfg(p.attrs);
   const int nblk = int((rows + LNB_ROWS - 1) / LNB_ROWS);
   auto ws = std::make_shared<Scratch>(size_t(nblk) * 2 * H * sizeof(float));
-  const size_t smem = size_t(16) * H * sizeof(float);
+  const size_t smem = size_t(16) * 8 * 32 * ((H + 255) / 256) * sizeof(float);  // [8 warps][2][8][NC*32]
   p.nkernels = 2;
   dispatch_float(S.dtype, [&](auto* tp) {
    using T = std::remove_pointer_t<decltype(tp)>;
@@ -403,7 +422,7 @@ static void b_layer_norm_dx(Plan& p) {
     constexpr int NC = decltype(nc)::value;
     static std::once_flag once;
     std::call_once(once, [] {
-      TCB_CUDA(cudaFuncSetAttribute(k_ln_bwd<T, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * 2048 * 4));
+      TCB_CUDA(cudaFuncSetAttribute(k_ln_bwd<T, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * 8 * 32 * 8 * 4));
     });
     p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
       bool vec = H % 8 == 0;
@@ -472,53 +491,68 @@ template <typename TI, typename TO, int NQ>
 __global__ void __launch_bounds__(256) k_softmax(const TI* __restrict__ x, TO* __restrict__ P,
                                                  TO* __restrict__ Pd, int64_t rows, int C, int Sq,
                                                  float scale, int causal, DropCfg d, bool vec) {
+  constexpr int RW = NQ == 1 ? 4 : NQ == 2 ? 2 : 1;  // rows per warp, loads batched
   const int lane = threadIdx.x & 31;
-  const int64_t row = blockIdx.x * int64_t(blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (row >= rows) return;
-  const int qi = int(row % Sq);
-  const int64_t base = row * C, lim = base + C;
-  float v[NQ][4];
-  float m = -INFINITY;
+  const int64_t row0 = (blockIdx.x * int64_t(blockDim.x >> 5) + (threadIdx.x >> 5)) * RW;
+  if (row0 >= rows) return;
+  float v[RW][NQ][4];
 #pragma unroll
-  for (int c = 0; c < NQ; ++c) {
-    const int j0 = (c * 32 + lane) * 4;
-    if (j0 < C) ld4(x, base + j0, lim, vec, v[c]);
+  for (int q = 0; q < RW; ++q)
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int j = j0 + k;
-      float t = (j < C) ? v[c][k] * scale : -INFINITY;
-      if (causal && j > qi) t = -INFINITY;
-      v[c][k] = t;
-      m = fmaxf(m, t);
+    for (int c = 0; c < NQ; ++c) {
+      const int j0 = (c * 32 + lane) * 4;
+      const int64_t base = (row0 + q) * C;
+      if (row0 + q < rows && j0 < C) ld4(x, base + j0, base + C, vec, v[q][c]);
     }
+  float m[RW], sum[RW];
+#pragma unroll
+  for (int q = 0; q < RW; ++q) {
+    const int qi = int((row0 + q) % Sq);
+    m[q] = -INFINITY;
+#pragma unroll
+    for (int c = 0; c < NQ; ++c)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int j = (c * 32 + lane) * 4 + k;
+        float t = (j < C) ? v[q][c][k] * scale : -INFINITY;
+        if (causal && j > qi) t = -INFINITY;
+        v[q][c][k] = t;
+        m[q] = fmaxf(m[q], t);
+      }
   }
-  m = warp_max(m);
-  float sum = 0.0f;
 #pragma unroll
-  for (int c = 0; c < NQ; ++c)
+  for (int q = 0; q < RW; ++q) m[q] = warp_max(m[q]);
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      v[c][k] = v[c][k] == -INFINITY ? 0.0f : expf(v[c][k] - m);
-      sum += v[c][k];
-    }
-  sum = warp_sum(sum);
+  for (int q = 0; q < RW; ++q) {
+    sum[q] = 0.0f;
 #pragma unroll
-  for (int c = 0; c < NQ; ++c) {
-    const int j0 = (c * 32 + lane) * 4;
-    if (j0 >= C) continue;
-    float o[4];
+    for (int c = 0; c < NQ; ++c)
 #pragma unroll
-    for (int k = 0; k < 4; ++k) o[k] = to_f(from_f<TO>(v[c][k] / sum));
-    st4(P, base + j0, lim, vec, o);
-    if (Pd) {
-      const uint64_t i0 = uint64_t(base + j0);
-      const uint32_t bits = d.p <= 0.0f ? 0xFu
-                            : (i0 & 3) == 0 ? dropout_bits4(d, i0 >> 2)
-                                            : (uint32_t(dropout_keep(d, i0)) | uint32_t(dropout_keep(d, i0 + 1)) << 1 |
-                                               uint32_t(dropout_keep(d, i0 + 2)) << 2 | uint32_t(dropout_keep(d, i0 + 3)) << 3);
+      for (int k = 0; k < 4; ++k) {
+        v[q][c][k] = v[q][c][k] == -INFINITY ? 0.0f : expf(v[q][c][k] - m[q]);
+        sum[q] += v[q][c][k];
+      }
+  }
 #pragma unroll
-      for (int k = 0; k < 4; ++k) o[k] = ((bits >> k) & 1u) ? o[k] * d.scale : 0.0f;
-      st4(Pd, base + j0, lim, vec, o);
+  for (int q = 0; q < RW; ++q) sum[q] = warp_sum(sum[q]);
+#pragma unroll
+  for (int q = 0; q < RW; ++q) {
+    if (row0 + q >= rows) break;
+    const int64_t base = (row0 + q) * C, lim = base + C;
+#pragma unroll
+    for (int c = 0; c < NQ; ++c) {
+      const int j0 = (c * 32 + lane) * 4;
+      if (j0 >= C) continue;
+      float o[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) o[k] = to_f(from_f<TO>(v[q][c][k] / sum[q]));
+      st4(P, base + j0, lim, vec, o);
+      if (Pd) {
+        const uint32_t bits = dropout_bits4(d, uint64_t(base + j0));
+#pragma unroll
+        for (int k = 0; k < 4; ++k) o[k] = ((bits >> k) & 1u) ? o[k] * d.scale : 0.0f;
+        st4(Pd, base + j0, lim, vec, o);
+      }
     }
   }
 }
@@ -528,44 +562,60 @@ template <typename TP, typename TG, typename TO, int NQ>
 __global__ void __launch_bounds__(256) k_softmax_bwd(const TP* __restrict__ P, const TG* __restrict__ dPd,
                                                      TO* __restrict__ dS, TO* __restrict__ Pd_o, int64_t rows,
                                                      int C, float scale, DropCfg d, bool vec) {
+  constexpr int RW = NQ == 1 ? 4 : NQ == 2 ? 2 : 1;
   const int lane = threadIdx.x & 31;
-  const int64_t row = blockIdx.x * int64_t(blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (row >= rows) return;
-  const int64_t base = row * C, lim = base + C;
-  float pv[NQ][4], dp[NQ][4];
-  float dot = 0.0f;
+  const int64_t row0 = (blockIdx.x * int64_t(blockDim.x >> 5) + (threadIdx.x >> 5)) * RW;
+  if (row0 >= rows) return;
+  float pv[RW][NQ][4], dp[RW][NQ][4];
 #pragma unroll
-  for (int c = 0; c < NQ; ++c) {
-    const int j0 = (c * 32 + lane) * 4;
+  for (int q = 0; q < RW; ++q)
 #pragma unroll
-    for (int k = 0; k < 4; ++k) pv[c][k] = dp[c][k] = 0.0f;
-    if (j0 >= C) continue;
-    ld4(P, base + j0, lim, vec, pv[c]);
-    ld4(dPd, base + j0, lim, vec, dp[c]);
-    const uint64_t i0 = uint64_t(base + j0);
-    const uint32_t bits = d.p <= 0.0f ? 0xFu
-                          : (i0 & 3) == 0 ? dropout_bits4(d, i0 >> 2)
-                                          : (uint32_t(dropout_keep(d, i0)) | uint32_t(dropout_keep(d, i0 + 1)) << 1 |
-                                             uint32_t(dropout_keep(d, i0 + 2)) << 2 | uint32_t(dropout_keep(d, i0 + 3)) << 3);
-    float pdv[4];
+    for (int c = 0; c < NQ; ++c) {
+      const int j0 = (c * 32 + lane) * 4;
+      const int64_t base = (row0 + q) * C;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const bool keep = (bits >> k) & 1u;
-      dp[c][k] = keep ? dp[c][k] * d.scale : 0.0f;
-      pdv[k] = keep ? pv[c][k] * d.scale : 0.0f;
-      dot += pv[c][k] * dp[c][k];
+      for (int k = 0; k < 4; ++k) pv[q][c][k] = dp[q][c][k] = 0.0f;
+      if (row0 + q < rows && j0 < C) {
+        ld4(P, base + j0, base + C, vec, pv[q][c]);
+        ld4(dPd, base + j0, base + C, vec, dp[q][c]);
+      }
     }
-    if (Pd_o) st4(Pd_o, base + j0, lim, vec, pdv);
+  float dot[RW];
+#pragma unroll
+  for (int q = 0; q < RW; ++q) {
+    dot[q] = 0.0f;
+    const int64_t base = (row0 + q) * C;
+#pragma unroll
+    for (int c = 0; c < NQ; ++c) {
+      const int j0 = (c * 32 + lane) * 4;
+      if (row0 + q >= rows || j0 >= C) continue;
+      const uint32_t bits = dropout_bits4(d, uint64_t(base + j0));
+      float pdv[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const bool keep = (bits >> k) & 1u;
+        dp[q][c][k] = keep ? dp[q][c][k] * d.scale : 0.0f;
+        pdv[k] = keep ? pv[q][c][k] * d.scale : 0.0f;
+        dot[q] += pv[q][c][k] * dp[q][c][k];
+      }
+      if (Pd_o) st4(Pd_o, base + j0, base + C, vec, pdv);
+    }
   }
-  dot = warp_sum(dot);
 #pragma unroll
-  for (int c = 0; c < NQ; ++c) {
-    const int j0 = (c * 32 + lane) * 4;
-    if (j0 >= C) continue;
-    float o[4];
+  for (int q = 0; q < RW; ++q) dot[q] = warp_sum(dot[q]);
 #pragma unroll
-    for (int k = 0; k < 4; ++k) o[k] = pv[c][k] * (dp[c][k] - dot) * scale;
-    st4(dS, base + j0, lim, vec, o);
+  for (int q = 0; q < RW; ++q) {
+    if (row0 + q >= rows) break;
+    const int64_t base = (row0 + q) * C;
+#pragma unroll
+    for (int c = 0; c < NQ; ++c) {
+      const int j0 = (c * 32 + lane) * 4;
+      if (j0 >= C) continue;
+      float o[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) o[k] = pv[q][c][k] * (dp[q][c][k] - dot[q]) * scale;
+      st4(dS, base + j0, base + C, vec, o);
+    }
   }
 }
 
@@ -578,6 +628,13 @@ static void dispatch_nq(int C, Fn&& f) {
   else if (nq <= 4) f(std::integral_constant<int, 4>{});
   else if (nq <= 8) f(std::integral_constant<int, 8>{});
   else fail(TCB_ERR_UNIMPLEMENTED, "softmax: row length > 1024 unsupported");
+}
+
+// grid for the softmax kernels: 8 warps per CTA, RW(NQ) rows per warp
+template <int NQ>
+static unsigned sm_grid(int64_t rows) {
+  constexpr int RW = NQ == 1 ? 4 : NQ == 2 ? 2 : 1;
+  return unsigned((rows + 8 * RW - 1) / (8 * RW));
 }
 
 template <typename Fn>
@@ -605,7 +662,7 @@ static void b_softmax(Plan& p) {
       const bool vec = C % 4 == 0 && reinterpret_cast<uintptr_t>(in[0].ptr) % 16 == 0 &&
                        reinterpret_cast<uintptr_t>(out[0].ptr) % 16 == 0 &&
                        (!pd || reinterpret_cast<uintptr_t>(out[1].ptr) % 16 == 0);
-      k_softmax<TI, TO, NQ><<<unsigned((rows + 7) / 8), 256, 0, s>>>(
+      k_softmax<TI, TO, NQ><<<sm_grid<NQ>(rows), 256, 0, s>>>(
           (const TI*)in[0].ptr, (TO*)out[0].ptr, pd ? (TO*)out[1].ptr : nullptr, rows, C, Sq, scale, causal, d, vec);
     };
    });
@@ -633,7 +690,7 @@ static void b_softmax_dx(Plan& p) {
         const bool vec = C % 4 == 0 && reinterpret_cast<uintptr_t>(in[0].ptr) % 16 == 0 &&
                          reinterpret_cast<uintptr_t>(in[1].ptr) % 16 == 0 &&
                          reinterpret_cast<uintptr_t>(out[0].ptr) % 16 == 0;
-        k_softmax_bwd<TP, TG, TO, NQ><<<unsigned((rows + 7) / 8), 256, 0, s>>>(
+        k_softmax_bwd<TP, TG, TO, NQ><<<sm_grid<NQ>(rows), 256, 0, s>>>(
             (const TP*)in[0].ptr, (const TG*)in[1].ptr, (TO*)out[0].ptr, nullptr, rows, C, scale, d, vec);
       };
      });
@@ -748,7 +805,7 @@ static void b_attention(Plan& p) {
       const int64_t rows = g.Z * g.S;
       T* Pd = g.d.p > 0.0f ? (T*)pd->p : nullptr;
       dispatch_nq(int(g.S), [&](auto nq) {
-        k_softmax<float, T, decltype(nq)::value><<<unsigned((rows + 7) / 8), 256, 0, s>>>(
+        k_softmax<float, T, decltype(nq)::value><<<sm_grid<decltype(nq)::value>(rows), 256, 0, s>>>(
             (const float*)scores->p, (T*)out[1].ptr, Pd, rows, int(g.S), int(g.S), 1.0f, g.causal, g.d,
             g.S % 4 == 0 && reinterpret_cast<uintptr_t>(out[1].ptr) % 16 == 0);
       });
@@ -784,7 +841,7 @@ static void b_attention_dx(Plan& p) {
       const int64_t rows = g.Z * g.S;
       T* Pd = g.d.p > 0.0f ? (T*)pd->p : nullptr;
       dispatch_nq(int(g.S), [&](auto nq) {
-        k_softmax_bwd<T, float, T, decltype(nq)::value><<<unsigned((rows + 7) / 8), 256, 0, s>>>(
+        k_softmax_bwd<T, float, T, decltype(nq)::value><<<sm_grid<decltype(nq)::value>(rows), 256, 0, s>>>(
             (const T*)in[1].ptr, (const float*)dpd->p, (T*)ds->p, Pd, rows, int(g.S), g.scale, g.d,
             g.S % 4 == 0 && reinterpret_cast<uintptr_t>(in[1].ptr) % 16 == 0);
       });
