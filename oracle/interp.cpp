@@ -62,42 +62,61 @@ std::vector<orc_attr> oattrs(const AttrMap& m, std::vector<std::string>& keep) {
   return out;
 }
 
-void run_step(Interp& I) {
+using Env = std::unordered_map<const ir::Var*, HVal>;
+
+// kind: 0 reduce_scatter (sum), 1 all_gather, 2 allreduce (sum); f32 slots
+using CollFn = int (*)(int kind, const float* in, int64_t in_n, float* out, int64_t out_n, int world, int rank);
+
+bool is_collective(const std::string& base) {
+  return base == "reduce_scatter" || base == "all_gather" || base == "allreduce";
+}
+int coll_kind(const std::string& base) { return base == "reduce_scatter" ? 0 : base == "all_gather" ? 1 : 2; }
+
+Env init_env(const Interp& I) {
+  Env env;
   const ir::FunctionIR& fn = *I.ts.fn;
-  auto seq = ir::flatten(fn);
-  std::unordered_map<const ir::Var*, HVal> env;
   for (size_t p = 0; p < fn.params.size(); ++p)
     env[fn.params[p].get()] = HVal{{I.state[p]}, {fn.params[p]->ty.tensor()}};
-  for (auto& b : seq.lets) {
-    const auto& e = b.value;
-    if (e->kind == ExprKind::TupleGet) {
-      const HVal& t = env.at(e->args[0]->var.get());
-      env[b.var.get()] = HVal{{t.fields.at(e->index)}, {t.types.at(e->index)}};
-      continue;
-    }
-    std::vector<TensorType> otys;
-    if (b.var->ty.is_tuple()) otys = b.var->ty.tuple().fields;
-    else otys = {b.var->ty.tensor()};
-    HVal out;
-    for (auto& t : otys) {
-      out.fields.push_back(std::make_shared<std::vector<uint32_t>>(size_t(numel(t)), 0u));
-      out.types.push_back(t);
-    }
-    std::vector<orc_tensor> ins, outs;
-    for (auto& a : e->args) {
-      HVal& v = env.at(a->var.get());
-      ins.push_back(odesc(*v.fields[0], v.types[0]));
-    }
-    for (size_t k = 0; k < otys.size(); ++k) outs.push_back(odesc(*out.fields[k], otys[k]));
-    std::vector<std::string> keep;
-    auto at = oattrs(e->call_attrs, keep);
-    const std::string base = base_name(e->op);
-    if (orc_exec(base.c_str(), ins.data(), int(ins.size()), outs.data(), int(outs.size()), at.data(),
-                 int(at.size())) != 0)
-      throw Error("oracle " + base + ": " + orc_last_error());
-    env[b.var.get()] = std::move(out);
+  return env;
+}
+
+HVal alloc_out(const ir::LetBinding& b) {
+  std::vector<TensorType> otys;
+  if (b.var->ty.is_tuple()) otys = b.var->ty.tuple().fields;
+  else otys = {b.var->ty.tensor()};
+  HVal out;
+  for (auto& t : otys) {
+    out.fields.push_back(std::make_shared<std::vector<uint32_t>>(size_t(numel(t)), 0u));
+    out.types.push_back(t);
   }
-  // returns -> state bindings; loss
+  return out;
+}
+
+// one let on one rank (everything except collectives with world > 1)
+void exec_let(Env& env, const ir::LetBinding& b) {
+  const auto& e = b.value;
+  if (e->kind == ExprKind::TupleGet) {
+    const HVal& t = env.at(e->args[0]->var.get());
+    env[b.var.get()] = HVal{{t.fields.at(e->index)}, {t.types.at(e->index)}};
+    return;
+  }
+  HVal out = alloc_out(b);
+  std::vector<orc_tensor> ins, outs;
+  for (auto& a : e->args) {
+    HVal& v = env.at(a->var.get());
+    ins.push_back(odesc(*v.fields[0], v.types[0]));
+  }
+  for (size_t k = 0; k < out.fields.size(); ++k) outs.push_back(odesc(*out.fields[k], out.types[k]));
+  std::vector<std::string> keep;
+  auto at = oattrs(e->call_attrs, keep);
+  const std::string base = base_name(e->op);
+  if (orc_exec(base.c_str(), ins.data(), int(ins.size()), outs.data(), int(outs.size()), at.data(),
+               int(at.size())) != 0)
+    throw Error("oracle " + base + ": " + orc_last_error());
+  env[b.var.get()] = std::move(out);
+}
+
+void finish_step(Interp& I, Env& env, const ir::LetSeq& seq) {
   const HVal& loss = env.at(seq.ret->args.at(0)->var.get());
   float lv;
   std::memcpy(&lv, loss.fields[0]->data(), 4);
@@ -106,6 +125,109 @@ void run_step(Interp& I) {
     const HVal& v = env.at(seq.ret->args.at(rj)->var.get());
     *I.state[pi] = *v.fields[0];
   }
+}
+
+/// single rank; collectives with world > 1 go through `coll` (e.g. gloo from
+/// Python) -- without it the oracle refuses them like exec_base does.
+void run_step(Interp& I, CollFn coll = nullptr, int rank = 0) {
+  auto seq = ir::flatten(*I.ts.fn);
+  Env env = init_env(I);
+  for (auto& b : seq.lets) {
+    const auto& e = b.value;
+    if (e->kind == ExprKind::Call && is_collective(base_name(e->op)) &&
+        ir::attr_int(e->call_attrs, "world", 1) > 1 && coll) {
+      HVal out = alloc_out(b);
+      HVal& in = env.at(e->args[0]->var.get());
+      const int world = int(ir::attr_int(e->call_attrs, "world", 1));
+      if (coll(coll_kind(base_name(e->op)), reinterpret_cast<const float*>(in.fields[0]->data()),
+               int64_t(in.fields[0]->size()), reinterpret_cast<float*>(out.fields[0]->data()),
+               int64_t(out.fields[0]->size()), world, rank))
+        throw ProtocolError("collective callback failed at %" + b.var->id);
+      env[b.var.get()] = std::move(out);
+      continue;
+    }
+    exec_let(env, b);
+  }
+  finish_step(I, env, seq);
+}
+
+/// The deterministic in-process bus: ranks execute the same
+/// let sequence in lockstep; a collective is a barrier where the bus reduces in
+/// fixed rank order 0..n-1 (so the simulation is bit-reproducible); a
+/// mismatched op across ranks raises ProtocolError.
+void run_world_step(std::vector<Interp>& R) {
+  const int N = int(R.size());
+  auto seq = ir::flatten(*R[0].ts.fn);
+  std::vector<ir::LetSeq> seqs;
+  for (auto& I : R) seqs.push_back(ir::flatten(*I.ts.fn));
+  std::vector<Env> env;
+  for (auto& I : R) env.push_back(init_env(I));
+  for (size_t li = 0; li < seq.lets.size(); ++li) {
+    const auto& b = seq.lets[li];
+    const auto& e = b.value;
+    for (int r = 1; r < N; ++r) {
+      const auto& br = seqs[r].lets.at(li);
+      if (br.value->kind != e->kind || br.value->op != e->op)
+        throw ProtocolError("bus: rank " + std::to_string(r) + " issued a different op at let " + std::to_string(li));
+    }
+    if (e->kind == ExprKind::Call && is_collective(base_name(e->op))) {
+      const std::string base = base_name(e->op);
+      // every rank built its own graph: look each rank's vars up in its own let
+      std::vector<const float*> in(N);
+      for (int r = 0; r < N; ++r)
+        in[r] = reinterpret_cast<const float*>(
+            env[r].at(seqs[r].lets[li].value->args[0]->var.get()).fields[0]->data());
+      const int64_t in_n = int64_t(env[0].at(e->args[0]->var.get()).fields[0]->size());
+      for (int r = 0; r < N; ++r) {
+        HVal out = alloc_out(seqs[r].lets[li]);
+        float* o = reinterpret_cast<float*>(out.fields[0]->data());
+        const int64_t out_n = int64_t(out.fields[0]->size());
+        if (base == "reduce_scatter") {  // shard r of the rank-ordered sum (zero padded)
+          for (int64_t k = 0; k < out_n; ++k) {
+            const int64_t g = int64_t(r) * out_n + k;
+            float acc = 0.0f;
+            for (int q = 0; q < N; ++q) acc += g < in_n ? in[q][g] : 0.0f;
+            o[k] = acc;
+          }
+        } else if (base == "all_gather") {  // concat of shards, truncated
+          for (int64_t k = 0; k < out_n; ++k) o[k] = in[k / in_n][k % in_n];
+        } else {  // allreduce
+          for (int64_t k = 0; k < out_n; ++k) {
+            float acc = 0.0f;
+            for (int q = 0; q < N; ++q) acc += in[q][k];
+            o[k] = acc;
+          }
+        }
+        env[r][seqs[r].lets[li].var.get()] = std::move(out);
+      }
+      continue;
+    }
+    for (int r = 0; r < N; ++r) exec_let(env[r], seqs[r].lets[li]);
+  }
+  for (int r = 0; r < N; ++r) finish_step(R[r], env[r], seqs[r]);
+}
+
+std::unique_ptr<Interp> make_interp(const std::string& cfg, int rank) {
+  ensure_registered({});
+  auto I = std::make_unique<Interp>();
+  I->ts = build_train_step(parse_cfg(cfg));
+  const auto& ps = I->ts.fn->params;
+  for (auto& p : ps) I->state.push_back(std::make_shared<std::vector<uint32_t>>(size_t(numel(p->ty.tensor())), 0u));
+  // params (this rank's shard under ZeRO) / half copy from the shared
+  // initialiser; m, v, step = 0
+  std::vector<float> p = init_params(I->ts);
+  const int64_t sh = int64_t(I->state[I->ts.i_params]->size());
+  std::memcpy(I->state[I->ts.i_params]->data(), p.data() + size_t(rank) * size_t(sh), size_t(sh) * 4);
+  if (I->ts.i_p16 >= 0) {
+    const DType cd = I->ts.fn->params[I->ts.i_p16]->ty.tensor().dtype;
+    for (size_t i = 0; i < p.size(); ++i) {
+      float q = cd == kBF16 ? orc_quantize_bf16(p[i]) : cd == kF16 ? orc_quantize_f16(p[i]) : p[i];
+      std::memcpy(&(*I->state[I->ts.i_p16])[i], &q, 4);
+    }
+  }
+  const int64_t T = I->ts.cfg.T();
+  for (int64_t t = 0; t < T; ++t) (*I->state[I->ts.i_pos])[t] = uint32_t(t % I->ts.cfg.S);
+  return I;
 }
 
 }  // namespace
@@ -117,22 +239,17 @@ const char* orc_interp_last_error(void) { return g_err.c_str(); }
 /// Same cfg string as tb_session_create (model keys only).
 void* orc_interp_create(const char* cfg) {
   try {
-    ensure_registered({});
-    auto I = std::make_unique<Interp>();
-    I->ts = build_train_step(parse_cfg(cfg ? cfg : ""));
-    const auto& ps = I->ts.fn->params;
-    for (auto& p : ps) I->state.push_back(std::make_shared<std::vector<uint32_t>>(size_t(numel(p->ty.tensor())), 0u));
-    // params / half copy from the shared initialiser; m, v, step = 0
-    std::vector<float> p = init_params(I->ts);
-    std::memcpy(I->state[I->ts.i_params]->data(), p.data(), p.size() * 4);
-    if (I->ts.i_p16 >= 0)
-      for (size_t i = 0; i < p.size(); ++i) {
-        float q = orc_quantize_bf16(p[i]);
-        std::memcpy(&(*I->state[I->ts.i_p16])[i], &q, 4);
-      }
-    const int64_t T = I->ts.cfg.T();
-    for (int64_t t = 0; t < T; ++t) (*I->state[I->ts.i_pos])[t] = uint32_t(t % I->ts.cfg.S);
-    return I.release();
+    return make_interp(cfg ? cfg : "", 0).release();
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
+
+/// one rank of a world (cfg carries world=N): params = shard `rank`
+void* orc_interp_create_rank(const char* cfg, int rank) {
+  try {
+    return make_interp(cfg ? cfg : "", rank).release();
   } catch (const std::exception& e) {
     g_err = e.what();
     return nullptr;
@@ -141,13 +258,14 @@ void* orc_interp_create(const char* cfg) {
 
 void orc_interp_destroy(void* h) { delete static_cast<Interp*>(h); }
 
-int orc_interp_step(void* h, const int32_t* ids, const int32_t* labels, float* loss) {
+/// coll: optional collective callback for world > 1 (NULL: refuse, as exec_base)
+int orc_interp_step_coll(void* h, const int32_t* ids, const int32_t* labels, float* loss, CollFn coll, int rank) {
   try {
     auto* I = static_cast<Interp*>(h);
     const int64_t T = I->ts.cfg.T();
     std::memcpy(I->state[I->ts.i_ids]->data(), ids, size_t(T) * 4);
     std::memcpy(I->state[I->ts.i_labels]->data(), labels, size_t(T) * 4);
-    run_step(*I);
+    run_step(*I, coll, rank);
     *loss = float(I->last_loss);
     return 0;
   } catch (const std::exception& e) {
@@ -155,6 +273,49 @@ int orc_interp_step(void* h, const int32_t* ids, const int32_t* labels, float* l
     return 1;
   }
 }
+
+int orc_interp_step(void* h, const int32_t* ids, const int32_t* labels, float* loss) {
+  return orc_interp_step_coll(h, ids, labels, loss, nullptr, 0);
+}
+
+/// lockstep world of N ranks on the in-process bus
+struct WorldH {
+  std::vector<Interp> ranks;
+};
+
+void* orc_world_create(const char* cfg, int n) {
+  try {
+    auto w = std::make_unique<WorldH>();
+    for (int r = 0; r < n; ++r) w->ranks.push_back(std::move(*make_interp(cfg ? cfg : "", r)));
+    return w.release();
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
+
+void orc_world_destroy(void* h) { delete static_cast<WorldH*>(h); }
+
+/// ids/labels: N consecutive per-rank batches of T tokens; losses: N floats
+int orc_world_step(void* h, const int32_t* ids, const int32_t* labels, float* losses) {
+  try {
+    auto* w = static_cast<WorldH*>(h);
+    const int64_t T = w->ranks[0].ts.cfg.T();
+    for (size_t r = 0; r < w->ranks.size(); ++r) {
+      auto& I = w->ranks[r];
+      std::memcpy(I.state[I.ts.i_ids]->data(), ids + r * T, size_t(T) * 4);
+      std::memcpy(I.state[I.ts.i_labels]->data(), labels + r * T, size_t(T) * 4);
+    }
+    run_world_step(w->ranks);
+    for (size_t r = 0; r < w->ranks.size(); ++r) losses[r] = float(w->ranks[r].last_loss);
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
+void* orc_world_rank(void* h, int r) { return &static_cast<WorldH*>(h)->ranks.at(size_t(r)); }
 
 /// copy function parameter `name` (f32 slots / i32) to host
 int orc_interp_read(void* h, const char* name, void* dst, int64_t nelem) {

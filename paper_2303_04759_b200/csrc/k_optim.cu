@@ -100,7 +100,7 @@ static void b_adam(Plan& p) {
             p.attrs.f("eps", 1e-8), p.attrs.f("grad_scale", 1.0)};
   const int64_t n = p.in[0].numel();
   const int hd = p.out.size() > 3 ? p.out[3].dtype : -1;
-  if (hd >= 0) require(hd == TCB_BF16 || hd == TCB_F16, "adam_update_ex: 4th output must be bf16/f16");
+  if (hd >= 0) require(is_float(hd), "adam_update_ex: 4th output must be a float copy");
   p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
     for (int i = 0; i < 4; ++i)
       if (reinterpret_cast<uintptr_t>(in[i].ptr) % 16 || (i < 3 && reinterpret_cast<uintptr_t>(out[i].ptr) % 16))
@@ -121,7 +121,8 @@ static void b_adam(Plan& p) {
       k_adam<float><<<grid, 256, 0, s>>>((const float*)in[0].ptr, (const float*)in[1].ptr,
                                          (const float*)in[2].ptr, (const float*)in[3].ptr,
                                          (const float*)in[4].ptr, (float*)out[0].ptr,
-                                         (float*)out[1].ptr, (float*)out[2].ptr, nullptr, n, c);
+                                         (float*)out[1].ptr, (float*)out[2].ptr,
+                                         hd == TCB_F32 ? (float*)out[3].ptr : nullptr, n, c);
   };
 }
 TCB_REGISTER("adam_update", b_adam);

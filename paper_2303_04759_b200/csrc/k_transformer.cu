@@ -906,7 +906,8 @@ TCB_REGISTER("embedding", b_embedding);
 // tiles); the first occurrence of each id also records its segment length at
 // the segment's head position (seg_len is zeroed beforehand).
 __global__ void __launch_bounds__(64) k_embed_rank(const int32_t* __restrict__ ids, int32_t* __restrict__ sorted,
-                                                   int32_t* __restrict__ seg_len, int64_t T) {
+                                                   int32_t* __restrict__ seg_len, int32_t* __restrict__ seg_head,
+                                                   int64_t T) {
   __shared__ int32_t tile[2048];
   const int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   const int32_t my = t < T ? ids[t] : 0;
@@ -925,7 +926,30 @@ __global__ void __launch_bounds__(64) k_embed_rank(const int32_t* __restrict__ i
   }
   if (t >= T) return;
   sorted[less + eq_before] = int32_t(t);
+  seg_head[less + eq_before] = int32_t(less);
   if (eq_before == 0) seg_len[less] = int32_t(eq);
+}
+
+constexpr int EMB_CHUNK = 128;  // rows per partial sum of a long segment
+
+// Segments longer than EMB_CHUNK are summed chunk by chunk (each chunk in
+// ascending t into part[chunk_start]) and folded here in chunk order onto
+// base: deterministic; for segments <= EMB_CHUNK rows k_embed_accum writes the
+// oracle's exact sequential sum directly.
+__global__ void __launch_bounds__(256) k_embed_fold(const int32_t* __restrict__ ids,
+                                                    const int32_t* __restrict__ sorted,
+                                                    const int32_t* __restrict__ seg_len,
+                                                    const float* __restrict__ part, float* __restrict__ out,
+                                                    int64_t H) {
+  const int64_t pos = blockIdx.x;
+  const int32_t len = seg_len[pos];
+  if (len <= EMB_CHUNK) return;
+  const int32_t id = ids[sorted[pos]];
+  const int64_t j = int64_t(blockIdx.y) * blockDim.x + threadIdx.x;
+  if (j >= H) return;
+  float acc = out[int64_t(id) * H + j];
+  for (int64_t c = pos; c < pos + len; c += EMB_CHUNK) acc = __fadd_rn(acc, part[c * H + j]);
+  out[int64_t(id) * H + j] = acc;
 }
 
 // block (pos, column tile): if sorted position `pos` starts a segment of equal
@@ -936,16 +960,19 @@ template <typename TD>
 __global__ void __launch_bounds__(256) k_embed_accum(const int32_t* __restrict__ ids,
                                                      const int32_t* __restrict__ sorted,
                                                      const int32_t* __restrict__ seg_len,
+                                                     const int32_t* __restrict__ seg_head,
                                                      const TD* __restrict__ dy, float* __restrict__ out,
-                                                     int64_t T, int64_t H) {
+                                                     float* __restrict__ part, int64_t T, int64_t H) {
   const int64_t pos = blockIdx.x;
-  const int32_t len = seg_len[pos];
-  if (len == 0) return;  // not a segment head
+  const int64_t head = seg_head[pos];
+  if ((pos - head) % EMB_CHUNK) return;  // not a chunk start
+  const int32_t len = seg_len[head];
+  const bool single = len <= EMB_CHUNK;
+  const int64_t end = (head + len) < (pos + EMB_CHUNK) ? (head + len) : (pos + EMB_CHUNK);
   const int32_t id = ids[sorted[pos]];
-  const int64_t end = pos + len;
   const int64_t j = int64_t(blockIdx.y) * blockDim.x + threadIdx.x;
   if (j >= H) return;
-  float acc = out[int64_t(id) * H + j];
+  float acc = single ? out[int64_t(id) * H + j] : 0.0f;
   int64_t q = pos;
   for (; q + 4 <= end; q += 4) {
     float v0 = to_f(dy[int64_t(sorted[q]) * H + j]);
@@ -955,7 +982,8 @@ __global__ void __launch_bounds__(256) k_embed_accum(const int32_t* __restrict__
     acc = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(acc, v0), v1), v2), v3);
   }
   for (; q < end; ++q) acc = __fadd_rn(acc, to_f(dy[int64_t(sorted[q]) * H + j]));
-  out[int64_t(id) * H + j] = acc;
+  if (single) out[int64_t(id) * H + j] = acc;
+  else part[pos * H + j] = acc;
 }
 
 static void b_embedding_dx(Plan& p) {
@@ -966,8 +994,9 @@ static void b_embedding_dx(Plan& p) {
   require(p.in[1].numel() == T * H, "embedding_dx: dy must be [T, H]");
   const bool has_base = p.in.size() > 2;
   if (has_base) require(p.in[2].dtype == TCB_F32 && p.in[2].numel() == V * H, "embedding_dx: base is f32 [V,H]");
-  auto sorted = std::make_shared<Scratch>(size_t(T) * 8);  // sorted[T] ++ seg_len[T]
-  p.nkernels = 3;
+  auto sorted = std::make_shared<Scratch>(size_t(T) * 12);  // sorted[T] ++ seg_len[T] ++ seg_head[T]
+  auto part = std::make_shared<Scratch>(size_t(T) * H * 4);  // chunk partials of long segments
+  p.nkernels = 4;
   dispatch_float(p.in[1].dtype, [&](auto* tp) {
     using TD = std::remove_pointer_t<decltype(tp)>;
     p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
@@ -979,10 +1008,14 @@ static void b_embedding_dx(Plan& p) {
       }
       int32_t* srt = (int32_t*)sorted->p;
       int32_t* seg = srt + T;
+      int32_t* hd = seg + T;
       TCB_CUDA(cudaMemsetAsync(seg, 0, size_t(T) * 4, s));
-      k_embed_rank<<<unsigned((T + 63) / 64), 64, 0, s>>>((const int32_t*)in[0].ptr, srt, seg, T);
-      k_embed_accum<TD><<<dim3(unsigned(T), unsigned((H + 255) / 256)), 256, 0, s>>>(
-          (const int32_t*)in[0].ptr, srt, seg, (const TD*)in[1].ptr, (float*)out[0].ptr, T, H);
+      const int32_t* ids = (const int32_t*)in[0].ptr;
+      const dim3 g2(unsigned(T), unsigned((H + 255) / 256));
+      k_embed_rank<<<unsigned((T + 63) / 64), 64, 0, s>>>(ids, srt, seg, hd, T);
+      k_embed_accum<TD><<<g2, 256, 0, s>>>(ids, srt, seg, hd, (const TD*)in[1].ptr, (float*)out[0].ptr,
+                                          (float*)part->p, T, H);
+      k_embed_fold<<<g2, 256, 0, s>>>(ids, srt, seg, (const float*)part->p, (float*)out[0].ptr, H);
     };
   });
 }

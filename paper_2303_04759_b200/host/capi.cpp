@@ -222,9 +222,15 @@ int tb_session_init_params(void* h) {
     const float* mine = p.data() + size_t(s->cfg.world > 1 ? s->rank * sh : 0);
     tcb_check(tcb_memcpy(s->vm.param_ptr(s->ts.i_params), mine, uint64_t(sh) * 4, 0, nullptr), "params");
     if (s->ts.i_p16 >= 0) {
-      std::vector<uint16_t> h16(p.size());
-      for (size_t i = 0; i < p.size(); ++i) h16[i] = bf16_bits(p[i]);
-      tcb_check(tcb_memcpy(s->vm.param_ptr(s->ts.i_p16), h16.data(), uint64_t(h16.size()) * 2, 0, nullptr), "p16");
+      const DType cd = s->ts.fn->params[s->ts.i_p16]->ty.tensor().dtype;
+      if (cd == kF32) {
+        tcb_check(tcb_memcpy(s->vm.param_ptr(s->ts.i_p16), p.data(), uint64_t(p.size()) * 4, 0, nullptr), "pcopy");
+      } else {
+        if (cd != kBF16) throw Error("init_params: unsupported compute-copy dtype");
+        std::vector<uint16_t> h16(p.size());
+        for (size_t i = 0; i < p.size(); ++i) h16[i] = bf16_bits(p[i]);
+        tcb_check(tcb_memcpy(s->vm.param_ptr(s->ts.i_p16), h16.data(), uint64_t(h16.size()) * 2, 0, nullptr), "p16");
+      }
     }
     if (s->ts.i_m >= 0) {
       tcb_check(tcb_memset(s->vm.param_ptr(s->ts.i_m), 0, uint64_t(sh) * 4, nullptr), "m");

@@ -293,14 +293,17 @@ inline void register_b200_dialect(OpRegistry& r, const std::vector<std::string>&
   for (auto* c : kCollectives) add(c);
 }
 
-/// One-time, process-wide registration (the registry is "built once, then
-/// read-only").
+/// Process-wide registration before any compile (the registry is "built once,
+/// then read-only").  Idempotent and additive: the registry is
+/// a process-unique object shared by every library that includes opreg.hpp
+/// (its static is emitted as a unique symbol), so a CPU-only user (the oracle
+/// interpreter, which registers no dialect) and the device runtime can load in
+/// either order.
 inline void ensure_registered(const std::vector<std::string>& b200_ops) {
-  static std::once_flag once;
-  std::call_once(once, [&] {
-    register_extension_ops(opreg::registry());
-    register_b200_dialect(opreg::registry(), b200_ops);
-  });
+  static std::mutex mu;
+  std::lock_guard<std::mutex> g(mu);
+  register_extension_ops(opreg::registry());
+  register_b200_dialect(opreg::registry(), b200_ops);
 }
 
 inline std::vector<std::string> split_ws(const std::string& s) {

@@ -184,8 +184,9 @@ inline TrainStep build_train_step(const ModelCfg& c) {
   const DType act = dtype_from(c.dtype);
   const int64_t T = c.T(), H = c.H, Vp = c.vocab_pad();
   const bool adam = c.opt == "adam";
-  if (c.world > 1 && !adam) throw Error("ZeRO partitioning is implemented for Adam");
-  if (c.world > 1 && !amp) throw Error("ZeRO path expects the AutoCast (half param copy) graph");
+  // a full compute copy of the parameters exists under AutoCast (bf16) and
+  // under ZeRO (the master is sharded; the gathered copy feeds the forward)
+  const bool copy = amp || c.world > 1;
 
   Graph g;
   auto P = [&](const std::string& n, TensorType t) {
@@ -198,7 +199,7 @@ inline TrainStep build_train_step(const ModelCfg& c) {
   if (c.kind == "bert") ts.i_type = P("type_ids", {kI32, {T}});
   const int64_t pstate = c.world > 1 ? ts.shard() : ts.P_pad;
   ts.i_params = P("params", {kF32, {pstate}});
-  if (amp) ts.i_p16 = P("p16", {act, {ts.P_pad}});
+  if (copy) ts.i_p16 = P("p16", {act, {ts.P_pad}});
   if (adam) {
     ts.i_m = P("m", {kF32, {pstate}});
     ts.i_v = P("v", {kF32, {pstate}});
@@ -206,7 +207,7 @@ inline TrainStep build_train_step(const ModelCfg& c) {
   }
   auto par = [&](int i) { return g.params()[i]; };
   VarPtr ids = par(ts.i_ids), labels = par(ts.i_labels), pos_ids = par(ts.i_pos);
-  VarPtr wsrc = amp ? par(ts.i_p16) : par(ts.i_params);
+  VarPtr wsrc = copy ? par(ts.i_p16) : par(ts.i_params);
 
   std::vector<Leaf> leaves;
   std::map<std::string, VarPtr> W;
@@ -298,28 +299,36 @@ inline TrainStep build_train_step(const ModelCfg& c) {
 
   // ---- optimizer (+ ZeRO-1)
   std::vector<VarPtr> rets{loss};
+  const std::string full_shape = std::to_string(ts.P_pad);
+  VarPtr gsh = grad;
+  if (c.world > 1)  // sum-reduce-scatter of one flat bucket
+    gsh = g.op("reduce_scatter", {grad}, {{"world", c.world}});
   if (!adam) {
-    VarPtr np = g.op("sgd_update", {par(ts.i_params), grad}, {{"lr", c.lr}});
+    // mean over ranks folded into the step size: lr / N
+    VarPtr np = g.op("sgd_update", {par(ts.i_params), gsh}, {{"lr", c.lr / double(c.world)}});
     rets.push_back(np);
     ts.state_binding.push_back({1, ts.i_params});
+    if (copy) {  // refresh the compute copy (cast, then gather under ZeRO)
+      VarPtr nh = amp ? g.op("convert", {np}, {{"to", c.dtype}}) : np;
+      if (c.world > 1) nh = g.op("all_gather", {nh}, {{"world", c.world}, {"shape", full_shape}});
+      rets.push_back(nh);
+      ts.state_binding.push_back({2, ts.i_p16});
+    }
   } else {
-    VarPtr gsh = grad;
-    if (c.world > 1)
-      gsh = g.op("reduce_scatter", {grad}, {{"world", c.world}});
     VarPtr step = par(ts.i_step);
     VarPtr step1 = g.op("add_scalar", {step}, {{"value", 1.0}});
     AttrMap aa{{"lr", c.lr}, {"beta1", c.beta1}, {"beta2", c.beta2}, {"eps", c.eps},
-               {"grad_scale", 1.0 / double(c.world)}, {"half", c.dtype == "f32" ? std::string("bf16") : c.dtype}};
+               {"grad_scale", 1.0 / double(c.world)}, {"half", c.dtype}};
     VarPtr up = g.op("adam_update_ex", {par(ts.i_params), gsh, par(ts.i_m), par(ts.i_v), step1}, aa);
     VarPtr np = g.get(up, 0), nm = g.get(up, 1), nv = g.get(up, 2), nh = g.get(up, 3);
     if (c.world > 1)
-      nh = g.op("all_gather", {nh}, {{"world", c.world}, {"shape", std::to_string(ts.P_pad)}});
+      nh = g.op("all_gather", {nh}, {{"world", c.world}, {"shape", full_shape}});
     rets.insert(rets.end(), {np, nm, nv, step1});
     ts.state_binding.push_back({1, ts.i_params});
     ts.state_binding.push_back({2, ts.i_m});
     ts.state_binding.push_back({3, ts.i_v});
     ts.state_binding.push_back({4, ts.i_step});
-    if (amp) {
+    if (copy) {
       rets.push_back(nh);
       ts.state_binding.push_back({5, ts.i_p16});
     }
