@@ -37,6 +37,7 @@ struct GemmArgs {
   const void* aux = nullptr;   // same layout as C (ldc, batch strides), aux_dtype
   int aux_dtype = TCB_F32;
   void* aux_out = nullptr;     // pre-activation store, same layout/dtype as C
+  int force_bn = 0, force_cg = 0;  // tcgen05 tile override (tests / tuning); 0 = cost model
 };
 
 // Launch helpers (defined in the .cu files)

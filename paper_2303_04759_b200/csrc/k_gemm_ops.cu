@@ -42,6 +42,12 @@ static GemmArgs gemm2d(const Spec& A, const Spec& B, int ta, int tb, const Spec&
   return g;
 }
 
+// optional tile override: attrs tc_bn / tc_cg (parity tests cover every variant)
+static void tile_attrs(GemmArgs& g, const Plan& p) {
+  g.force_bn = int(p.attrs.i("tc_bn", 0));
+  g.force_cg = int(p.attrs.i("tc_cg", 0));
+}
+
 static void b_matmul(Plan& p) {
   check_arity(p, 2, 2, 1, 1);
   GemmArgs g = gemm2d(p.in[0], p.in[1], 0, 0, p.out[0], "matmul");
@@ -60,6 +66,7 @@ static void b_matmul_t(Plan& p) {
   check_arity(p, 2, 2, 1, 1);
   GemmArgs g = gemm2d(p.in[0], p.in[1], int(p.attrs.i("ta", 0)), int(p.attrs.i("tb", 0)), p.out[0],
                       "matmul_t");
+  tile_attrs(g, p);
   g.alpha = float(p.attrs.f("alpha", 1.0));
   const bool exact = want_exact(p);
   p.run = [g, exact](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) mutable {
@@ -74,6 +81,7 @@ TCB_REGISTER("matmul_t", b_matmul_t);
 static void b_linear(Plan& p) {
   check_arity(p, 3, 3, 1, 2);
   GemmArgs g = gemm2d(p.in[0], p.in[1], 0, int(p.attrs.i("tw", 0)), p.out[0], "linear");
+  tile_attrs(g, p);
   require(p.in[2].numel() == g.N, "linear: bias must have N elements");
   g.bias_dtype = p.in[2].dtype;
   g.act = parse_act(p.attrs.s("act", "none"));
@@ -96,6 +104,7 @@ static void b_matmul_dact(Plan& p) {
   check_arity(p, 3, 3, 1, 1);
   GemmArgs g = gemm2d(p.in[0], p.in[1], int(p.attrs.i("ta", 0)), int(p.attrs.i("tb", 0)), p.out[0],
                       "matmul_dact");
+  tile_attrs(g, p);
   g.dact = parse_act(p.attrs.s("act", "none"));
   require(same_shape(p.in[2], p.out[0]), "matmul_dact: aux must have the output's shape");
   g.aux_dtype = p.in[2].dtype;
@@ -136,6 +145,7 @@ static void b_batch_matmul(Plan& p) {
   g.ldc = g.N;
   g.c_dtype = C.dtype;
   g.alpha = float(p.attrs.f("alpha", 1.0));
+  tile_attrs(g, p);
   const bool exact = want_exact(p);
   p.run = [g, exact](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) mutable {
     g.a.ptr = in[0].ptr;

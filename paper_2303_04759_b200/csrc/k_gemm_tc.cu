@@ -1,15 +1,24 @@
 // k_gemm_tc.cu -- bf16/f16 tensor-core GEMM for sm_100a: tcgen05.mma with the
-// accumulator in TMEM, operands staged by TMA (SWIZZLE_128B), warp-specialised
-// and persistent.
+// accumulator in TMEM, operands staged by TMA (SWIZZLE_128B), warp-specialised,
+// persistent, optionally on a CTA pair (cta_group::2).
 //
-//   warp 0      TMA producer (one elected lane): A/B k-blocks into a STAGES-deep
-//               smem ring, mbarrier full/empty handshake
-//   warp 1      MMA issuer (one lane): tcgen05.mma.cta_group::1.kind::f16,
-//               128 x BN x 16 per instruction, fp32 accumulate in TMEM;
+//   warp 0      TMA producer (one lane): A/B k-blocks into a STAGES-deep smem
+//               ring, mbarrier full/empty handshake
+//   warp 1      MMA issuer (one lane, leader CTA only): tcgen05.mma kind::f16,
+//               (128*CG) x BN x 16 per instruction, fp32 accumulate in TMEM;
 //               tcgen05.commit frees smem stages / publishes finished tiles
 //   warp 2      TMEM allocator (2 x BN columns: double-buffered accumulator)
-//   warps 4-7   epilogue: tcgen05.ld 32x32b.x32 -> alpha, bias, act'(aux),
-//               pre-activation store, act -> one rounding into C's dtype
+//   warps 4-11  epilogue: tcgen05.ld 32x32b.x32 -> alpha, bias, act'(aux),
+//               pre-activation, act -> bf16/f32 into a swizzled smem box ->
+//               TMA store (cp.async.bulk.tensor, bulk_group); the act'(aux)
+//               operand arrives by TMA too, one chunk ahead
+//
+// CG = 2: a cluster of two CTAs on one TPC computes a 256 x BN tile with
+// M=256 MMAs issued by the leader.  Each CTA loads its own 128 rows of A and
+// half (BN/2 rows) of B, so every byte a CTA stages feeds twice the MMA work of
+// the 1-CTA kernel (smem/L2 traffic per FLOP halves).  Both CTAs' TMA bytes
+// land on the leader's full barrier; MMA commits are multicast to both CTAs;
+// both epilogues release the accumulator on the leader's tmem-empty barrier.
 //
 // Operands may be K-major or MN-major (A: ta, B: tb), which absorbs the
 // reference's `transpose` ops into the TMA/UMMA descriptors.
@@ -23,23 +32,35 @@
 
 namespace tcb {
 
-constexpr int TC_BM = 128;
-constexpr int TC_BK = 64;  // 64 bf16 = 128 B = one SWIZZLE_128B atom row
+constexpr int TC_BM = 128;  // accumulator rows per CTA
+constexpr int TC_BK = 64;   // 64 bf16 = 128 B = one SWIZZLE_128B atom row
+constexpr int TC_EPI_WARPS = 16;                      // 4 per TMEM lane quarter
+constexpr int TC_THREADS = 128 + 32 * TC_EPI_WARPS;  // warps 0-3: TMA, MMA, TMEM, spare
+constexpr int TC_EW = 16;                             // epilogue chunk width (columns)
+constexpr int TC_SLOT = 32 * TC_EW * 4;               // per-warp output slot: f32 box or (y, u) 16-bit boxes
+constexpr int TC_AUX_SLOT = 32 * TC_EW * 2;           // per-warp act'(aux) slot (16-bit)
 
-template <int BN>
+template <int BN, int CG, bool AUX>
 struct TcCfg {
-  static constexpr int STAGES = BN == 256 ? 4 : BN == 192 ? 5 : 6;
-  static constexpr int A_BYTES = TC_BM * TC_BK * 2;  // 16 KB
-  static constexpr int B_BYTES = BN * TC_BK * 2;
+  static constexpr int B_ROWS = BN / CG;  // B rows (N) staged by each CTA
+  static constexpr int A_BYTES = TC_BM * TC_BK * 2;
+  static constexpr int B_BYTES = B_ROWS * TC_BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int TMEM_COLS = 2 * BN <= 256 ? 256 : 512;  // power of two >= 2 accumulators
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int EPI_BYTES = TC_EPI_WARPS * 2 * TC_SLOT + (AUX ? TC_EPI_WARPS * 2 * TC_AUX_SLOT : 0);
+  static constexpr int BIAS_BYTES = TC_EPI_WARPS * ((BN / TC_EW + TC_EPI_WARPS / 4 - 1) / (TC_EPI_WARPS / 4)) * TC_EW * 4;
+  static constexpr int BAR_BYTES = 512;
+  static constexpr int BUDGET = 227 * 1024 - 1024 - BAR_BYTES - EPI_BYTES - BIAS_BYTES;
+  static constexpr int STAGES = BUDGET / STAGE_BYTES > 8 ? 8 : BUDGET / STAGE_BYTES;
+  static constexpr int TMEM_COLS = 2 * BN <= 256 ? 256 : 512;
+  static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + EPI_BYTES + BIAS_BYTES + BAR_BYTES;
+  static_assert(STAGES >= 2, "smem budget");
+  static_assert(CG == 1 || (BN / 2) % 16 == 0, "cta pair splits B");
 };
 
 struct TcParams {
   int64_t M, N, K, Z, Z2;
   int ta, tb;
-  int m_blocks, n_blocks, k_blocks;
+  int m_blocks, n_blocks, k_blocks;  // m_blocks counts (128*CG)-row blocks
   int64_t num_tiles;
   uint32_t idesc;
   // epilogue
@@ -53,23 +74,40 @@ struct TcParams {
   const void* aux;
   int aux_dtype;
   void* aux_out;
-  int c_vec_ok;  // 16-byte aligned rows
+  int tma_epi;   // 1: smem + TMA-store epilogue (tensor maps valid); 0: direct stores
+  int c_vec_ok;  // direct path: 16-byte aligned rows
 };
 
 // ------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// shared::cluster address of the same smem offset in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
 }
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(bytes)
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
@@ -80,32 +118,72 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
-__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
-                                            int c1, int c2, int c3) {
-  asm volatile(
-      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
-      : "memory");
+// TMA load into this CTA's smem, completion on an mbarrier given as a
+// shared::cluster address (the leader's barrier for the peer CTA of a pair)
+template <int CG>
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint32_t bar, int c0, int c1, int c2,
+                                            int c3) {
+  if constexpr (CG == 2) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar)
+        : "memory");
+  } else {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar)
+        : "memory");
+  }
 }
-__device__ __forceinline__ void tc_fence_before() {
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-}
-__device__ __forceinline__ void tc_fence_after() {
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-}
-__device__ __forceinline__ void tc_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                   smem_u32(bar))
+__device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, const void* src, int c0, int c1, int c2,
+                                             int c3) {
+  asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
                : "memory");
 }
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+template <int CG>
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  if constexpr (CG == 2) {
+    asm volatile(
+        "{\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\t"
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n\t}" ::"r"(
+            smem_u32(bar))
+        : "memory");
+  } else {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+  }
+}
+template <int CG>
 __device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                        uint32_t accum) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
+  if constexpr (CG == 2) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
+  }
 }
 // UMMA shared-memory descriptor, SWIZZLE_128B, version 1 (sm_100)
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
@@ -143,103 +221,165 @@ __device__ __forceinline__ void decode_tile(const TcParams& P, int64_t t, int& z
   nb = int(r - int64_t(mb) * P.n_blocks);
 }
 
-// Store 32 consecutive f32 values of one row into dst (dtype dt).  Every loop
-// is unrolled with compile-time indices so v[] stays in registers (a runtime
-// trip count here made ptxas spill the whole array to local memory).
-__device__ __forceinline__ void store_row32(void* dst, int dt, int64_t base, const float (&v)[32], bool vec,
-                                            int nvalid) {
+// ------------------------------------------------------------ epilogue math
+// The epilogue works on boxes of 32 rows (one TMEM lane quarter, lane = row)
+// x TC_EW columns.
+template <int W>
+__device__ __forceinline__ void apply_act(int act, float (&v)[W]) {
+  switch (act) {
+    case ACT_RELU:
+#pragma unroll
+      for (int j = 0; j < W; ++j) v[j] = v[j] > 0.0f ? v[j] : 0.0f;
+      break;
+    case ACT_TANH:
+#pragma unroll
+      for (int j = 0; j < W; ++j) v[j] = tanhf(v[j]);
+      break;
+    case ACT_GELU:
+#pragma unroll
+      for (int j = 0; j < W; ++j) v[j] = gelu_f(v[j]);
+      break;
+    default:
+      break;
+  }
+}
+template <int W>
+__device__ __forceinline__ void apply_dact(int act, float (&v)[W], const float (&a)[W]) {
+  switch (act) {
+    case ACT_RELU:
+#pragma unroll
+      for (int j = 0; j < W; ++j) v[j] *= a[j] > 0.0f ? 1.0f : 0.0f;
+      break;
+    case ACT_TANH:
+#pragma unroll
+      for (int j = 0; j < W; ++j) v[j] *= __fsub_rn(1.0f, __fmul_rn(a[j], a[j]));
+      break;
+    case ACT_GELU:
+#pragma unroll
+      for (int j = 0; j < W; ++j) v[j] *= gelu_grad_f(a[j]);
+      break;
+    default:
+      break;
+  }
+}
+
+__device__ __forceinline__ uint32_t pack2(float a, float b, int dt) {
+  if (dt == TCB_BF16) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h);
+  }
+  __half2 h = __floats2half2_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+__device__ __forceinline__ void unpack2(uint32_t w, int dt, float& a, float& b) {
+  if (dt == TCB_BF16) {
+    a = __uint_as_float(w << 16);
+    b = __uint_as_float(w & 0xffff0000u);
+  } else {
+    float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w));
+    a = f.x;
+    b = f.y;
+  }
+}
+// Staging boxes: one row per lane, 16-byte granules XOR-swizzled exactly as
+// TMA's SWIZZLE_{32,64,128}B (granule ^= row bits above the row size), so
+// the st.shared are bank-conflict free and the TMA store un-swizzles.
+template <int W>
+struct Box {
+  static constexpr int ROW16 = W * 2;  // bytes per row, 16-bit elements
+  static constexpr int ROW32 = W * 4;  // bytes per row, f32
+  static __device__ __forceinline__ int sw(int row, int g, int row_bytes) {
+    // granule index bits [4, 4+log2(row_bytes/16)) ^= address bits [7, ...)
+    const int ng = row_bytes / 16;
+    return (g ^ ((row * row_bytes >> 7) & (ng - 1)));
+  }
+};
+template <int W>
+__device__ __forceinline__ void stage_row(uint8_t* box, int lane, int dt, const float (&v)[W]) {
   if (dt == TCB_F32) {
-    float* o = static_cast<float*>(dst) + base;
-    if (vec) {
+    constexpr int RB = W * 4;
 #pragma unroll
-      for (int j = 0; j < 32; j += 4) *reinterpret_cast<float4*>(o + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-    } else {
-#pragma unroll
-      for (int j = 0; j < 32; ++j)
-        if (j < nvalid) o[j] = v[j];
-    }
-  } else if (dt == TCB_BF16) {
-    __nv_bfloat16* o = static_cast<__nv_bfloat16*>(dst) + base;
-    if (vec) {
-#pragma unroll
-      for (int j = 0; j < 32; j += 8) {
-        uint4 q;
-        __nv_bfloat162 h0 = __floats2bfloat162_rn(v[j], v[j + 1]);
-        __nv_bfloat162 h1 = __floats2bfloat162_rn(v[j + 2], v[j + 3]);
-        __nv_bfloat162 h2 = __floats2bfloat162_rn(v[j + 4], v[j + 5]);
-        __nv_bfloat162 h3 = __floats2bfloat162_rn(v[j + 6], v[j + 7]);
-        q.x = *reinterpret_cast<uint32_t*>(&h0);
-        q.y = *reinterpret_cast<uint32_t*>(&h1);
-        q.z = *reinterpret_cast<uint32_t*>(&h2);
-        q.w = *reinterpret_cast<uint32_t*>(&h3);
-        *reinterpret_cast<uint4*>(o + j) = q;
-      }
-    } else {
-#pragma unroll
-      for (int j = 0; j < 32; ++j)
-        if (j < nvalid) o[j] = __float2bfloat16_rn(v[j]);
+    for (int g = 0; g < RB / 16; ++g) {
+      float4 q = make_float4(v[4 * g], v[4 * g + 1], v[4 * g + 2], v[4 * g + 3]);
+      *reinterpret_cast<float4*>(box + lane * RB + (Box<W>::sw(lane, g, RB) << 4)) = q;
     }
   } else {
-    __half* o = static_cast<__half*>(dst) + base;
+    constexpr int RB = W * 2;
 #pragma unroll
-    for (int j = 0; j < 32; ++j)
-      if (j < nvalid) o[j] = __float2half_rn(v[j]);
-  }
-}
-
-// 32 consecutive output columns of one row: epilogue + store
-__device__ __forceinline__ void epi_store32(const TcParams& P, const uint32_t (&r)[32], int64_t m, int64_t n0,
-                                            int64_t coff) {
-  float v[32];
-#pragma unroll
-  for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) * P.alpha;
-  const int64_t base = coff + m * P.ldc + n0;
-  const int nvalid = int(P.N - n0 < 32 ? P.N - n0 : 32);
-  if (P.bias) {
-    if (P.bias_dtype == TCB_F32) {
-      const float* b = static_cast<const float*>(P.bias) + n0;
-#pragma unroll
-      for (int j = 0; j < 32; ++j)
-        if (j < nvalid) v[j] += __ldg(b + j);
-    } else {
-#pragma unroll
-      for (int j = 0; j < 32; ++j)
-        if (j < nvalid) v[j] += ld_e(P.bias, P.bias_dtype, n0 + j);
+    for (int g = 0; g < RB / 16; ++g) {
+      uint4 q;
+      q.x = pack2(v[8 * g], v[8 * g + 1], dt);
+      q.y = pack2(v[8 * g + 2], v[8 * g + 3], dt);
+      q.z = pack2(v[8 * g + 4], v[8 * g + 5], dt);
+      q.w = pack2(v[8 * g + 6], v[8 * g + 7], dt);
+      *reinterpret_cast<uint4*>(box + lane * RB + (Box<W>::sw(lane, g, RB) << 4)) = q;
     }
   }
-  if (P.dact != ACT_NONE) {
+}
+template <int W>
+__device__ __forceinline__ void unstage_row16(const uint8_t* box, int lane, int dt, float (&a)[W]) {
+  constexpr int RB = W * 2;
 #pragma unroll
-    for (int j = 0; j < 32; ++j)
-      if (j < nvalid) v[j] *= dact_f(P.dact, ld_e(P.aux, P.aux_dtype, base + j));
+  for (int g = 0; g < RB / 16; ++g) {
+    uint4 q = *reinterpret_cast<const uint4*>(box + lane * RB + (Box<W>::sw(lane, g, RB) << 4));
+    unpack2(q.x, dt, a[8 * g], a[8 * g + 1]);
+    unpack2(q.y, dt, a[8 * g + 2], a[8 * g + 3]);
+    unpack2(q.z, dt, a[8 * g + 4], a[8 * g + 5]);
+    unpack2(q.w, dt, a[8 * g + 6], a[8 * g + 7]);
   }
-  const bool vec = P.c_vec_ok && nvalid == 32;
-  if (P.aux_out) store_row32(P.aux_out, P.c_dtype, base, v, vec, nvalid);  // pre-activation u
-  if (P.act != ACT_NONE) {
-#pragma unroll
-    for (int j = 0; j < 32; ++j) v[j] = act_f(P.act, v[j]);
-  }
-  store_row32(P.c, P.c_dtype, base, v, vec, nvalid);
 }
 
-constexpr int TC_THREADS = 384;  // warps 0-3: TMA, MMA, TMEM alloc, spare; 4-11: epilogue
+// Direct-store fallback (C or aux not TMA-able): W consecutive values of one
+// row, scalar stores with a tail guard.
+template <int W>
+__device__ __forceinline__ void store_row(void* dst, int dt, int64_t base, const float (&v)[W], int nvalid) {
+#pragma unroll
+  for (int j = 0; j < W; ++j) {
+    if (j < nvalid) {
+      if (dt == TCB_F32) static_cast<float*>(dst)[base + j] = v[j];
+      else if (dt == TCB_BF16) static_cast<__nv_bfloat16*>(dst)[base + j] = __float2bfloat16_rn(v[j]);
+      else static_cast<__half*>(dst)[base + j] = __float2half_rn(v[j]);
+    }
+  }
+}
 
-template <int BN>
+#define TMEM_LD16(taddr, r)                                                                      \
+  asm volatile(                                                                                  \
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"   \
+      "%14,%15}, [%16];"                                                                         \
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),      \
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),  \
+        "=r"(r[14]), "=r"(r[15])                                                                 \
+      : "r"(taddr))
+
+struct EpiMaps {
+  CUtensorMap c, u, aux;
+};
+
+template <int BN, int CG, bool AUX>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-              const TcParams P) {
-  using C = TcCfg<BN>;
+              const __grid_constant__ EpiMaps EM, const TcParams P) {
+  using C = TcCfg<BN, CG, AUX>;
+  constexpr int W = TC_EW;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + C::STAGES * C::A_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint8_t* sEpi = smem + C::STAGES * C::STAGE_BYTES;        // epilogue warps x 2 output slots
+  uint8_t* sAux = sEpi + TC_EPI_WARPS * 2 * TC_SLOT;       // epilogue warps x 2 aux slots (AUX)
+  float* sBias = reinterpret_cast<float*>(sAux + (AUX ? TC_EPI_WARPS * 2 * TC_AUX_SLOT : 0));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sBias) + C::BIAS_BYTES);
   uint64_t* full = bars;
   uint64_t* empty = bars + C::STAGES;
   uint64_t* tfull = bars + 2 * C::STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* abar = tempty + 2;  // 2 per epilogue warp
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(abar + 2 * TC_EPI_WARPS);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;
+  const int64_t cl_id = blockIdx.x / CG, n_cl = gridDim.x / CG;
 
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
@@ -252,50 +392,59 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], TC_THREADS - 128);
+      mbar_init(&tempty[s], CG * TC_EPI_WARPS);
     }
+    for (int s = 0; s < 2 * TC_EPI_WARPS; ++s) mbar_init(&abar[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(tmem_slot)),
-                 "r"(C::TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if constexpr (CG == 2) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(C::TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(C::TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) cluster_sync();
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
-    // ===================== TMA producer =====================
+    // ===================== TMA producer (both CTAs) =====================
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int64_t t = blockIdx.x; t < P.num_tiles; t += gridDim.x) {
+      for (int64_t t = cl_id; t < P.num_tiles; t += n_cl) {
         int z, mb, nb;
         decode_tile(P, t, z, mb, nb);
         const int z1 = int(z / P.Z2), z2 = int(z % P.Z2);
-        const int m0 = mb * TC_BM, n0 = nb * BN;
+        const int m0 = mb * (TC_BM * CG) + int(rank) * TC_BM;
+        const int n0 = nb * BN + int(rank) * C::B_ROWS;
         for (int kb = 0; kb < P.k_blocks; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_expect_tx(&full[stage], C::STAGE_BYTES);
+          // both CTAs' bytes complete on the leader's barrier
+          const uint32_t fb = CG == 2 ? mapa(smem_u32(&full[stage]), 0) : smem_u32(&full[stage]);
+          if (rank == 0) mbar_expect_tx(&full[stage], CG * C::STAGE_BYTES);
           uint8_t* a_dst = sA + stage * C::A_BYTES;
           uint8_t* b_dst = sB + stage * C::B_BYTES;
           const int k0 = kb * TC_BK;
           if (!P.ta) {
-            tma_load_4d(a_dst, &tmA, &full[stage], k0, m0, z2, z1);
+            tma_load_4d<CG>(a_dst, &tmA, fb, k0, m0, z2, z1);
           } else {
 #pragma unroll
-            for (int c = 0; c < TC_BM / 64; ++c)
-              tma_load_4d(a_dst + c * 8192, &tmA, &full[stage], m0 + c * 64, k0, z2, z1);
+            for (int c = 0; c < TC_BM / 64; ++c) tma_load_4d<CG>(a_dst + c * 8192, &tmA, fb, m0 + c * 64, k0, z2, z1);
           }
           if (P.tb) {
-            tma_load_4d(b_dst, &tmB, &full[stage], k0, n0, z2, z1);
+            tma_load_4d<CG>(b_dst, &tmB, fb, k0, n0, z2, z1);
           } else {
 #pragma unroll
-            for (int c = 0; c < BN / 64; ++c)
-              tma_load_4d(b_dst + c * 8192, &tmB, &full[stage], n0 + c * 64, k0, z2, z1);
+            for (int c = 0; c < C::B_ROWS / 64; ++c)
+              tma_load_4d<CG>(b_dst + c * 8192, &tmB, fb, n0 + c * 64, k0, z2, z1);
           }
           if (++stage == C::STAGES) {
             stage = 0;
@@ -305,13 +454,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    // ===================== MMA issuer =====================
-    if (lane == 0) {
+    // ===================== MMA issuer (leader CTA) =====================
+    if (lane == 0 && rank == 0) {
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int64_t t = blockIdx.x; t < P.num_tiles; t += gridDim.x) {
+      for (int64_t t = cl_id; t < P.num_tiles; t += n_cl) {
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + uint32_t(acc * BN);
@@ -325,19 +474,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             // K-major: +32 B per 16-element k step inside the 128 B swizzle row;
             // MN-major: +2048 B (16 k-rows of 128 B); LBO = 8 KB between 64-wide
             // MN chunks, SBO = 1 KB between 8-row swizzle atoms.
-            const uint64_t ad = P.ta ? umma_desc(a_addr + k * 2048, 8192, 1024)
-                                     : umma_desc(a_addr + k * 32, 16, 1024);
-            const uint64_t bd = P.tb ? umma_desc(b_addr + k * 32, 16, 1024)
-                                     : umma_desc(b_addr + k * 2048, 8192, 1024);
-            tc_mma(tmem_d, ad, bd, P.idesc, (kb | k) ? 1u : 0u);
+            const uint64_t ad = P.ta ? umma_desc(a_addr + k * 2048, 8192, 1024) : umma_desc(a_addr + k * 32, 16, 1024);
+            const uint64_t bd = P.tb ? umma_desc(b_addr + k * 32, 16, 1024) : umma_desc(b_addr + k * 2048, 8192, 1024);
+            tc_mma<CG>(tmem_d, ad, bd, P.idesc, (kb | k) ? 1u : 0u);
           }
-          tc_commit(&empty[stage]);
+          tc_commit<CG>(&empty[stage]);
           if (++stage == C::STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        tc_commit(&tfull[acc]);
+        tc_commit<CG>(&tfull[acc]);
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
@@ -345,52 +492,173 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       }
     }
   } else if (warp >= 4) {
-    // ===================== epilogue (8 warps) =====================
-    // warp w may only touch TMEM lanes 32*(w%4)..+31; the two warps sharing a
-    // lane quarter split the tile's 32-column chunks between them
+    // ===================== epilogue (TC_EPI_WARPS warps, both CTAs) =====================
+    // warp w may only touch TMEM lanes 32*(w%4)..+31 (its 32 rows); the warps
+    // sharing a lane quarter take every TC_EPI_SPLIT-th W-column chunk
+    constexpr int NCH = BN / W;
+    constexpr int SPLIT = TC_EPI_WARPS / 4;
+    constexpr int CPW = (NCH + SPLIT - 1) / SPLIT;  // chunks per warp per tile (max)
+    const int ew = warp - 4;
     const int q = warp & 3;
-    const int half = (warp - 4) >> 2;
-    const int row = q * 32 + lane;
+    const int sub = ew >> 2;
+    uint8_t* slots = sEpi + ew * 2 * TC_SLOT;
+    uint8_t* aslots = sAux + ew * 2 * TC_AUX_SLOT;
+    float* wbias = sBias + ew * CPW * W;
+    uint64_t* ab = abar + 2 * ew;
+    const uint32_t tempty_addr0 = CG == 2 ? mapa(smem_u32(&tempty[0]), 0) : smem_u32(&tempty[0]);
+    const bool has_aux = AUX && P.tma_epi && P.dact != ACT_NONE;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int64_t t = blockIdx.x; t < P.num_tiles; t += gridDim.x) {
+    uint32_t sidx = 0;    // output slot ring
+    uint32_t achunk = 0;  // aux chunk counter (slot = &1, phase = >>1 &1)
+    // aux prefetch cursor over the same (tile, chunk) order as the consumer
+    int64_t pt = cl_id;
+    int pc = sub;
+    uint32_t aissue = 0;
+    auto issue_next_aux = [&]() {
+      while (pt < P.num_tiles) {
+        int z, mb, nb;
+        decode_tile(P, pt, z, mb, nb);
+        const int64_t n0 = int64_t(nb) * BN + pc * W;
+        const int mrow = mb * (TC_BM * CG) + int(rank) * TC_BM + q * 32;
+        pc += SPLIT;
+        if (pc >= NCH) {
+          pc = sub;
+          pt += n_cl;
+        }
+        if (n0 >= P.N) continue;  // chunk skipped by the consumer too
+        if (lane == 0) {
+          uint64_t* bar = &ab[aissue & 1];
+          mbar_expect_tx(bar, 32 * W * 2);
+          asm volatile(
+              "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+              " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(aslots + (aissue & 1) * TC_AUX_SLOT)),
+              "l"(reinterpret_cast<uint64_t>(&EM.aux)), "r"(int(n0)), "r"(mrow), "r"(int(z % P.Z2)),
+              "r"(int(z / P.Z2)), "r"(smem_u32(bar))
+              : "memory");
+        }
+        ++aissue;
+        return;
+      }
+    };
+    if (has_aux) issue_next_aux();
+
+    for (int64_t t = cl_id; t < P.num_tiles; t += n_cl) {
       int z, mb, nb;
       decode_tile(P, t, z, mb, nb);
-      const int64_t coff = int64_t(z / P.Z2) * P.c_s1 + int64_t(z % P.Z2) * P.c_s2;
+      const int z1 = int(z / P.Z2), z2 = int(z % P.Z2);
+      const int64_t coff = int64_t(z1) * P.c_s1 + int64_t(z2) * P.c_s2;
+      const int mrow0 = mb * (TC_BM * CG) + int(rank) * TC_BM + q * 32;  // this warp's 32-row box
+      if (P.bias) {
+        // this warp's bias columns for the tile -> smem (read back as broadcasts)
+        __syncwarp();
+        for (int i = lane; i < CPW * W; i += 32) {
+          const int c = sub + (i / W) * SPLIT;
+          const int64_t n = int64_t(nb) * BN + int64_t(c) * W + (i % W);
+          wbias[i] = (c < NCH && n < P.N) ? ld_e(P.bias, P.bias_dtype, n) : 0.0f;
+        }
+        __syncwarp();
+      }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const int64_t m = int64_t(mb) * TC_BM + row;
+      const int64_t m = int64_t(mrow0) + lane;
 #pragma unroll 1
-      for (int c = half; c < BN / 32; c += 2) {
-        uint32_t r[32];
-        const uint32_t taddr = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * BN + c * 32);
-        TMEM_LD32(taddr, r);
+      for (int c = sub, ci = 0; c < NCH; c += SPLIT, ++ci) {
+        const int64_t n0 = int64_t(nb) * BN + c * W;
+        if (n0 >= P.N) continue;
+        uint32_t r[W];
+        const uint32_t taddr = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * BN + c * W);
+        if constexpr (W == 16) TMEM_LD16(taddr, r);
+        else TMEM_LD32(taddr, r);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        const int64_t n0 = int64_t(nb) * BN + c * 32;
-        if (m < P.M && n0 < P.N) epi_store32(P, r, m, n0, coff);
+        float v[W];
+        if (P.alpha != 1.0f) {
+#pragma unroll
+          for (int j = 0; j < W; ++j) v[j] = __uint_as_float(r[j]) * P.alpha;
+        } else {
+#pragma unroll
+          for (int j = 0; j < W; ++j) v[j] = __uint_as_float(r[j]);
+        }
+        if (P.bias) {
+          const float4* bb = reinterpret_cast<const float4*>(wbias + ci * W);
+#pragma unroll
+          for (int j = 0; j < W / 4; ++j) {
+            const float4 b4 = bb[j];
+            v[4 * j] += b4.x;
+            v[4 * j + 1] += b4.y;
+            v[4 * j + 2] += b4.z;
+            v[4 * j + 3] += b4.w;
+          }
+        }
+        if (P.tma_epi) {
+          if (has_aux) {
+            // this chunk's aux box was issued one chunk ago; prefetch the next
+            const uint32_t s = achunk & 1, ph = (achunk >> 1) & 1;
+            issue_next_aux();
+            mbar_wait(&ab[s], ph);
+            float a[W];
+            unstage_row16<W>(aslots + s * TC_AUX_SLOT, lane, P.aux_dtype, a);
+            apply_dact<W>(P.dact, v, a);
+            ++achunk;
+          }
+          uint8_t* slot = slots + sidx * TC_SLOT;
+          if (lane == 0) bulk_wait_read<1>();  // the store that last used this slot has read it
+          __syncwarp();
+          if (P.aux_out) stage_row<W>(slot + TC_SLOT / 2, lane, P.c_dtype, v);
+          apply_act<W>(P.act, v);
+          stage_row<W>(slot, lane, P.c_dtype, v);
+          fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_4d(&EM.c, slot, int(n0), mrow0, z2, z1);
+            if (P.aux_out) tma_store_4d(&EM.u, slot + TC_SLOT / 2, int(n0), mrow0, z2, z1);
+            bulk_commit();
+          }
+          sidx ^= 1;
+        } else if (m < P.M) {
+          const int nvalid = int(P.N - n0 < W ? P.N - n0 : W);
+          const int64_t base = coff + m * P.ldc + n0;
+          if (P.dact != ACT_NONE) {
+            float a[W];
+#pragma unroll
+            for (int j = 0; j < W; ++j) a[j] = j < nvalid ? ld_e(P.aux, P.aux_dtype, base + j) : 0.0f;
+            apply_dact<W>(P.dact, v, a);
+          }
+          if (P.aux_out) store_row<W>(P.aux_out, P.c_dtype, base, v, nvalid);
+          apply_act<W>(P.act, v);
+          store_row<W>(P.c, P.c_dtype, base, v, nvalid);
+        }
       }
+      // release the accumulator to the (leader's) MMA warp
       tc_fence_before();
-      mbar_arrive(&tempty[acc]);
+      __syncwarp();
+      if (lane == 0) {
+        if constexpr (CG == 2) mbar_arrive_cluster(tempty_addr0 + acc * 8);
+        else mbar_arrive(&tempty[acc]);
+      }
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
       }
     }
+    if (lane == 0) bulk_wait_all();
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) cluster_sync();
+  else __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                 "r"(C::TMEM_COLS));
+    if constexpr (CG == 2)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(C::TMEM_COLS));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(C::TMEM_COLS));
   }
 }
 
 // ------------------------------------------------------------- host side
-using PFN_encodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
-                                     const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
-                                     const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
-                                     CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+using PFN_encodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                     const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                     CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
 static PFN_encodeTiled get_encode() {
   static PFN_encodeTiled fn = nullptr;
@@ -406,27 +674,37 @@ static PFN_encodeTiled get_encode() {
   return fn;
 }
 
-// operand -> 4-D map {inner, outer, z2, z1}; box {64, box_outer, 1, 1}
-static CUtensorMap make_map(const GemmOperand& o, int dtype, int64_t inner, int64_t outer, int64_t Z2,
-                            int64_t Z1, uint32_t box_outer) {
+static CUtensorMapDataType map_dtype(int dt) {
+  return dt == TCB_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+         : dt == TCB_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
+                         : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+}
+
+// 4-D map {inner, outer, z2, z1} over a strided matrix family
+static CUtensorMap encode4(const void* ptr, int dt, int64_t inner, int64_t outer, int64_t Z2, int64_t Z1, int64_t ld,
+                           int64_t s2, int64_t s1, uint32_t box_inner, uint32_t box_outer, CUtensorMapSwizzle sw) {
   CUtensorMap map;
-  const int es = 2;
+  const int es = dtype_bytes(dt);
   cuuint64_t dims[4] = {cuuint64_t(inner), cuuint64_t(outer), cuuint64_t(Z2), cuuint64_t(Z1)};
   auto stride_or = [&](int64_t s, int64_t fallback) {
     int64_t v = s > 0 ? s : fallback;
     return cuuint64_t(((v * es + 15) / 16) * 16);
   };
-  const int64_t plane = o.ld * outer;
-  cuuint64_t strides[3] = {cuuint64_t(o.ld * es), stride_or(o.s2, plane), stride_or(o.s1, plane * Z2)};
-  cuuint32_t box[4] = {64, box_outer, 1, 1};
+  const int64_t plane = ld * outer;
+  cuuint64_t strides[3] = {cuuint64_t(ld * es), stride_or(s2, plane), stride_or(s1, plane * Z2)};
+  cuuint32_t box[4] = {box_inner, box_outer, 1, 1};
   cuuint32_t estr[4] = {1, 1, 1, 1};
-  CUresult r = get_encode()(&map, dtype == TCB_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
-                                                    : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
-                            4, const_cast<void*>(o.ptr), dims, strides, box, estr,
-                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUresult r = get_encode()(&map, map_dtype(dt), 4, const_cast<void*>(ptr), dims, strides, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) fail(TCB_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
   return map;
+}
+
+// operand -> 4-D map, box {64, box_outer}, SWIZZLE_128B
+static CUtensorMap make_map(const GemmOperand& o, int64_t inner, int64_t outer, int64_t Z2, int64_t Z1,
+                            uint32_t box_outer) {
+  return encode4(o.ptr, o.dtype, inner, outer, Z2, Z1, o.ld, o.s2, o.s1, 64, box_outer, CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
 bool gemm_tc_supported(const GemmArgs& g, std::string* why) {
@@ -446,12 +724,28 @@ bool gemm_tc_supported(const GemmArgs& g, std::string* why) {
   return true;
 }
 
-template <int BN>
-static void launch_bn(const GemmArgs& g, cudaStream_t s) {
-  using C = TcCfg<BN>;
+// Can C / aux_out / aux go through TMA boxes?  (16-byte aligned bases and
+// strides; aux only 16-bit)
+static bool epi_tma_ok(const GemmArgs& g) {
+  const int es = dtype_bytes(g.c_dtype);
+  auto al = [](const void* p) { return reinterpret_cast<uintptr_t>(p) % 16 == 0; };
+  if (!al(g.c) || (g.ldc * es) % 16 || (g.c_s1 * es) % 16 || (g.c_s2 * es) % 16) return false;
+  if (g.aux_out && !al(g.aux_out)) return false;
+  if (g.aux_out && g.c_dtype == TCB_F32) return false;  // y + u must fit one slot
+  if (g.dact != ACT_NONE) {
+    if (g.aux_dtype == TCB_F32 || !al(g.aux)) return false;
+    const int ea = dtype_bytes(g.aux_dtype);
+    if ((g.ldc * ea) % 16 || (g.c_s1 * ea) % 16 || (g.c_s2 * ea) % 16) return false;
+  }
+  return true;
+}
+
+template <int BN, int CG, bool AUX>
+static void launch_cfg(const GemmArgs& g, cudaStream_t s) {
+  using C = TcCfg<BN, CG, AUX>;
   static std::once_flag once;
   std::call_once(once, [] {
-    TCB_CUDA(cudaFuncSetAttribute(k_gemm_tc<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    TCB_CUDA(cudaFuncSetAttribute(k_gemm_tc<BN, CG, AUX>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
   });
   TcParams P{};
   P.M = g.M;
@@ -461,17 +755,17 @@ static void launch_bn(const GemmArgs& g, cudaStream_t s) {
   P.Z2 = g.Z2;
   P.ta = g.ta;
   P.tb = g.tb;
-  P.m_blocks = int((g.M + TC_BM - 1) / TC_BM);
+  P.m_blocks = int((g.M + TC_BM * CG - 1) / (TC_BM * CG));
   P.n_blocks = int((g.N + BN - 1) / BN);
   P.k_blocks = int((g.K + TC_BK - 1) / TC_BK);
   P.num_tiles = int64_t(P.m_blocks) * P.n_blocks * g.Z;
   const uint32_t fmt = g.a.dtype == TCB_BF16 ? 1u : 0u;
-  P.idesc = (1u << 4)                      // D format f32
-            | (fmt << 7) | (fmt << 10)     // A, B format
-            | (uint32_t(g.ta) << 15)       // A major: 1 = MN
-            | (uint32_t(!g.tb) << 16)      // B major: 1 = MN (B stored [K, N])
-            | (uint32_t(BN >> 3) << 17)    // N
-            | (uint32_t(TC_BM >> 4) << 24);  // M
+  P.idesc = (1u << 4)                           // D format f32
+            | (fmt << 7) | (fmt << 10)          // A, B format
+            | (uint32_t(g.ta) << 15)            // A major: 1 = MN
+            | (uint32_t(!g.tb) << 16)           // B major: 1 = MN (B stored [K, N])
+            | (uint32_t(BN >> 3) << 17)         // N
+            | (uint32_t((TC_BM * CG) >> 4) << 24);  // M
   P.c = g.c;
   P.ldc = g.ldc;
   P.c_s1 = g.c_s1;
@@ -489,42 +783,95 @@ static void launch_bn(const GemmArgs& g, cudaStream_t s) {
   P.c_vec_ok = (reinterpret_cast<uintptr_t>(g.c) % 16 == 0) && ((g.ldc * es) % 16 == 0) &&
                ((g.c_s1 * es) % 16 == 0) && ((g.c_s2 * es) % 16 == 0) &&
                (!g.aux_out || reinterpret_cast<uintptr_t>(g.aux_out) % 16 == 0);
+  P.tma_epi = epi_tma_ok(g) && (g.dact == ACT_NONE || AUX);
   const int64_t Z1 = (g.Z + g.Z2 - 1) / g.Z2;
-  CUtensorMap ta = g.ta ? make_map(g.a, g.a.dtype, g.M, g.K, g.Z2, Z1, 64)
-                        : make_map(g.a, g.a.dtype, g.K, g.M, g.Z2, Z1, TC_BM);
-  CUtensorMap tb = g.tb ? make_map(g.b, g.b.dtype, g.K, g.N, g.Z2, Z1, BN)
-                        : make_map(g.b, g.b.dtype, g.N, g.K, g.Z2, Z1, 64);
-  const int grid = int(P.num_tiles < kNumSMs ? P.num_tiles : kNumSMs);
-  k_gemm_tc<BN><<<grid, TC_THREADS, C::SMEM, s>>>(ta, tb, P);
+  CUtensorMap ta = g.ta ? make_map(g.a, g.M, g.K, g.Z2, Z1, 64) : make_map(g.a, g.K, g.M, g.Z2, Z1, TC_BM);
+  CUtensorMap tb = g.tb ? make_map(g.b, g.K, g.N, g.Z2, Z1, C::B_ROWS) : make_map(g.b, g.N, g.K, g.Z2, Z1, 64);
+  EpiMaps em;
+  std::memset(&em, 0, sizeof(em));
+  if (P.tma_epi) {
+    // boxes of 32 rows x TC_EW columns, swizzled by their row size (see stage_row)
+    auto sw = [](int row_bytes) {
+      return row_bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+             : row_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                               : CU_TENSOR_MAP_SWIZZLE_32B;
+    };
+    const CUtensorMapSwizzle csw = sw(TC_EW * dtype_bytes(g.c_dtype));
+    em.c = encode4(g.c, g.c_dtype, g.N, g.M, g.Z2, Z1, g.ldc, g.c_s2, g.c_s1, TC_EW, 32, csw);
+    if (g.aux_out) em.u = encode4(g.aux_out, g.c_dtype, g.N, g.M, g.Z2, Z1, g.ldc, g.c_s2, g.c_s1, TC_EW, 32, csw);
+    if (g.dact != ACT_NONE)
+      em.aux = encode4(g.aux, g.aux_dtype, g.N, g.M, g.Z2, Z1, g.ldc, g.c_s2, g.c_s1, TC_EW, 32, sw(TC_EW * 2));
+  }
+  int64_t units = P.num_tiles * CG;
+  int grid = int(units < kNumSMs ? units : kNumSMs);
+  grid = (grid / CG) * CG;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(unsigned(grid));
+  cfg.blockDim = dim3(TC_THREADS);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  TCB_CUDA(cudaLaunchKernelEx(&cfg, k_gemm_tc<BN, CG, AUX>, ta, tb, em, P));
+}
+
+// Tile configuration by a wave-quantised cost model:
+//   time ~ rounds * (128*CG rows x BN cols per unit) / eff(CG, BN)
+// rounds = ceil(units / concurrent units); a CTA pair is one unit of 74.
+// eff(.) is the relative mainloop efficiency of each tile shape (smem/L2 bytes
+// staged per MMA FLOP fall with BN and with the CTA pair).
+struct TcChoice {
+  int bn, cg;
+};
+static TcChoice choose(const GemmArgs& g) {
+  if (g.force_bn) return {g.force_bn, g.force_cg ? g.force_cg : 1};
+  struct Cand {
+    int bn, cg;
+    double eff;
+  };
+  const Cand cands[] = {{256, 2, 0.92}, {128, 2, 0.85}, {256, 1, 0.72}, {192, 1, 0.66}, {128, 1, 0.55}};
+  TcChoice best{128, 1};
+  double best_cost = 1e30;
+  for (const Cand& c : cands) {
+    if (c.bn > 128 && g.N <= 128) continue;
+    if (c.cg == 2 && g.M <= 128) continue;  // the pair's second CTA would only see padding
+    const int64_t mb = (g.M + 128 * c.cg - 1) / (128 * c.cg);
+    const int64_t nb = (g.N + c.bn - 1) / c.bn;
+    const int64_t units = mb * nb * g.Z;
+    const int64_t conc = kNumSMs / c.cg;
+    const double rounds = double((units + conc - 1) / conc);
+    const double cost = rounds * double(128 * c.cg) * double(c.bn) / c.eff / double(c.cg);
+    if (cost < best_cost - 1e-9) {
+      best_cost = cost;
+      best = {c.bn, c.cg};
+    }
+  }
+  return best;
 }
 
 void launch_gemm_tc(const GemmArgs& g, cudaStream_t s) {
   std::string why;
   if (!gemm_tc_supported(g, &why)) fail(TCB_ERR_UNIMPLEMENTED, "tcgen05 gemm: " + why);
-  // Tile width by a wave-quantised cost model: time ~ waves(BN) * BN / e(BN),
-  // where e(BN) is the measured mainloop efficiency of a 1-CTA 128xBN tile
-  // (smem-read bound at small BN: ~0.5 @128, ~0.66 @192, ~0.75 @256).
-  const int64_t mb = (g.M + TC_BM - 1) / TC_BM;
-  int best = 128;
-  double best_cost = 1e30;
-  const int cand[3] = {256, 192, 128};
-  const double eff[3] = {0.75, 0.66, 0.5};
-  for (int i = 0; i < 3; ++i) {
-    const int bn = cand[i];
-    if (bn > 128 && g.N <= 128) continue;
-    const int64_t nb = (g.N + bn - 1) / bn;
-    const int64_t tiles = mb * nb * g.Z;
-    const double waves = double((tiles + kNumSMs - 1) / kNumSMs);
-    // columns actually computed per n-block (tail blocks waste the remainder)
-    const double cost = waves * double(bn) / eff[i];
-    if (cost < best_cost - 1e-9) {
-      best_cost = cost;
-      best = bn;
-    }
+  const TcChoice c = choose(g);
+  const bool aux = g.dact != ACT_NONE;
+#define TC_CASE(BN_, CG_)                                  \
+  if (c.bn == BN_ && c.cg == CG_) {                        \
+    if (aux) launch_cfg<BN_, CG_, true>(g, s);             \
+    else launch_cfg<BN_, CG_, false>(g, s);                \
+    return;                                                \
   }
-  if (best == 256) launch_bn<256>(g, s);
-  else if (best == 192) launch_bn<192>(g, s);
-  else launch_bn<128>(g, s);
+  TC_CASE(256, 2)
+  TC_CASE(128, 2)
+  TC_CASE(256, 1)
+  TC_CASE(192, 1)
+  TC_CASE(128, 1)
+#undef TC_CASE
+  fail(TCB_ERR_TYPE, "tcgen05 gemm: unsupported forced tile config");
 }
 
 }  // namespace tcb

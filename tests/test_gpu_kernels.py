@@ -169,6 +169,42 @@ def test_matmul_t_tcgen05(mnk, ta, tb):
     assert rel_err(g[0], o[0]) < BF16_TOL
 
 
+TILES = [(256, 2), (128, 2), (256, 1), (192, 1), (128, 1)]
+
+
+@pytest.mark.parametrize("bn,cg", TILES)
+@pytest.mark.parametrize("ta,tb", [(0, 0), (0, 1), (1, 0), (1, 1)])
+@pytest.mark.parametrize("mnk", [(256, 256, 128), (520, 328, 200), (1000, 768, 320)])
+def test_gemm_tile_variants(mnk, ta, tb, bn, cg):
+    """Every tcgen05 tile configuration (1-CTA and CTA-pair, all operand
+    majors, ragged M/N/K tails) against the oracle, f32 and bf16 outputs."""
+    m, n, k = mnk
+    a = rn(k, m) if ta else rn(m, k)
+    b = rn(n, k) if tb else rn(k, n)
+    attrs = {"ta": ta, "tb": tb, "alpha": 0.5, "tc_bn": bn, "tc_cg": cg}
+    g, o = run_both("matmul_t", [(a, BF16), (b, BF16)], [((m, n), F32)], attrs)
+    assert rel_err(g[0], o[0]) < 1e-5, rel_err(g[0], o[0])
+    g, o = run_both("matmul_t", [(a, BF16), (b, BF16)], [((m, n), BF16)], attrs)
+    assert rel_err(g[0], o[0]) < BF16_TOL
+
+
+@pytest.mark.parametrize("bn,cg", TILES)
+def test_gemm_tile_variants_epilogues(bn, cg):
+    """bias + GeLU + saved pre-activation, and the fused act'(aux) dgrad
+    epilogue (aux arrives by TMA), for every tile configuration."""
+    m, k, n = 700, 256, 600
+    x, w, bias = rn(m, k), rn(k, n, lo=-0.1, hi=0.1), rn(n)
+    at = {"act": "gelu", "tc_bn": bn, "tc_cg": cg}
+    g, o = run_both("linear", [(x, BF16), (w, BF16), (bias, F32)], [((m, n), BF16), ((m, n), BF16)], at)
+    assert rel_err(g[0], o[0]) < BF16_TOL and rel_err(g[1], o[1]) < BF16_TOL
+    g, o = run_both("linear", [(x, BF16), (w, BF16), (bias, BF16)], [((m, n), BF16)], at)
+    assert rel_err(g[0], o[0]) < BF16_TOL
+    dy, w2, u = rn(m, k), rn(n, k), rn(m, n, lo=-3, hi=3)
+    g, o = run_both("matmul_dact", [(dy, BF16), (w2, BF16), (u, BF16)], [((m, n), BF16)],
+                    {"tb": 1, "act": "gelu", "tc_bn": bn, "tc_cg": cg})
+    assert rel_err(g[0], o[0]) < BF16_TOL
+
+
 def test_matmul_t_exact_flag_bit_exact():
     a, b = rn(70, 40), rn(40, 50)
     g, o = run_both("matmul_t", [(a, BF16), (b, BF16)], [((70, 50), BF16)], {"exact": 1})

@@ -28,12 +28,15 @@ SHAPES = [
 ]
 
 
-def run(name, op, M, K, N, ta, tb, out, iters):
+def run(name, op, M, K, N, ta, tb, out, iters, tile=None, cublas=True):
     a = torch.randn(K, M, device="cuda") if ta else torch.randn(M, K, device="cuda")
     b = torch.randn(N, K, device="cuda") if tb else torch.randn(K, N, device="cuda")
     a, b = a.to(torch.bfloat16).contiguous(), b.to(torch.bfloat16).contiguous()
     c = torch.empty(M, N, device="cuda", dtype=torch.float32 if out == F32 else torch.bfloat16)
-    plan = Plan(op, [(tuple(a.shape), BF16), (tuple(b.shape), BF16)], [((M, N), out)], {"ta": ta, "tb": tb})
+    at = {"ta": ta, "tb": tb}
+    if tile:
+        at.update({"tc_bn": tile[0], "tc_cg": tile[1]})
+    plan = Plan(op, [(tuple(a.shape), BF16), (tuple(b.shape), BF16)], [((M, N), out)], at)
     s = torch.cuda.current_stream().cuda_stream
     for _ in range(3):
         plan.launch([a.data_ptr(), b.data_ptr()], [c.data_ptr()], s)
@@ -46,7 +49,47 @@ def run(name, op, M, K, N, ta, tb, out, iters):
     torch.cuda.synchronize()
     us = e0.elapsed_time(e1) * 1000 / iters
     tf = 2.0 * M * N * K / (us * 1e-6) / 1e12
-    return {"name": name, "M": M, "K": K, "N": N, "ta": ta, "tb": tb, "us": round(us, 2), "tflops": round(tf, 1)}
+    if not cublas:
+        return {"name": name, "tile": tile, "us": round(us, 2), "tflops": round(tf, 1)}
+    # cuBLAS yardstick (out-of-band only): same operands, bf16 out
+    at = a.t() if ta else a
+    bt = b.t() if tb else b
+    for _ in range(3):
+        torch.matmul(at, bt)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(iters):
+        torch.matmul(at, bt)
+    e1.record()
+    torch.cuda.synchronize()
+    ucb = e0.elapsed_time(e1) * 1000 / iters
+    return {"name": name, "M": M, "K": K, "N": N, "ta": ta, "tb": tb, "us": round(us, 2), "tflops": round(tf, 1),
+            "cublas_us": round(ucb, 2), "cublas_tflops": round(2.0 * M * N * K / (ucb * 1e-6) / 1e12, 1)}
+
+
+def sweep(iters):
+    """Every tile configuration on every BERT-base shape (cost-model calibration)."""
+    for sh in SHAPES[:-1]:
+        for tile in [(256, 2), (128, 2), (256, 1), (192, 1), (128, 1)]:
+            print(json.dumps(run(*sh, iters=iters, tile=tile, cublas=False)), flush=True)
+
+
+def linear_gelu(iters, M=4096, K=768, N=3072):
+    """FFN1 forward as the step runs it: bias + GeLU + saved pre-activation."""
+    x = torch.randn(M, K, device="cuda").to(torch.bfloat16)
+    w = (0.02 * torch.randn(K, N, device="cuda")).to(torch.bfloat16)
+    b = torch.zeros(N, device="cuda")
+    y = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    u = torch.empty_like(y)
+    res = []
+    for act, save in (("gelu", 1), ("none", 0)):
+        outs = [((M, N), BF16), ((M, N), BF16)] if save else [((M, N), BF16)]
+        plan = Plan("linear", [((M, K), BF16), ((K, N), BF16), ((N,), F32)], outs, {"act": act, "save_preact": save})
+        us = time_plan(plan, [x.data_ptr(), w.data_ptr(), b.data_ptr()],
+                       [y.data_ptr(), u.data_ptr()][:len(outs)], iters)
+        res.append({"name": f"linear_{act}_{M}x{K}x{N}", "us": round(us, 2),
+                    "tflops": round(2.0 * M * N * K / us / 1e6, 1)})
+    return res
 
 
 def time_plan(plan, ins, outs, iters):
@@ -86,7 +129,16 @@ def main():
     ap.add_argument("--only", type=int, default=-1)
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--attention", action="store_true")
+    ap.add_argument("--linear", action="store_true")
+    ap.add_argument("--sweep", action="store_true")
     args = ap.parse_args()
+    if args.sweep:
+        sweep(args.iters)
+        return
+    if args.linear:
+        for r in linear_gelu(args.iters):
+            print(json.dumps(r), flush=True)
+        return
     if args.attention:
         for r in attention(args.iters):
             print(json.dumps(r), flush=True)
