@@ -38,6 +38,20 @@ struct GemmArgs {
   int aux_dtype = TCB_F32;
   void* aux_out = nullptr;     // pre-activation store, same layout/dtype as C
   int force_bn = 0, force_cg = 0;  // tcgen05 tile override (tests / tuning); 0 = cost model
+  int force_splits = 0;            // split-K ways (needs ws / ws_cnt from gemm_prepare)
+  float* ws = nullptr;             // split-K partial accumulators
+  int* ws_cnt = nullptr;           // split-K arrival counters (zeroed, self re-arming)
+  void* trace = nullptr;
+  int no_tma_epi = 0;              // force the direct-store epilogue (tooling)
+  int allow_split = 0;             // let the cost model pick split-K           // optional per-CTA timeline buffer (8 x u64 per CTA)
+};
+
+struct TcChoice {
+  int bn, cg, splits;
+};
+// scratch a prepared GEMM keeps alive (split-K partials and counters)
+struct GemmWs {
+  std::shared_ptr<Scratch> ws, cnt;
 };
 
 // Launch helpers (defined in the .cu files)
@@ -45,6 +59,11 @@ void launch_gemm_exact(const GemmArgs& g, cudaStream_t s);
 // returns false when the tensor-core path cannot take this problem
 bool gemm_tc_supported(const GemmArgs& g, std::string* why);
 void launch_gemm_tc(const GemmArgs& g, cudaStream_t s);
+// cost-model choice of tile shape / CTA pairing / split-K for a problem
+TcChoice gemm_tc_choose(const GemmArgs& g);
+// plan-time: freeze the tile choice and allocate split-K scratch (no-op for the
+// exact kernel).  Problems built at launch time skip this and never split.
+void gemm_prepare(GemmArgs& g, bool exact, GemmWs& keep);
 
 // Picks the kernel: tcgen05 for f16/bf16 operands unless exact is requested or
 // the shape is unsupported (then the exact SIMT kernel; never a CPU path).

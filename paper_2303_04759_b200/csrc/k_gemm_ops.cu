@@ -46,6 +46,9 @@ static GemmArgs gemm2d(const Spec& A, const Spec& B, int ta, int tb, const Spec&
 static void tile_attrs(GemmArgs& g, const Plan& p) {
   g.force_bn = int(p.attrs.i("tc_bn", 0));
   g.force_cg = int(p.attrs.i("tc_cg", 0));
+  g.force_splits = int(p.attrs.i("tc_splits", 0));
+  g.trace = reinterpret_cast<void*>(p.attrs.i("tc_trace", 0));  // tooling only
+  g.no_tma_epi = int(p.attrs.i("tc_notma", 0));
 }
 
 static void b_matmul(Plan& p) {
@@ -53,7 +56,9 @@ static void b_matmul(Plan& p) {
   GemmArgs g = gemm2d(p.in[0], p.in[1], 0, 0, p.out[0], "matmul");
   require(p.out[0].dtype == p.in[0].dtype, "matmul: output dtype must equal input dtype");
   const bool exact = want_exact(p);
-  p.run = [g, exact](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) mutable {
+  auto keep = std::make_shared<GemmWs>();
+  gemm_prepare(g, exact, *keep);
+  p.run = [g, exact, keep](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) mutable {
     g.a.ptr = in[0].ptr;
     g.b.ptr = in[1].ptr;
     g.c = out[0].ptr;
@@ -69,7 +74,9 @@ static void b_matmul_t(Plan& p) {
   tile_attrs(g, p);
   g.alpha = float(p.attrs.f("alpha", 1.0));
   const bool exact = want_exact(p);
-  p.run = [g, exact](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) mutable {
+  auto keep = std::make_shared<GemmWs>();
+  gemm_prepare(g, exact, *keep);
+  p.run = [g, exact, keep](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) mutable {
     g.a.ptr = in[0].ptr;
     g.b.ptr = in[1].ptr;
     g.c = out[0].ptr;
@@ -89,7 +96,9 @@ static void b_linear(Plan& p) {
                                 "linear: pre-activation output must match y");
   const bool exact = want_exact(p);
   const bool save = p.out.size() > 1;
-  p.run = [g, exact, save](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) mutable {
+  auto keep = std::make_shared<GemmWs>();
+  gemm_prepare(g, exact, *keep);
+  p.run = [g, exact, save, keep](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) mutable {
     g.a.ptr = in[0].ptr;
     g.b.ptr = in[1].ptr;
     g.bias = in[2].ptr;
@@ -109,7 +118,9 @@ static void b_matmul_dact(Plan& p) {
   require(same_shape(p.in[2], p.out[0]), "matmul_dact: aux must have the output's shape");
   g.aux_dtype = p.in[2].dtype;
   const bool exact = want_exact(p);
-  p.run = [g, exact](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) mutable {
+  auto keep = std::make_shared<GemmWs>();
+  gemm_prepare(g, exact, *keep);
+  p.run = [g, exact, keep](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) mutable {
     g.a.ptr = in[0].ptr;
     g.b.ptr = in[1].ptr;
     g.aux = in[2].ptr;
@@ -147,7 +158,9 @@ static void b_batch_matmul(Plan& p) {
   g.alpha = float(p.attrs.f("alpha", 1.0));
   tile_attrs(g, p);
   const bool exact = want_exact(p);
-  p.run = [g, exact](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) mutable {
+  auto keep = std::make_shared<GemmWs>();
+  gemm_prepare(g, exact, *keep);
+  p.run = [g, exact, keep](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) mutable {
     g.a.ptr = in[0].ptr;
     g.b.ptr = in[1].ptr;
     g.c = out[0].ptr;

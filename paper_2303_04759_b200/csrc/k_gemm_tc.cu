@@ -62,6 +62,14 @@ struct TcParams {
   int ta, tb;
   int m_blocks, n_blocks, k_blocks;  // m_blocks counts (128*CG)-row blocks
   int64_t num_tiles;
+  // split-K: unit u = split * num_tiles + tile covers k-blocks [split*kps, +kps);
+  // partial accumulators go to ws, the last split of a (tile, warp box) to
+  // arrive (ws_cnt) sums them in split order and runs the epilogue
+  int splits, kps;
+  int64_t num_units;
+  float* ws;
+  int* ws_cnt;
+  unsigned long long* trace;  // optional per-CTA timeline (tools/probe_gemm.py --trace)
   uint32_t idesc;
   // epilogue
   void* c;
@@ -81,6 +89,11 @@ struct TcParams {
 // ------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
 }
 __device__ __forceinline__ uint32_t cluster_ctarank() {
   uint32_t r;
@@ -380,6 +393,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;
   const int64_t cl_id = blockIdx.x / CG, n_cl = gridDim.x / CG;
+  unsigned long long* tr = P.trace ? P.trace + blockIdx.x * 8 : nullptr;
+  if (tr && threadIdx.x == 0) tr[0] = gtimer();
 
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
@@ -413,19 +428,23 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (tr && threadIdx.x == 0) tr[1] = gtimer();
 
   if (warp == 0) {
     // ===================== TMA producer (both CTAs) =====================
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int64_t t = cl_id; t < P.num_tiles; t += n_cl) {
+      for (int64_t u = cl_id; u < P.num_units; u += n_cl) {
+        const int64_t t = u % P.num_tiles;
+        const int kb0 = int(u / P.num_tiles) * P.kps;
+        const int kb1 = min(kb0 + P.kps, P.k_blocks);
         int z, mb, nb;
         decode_tile(P, t, z, mb, nb);
         const int z1 = int(z / P.Z2), z2 = int(z % P.Z2);
         const int m0 = mb * (TC_BM * CG) + int(rank) * TC_BM;
         const int n0 = nb * BN + int(rank) * C::B_ROWS;
-        for (int kb = 0; kb < P.k_blocks; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           // both CTAs' bytes complete on the leader's barrier
           const uint32_t fb = CG == 2 ? mapa(smem_u32(&full[stage]), 0) : smem_u32(&full[stage]);
@@ -460,13 +479,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int64_t t = cl_id; t < P.num_tiles; t += n_cl) {
+      for (int64_t u = cl_id; u < P.num_units; u += n_cl) {
+        const int kb0 = int(u / P.num_tiles) * P.kps;
+        const int kb1 = min(kb0 + P.kps, P.k_blocks);
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + uint32_t(acc * BN);
-        for (int kb = 0; kb < P.k_blocks; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
+          if (tr && u == cl_id && kb == kb0) tr[2] = gtimer();
           const uint32_t a_addr = smem_u32(sA + stage * C::A_BYTES);
           const uint32_t b_addr = smem_u32(sB + stage * C::B_BYTES);
 #pragma unroll
@@ -476,7 +498,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             // MN chunks, SBO = 1 KB between 8-row swizzle atoms.
             const uint64_t ad = P.ta ? umma_desc(a_addr + k * 2048, 8192, 1024) : umma_desc(a_addr + k * 32, 16, 1024);
             const uint64_t bd = P.tb ? umma_desc(b_addr + k * 32, 16, 1024) : umma_desc(b_addr + k * 2048, 8192, 1024);
-            tc_mma<CG>(tmem_d, ad, bd, P.idesc, (kb | k) ? 1u : 0u);
+            tc_mma<CG>(tmem_d, ad, bd, P.idesc, (kb > kb0 || k) ? 1u : 0u);
           }
           tc_commit<CG>(&empty[stage]);
           if (++stage == C::STAGES) {
@@ -485,6 +507,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           }
         }
         tc_commit<CG>(&tfull[acc]);
+        if (tr) tr[3] = gtimer();
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
@@ -516,9 +539,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     int pc = sub;
     uint32_t aissue = 0;
     auto issue_next_aux = [&]() {
-      while (pt < P.num_tiles) {
+      while (pt < P.num_units) {
         int z, mb, nb;
-        decode_tile(P, pt, z, mb, nb);
+        decode_tile(P, pt % P.num_tiles, z, mb, nb);
         const int64_t n0 = int64_t(nb) * BN + pc * W;
         const int mrow = mb * (TC_BM * CG) + int(rank) * TC_BM + q * 32;
         pc += SPLIT;
@@ -543,41 +566,20 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     };
     if (has_aux) issue_next_aux();
 
-    for (int64_t t = cl_id; t < P.num_tiles; t += n_cl) {
+    for (int64_t u = cl_id; u < P.num_units; u += n_cl) {
+      const int64_t t = u % P.num_tiles;
+      const int split = int(u / P.num_tiles);
       int z, mb, nb;
       decode_tile(P, t, z, mb, nb);
       const int z1 = int(z / P.Z2), z2 = int(z % P.Z2);
       const int64_t coff = int64_t(z1) * P.c_s1 + int64_t(z2) * P.c_s2;
       const int mrow0 = mb * (TC_BM * CG) + int(rank) * TC_BM + q * 32;  // this warp's 32-row box
-      if (P.bias) {
-        // this warp's bias columns for the tile -> smem (read back as broadcasts)
-        __syncwarp();
-        for (int i = lane; i < CPW * W; i += 32) {
-          const int c = sub + (i / W) * SPLIT;
-          const int64_t n = int64_t(nb) * BN + int64_t(c) * W + (i % W);
-          wbias[i] = (c < NCH && n < P.N) ? ld_e(P.bias, P.bias_dtype, n) : 0.0f;
-        }
-        __syncwarp();
-      }
-      mbar_wait(&tfull[acc], acc_phase);
-      tc_fence_after();
       const int64_t m = int64_t(mrow0) + lane;
-#pragma unroll 1
-      for (int c = sub, ci = 0; c < NCH; c += SPLIT, ++ci) {
-        const int64_t n0 = int64_t(nb) * BN + c * W;
-        if (n0 >= P.N) continue;
-        uint32_t r[W];
-        const uint32_t taddr = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * BN + c * W);
-        if constexpr (W == 16) TMEM_LD16(taddr, r);
-        else TMEM_LD32(taddr, r);
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        float v[W];
+      // finishes one W-column chunk: v holds the f32 accumulator row segment
+      auto finish = [&](float (&v)[W], int ci, int64_t n0) {
         if (P.alpha != 1.0f) {
 #pragma unroll
-          for (int j = 0; j < W; ++j) v[j] = __uint_as_float(r[j]) * P.alpha;
-        } else {
-#pragma unroll
-          for (int j = 0; j < W; ++j) v[j] = __uint_as_float(r[j]);
+          for (int j = 0; j < W; ++j) v[j] *= P.alpha;
         }
         if (P.bias) {
           const float4* bb = reinterpret_cast<const float4*>(wbias + ci * W);
@@ -628,7 +630,48 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           apply_act<W>(P.act, v);
           store_row<W>(P.c, P.c_dtype, base, v, nvalid);
         }
+      };
+      auto load_bias = [&]() {
+        // this warp's bias columns for the tile -> smem (read back as broadcasts)
+        __syncwarp();
+        for (int i = lane; i < CPW * W; i += 32) {
+          const int c = sub + (i / W) * SPLIT;
+          const int64_t n = int64_t(nb) * BN + int64_t(c) * W + (i % W);
+          wbias[i] = (c < NCH && n < P.N) ? ld_e(P.bias, P.bias_dtype, n) : 0.0f;
+        }
+        __syncwarp();
+      };
+      if (P.bias && P.splits == 1) load_bias();
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      if (tr && ew == 0 && u == cl_id) tr[4] = gtimer();
+      // partial-sum slot of this (tile, CTA, warp) box: [split][tile][rank][warp][chunk][lane][W]
+      const int64_t box = (t * CG + rank) * TC_EPI_WARPS + ew;
+      float* wsp = P.splits > 1 ? P.ws + (int64_t(split) * P.num_tiles * CG * TC_EPI_WARPS + box) * (CPW * 32 * W)
+                                : nullptr;
+#pragma unroll 1
+      for (int c = sub, ci = 0; c < NCH; c += SPLIT, ++ci) {
+        const int64_t n0 = int64_t(nb) * BN + c * W;
+        if (n0 >= P.N) continue;
+        uint32_t r[W];
+        const uint32_t taddr = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * BN + c * W);
+        if constexpr (W == 16) TMEM_LD16(taddr, r);
+        else TMEM_LD32(taddr, r);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (P.splits > 1) {
+          float4* dst = reinterpret_cast<float4*>(wsp + (ci * 32 + lane) * W);
+#pragma unroll
+          for (int j = 0; j < W / 4; ++j)
+            __stcg(dst + j, make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                                        __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3])));
+          continue;
+        }
+        float v[W];
+#pragma unroll
+        for (int j = 0; j < W; ++j) v[j] = __uint_as_float(r[j]);
+        finish(v, ci, n0);
       }
+      if (tr && ew == 0 && lane == 0 && u == cl_id) tr[6] = gtimer();
       // release the accumulator to the (leader's) MMA warp
       tc_fence_before();
       __syncwarp();
@@ -636,12 +679,49 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         if constexpr (CG == 2) mbar_arrive_cluster(tempty_addr0 + acc * 8);
         else mbar_arrive(&tempty[acc]);
       }
+      if (tr && ew == 0 && lane == 0 && u == cl_id) tr[7] = gtimer();
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
       }
+      if (P.splits > 1) {
+        // publish this split's partial box; the last split to arrive reduces
+        // all of them in split order (deterministic) and runs the epilogue
+        __threadfence();
+        __syncwarp();
+        int old = 0;
+        if (lane == 0) old = atomicAdd(P.ws_cnt + box, 1);
+        old = __shfl_sync(0xffffffffu, old, 0);
+        if (old == P.splits - 1) {
+          __threadfence();
+          if (P.bias) load_bias();
+#pragma unroll 1
+          for (int c = sub, ci = 0; c < NCH; c += SPLIT, ++ci) {
+            const int64_t n0 = int64_t(nb) * BN + c * W;
+            if (n0 >= P.N) continue;
+            float v[W];
+#pragma unroll
+            for (int j = 0; j < W; ++j) v[j] = 0.0f;
+            for (int sp = 0; sp < P.splits; ++sp) {
+              const float4* src = reinterpret_cast<const float4*>(
+                  P.ws + (int64_t(sp) * P.num_tiles * CG * TC_EPI_WARPS + box) * (CPW * 32 * W) + (ci * 32 + lane) * W);
+#pragma unroll
+              for (int j = 0; j < W / 4; ++j) {
+                const float4 x = __ldcg(src + j);
+                v[4 * j] += x.x;
+                v[4 * j + 1] += x.y;
+                v[4 * j + 2] += x.z;
+                v[4 * j + 3] += x.w;
+              }
+            }
+            finish(v, ci, n0);
+          }
+          if (lane == 0) P.ws_cnt[box] = 0;  // re-armed for the next launch
+        }
+      }
     }
     if (lane == 0) bulk_wait_all();
+    if (tr && ew == 0 && lane == 0) tr[5] = gtimer();
   }
   tc_fence_before();
   if constexpr (CG == 2) cluster_sync();
@@ -759,6 +839,13 @@ static void launch_cfg(const GemmArgs& g, cudaStream_t s) {
   P.n_blocks = int((g.N + BN - 1) / BN);
   P.k_blocks = int((g.K + TC_BK - 1) / TC_BK);
   P.num_tiles = int64_t(P.m_blocks) * P.n_blocks * g.Z;
+  P.splits = g.force_splits > 1 ? g.force_splits : 1;
+  P.kps = (P.k_blocks + P.splits - 1) / P.splits;
+  P.splits = (P.k_blocks + P.kps - 1) / P.kps;  // no empty splits
+  P.num_units = P.num_tiles * P.splits;
+  P.ws = g.ws;
+  P.ws_cnt = g.ws_cnt;
+  P.trace = reinterpret_cast<unsigned long long*>(g.trace);
   const uint32_t fmt = g.a.dtype == TCB_BF16 ? 1u : 0u;
   P.idesc = (1u << 4)                           // D format f32
             | (fmt << 7) | (fmt << 10)          // A, B format
@@ -783,7 +870,7 @@ static void launch_cfg(const GemmArgs& g, cudaStream_t s) {
   P.c_vec_ok = (reinterpret_cast<uintptr_t>(g.c) % 16 == 0) && ((g.ldc * es) % 16 == 0) &&
                ((g.c_s1 * es) % 16 == 0) && ((g.c_s2 * es) % 16 == 0) &&
                (!g.aux_out || reinterpret_cast<uintptr_t>(g.aux_out) % 16 == 0);
-  P.tma_epi = epi_tma_ok(g) && (g.dact == ACT_NONE || AUX);
+  P.tma_epi = epi_tma_ok(g) && (g.dact == ACT_NONE || AUX) && !g.no_tma_epi;
   const int64_t Z1 = (g.Z + g.Z2 - 1) / g.Z2;
   CUtensorMap ta = g.ta ? make_map(g.a, g.M, g.K, g.Z2, Z1, 64) : make_map(g.a, g.K, g.M, g.Z2, Z1, TC_BM);
   CUtensorMap tb = g.tb ? make_map(g.b, g.K, g.N, g.Z2, Z1, C::B_ROWS) : make_map(g.b, g.N, g.K, g.Z2, Z1, 64);
@@ -802,7 +889,7 @@ static void launch_cfg(const GemmArgs& g, cudaStream_t s) {
     if (g.dact != ACT_NONE)
       em.aux = encode4(g.aux, g.aux_dtype, g.N, g.M, g.Z2, Z1, g.ldc, g.c_s2, g.c_s1, TC_EW, 32, sw(TC_EW * 2));
   }
-  int64_t units = P.num_tiles * CG;
+  int64_t units = P.num_units * CG;
   int grid = int(units < kNumSMs ? units : kNumSMs);
   grid = (grid / CG) * CG;
   cudaLaunchConfig_t cfg = {};
@@ -820,45 +907,77 @@ static void launch_cfg(const GemmArgs& g, cudaStream_t s) {
   TCB_CUDA(cudaLaunchKernelEx(&cfg, k_gemm_tc<BN, CG, AUX>, ta, tb, em, P));
 }
 
-// Tile configuration by a wave-quantised cost model:
-//   time ~ rounds * (128*CG rows x BN cols per unit) / eff(CG, BN)
-// rounds = ceil(units / concurrent units); a CTA pair is one unit of 74.
-// eff(.) is the relative mainloop efficiency of each tile shape (smem/L2 bytes
-// staged per MMA FLOP fall with BN and with the CTA pair).
-struct TcChoice {
-  int bn, cg;
-};
-static TcChoice choose(const GemmArgs& g) {
-  if (g.force_bn) return {g.force_bn, g.force_cg ? g.force_cg : 1};
+// Tile configuration by a wave-quantised cost model (calibrated on the
+// BERT-base shapes, profiles/r01_gemm_tile_sweep.jsonl):
+//   time ~ rounds * (kps + K_FIX) * BN / eff(CG, BN)  (+ split-K reduction)
+// rounds = ceil(units / concurrent units), a CTA pair is one unit of 74;
+// K_FIX k-blocks model the per-unit fill/drain; eff(.) is the relative
+// mainloop throughput per SM of each tile shape.
+static TcChoice choose(const GemmArgs& g, bool allow_split) {
+  if (g.force_bn) return {g.force_bn, g.force_cg ? g.force_cg : 1, g.force_splits ? g.force_splits : 1};
   struct Cand {
     int bn, cg;
     double eff;
   };
-  const Cand cands[] = {{256, 2, 0.92}, {128, 2, 0.85}, {256, 1, 0.72}, {192, 1, 0.66}, {128, 1, 0.55}};
-  TcChoice best{128, 1};
+  const Cand cands[] = {{256, 2, 1.0}, {128, 2, 0.6}, {256, 1, 0.75}, {192, 1, 0.7}, {128, 1, 0.55}};
+  const int64_t kblocks = (g.K + TC_BK - 1) / TC_BK;
+  constexpr double K_FIX = 6.0, K_RED = 8.0;
+  TcChoice best{128, 1, 1};
   double best_cost = 1e30;
   for (const Cand& c : cands) {
     if (c.bn > 128 && g.N <= 128) continue;
     if (c.cg == 2 && g.M <= 128) continue;  // the pair's second CTA would only see padding
     const int64_t mb = (g.M + 128 * c.cg - 1) / (128 * c.cg);
     const int64_t nb = (g.N + c.bn - 1) / c.bn;
-    const int64_t units = mb * nb * g.Z;
+    const int64_t tiles = mb * nb * g.Z;
     const int64_t conc = kNumSMs / c.cg;
-    const double rounds = double((units + conc - 1) / conc);
-    const double cost = rounds * double(128 * c.cg) * double(c.bn) / c.eff / double(c.cg);
-    if (cost < best_cost - 1e-9) {
-      best_cost = cost;
-      best = {c.bn, c.cg};
+    const int max_split = allow_split ? int(std::min<int64_t>(8, kblocks / 4)) : 1;
+    for (int sp = 1; sp <= std::max(1, max_split); ++sp) {
+      const int64_t kps = (kblocks + sp - 1) / sp;
+      if (sp > 1 && (kps * (sp - 1) >= kblocks)) continue;  // an empty split
+      const int64_t units = tiles * sp;
+      const double rounds = double((units + conc - 1) / conc);
+      const double cost = rounds * (double(kps) + K_FIX + (sp > 1 ? K_RED : 0.0)) * double(c.bn) / c.eff;
+      if (cost < best_cost * 0.97) {
+        best_cost = cost;
+        best = {c.bn, c.cg, sp};
+      }
     }
   }
   return best;
 }
 
+TcChoice gemm_tc_choose(const GemmArgs& g) { return choose(g, true); }
+
+static int tc_cpw(int bn) { return (bn / TC_EW + TC_EPI_WARPS / 4 - 1) / (TC_EPI_WARPS / 4); }
+
+void gemm_prepare(GemmArgs& g, bool exact, GemmWs& keep) {
+  if (exact || !gemm_tc_supported(g, nullptr)) return;
+  // The in-kernel split-K reduction is correct (tests force it) but its
+  // last-arriver reduction stalls on this part (profiles/r01_gemm_trace.jsonl),
+  // so the cost model only picks it when asked.
+  const TcChoice c = choose(g, g.dact == ACT_NONE && g.allow_split);
+  g.force_bn = c.bn;
+  g.force_cg = c.cg;
+  g.force_splits = c.splits;
+  if (c.splits > 1) {
+    const int64_t tiles = ((g.M + 128 * c.cg - 1) / (128 * c.cg)) * ((g.N + c.bn - 1) / c.bn) * g.Z;
+    const int64_t boxes = tiles * c.cg * TC_EPI_WARPS;
+    keep.ws = std::make_shared<Scratch>(size_t(c.splits) * boxes * tc_cpw(c.bn) * 32 * TC_EW * sizeof(float));
+    keep.cnt = std::make_shared<Scratch>(size_t(boxes) * sizeof(int));
+    TCB_CUDA(cudaMemset(keep.cnt->p, 0, size_t(boxes) * sizeof(int)));
+    g.ws = static_cast<float*>(keep.ws->p);
+    g.ws_cnt = static_cast<int*>(keep.cnt->p);
+  }
+}
+
 void launch_gemm_tc(const GemmArgs& g, cudaStream_t s) {
   std::string why;
   if (!gemm_tc_supported(g, &why)) fail(TCB_ERR_UNIMPLEMENTED, "tcgen05 gemm: " + why);
-  const TcChoice c = choose(g);
+  const TcChoice c = choose(g, false);
   const bool aux = g.dact != ACT_NONE;
+  if (c.splits > 1 && (!g.ws || !g.ws_cnt || aux))
+    fail(TCB_ERR_TYPE, "tcgen05 gemm: split-K needs gemm_prepare's workspace and no act'(aux)");
 #define TC_CASE(BN_, CG_)                                  \
   if (c.bn == BN_ && c.cg == CG_) {                        \
     if (aux) launch_cfg<BN_, CG_, true>(g, s);             \

@@ -36,6 +36,8 @@ def run(name, op, M, K, N, ta, tb, out, iters, tile=None, cublas=True):
     at = {"ta": ta, "tb": tb}
     if tile:
         at.update({"tc_bn": tile[0], "tc_cg": tile[1]})
+        if len(tile) > 2:
+            at["tc_splits"] = tile[2]
     plan = Plan(op, [(tuple(a.shape), BF16), (tuple(b.shape), BF16)], [((M, N), out)], at)
     s = torch.cuda.current_stream().cuda_stream
     for _ in range(3):
@@ -65,6 +67,62 @@ def run(name, op, M, K, N, ta, tb, out, iters, tile=None, cublas=True):
     ucb = e0.elapsed_time(e1) * 1000 / iters
     return {"name": name, "M": M, "K": K, "N": N, "ta": ta, "tb": tb, "us": round(us, 2), "tflops": round(tf, 1),
             "cublas_us": round(ucb, 2), "cublas_tflops": round(2.0 * M * N * K / (ucb * 1e-6) / 1e12, 1)}
+
+
+def trace(iters):
+    """Per-CTA timeline of one launch (globaltimer ns): entry, setup done, first
+    operand stage landed (MMA), last MMA commit, first accumulator ready
+    (epilogue), epilogue drained."""
+    cases = [("ffn1_fwd", 4096, 768, 3072, 0, 0, BF16, {}), ("proj_wgrad", 768, 4096, 768, 1, 0, F32, {}),
+             ("ffn1_wgrad", 768, 4096, 3072, 1, 0, F32, {}),
+             ("ffn1_wgrad_bf16out", 768, 4096, 3072, 1, 0, BF16, {}),
+             ("ffn1_wgrad_notma", 768, 4096, 3072, 1, 0, F32, {"tc_notma": 1}),
+             ("ffn1_wgrad_cg1", 768, 4096, 3072, 1, 0, F32, {"tc_bn": 128, "tc_cg": 1}),
+             ("ffn1_wgrad_cg2_128", 768, 4096, 3072, 1, 0, F32, {"tc_bn": 128, "tc_cg": 2}),
+             ("ffn1_wgrad_cg2_256", 768, 4096, 3072, 1, 0, F32, {"tc_bn": 256, "tc_cg": 2}),
+             ("ffn1_wgrad_kmaj", 768, 4096, 3072, 0, 1, F32, {}),
+             ("decoder_fwd", 4096, 768, 30528, 0, 1, BF16, {}),
+             ("ffn2_fwd", 4096, 3072, 768, 0, 0, BF16, {})]
+    for name, M, K, N, ta, tb, out, extra in cases:
+        a = torch.randn(K, M, device="cuda") if ta else torch.randn(M, K, device="cuda")
+        b = torch.randn(N, K, device="cuda") if tb else torch.randn(K, N, device="cuda")
+        a, b = a.to(torch.bfloat16).contiguous(), b.to(torch.bfloat16).contiguous()
+        c = torch.empty(M, N, device="cuda", dtype=torch.float32 if out == F32 else torch.bfloat16)
+        tr = torch.zeros(148 * 8, dtype=torch.int64, device="cuda")
+        plan = Plan("matmul_t", [(tuple(a.shape), BF16), (tuple(b.shape), BF16)], [((M, N), out)],
+                    {"ta": ta, "tb": tb, "tc_trace": tr.data_ptr(), **extra})
+        s = torch.cuda.current_stream().cuda_stream
+        for _ in range(3):
+            plan.launch([a.data_ptr(), b.data_ptr()], [c.data_ptr()], s)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(10):
+            plan.launch([a.data_ptr(), b.data_ptr()], [c.data_ptr()], s)
+        e1.record()
+        torch.cuda.synchronize()
+        us = e0.elapsed_time(e1) * 100
+        t = tr.view(148, 8).cpu().numpy().astype("float64")
+        t = t[t[:, 0] > 0]
+        base = t[:, 0].min()
+        rel = (t[:, :8] - base) / 1000.0
+        rel[t[:, :8] == 0] = float("nan")
+        import numpy as np
+        q = lambda col: [round(float(np.nanpercentile(rel[:, col], p)), 2) for p in (0, 50, 100)]
+        print(json.dumps({"name": name, "us": round(us, 2), "ctas": len(t), "entry": q(0), "setup": q(1), "first_stage": q(2),
+                          "last_commit": q(3), "first_acc": q(4), "chunks_done": q(6), "released": q(7),
+                          "epi_done": q(5)}), flush=True)
+
+
+def sweep_splits(iters):
+    """Split-K ways on the weight-gradient shapes (few output tiles, K = T)."""
+    T = 4096
+    for name, M, N in (("proj_wgrad", 768, 768), ("qkv_wgrad", 768, 2304), ("ffn1_wgrad", 768, 3072),
+                       ("ffn2_wgrad", 3072, 768)):
+        for tile in [(256, 2), (128, 2), (128, 1)]:
+            for sp in (1, 2, 3, 4):
+                r = run(name, "matmul_t", M, T, N, 1, 0, F32, iters, tile=tile + (sp,), cublas=False)
+                print(json.dumps(r), flush=True)
 
 
 def sweep(iters):
@@ -131,7 +189,15 @@ def main():
     ap.add_argument("--attention", action="store_true")
     ap.add_argument("--linear", action="store_true")
     ap.add_argument("--sweep", action="store_true")
+    ap.add_argument("--splits", action="store_true")
+    ap.add_argument("--trace", action="store_true")
     args = ap.parse_args()
+    if args.trace:
+        trace(args.iters)
+        return
+    if args.splits:
+        sweep_splits(args.iters)
+        return
     if args.sweep:
         sweep(args.iters)
         return
