@@ -1,0 +1,457 @@
+// k_attention.cu -- fused multi-head attention for short sequences (S <= 128,
+// head dim 64): one CTA per (batch, head), everything on-chip.
+//
+// Forward  (oracle.c attention_fwd):
+//   TMA Q, K, V head tiles straight out of qkv [T, 3H] (no split copies)
+//   S  = Q K^T                 tcgen05.mma 128x128x64 -> TMEM
+//   P  = softmax(scale * S)    8 warps: a (query row = TMEM lane, 64-key
+//                              half) per thread, halves combined in smem
+//   probs <- P (bf16)          swizzled smem tile -> TMA store (saved for bwd)
+//   Pd = dropout(P)            Philox keep bits, same indices as k_softmax
+//   O  = Pd V                  tcgen05.mma 128x64x128 (Pd = K-major A from
+//                              smem, V = MN-major B) -> TMEM -> TMA store ctx
+// Backward (oracle.c attention_bwd):
+//   dPd = dO V^T  -> TMEM;  per row: dP = keep*dPd/(1-p), rowdot = P.dP,
+//   dS = P (dP - rowdot) scale (bf16 smem), Pd in place of P;
+//   dV = Pd^T dO, dQ = dS K, dK = dS^T Q: the transposed operands are the same
+//   smem tiles read through MN-major UMMA descriptors; dQ/dK/dV -> TMA stores
+//   into dqkv.
+// Scores/P never touch HBM except the bf16 P the backward needs: per head the
+// forward moves 48 KB in + 16 KB ctx + 32 KB probs, the backward 96 KB in +
+// 48 KB out.
+#include "gemm.cuh"
+#include "tc_ptx.cuh"
+
+namespace tcb {
+
+constexpr int AT_S = 128;         // query / key tile (sequence padded to 128)
+constexpr int AT_D = 64;          // head dim (one SWIZZLE_128B row)
+constexpr int AT_TILE = 16384;    // 128 rows x 128 B
+constexpr int AT_THREADS = 256;   // 8 warps: 2 per TMEM lane quarter, one per 64-key half
+
+struct AttnArgs {
+  int S, H, A, dh, causal;
+  float scale;
+  DropCfg d;
+};
+
+// byte offset of granule g (8 bf16) of row r in a [128 rows x 128 B] SW128 tile
+__device__ __forceinline__ uint32_t sw128(int r, int g) { return uint32_t(r * 128 + ((g ^ (r & 7)) << 4)); }
+
+__device__ __forceinline__ uint32_t pack_bf2(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+__device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
+
+__device__ __forceinline__ void tma_load_3(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                           int c2) {
+  tma_load_4d<1>(dst, map, smem_u32(bar), c0, c1, c2, 0);
+}
+
+// keep bits for 64 row elements j0 .. j0+63 of flat index base + j (base, j0 % 8 == 0)
+__device__ __forceinline__ void keep_bits64(const DropCfg& d, uint64_t base, int j0, int S, uint32_t (&kb)[2]) {
+  kb[0] = kb[1] = 0xffffffffu;
+  if (d.p <= 0.0f) return;
+#pragma unroll
+  for (int g = 0; g < 8; ++g) {
+    if (j0 + g * 8 < S) {
+      const uint32_t b = dropout_bits8q(d, ((base + j0) >> 3) + g);
+      kb[g >> 2] = (kb[g >> 2] & ~(0xffu << ((g & 3) * 8))) | (b << ((g & 3) * 8));
+    }
+  }
+}
+// e^x on the MUFU path (ex2.approx); the oracle's expf differs by a few ulp
+__device__ __forceinline__ float fast_exp(float x) { return exp2f(x * 1.4426950408889634f); }
+
+// ------------------------------------------------------------------ forward
+// Thread layout: warp w owns TMEM lane quarter q = w % 4 (query rows 32q..+31)
+// and key half hf = w / 4 (columns 64hf..+63, exactly one SW128 P tile); the
+// two halves of a row combine max / sum through smem.
+__global__ void __launch_bounds__(AT_THREADS) k_attn_fwd(const __grid_constant__ CUtensorMap m_qkv,
+                                                         const __grid_constant__ CUtensorMap m_probs,
+                                                         const __grid_constant__ CUtensorMap m_ctx,
+                                                         const AttnArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = sm;
+  uint8_t* sK = sm + AT_TILE;
+  uint8_t* sV = sm + 2 * AT_TILE;
+  uint8_t* sP = sm + 3 * AT_TILE;  // 2 tiles: keys 0-63, 64-127
+  float* red = reinterpret_cast<float*>(sm + 5 * AT_TILE);  // [2 stats][2 halves][128 rows]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(red + 512);    // load, mma1, mma2
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 3);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int z = blockIdx.x, b = z / a.A, h = z % a.A;
+  const int q = warp & 3, hf = warp >> 2;
+  const int row = q * 32 + lane;  // query row = TMEM lane
+  const int j0 = hf * 64;         // this thread's key columns
+  if (tid == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&m_qkv)) : "memory");
+    for (int i = 0; i < 3; ++i) mbar_init(&bar[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) tmem_alloc1<256>(tslot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tm = *tslot;
+
+  if (tid == 0) {
+    mbar_expect_tx(&bar[0], 3 * AT_TILE);
+    tma_load_3(sQ, &m_qkv, &bar[0], h * AT_D, 0, b);
+    tma_load_3(sK, &m_qkv, &bar[0], a.H + h * AT_D, 0, b);
+    tma_load_3(sV, &m_qkv, &bar[0], 2 * a.H + h * AT_D, 0, b);
+    mbar_wait(&bar[0], 0);
+    tc_fence_after();
+    constexpr uint32_t id1 = umma_idesc(128, 128, true, false, false);
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      tc_mma<1>(tm, umma_desc(smem_u32(sQ) + k * 32, 16, 1024), umma_desc(smem_u32(sK) + k * 32, 16, 1024), id1,
+                k ? 1u : 0u);
+    tc_commit<1>(&bar[1]);
+  }
+  // dropout keep bits overlap the QK^T MMA
+  uint32_t kb[2];
+  keep_bits64(a.d, (uint64_t(z) * a.S + row) * a.S, j0, a.S, kb);
+  mbar_wait(&bar[1], 0);
+  tc_fence_after();
+
+  // ---- softmax over this thread's 64 scores
+  float v[64];
+  const uint32_t trow = tm + (uint32_t(q * 32) << 16);
+  {
+    uint32_t r[32];
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      TMEM_LD32(trow + j0 + c * 32, r);
+      tmem_wait_ld();
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[c * 32 + j] = __uint_as_float(r[j]);
+    }
+  }
+  float mx = -INFINITY;
+#pragma unroll
+  for (int j = 0; j < 64; ++j) {
+    const int col = j0 + j;
+    float t = v[j] * a.scale;
+    if (col >= a.S || (a.causal && col > row)) t = -INFINITY;
+    v[j] = t;
+    mx = fmaxf(mx, t);
+  }
+  red[hf * 128 + row] = mx;
+  __syncthreads();
+  mx = fmaxf(red[row], red[128 + row]);
+  float sum = 0.0f;
+#pragma unroll
+  for (int j = 0; j < 64; ++j) {
+    v[j] = v[j] == -INFINITY ? 0.0f : fast_exp(v[j] - mx);
+    sum += v[j];
+  }
+  red[256 + hf * 128 + row] = sum;
+  __syncthreads();
+  const float inv = row < a.S ? 1.0f / (red[256 + row] + red[384 + row]) : 0.0f;
+  uint8_t* tileP = sP + hf * AT_TILE;
+  // P rounded to bf16 (the stored probs) = this half's K-major A tile
+#pragma unroll
+  for (int g = 0; g < 8; ++g) {
+    uint4 w;
+    w.x = pack_bf2(v[g * 8 + 0] * inv, v[g * 8 + 1] * inv);
+    w.y = pack_bf2(v[g * 8 + 2] * inv, v[g * 8 + 3] * inv);
+    w.z = pack_bf2(v[g * 8 + 4] * inv, v[g * 8 + 5] * inv);
+    w.w = pack_bf2(v[g * 8 + 6] * inv, v[g * 8 + 7] * inv);
+    *reinterpret_cast<uint4*>(tileP + sw128(row, g)) = w;
+    v[g * 8 + 0] = bf_lo(w.x), v[g * 8 + 1] = bf_hi(w.x), v[g * 8 + 2] = bf_lo(w.y), v[g * 8 + 3] = bf_hi(w.y);
+    v[g * 8 + 4] = bf_lo(w.z), v[g * 8 + 5] = bf_hi(w.z), v[g * 8 + 6] = bf_lo(w.w), v[g * 8 + 7] = bf_hi(w.w);
+  }
+  fence_proxy_async();
+  __syncthreads();
+  if (tid == 0) {
+    tma_store_4d(&m_probs, sP, 0, 0, z, 0);
+    if (a.S > 64) tma_store_4d(&m_probs, sP + AT_TILE, 64, 0, z, 0);
+    bulk_commit();
+  }
+  if (a.d.p > 0.0f) {
+    // Pd = bf16(P * keep / (1-p)) over the same tile once the probs store has read it
+    if (tid == 0) bulk_wait_read<0>();
+    __syncthreads();
+#pragma unroll
+    for (int g = 0; g < 8; ++g) {
+      float pd[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const int j = g * 8 + e;
+        pd[e] = ((kb[j >> 5] >> (j & 31)) & 1u) ? v[j] * a.d.scale : 0.0f;
+      }
+      uint4 w;
+      w.x = pack_bf2(pd[0], pd[1]);
+      w.y = pack_bf2(pd[2], pd[3]);
+      w.z = pack_bf2(pd[4], pd[5]);
+      w.w = pack_bf2(pd[6], pd[7]);
+      *reinterpret_cast<uint4*>(tileP + sw128(row, g)) = w;
+    }
+    fence_proxy_async();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (tid == 0) {
+    tc_fence_after();
+    constexpr uint32_t id2 = umma_idesc(128, 64, true, false, true);
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      tc_mma<1>(tm + 128, umma_desc(smem_u32(sP) + (k >> 2) * AT_TILE + (k & 3) * 32, 16, 1024),
+                umma_desc(smem_u32(sV) + k * 2048, AT_TILE, 1024), id2, k ? 1u : 0u);
+    tc_commit<1>(&bar[2]);
+  }
+  mbar_wait(&bar[2], 0);
+  tc_fence_after();
+  // ---- ctx row, this thread's 32 head-dim columns -> bf16 -> staging (sQ) -> TMA store
+  {
+    uint32_t r[32];
+    TMEM_LD32(trow + 128 + hf * 32, r);
+    tmem_wait_ld();
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+      uint4 w;
+      w.x = pack_bf2(__uint_as_float(r[g * 8 + 0]), __uint_as_float(r[g * 8 + 1]));
+      w.y = pack_bf2(__uint_as_float(r[g * 8 + 2]), __uint_as_float(r[g * 8 + 3]));
+      w.z = pack_bf2(__uint_as_float(r[g * 8 + 4]), __uint_as_float(r[g * 8 + 5]));
+      w.w = pack_bf2(__uint_as_float(r[g * 8 + 6]), __uint_as_float(r[g * 8 + 7]));
+      *reinterpret_cast<uint4*>(sQ + sw128(row, hf * 4 + g)) = w;
+    }
+  }
+  fence_proxy_async();
+  tc_fence_before();
+  __syncthreads();
+  if (tid == 0) {
+    tma_store_4d(&m_ctx, sQ, h * AT_D, 0, b, 0);
+    bulk_commit();
+    bulk_wait_all();
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_free1<256>(tm);
+  }
+}
+
+// ----------------------------------------------------------------- backward
+__global__ void __launch_bounds__(AT_THREADS) k_attn_bwd(const __grid_constant__ CUtensorMap m_qkv,
+                                                         const __grid_constant__ CUtensorMap m_probs,
+                                                         const __grid_constant__ CUtensorMap m_dctx,
+                                                         const __grid_constant__ CUtensorMap m_dqkv,
+                                                         const AttnArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = sm;
+  uint8_t* sK = sm + AT_TILE;
+  uint8_t* sV = sm + 2 * AT_TILE;
+  uint8_t* sO = sm + 3 * AT_TILE;   // dO
+  uint8_t* sP = sm + 4 * AT_TILE;   // 2 tiles: P, then Pd in place
+  uint8_t* sS = sm + 6 * AT_TILE;   // 2 tiles: dS
+  float* red = reinterpret_cast<float*>(sm + 8 * AT_TILE);  // [2 halves][128 rows]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(red + 256);   // load, mma1, mma2
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 3);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int z = blockIdx.x, b = z / a.A, h = z % a.A;
+  const int q = warp & 3, hf = warp >> 2;
+  const int row = q * 32 + lane;
+  const int j0 = hf * 64;
+  if (tid == 0) {
+    for (int i = 0; i < 3; ++i) mbar_init(&bar[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) tmem_alloc1<256>(tslot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tm = *tslot;
+
+  if (tid == 0) {
+    mbar_expect_tx(&bar[0], 6 * AT_TILE);
+    tma_load_3(sQ, &m_qkv, &bar[0], h * AT_D, 0, b);
+    tma_load_3(sK, &m_qkv, &bar[0], a.H + h * AT_D, 0, b);
+    tma_load_3(sV, &m_qkv, &bar[0], 2 * a.H + h * AT_D, 0, b);
+    tma_load_3(sO, &m_dctx, &bar[0], h * AT_D, 0, b);
+    tma_load_3(sP, &m_probs, &bar[0], 0, 0, z);
+    tma_load_3(sP + AT_TILE, &m_probs, &bar[0], 64, 0, z);
+    mbar_wait(&bar[0], 0);
+    tc_fence_after();
+    // dPd = dO V^T  (A = dO K-major, B = V K-major: [key][dh])
+    constexpr uint32_t id1 = umma_idesc(128, 128, true, false, false);
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      tc_mma<1>(tm, umma_desc(smem_u32(sO) + k * 32, 16, 1024), umma_desc(smem_u32(sV) + k * 32, 16, 1024), id1,
+                k ? 1u : 0u);
+    tc_commit<1>(&bar[1]);
+  }
+  uint32_t kb[2];
+  keep_bits64(a.d, (uint64_t(z) * a.S + row) * a.S, j0, a.S, kb);
+  const float sd = a.d.p > 0.0f ? a.d.scale : 1.0f;
+  mbar_wait(&bar[1], 0);
+  tc_fence_after();
+
+  const uint32_t trow = tm + (uint32_t(q * 32) << 16) + j0;
+  uint8_t* tileP = sP + hf * AT_TILE;
+  uint8_t* tileS = sS + hf * AT_TILE;
+  // pass 1: rowdot = sum_j P_j * dP_j (this half), combined through smem
+  float dp[64];
+  float rowdot = 0.0f;
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    uint32_t r[32];
+    TMEM_LD32(trow + c * 32, r);
+    tmem_wait_ld();
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+      const uint4 w = *reinterpret_cast<const uint4*>(tileP + sw128(row, c * 4 + g));
+      const float p[8] = {bf_lo(w.x), bf_hi(w.x), bf_lo(w.y), bf_hi(w.y), bf_lo(w.z), bf_hi(w.z), bf_lo(w.w), bf_hi(w.w)};
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const int j = c * 32 + g * 8 + e;
+        const bool keep = (kb[j >> 5] >> (j & 31)) & 1u;
+        dp[j] = keep ? __uint_as_float(r[g * 8 + e]) * sd : 0.0f;
+        rowdot += p[e] * dp[j];
+      }
+    }
+  }
+  red[hf * 128 + row] = rowdot;
+  __syncthreads();
+  rowdot = red[row] + red[128 + row];
+  // pass 2: dS = P (dP - rowdot) scale -> sS; Pd -> sP (in place)
+#pragma unroll
+  for (int g = 0; g < 8; ++g) {
+    uint8_t* pp = tileP + sw128(row, g);
+    const uint4 w = *reinterpret_cast<const uint4*>(pp);
+    const float p[8] = {bf_lo(w.x), bf_hi(w.x), bf_lo(w.y), bf_hi(w.y), bf_lo(w.z), bf_hi(w.z), bf_lo(w.w), bf_hi(w.w)};
+    float ds[8], pd[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int j = g * 8 + e;
+      const bool keep = (kb[j >> 5] >> (j & 31)) & 1u;
+      pd[e] = keep ? p[e] * sd : 0.0f;
+      ds[e] = p[e] * (dp[j] - rowdot) * a.scale;
+    }
+    uint4 o;
+    o.x = pack_bf2(ds[0], ds[1]);
+    o.y = pack_bf2(ds[2], ds[3]);
+    o.z = pack_bf2(ds[4], ds[5]);
+    o.w = pack_bf2(ds[6], ds[7]);
+    *reinterpret_cast<uint4*>(tileS + sw128(row, g)) = o;
+    if (a.d.p > 0.0f) {
+      o.x = pack_bf2(pd[0], pd[1]);
+      o.y = pack_bf2(pd[2], pd[3]);
+      o.z = pack_bf2(pd[4], pd[5]);
+      o.w = pack_bf2(pd[6], pd[7]);
+      *reinterpret_cast<uint4*>(pp) = o;
+    }
+  }
+  fence_proxy_async();
+  tc_fence_before();
+  __syncthreads();
+  if (tid == 0) {
+    tc_fence_after();
+    // M = 128 over two 64-wide MN chunks of a [K=128 rows][128 B] tile pair: LBO = tile
+    constexpr uint32_t id_mm = umma_idesc(128, 64, true, true, true);   // A MN-major, B MN-major
+    constexpr uint32_t id_km = umma_idesc(128, 64, true, false, true);  // A K-major, B MN-major
+#pragma unroll
+    for (int k = 0; k < 8; ++k)  // dV = Pd^T dO -> cols 128..191
+      tc_mma<1>(tm + 128, umma_desc(smem_u32(sP) + k * 2048, AT_TILE, 1024),
+                umma_desc(smem_u32(sO) + k * 2048, AT_TILE, 1024), id_mm, k ? 1u : 0u);
+#pragma unroll
+    for (int k = 0; k < 8; ++k)  // dQ = dS K -> cols 0..63
+      tc_mma<1>(tm, umma_desc(smem_u32(sS) + (k >> 2) * AT_TILE + (k & 3) * 32, 16, 1024),
+                umma_desc(smem_u32(sK) + k * 2048, AT_TILE, 1024), id_km, k ? 1u : 0u);
+#pragma unroll
+    for (int k = 0; k < 8; ++k)  // dK = dS^T Q -> cols 64..127
+      tc_mma<1>(tm + 64, umma_desc(smem_u32(sS) + k * 2048, AT_TILE, 1024),
+                umma_desc(smem_u32(sQ) + k * 2048, AT_TILE, 1024), id_mm, k ? 1u : 0u);
+    tc_commit<1>(&bar[2]);
+  }
+  mbar_wait(&bar[2], 0);
+  tc_fence_after();
+  // dQ (query row), dK, dV (key row = TMEM lane): this thread's 32 head-dim
+  // columns of each -> bf16 staging in sQ / sK / sV
+  uint8_t* stage[3] = {sQ, sK, sV};
+  const uint32_t col[3] = {0, 64, 128};
+  const uint32_t tbase = tm + (uint32_t(q * 32) << 16) + hf * 32;
+#pragma unroll
+  for (int t = 0; t < 3; ++t) {
+    uint32_t r[32];
+    TMEM_LD32(tbase + col[t], r);
+    tmem_wait_ld();
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+      uint4 w;
+      w.x = pack_bf2(__uint_as_float(r[g * 8 + 0]), __uint_as_float(r[g * 8 + 1]));
+      w.y = pack_bf2(__uint_as_float(r[g * 8 + 2]), __uint_as_float(r[g * 8 + 3]));
+      w.z = pack_bf2(__uint_as_float(r[g * 8 + 4]), __uint_as_float(r[g * 8 + 5]));
+      w.w = pack_bf2(__uint_as_float(r[g * 8 + 6]), __uint_as_float(r[g * 8 + 7]));
+      *reinterpret_cast<uint4*>(stage[t] + sw128(row, hf * 4 + g)) = w;
+    }
+  }
+  fence_proxy_async();
+  tc_fence_before();
+  __syncthreads();
+  if (tid == 0) {
+    tma_store_4d(&m_dqkv, sQ, h * AT_D, 0, b, 0);
+    tma_store_4d(&m_dqkv, sK, a.H + h * AT_D, 0, b, 0);
+    tma_store_4d(&m_dqkv, sV, 2 * a.H + h * AT_D, 0, b, 0);
+    bulk_commit();
+    bulk_wait_all();
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_free1<256>(tm);
+  }
+}
+
+// ------------------------------------------------------------------ host
+constexpr int AT_FWD_SMEM = 1024 + 5 * AT_TILE + 2048 + 64;
+constexpr int AT_BWD_SMEM = 1024 + 8 * AT_TILE + 1024 + 64;
+
+bool attn_fused_ok(int dt, int64_t S, int64_t H, int64_t A, bool exact) {
+  return !exact && dt == TCB_BF16 && A > 0 && H % A == 0 && H / A == AT_D && S >= 8 && S <= AT_S && S % 8 == 0;
+}
+
+// [rows=S per batch] x [cols] bf16 family -> 3-D map {cols, S, B}, box {64, 128}
+static CUtensorMap seq_map(const void* p, int64_t cols, int64_t S, int64_t B) {
+  return encode4(p, TCB_BF16, cols, S, B, 1, cols, S * cols, S * cols * B, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
+void launch_attn_fwd(const void* qkv, void* ctx, void* probs, int64_t B, int64_t S, int64_t H, int64_t A, float scale,
+                     int causal, const DropCfg& d, cudaStream_t s) {
+  static std::once_flag once;
+  std::call_once(once, [] {
+    TCB_CUDA(cudaFuncSetAttribute(k_attn_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, AT_FWD_SMEM));
+  });
+  const CUtensorMap mq = seq_map(qkv, 3 * H, S, B);
+  const CUtensorMap mc = seq_map(ctx, H, S, B);
+  const CUtensorMap mp = encode4(probs, TCB_BF16, S, S, B * A, 1, S, S * S, S * S * B * A, 64, 128,
+                                 CU_TENSOR_MAP_SWIZZLE_128B);
+  AttnArgs a{int(S), int(H), int(A), int(H / A), causal, scale, d};
+  k_attn_fwd<<<unsigned(B * A), AT_THREADS, AT_FWD_SMEM, s>>>(mq, mp, mc, a);
+  TCB_CUDA(cudaGetLastError());
+}
+
+void launch_attn_bwd(const void* qkv, const void* probs, const void* dctx, void* dqkv, int64_t B, int64_t S, int64_t H,
+                     int64_t A, float scale, int causal, const DropCfg& d, cudaStream_t s) {
+  static std::once_flag once;
+  std::call_once(once, [] {
+    TCB_CUDA(cudaFuncSetAttribute(k_attn_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, AT_BWD_SMEM));
+  });
+  const CUtensorMap mq = seq_map(qkv, 3 * H, S, B);
+  const CUtensorMap mo = seq_map(dctx, H, S, B);
+  const CUtensorMap md = seq_map(dqkv, 3 * H, S, B);
+  const CUtensorMap mp = encode4(probs, TCB_BF16, S, S, B * A, 1, S, S * S, S * S * B * A, 64, 128,
+                                 CU_TENSOR_MAP_SWIZZLE_128B);
+  AttnArgs a{int(S), int(H), int(A), int(H / A), causal, scale, d};
+  k_attn_bwd<<<unsigned(B * A), AT_THREADS, AT_BWD_SMEM, s>>>(mq, mp, mo, md, a);
+  TCB_CUDA(cudaGetLastError());
+}
+
+}  // namespace tcb

@@ -789,6 +789,12 @@ static void b_attention(Plan& p) {
   const AttnGeom g = attn_geom(p);
   require(p.out[0].numel() == g.B * g.S * g.H, "attention: ctx must be [T, H]");
   require(p.out[1].numel() == g.Z * g.S * g.S, "attention: probs must be [B*A*S, S]");
+  if (attn_fused_ok(g.dt, g.S, g.H, g.A, g.exact) && !p.attrs.i("unfused", 0)) {
+    p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
+      launch_attn_fwd(in[0].ptr, out[0].ptr, out[1].ptr, g.B, g.S, g.H, g.A, g.scale, g.causal, g.d, s);
+    };
+    return;
+  }
   const size_t nsq = size_t(g.Z) * g.S * g.S;
   auto scores = std::make_shared<Scratch>(nsq * 4);
   auto pd = std::make_shared<Scratch>(g.d.p > 0.0f ? nsq * dtype_bytes(g.dt) : 0);
@@ -824,6 +830,12 @@ static void b_attention_dx(Plan& p) {
   check_arity(p, 3, 3, 1, 1);
   const AttnGeom g = attn_geom(p);
   require(p.out[0].numel() == p.in[0].numel(), "attention_dx: dqkv must be [T, 3H]");
+  if (attn_fused_ok(g.dt, g.S, g.H, g.A, g.exact) && !p.attrs.i("unfused", 0)) {
+    p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
+      launch_attn_bwd(in[0].ptr, in[1].ptr, in[2].ptr, out[0].ptr, g.B, g.S, g.H, g.A, g.scale, g.causal, g.d, s);
+    };
+    return;
+  }
   const size_t nsq = size_t(g.Z) * g.S * g.S;
   auto dpd = std::make_shared<Scratch>(nsq * 4);
   auto ds = std::make_shared<Scratch>(nsq * dtype_bytes(g.dt));

@@ -370,6 +370,29 @@ def test_attention_fwd_bwd(dt, p, causal):
     assert rel_err(g[0], o[0]) < (1e-5 if dt == F32 else 3e-2), rel_err(g[0], o[0])
 
 
+@pytest.mark.parametrize("S", [128, 72, 40])
+@pytest.mark.parametrize("p,causal", [(0.0, 0), (0.1, 0), (0.1, 1)])
+def test_attention_fused_tcgen05(S, p, causal):
+    """Fused tcgen05 attention (one CTA per head, S <= 128, dh 64) against the
+    oracle and against the unfused GEMM + row-softmax path on the GPU."""
+    B, A, dh = 3, 2, 64
+    H, T = A * dh, B * S
+    qkv = rn(T, 3 * H, lo=-2, hi=2)
+    at = {"heads": A, "seq": S, "p": p, "seed": 5, "salt": 11, "causal": causal}
+    outs = [((T, H), BF16), ((B * A * S, S), BF16)]
+    g, o = run_both("attention", [(qkv, BF16)], outs, at)
+    assert rel_err(g[1], o[1]) < 1e-2, rel_err(g[1], o[1])
+    assert rel_err(g[0], o[0]) < 2e-2, rel_err(g[0], o[0])
+    gu, _ = run_both("attention", [(qkv, BF16)], outs, {**at, "unfused": 1})
+    assert rel_err(g[0], gu[0]) < 1e-2 and rel_err(g[1], gu[1]) < 1e-2
+    probs, dctx = o[1], rn(T, H)
+    ins = [(qkv, BF16), (probs, BF16), (dctx, BF16)]
+    g, o = run_both("attention_dx", ins, [((T, 3 * H), BF16)], at)
+    assert rel_err(g[0], o[0]) < 3e-2, rel_err(g[0], o[0])
+    gu, _ = run_both("attention_dx", ins, [((T, 3 * H), BF16)], {**at, "unfused": 1})
+    assert rel_err(g[0], gu[0]) < 2e-2, rel_err(g[0], gu[0])
+
+
 def test_embedding_bit_exact():
     V, H, T = 1000, 96, 513
     ids = RNG.integers(0, V, size=T).astype(np.int32)
