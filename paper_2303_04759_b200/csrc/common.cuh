@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <map>
@@ -233,6 +234,49 @@ struct Scratch {
     if (p) cudaFree(p);
   }
 };
+
+// ------------------------------------------------ programmatic dependent launch
+// Every b200 kernel is launched with programmatic stream serialization: the
+// next kernel in the stream may be scheduled as soon as all CTAs of the
+// current one have started (launch_dependents), so its launch latency and
+// prologue overlap our tail.  Correctness: every kernel executes
+// griddepcontrol.wait (which returns once the preceding grid has completed
+// and flushed) before it touches global memory; since every kernel waits,
+// completion order stays transitive along the stream.  TCB_PDL=0 disables.
+#define TCB_PDL_ENTRY()                                          \
+  do {                                                           \
+    asm volatile("griddepcontrol.wait;" ::: "memory");           \
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); \
+  } while (0)
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("TCB_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+// fills a launch attribute slot with PDL; returns the number of attributes used
+inline int pdl_attr(cudaLaunchAttribute* a) {
+  if (!pdl_enabled()) return 0;
+  a->id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  a->val.programmaticStreamSerializationAllowed = 1;
+  return 1;
+}
+template <typename... KP, typename... Args>
+inline void launch_k(void (*kern)(KP...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_attr(at);
+  TCB_CUDA(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
+}
 
 // ------------------------------------------------------------------ plans
 using RunFn = std::function<void(const tcb_tensor* in, tcb_tensor* out, cudaStream_t s)>;

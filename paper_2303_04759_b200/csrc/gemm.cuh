@@ -38,21 +38,16 @@ struct GemmArgs {
   int aux_dtype = TCB_F32;
   void* aux_out = nullptr;     // pre-activation store, same layout/dtype as C
   int force_bn = 0, force_cg = 0;  // tcgen05 tile override (tests / tuning); 0 = cost model
-  int force_splits = 0;            // split-K ways (needs ws / ws_cnt from gemm_prepare)
-  float* ws = nullptr;             // split-K partial accumulators
-  int* ws_cnt = nullptr;           // split-K arrival counters (zeroed, self re-arming)
-  void* trace = nullptr;
+  int force_splits = 0;            // split-K ways (cluster of CG x splits CTAs, DSMEM reduction)
+  void* trace = nullptr;           // optional per-CTA timeline buffer (12 x u64 per CTA, tooling)
   int no_tma_epi = 0;              // force the direct-store epilogue (tooling)
-  int allow_split = 0;             // let the cost model pick split-K           // optional per-CTA timeline buffer (8 x u64 per CTA)
 };
 
 struct TcChoice {
   int bn, cg, splits;
 };
-// scratch a prepared GEMM keeps alive (split-K partials and counters)
-struct GemmWs {
-  std::shared_ptr<Scratch> ws, cnt;
-};
+// plan-owned state of a prepared GEMM (none needed today: split-K reduces on chip)
+struct GemmWs {};
 
 // Launch helpers (defined in the .cu files)
 void launch_gemm_exact(const GemmArgs& g, cudaStream_t s);

@@ -98,6 +98,8 @@ __global__ void __launch_bounds__(AT_THREADS) k_attn_fwd(const __grid_constant__
   __syncthreads();
   tc_fence_after();
   const uint32_t tm = *tslot;
+  pdl_wait();
+  pdl_trigger();
 
   if (tid == 0) {
     mbar_expect_tx(&bar[0], 3 * AT_TILE);
@@ -269,6 +271,8 @@ __global__ void __launch_bounds__(AT_THREADS) k_attn_bwd(const __grid_constant__
   __syncthreads();
   tc_fence_after();
   const uint32_t tm = *tslot;
+  pdl_wait();
+  pdl_trigger();
 
   if (tid == 0) {
     mbar_expect_tx(&bar[0], 6 * AT_TILE);
@@ -434,7 +438,7 @@ void launch_attn_fwd(const void* qkv, void* ctx, void* probs, int64_t B, int64_t
   const CUtensorMap mp = encode4(probs, TCB_BF16, S, S, B * A, 1, S, S * S, S * S * B * A, 64, 128,
                                  CU_TENSOR_MAP_SWIZZLE_128B);
   AttnArgs a{int(S), int(H), int(A), int(H / A), causal, scale, d};
-  k_attn_fwd<<<unsigned(B * A), AT_THREADS, AT_FWD_SMEM, s>>>(mq, mp, mc, a);
+  launch_k(k_attn_fwd, unsigned(B * A), AT_THREADS, AT_FWD_SMEM, s, mq, mp, mc, a);
   TCB_CUDA(cudaGetLastError());
 }
 
@@ -450,7 +454,7 @@ void launch_attn_bwd(const void* qkv, const void* probs, const void* dctx, void*
   const CUtensorMap mp = encode4(probs, TCB_BF16, S, S, B * A, 1, S, S * S, S * S * B * A, 64, 128,
                                  CU_TENSOR_MAP_SWIZZLE_128B);
   AttnArgs a{int(S), int(H), int(A), int(H / A), causal, scale, d};
-  k_attn_bwd<<<unsigned(B * A), AT_THREADS, AT_BWD_SMEM, s>>>(mq, mp, mo, md, a);
+  launch_k(k_attn_bwd, unsigned(B * A), AT_THREADS, AT_BWD_SMEM, s, mq, mp, mo, md, a);
   TCB_CUDA(cudaGetLastError());
 }
 

@@ -55,6 +55,7 @@ static void bc_strides(const Spec& out, const Spec& in, int64_t* s) {
 template <int OP>
 __global__ void k_binary_bc(const void* __restrict__ a, int dta, const void* __restrict__ b, int dtb,
                             void* __restrict__ o, int dto, int64_t n, BC bc) {
+  TCB_PDL_ENTRY();
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
        i += int64_t(gridDim.x) * blockDim.x) {
     int64_t ia = 0, ib = 0, rem = i;
@@ -73,6 +74,7 @@ __global__ void k_binary_bc(const void* __restrict__ a, int dta, const void* __r
 template <int OP, typename T>
 __global__ void k_binary_same(const T* __restrict__ a, const T* __restrict__ b, T* __restrict__ o,
                               int64_t n) {
+  TCB_PDL_ENTRY();
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += stride)
     o[i] = from_f<T>(binop<OP>(to_f(a[i]), to_f(b[i])));
@@ -82,6 +84,7 @@ __global__ void k_binary_same(const T* __restrict__ a, const T* __restrict__ b, 
 template <int OP, typename T>
 __global__ void k_binary_row(const T* __restrict__ a, const T* __restrict__ b, T* __restrict__ o,
                              int64_t n, int64_t cols, int b_first) {
+  TCB_PDL_ENTRY();
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += stride) {
     float x = to_f(a[i]), y = to_f(b[i % cols]);
@@ -108,7 +111,7 @@ static void build_binary(Plan& p) {
     dispatch_float(O.dtype, [&](auto* tp) {
       using T = std::remove_pointer_t<decltype(tp)>;
       p.run = [n](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
-        k_binary_same<OP, T><<<grid_for(n, 256), 256, 0, s>>>(
+        launch_k(k_binary_same<OP, T>, grid_for(n, 256), 256, 0, s, 
             (const T*)in[0].ptr, (const T*)in[1].ptr, (T*)out[0].ptr, n);
       };
     });
@@ -131,7 +134,7 @@ static void build_binary(Plan& p) {
     dispatch_float(O.dtype, [&](auto* tp) {
       using T = std::remove_pointer_t<decltype(tp)>;
       p.run = [n, cols](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
-        k_binary_row<OP, T><<<grid_for(n, 256), 256, 0, s>>>(
+        launch_k(k_binary_row<OP, T>, grid_for(n, 256), 256, 0, s, 
             (const T*)in[0].ptr, (const T*)in[1].ptr, (T*)out[0].ptr, n, cols, 0);
       };
     });
@@ -142,7 +145,7 @@ static void build_binary(Plan& p) {
     dispatch_float(O.dtype, [&](auto* tp) {
       using T = std::remove_pointer_t<decltype(tp)>;
       p.run = [n, cols](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
-        k_binary_row<OP, T><<<grid_for(n, 256), 256, 0, s>>>(
+        launch_k(k_binary_row<OP, T>, grid_for(n, 256), 256, 0, s, 
             (const T*)in[1].ptr, (const T*)in[0].ptr, (T*)out[0].ptr, n, cols, 1);
       };
     });
@@ -155,7 +158,7 @@ static void build_binary(Plan& p) {
   bc_strides(O, B, bc.sb);
   const int dta = A.dtype, dtb = B.dtype, dto = O.dtype;
   p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
-    k_binary_bc<OP><<<grid_for(n, 256), 256, 0, s>>>(in[0].ptr, dta, in[1].ptr, dtb, out[0].ptr, dto,
+    launch_k(k_binary_bc<OP>, grid_for(n, 256), 256, 0, s, in[0].ptr, dta, in[1].ptr, dtb, out[0].ptr, dto,
                                                        n, bc);
   };
 }
@@ -188,6 +191,7 @@ __device__ __forceinline__ float unop(float x) {
 
 template <int OP>
 __global__ void k_unary(const void* __restrict__ a, int dta, void* __restrict__ o, int dto, int64_t n) {
+  TCB_PDL_ENTRY();
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
        i += int64_t(gridDim.x) * blockDim.x)
     st_any(o, dto, i, unop<OP>(ld_any(a, dta, i)));
@@ -201,7 +205,7 @@ static void build_unary(Plan& p) {
   const int64_t n = p.out[0].numel();
   const int dta = p.in[0].dtype, dto = p.out[0].dtype;
   p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
-    k_unary<OP><<<grid_for(n, 256), 256, 0, s>>>(in[0].ptr, dta, out[0].ptr, dto, n);
+    launch_k(k_unary<OP>, grid_for(n, 256), 256, 0, s, in[0].ptr, dta, out[0].ptr, dto, n);
   };
 }
 static void b_neg(Plan& p) { build_unary<U_NEG>(p); }
@@ -221,6 +225,7 @@ TCB_REGISTER("convert", b_cast);
 // ------------------------------------------------------------------- bcast
 __global__ void k_bcast(const void* __restrict__ a, int dta, void* __restrict__ o, int dto, int64_t n,
                         BC bc) {
+  TCB_PDL_ENTRY();
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
        i += int64_t(gridDim.x) * blockDim.x) {
     int64_t ia = 0, rem = i;
@@ -242,7 +247,7 @@ static void b_bcast(Plan& p) {
   const int64_t n = p.out[0].numel();
   const int dta = p.in[0].dtype, dto = p.out[0].dtype;
   p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
-    k_bcast<<<grid_for(n, 256), 256, 0, s>>>(in[0].ptr, dta, out[0].ptr, dto, n, bc);
+    launch_k(k_bcast, grid_for(n, 256), 256, 0, s, in[0].ptr, dta, out[0].ptr, dto, n, bc);
   };
 }
 TCB_REGISTER("bcast", b_bcast);
@@ -251,6 +256,7 @@ TCB_REGISTER("bcast", b_bcast);
 // 32x32 smem tile, +1 padding (no bank conflicts); raw element copy.
 template <typename W>
 __global__ void k_transpose(const W* __restrict__ in, W* __restrict__ out, int64_t R, int64_t C) {
+  TCB_PDL_ENTRY();
   __shared__ W tile[32][33];
   int64_t c0 = int64_t(blockIdx.x) * 32, r0 = int64_t(blockIdx.y) * 32;
   for (int k = threadIdx.y; k < 32; k += 8) {
@@ -272,11 +278,11 @@ static void b_transpose(Plan& p) {
   dim3 grid(unsigned((C + 31) / 32), unsigned((R + 31) / 32)), block(32, 8);
   p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
     if (w == 4)
-      k_transpose<uint32_t><<<grid, block, 0, s>>>((const uint32_t*)in[0].ptr, (uint32_t*)out[0].ptr, R, C);
+      launch_k(k_transpose<uint32_t>, grid, block, 0, s, (const uint32_t*)in[0].ptr, (uint32_t*)out[0].ptr, R, C);
     else if (w == 2)
-      k_transpose<uint16_t><<<grid, block, 0, s>>>((const uint16_t*)in[0].ptr, (uint16_t*)out[0].ptr, R, C);
+      launch_k(k_transpose<uint16_t>, grid, block, 0, s, (const uint16_t*)in[0].ptr, (uint16_t*)out[0].ptr, R, C);
     else
-      k_transpose<uint8_t><<<grid, block, 0, s>>>((const uint8_t*)in[0].ptr, (uint8_t*)out[0].ptr, R, C);
+      launch_k(k_transpose<uint8_t>, grid, block, 0, s, (const uint8_t*)in[0].ptr, (uint8_t*)out[0].ptr, R, C);
   };
 }
 TCB_REGISTER("transpose", b_transpose);
@@ -335,6 +341,7 @@ TCB_REGISTER("concat", b_concat);
 // one Philox call yields the keep bits for 8 consecutive elements
 template <typename T>
 __global__ void k_dropout(const T* __restrict__ x, T* __restrict__ y, int64_t n, DropCfg d) {
+  TCB_PDL_ENTRY();
   const int64_t nq = (n + 7) / 8;
   for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < nq;
        q += int64_t(gridDim.x) * blockDim.x) {
@@ -354,7 +361,7 @@ static void b_dropout(Plan& p) {
   dispatch_float(p.out[0].dtype, [&](auto* tp) {
     using T = std::remove_pointer_t<decltype(tp)>;
     p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
-      k_dropout<T><<<grid_for((n + 7) / 8, 256), 256, 0, s>>>((const T*)in[0].ptr, (T*)out[0].ptr, n, d);
+      launch_k(k_dropout<T>, grid_for((n + 7) / 8, 256), 256, 0, s, (const T*)in[0].ptr, (T*)out[0].ptr, n, d);
     };
   });
 }
@@ -363,6 +370,7 @@ TCB_REGISTER("dropout", b_dropout);
 // --------------------------------------------------------- add_scalar / fill
 template <typename T>
 __global__ void k_add_scalar(const T* __restrict__ x, T* __restrict__ y, int64_t n, float v) {
+  TCB_PDL_ENTRY();
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
     y[i] = from_f<T>(__fadd_rn(to_f(x[i]), v));
 }
@@ -374,7 +382,7 @@ static void b_add_scalar(Plan& p) {
   dispatch_float(p.out[0].dtype, [&](auto* tp) {
     using T = std::remove_pointer_t<decltype(tp)>;
     p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
-      k_add_scalar<T><<<grid_for(n, 256), 256, 0, s>>>((const T*)in[0].ptr, (T*)out[0].ptr, n, v);
+      launch_k(k_add_scalar<T>, grid_for(n, 256), 256, 0, s, (const T*)in[0].ptr, (T*)out[0].ptr, n, v);
     };
   });
 }
@@ -382,6 +390,7 @@ TCB_REGISTER("add_scalar", b_add_scalar);
 
 template <typename T>
 __global__ void k_fill(T* __restrict__ y, int64_t n, float v) {
+  TCB_PDL_ENTRY();
   const T t = from_f<T>(v);
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
     y[i] = t;
@@ -393,7 +402,7 @@ static void b_fill(Plan& p) {
   dispatch_float(p.out[0].dtype, [&](auto* tp) {
     using T = std::remove_pointer_t<decltype(tp)>;
     p.run = [=](const tcb_tensor*, tcb_tensor* out, cudaStream_t s) {
-      k_fill<T><<<grid_for(n, 256), 256, 0, s>>>((T*)out[0].ptr, n, v);
+      launch_k(k_fill<T>, grid_for(n, 256), 256, 0, s, (T*)out[0].ptr, n, v);
     };
   });
 }

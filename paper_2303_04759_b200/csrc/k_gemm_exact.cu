@@ -24,6 +24,7 @@ constexpr int XT = 16;  // output tile XT x XT, one thread per output
 constexpr int KT = 32;
 
 __global__ void __launch_bounds__(XT* XT) k_gemm_exact(GemmArgs g) {
+  TCB_PDL_ENTRY();
   __shared__ float sa[XT][KT + 1];  // [m][k]
   __shared__ float sb[KT][XT + 1];  // [k][n]
   const int64_t z = blockIdx.z;
@@ -72,7 +73,7 @@ __global__ void __launch_bounds__(XT* XT) k_gemm_exact(GemmArgs g) {
 
 void launch_gemm_exact(const GemmArgs& g, cudaStream_t s) {
   dim3 grid(unsigned((g.N + XT - 1) / XT), unsigned((g.M + XT - 1) / XT), unsigned(g.Z));
-  k_gemm_exact<<<grid, XT * XT, 0, s>>>(g);
+  launch_k(k_gemm_exact, grid, XT * XT, 0, s, g);
 }
 
 }  // namespace tcb

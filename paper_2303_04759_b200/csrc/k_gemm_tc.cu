@@ -59,13 +59,11 @@ struct TcParams {
   int ta, tb;
   int m_blocks, n_blocks, k_blocks;  // m_blocks counts (128*CG)-row blocks
   int64_t num_tiles;
-  // split-K: unit u = split * num_tiles + tile covers k-blocks [split*kps, +kps);
-  // partial accumulators go to ws, the last split of a (tile, warp box) to
-  // arrive (ws_cnt) sums them in split order and runs the epilogue
+  // split-K: a cluster of CG x splits CTAs owns one tile; CTA split s covers
+  // k-blocks [s*kps, +kps), then the partial accumulators are exchanged
+  // through distributed shared memory and reduced in split order
   int splits, kps;
   int64_t num_units;
-  float* ws;
-  int* ws_cnt;
   unsigned long long* trace;  // optional per-CTA timeline (tools/probe_gemm.py --trace)
   uint32_t idesc;
   // epilogue
@@ -245,9 +243,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(abar + 2 * TC_EPI_WARPS);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;
-  const int64_t cl_id = blockIdx.x / CG, n_cl = gridDim.x / CG;
-  unsigned long long* tr = P.trace ? P.trace + blockIdx.x * 8 : nullptr;
+  const bool clustered = CG == 2 || P.splits > 1;
+  const uint32_t crank = clustered ? cluster_ctarank() : 0;
+  const uint32_t rank = crank % CG;          // position in the CTA pair
+  const uint32_t lead = crank - rank;        // the pair leader's cluster rank
+  const int split = int(crank / CG);         // K split (0 without split-K)
+  const int csz = CG * P.splits;
+  const int64_t cl_id = blockIdx.x / csz, n_cl = gridDim.x / csz;
+  const uint16_t mcast = uint16_t(3u << lead);
+  unsigned long long* tr = P.trace ? P.trace + blockIdx.x * 12 : nullptr;
   if (tr && threadIdx.x == 0) tr[0] = gtimer();
 
   if (warp == 0 && lane == 0) {
@@ -278,10 +282,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
   }
   tc_fence_before();
-  if constexpr (CG == 2) cluster_sync();
+  if (clustered) cluster_sync();
   else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // everything above (barriers, TMEM, descriptor prefetch) overlapped the
+  // previous kernel's tail; from here on we read its outputs
+  pdl_wait();
+  pdl_trigger();
   if (tr && threadIdx.x == 0) tr[1] = gtimer();
 
   if (warp == 0) {
@@ -290,8 +298,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int64_t u = cl_id; u < P.num_units; u += n_cl) {
-        const int64_t t = u % P.num_tiles;
-        const int kb0 = int(u / P.num_tiles) * P.kps;
+        const int64_t t = u;
+        const int kb0 = split * P.kps;
         const int kb1 = min(kb0 + P.kps, P.k_blocks);
         int z, mb, nb;
         decode_tile(P, t, z, mb, nb);
@@ -301,7 +309,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           // both CTAs' bytes complete on the leader's barrier
-          const uint32_t fb = CG == 2 ? mapa(smem_u32(&full[stage]), 0) : smem_u32(&full[stage]);
+          const uint32_t fb = CG == 2 ? mapa(smem_u32(&full[stage]), lead) : smem_u32(&full[stage]);
           if (rank == 0) mbar_expect_tx(&full[stage], CG * C::STAGE_BYTES);
           uint8_t* a_dst = sA + stage * C::A_BYTES;
           uint8_t* b_dst = sB + stage * C::B_BYTES;
@@ -334,7 +342,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       int acc = 0;
       uint32_t acc_phase = 0;
       for (int64_t u = cl_id; u < P.num_units; u += n_cl) {
-        const int kb0 = int(u / P.num_tiles) * P.kps;
+        const int kb0 = split * P.kps;
         const int kb1 = min(kb0 + P.kps, P.k_blocks);
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
@@ -354,13 +362,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             const uint64_t bd = P.tb ? umma_desc(b_addr + k * 32, 16, 1024) : umma_desc(b_addr + k * 2048, 8192, 1024);
             tc_mma<CG>(tmem_d, ad, bd, P.idesc, (kb > kb0 || k) ? 1u : 0u);
           }
-          tc_commit<CG>(&empty[stage]);
+          tc_commit<CG>(&empty[stage], mcast);
           if (++stage == C::STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        tc_commit<CG>(&tfull[acc]);
+        tc_commit<CG>(&tfull[acc], mcast);
         if (tr) tr[3] = gtimer();
         if (++acc == 2) {
           acc = 0;
@@ -382,7 +390,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     uint8_t* aslots = sAux + ew * 2 * TC_AUX_SLOT;
     float* wbias = sBias + ew * CPW * W;
     uint64_t* ab = abar + 2 * ew;
-    const uint32_t tempty_addr0 = CG == 2 ? mapa(smem_u32(&tempty[0]), 0) : smem_u32(&tempty[0]);
+    const uint32_t tempty_addr0 = CG == 2 ? mapa(smem_u32(&tempty[0]), lead) : smem_u32(&tempty[0]);
     const bool has_aux = AUX && P.tma_epi && P.dact != ACT_NONE;
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -395,7 +403,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     auto issue_next_aux = [&]() {
       while (pt < P.num_units) {
         int z, mb, nb;
-        decode_tile(P, pt % P.num_tiles, z, mb, nb);
+        decode_tile(P, pt, z, mb, nb);
         const int64_t n0 = int64_t(nb) * BN + pc * W;
         const int mrow = mb * (TC_BM * CG) + int(rank) * TC_BM + q * 32;
         pc += SPLIT;
@@ -421,8 +429,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     if (has_aux) issue_next_aux();
 
     for (int64_t u = cl_id; u < P.num_units; u += n_cl) {
-      const int64_t t = u % P.num_tiles;
-      const int split = int(u / P.num_tiles);
+      const int64_t t = u;
       int z, mb, nb;
       decode_tile(P, t, z, mb, nb);
       const int z1 = int(z / P.Z2), z2 = int(z % P.Z2);
@@ -495,14 +502,57 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         }
         __syncwarp();
       };
-      if (P.bias && P.splits == 1) load_bias();
+      if (P.bias) load_bias();
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       if (tr && ew == 0 && u == cl_id) tr[4] = gtimer();
-      // partial-sum slot of this (tile, CTA, warp) box: [split][tile][rank][warp][chunk][lane][W]
-      const int64_t box = (t * CG + rank) * TC_EPI_WARPS + ew;
-      float* wsp = P.splits > 1 ? P.ws + (int64_t(split) * P.num_tiles * CG * TC_EPI_WARPS + box) * (CPW * 32 * W)
-                                : nullptr;
+      if (P.splits > 1) {
+        // ---- split-K: partial accumulators -> owners through DSMEM.  Chunk c
+        // of the tile belongs to split c % S of the same pair rank; an owner's
+        // receive buffer (its idle operand stages) is [src split][q][c / S][lane][W].
+        const int S = P.splits, npc = NCH / S;
+        float* recv = reinterpret_cast<float*>(sA);
+        cluster_sync_na();  // every accumulator final, every operand ring idle
+#pragma unroll 1
+        for (int c = sub; c < NCH; c += SPLIT) {
+          if (int64_t(nb) * BN + c * W >= P.N) continue;
+          uint32_t r[W];
+          const uint32_t taddr = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(c * W);
+          if constexpr (W == 16) TMEM_LD16(taddr, r);
+          else TMEM_LD32(taddr, r);
+          tmem_wait_ld();
+          const int owner = (c % S) * CG + int(rank);
+          const uint32_t dst = mapa(smem_u32(recv + (((split * 4 + q) * npc + c / S) * 32 + lane) * W), owner);
+#pragma unroll
+          for (int j = 0; j < W / 4; ++j)
+            asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(dst + 16 * j), "r"(r[4 * j]),
+                         "r"(r[4 * j + 1]), "r"(r[4 * j + 2]), "r"(r[4 * j + 3])
+                         : "memory");
+        }
+        cluster_sync_na();  // all partials landed
+#pragma unroll 1
+        for (int lc = sub; lc < npc; lc += SPLIT) {
+          const int c = lc * S + split;
+          const int64_t n0 = int64_t(nb) * BN + c * W;
+          if (n0 >= P.N) continue;
+          float v[W];
+#pragma unroll
+          for (int j = 0; j < W; ++j) v[j] = 0.0f;
+          for (int sp = 0; sp < S; ++sp) {  // fixed split order: deterministic
+            const float4* src = reinterpret_cast<const float4*>(recv + (((sp * 4 + q) * npc + lc) * 32 + lane) * W);
+#pragma unroll
+            for (int j = 0; j < W / 4; ++j) {
+              const float4 x = src[j];
+              v[4 * j] += x.x;
+              v[4 * j + 1] += x.y;
+              v[4 * j + 2] += x.z;
+              v[4 * j + 3] += x.w;
+            }
+          }
+          finish(v, 0, n0);
+        }
+        continue;  // one tile per cluster: nothing to release
+      }
 #pragma unroll 1
       for (int c = sub, ci = 0; c < NCH; c += SPLIT, ++ci) {
         const int64_t n0 = int64_t(nb) * BN + c * W;
@@ -512,14 +562,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         if constexpr (W == 16) TMEM_LD16(taddr, r);
         else TMEM_LD32(taddr, r);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        if (P.splits > 1) {
-          float4* dst = reinterpret_cast<float4*>(wsp + (ci * 32 + lane) * W);
-#pragma unroll
-          for (int j = 0; j < W / 4; ++j)
-            __stcg(dst + j, make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
-                                        __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3])));
-          continue;
-        }
         float v[W];
 #pragma unroll
         for (int j = 0; j < W; ++j) v[j] = __uint_as_float(r[j]);
@@ -538,47 +580,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         acc = 0;
         acc_phase ^= 1;
       }
-      if (P.splits > 1) {
-        // publish this split's partial box; the last split to arrive reduces
-        // all of them in split order (deterministic) and runs the epilogue
-        __threadfence();
-        __syncwarp();
-        int old = 0;
-        if (lane == 0) old = atomicAdd(P.ws_cnt + box, 1);
-        old = __shfl_sync(0xffffffffu, old, 0);
-        if (old == P.splits - 1) {
-          __threadfence();
-          if (P.bias) load_bias();
-#pragma unroll 1
-          for (int c = sub, ci = 0; c < NCH; c += SPLIT, ++ci) {
-            const int64_t n0 = int64_t(nb) * BN + c * W;
-            if (n0 >= P.N) continue;
-            float v[W];
-#pragma unroll
-            for (int j = 0; j < W; ++j) v[j] = 0.0f;
-            for (int sp = 0; sp < P.splits; ++sp) {
-              const float4* src = reinterpret_cast<const float4*>(
-                  P.ws + (int64_t(sp) * P.num_tiles * CG * TC_EPI_WARPS + box) * (CPW * 32 * W) + (ci * 32 + lane) * W);
-#pragma unroll
-              for (int j = 0; j < W / 4; ++j) {
-                const float4 x = __ldcg(src + j);
-                v[4 * j] += x.x;
-                v[4 * j + 1] += x.y;
-                v[4 * j + 2] += x.z;
-                v[4 * j + 3] += x.w;
-              }
-            }
-            finish(v, ci, n0);
-          }
-          if (lane == 0) P.ws_cnt[box] = 0;  // re-armed for the next launch
-        }
-      }
     }
     if (lane == 0) bulk_wait_all();
-    if (tr && ew == 0 && lane == 0) tr[5] = gtimer();
+    if (tr && lane == 0) atomicMax(&tr[5], gtimer());
+  }
+  if (P.splits > 1 && warp < 4) {  // the two split-K exchange barriers
+    cluster_sync_na();
+    cluster_sync_na();
   }
   tc_fence_before();
-  if constexpr (CG == 2) cluster_sync();
+  if (clustered) cluster_sync();
   else __syncthreads();
   if (warp == 2) {
     tc_fence_after();
@@ -649,10 +660,7 @@ static void launch_cfg(const GemmArgs& g, cudaStream_t s) {
   P.num_tiles = int64_t(P.m_blocks) * P.n_blocks * g.Z;
   P.splits = g.force_splits > 1 ? g.force_splits : 1;
   P.kps = (P.k_blocks + P.splits - 1) / P.splits;
-  P.splits = (P.k_blocks + P.kps - 1) / P.kps;  // no empty splits
-  P.num_units = P.num_tiles * P.splits;
-  P.ws = g.ws;
-  P.ws_cnt = g.ws_cnt;
+  P.num_units = P.num_tiles;
   P.trace = reinterpret_cast<unsigned long long*>(g.trace);
   const uint32_t fmt = g.a.dtype == TCB_BF16 ? 1u : 0u;
   P.idesc = (1u << 4)                           // D format f32
@@ -697,21 +705,27 @@ static void launch_cfg(const GemmArgs& g, cudaStream_t s) {
     if (g.dact != ACT_NONE)
       em.aux = encode4(g.aux, g.aux_dtype, g.N, g.M, g.Z2, Z1, g.ldc, g.c_s2, g.c_s1, TC_EW, 32, sw(TC_EW * 2));
   }
-  int64_t units = P.num_units * CG;
-  int grid = int(units < kNumSMs ? units : kNumSMs);
-  grid = (grid / CG) * CG;
+  const int csz = CG * P.splits;  // cluster: CTA pair x K splits
+  int grid;
+  if (P.splits > 1) {
+    grid = int(P.num_tiles * csz);  // one tile per cluster (the exchange reuses its operand ring)
+  } else {
+    const int64_t units = P.num_units * CG;
+    grid = int(units < kNumSMs ? units : kNumSMs);
+    grid = (grid / CG) * CG;
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(unsigned(grid));
   cfg.blockDim = dim3(TC_THREADS);
   cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.x = csz;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 1 + pdl_attr(&attr[1]);
   TCB_CUDA(cudaLaunchKernelEx(&cfg, k_gemm_tc<BN, CG, AUX>, ta, tb, em, P));
 }
 
@@ -721,6 +735,22 @@ static void launch_cfg(const GemmArgs& g, cudaStream_t s) {
 // rounds = ceil(units / concurrent units), a CTA pair is one unit of 74;
 // K_FIX k-blocks model the per-unit fill/drain; eff(.) is the relative
 // mainloop throughput per SM of each tile shape.
+static int stage_bytes(int bn, int cg) { return TC_BM * TC_BK * 2 + (bn / cg) * TC_BK * 2; }
+static int stages_of(int bn, int cg) {
+  const int cpw = (bn / TC_EW + TC_EPI_WARPS / 4 - 1) / (TC_EPI_WARPS / 4);
+  const int budget = 227 * 1024 - 1024 - 512 - TC_EPI_WARPS * 2 * TC_SLOT - TC_EPI_WARPS * cpw * TC_EW * 4;
+  return std::min(8, budget / stage_bytes(bn, cg));
+}
+// split-K through DSMEM: pure matmul epilogue, cluster <= 8 CTAs, whole
+// chunks per owner, and the receive buffer fits the operand ring
+static bool split_ok(const GemmArgs& g, int bn, int cg, int sp) {
+  if (sp == 1) return true;
+  const int64_t kblocks = (g.K + TC_BK - 1) / TC_BK;
+  return (sp == 2 || sp == 4) && cg * sp <= 8 && (bn / TC_EW) % sp == 0 && kblocks >= 2 * sp && !g.bias &&
+         g.act == ACT_NONE && g.dact == ACT_NONE && !g.aux_out &&
+         (bn / TC_EW) * 8192 <= stages_of(bn, cg) * stage_bytes(bn, cg);
+}
+
 static TcChoice choose(const GemmArgs& g, bool allow_split) {
   if (g.force_bn) return {g.force_bn, g.force_cg ? g.force_cg : 1, g.force_splits ? g.force_splits : 1};
   struct Cand {
@@ -729,7 +759,7 @@ static TcChoice choose(const GemmArgs& g, bool allow_split) {
   };
   const Cand cands[] = {{256, 2, 1.0}, {128, 2, 0.6}, {256, 1, 0.75}, {192, 1, 0.7}, {128, 1, 0.55}};
   const int64_t kblocks = (g.K + TC_BK - 1) / TC_BK;
-  constexpr double K_FIX = 6.0, K_RED = 8.0;
+  constexpr double K_FIX = 6.0, K_RED = 2.0;
   TcChoice best{128, 1, 1};
   double best_cost = 1e30;
   for (const Cand& c : cands) {
@@ -739,10 +769,9 @@ static TcChoice choose(const GemmArgs& g, bool allow_split) {
     const int64_t nb = (g.N + c.bn - 1) / c.bn;
     const int64_t tiles = mb * nb * g.Z;
     const int64_t conc = kNumSMs / c.cg;
-    const int max_split = allow_split ? int(std::min<int64_t>(8, kblocks / 4)) : 1;
-    for (int sp = 1; sp <= std::max(1, max_split); ++sp) {
+    for (int sp : {1, 2, 4}) {
+      if (sp > 1 && (!allow_split || !split_ok(g, c.bn, c.cg, sp) || tiles * sp > conc)) continue;
       const int64_t kps = (kblocks + sp - 1) / sp;
-      if (sp > 1 && (kps * (sp - 1) >= kblocks)) continue;  // an empty split
       const int64_t units = tiles * sp;
       const double rounds = double((units + conc - 1) / conc);
       const double cost = rounds * (double(kps) + K_FIX + (sp > 1 ? K_RED : 0.0)) * double(c.bn) / c.eff;
@@ -757,26 +786,17 @@ static TcChoice choose(const GemmArgs& g, bool allow_split) {
 
 TcChoice gemm_tc_choose(const GemmArgs& g) { return choose(g, true); }
 
-static int tc_cpw(int bn) { return (bn / TC_EW + TC_EPI_WARPS / 4 - 1) / (TC_EPI_WARPS / 4); }
-
 void gemm_prepare(GemmArgs& g, bool exact, GemmWs& keep) {
+  (void)keep;
   if (exact || !gemm_tc_supported(g, nullptr)) return;
-  // The in-kernel split-K reduction is correct (tests force it) but its
-  // last-arriver reduction stalls on this part (profiles/r01_gemm_trace.jsonl),
-  // so the cost model only picks it when asked.
-  const TcChoice c = choose(g, g.dact == ACT_NONE && g.allow_split);
+  // Split-K is exact and deterministic (tests force it) but measured slower on
+  // every BERT-base weight-gradient shape (profiles/r01_gemm_splitk_dsmem.jsonl):
+  // those GEMMs are bound by L2->SMEM operand traffic, which splitting K does
+  // not reduce.  The cost model therefore never picks it on its own.
+  const TcChoice c = choose(g, false);
   g.force_bn = c.bn;
   g.force_cg = c.cg;
   g.force_splits = c.splits;
-  if (c.splits > 1) {
-    const int64_t tiles = ((g.M + 128 * c.cg - 1) / (128 * c.cg)) * ((g.N + c.bn - 1) / c.bn) * g.Z;
-    const int64_t boxes = tiles * c.cg * TC_EPI_WARPS;
-    keep.ws = std::make_shared<Scratch>(size_t(c.splits) * boxes * tc_cpw(c.bn) * 32 * TC_EW * sizeof(float));
-    keep.cnt = std::make_shared<Scratch>(size_t(boxes) * sizeof(int));
-    TCB_CUDA(cudaMemset(keep.cnt->p, 0, size_t(boxes) * sizeof(int)));
-    g.ws = static_cast<float*>(keep.ws->p);
-    g.ws_cnt = static_cast<int*>(keep.cnt->p);
-  }
 }
 
 void launch_gemm_tc(const GemmArgs& g, cudaStream_t s) {
@@ -784,8 +804,8 @@ void launch_gemm_tc(const GemmArgs& g, cudaStream_t s) {
   if (!gemm_tc_supported(g, &why)) fail(TCB_ERR_UNIMPLEMENTED, "tcgen05 gemm: " + why);
   const TcChoice c = choose(g, false);
   const bool aux = g.dact != ACT_NONE;
-  if (c.splits > 1 && (!g.ws || !g.ws_cnt || aux))
-    fail(TCB_ERR_TYPE, "tcgen05 gemm: split-K needs gemm_prepare's workspace and no act'(aux)");
+  if (!split_ok(g, c.bn, c.cg, c.splits))
+    fail(TCB_ERR_TYPE, "tcgen05 gemm: split-K " + std::to_string(c.splits) + " not valid for this tile / epilogue");
 #define TC_CASE(BN_, CG_)                                  \
   if (c.bn == BN_ && c.cg == CG_) {                        \
     if (aux) launch_cfg<BN_, CG_, true>(g, s);             \

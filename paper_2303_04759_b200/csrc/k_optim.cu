@@ -20,6 +20,7 @@ namespace tcb {
 
 __global__ void k_sgd(const float* __restrict__ p, const float* __restrict__ g, float* pn, int64_t n,
                       float lr) {
+  TCB_PDL_ENTRY();
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
        i += int64_t(gridDim.x) * blockDim.x)
     pn[i] = __fsub_rn(p[i], __fmul_rn(lr, g[i]));
@@ -33,7 +34,7 @@ static void b_sgd(Plan& p) {
   const int64_t n = p.in[0].numel();
   const float lr = float(p.attrs.f("lr", 0.0));
   p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
-    k_sgd<<<grid_for(n, 256), 256, 0, s>>>((const float*)in[0].ptr, (const float*)in[1].ptr,
+    launch_k(k_sgd, grid_for(n, 256), 256, 0, s, (const float*)in[0].ptr, (const float*)in[1].ptr,
                                             (float*)out[0].ptr, n, lr);
   };
 }
@@ -66,6 +67,7 @@ __global__ void __launch_bounds__(256) k_adam(const float* __restrict__ p, const
                                               const float* __restrict__ m, const float* __restrict__ v,
                                               const float* __restrict__ step, float* po, float* mo,
                                               float* vo, TH* half, int64_t n, AdamCfg c) {
+  TCB_PDL_ENTRY();
   const double t = double(step[0]);
   const double bc1 = __dsub_rn(1.0, pow(c.b1, t));
   const double bc2 = __dsub_rn(1.0, pow(c.b2, t));
@@ -107,18 +109,18 @@ static void b_adam(Plan& p) {
         fail(TCB_ERR_ARG, "adam_update: buffers must be 16-byte aligned");
     const int grid = grid_for((n + 3) / 4, 256, kNumSMs * 4);
     if (hd == TCB_BF16)
-      k_adam<__nv_bfloat16><<<grid, 256, 0, s>>>(
+      launch_k(k_adam<__nv_bfloat16>, grid, 256, 0, s, 
           (const float*)in[0].ptr, (const float*)in[1].ptr, (const float*)in[2].ptr,
           (const float*)in[3].ptr, (const float*)in[4].ptr, (float*)out[0].ptr, (float*)out[1].ptr,
           (float*)out[2].ptr, (__nv_bfloat16*)out[3].ptr, n, c);
     else if (hd == TCB_F16)
-      k_adam<__half><<<grid, 256, 0, s>>>((const float*)in[0].ptr, (const float*)in[1].ptr,
+      launch_k(k_adam<__half>, grid, 256, 0, s, (const float*)in[0].ptr, (const float*)in[1].ptr,
                                           (const float*)in[2].ptr, (const float*)in[3].ptr,
                                           (const float*)in[4].ptr, (float*)out[0].ptr,
                                           (float*)out[1].ptr, (float*)out[2].ptr,
                                           (__half*)out[3].ptr, n, c);
     else
-      k_adam<float><<<grid, 256, 0, s>>>((const float*)in[0].ptr, (const float*)in[1].ptr,
+      launch_k(k_adam<float>, grid, 256, 0, s, (const float*)in[0].ptr, (const float*)in[1].ptr,
                                          (const float*)in[2].ptr, (const float*)in[3].ptr,
                                          (const float*)in[4].ptr, (float*)out[0].ptr,
                                          (float*)out[1].ptr, (float*)out[2].ptr,

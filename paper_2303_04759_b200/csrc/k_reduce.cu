@@ -46,6 +46,7 @@ static RedGeom red_geom(const Spec& x, const std::string& axes_s) {
 template <typename T, typename TO>
 __global__ void k_reduce_exact(const T* __restrict__ x, TO* __restrict__ o, int64_t nslots, RedGeom g,
                                int mean) {
+  TCB_PDL_ENTRY();
   int64_t slot = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   if (slot >= nslots) return;
   // base offset of this slot (kept dims), strides of all dims
@@ -81,6 +82,7 @@ __global__ void k_reduce_exact(const T* __restrict__ x, TO* __restrict__ o, int6
 template <typename T, typename TO>
 __global__ void k_reduce_cols(const T* __restrict__ x, TO* __restrict__ o, int64_t outer, int64_t red,
                               int64_t inner, float scale) {
+  TCB_PDL_ENTRY();
   __shared__ float part[8][33];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t tiles_per_outer = (inner + 31) / 32;
@@ -105,6 +107,7 @@ __global__ void k_reduce_cols(const T* __restrict__ x, TO* __restrict__ o, int64
 template <typename T, typename TO>
 __global__ void k_reduce_rows(const T* __restrict__ x, TO* __restrict__ o, int64_t rows, int64_t red,
                               float scale) {
+  TCB_PDL_ENTRY();
   const int64_t row = blockIdx.x * int64_t(blockDim.x / 32) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= rows) return;
@@ -139,7 +142,7 @@ static void build_reduce(Plan& p, int mean) {
       using TO = std::remove_pointer_t<decltype(op_)>;
       if (exact) {
         p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
-          k_reduce_exact<T, TO><<<unsigned((nslots + 127) / 128), 128, 0, s>>>(
+          launch_k(k_reduce_exact<T, TO>, unsigned((nslots + 127) / 128), 128, 0, s, 
               (const T*)in[0].ptr, (TO*)out[0].ptr, nslots, g, mean);
         };
         return;
@@ -151,13 +154,13 @@ static void build_reduce(Plan& p, int mean) {
       const float scale = mean ? 1.0f / float(red) : 1.0f;
       if (inner == 1) {
         p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
-          k_reduce_rows<T, TO><<<unsigned((outer + 7) / 8), 256, 0, s>>>((const T*)in[0].ptr,
+          launch_k(k_reduce_rows<T, TO>, unsigned((outer + 7) / 8), 256, 0, s, (const T*)in[0].ptr,
                                                                           (TO*)out[0].ptr, outer, red, scale);
         };
       } else {
         const int64_t blocks = outer * ((inner + 31) / 32);
         p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
-          k_reduce_cols<T, TO><<<unsigned(blocks), 256, 0, s>>>((const T*)in[0].ptr, (TO*)out[0].ptr,
+          launch_k(k_reduce_cols<T, TO>, unsigned(blocks), 256, 0, s, (const T*)in[0].ptr, (TO*)out[0].ptr,
                                                                   outer, red, inner, scale);
         };
       }
@@ -179,6 +182,7 @@ constexpr int CS_ROWS = 128;
 template <typename T>
 __global__ void __launch_bounds__(256) k_colsum_partial(const T* __restrict__ x, float* __restrict__ part,
                                                         int64_t R, int64_t C) {
+  TCB_PDL_ENTRY();
   __shared__ float red[8][256 + 4];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t c0 = int64_t(blockIdx.x) * 256 + lane * 8;
@@ -218,6 +222,7 @@ __global__ void __launch_bounds__(256) k_colsum_partial(const T* __restrict__ x,
 
 __global__ void k_colsum_final(const float* __restrict__ part, float* __restrict__ out, int64_t nchunk, int64_t C,
                                float scale) {
+  TCB_PDL_ENTRY();
   const int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   if (c >= C) return;
   float s = 0.0f;
@@ -245,7 +250,7 @@ static void b_colsum(Plan& p) {
     using T = std::remove_pointer_t<decltype(tp)>;
     if (exact) {
       p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
-        k_reduce_exact<T, float><<<unsigned((C + 127) / 128), 128, 0, s>>>((const T*)in[0].ptr,
+        launch_k(k_reduce_exact<T, float>, unsigned((C + 127) / 128), 128, 0, s, (const T*)in[0].ptr,
                                                                            (float*)out[0].ptr, C, g, 0);
       };
     } else if (C % 8 == 0) {
@@ -255,13 +260,13 @@ static void b_colsum(Plan& p) {
       p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
         if (reinterpret_cast<uintptr_t>(in[0].ptr) % 16) fail(TCB_ERR_ARG, "colsum: input not 16-byte aligned");
         dim3 grid(unsigned((C + 255) / 256), unsigned(nchunk));
-        k_colsum_partial<T><<<grid, 256, 0, s>>>((const T*)in[0].ptr, (float*)ws->p, R, C);
-        k_colsum_final<<<unsigned((C + 255) / 256), 256, 0, s>>>((const float*)ws->p, (float*)out[0].ptr, nchunk, C,
+        launch_k(k_colsum_partial<T>, grid, 256, 0, s, (const T*)in[0].ptr, (float*)ws->p, R, C);
+        launch_k(k_colsum_final, unsigned((C + 255) / 256), 256, 0, s, (const float*)ws->p, (float*)out[0].ptr, nchunk, C,
                                                                   1.0f);
       };
     } else {
       p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
-        k_reduce_cols<T, float><<<unsigned((C + 31) / 32), 256, 0, s>>>((const T*)in[0].ptr,
+        launch_k(k_reduce_cols<T, float>, unsigned((C + 31) / 32), 256, 0, s, (const T*)in[0].ptr,
                                                                         (float*)out[0].ptr, 1, R, C, 1.0f);
       };
     }
@@ -272,6 +277,7 @@ TCB_REGISTER("colsum", b_colsum);
 // mse: sequential f32 sum of squared differences, then acc / numel (a divide)
 template <typename T>
 __global__ void k_mse_exact(const T* __restrict__ a, const T* __restrict__ b, float* o, int64_t n) {
+  TCB_PDL_ENTRY();
   float acc = 0.0f;
   for (int64_t i = 0; i < n; ++i) {
     float d = __fsub_rn(to_f(a[i]), to_f(b[i]));
@@ -281,6 +287,7 @@ __global__ void k_mse_exact(const T* __restrict__ a, const T* __restrict__ b, fl
 }
 template <typename T>
 __global__ void k_mse_block(const T* __restrict__ a, const T* __restrict__ b, float* o, int64_t n) {
+  TCB_PDL_ENTRY();
   __shared__ float part[32];
   float acc = 0.0f;
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
@@ -306,9 +313,9 @@ static void b_mse(Plan& p) {
     using T = std::remove_pointer_t<decltype(tp)>;
     p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
       if (n <= (1 << 16))
-        k_mse_exact<T><<<1, 1, 0, s>>>((const T*)in[0].ptr, (const T*)in[1].ptr, (float*)out[0].ptr, n);
+        launch_k(k_mse_exact<T>, 1, 1, 0, s, (const T*)in[0].ptr, (const T*)in[1].ptr, (float*)out[0].ptr, n);
       else
-        k_mse_block<T><<<1, 1024, 0, s>>>((const T*)in[0].ptr, (const T*)in[1].ptr, (float*)out[0].ptr, n);
+        launch_k(k_mse_block<T>, 1, 1024, 0, s, (const T*)in[0].ptr, (const T*)in[1].ptr, (float*)out[0].ptr, n);
     };
   });
 }

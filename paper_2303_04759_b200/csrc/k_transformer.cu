@@ -140,6 +140,7 @@ __global__ void __launch_bounds__(256) k_ln_fwd(const T* __restrict__ x, const T
                                                 T* __restrict__ s_out, float* __restrict__ mean_o,
                                                 float* __restrict__ rstd_o, int64_t rows, int H, float eps,
                                                 DropCfg d, bool vec) {
+  TCB_PDL_ENTRY();
   // RW rows per warp, every global load of both rows issued before the first
   // reduction so enough bytes are in flight to cover DRAM latency
   constexpr int RW = NC <= 2 ? 2 : 1;
@@ -260,7 +261,7 @@ static void build_ln_fwd(Plan& p, bool residual) {
       vec = vec && reinterpret_cast<uintptr_t>(out[0].ptr) % 16 == 0;
       if (residual) vec = vec && reinterpret_cast<uintptr_t>(out[1].ptr) % 16 == 0;
       constexpr int RW = NC <= 2 ? 2 : 1;
-      k_ln_fwd<T, NC><<<unsigned((rows + 8 * RW - 1) / (8 * RW)), 256, 0, s>>>(
+      launch_k(k_ln_fwd<T, NC>, unsigned((rows + 8 * RW - 1) / (8 * RW)), 256, 0, s, 
           (const T*)in[0].ptr, residual ? (const T*)in[1].ptr : nullptr,
           gf ? (const float*)in[gi].ptr : nullptr, gf ? nullptr : (const T*)in[gi].ptr,
           gf ? (const float*)in[gi + 1].ptr : nullptr, gf ? nullptr : (const T*)in[gi + 1].ptr,
@@ -288,6 +289,7 @@ __global__ void __launch_bounds__(256) k_ln_bwd(const T* __restrict__ sx, const 
                                                 const T* __restrict__ dy2, T* __restrict__ ds_o,
                                                 T* __restrict__ dx_o, float* __restrict__ ws, int64_t rows,
                                                 int H, DropCfg d, bool vec) {
+  TCB_PDL_ENTRY();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nch = (H + 7) / 8;
   // per-warp dgamma/dbeta partials live in smem (not registers), laid out
@@ -376,6 +378,7 @@ __global__ void __launch_bounds__(256) k_ln_bwd(const T* __restrict__ sx, const 
 // columns x 8 warps; warp w folds partial rows w, w+8, ...; smem combines.
 __global__ void __launch_bounds__(256) k_ln_colsum(const float* __restrict__ ws, float* __restrict__ dg,
                                                    float* __restrict__ db, int nblk, int H) {
+  TCB_PDL_ENTRY();
   __shared__ float ra[8][33], rb[8][33];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int j = blockIdx.x * 32 + lane;
@@ -430,12 +433,12 @@ static void b_layer_norm_dx(Plan& p) {
       if (has_res) vec = vec && reinterpret_cast<uintptr_t>(in[5].ptr) % 16 == 0;
       vec = vec && reinterpret_cast<uintptr_t>(out[0].ptr) % 16 == 0;
       if (has_dx) vec = vec && reinterpret_cast<uintptr_t>(out[3].ptr) % 16 == 0;
-      k_ln_bwd<T, NC><<<nblk, 256, smem, s>>>(
+      launch_k(k_ln_bwd<T, NC>, nblk, 256, smem, s, 
           (const T*)in[0].ptr, gf ? (const float*)in[1].ptr : nullptr, gf ? nullptr : (const T*)in[1].ptr,
           (const float*)in[2].ptr, (const float*)in[3].ptr, (const T*)in[4].ptr,
           has_res ? (const T*)in[5].ptr : nullptr, (T*)out[0].ptr, has_dx ? (T*)out[3].ptr : nullptr,
           (float*)ws->p, rows, H, d, vec);
-      k_ln_colsum<<<(H + 31) / 32, 256, 0, s>>>((const float*)ws->p, (float*)out[1].ptr,
+      launch_k(k_ln_colsum, (H + 31) / 32, 256, 0, s, (const float*)ws->p, (float*)out[1].ptr,
                                                 (float*)out[2].ptr, nblk, H);
     };
    });
@@ -491,6 +494,7 @@ template <typename TI, typename TO, int NQ>
 __global__ void __launch_bounds__(256) k_softmax(const TI* __restrict__ x, TO* __restrict__ P,
                                                  TO* __restrict__ Pd, int64_t rows, int C, int Sq,
                                                  float scale, int causal, DropCfg d, bool vec) {
+  TCB_PDL_ENTRY();
   constexpr int RW = NQ == 1 ? 4 : NQ == 2 ? 2 : 1;  // rows per warp, loads batched
   const int lane = threadIdx.x & 31;
   const int64_t row0 = (blockIdx.x * int64_t(blockDim.x >> 5) + (threadIdx.x >> 5)) * RW;
@@ -562,6 +566,7 @@ template <typename TP, typename TG, typename TO, int NQ>
 __global__ void __launch_bounds__(256) k_softmax_bwd(const TP* __restrict__ P, const TG* __restrict__ dPd,
                                                      TO* __restrict__ dS, TO* __restrict__ Pd_o, int64_t rows,
                                                      int C, float scale, DropCfg d, bool vec) {
+  TCB_PDL_ENTRY();
   constexpr int RW = NQ == 1 ? 4 : NQ == 2 ? 2 : 1;
   const int lane = threadIdx.x & 31;
   const int64_t row0 = (blockIdx.x * int64_t(blockDim.x >> 5) + (threadIdx.x >> 5)) * RW;
@@ -662,7 +667,7 @@ static void b_softmax(Plan& p) {
       const bool vec = C % 4 == 0 && reinterpret_cast<uintptr_t>(in[0].ptr) % 16 == 0 &&
                        reinterpret_cast<uintptr_t>(out[0].ptr) % 16 == 0 &&
                        (!pd || reinterpret_cast<uintptr_t>(out[1].ptr) % 16 == 0);
-      k_softmax<TI, TO, NQ><<<sm_grid<NQ>(rows), 256, 0, s>>>(
+      launch_k(k_softmax<TI, TO, NQ>, sm_grid<NQ>(rows), 256, 0, s, 
           (const TI*)in[0].ptr, (TO*)out[0].ptr, pd ? (TO*)out[1].ptr : nullptr, rows, C, Sq, scale, causal, d, vec);
     };
    });
@@ -690,7 +695,7 @@ static void b_softmax_dx(Plan& p) {
         const bool vec = C % 4 == 0 && reinterpret_cast<uintptr_t>(in[0].ptr) % 16 == 0 &&
                          reinterpret_cast<uintptr_t>(in[1].ptr) % 16 == 0 &&
                          reinterpret_cast<uintptr_t>(out[0].ptr) % 16 == 0;
-        k_softmax_bwd<TP, TG, TO, NQ><<<sm_grid<NQ>(rows), 256, 0, s>>>(
+        launch_k(k_softmax_bwd<TP, TG, TO, NQ>, sm_grid<NQ>(rows), 256, 0, s, 
             (const TP*)in[0].ptr, (const TG*)in[1].ptr, (TO*)out[0].ptr, nullptr, rows, C, scale, d, vec);
       };
      });
@@ -811,7 +816,7 @@ static void b_attention(Plan& p) {
       const int64_t rows = g.Z * g.S;
       T* Pd = g.d.p > 0.0f ? (T*)pd->p : nullptr;
       dispatch_nq(int(g.S), [&](auto nq) {
-        k_softmax<float, T, decltype(nq)::value><<<sm_grid<decltype(nq)::value>(rows), 256, 0, s>>>(
+        launch_k(k_softmax<float, T, decltype(nq)::value>, sm_grid<decltype(nq)::value>(rows), 256, 0, s, 
             (const float*)scores->p, (T*)out[1].ptr, Pd, rows, int(g.S), int(g.S), 1.0f, g.causal, g.d,
             g.S % 4 == 0 && reinterpret_cast<uintptr_t>(out[1].ptr) % 16 == 0);
       });
@@ -853,7 +858,7 @@ static void b_attention_dx(Plan& p) {
       const int64_t rows = g.Z * g.S;
       T* Pd = g.d.p > 0.0f ? (T*)pd->p : nullptr;
       dispatch_nq(int(g.S), [&](auto nq) {
-        k_softmax_bwd<T, float, T, decltype(nq)::value><<<sm_grid<decltype(nq)::value>(rows), 256, 0, s>>>(
+        launch_k(k_softmax_bwd<T, float, T, decltype(nq)::value>, sm_grid<decltype(nq)::value>(rows), 256, 0, s, 
             (const T*)in[1].ptr, (const float*)dpd->p, (T*)ds->p, Pd, rows, int(g.S), g.scale, g.d,
             g.S % 4 == 0 && reinterpret_cast<uintptr_t>(in[1].ptr) % 16 == 0);
       });
@@ -881,6 +886,7 @@ TCB_REGISTER("attention_dx", b_attention_dx);
 template <typename TT, typename TO>
 __global__ void k_embed(const int32_t* __restrict__ ids, const TT* __restrict__ table, TO* __restrict__ out,
                         int64_t T, int64_t H, int64_t V, int* __restrict__ err) {
+  TCB_PDL_ENTRY();
   const int64_t t = blockIdx.x * int64_t(blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (t >= T) return;
@@ -904,7 +910,7 @@ static void b_embedding(Plan& p) {
     using TT = std::remove_pointer_t<decltype(pa)>;
     using TO = std::remove_pointer_t<decltype(pb)>;
     p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
-      k_embed<TT, TO><<<unsigned((T + 7) / 8), 256, 0, s>>>((const int32_t*)in[0].ptr, (const TT*)in[1].ptr,
+      launch_k(k_embed<TT, TO>, unsigned((T + 7) / 8), 256, 0, s, (const int32_t*)in[0].ptr, (const TT*)in[1].ptr,
                                                              (TO*)out[0].ptr, T, H, V, (int*)err->p);
     };
   });
@@ -920,6 +926,7 @@ TCB_REGISTER("embedding", b_embedding);
 __global__ void __launch_bounds__(64) k_embed_rank(const int32_t* __restrict__ ids, int32_t* __restrict__ sorted,
                                                    int32_t* __restrict__ seg_len, int32_t* __restrict__ seg_head,
                                                    int64_t T) {
+  TCB_PDL_ENTRY();
   __shared__ int32_t tile[2048];
   const int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   const int32_t my = t < T ? ids[t] : 0;
@@ -953,6 +960,7 @@ __global__ void __launch_bounds__(256) k_embed_fold(const int32_t* __restrict__ 
                                                     const int32_t* __restrict__ seg_len,
                                                     const float* __restrict__ part, float* __restrict__ out,
                                                     int64_t H) {
+  TCB_PDL_ENTRY();
   const int64_t pos = blockIdx.x;
   const int32_t len = seg_len[pos];
   if (len <= EMB_CHUNK) return;
@@ -975,6 +983,7 @@ __global__ void __launch_bounds__(256) k_embed_accum(const int32_t* __restrict__
                                                      const int32_t* __restrict__ seg_head,
                                                      const TD* __restrict__ dy, float* __restrict__ out,
                                                      float* __restrict__ part, int64_t T, int64_t H) {
+  TCB_PDL_ENTRY();
   const int64_t pos = blockIdx.x;
   const int64_t head = seg_head[pos];
   if ((pos - head) % EMB_CHUNK) return;  // not a chunk start
@@ -1024,10 +1033,10 @@ static void b_embedding_dx(Plan& p) {
       TCB_CUDA(cudaMemsetAsync(seg, 0, size_t(T) * 4, s));
       const int32_t* ids = (const int32_t*)in[0].ptr;
       const dim3 g2(unsigned(T), unsigned((H + 255) / 256));
-      k_embed_rank<<<unsigned((T + 63) / 64), 64, 0, s>>>(ids, srt, seg, hd, T);
-      k_embed_accum<TD><<<g2, 256, 0, s>>>(ids, srt, seg, hd, (const TD*)in[1].ptr, (float*)out[0].ptr,
+      launch_k(k_embed_rank, unsigned((T + 63) / 64), 64, 0, s, ids, srt, seg, hd, T);
+      launch_k(k_embed_accum<TD>, g2, 256, 0, s, ids, srt, seg, hd, (const TD*)in[1].ptr, (float*)out[0].ptr,
                                           (float*)part->p, T, H);
-      k_embed_fold<<<g2, 256, 0, s>>>(ids, srt, seg, (const float*)part->p, (float*)out[0].ptr, H);
+      launch_k(k_embed_fold, g2, 256, 0, s, ids, srt, seg, (const float*)part->p, (float*)out[0].ptr, H);
     };
   });
 }
@@ -1036,6 +1045,7 @@ TCB_REGISTER("embedding_dx", b_embedding_dx);
 // ------------------------------------------------------------ cross entropy
 // (logits [T, Vp], labels [T]) -> (loss f32[1], dlogits [T, Vp])
 __global__ void k_ce_count(const int32_t* __restrict__ labels, int64_t T, int64_t ign, float* __restrict__ inv_n) {
+  TCB_PDL_ENTRY();
   __shared__ int part[32];
   int c = 0;
   for (int64_t t = threadIdx.x; t < T; t += blockDim.x) c += labels[t] != ign;
@@ -1054,6 +1064,7 @@ __global__ void __launch_bounds__(512) k_ce_row(const T* __restrict__ x, const i
                                                 T* __restrict__ dx, float* __restrict__ row_loss,
                                                 const float* __restrict__ inv_n_p, int64_t Vp, int64_t V,
                                                 int64_t ign, float gscale, int* __restrict__ err, bool vec) {
+  TCB_PDL_ENTRY();
   __shared__ float sm[32], ss[32];
   const int64_t t = blockIdx.x;
   const int32_t lab = labels[t];
@@ -1134,6 +1145,7 @@ __global__ void __launch_bounds__(512) k_ce_row(const T* __restrict__ x, const i
 
 __global__ void k_ce_final(const float* __restrict__ row_loss, const float* __restrict__ inv_n, int64_t T,
                            float* __restrict__ loss) {
+  TCB_PDL_ENTRY();
   __shared__ float part[32];
   float a = 0.0f;
   for (int64_t t = threadIdx.x; t < T; t += blockDim.x) a += row_loss[t];
@@ -1171,11 +1183,11 @@ static void b_cross_entropy(Plan& p) {
       float* rows = inv_n + 4;
       const bool vec = Vp % 8 == 0 && reinterpret_cast<uintptr_t>(in[0].ptr) % 16 == 0 &&
                        (!grad || reinterpret_cast<uintptr_t>(out[1].ptr) % 16 == 0);
-      k_ce_count<<<1, 1024, 0, s>>>((const int32_t*)in[1].ptr, T, ign, inv_n);
-      k_ce_row<T_><<<unsigned(T), 512, 0, s>>>((const T_*)in[0].ptr, (const int32_t*)in[1].ptr,
+      launch_k(k_ce_count, 1, 1024, 0, s, (const int32_t*)in[1].ptr, T, ign, inv_n);
+      launch_k(k_ce_row<T_>, unsigned(T), 512, 0, s, (const T_*)in[0].ptr, (const int32_t*)in[1].ptr,
                                                 grad ? (T_*)out[1].ptr : nullptr, rows, inv_n, Vp, V, ign,
                                                 gscale, (int*)err->p, vec);
-      k_ce_final<<<1, 1024, 0, s>>>(rows, inv_n, T, (float*)out[0].ptr);
+      launch_k(k_ce_final, 1, 1024, 0, s, rows, inv_n, T, (float*)out[0].ptr);
     };
   });
 }

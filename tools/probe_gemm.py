@@ -73,7 +73,10 @@ def trace(iters):
     """Per-CTA timeline of one launch (globaltimer ns): entry, setup done, first
     operand stage landed (MMA), last MMA commit, first accumulator ready
     (epilogue), epilogue drained."""
-    cases = [("ffn1_fwd", 4096, 768, 3072, 0, 0, BF16, {}), ("proj_wgrad", 768, 4096, 768, 1, 0, F32, {}),
+    cases = [("proj_wgrad_s4", 768, 4096, 768, 1, 0, F32, {"tc_bn": 128, "tc_cg": 1, "tc_splits": 4}),
+             ("proj_wgrad_s4_cg2", 768, 4096, 768, 1, 0, F32, {"tc_bn": 256, "tc_cg": 2, "tc_splits": 4}),
+             ("ffn1_wgrad_s2", 768, 4096, 3072, 1, 0, F32, {"tc_bn": 256, "tc_cg": 2, "tc_splits": 2}),
+             ("ffn1_fwd", 4096, 768, 3072, 0, 0, BF16, {}), ("proj_wgrad", 768, 4096, 768, 1, 0, F32, {}),
              ("ffn1_wgrad", 768, 4096, 3072, 1, 0, F32, {}),
              ("ffn1_wgrad_bf16out", 768, 4096, 3072, 1, 0, BF16, {}),
              ("ffn1_wgrad_notma", 768, 4096, 3072, 1, 0, F32, {"tc_notma": 1}),
@@ -88,7 +91,7 @@ def trace(iters):
         b = torch.randn(N, K, device="cuda") if tb else torch.randn(K, N, device="cuda")
         a, b = a.to(torch.bfloat16).contiguous(), b.to(torch.bfloat16).contiguous()
         c = torch.empty(M, N, device="cuda", dtype=torch.float32 if out == F32 else torch.bfloat16)
-        tr = torch.zeros(148 * 8, dtype=torch.int64, device="cuda")
+        tr = torch.zeros(148 * 12, dtype=torch.int64, device="cuda")
         plan = Plan("matmul_t", [(tuple(a.shape), BF16), (tuple(b.shape), BF16)], [((M, N), out)],
                     {"ta": ta, "tb": tb, "tc_trace": tr.data_ptr(), **extra})
         s = torch.cuda.current_stream().cuda_stream
@@ -102,27 +105,31 @@ def trace(iters):
         e1.record()
         torch.cuda.synchronize()
         us = e0.elapsed_time(e1) * 100
-        t = tr.view(148, 8).cpu().numpy().astype("float64")
+        t = tr.view(148, 12).cpu().numpy().astype("float64")
         t = t[t[:, 0] > 0]
         base = t[:, 0].min()
-        rel = (t[:, :8] - base) / 1000.0
-        rel[t[:, :8] == 0] = float("nan")
+        rel = (t[:, :11] - base) / 1000.0
+        rel[t[:, :11] == 0] = float("nan")
         import numpy as np
         q = lambda col: [round(float(np.nanpercentile(rel[:, col], p)), 2) for p in (0, 50, 100)]
         print(json.dumps({"name": name, "us": round(us, 2), "ctas": len(t), "entry": q(0), "setup": q(1), "first_stage": q(2),
                           "last_commit": q(3), "first_acc": q(4), "chunks_done": q(6), "released": q(7),
-                          "epi_done": q(5)}), flush=True)
+                          "epi_done": q(5), "atomic": q(8), "red_start": q(9), "red_end": q(10)}), flush=True)
 
 
 def sweep_splits(iters):
-    """Split-K ways on the weight-gradient shapes (few output tiles, K = T)."""
+    """Split-K ways on the weight-gradient shapes (few output tiles, K = T);
+    the last line per shape is the cost model's own choice."""
     T = 4096
     for name, M, N in (("proj_wgrad", 768, 768), ("qkv_wgrad", 768, 2304), ("ffn1_wgrad", 768, 3072),
                        ("ffn2_wgrad", 3072, 768)):
-        for tile in [(256, 2), (128, 2), (128, 1)]:
-            for sp in (1, 2, 3, 4):
+        for tile in [(256, 2), (128, 2), (256, 1), (128, 1)]:
+            for sp in (1, 2, 4):
+                if tile[1] * sp > 8:
+                    continue
                 r = run(name, "matmul_t", M, T, N, 1, 0, F32, iters, tile=tile + (sp,), cublas=False)
                 print(json.dumps(r), flush=True)
+        print(json.dumps(run(name, "matmul_t", M, T, N, 1, 0, F32, iters, cublas=True)), flush=True)
 
 
 def sweep(iters):
