@@ -177,7 +177,7 @@ TCB_REGISTER("mean", b_mean);
 // 16-byte load per row), the 8 warps interleave rows, smem folds the warps and
 // the block writes one partial row; k_colsum_final adds the partials in chunk
 // order.  Deterministic; fills the machine at any R.
-constexpr int CS_ROWS = 128;
+constexpr int CS_ROWS = 32;  // rows per block: 4 per warp, all loads in flight at once
 
 template <typename T>
 __global__ void __launch_bounds__(256) k_colsum_partial(const T* __restrict__ x, float* __restrict__ part,
@@ -192,20 +192,27 @@ __global__ void __launch_bounds__(256) k_colsum_partial(const T* __restrict__ x,
 #pragma unroll
   for (int k = 0; k < 8; ++k) acc[k] = 0.0f;
   if (c0 < C) {
-    for (int64_t r = r0 + warp; r < r1; r += 8) {
-      float f[8];
-      if constexpr (sizeof(T) == 2) {
-        uint4 q = *reinterpret_cast<const uint4*>(x + r * C + c0);
-        const T* h = reinterpret_cast<const T*>(&q);
+    constexpr int RPW = CS_ROWS / 8;
+    if constexpr (sizeof(T) == 2) {
+      uint4 q[RPW];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) f[k] = to_f(h[k]);
-      } else {
-        float4 a = *reinterpret_cast<const float4*>(x + r * C + c0);
-        float4 b = *reinterpret_cast<const float4*>(x + r * C + c0 + 4);
-        f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w; f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
+      for (int i = 0; i < RPW; ++i) {
+        const int64_t r = r0 + warp + 8 * i;
+        q[i] = r < r1 ? *reinterpret_cast<const uint4*>(x + r * C + c0) : make_uint4(0, 0, 0, 0);
       }
 #pragma unroll
-      for (int k = 0; k < 8; ++k) acc[k] += f[k];
+      for (int i = 0; i < RPW; ++i) {
+        const T* h = reinterpret_cast<const T*>(&q[i]);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc[k] += to_f(h[k]);
+      }
+    } else {
+      for (int64_t r = r0 + warp; r < r1; r += 8) {
+        float4 a = *reinterpret_cast<const float4*>(x + r * C + c0);
+        float4 b = *reinterpret_cast<const float4*>(x + r * C + c0 + 4);
+        acc[0] += a.x; acc[1] += a.y; acc[2] += a.z; acc[3] += a.w;
+        acc[4] += b.x; acc[5] += b.y; acc[6] += b.z; acc[7] += b.w;
+      }
     }
   }
 #pragma unroll
@@ -220,14 +227,27 @@ __global__ void __launch_bounds__(256) k_colsum_partial(const T* __restrict__ x,
   }
 }
 
-__global__ void k_colsum_final(const float* __restrict__ part, float* __restrict__ out, int64_t nchunk, int64_t C,
-                               float scale) {
+// block = 32 columns x 8 warps; warp w sums partial rows w, w+8, ... (loads
+// unrolled 4 deep), then warp 0 adds the 8 warp sums in order: deterministic
+__global__ void __launch_bounds__(256) k_colsum_final(const float* __restrict__ part, float* __restrict__ out,
+                                                      int64_t nchunk, int64_t C, float scale) {
   TCB_PDL_ENTRY();
-  const int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-  if (c >= C) return;
+  __shared__ float red[8][33];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t c = int64_t(blockIdx.x) * 32 + lane;
   float s = 0.0f;
-  for (int64_t k = 0; k < nchunk; ++k) s += part[k * C + c];
-  out[c] = s * scale;
+  if (c < C) {
+#pragma unroll 4
+    for (int64_t k = warp; k < nchunk; k += 8) s += part[k * C + c];
+  }
+  red[warp][lane] = s;
+  __syncthreads();
+  if (warp == 0 && c < C) {
+    float t = 0.0f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) t += red[w][lane];
+    out[c] = t * scale;
+  }
 }
 
 // colsum: f32 column sums over all leading dims (bias gradients of [T, N]
@@ -261,7 +281,7 @@ static void b_colsum(Plan& p) {
         if (reinterpret_cast<uintptr_t>(in[0].ptr) % 16) fail(TCB_ERR_ARG, "colsum: input not 16-byte aligned");
         dim3 grid(unsigned((C + 255) / 256), unsigned(nchunk));
         launch_k(k_colsum_partial<T>, grid, 256, 0, s, (const T*)in[0].ptr, (float*)ws->p, R, C);
-        launch_k(k_colsum_final, unsigned((C + 255) / 256), 256, 0, s, (const float*)ws->p, (float*)out[0].ptr, nchunk, C,
+        launch_k(k_colsum_final, unsigned((C + 31) / 32), 256, 0, s, (const float*)ws->p, (float*)out[0].ptr, nchunk, C,
                                                                   1.0f);
       };
     } else {

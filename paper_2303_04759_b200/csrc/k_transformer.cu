@@ -923,27 +923,41 @@ TCB_REGISTER("embedding", b_embedding);
 // Stable counting rank of token t among all T ids (ids staged through smem in
 // tiles); the first occurrence of each id also records its segment length at
 // the segment's head position (seg_len is zeroed beforehand).
-__global__ void __launch_bounds__(64) k_embed_rank(const int32_t* __restrict__ ids, int32_t* __restrict__ sorted,
-                                                   int32_t* __restrict__ seg_len, int32_t* __restrict__ seg_head,
-                                                   int64_t T) {
+// Stable rank of every token by (id, t): rank = #{u : id_u < id_t} +
+// #{u < t : id_u == id_t}.  One warp per token, lanes split the scan of a
+// shared-memory id tile and combine with shuffles (O(T^2 / 32) per warp, spread
+// over the whole GPU: T = 4096 is ~2 us).  Writes the sorted order and, per
+// sorted position, its segment head and (at heads) the segment length.
+constexpr int RANK_TILE = 4096;
+__global__ void __launch_bounds__(256) k_embed_rank(const int32_t* __restrict__ ids, int32_t* __restrict__ sorted,
+                                                    int32_t* __restrict__ seg_len, int32_t* __restrict__ seg_head,
+                                                    int64_t T) {
   TCB_PDL_ENTRY();
-  __shared__ int32_t tile[2048];
-  const int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  __shared__ int32_t tile[RANK_TILE];
+  const int lane = threadIdx.x & 31;
+  const int64_t t = blockIdx.x * 8 + (threadIdx.x >> 5);
   const int32_t my = t < T ? ids[t] : 0;
-  int64_t less = 0, eq_before = 0, eq = 0;
-  for (int64_t u0 = 0; u0 < T; u0 += 2048) {
-    const int64_t n = T - u0 < 2048 ? T - u0 : 2048;
+  int less = 0, eq_before = 0, eq = 0;
+  for (int64_t u0 = 0; u0 < T; u0 += RANK_TILE) {
+    const int n = int(T - u0 < RANK_TILE ? T - u0 : RANK_TILE);
     __syncthreads();
-    for (int64_t k = threadIdx.x; k < n; k += blockDim.x) tile[k] = ids[u0 + k];
+    for (int k = threadIdx.x; k < n; k += blockDim.x) tile[k] = ids[u0 + k];
     __syncthreads();
-    for (int64_t k = 0; k < n; ++k) {
+#pragma unroll 8
+    for (int k = lane; k < n; k += 32) {
       const int32_t o = tile[k];
       less += o < my;
       eq += o == my;
       eq_before += (o == my) & (u0 + k < t);
     }
   }
-  if (t >= T) return;
+#pragma unroll
+  for (int m = 16; m; m >>= 1) {
+    less += __shfl_xor_sync(0xffffffffu, less, m);
+    eq += __shfl_xor_sync(0xffffffffu, eq, m);
+    eq_before += __shfl_xor_sync(0xffffffffu, eq_before, m);
+  }
+  if (t >= T || lane) return;
   sorted[less + eq_before] = int32_t(t);
   seg_head[less + eq_before] = int32_t(less);
   if (eq_before == 0) seg_len[less] = int32_t(eq);
@@ -1033,7 +1047,7 @@ static void b_embedding_dx(Plan& p) {
       TCB_CUDA(cudaMemsetAsync(seg, 0, size_t(T) * 4, s));
       const int32_t* ids = (const int32_t*)in[0].ptr;
       const dim3 g2(unsigned(T), unsigned((H + 255) / 256));
-      launch_k(k_embed_rank, unsigned((T + 63) / 64), 64, 0, s, ids, srt, seg, hd, T);
+      launch_k(k_embed_rank, unsigned((T + 7) / 8), 256, 0, s, ids, srt, seg, hd, T);
       launch_k(k_embed_accum<TD>, g2, 256, 0, s, ids, srt, seg, hd, (const TD*)in[1].ptr, (float*)out[0].ptr,
                                           (float*)part->p, T, H);
       launch_k(k_embed_fold, g2, 256, 0, s, ids, srt, seg, (const float*)part->p, (float*)out[0].ptr, H);
