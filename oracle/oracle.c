@@ -658,7 +658,15 @@ static int layer_norm_bwd(const orc_tensor* const* in, int nin, orc_tensor* out,
   const float inv = 1.0f / (float)H;
   float* dg = F(&out[1]);
   float* db = F(&out[2]);
+  /* bias_grad: column sums (row order) of the outgoing gradient as stored --
+   * exactly colsum() of that output, fused (host/graph.hpp pattern 4) */
+  const int bias_grad = (int)aint(a, na, "bias_grad", 0);
+  const int has_dx = nout - bias_grad > 3;
+  float* dbias = bias_grad ? F(&out[has_dx ? 4 : 3]) : NULL;
+  const orc_tensor* gout = has_dx ? &out[3] : &out[0];
   for (int64_t j = 0; j < H; ++j) dg[j] = db[j] = 0.0f;
+  if (dbias)
+    for (int64_t j = 0; j < H; ++j) dbias[j] = 0.0f;
   for (int64_t t = 0; t < T; ++t) {
     const float mean = F(mean_t)[t], rstd = F(rstd_t)[t];
     float c1 = 0.0f, c2 = 0.0f;
@@ -679,13 +687,14 @@ static int layer_norm_bwd(const orc_tensor* const* in, int nin, orc_tensor* out,
       float gg = dyv * F(g)[j];
       float dsv = rstd * (gg - c2 - xh * c1);
       F(&out[0])[t * H + j] = rnd(out[0].dtype, dsv);
-      if (nout > 3) {
+      if (has_dx) {
         uint64_t idx = (uint64_t)(t * H + j);
         F(&out[3])[t * H + j] =
             rnd(out[3].dtype, orc_dropout_keep(seed, salt, idx, p) ? dsv * sp : 0.0f);
       }
       dg[j] += dyv * xh;
       db[j] += dyv;
+      if (dbias) dbias[j] += F(gout)[t * H + j];
     }
   }
   return 0;

@@ -237,6 +237,113 @@ __global__ void __launch_bounds__(256) k_ln_fwd(const T* __restrict__ x, const T
   }
 }
 
+// 16-bit vector fast path (bf16/f16, H % 8 == 0, 16-byte rows): two rows per
+// warp with every load of both rows issued up front and kept packed (8
+// elements per uint4), so a 2-CTA/SM wave holds all BERT-base rows in flight.
+template <typename T>
+__device__ __forceinline__ void unpack8(const uint4& q, float* f) {
+  const T* h = reinterpret_cast<const T*>(&q);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) f[k] = to_f(h[k]);
+}
+template <typename T>
+__device__ __forceinline__ uint4 pack8(const float* f) {
+  uint4 q;
+  T* h = reinterpret_cast<T*>(&q);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) h[k] = from_f<T>(f[k]);
+  return q;
+}
+
+template <typename T, int NC>
+__global__ void __launch_bounds__(256) k_ln_fwd16(const T* __restrict__ x, const T* __restrict__ r,
+                                                  const float* __restrict__ gamma_f, const T* __restrict__ gamma_t,
+                                                  const float* __restrict__ beta_f, const T* __restrict__ beta_t,
+                                                  T* __restrict__ y, T* __restrict__ s_out, float* __restrict__ mean_o,
+                                                  float* __restrict__ rstd_o, int64_t rows, int H, float eps,
+                                                  DropCfg d) {
+  TCB_PDL_ENTRY();
+  constexpr int RW = 2;
+  const int lane = threadIdx.x & 31;
+  const int64_t row0 = (blockIdx.x * int64_t(blockDim.x >> 5) + (threadIdx.x >> 5)) * RW;
+  if (row0 >= rows) return;
+  const int nch = H / 8;
+  uint4 xq[RW][NC], rq[RW][NC];
+#pragma unroll
+  for (int q = 0; q < RW; ++q)
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const int ch = lane + c * 32;
+      if (row0 + q < rows && ch < nch) {
+        const int64_t i = (row0 + q) * H + ch * 8;
+        xq[q][c] = __ldg(reinterpret_cast<const uint4*>(x + i));
+        if (r) rq[q][c] = __ldg(reinterpret_cast<const uint4*>(r + i));
+      }
+    }
+  const float inv = 1.0f / float(H);
+#pragma unroll
+  for (int q = 0; q < RW; ++q) {
+    const int64_t row = row0 + q;
+    if (row >= rows) break;
+    float v[NC][8];
+    float sum = 0.0f;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const int ch = lane + c * 32;
+      if (ch < nch) {
+        const int64_t i = row * H + ch * 8;
+        unpack8<T>(xq[q][c], v[c]);
+        if (r) {
+          float rv[8];
+          unpack8<T>(rq[q][c], rv);
+          const uint32_t bits = d.p > 0.0f ? dropout_bits8q(d, uint64_t(i) >> 3) : 0xFFu;
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const float xv = ((bits >> k) & 1u) ? __fmul_rn(v[c][k], d.scale) : 0.0f;
+            v[c][k] = to_f(from_f<T>(__fadd_rn(xv, rv[k])));  // s rounded to storage dtype
+          }
+          *reinterpret_cast<uint4*>(s_out + i) = pack8<T>(v[c]);
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) sum += v[c][k];
+      } else {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[c][k] = 0.0f;
+      }
+    }
+    const float mean = warp_sum(sum) * inv;
+    float sq = 0.0f;
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+      if (lane + c * 32 < nch)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const float dd = v[c][k] - mean;
+          sq += dd * dd;
+        }
+    const float rstd = 1.0f / sqrtf(warp_sum(sq) * inv + eps);
+    if (lane == 0) {
+      mean_o[row] = mean;
+      rstd_o[row] = rstd;
+    }
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const int ch = lane + c * 32;
+      if (ch < nch) {
+        float o[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int j = ch * 8 + k;
+          const float g = gamma_f ? __ldg(gamma_f + j) : to_f(gamma_t[j]);
+          const float b = beta_f ? __ldg(beta_f + j) : to_f(beta_t[j]);
+          o[k] = (v[c][k] - mean) * rstd * g + b;
+        }
+        *reinterpret_cast<uint4*>(y + row * H + ch * 8) = pack8<T>(o);
+      }
+    }
+  }
+}
+
 static void build_ln_fwd(Plan& p, bool residual) {
   if (residual) check_arity(p, 4, 4, 4, 4);
   else check_arity(p, 3, 3, 3, 3);
@@ -260,6 +367,16 @@ static void build_ln_fwd(Plan& p, bool residual) {
       for (int i = 0; i < (residual ? 2 : 1); ++i) vec = vec && reinterpret_cast<uintptr_t>(in[i].ptr) % 16 == 0;
       vec = vec && reinterpret_cast<uintptr_t>(out[0].ptr) % 16 == 0;
       if (residual) vec = vec && reinterpret_cast<uintptr_t>(out[1].ptr) % 16 == 0;
+      if constexpr (sizeof(T) == 2) {
+        if (vec) {
+          launch_k(k_ln_fwd16<T, NC>, unsigned((rows + 15) / 16), 256, 0, s, (const T*)in[0].ptr,
+                   residual ? (const T*)in[1].ptr : nullptr, gf ? (const float*)in[gi].ptr : nullptr,
+                   gf ? nullptr : (const T*)in[gi].ptr, gf ? (const float*)in[gi + 1].ptr : nullptr,
+                   gf ? nullptr : (const T*)in[gi + 1].ptr, (T*)out[0].ptr, residual ? (T*)out[1].ptr : nullptr,
+                   (float*)out[residual ? 2 : 1].ptr, (float*)out[residual ? 3 : 2].ptr, rows, H, eps, d);
+          return;
+        }
+      }
       constexpr int RW = NC <= 2 ? 2 : 1;
       launch_k(k_ln_fwd<T, NC>, unsigned((rows + 8 * RW - 1) / (8 * RW)), 256, 0, s, 
           (const T*)in[0].ptr, residual ? (const T*)in[1].ptr : nullptr,
@@ -287,8 +404,8 @@ __global__ void __launch_bounds__(256) k_ln_bwd(const T* __restrict__ sx, const 
                                                 const T* __restrict__ gamma_t, const float* __restrict__ mean,
                                                 const float* __restrict__ rstd, const T* __restrict__ dy,
                                                 const T* __restrict__ dy2, T* __restrict__ ds_o,
-                                                T* __restrict__ dx_o, float* __restrict__ ws, int64_t rows,
-                                                int H, DropCfg d, bool vec) {
+                                                T* __restrict__ dx_o, float* __restrict__ ws, int nparts,
+                                                int64_t rows, int H, DropCfg d, bool vec) {
   TCB_PDL_ENTRY();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nch = (H + 7) / 8;
@@ -296,12 +413,13 @@ __global__ void __launch_bounds__(256) k_ln_bwd(const T* __restrict__ sx, const 
   // [warp][2][k][chunk] so a warp's accesses are bank-conflict free
   extern __shared__ float red[];
   constexpr int CP = NC * 32;  // chunk pitch
-  float* pg = red + (warp * 2 + 0) * 8 * CP;
-  float* pb = red + (warp * 2 + 1) * 8 * CP;
+  float* pg = red + (warp * 3 + 0) * 8 * CP;
+  float* pb = red + (warp * 3 + 1) * 8 * CP;
+  float* pz = red + (warp * 3 + 2) * 8 * CP;  // bias grad: column sums of the outgoing gradient
 #pragma unroll
   for (int c = 0; c < NC; ++c)
 #pragma unroll
-    for (int k = 0; k < 8; ++k) pg[k * CP + c * 32 + lane] = pb[k * CP + c * 32 + lane] = 0.0f;
+    for (int k = 0; k < 8; ++k) pg[k * CP + c * 32 + lane] = pb[k * CP + c * 32 + lane] = pz[k * CP + c * 32 + lane] = 0.0f;
   const float inv = 1.0f / float(H);
   for (int rr = 0; rr < LNB_ROWS / 8; ++rr) {
     const int64_t row = int64_t(blockIdx.x) * LNB_ROWS + warp * (LNB_ROWS / 8) + rr;
@@ -357,6 +475,11 @@ __global__ void __launch_bounds__(256) k_ln_bwd(const T* __restrict__ sx, const 
           for (int k = 0; k < 8; ++k) o[k] = ((bits >> k) & 1u) ? o[k] * d.scale : 0.0f;
           st8(dx_o, i, (row + 1) * int64_t(H), vec, o);
         }
+        if (nparts > 2) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            if (ch * 8 + k < H) pz[k * CP + c * 32 + lane] += to_f(from_f<T>(o[k]));
+        }
       }
     }
   }
@@ -364,60 +487,182 @@ __global__ void __launch_bounds__(256) k_ln_bwd(const T* __restrict__ sx, const 
   __syncthreads();
   for (int j = threadIdx.x; j < H; j += blockDim.x) {
     const int off = (j & 7) * CP + (j >> 3);
-    float a = 0.0f, b = 0.0f;
-    for (int w = 0; w < 8; ++w) {
-      a += red[(w * 2 + 0) * 8 * CP + off];
-      b += red[(w * 2 + 1) * 8 * CP + off];
+    for (int a = 0; a < nparts; ++a) {
+      float acc = 0.0f;
+      for (int w = 0; w < 8; ++w) acc += red[(w * 3 + a) * 8 * CP + off];
+      ws[(int64_t(blockIdx.x) * nparts + a) * H + j] = acc;
     }
-    ws[(int64_t(blockIdx.x) * 2 + 0) * H + j] = a;
-    ws[(int64_t(blockIdx.x) * 2 + 1) * H + j] = b;
+  }
+}
+
+// 16-bit vector fast path: both rows' loads issued up front (packed), the
+// per-lane column partials (dgamma, dbeta, and with bias_grad the column sum of
+// the outgoing gradient) accumulate in per-warp smem rows, folded per CTA.
+template <typename T, int NC>
+__global__ void __launch_bounds__(256) k_ln_bwd16(const T* __restrict__ sx, const float* __restrict__ gamma_f,
+                                                  const T* __restrict__ gamma_t, const float* __restrict__ mean,
+                                                  const float* __restrict__ rstd, const T* __restrict__ dy,
+                                                  const T* __restrict__ dy2, T* __restrict__ ds_o,
+                                                  T* __restrict__ dx_o, float* __restrict__ ws, int nparts,
+                                                  int64_t rows, int H, DropCfg d) {
+  TCB_PDL_ENTRY();
+  constexpr int RW = LNB_ROWS / 8;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nch = H / 8;
+  extern __shared__ float red[];
+  constexpr int CP = NC * 32;  // chunk pitch
+  float* pp[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) pp[a] = red + (warp * 3 + a) * 8 * CP;
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) pp[a][k * CP + c * 32 + lane] = 0.0f;
+  const int64_t row0 = int64_t(blockIdx.x) * LNB_ROWS + warp * RW;
+  uint4 sq[RW][NC], dq[RW][NC], d2q[RW][NC];
+#pragma unroll
+  for (int q = 0; q < RW; ++q)
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const int ch = lane + c * 32;
+      if (row0 + q < rows && ch < nch) {
+        const int64_t i = (row0 + q) * H + ch * 8;
+        sq[q][c] = __ldg(reinterpret_cast<const uint4*>(sx + i));
+        dq[q][c] = __ldg(reinterpret_cast<const uint4*>(dy + i));
+        if (dy2) d2q[q][c] = __ldg(reinterpret_cast<const uint4*>(dy2 + i));
+      }
+    }
+  const float inv = 1.0f / float(H);
+#pragma unroll
+  for (int q = 0; q < RW; ++q) {
+    const int64_t row = row0 + q;
+    if (row >= rows) break;
+    const float mu = mean[row], rs = rstd[row];
+    float xh[NC][8], g[NC][8];
+    float c1 = 0.0f, c2 = 0.0f;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const int ch = lane + c * 32;
+      if (ch < nch) {
+        float sv[8], dv[8];
+        unpack8<T>(sq[q][c], sv);
+        unpack8<T>(dq[q][c], dv);
+        if (dy2) {
+          float d2[8];
+          unpack8<T>(d2q[q][c], d2);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) dv[k] = __fadd_rn(dv[k], d2[k]);
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int j = ch * 8 + k;
+          const float gm = gamma_f ? __ldg(gamma_f + j) : to_f(gamma_t[j]);
+          xh[c][k] = (sv[k] - mu) * rs;
+          g[c][k] = dv[k] * gm;
+          c1 += g[c][k] * xh[c][k];
+          c2 += g[c][k];
+          pp[0][k * CP + c * 32 + lane] += dv[k] * xh[c][k];
+          pp[1][k * CP + c * 32 + lane] += dv[k];
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) xh[c][k] = g[c][k] = 0.0f;
+      }
+    }
+    c1 = warp_sum(c1) * inv;
+    c2 = warp_sum(c2) * inv;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const int ch = lane + c * 32;
+      if (ch < nch) {
+        const int64_t i = row * H + ch * 8;
+        float o[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) o[k] = rs * (g[c][k] - c2 - xh[c][k] * c1);
+        uint4 w = pack8<T>(o);
+        *reinterpret_cast<uint4*>(ds_o + i) = w;
+        if (dx_o) {
+          const uint32_t bits = d.p > 0.0f ? dropout_bits8q(d, uint64_t(i) >> 3) : 0xFFu;
+#pragma unroll
+          for (int k = 0; k < 8; ++k) o[k] = ((bits >> k) & 1u) ? o[k] * d.scale : 0.0f;
+          w = pack8<T>(o);
+          *reinterpret_cast<uint4*>(dx_o + i) = w;
+        }
+        if (nparts > 2) {  // bias grad: the outgoing gradient as stored
+          float f[8];
+          unpack8<T>(w, f);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) pp[2][k * CP + c * 32 + lane] += f[k];
+        }
+      }
+    }
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < H; j += blockDim.x) {
+    const int off = (j & 7) * CP + (j >> 3);
+    for (int a = 0; a < nparts; ++a) {
+      float acc = 0.0f;
+      for (int w = 0; w < 8; ++w) acc += red[(w * 3 + a) * 8 * CP + off];
+      ws[(int64_t(blockIdx.x) * nparts + a) * H + j] = acc;
+    }
   }
 }
 
 // sum the per-CTA partials in fixed order -> dgamma, dbeta (f32): block = 32
 // columns x 8 warps; warp w folds partial rows w, w+8, ...; smem combines.
 __global__ void __launch_bounds__(256) k_ln_colsum(const float* __restrict__ ws, float* __restrict__ dg,
-                                                   float* __restrict__ db, int nblk, int H) {
+                                                   float* __restrict__ db, float* __restrict__ dbias, int nblk,
+                                                   int H) {
   TCB_PDL_ENTRY();
-  __shared__ float ra[8][33], rb[8][33];
+  __shared__ float ra[3][8][33];
+  const int np = dbias ? 3 : 2;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int j = blockIdx.x * 32 + lane;
-  float a = 0.0f, b = 0.0f;
+  float acc[3] = {0.0f, 0.0f, 0.0f};
   if (j < H) {
 #pragma unroll 4
     for (int k = warp; k < nblk; k += 8) {
-      a += ws[(int64_t(k) * 2 + 0) * H + j];
-      b += ws[(int64_t(k) * 2 + 1) * H + j];
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+        if (a < np) acc[a] += ws[(int64_t(k) * np + a) * H + j];
     }
   }
-  ra[warp][lane] = a;
-  rb[warp][lane] = b;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) ra[a][warp][lane] = acc[a];
   __syncthreads();
   if (warp == 0 && j < H) {
-    float sa = 0.0f, sb = 0.0f;
+    float t[3] = {0.0f, 0.0f, 0.0f};
 #pragma unroll
-    for (int w = 0; w < 8; ++w) {
-      sa += ra[w][lane];
-      sb += rb[w][lane];
-    }
-    dg[j] = sa;
-    db[j] = sb;
+    for (int w = 0; w < 8; ++w)
+#pragma unroll
+      for (int a = 0; a < 3; ++a) t[a] += ra[a][w][lane];
+    dg[j] = t[0];
+    db[j] = t[1];
+    if (dbias) dbias[j] = t[2];
   }
 }
 
 static void b_layer_norm_dx(Plan& p) {
-  check_arity(p, 5, 6, 3, 4);
+  check_arity(p, 5, 6, 3, 5);
   const Spec& S = p.in[0];
   const int H = int(S.dim(-1));
   const int64_t rows = S.numel() / H;
   require(H <= LN_MAXC * 8 * 32, "layer_norm_dx: hidden size > 2048 unsupported");
   require(p.out[1].dtype == TCB_F32 && p.out[2].dtype == TCB_F32, "layer_norm_dx: dgamma/dbeta are f32");
   const bool gf = p.in[1].dtype == TCB_F32;
-  const bool has_res = p.in.size() > 5, has_dx = p.out.size() > 3;
   const DropCfg d = drop_cfg(p.attrs);
+  const bool bias = p.attrs.i("bias_grad", 0) != 0;
+  const bool has_res = p.in.size() > 5, has_dx = int(p.out.size()) - int(bias) > 3;
+  const int di = has_dx ? 4 : 3;  // index of the fused bias-grad output
+  require(int(p.out.size()) - int(bias) >= 3, "layer_norm_dx: outputs (ds, dg, db [, dx] [, dbias])");
+  if (bias) require(p.out[di].dtype == TCB_F32 && p.out[di].numel() == H, "layer_norm_dx: dbias is f32 [H]");
+  const int np = bias ? 3 : 2;
   const int nblk = int((rows + LNB_ROWS - 1) / LNB_ROWS);
-  auto ws = std::make_shared<Scratch>(size_t(nblk) * 2 * H * sizeof(float));
-  const size_t smem = size_t(16) * 8 * 32 * ((H + 255) / 256) * sizeof(float);  // [8 warps][2][8][NC*32]
+  auto ws = std::make_shared<Scratch>(size_t(nblk) * np * H * sizeof(float));
+  const int ncs = (H + 255) / 256;
+  const size_t smem = size_t(8) * 3 * 8 * 32 * ncs * sizeof(float);  // [8 warps][3][8][NC*32]
   p.nkernels = 2;
   dispatch_float(S.dtype, [&](auto* tp) {
    using T = std::remove_pointer_t<decltype(tp)>;
@@ -425,7 +670,9 @@ static void b_layer_norm_dx(Plan& p) {
     constexpr int NC = decltype(nc)::value;
     static std::once_flag once;
     std::call_once(once, [] {
-      TCB_CUDA(cudaFuncSetAttribute(k_ln_bwd<T, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * 8 * 32 * 8 * 4));
+      constexpr int sm = 8 * 3 * 8 * 32 * NC * 4;
+      TCB_CUDA(cudaFuncSetAttribute(k_ln_bwd<T, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+      TCB_CUDA(cudaFuncSetAttribute(k_ln_bwd16<T, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
     });
     p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
       bool vec = H % 8 == 0;
@@ -433,13 +680,22 @@ static void b_layer_norm_dx(Plan& p) {
       if (has_res) vec = vec && reinterpret_cast<uintptr_t>(in[5].ptr) % 16 == 0;
       vec = vec && reinterpret_cast<uintptr_t>(out[0].ptr) % 16 == 0;
       if (has_dx) vec = vec && reinterpret_cast<uintptr_t>(out[3].ptr) % 16 == 0;
-      launch_k(k_ln_bwd<T, NC>, nblk, 256, smem, s, 
-          (const T*)in[0].ptr, gf ? (const float*)in[1].ptr : nullptr, gf ? nullptr : (const T*)in[1].ptr,
-          (const float*)in[2].ptr, (const float*)in[3].ptr, (const T*)in[4].ptr,
-          has_res ? (const T*)in[5].ptr : nullptr, (T*)out[0].ptr, has_dx ? (T*)out[3].ptr : nullptr,
-          (float*)ws->p, rows, H, d, vec);
-      launch_k(k_ln_colsum, (H + 31) / 32, 256, 0, s, (const float*)ws->p, (float*)out[1].ptr,
-                                                (float*)out[2].ptr, nblk, H);
+      const float* gfp = gf ? (const float*)in[1].ptr : nullptr;
+      const T* gtp = gf ? nullptr : (const T*)in[1].ptr;
+      const T* d2 = has_res ? (const T*)in[5].ptr : nullptr;
+      T* dxp = has_dx ? (T*)out[3].ptr : nullptr;
+      bool fast = false;
+      if constexpr (sizeof(T) == 2) fast = vec;
+      if (fast) {
+        launch_k(k_ln_bwd16<T, NC>, nblk, 256, smem, s, (const T*)in[0].ptr, gfp, gtp, (const float*)in[2].ptr,
+                 (const float*)in[3].ptr, (const T*)in[4].ptr, d2, (T*)out[0].ptr, dxp, (float*)ws->p, np, rows, H, d);
+      } else {
+        launch_k(k_ln_bwd<T, NC>, nblk, 256, smem, s, (const T*)in[0].ptr, gfp, gtp, (const float*)in[2].ptr,
+                 (const float*)in[3].ptr, (const T*)in[4].ptr, d2, (T*)out[0].ptr, dxp, (float*)ws->p, np, rows, H, d,
+                 vec);
+      }
+      launch_k(k_ln_colsum, (H + 31) / 32, 256, 0, s, (const float*)ws->p, (float*)out[1].ptr, (float*)out[2].ptr,
+               bias ? (float*)out[di].ptr : nullptr, nblk, H);
     };
    });
   });

@@ -210,13 +210,16 @@ inline void register_extension_ops(OpRegistry& r) {
     int64_t H = x.shape.back(), Tn = numel(x) / H;
     return TupleType{{x, x, TensorType{kF32, {Tn}}, TensorType{kF32, {Tn}}}};
   });
-  // layer_norm_dx(s, gamma, mean, rstd, dy [, dy2]) -> (ds, dgamma, dbeta [, dx if p > 0])
+  // layer_norm_dx(s, gamma, mean, rstd, dy [, dy2]) -> (ds, dgamma, dbeta [, dx if p > 0]
+  //   [, dbias = column sums of the outgoing gradient if bias_grad])
   reg("layer_norm_dx", -1, O, [](const V& in, const AttrMap& a) -> Type {
     if (in.size() != 5 && in.size() != 6) throw TypeError("layer_norm_dx: 5 or 6 inputs");
     auto s = rel::T(in[0], "layer_norm_dx");
     TensorType g{kF32, {s.shape.back()}};
-    if (ir::attr_double(a, "p", 0.0) > 0.0) return TupleType{{s, g, g, s}};
-    return TupleType{{s, g, g}};
+    TupleType t{{s, g, g}};
+    if (ir::attr_double(a, "p", 0.0) > 0.0) t.fields.push_back(s);
+    if (ir::attr_int(a, "bias_grad", 0)) t.fields.push_back(g);
+    return t;
   });
   reg("gelu", 1, E, [](const V& in, const AttrMap&) -> Type { return rel::T(in[0], "gelu"); });
   reg("gelu_dx", 2, E, [](const V& in, const AttrMap&) -> Type { return rel::T(in[1], "gelu_dx"); });

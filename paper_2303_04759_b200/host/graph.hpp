@@ -395,7 +395,7 @@ inline UseInfo count_uses(const LetSeq& s) {
 }
 
 struct FusionStats {
-  int dact = 0, ln_dy2 = 0, emb_base = 0, dead = 0;
+  int dact = 0, ln_dy2 = 0, emb_base = 0, ln_bias = 0, dead = 0;
 };
 
 /// Pattern fusion + dead-let elimination.  Each rewrite needs the absorbed
@@ -451,6 +451,34 @@ inline FusionStats fuse(LetSeq& s, bool patterns = true) {
           removed.insert(def[src.get()]);
           ++st.ln_dy2;
           continue;
+        }
+      }
+    }
+    // 4. colsum(get(layer_norm_dx(...), k)), k = the gradient leaving the
+    //    LayerNorm (dx when p > 0, else ds) -> an extra f32 [H] output of
+    //    layer_norm_dx (attr bias_grad): the bias gradient of the linear that
+    //    fed the LayerNorm, summed in the same row order, with no extra pass
+    if (op == "colsum") {
+      auto src = arg_var(b.value, 0);
+      auto it = src ? def.find(src.get()) : def.end();
+      if (it != def.end() && !removed.count(it->second) && s.lets[it->second].value->kind == ExprKind::TupleGet) {
+        auto& gl = s.lets[it->second];
+        auto tv = gl.value->args[0]->kind == ExprKind::VarRef ? gl.value->args[0]->var : nullptr;
+        auto* lp = producer(tv);
+        if (lp && lp->value->op == "layer_norm_dx" && !lp->value->call_attrs.count("bias_grad")) {
+          const bool has_dx = ir::attr_double(lp->value->call_attrs, "p", 0.0) > 0.0;
+          if (gl.value->index == (has_dx ? 3 : 0)) {
+            lp->value->call_attrs["bias_grad"] = std::int64_t(1);
+            TupleType tt = lp->var->ty.tuple();
+            tt.fields.push_back(b.value->ty.tensor());
+            lp->var->ty = tt;
+            lp->value->ty = tt;
+            auto e = ir::tuple_get(ir::var_ref(lp->var), int(tt.fields.size()) - 1);
+            e->ty = b.value->ty;
+            b.value = e;
+            ++st.ln_bias;
+            continue;
+          }
         }
       }
     }

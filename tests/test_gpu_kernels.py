@@ -337,6 +337,15 @@ def test_add_layer_norm_and_backward(p):
                     [((T, H), BF16), ((H,), F32), ((H,), F32), ((T, H), BF16)], attrs)
     assert rel_err(g[0], o[0]) < 5e-3 and rel_err(g[3], o[3]) < 5e-3
     assert rel_err(g[1], o[1]) < 1e-5 and rel_err(g[2], o[2]) < 1e-5
+    # fused bias gradient (graph pattern 4): column sums of the outgoing gradient
+    outs = [((T, H), BF16), ((H,), F32), ((H,), F32), ((T, H), BF16), ((H,), F32)]
+    g, o = run_both("layer_norm_dx", [(s, BF16), (gm, F32), (mean, F32), (rstd, F32), (dy, BF16), (dy2, BF16)],
+                    outs, {**attrs, "bias_grad": 1})
+    assert rel_err(g[4], o[4]) < 1e-5, rel_err(g[4], o[4])
+    assert rel_err(g[3], o[3]) < 5e-3 and rel_err(g[1], o[1]) < 1e-5
+    g, o = run_both("layer_norm_dx", [(s, BF16), (gm, F32), (mean, F32), (rstd, F32), (dy, BF16)],
+                    outs[:3] + outs[4:], {**attrs, "p": 0.0, "bias_grad": 1})
+    assert rel_err(g[3], o[3]) < 1e-5 and rel_err(g[0], o[0]) < 5e-3
 
 
 def test_layer_norm_dx_f32():
