@@ -227,25 +227,25 @@ __global__ void __launch_bounds__(256) k_colsum_partial(const T* __restrict__ x,
   }
 }
 
-// block = 32 columns x 8 warps; warp w sums partial rows w, w+8, ... (loads
-// unrolled 4 deep), then warp 0 adds the 8 warp sums in order: deterministic
-__global__ void __launch_bounds__(256) k_colsum_final(const float* __restrict__ part, float* __restrict__ out,
-                                                      int64_t nchunk, int64_t C, float scale) {
+// block = 32 columns x 32 warps; warp w sums partial rows w, w+32, ... (loads
+// unrolled 4 deep), then warp 0 adds the 32 warp sums in order: deterministic
+__global__ void __launch_bounds__(1024) k_colsum_final(const float* __restrict__ part, float* __restrict__ out,
+                                                       int64_t nchunk, int64_t C, float scale) {
   TCB_PDL_ENTRY();
-  __shared__ float red[8][33];
+  __shared__ float red[32][33];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t c = int64_t(blockIdx.x) * 32 + lane;
   float s = 0.0f;
   if (c < C) {
 #pragma unroll 4
-    for (int64_t k = warp; k < nchunk; k += 8) s += part[k * C + c];
+    for (int64_t k = warp; k < nchunk; k += 32) s += part[k * C + c];
   }
   red[warp][lane] = s;
   __syncthreads();
   if (warp == 0 && c < C) {
     float t = 0.0f;
-#pragma unroll
-    for (int w = 0; w < 8; ++w) t += red[w][lane];
+#pragma unroll 8
+    for (int w = 0; w < 32; ++w) t += red[w][lane];
     out[c] = t * scale;
   }
 }
@@ -281,7 +281,7 @@ static void b_colsum(Plan& p) {
         if (reinterpret_cast<uintptr_t>(in[0].ptr) % 16) fail(TCB_ERR_ARG, "colsum: input not 16-byte aligned");
         dim3 grid(unsigned((C + 255) / 256), unsigned(nchunk));
         launch_k(k_colsum_partial<T>, grid, 256, 0, s, (const T*)in[0].ptr, (float*)ws->p, R, C);
-        launch_k(k_colsum_final, unsigned((C + 31) / 32), 256, 0, s, (const float*)ws->p, (float*)out[0].ptr, nchunk, C,
+        launch_k(k_colsum_final, unsigned((C + 31) / 32), 1024, 0, s, (const float*)ws->p, (float*)out[0].ptr, nchunk, C,
                                                                   1.0f);
       };
     } else {

@@ -612,18 +612,21 @@ __global__ void __launch_bounds__(256) k_ln_bwd16(const T* __restrict__ sx, cons
 
 // sum the per-CTA partials in fixed order -> dgamma, dbeta (f32): block = 32
 // columns x 8 warps; warp w folds partial rows w, w+8, ...; smem combines.
-__global__ void __launch_bounds__(256) k_ln_colsum(const float* __restrict__ ws, float* __restrict__ dg,
-                                                   float* __restrict__ db, float* __restrict__ dbias, int nblk,
-                                                   int H) {
+// fold the per-CTA partial rows ws[k][a][j] (k < nblk, a < np) in fixed order:
+// block = 32 columns x 32 warps, warp w sums rows w, w+32, ... (loads
+// unrolled), then warp a folds the 32 warp sums of part a in warp order
+__global__ void __launch_bounds__(1024) k_ln_colsum(const float* __restrict__ ws, float* __restrict__ dg,
+                                                    float* __restrict__ db, float* __restrict__ dbias, int nblk,
+                                                    int H) {
   TCB_PDL_ENTRY();
-  __shared__ float ra[3][8][33];
+  __shared__ float ra[3][32][33];
   const int np = dbias ? 3 : 2;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int j = blockIdx.x * 32 + lane;
   float acc[3] = {0.0f, 0.0f, 0.0f};
   if (j < H) {
 #pragma unroll 4
-    for (int k = warp; k < nblk; k += 8) {
+    for (int k = warp; k < nblk; k += 32) {
 #pragma unroll
       for (int a = 0; a < 3; ++a)
         if (a < np) acc[a] += ws[(int64_t(k) * np + a) * H + j];
@@ -632,15 +635,11 @@ __global__ void __launch_bounds__(256) k_ln_colsum(const float* __restrict__ ws,
 #pragma unroll
   for (int a = 0; a < 3; ++a) ra[a][warp][lane] = acc[a];
   __syncthreads();
-  if (warp == 0 && j < H) {
-    float t[3] = {0.0f, 0.0f, 0.0f};
-#pragma unroll
-    for (int w = 0; w < 8; ++w)
-#pragma unroll
-      for (int a = 0; a < 3; ++a) t[a] += ra[a][w][lane];
-    dg[j] = t[0];
-    db[j] = t[1];
-    if (dbias) dbias[j] = t[2];
+  if (warp < np && j < H) {
+    float t = 0.0f;
+#pragma unroll 8
+    for (int w = 0; w < 32; ++w) t += ra[warp][w][lane];
+    (warp == 0 ? dg : warp == 1 ? db : dbias)[j] = t;
   }
 }
 
@@ -694,7 +693,7 @@ static void b_layer_norm_dx(Plan& p) {
                  (const float*)in[3].ptr, (const T*)in[4].ptr, d2, (T*)out[0].ptr, dxp, (float*)ws->p, np, rows, H, d,
                  vec);
       }
-      launch_k(k_ln_colsum, (H + 31) / 32, 256, 0, s, (const float*)ws->p, (float*)out[1].ptr, (float*)out[2].ptr,
+      launch_k(k_ln_colsum, (H + 31) / 32, 1024, 0, s, (const float*)ws->p, (float*)out[1].ptr, (float*)out[2].ptr,
                bias ? (float*)out[di].ptr : nullptr, nblk, H);
     };
    });
