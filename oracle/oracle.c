@@ -935,6 +935,34 @@ int orc_exec(const char* op, const orc_tensor* in, int nin, orc_tensor* out, int
       }
     return 0;
   }
+  /* matmul_pair(a0, b0 [, aux0], a1, b1): problem 0 is matmul_t (n0 = 2) or
+   * matmul_dact (n0 = 3), problem 1 matmul_t -- the same arithmetic as the two
+   * separate ops (horizontal fusion only changes the launch). */
+  if (!strcmp(op, "matmul_pair")) {
+    const int n0 = (int)aint(A, na, "n0", 2);
+    if (nin != n0 + 2 || nout != 2) return fail("matmul_pair: expects %d inputs, 2 outputs", n0 + 2);
+    for (int p = 0; p < 2; ++p) {
+      char kt[8], kb[8], kal[8];
+      snprintf(kt, sizeof kt, "ta%d", p);
+      snprintf(kb, sizeof kb, "tb%d", p);
+      snprintf(kal, sizeof kal, "alpha%d", p);
+      const orc_tensor* a0 = &in[p ? n0 : 0];
+      const orc_tensor* b0 = &in[p ? n0 + 1 : 1];
+      int ta = (int)aint(A, na, kt, 0), tb = (int)aint(A, na, kb, 0);
+      int64_t M = ta ? a0->shape[1] : a0->shape[0];
+      int64_t K = ta ? a0->shape[0] : a0->shape[1];
+      int64_t N = tb ? b0->shape[0] : b0->shape[1];
+      gemm_acc(F(a0), F(b0), F(&out[p]), M, N, K, ta, tb, (float)adbl(A, na, kal, 1.0));
+      if (p == 0 && n0 == 3) {
+        int act = parse_act(astr(A, na, "act0", "none"));
+        for (int64_t i = 0; i < M * N; ++i)
+          F(&out[0])[i] = rnd(out[0].dtype, F(&out[0])[i] * dact_f(act, F(&in[2])[i]));
+      } else {
+        round_all(&out[p], M * N);
+      }
+    }
+    return 0;
+  }
   /* matmul_dact(a, b, aux): (op(a) op(b)) * act'(aux) -- a backward GEMM with the
    * activation derivative fused into its epilogue. */
   if (!strcmp(op, "matmul_dact")) {

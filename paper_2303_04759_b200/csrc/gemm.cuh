@@ -54,6 +54,8 @@ void launch_gemm_exact(const GemmArgs& g, cudaStream_t s);
 // returns false when the tensor-core path cannot take this problem
 bool gemm_tc_supported(const GemmArgs& g, std::string* why);
 void launch_gemm_tc(const GemmArgs& g, cudaStream_t s);
+// two independent problems in one persistent launch (same tile shape)
+void launch_gemm_tc_pair(const GemmArgs& g0, const GemmArgs& g1, cudaStream_t s);
 // cost-model choice of tile shape / CTA pairing / split-K for a problem
 TcChoice gemm_tc_choose(const GemmArgs& g);
 // plan-time: freeze the tile choice and allocate split-K scratch (no-op for the

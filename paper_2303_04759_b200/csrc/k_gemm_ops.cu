@@ -130,6 +130,44 @@ static void b_matmul_dact(Plan& p) {
 }
 TCB_REGISTER("matmul_dact", b_matmul_dact);
 
+// matmul_pair(a0, b0 [, aux0], a1, b1): two independent GEMMs, one persistent
+// launch (launch_gemm_tc_pair); any other dtype runs them back to back
+static void b_matmul_pair(Plan& p) {
+  const int n0 = int(p.attrs.i("n0", 2));
+  require(n0 == 2 || n0 == 3, "matmul_pair: n0 must be 2 or 3");
+  check_arity(p, n0 + 2, n0 + 2, 2, 2);
+  GemmArgs g0 = gemm2d(p.in[0], p.in[1], int(p.attrs.i("ta0", 0)), int(p.attrs.i("tb0", 0)), p.out[0], "matmul_pair");
+  GemmArgs g1 = gemm2d(p.in[n0], p.in[n0 + 1], int(p.attrs.i("ta1", 0)), int(p.attrs.i("tb1", 0)), p.out[1],
+                       "matmul_pair");
+  g0.alpha = float(p.attrs.f("alpha0", 1.0));
+  g1.alpha = float(p.attrs.f("alpha1", 1.0));
+  if (n0 == 3) {
+    g0.dact = parse_act(p.attrs.s("act0", "none"));
+    require(same_shape(p.in[2], p.out[0]), "matmul_pair: aux0 must have output 0's shape");
+    g0.aux_dtype = p.in[2].dtype;
+  }
+  g0.force_bn = g1.force_bn = int(p.attrs.i("tc_bn", 0));
+  g0.force_cg = g1.force_cg = int(p.attrs.i("tc_cg", 0));
+  const bool exact = want_exact(p) || p.in[n0].dtype != TCB_BF16;
+  p.nkernels = exact ? 2 : 1;
+  p.run = [g0, g1, exact, n0](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) mutable {
+    g0.a.ptr = in[0].ptr;
+    g0.b.ptr = in[1].ptr;
+    if (n0 == 3) g0.aux = in[2].ptr;
+    g0.c = out[0].ptr;
+    g1.a.ptr = in[n0].ptr;
+    g1.b.ptr = in[n0 + 1].ptr;
+    g1.c = out[1].ptr;
+    if (!exact && gemm_tc_supported(g0, nullptr) && gemm_tc_supported(g1, nullptr)) {
+      launch_gemm_tc_pair(g0, g1, s);
+    } else {
+      launch_gemm(g0, exact, s);
+      launch_gemm(g1, exact, s);
+    }
+  };
+}
+TCB_REGISTER("matmul_pair", b_matmul_pair);
+
 static void b_batch_matmul(Plan& p) {
   check_arity(p, 2, 2, 1, 1);
   const Spec &A = p.in[0], &B = p.in[1], &C = p.out[0];

@@ -54,17 +54,12 @@ struct TcCfg {
   static_assert(CG == 1 || (BN / 2) % 16 == 0, "cta pair splits B");
 };
 
-struct TcParams {
+struct TcProb {
   int64_t M, N, K, Z, Z2;
   int ta, tb;
   int m_blocks, n_blocks, k_blocks;  // m_blocks counts (128*CG)-row blocks
   int64_t num_tiles;
-  // split-K: a cluster of CG x splits CTAs owns one tile; CTA split s covers
-  // k-blocks [s*kps, +kps), then the partial accumulators are exchanged
-  // through distributed shared memory and reduced in split order
-  int splits, kps;
-  int64_t num_units;
-  unsigned long long* trace;  // optional per-CTA timeline (tools/probe_gemm.py --trace)
+  int kps;  // k-blocks per K split
   uint32_t idesc;
   // epilogue
   void* c;
@@ -80,6 +75,24 @@ struct TcParams {
   int tma_epi;   // 1: smem + TMA-store epilogue (tensor maps valid); 0: direct stores
   int c_vec_ok;  // direct path: 16-byte aligned rows
 };
+// One launch runs one or two GEMM problems with the same tile shape (a
+// "grouped" launch: the backward's data-gradient and weight-gradient GEMMs of a
+// linear share dY and run side by side, filling the SMs the small weight
+// gradient leaves idle).  Units [0, pr[0].num_tiles) belong to problem 0.
+struct TcParams {
+  TcProb pr[2];
+  int nprob;
+  // split-K (single problem): a cluster of CG x splits CTAs owns one tile; CTA
+  // split s covers k-blocks [s*kps, +kps), then the partial accumulators are
+  // exchanged through distributed shared memory and reduced in split order
+  int splits;
+  int64_t num_units;
+  unsigned long long* trace;  // optional per-CTA timeline (tools/probe_gemm.py --trace)
+};
+__device__ __forceinline__ int unit_prob(const TcParams& P, int64_t u) {
+  return (P.nprob > 1 && u >= P.pr[0].num_tiles) ? 1 : 0;
+}
+
 
 __device__ __forceinline__ float ld_e(const void* p, int dt, int64_t i) {
   if (dt == TCB_F32) return static_cast<const float*>(p)[i];
@@ -87,7 +100,7 @@ __device__ __forceinline__ float ld_e(const void* p, int dt, int64_t i) {
   return __half2float(static_cast<const __half*>(p)[i]);
 }
 
-__device__ __forceinline__ void decode_tile(const TcParams& P, int64_t t, int& z, int& mb, int& nb) {
+__device__ __forceinline__ void decode_tile(const TcProb& P, int64_t t, int& z, int& mb, int& nb) {
   const int64_t per_z = int64_t(P.m_blocks) * P.n_blocks;
   z = int(t / per_z);
   int64_t r = t - int64_t(z) * per_z;
@@ -111,7 +124,7 @@ __device__ __forceinline__ void apply_act(int act, float (&v)[W]) {
       break;
     case ACT_GELU:
 #pragma unroll
-      for (int j = 0; j < W; ++j) v[j] = gelu_f(v[j]);
+      for (int j = 0; j < W; ++j) v[j] = fast_gelu(v[j]);
       break;
     default:
       break;
@@ -130,7 +143,7 @@ __device__ __forceinline__ void apply_dact(int act, float (&v)[W], const float (
       break;
     case ACT_GELU:
 #pragma unroll
-      for (int j = 0; j < W; ++j) v[j] *= gelu_grad_f(a[j]);
+      for (int j = 0; j < W; ++j) v[j] *= fast_gelu_grad(a[j]);
       break;
     default:
       break;
@@ -223,8 +236,9 @@ struct EpiMaps {
 
 template <int BN, int CG, bool AUX>
 __global__ void __launch_bounds__(TC_THREADS, 1)
-    k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-              const __grid_constant__ EpiMaps EM, const TcParams P) {
+    k_gemm_tc(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmB0,
+              const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmB1,
+              const __grid_constant__ EpiMaps EM0, const __grid_constant__ EpiMaps EM1, const TcParams P) {
   using C = TcCfg<BN, CG, AUX>;
   constexpr int W = TC_EW;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -255,8 +269,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   if (tr && threadIdx.x == 0) tr[0] = gtimer();
 
   if (warp == 0 && lane == 0) {
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA0)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB0)) : "memory");
+    if (P.nprob > 1) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA1)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB1)) : "memory");
+    }
   }
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
@@ -298,12 +316,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int64_t u = cl_id; u < P.num_units; u += n_cl) {
-        const int64_t t = u;
-        const int kb0 = split * P.kps;
-        const int kb1 = min(kb0 + P.kps, P.k_blocks);
+        const int prob = unit_prob(P, u);
+        const TcProb& Q = P.pr[prob];
+        const CUtensorMap* mA = prob ? &tmA1 : &tmA0;
+        const CUtensorMap* mB = prob ? &tmB1 : &tmB0;
+        const int64_t t = u - (prob ? P.pr[0].num_tiles : 0);
+        const int kb0 = split * Q.kps;
+        const int kb1 = min(kb0 + Q.kps, Q.k_blocks);
         int z, mb, nb;
-        decode_tile(P, t, z, mb, nb);
-        const int z1 = int(z / P.Z2), z2 = int(z % P.Z2);
+        decode_tile(Q, t, z, mb, nb);
+        const int z1 = int(z / Q.Z2), z2 = int(z % Q.Z2);
         const int m0 = mb * (TC_BM * CG) + int(rank) * TC_BM;
         const int n0 = nb * BN + int(rank) * C::B_ROWS;
         for (int kb = kb0; kb < kb1; ++kb) {
@@ -314,18 +336,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           uint8_t* a_dst = sA + stage * C::A_BYTES;
           uint8_t* b_dst = sB + stage * C::B_BYTES;
           const int k0 = kb * TC_BK;
-          if (!P.ta) {
-            tma_load_4d<CG>(a_dst, &tmA, fb, k0, m0, z2, z1);
+          if (!Q.ta) {
+            tma_load_4d<CG>(a_dst, mA, fb, k0, m0, z2, z1);
           } else {
 #pragma unroll
-            for (int c = 0; c < TC_BM / 64; ++c) tma_load_4d<CG>(a_dst + c * 8192, &tmA, fb, m0 + c * 64, k0, z2, z1);
+            for (int c = 0; c < TC_BM / 64; ++c) tma_load_4d<CG>(a_dst + c * 8192, mA, fb, m0 + c * 64, k0, z2, z1);
           }
-          if (P.tb) {
-            tma_load_4d<CG>(b_dst, &tmB, fb, k0, n0, z2, z1);
+          if (Q.tb) {
+            tma_load_4d<CG>(b_dst, mB, fb, k0, n0, z2, z1);
           } else {
 #pragma unroll
             for (int c = 0; c < C::B_ROWS / 64; ++c)
-              tma_load_4d<CG>(b_dst + c * 8192, &tmB, fb, n0 + c * 64, k0, z2, z1);
+              tma_load_4d<CG>(b_dst + c * 8192, mB, fb, n0 + c * 64, k0, z2, z1);
           }
           if (++stage == C::STAGES) {
             stage = 0;
@@ -342,8 +364,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       int acc = 0;
       uint32_t acc_phase = 0;
       for (int64_t u = cl_id; u < P.num_units; u += n_cl) {
-        const int kb0 = split * P.kps;
-        const int kb1 = min(kb0 + P.kps, P.k_blocks);
+        const TcProb& Q = P.pr[unit_prob(P, u)];
+        const int kb0 = split * Q.kps;
+        const int kb1 = min(kb0 + Q.kps, Q.k_blocks);
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + uint32_t(acc * BN);
@@ -358,9 +381,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             // K-major: +32 B per 16-element k step inside the 128 B swizzle row;
             // MN-major: +2048 B (16 k-rows of 128 B); LBO = 8 KB between 64-wide
             // MN chunks, SBO = 1 KB between 8-row swizzle atoms.
-            const uint64_t ad = P.ta ? umma_desc(a_addr + k * 2048, 8192, 1024) : umma_desc(a_addr + k * 32, 16, 1024);
-            const uint64_t bd = P.tb ? umma_desc(b_addr + k * 32, 16, 1024) : umma_desc(b_addr + k * 2048, 8192, 1024);
-            tc_mma<CG>(tmem_d, ad, bd, P.idesc, (kb > kb0 || k) ? 1u : 0u);
+            const uint64_t ad = Q.ta ? umma_desc(a_addr + k * 2048, 8192, 1024) : umma_desc(a_addr + k * 32, 16, 1024);
+            const uint64_t bd = Q.tb ? umma_desc(b_addr + k * 32, 16, 1024) : umma_desc(b_addr + k * 2048, 8192, 1024);
+            tc_mma<CG>(tmem_d, ad, bd, Q.idesc, (kb > kb0 || k) ? 1u : 0u);
           }
           tc_commit<CG>(&empty[stage], mcast);
           if (++stage == C::STAGES) {
@@ -391,7 +414,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     float* wbias = sBias + ew * CPW * W;
     uint64_t* ab = abar + 2 * ew;
     const uint32_t tempty_addr0 = CG == 2 ? mapa(smem_u32(&tempty[0]), lead) : smem_u32(&tempty[0]);
-    const bool has_aux = AUX && P.tma_epi && P.dact != ACT_NONE;
     int acc = 0;
     uint32_t acc_phase = 0;
     uint32_t sidx = 0;    // output slot ring
@@ -402,8 +424,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     uint32_t aissue = 0;
     auto issue_next_aux = [&]() {
       while (pt < P.num_units) {
+        const int prob = unit_prob(P, pt);
+        const TcProb& Q = P.pr[prob];
+        if (!(Q.tma_epi && Q.dact != ACT_NONE)) {  // this problem has no act'(aux): skip its units
+          pc = sub;
+          pt += n_cl;
+          continue;
+        }
         int z, mb, nb;
-        decode_tile(P, pt, z, mb, nb);
+        decode_tile(Q, pt - (prob ? P.pr[0].num_tiles : 0), z, mb, nb);
         const int64_t n0 = int64_t(nb) * BN + pc * W;
         const int mrow = mb * (TC_BM * CG) + int(rank) * TC_BM + q * 32;
         pc += SPLIT;
@@ -411,38 +440,42 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           pc = sub;
           pt += n_cl;
         }
-        if (n0 >= P.N) continue;  // chunk skipped by the consumer too
+        if (n0 >= Q.N) continue;  // chunk skipped by the consumer too
         if (lane == 0) {
           uint64_t* bar = &ab[aissue & 1];
           mbar_expect_tx(bar, 32 * W * 2);
           asm volatile(
               "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
               " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(aslots + (aissue & 1) * TC_AUX_SLOT)),
-              "l"(reinterpret_cast<uint64_t>(&EM.aux)), "r"(int(n0)), "r"(mrow), "r"(int(z % P.Z2)),
-              "r"(int(z / P.Z2)), "r"(smem_u32(bar))
+              "l"(reinterpret_cast<uint64_t>(prob ? &EM1.aux : &EM0.aux)), "r"(int(n0)), "r"(mrow), "r"(int(z % Q.Z2)),
+              "r"(int(z / Q.Z2)), "r"(smem_u32(bar))
               : "memory");
         }
         ++aissue;
         return;
       }
     };
-    if (has_aux) issue_next_aux();
+    if (AUX) issue_next_aux();
 
     for (int64_t u = cl_id; u < P.num_units; u += n_cl) {
-      const int64_t t = u;
+      const int prob = unit_prob(P, u);
+      const TcProb& Q = P.pr[prob];
+      const EpiMaps& EM = prob ? EM1 : EM0;
+      const bool has_aux = AUX && Q.tma_epi && Q.dact != ACT_NONE;
+      const int64_t t = u - (prob ? P.pr[0].num_tiles : 0);
       int z, mb, nb;
-      decode_tile(P, t, z, mb, nb);
-      const int z1 = int(z / P.Z2), z2 = int(z % P.Z2);
-      const int64_t coff = int64_t(z1) * P.c_s1 + int64_t(z2) * P.c_s2;
+      decode_tile(Q, t, z, mb, nb);
+      const int z1 = int(z / Q.Z2), z2 = int(z % Q.Z2);
+      const int64_t coff = int64_t(z1) * Q.c_s1 + int64_t(z2) * Q.c_s2;
       const int mrow0 = mb * (TC_BM * CG) + int(rank) * TC_BM + q * 32;  // this warp's 32-row box
       const int64_t m = int64_t(mrow0) + lane;
       // finishes one W-column chunk: v holds the f32 accumulator row segment
       auto finish = [&](float (&v)[W], int ci, int64_t n0) {
-        if (P.alpha != 1.0f) {
+        if (Q.alpha != 1.0f) {
 #pragma unroll
-          for (int j = 0; j < W; ++j) v[j] *= P.alpha;
+          for (int j = 0; j < W; ++j) v[j] *= Q.alpha;
         }
-        if (P.bias) {
+        if (Q.bias) {
           const float4* bb = reinterpret_cast<const float4*>(wbias + ci * W);
 #pragma unroll
           for (int j = 0; j < W / 4; ++j) {
@@ -453,43 +486,43 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             v[4 * j + 3] += b4.w;
           }
         }
-        if (P.tma_epi) {
+        if (Q.tma_epi) {
           if (has_aux) {
             // this chunk's aux box was issued one chunk ago; prefetch the next
             const uint32_t s = achunk & 1, ph = (achunk >> 1) & 1;
             issue_next_aux();
             mbar_wait(&ab[s], ph);
             float a[W];
-            unstage_row16<W>(aslots + s * TC_AUX_SLOT, lane, P.aux_dtype, a);
-            apply_dact<W>(P.dact, v, a);
+            unstage_row16<W>(aslots + s * TC_AUX_SLOT, lane, Q.aux_dtype, a);
+            apply_dact<W>(Q.dact, v, a);
             ++achunk;
           }
           uint8_t* slot = slots + sidx * TC_SLOT;
           if (lane == 0) bulk_wait_read<1>();  // the store that last used this slot has read it
           __syncwarp();
-          if (P.aux_out) stage_row<W>(slot + TC_SLOT / 2, lane, P.c_dtype, v);
-          apply_act<W>(P.act, v);
-          stage_row<W>(slot, lane, P.c_dtype, v);
+          if (Q.aux_out) stage_row<W>(slot + TC_SLOT / 2, lane, Q.c_dtype, v);
+          apply_act<W>(Q.act, v);
+          stage_row<W>(slot, lane, Q.c_dtype, v);
           fence_proxy_async();
           __syncwarp();
           if (lane == 0) {
             tma_store_4d(&EM.c, slot, int(n0), mrow0, z2, z1);
-            if (P.aux_out) tma_store_4d(&EM.u, slot + TC_SLOT / 2, int(n0), mrow0, z2, z1);
+            if (Q.aux_out) tma_store_4d(&EM.u, slot + TC_SLOT / 2, int(n0), mrow0, z2, z1);
             bulk_commit();
           }
           sidx ^= 1;
-        } else if (m < P.M) {
-          const int nvalid = int(P.N - n0 < W ? P.N - n0 : W);
-          const int64_t base = coff + m * P.ldc + n0;
-          if (P.dact != ACT_NONE) {
+        } else if (m < Q.M) {
+          const int nvalid = int(Q.N - n0 < W ? Q.N - n0 : W);
+          const int64_t base = coff + m * Q.ldc + n0;
+          if (Q.dact != ACT_NONE) {
             float a[W];
 #pragma unroll
-            for (int j = 0; j < W; ++j) a[j] = j < nvalid ? ld_e(P.aux, P.aux_dtype, base + j) : 0.0f;
-            apply_dact<W>(P.dact, v, a);
+            for (int j = 0; j < W; ++j) a[j] = j < nvalid ? ld_e(Q.aux, Q.aux_dtype, base + j) : 0.0f;
+            apply_dact<W>(Q.dact, v, a);
           }
-          if (P.aux_out) store_row<W>(P.aux_out, P.c_dtype, base, v, nvalid);
-          apply_act<W>(P.act, v);
-          store_row<W>(P.c, P.c_dtype, base, v, nvalid);
+          if (Q.aux_out) store_row<W>(Q.aux_out, Q.c_dtype, base, v, nvalid);
+          apply_act<W>(Q.act, v);
+          store_row<W>(Q.c, Q.c_dtype, base, v, nvalid);
         }
       };
       auto load_bias = [&]() {
@@ -498,11 +531,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         for (int i = lane; i < CPW * W; i += 32) {
           const int c = sub + (i / W) * SPLIT;
           const int64_t n = int64_t(nb) * BN + int64_t(c) * W + (i % W);
-          wbias[i] = (c < NCH && n < P.N) ? ld_e(P.bias, P.bias_dtype, n) : 0.0f;
+          wbias[i] = (c < NCH && n < Q.N) ? ld_e(Q.bias, Q.bias_dtype, n) : 0.0f;
         }
         __syncwarp();
       };
-      if (P.bias) load_bias();
+      if (Q.bias) load_bias();
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       if (tr && ew == 0 && u == cl_id) tr[4] = gtimer();
@@ -515,7 +548,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         cluster_sync_na();  // every accumulator final, every operand ring idle
 #pragma unroll 1
         for (int c = sub; c < NCH; c += SPLIT) {
-          if (int64_t(nb) * BN + c * W >= P.N) continue;
+          if (int64_t(nb) * BN + c * W >= Q.N) continue;
           uint32_t r[W];
           const uint32_t taddr = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(c * W);
           if constexpr (W == 16) TMEM_LD16(taddr, r);
@@ -534,7 +567,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         for (int lc = sub; lc < npc; lc += SPLIT) {
           const int c = lc * S + split;
           const int64_t n0 = int64_t(nb) * BN + c * W;
-          if (n0 >= P.N) continue;
+          if (n0 >= Q.N) continue;
           float v[W];
 #pragma unroll
           for (int j = 0; j < W; ++j) v[j] = 0.0f;
@@ -556,7 +589,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 #pragma unroll 1
       for (int c = sub, ci = 0; c < NCH; c += SPLIT, ++ci) {
         const int64_t n0 = int64_t(nb) * BN + c * W;
-        if (n0 >= P.N) continue;
+        if (n0 >= Q.N) continue;
         uint32_t r[W];
         const uint32_t taddr = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * BN + c * W);
         if constexpr (W == 16) TMEM_LD16(taddr, r);
@@ -639,14 +672,10 @@ static bool epi_tma_ok(const GemmArgs& g) {
   return true;
 }
 
+// one problem's kernel parameters and tensor maps for tile shape (BN, CG)
 template <int BN, int CG, bool AUX>
-static void launch_cfg(const GemmArgs& g, cudaStream_t s) {
+static void fill_prob(const GemmArgs& g, int splits, TcProb& P, CUtensorMap& ta, CUtensorMap& tb, EpiMaps& em) {
   using C = TcCfg<BN, CG, AUX>;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    TCB_CUDA(cudaFuncSetAttribute(k_gemm_tc<BN, CG, AUX>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-  });
-  TcParams P{};
   P.M = g.M;
   P.N = g.N;
   P.K = g.K;
@@ -658,17 +687,8 @@ static void launch_cfg(const GemmArgs& g, cudaStream_t s) {
   P.n_blocks = int((g.N + BN - 1) / BN);
   P.k_blocks = int((g.K + TC_BK - 1) / TC_BK);
   P.num_tiles = int64_t(P.m_blocks) * P.n_blocks * g.Z;
-  P.splits = g.force_splits > 1 ? g.force_splits : 1;
-  P.kps = (P.k_blocks + P.splits - 1) / P.splits;
-  P.num_units = P.num_tiles;
-  P.trace = reinterpret_cast<unsigned long long*>(g.trace);
-  const uint32_t fmt = g.a.dtype == TCB_BF16 ? 1u : 0u;
-  P.idesc = (1u << 4)                           // D format f32
-            | (fmt << 7) | (fmt << 10)          // A, B format
-            | (uint32_t(g.ta) << 15)            // A major: 1 = MN
-            | (uint32_t(!g.tb) << 16)           // B major: 1 = MN (B stored [K, N])
-            | (uint32_t(BN >> 3) << 17)         // N
-            | (uint32_t((TC_BM * CG) >> 4) << 24);  // M
+  P.kps = (P.k_blocks + splits - 1) / splits;
+  P.idesc = umma_idesc(TC_BM * CG, BN, g.a.dtype == TCB_BF16, g.ta != 0, g.tb == 0);
   P.c = g.c;
   P.ldc = g.ldc;
   P.c_s1 = g.c_s1;
@@ -688,9 +708,8 @@ static void launch_cfg(const GemmArgs& g, cudaStream_t s) {
                (!g.aux_out || reinterpret_cast<uintptr_t>(g.aux_out) % 16 == 0);
   P.tma_epi = epi_tma_ok(g) && (g.dact == ACT_NONE || AUX) && !g.no_tma_epi;
   const int64_t Z1 = (g.Z + g.Z2 - 1) / g.Z2;
-  CUtensorMap ta = g.ta ? make_map(g.a, g.M, g.K, g.Z2, Z1, 64) : make_map(g.a, g.K, g.M, g.Z2, Z1, TC_BM);
-  CUtensorMap tb = g.tb ? make_map(g.b, g.K, g.N, g.Z2, Z1, C::B_ROWS) : make_map(g.b, g.N, g.K, g.Z2, Z1, 64);
-  EpiMaps em;
+  ta = g.ta ? make_map(g.a, g.M, g.K, g.Z2, Z1, 64) : make_map(g.a, g.K, g.M, g.Z2, Z1, TC_BM);
+  tb = g.tb ? make_map(g.b, g.K, g.N, g.Z2, Z1, C::B_ROWS) : make_map(g.b, g.N, g.K, g.Z2, Z1, 64);
   std::memset(&em, 0, sizeof(em));
   if (P.tma_epi) {
     // boxes of 32 rows x TC_EW columns, swizzled by their row size (see stage_row)
@@ -705,10 +724,33 @@ static void launch_cfg(const GemmArgs& g, cudaStream_t s) {
     if (g.dact != ACT_NONE)
       em.aux = encode4(g.aux, g.aux_dtype, g.N, g.M, g.Z2, Z1, g.ldc, g.c_s2, g.c_s1, TC_EW, 32, sw(TC_EW * 2));
   }
+}
+
+// launch n (1 or 2) problems with one tile shape in a single persistent grid
+template <int BN, int CG, bool AUX>
+static void launch_cfg(const GemmArgs* gs, int n, cudaStream_t s) {
+  using C = TcCfg<BN, CG, AUX>;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    TCB_CUDA(cudaFuncSetAttribute(k_gemm_tc<BN, CG, AUX>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+  });
+  TcParams P{};
+  P.nprob = n;
+  P.splits = (n == 1 && gs[0].force_splits > 1) ? gs[0].force_splits : 1;
+  P.trace = reinterpret_cast<unsigned long long*>(gs[0].trace);
+  CUtensorMap ta[2], tb[2];
+  EpiMaps em[2];
+  for (int i = 0; i < n; ++i) fill_prob<BN, CG, AUX>(gs[i], P.splits, P.pr[i], ta[i], tb[i], em[i]);
+  if (n == 1) {
+    ta[1] = ta[0];
+    tb[1] = tb[0];
+    em[1] = em[0];
+  }
+  P.num_units = P.pr[0].num_tiles + (n > 1 ? P.pr[1].num_tiles : 0);
   const int csz = CG * P.splits;  // cluster: CTA pair x K splits
   int grid;
   if (P.splits > 1) {
-    grid = int(P.num_tiles * csz);  // one tile per cluster (the exchange reuses its operand ring)
+    grid = int(P.num_units * csz);  // one tile per cluster (the exchange reuses its operand ring)
   } else {
     const int64_t units = P.num_units * CG;
     grid = int(units < kNumSMs ? units : kNumSMs);
@@ -726,7 +768,7 @@ static void launch_cfg(const GemmArgs& g, cudaStream_t s) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1 + pdl_attr(&attr[1]);
-  TCB_CUDA(cudaLaunchKernelEx(&cfg, k_gemm_tc<BN, CG, AUX>, ta, tb, em, P));
+  TCB_CUDA(cudaLaunchKernelEx(&cfg, k_gemm_tc<BN, CG, AUX>, ta[0], tb[0], ta[1], tb[1], em[0], em[1], P));
 }
 
 // Tile configuration by a wave-quantised cost model (calibrated on the
@@ -799,17 +841,13 @@ void gemm_prepare(GemmArgs& g, bool exact, GemmWs& keep) {
   g.force_splits = c.splits;
 }
 
-void launch_gemm_tc(const GemmArgs& g, cudaStream_t s) {
-  std::string why;
-  if (!gemm_tc_supported(g, &why)) fail(TCB_ERR_UNIMPLEMENTED, "tcgen05 gemm: " + why);
-  const TcChoice c = choose(g, false);
-  const bool aux = g.dact != ACT_NONE;
-  if (!split_ok(g, c.bn, c.cg, c.splits))
-    fail(TCB_ERR_TYPE, "tcgen05 gemm: split-K " + std::to_string(c.splits) + " not valid for this tile / epilogue");
+static void dispatch_tc(const GemmArgs* gs, int n, const TcChoice& c, cudaStream_t s) {
+  bool aux = false;
+  for (int i = 0; i < n; ++i) aux = aux || gs[i].dact != ACT_NONE;
 #define TC_CASE(BN_, CG_)                                  \
   if (c.bn == BN_ && c.cg == CG_) {                        \
-    if (aux) launch_cfg<BN_, CG_, true>(g, s);             \
-    else launch_cfg<BN_, CG_, false>(g, s);                \
+    if (aux) launch_cfg<BN_, CG_, true>(gs, n, s);         \
+    else launch_cfg<BN_, CG_, false>(gs, n, s);            \
     return;                                                \
   }
   TC_CASE(256, 2)
@@ -819,6 +857,28 @@ void launch_gemm_tc(const GemmArgs& g, cudaStream_t s) {
   TC_CASE(128, 1)
 #undef TC_CASE
   fail(TCB_ERR_TYPE, "tcgen05 gemm: unsupported forced tile config");
+}
+
+void launch_gemm_tc(const GemmArgs& g, cudaStream_t s) {
+  std::string why;
+  if (!gemm_tc_supported(g, &why)) fail(TCB_ERR_UNIMPLEMENTED, "tcgen05 gemm: " + why);
+  const TcChoice c = choose(g, false);
+  if (!split_ok(g, c.bn, c.cg, c.splits))
+    fail(TCB_ERR_TYPE, "tcgen05 gemm: split-K " + std::to_string(c.splits) + " not valid for this tile / epilogue");
+  dispatch_tc(&g, 1, c, s);
+}
+
+// Two independent problems in one grid (same tile shape, no split-K); the
+// problem with more k-blocks per tile goes first so its long tiles start early.
+void launch_gemm_tc_pair(const GemmArgs& g0, const GemmArgs& g1, cudaStream_t s) {
+  std::string why;
+  for (const GemmArgs* g : {&g0, &g1})
+    if (!gemm_tc_supported(*g, &why)) fail(TCB_ERR_UNIMPLEMENTED, "tcgen05 gemm pair: " + why);
+  TcChoice c{g0.force_bn ? g0.force_bn : 256, g0.force_cg ? g0.force_cg : 2, 1};
+  if (c.cg == 2 && (g0.M <= 128 || g1.M <= 128)) c.cg = 1;
+  const bool swap = g1.K > g0.K;
+  GemmArgs gs[2] = {swap ? g1 : g0, swap ? g0 : g1};
+  dispatch_tc(gs, 2, c, s);
 }
 
 }  // namespace tcb

@@ -125,7 +125,8 @@ static void prepare(Session& s, const char* cfg_c) {
 
 /// CPU-only: build the step graph and its memory plan without a device.
 /// out: P, P_pad, lets, planner_peak, arena_plan_bytes, state_bytes, fused_dact,
-/// fused_ln_dy2, fused_emb, dead, remat_replays, peak_before_remat, peak_after_remat
+/// fused_ln_dy2, fused_emb, dead, remat_replays, peak_before_remat, peak_after_remat,
+/// fused_ln_bias, fused_pairs
 int tb_graph_info(const char* cfg, int64_t* out, int n) {
   TB_TRY({
     Session s;
@@ -134,7 +135,8 @@ int tb_graph_info(const char* cfg, int64_t* out, int n) {
     MemProfile mp = peak_memory(L);
     ArenaPlan ap = plan_arena(L);
     int64_t v[] = {s.ts.P, s.ts.P_pad, L.n, mp.peak, ap.size, mp.state_bytes, s.ts.fusion.dact, s.ts.fusion.ln_dy2,
-                   s.ts.fusion.emb_base, s.ts.fusion.dead, s.remat.replays, s.remat.peak_before, s.remat.peak_after};
+                   s.ts.fusion.emb_base, s.ts.fusion.dead, s.remat.replays, s.remat.peak_before, s.remat.peak_after,
+                   s.ts.fusion.ln_bias, s.ts.fusion.pairs};
     for (int i = 0; i < n && i < int(sizeof v / sizeof v[0]); ++i) out[i] = v[i];
   });
 }

@@ -175,6 +175,24 @@ inline void register_extension_ops(OpRegistry& r) {
     if (u.shape != mn) throw TypeError("matmul_dact: aux shape must equal the product's");
     return TensorType{x.dtype, mn};
   });
+  // matmul_pair(a0, b0 [, aux0], a1, b1) {n0, ta0, tb0, alpha0, act0, out0, ta1, tb1, alpha1, out1}
+  //   -> (matmul_t / matmul_dact of problem 0, matmul_t of problem 1): two
+  //   independent GEMMs in one launch (horizontal fusion of a linear's
+  //   data- and weight-gradient, which share dY)
+  reg("matmul_pair", -1, O, [](const V& in, const AttrMap& a) -> Type {
+    const int n0 = int(rel::a_int(a, "n0", 2));
+    if ((n0 != 2 && n0 != 3) || int(in.size()) != n0 + 2) throw TypeError("matmul_pair: (a0, b0 [, aux0], a1, b1)");
+    auto x0 = rel::T(in[0], "matmul_pair"), y0 = rel::T(in[1], "matmul_pair");
+    auto x1 = rel::T(in[n0], "matmul_pair"), y1 = rel::T(in[n0 + 1], "matmul_pair");
+    auto mn0 = gemm_shape(x0, y0, int(rel::a_int(a, "ta0", 0)), int(rel::a_int(a, "tb0", 0)), "matmul_pair");
+    auto mn1 = gemm_shape(x1, y1, int(rel::a_int(a, "ta1", 0)), int(rel::a_int(a, "tb1", 0)), "matmul_pair");
+    if (n0 == 3 && rel::T(in[2], "matmul_pair").shape != mn0) throw TypeError("matmul_pair: aux0 shape");
+    auto od = [&](const char* k, DType d) {
+      auto it = a.find(k);
+      return it == a.end() ? d : dtype_from(ir::attr_string(a, k, ""));
+    };
+    return TupleType{{TensorType{od("out0", x0.dtype), mn0}, TensorType{od("out1", x1.dtype), mn1}}};
+  });
   reg("batch_matmul", 2, O, [](const V& in, const AttrMap& a) -> Type {
     auto x = rel::T(in[0], "batch_matmul"), y = rel::T(in[1], "batch_matmul");
     rel::need_rank(x, 3, "batch_matmul");

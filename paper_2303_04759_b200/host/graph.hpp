@@ -395,8 +395,105 @@ inline UseInfo count_uses(const LetSeq& s) {
 }
 
 struct FusionStats {
-  int dact = 0, ln_dy2 = 0, emb_base = 0, ln_bias = 0, dead = 0;
+  int dact = 0, ln_dy2 = 0, emb_base = 0, ln_bias = 0, pairs = 0, dead = 0;
 };
+
+/// Horizontal fusion (SPEC.md:533-540 applied to GEMMs): a weight-gradient
+/// matmul_t and the nearest bf16 GEMM sharing an operand with it within
+/// `window` lets (the linear's data gradient -- matmul_t or matmul_dact on the
+/// same dY) become one matmul_pair: one persistent launch whose tiles fill the
+/// SMs the small weight-gradient GEMM leaves idle.  The pair is placed at the
+/// later member (every argument of both is defined by then); the earlier
+/// member must have no use before that point.  Both become tuple_gets.
+inline int fuse_gemm_pairs(LetSeq& s, int window = 6) {
+  const int n = int(s.lets.size());
+  auto is_gemm = [](const ExprPtr& e) {
+    return e->kind == ExprKind::Call && (e->op == "matmul_t" || e->op == "matmul_dact");
+  };
+  const DType bf16 = dtype_from("bf16");
+  auto bf16_operands = [&](const ExprPtr& e) {
+    for (int k = 0; k < 2; ++k)
+      if (e->args[k]->kind != ExprKind::VarRef || e->args[k]->var->ty.tensor().dtype != bf16) return false;
+    return true;
+  };
+  auto uses = [&](int k, const ir::Var* v) {
+    for (auto& a : s.lets[k].value->args)
+      if (a->kind == ExprKind::VarRef && a->var.get() == v) return true;
+    return false;
+  };
+  std::vector<char> used(n, 0), drop(n, 0);
+  std::map<int, std::vector<LetBinding>> at_pos;  // replacement lets for position hi
+  int n_pairs = 0;
+  for (int j = 0; j < n; ++j) {
+    auto& b2 = s.lets[j];
+    if (used[j] || !is_gemm(b2.value) || b2.value->op != "matmul_t" || !bf16_operands(b2.value)) continue;
+    if (ir::attr_string(b2.value->call_attrs, "out", "") != "f32") continue;  // weight gradients only
+    for (int d = 1; d <= window; ++d) {
+      int cand[2] = {j - d, j + d};
+      int i = -1;
+      for (int c : cand) {
+        if (c < 0 || c >= n || used[c]) continue;
+        auto& b1 = s.lets[c];
+        if (!is_gemm(b1.value) || !bf16_operands(b1.value) || b1.var->ty.is_tuple()) continue;
+        if (b1.value->op == "matmul_t" && ir::attr_string(b1.value->call_attrs, "out", "") == "f32") continue;
+        bool share = false;
+        for (auto& a2 : b2.value->args)
+          for (auto& a1 : b1.value->args)
+            if (a1->kind == ExprKind::VarRef && a2->kind == ExprKind::VarRef && a1->var == a2->var) share = true;
+        if (!share) continue;
+        const int lo = std::min(c, j), hi = std::max(c, j);
+        bool free_between = true;
+        for (int k = lo + 1; k <= hi && free_between; ++k)
+          if (uses(k, s.lets[lo].var.get())) free_between = false;
+        if (!free_between) continue;
+        i = c;
+        break;
+      }
+      if (i < 0) continue;
+      auto& b1 = s.lets[i];
+      AttrMap at;
+      const auto& a1 = b1.value->call_attrs;
+      const auto& a2 = b2.value->call_attrs;
+      const bool dact = b1.value->op == "matmul_dact";
+      at["n0"] = std::int64_t(dact ? 3 : 2);
+      at["ta0"] = ir::attr_int(a1, "ta", 0);
+      at["tb0"] = ir::attr_int(a1, "tb", 0);
+      at["alpha0"] = ir::attr_double(a1, "alpha", 1.0);
+      if (dact) at["act0"] = ir::attr_string(a1, "act", "none");
+      if (a1.count("out")) at["out0"] = ir::attr_string(a1, "out", "");
+      at["ta1"] = ir::attr_int(a2, "ta", 0);
+      at["tb1"] = ir::attr_int(a2, "tb", 0);
+      at["alpha1"] = ir::attr_double(a2, "alpha", 1.0);
+      at["out1"] = ir::attr_string(a2, "out", "");
+      std::vector<ExprPtr> args(b1.value->args.begin(), b1.value->args.end());
+      args.insert(args.end(), b2.value->args.begin(), b2.value->args.end());
+      auto call = ir::call("matmul_pair", args, at);
+      TupleType tt{{b1.var->ty.tensor(), b2.var->ty.tensor()}};
+      call->ty = tt;
+      auto pv = ir::make_var(b1.var->id + "_pair", tt);
+      auto g0 = ir::tuple_get(ir::var_ref(pv), 0);
+      g0->ty = b1.var->ty;
+      auto g1 = ir::tuple_get(ir::var_ref(pv), 1);
+      g1->ty = b2.var->ty;
+      const int lo = std::min(i, j), hi = std::max(i, j);
+      at_pos[hi] = {LetBinding{pv, call}, LetBinding{b1.var, g0}, LetBinding{b2.var, g1}};
+      drop[lo] = 1;
+      used[i] = used[j] = 1;
+      ++n_pairs;
+      break;
+    }
+  }
+  LetSeq out;
+  out.ret = s.ret;
+  for (int k = 0; k < n; ++k) {
+    if (drop[k]) continue;
+    auto it = at_pos.find(k);
+    if (it == at_pos.end()) out.lets.push_back(s.lets[k]);
+    else out.lets.insert(out.lets.end(), it->second.begin(), it->second.end());
+  }
+  s = std::move(out);
+  return n_pairs;
+}
 
 /// Pattern fusion + dead-let elimination.  Each rewrite needs the absorbed
 /// producer to have exactly one use (SPEC.md:381-388 materialization rule).
@@ -523,6 +620,7 @@ inline FusionStats fuse(LetSeq& s, bool patterns = true) {
     out = std::move(keep);
   }
   s = std::move(out);
+  if (patterns) st.pairs = fuse_gemm_pairs(s);
   return st;
 }
 

@@ -382,6 +382,13 @@ inline double op_cost(const ir::ExprPtr& call) {
     double k = a.shape[ir::attr_int(call->call_attrs, "ta", 0) ? 0 : 1];
     return double(numel(a)) / k * k * double(numel(T(1))) / k;
   }
+  if (base == "matmul_pair") {
+    const int n0 = int(ir::attr_int(call->call_attrs, "n0", 2));
+    const auto &a0 = T(0), &b0 = T(1), &a1 = T(size_t(n0)), &b1 = T(size_t(n0) + 1);
+    double k0 = a0.shape[ir::attr_int(call->call_attrs, "ta0", 0) ? 0 : 1];
+    double k1 = a1.shape[ir::attr_int(call->call_attrs, "ta1", 0) ? 0 : 1];
+    return double(numel(a0)) * double(numel(b0)) / k0 + double(numel(a1)) * double(numel(b1)) / k1;
+  }
   if (base == "attention" || base == "attention_dx") {
     const auto& q = T(0);
     double S = double(ir::attr_int(call->call_attrs, "seq", q.shape[0]));

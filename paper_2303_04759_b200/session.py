@@ -148,7 +148,7 @@ INFO_FIELDS = ["P", "P_pad", "T", "arena_bytes", "state_bytes", "planner_peak", 
                "remat_replays", "peak_before_remat", "compile_us", "shard"]
 GRAPH_FIELDS = ["P", "P_pad", "lets", "planner_peak", "arena_plan_bytes", "state_bytes", "fused_dact",
                 "fused_ln_dy2", "fused_emb", "dead", "remat_replays", "peak_before_remat",
-                "peak_after_remat"]
+                "peak_after_remat", "fused_ln_bias", "fused_pairs"]
 
 
 def graph_info(cfg: ModelConfig) -> dict:

@@ -215,6 +215,30 @@ def test_gemm_split_k(bn, cg, splits, ta, tb):
     assert all(torch.equal(outs[0], x) for x in outs[1:])
 
 
+@pytest.mark.parametrize("dact", [0, 1])
+@pytest.mark.parametrize("tile", [(256, 2), (128, 1)])
+def test_matmul_pair(dact, tile):
+    """Two independent GEMMs in one persistent launch (a linear's data gradient
+    [with act'(aux)] and weight gradient sharing dY), each against the oracle."""
+    T, H, F = 640, 192, 320  # ragged: 640 = 2.5 pair tiles
+    dy, w, x = rn(T, F), rn(H, F), rn(T, H)
+    ins = [(dy, BF16), (w, BF16)]
+    at = {"n0": 2, "ta0": 0, "tb0": 1, "ta1": 1, "tb1": 0, "out1": "f32", "alpha1": 1.0,
+          "tc_bn": tile[0], "tc_cg": tile[1]}
+    if dact:
+        dy, w, u = rn(T, H), rn(F, H), rn(T, F, lo=-3, hi=3)
+        ins = [(dy, BF16), (w, BF16), (u, BF16)]
+        x = rn(T, F)
+        at.update({"n0": 3, "act0": "gelu"})
+        outs = [((T, F), BF16), ((F, H), F32)]
+    else:
+        outs = [((T, H), BF16), ((H, F), F32)]
+    ins += [(x, BF16), (dy, BF16)]
+    g, o = run_both("matmul_pair", ins, outs, at)
+    assert rel_err(g[0], o[0]) < BF16_TOL, rel_err(g[0], o[0])
+    assert rel_err(g[1], o[1]) < 1e-5, rel_err(g[1], o[1])
+
+
 def test_gemm_split_k_rejects_fused_epilogue():
     """Split-K only covers the pure matmul epilogue; asking for it with bias/act fails loudly."""
     from paper_2303_04759_b200.runtime import TcbError
@@ -341,11 +365,12 @@ def test_add_layer_norm_and_backward(p):
     outs = [((T, H), BF16), ((H,), F32), ((H,), F32), ((T, H), BF16), ((H,), F32)]
     g, o = run_both("layer_norm_dx", [(s, BF16), (gm, F32), (mean, F32), (rstd, F32), (dy, BF16), (dy2, BF16)],
                     outs, {**attrs, "bias_grad": 1})
-    assert rel_err(g[4], o[4]) < 1e-5, rel_err(g[4], o[4])
+    # the column sums inherit the bf16 rounding differences of dx (5e-3 norm-wise)
+    assert rel_err(g[4], o[4]) < 1e-4, rel_err(g[4], o[4])
     assert rel_err(g[3], o[3]) < 5e-3 and rel_err(g[1], o[1]) < 1e-5
     g, o = run_both("layer_norm_dx", [(s, BF16), (gm, F32), (mean, F32), (rstd, F32), (dy, BF16)],
                     outs[:3] + outs[4:], {**attrs, "p": 0.0, "bias_grad": 1})
-    assert rel_err(g[3], o[3]) < 1e-5 and rel_err(g[0], o[0]) < 5e-3
+    assert rel_err(g[3], o[3]) < 1e-4 and rel_err(g[0], o[0]) < 5e-3
 
 
 def test_layer_norm_dx_f32():
