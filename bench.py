@@ -27,6 +27,8 @@ import sys
 import threading
 import time
 
+import numpy as np
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -216,6 +218,47 @@ def gemm_roofline(stream, peaks, iters=50):
             "kernel": f"b200.linear tcgen05 {M}x{K}x{N} bf16 (+bias+gelu+preact)", "us_per_launch": round(ms * 1e3, 2)}
 
 
+def max_batch_report(stream_sync_free_bytes: int):
+    """The metric's second half: max trainable batch under rematerialisation.
+    The planner (CPU) finds the largest BERT-base seq128 batch whose static
+    arena + state fits the device budget with and without remat; then ONE
+    training step at that batch runs on the GPU (with the remat plan) to show
+    it trains, timed with CUDA events."""
+    import torch
+    from paper_2303_04759_b200.session import ModelConfig, Session, max_batch_under_remat, synthetic_batch
+    budget = int(stream_sync_free_bytes * 0.92) - (2 << 30)
+    b_remat, gi = max_batch_under_remat(ModelConfig.bert_base, budget)
+    b_plain, _ = max_batch_under_remat(ModelConfig.bert_base, budget, remat=False)
+    out = {"model": "bert-base seq128 bf16 Adam", "budget_gb": round(budget / 1e9, 1), "max_batch": b_remat,
+           "max_batch_no_remat": b_plain, "remat_replays": gi.get("remat_replays"),
+           "planned_bytes_gb": round((gi.get("arena_plan_bytes", 0) + gi.get("state_bytes", 0)) / 1e9, 1)}
+    try:
+        cfg = ModelConfig.bert_base(B=b_remat)
+        cfg.extra["budget"] = budget
+        s = Session(cfg)
+        s.init_params()
+        ids, labels = synthetic_batch(cfg)
+        s.set_batch(ids, labels)
+        s.step(graph=False)
+        s.sync()
+        ev = Events()
+        ev.start(s.stream)
+        s.step(graph=False)
+        ev.stop(s.stream)
+        s.sync()
+        ms = ev.ms()
+        loss = s.loss()
+        out.update({"verified_on_gpu": bool(np.isfinite(loss)), "step_ms": round(ms, 1),
+                    "samples_per_s": round(b_remat / (ms * 1e-3), 1), "loss": round(loss, 4)})
+        s.close()
+        del s
+        torch.cuda.empty_cache()
+    except Exception as e:  # planner said it fits; report what the device said
+        out["verified_on_gpu"] = False
+        out["error"] = str(e)[:200]
+    return out
+
+
 def cpu_baseline_port():
     """The CPU oracle (ANF interpreter over the exec_base restatement, one
     thread) on a bounded sample: ONE C2 training step at B=1 (1 sample, S=128,
@@ -320,6 +363,12 @@ def run_ours(args):
         "clocks": clk,
         "roofline": roof,
     }
+    if world == 1 and not args.no_max_batch:
+        s.close()
+        del s
+        import torch
+        free, total = torch.cuda.mem_get_info()
+        out["config"]["max_batch_under_remat"] = max_batch_report(free)
     if world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline_port()
     print(json.dumps(out), flush=True)
@@ -372,6 +421,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-max-batch", action="store_true")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     if args.impl == "reference":

@@ -143,6 +143,46 @@ def synthetic_batch(cfg: ModelConfig, seed: int | None = None):
     return ids, labels
 
 
+def plan_fits(cfg: ModelConfig, budget: int, remat: bool) -> tuple[bool, dict]:
+    """CPU planner: does the step at cfg fit `budget` device bytes (static
+    arena + parameter/optimizer state)?  With remat, the rematerialisation pass
+     runs under the budget first; an infeasible plan
+    (no evictable tensor) does not fit."""
+    c = ModelConfig(**{f.name: getattr(cfg, f.name) for f in fields(cfg) if f.name != "extra"})
+    c.extra = dict(cfg.extra)
+    if remat:
+        c.extra["budget"] = int(budget)
+    try:
+        gi = graph_info(c)
+    except RuntimeError:
+        return False, {}
+    return gi["arena_plan_bytes"] + gi["state_bytes"] <= budget, gi
+
+
+def max_batch_under_remat(factory, budget: int, b0: int = 32, remat: bool = True) -> tuple[int, dict]:
+    """Largest per-GPU batch the planner fits in `budget` bytes: doubling from
+    b0, then bisection ('double B until BudgetInfeasible,
+    then bisect').  Returns (B, graph_info at B)."""
+    ok, gi = plan_fits(factory(B=b0), budget, remat)
+    if not ok:
+        return 0, {}
+    lo, hi, best = b0, None, gi
+    while hi is None:
+        ok, g = plan_fits(factory(B=lo * 2), budget, remat)
+        if ok:
+            lo, best = lo * 2, g
+        else:
+            hi = lo * 2
+    while hi - lo > 1:
+        mid = (lo + hi) // 2
+        ok, g = plan_fits(factory(B=mid), budget, remat)
+        if ok:
+            lo, best = mid, g
+        else:
+            hi = mid
+    return lo, best
+
+
 INFO_FIELDS = ["P", "P_pad", "T", "arena_bytes", "state_bytes", "planner_peak", "instructions",
                "kernels_per_step", "lets", "fused_dact", "fused_ln_dy2", "fused_emb", "dead",
                "remat_replays", "peak_before_remat", "compile_us", "shard"]
