@@ -131,10 +131,20 @@ __device__ __forceinline__ float gelu_grad_f(float x) {
 // adding a few ulp) sharing one exponential exp(-x^2/2) with the pdf term.
 // ~14 instructions instead of ~35 for erff/expf; the bf16 results differ from
 // the oracle's erff in a handful of last-bit roundings (tolerance-checked).
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 __device__ __forceinline__ void fast_phi(float x, float& phi, float& e) {
   const float ax = fabsf(x);
-  e = exp2f(x * x * -0.72134752044448170f);                       // exp(-x^2/2)
-  const float t = __frcp_rn(fmaf(0.23164188f, ax, 1.0f));         // 1/(1 + p z), z = |x|/sqrt(2)
+  e = ex2_approx(x * x * -0.72134752044448170f);                   // exp(-x^2/2)
+  const float t = rcp_approx(fmaf(0.23164188f, ax, 1.0f));         // 1/(1 + p z), z = |x|/sqrt(2)
   float poly = fmaf(t, 1.061405429f, -1.453152027f);
   poly = fmaf(t, poly, 1.421413741f);
   poly = fmaf(t, poly, -0.284496736f);
