@@ -36,6 +36,7 @@ constexpr int TC_THREADS = 128 + 32 * TC_EPI_WARPS;  // warps 0-3: TMA, MMA, TME
 constexpr int TC_EW = 16;                             // epilogue chunk width (columns)
 constexpr int TC_SLOT = 32 * TC_EW * 4;               // per-warp output slot: f32 box or (y, u) 16-bit boxes
 constexpr int TC_AUX_SLOT = 32 * TC_EW * 2;           // per-warp act'(aux) slot (16-bit)
+constexpr int TC_AUX_RING = 3;                        // aux boxes in flight per warp (2 chunks ahead)
 
 template <int BN, int CG, bool AUX>
 struct TcCfg {
@@ -43,9 +44,10 @@ struct TcCfg {
   static constexpr int A_BYTES = TC_BM * TC_BK * 2;
   static constexpr int B_BYTES = B_ROWS * TC_BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int EPI_BYTES = TC_EPI_WARPS * 2 * TC_SLOT + (AUX ? TC_EPI_WARPS * 2 * TC_AUX_SLOT : 0);
+  static constexpr int EPI_BYTES =
+      TC_EPI_WARPS * 2 * TC_SLOT + (AUX ? TC_EPI_WARPS * TC_AUX_RING * TC_AUX_SLOT : 0);
   static constexpr int BIAS_BYTES = TC_EPI_WARPS * ((BN / TC_EW + TC_EPI_WARPS / 4 - 1) / (TC_EPI_WARPS / 4)) * TC_EW * 4;
-  static constexpr int BAR_BYTES = 512;
+  static constexpr int BAR_BYTES = 1024;
   static constexpr int BUDGET = 227 * 1024 - 1024 - BAR_BYTES - EPI_BYTES - BIAS_BYTES;
   static constexpr int STAGES = BUDGET / STAGE_BYTES > 8 ? 8 : BUDGET / STAGE_BYTES;
   static constexpr int TMEM_COLS = 2 * BN <= 256 ? 256 : 512;
@@ -247,14 +249,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   uint8_t* sB = smem + C::STAGES * C::A_BYTES;
   uint8_t* sEpi = smem + C::STAGES * C::STAGE_BYTES;        // epilogue warps x 2 output slots
   uint8_t* sAux = sEpi + TC_EPI_WARPS * 2 * TC_SLOT;       // epilogue warps x 2 aux slots (AUX)
-  float* sBias = reinterpret_cast<float*>(sAux + (AUX ? TC_EPI_WARPS * 2 * TC_AUX_SLOT : 0));
+  float* sBias = reinterpret_cast<float*>(sAux + (AUX ? TC_EPI_WARPS * TC_AUX_RING * TC_AUX_SLOT : 0));
   uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sBias) + C::BIAS_BYTES);
   uint64_t* full = bars;
   uint64_t* empty = bars + C::STAGES;
   uint64_t* tfull = bars + 2 * C::STAGES;
   uint64_t* tempty = tfull + 2;
-  uint64_t* abar = tempty + 2;  // 2 per epilogue warp
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(abar + 2 * TC_EPI_WARPS);
+  uint64_t* abar = tempty + 2;  // TC_AUX_RING per epilogue warp
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(abar + TC_AUX_RING * TC_EPI_WARPS);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool clustered = CG == 2 || P.splits > 1;
@@ -285,7 +287,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       mbar_init(&tfull[s], 1);
       mbar_init(&tempty[s], CG * TC_EPI_WARPS);
     }
-    for (int s = 0; s < 2 * TC_EPI_WARPS; ++s) mbar_init(&abar[s], 1);
+    for (int s = 0; s < TC_AUX_RING * TC_EPI_WARPS; ++s) mbar_init(&abar[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
@@ -410,14 +412,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const int q = warp & 3;
     const int sub = ew >> 2;
     uint8_t* slots = sEpi + ew * 2 * TC_SLOT;
-    uint8_t* aslots = sAux + ew * 2 * TC_AUX_SLOT;
+    uint8_t* aslots = sAux + ew * TC_AUX_RING * TC_AUX_SLOT;
     float* wbias = sBias + ew * CPW * W;
-    uint64_t* ab = abar + 2 * ew;
+    uint64_t* ab = abar + TC_AUX_RING * ew;
     const uint32_t tempty_addr0 = CG == 2 ? mapa(smem_u32(&tempty[0]), lead) : smem_u32(&tempty[0]);
     int acc = 0;
     uint32_t acc_phase = 0;
     uint32_t sidx = 0;    // output slot ring
-    uint32_t achunk = 0;  // aux chunk counter (slot = &1, phase = >>1 &1)
+    uint32_t achunk = 0;  // aux chunk counter: ring slot achunk % RING, phase (achunk / RING) & 1
     // aux prefetch cursor over the same (tile, chunk) order as the consumer
     int64_t pt = cl_id;
     int pc = sub;
@@ -442,11 +444,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         }
         if (n0 >= Q.N) continue;  // chunk skipped by the consumer too
         if (lane == 0) {
-          uint64_t* bar = &ab[aissue & 1];
+          uint64_t* bar = &ab[aissue % TC_AUX_RING];
           mbar_expect_tx(bar, 32 * W * 2);
           asm volatile(
               "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
-              " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(aslots + (aissue & 1) * TC_AUX_SLOT)),
+              " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(aslots + (aissue % TC_AUX_RING) * TC_AUX_SLOT)),
               "l"(reinterpret_cast<uint64_t>(prob ? &EM1.aux : &EM0.aux)), "r"(int(n0)), "r"(mrow), "r"(int(z % Q.Z2)),
               "r"(int(z / Q.Z2)), "r"(smem_u32(bar))
               : "memory");
@@ -455,7 +457,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         return;
       }
     };
-    if (AUX) issue_next_aux();
+    if (AUX)
+      for (int k = 0; k < TC_AUX_RING - 1; ++k) issue_next_aux();
 
     for (int64_t u = cl_id; u < P.num_units; u += n_cl) {
       const int prob = unit_prob(P, u);
@@ -488,8 +491,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         }
         if (Q.tma_epi) {
           if (has_aux) {
-            // this chunk's aux box was issued one chunk ago; prefetch the next
-            const uint32_t s = achunk & 1, ph = (achunk >> 1) & 1;
+            // this chunk's aux box was issued RING-1 chunks ago; keep the ring full
+            const uint32_t s = achunk % TC_AUX_RING, ph = (achunk / TC_AUX_RING) & 1;
             issue_next_aux();
             mbar_wait(&ab[s], ph);
             float a[W];

@@ -154,6 +154,16 @@ def linear_gelu(iters, M=4096, K=768, N=3072):
                        [y.data_ptr(), u.data_ptr()][:len(outs)], iters)
         res.append({"name": f"linear_{act}_{M}x{K}x{N}", "us": round(us, 2),
                     "tflops": round(2.0 * M * N * K / us / 1e6, 1)})
+    # the FFN2 backward data gradient with the fused GELU' epilogue vs plain
+    dy = torch.randn(M, K, device="cuda").to(torch.bfloat16)
+    w2 = (0.02 * torch.randn(N, K, device="cuda")).to(torch.bfloat16)
+    plan = Plan("matmul_dact", [((M, K), BF16), ((N, K), BF16), ((M, N), BF16)], [((M, N), BF16)],
+                {"tb": 1, "act": "gelu"})
+    us = time_plan(plan, [dy.data_ptr(), w2.data_ptr(), u.data_ptr()], [y.data_ptr()], iters)
+    res.append({"name": f"matmul_dact_gelu_{M}x{K}x{N}", "us": round(us, 2), "tflops": round(2.0 * M * N * K / us / 1e6, 1)})
+    plan = Plan("matmul_t", [((M, K), BF16), ((N, K), BF16)], [((M, N), BF16)], {"tb": 1})
+    us = time_plan(plan, [dy.data_ptr(), w2.data_ptr()], [y.data_ptr()], iters)
+    res.append({"name": f"matmul_t_tb_{M}x{K}x{N}", "us": round(us, 2), "tflops": round(2.0 * M * N * K / us / 1e6, 1)})
     return res
 
 
