@@ -65,7 +65,7 @@ void gemm_prepare(GemmArgs& g, bool exact, GemmWs& keep);
 // Fused short-sequence attention (k_attention.cu): bf16, head dim 64, S <= 128
 bool attn_fused_ok(int dt, int64_t S, int64_t H, int64_t A, bool exact);
 void launch_attn_fwd(const void* qkv, void* ctx, void* probs, int64_t B, int64_t S, int64_t H, int64_t A, float scale,
-                     int causal, const DropCfg& d, cudaStream_t s);
+                     int causal, const DropCfg& d, cudaStream_t s, void* trace = nullptr);
 void launch_attn_bwd(const void* qkv, const void* probs, const void* dctx, void* dqkv, int64_t B, int64_t S, int64_t H,
                      int64_t A, float scale, int causal, const DropCfg& d, cudaStream_t s);
 

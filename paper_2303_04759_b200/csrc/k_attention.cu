@@ -30,7 +30,8 @@ constexpr int AT_TILE = 16384;    // 128 rows x 128 B
 constexpr int AT_THREADS = 256;   // 8 warps: 2 per TMEM lane quarter, one per 64-key half
 
 struct AttnArgs {
-  int S, H, A, dh, causal;
+  int S, H, A, dh, causal, Z;
+  unsigned long long* trace;
   float scale;
   DropCfg d;
 };
@@ -62,8 +63,8 @@ __device__ __forceinline__ void keep_bits64(const DropCfg& d, uint64_t base, int
     }
   }
 }
-// e^x on the MUFU path (ex2.approx); the oracle's expf differs by a few ulp
-__device__ __forceinline__ float fast_exp(float x) { return exp2f(x * 1.4426950408889634f); }
+// e^x on the MUFU path (ex2.approx; -inf -> 0); the oracle's expf differs by a few ulp
+__device__ __forceinline__ float fast_exp(float x) { return ex2_approx(x * 1.4426950408889634f); }
 
 // ------------------------------------------------------------------ forward
 // Thread layout: warp w owns TMEM lane quarter q = w % 4 (query rows 32q..+31)
@@ -73,24 +74,26 @@ __global__ void __launch_bounds__(AT_THREADS) k_attn_fwd(const __grid_constant__
                                                          const __grid_constant__ CUtensorMap m_probs,
                                                          const __grid_constant__ CUtensorMap m_ctx,
                                                          const AttnArgs a) {
+  // Persistent over heads z = blockIdx.x, +gridDim.x, ...: the Q/K/V tiles of
+  // the next head stream in (TMA, second buffer) while this head's softmax and
+  // PV product run; ctx / probs leave through asynchronous TMA stores.
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ = sm;
-  uint8_t* sK = sm + AT_TILE;
-  uint8_t* sV = sm + 2 * AT_TILE;
-  uint8_t* sP = sm + 3 * AT_TILE;  // 2 tiles: keys 0-63, 64-127
-  float* red = reinterpret_cast<float*>(sm + 5 * AT_TILE);  // [2 stats][2 halves][128 rows]
-  uint64_t* bar = reinterpret_cast<uint64_t*>(red + 512);    // load, mma1, mma2
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 3);
+  uint8_t* sQKV = sm;                        // 2 buffers x (Q, K, V)
+  uint8_t* sP = sm + 6 * AT_TILE;            // 2 tiles: keys 0-63, 64-127 (probs, stored)
+  uint8_t* sPd = sm + 8 * AT_TILE;           // 2 tiles: dropout(P), the PV operand (p > 0)
+  float* red = reinterpret_cast<float*>(sm + 10 * AT_TILE);  // [2 stats][2 halves][128 rows]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(red + 512);   // load[2], mma1, mma2
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 4);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int z = blockIdx.x, b = z / a.A, h = z % a.A;
   const int q = warp & 3, hf = warp >> 2;
   const int row = q * 32 + lane;  // query row = TMEM lane
   const int j0 = hf * 64;         // this thread's key columns
+  const int Z = gridDim.x > 0 ? a.Z : 0;
   if (tid == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&m_qkv)) : "memory");
-    for (int i = 0; i < 3; ++i) mbar_init(&bar[i], 1);
+    for (int i = 0; i < 4; ++i) mbar_init(&bar[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) tmem_alloc1<256>(tslot);
@@ -101,137 +104,173 @@ __global__ void __launch_bounds__(AT_THREADS) k_attn_fwd(const __grid_constant__
   pdl_wait();
   pdl_trigger();
 
-  if (tid == 0) {
-    mbar_expect_tx(&bar[0], 3 * AT_TILE);
-    tma_load_3(sQ, &m_qkv, &bar[0], h * AT_D, 0, b);
-    tma_load_3(sK, &m_qkv, &bar[0], a.H + h * AT_D, 0, b);
-    tma_load_3(sV, &m_qkv, &bar[0], 2 * a.H + h * AT_D, 0, b);
-    mbar_wait(&bar[0], 0);
-    tc_fence_after();
-    constexpr uint32_t id1 = umma_idesc(128, 128, true, false, false);
-#pragma unroll
-    for (int k = 0; k < 4; ++k)
-      tc_mma<1>(tm, umma_desc(smem_u32(sQ) + k * 32, 16, 1024), umma_desc(smem_u32(sK) + k * 32, 16, 1024), id1,
-                k ? 1u : 0u);
-    tc_commit<1>(&bar[1]);
-  }
-  // dropout keep bits overlap the QK^T MMA
-  uint32_t kb[2];
-  keep_bits64(a.d, (uint64_t(z) * a.S + row) * a.S, j0, a.S, kb);
-  mbar_wait(&bar[1], 0);
-  tc_fence_after();
-
-  // ---- softmax over this thread's 64 scores
-  float v[64];
+  auto issue_load = [&](int zz, int buf) {
+    const int bb = zz / a.A, hh = zz % a.A;
+    uint8_t* dst = sQKV + buf * 3 * AT_TILE;
+    mbar_expect_tx(&bar[buf], 3 * AT_TILE);
+    tma_load_3(dst, &m_qkv, &bar[buf], hh * AT_D, 0, bb);
+    tma_load_3(dst + AT_TILE, &m_qkv, &bar[buf], a.H + hh * AT_D, 0, bb);
+    tma_load_3(dst + 2 * AT_TILE, &m_qkv, &bar[buf], 2 * a.H + hh * AT_D, 0, bb);
+  };
+  if (tid == 0 && int(blockIdx.x) < Z) issue_load(blockIdx.x, 0);
   const uint32_t trow = tm + (uint32_t(q * 32) << 16);
-  {
-    uint32_t r[32];
+  int it = 0;
+  unsigned long long* tr = a.trace ? a.trace + blockIdx.x * 8 : nullptr;
+  auto T = [&](int k) {
+    if (tr && tid == 0 && it == 1) tr[k] = gtimer();
+  };
+  for (int z = blockIdx.x; z < Z; z += gridDim.x, ++it) {
+    T(0);
+    const int buf = it & 1;
+    const int b = z / a.A, h = z % a.A;
+    uint8_t* sQ = sQKV + buf * 3 * AT_TILE;
+    uint8_t* sK = sQ + AT_TILE;
+    uint8_t* sV = sQ + 2 * AT_TILE;
+    if (tid == 0) {
+      const int zn = z + int(gridDim.x);
+      if (zn < Z) {
+        // the other buffer last held head it-1: its MMAs are complete and its
+        // Q tile (ctx staging) has been read by that head's store
+        bulk_wait_read<0>();
+        issue_load(zn, buf ^ 1);
+      }
+      mbar_wait(&bar[buf], (it >> 1) & 1);
+      T(1);
+      tc_fence_after();
+      constexpr uint32_t id1 = umma_idesc(128, 128, true, false, false);
 #pragma unroll
-    for (int c = 0; c < 2; ++c) {
-      TMEM_LD32(trow + j0 + c * 32, r);
-      tmem_wait_ld();
-#pragma unroll
-      for (int j = 0; j < 32; ++j) v[c * 32 + j] = __uint_as_float(r[j]);
+      for (int k = 0; k < 4; ++k)
+        tc_mma<1>(tm, umma_desc(smem_u32(sQ) + k * 32, 16, 1024), umma_desc(smem_u32(sK) + k * 32, 16, 1024), id1,
+                  k ? 1u : 0u);
+      tc_commit<1>(&bar[2]);
     }
-  }
-  float mx = -INFINITY;
+    // dropout keep bits overlap the QK^T MMA
+    uint32_t kb[2];
+    keep_bits64(a.d, (uint64_t(z) * a.S + row) * a.S, j0, a.S, kb);
+    mbar_wait(&bar[2], it & 1);
+    tc_fence_after();
+    T(2);
+
+    // ---- softmax over this thread's 64 scores
+    float v[64];
+    {
+      uint32_t r[32];
 #pragma unroll
-  for (int j = 0; j < 64; ++j) {
-    const int col = j0 + j;
-    float t = v[j] * a.scale;
-    if (col >= a.S || (a.causal && col > row)) t = -INFINITY;
-    v[j] = t;
-    mx = fmaxf(mx, t);
-  }
-  red[hf * 128 + row] = mx;
-  __syncthreads();
-  mx = fmaxf(red[row], red[128 + row]);
-  float sum = 0.0f;
+      for (int c = 0; c < 2; ++c) {
+        TMEM_LD32(trow + j0 + c * 32, r);
+        tmem_wait_ld();
 #pragma unroll
-  for (int j = 0; j < 64; ++j) {
-    v[j] = v[j] == -INFINITY ? 0.0f : fast_exp(v[j] - mx);
-    sum += v[j];
-  }
-  red[256 + hf * 128 + row] = sum;
-  __syncthreads();
-  const float inv = row < a.S ? 1.0f / (red[256 + row] + red[384 + row]) : 0.0f;
-  uint8_t* tileP = sP + hf * AT_TILE;
-  // P rounded to bf16 (the stored probs) = this half's K-major A tile
+        for (int j = 0; j < 32; ++j) v[c * 32 + j] = __uint_as_float(r[j]);
+      }
+    }
+    // scores scaled into the log2 domain: p = 2^(s*scale*log2e - max)
+    const float sl2 = a.scale * 1.4426950408889634f;
+    const int lim = a.causal ? min(a.S, row + 1) : a.S;  // valid key columns of this row
+    float mx = -INFINITY;
 #pragma unroll
-  for (int g = 0; g < 8; ++g) {
-    uint4 w;
-    w.x = pack_bf2(v[g * 8 + 0] * inv, v[g * 8 + 1] * inv);
-    w.y = pack_bf2(v[g * 8 + 2] * inv, v[g * 8 + 3] * inv);
-    w.z = pack_bf2(v[g * 8 + 4] * inv, v[g * 8 + 5] * inv);
-    w.w = pack_bf2(v[g * 8 + 6] * inv, v[g * 8 + 7] * inv);
-    *reinterpret_cast<uint4*>(tileP + sw128(row, g)) = w;
-    v[g * 8 + 0] = bf_lo(w.x), v[g * 8 + 1] = bf_hi(w.x), v[g * 8 + 2] = bf_lo(w.y), v[g * 8 + 3] = bf_hi(w.y);
-    v[g * 8 + 4] = bf_lo(w.z), v[g * 8 + 5] = bf_hi(w.z), v[g * 8 + 6] = bf_lo(w.w), v[g * 8 + 7] = bf_hi(w.w);
-  }
-  fence_proxy_async();
-  __syncthreads();
-  if (tid == 0) {
-    tma_store_4d(&m_probs, sP, 0, 0, z, 0);
-    if (a.S > 64) tma_store_4d(&m_probs, sP + AT_TILE, 64, 0, z, 0);
-    bulk_commit();
-  }
-  if (a.d.p > 0.0f) {
-    // Pd = bf16(P * keep / (1-p)) over the same tile once the probs store has read it
+    for (int j = 0; j < 64; ++j) {
+      const float t = j0 + j < lim ? v[j] * sl2 : -INFINITY;
+      v[j] = t;
+      mx = fmaxf(mx, t);
+    }
+    red[hf * 128 + row] = mx;
+    // the previous head's probs store must have read sP before it is rewritten
     if (tid == 0) bulk_wait_read<0>();
     __syncthreads();
+    mx = fmaxf(red[row], red[128 + row]);
+    float sum = 0.0f;
+#pragma unroll
+    for (int j = 0; j < 64; ++j) {
+      v[j] = ex2_approx(v[j] - mx);  // ex2(-inf) = 0 for masked columns
+      sum += v[j];
+    }
+    red[256 + hf * 128 + row] = sum;
+    __syncthreads();
+    const float inv = row < a.S ? 1.0f / (red[256 + row] + red[384 + row]) : 0.0f;
+    uint8_t* tileP = sP + hf * AT_TILE;
+    // P rounded to bf16 (the stored probs) = this half's K-major A tile
 #pragma unroll
     for (int g = 0; g < 8; ++g) {
-      float pd[8];
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const int j = g * 8 + e;
-        pd[e] = ((kb[j >> 5] >> (j & 31)) & 1u) ? v[j] * a.d.scale : 0.0f;
-      }
       uint4 w;
-      w.x = pack_bf2(pd[0], pd[1]);
-      w.y = pack_bf2(pd[2], pd[3]);
-      w.z = pack_bf2(pd[4], pd[5]);
-      w.w = pack_bf2(pd[6], pd[7]);
+      w.x = pack_bf2(v[g * 8 + 0] * inv, v[g * 8 + 1] * inv);
+      w.y = pack_bf2(v[g * 8 + 2] * inv, v[g * 8 + 3] * inv);
+      w.z = pack_bf2(v[g * 8 + 4] * inv, v[g * 8 + 5] * inv);
+      w.w = pack_bf2(v[g * 8 + 6] * inv, v[g * 8 + 7] * inv);
       *reinterpret_cast<uint4*>(tileP + sw128(row, g)) = w;
+      v[g * 8 + 0] = bf_lo(w.x), v[g * 8 + 1] = bf_hi(w.x), v[g * 8 + 2] = bf_lo(w.y), v[g * 8 + 3] = bf_hi(w.y);
+      v[g * 8 + 4] = bf_lo(w.z), v[g * 8 + 5] = bf_hi(w.z), v[g * 8 + 6] = bf_lo(w.w), v[g * 8 + 7] = bf_hi(w.w);
     }
     fence_proxy_async();
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (tid == 0) {
-    tc_fence_after();
-    constexpr uint32_t id2 = umma_idesc(128, 64, true, false, true);
-#pragma unroll
-    for (int k = 0; k < 8; ++k)
-      tc_mma<1>(tm + 128, umma_desc(smem_u32(sP) + (k >> 2) * AT_TILE + (k & 3) * 32, 16, 1024),
-                umma_desc(smem_u32(sV) + k * 2048, AT_TILE, 1024), id2, k ? 1u : 0u);
-    tc_commit<1>(&bar[2]);
-  }
-  mbar_wait(&bar[2], 0);
-  tc_fence_after();
-  // ---- ctx row, this thread's 32 head-dim columns -> bf16 -> staging (sQ) -> TMA store
-  {
-    uint32_t r[32];
-    TMEM_LD32(trow + 128 + hf * 32, r);
-    tmem_wait_ld();
-#pragma unroll
-    for (int g = 0; g < 4; ++g) {
-      uint4 w;
-      w.x = pack_bf2(__uint_as_float(r[g * 8 + 0]), __uint_as_float(r[g * 8 + 1]));
-      w.y = pack_bf2(__uint_as_float(r[g * 8 + 2]), __uint_as_float(r[g * 8 + 3]));
-      w.z = pack_bf2(__uint_as_float(r[g * 8 + 4]), __uint_as_float(r[g * 8 + 5]));
-      w.w = pack_bf2(__uint_as_float(r[g * 8 + 6]), __uint_as_float(r[g * 8 + 7]));
-      *reinterpret_cast<uint4*>(sQ + sw128(row, hf * 4 + g)) = w;
+    __syncthreads();
+    T(3);
+    if (tid == 0) {
+      tma_store_4d(&m_probs, sP, 0, 0, z, 0);
+      if (a.S > 64) tma_store_4d(&m_probs, sP + AT_TILE, 64, 0, z, 0);
+      bulk_commit();
     }
+    uint8_t* sA = sP;
+    if (a.d.p > 0.0f) {
+      // Pd = bf16(P * keep / (1-p)) into its own tile: the probs store keeps reading sP
+      sA = sPd;
+      uint8_t* tileP = sPd + hf * AT_TILE;
+#pragma unroll
+      for (int g = 0; g < 8; ++g) {
+        float pd[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const int j = g * 8 + e;
+          pd[e] = ((kb[j >> 5] >> (j & 31)) & 1u) ? v[j] * a.d.scale : 0.0f;
+        }
+        uint4 w;
+        w.x = pack_bf2(pd[0], pd[1]);
+        w.y = pack_bf2(pd[2], pd[3]);
+        w.z = pack_bf2(pd[4], pd[5]);
+        w.w = pack_bf2(pd[6], pd[7]);
+        *reinterpret_cast<uint4*>(tileP + sw128(row, g)) = w;
+      }
+      fence_proxy_async();
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (tid == 0) {
+      tc_fence_after();
+      constexpr uint32_t id2 = umma_idesc(128, 64, true, false, true);
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+          tc_mma<1>(tm + 128, umma_desc(smem_u32(sA) + (k >> 2) * AT_TILE + (k & 3) * 32, 16, 1024),
+                  umma_desc(smem_u32(sV) + k * 2048, AT_TILE, 1024), id2, k ? 1u : 0u);
+      tc_commit<1>(&bar[3]);
+    }
+    mbar_wait(&bar[3], it & 1);
+    tc_fence_after();
+    T(4);
+    // ---- ctx row, this thread's 32 head-dim columns -> bf16 -> staging (this
+    // head's Q tile, no longer needed) -> TMA store
+    {
+      uint32_t r[32];
+      TMEM_LD32(trow + 128 + hf * 32, r);
+      tmem_wait_ld();
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        uint4 w;
+        w.x = pack_bf2(__uint_as_float(r[g * 8 + 0]), __uint_as_float(r[g * 8 + 1]));
+        w.y = pack_bf2(__uint_as_float(r[g * 8 + 2]), __uint_as_float(r[g * 8 + 3]));
+        w.z = pack_bf2(__uint_as_float(r[g * 8 + 4]), __uint_as_float(r[g * 8 + 5]));
+        w.w = pack_bf2(__uint_as_float(r[g * 8 + 6]), __uint_as_float(r[g * 8 + 7]));
+        *reinterpret_cast<uint4*>(sQ + sw128(row, hf * 4 + g)) = w;
+      }
+    }
+    fence_proxy_async();
+    tc_fence_before();
+    __syncthreads();
+    if (tid == 0) {
+      tma_store_4d(&m_ctx, sQ, h * AT_D, 0, b, 0);
+      bulk_commit();
+    }
+    T(5);
   }
-  fence_proxy_async();
+  if (tid == 0) bulk_wait_all();
   tc_fence_before();
-  __syncthreads();
-  if (tid == 0) {
-    tma_store_4d(&m_ctx, sQ, h * AT_D, 0, b, 0);
-    bulk_commit();
-    bulk_wait_all();
-  }
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
@@ -245,25 +284,22 @@ __global__ void __launch_bounds__(AT_THREADS) k_attn_bwd(const __grid_constant__
                                                          const __grid_constant__ CUtensorMap m_dctx,
                                                          const __grid_constant__ CUtensorMap m_dqkv,
                                                          const AttnArgs a) {
+  // Persistent over heads like the forward: buffer set it&1 holds this head's
+  // inputs (Q, K, V, dO, P) while the next head's stream into the other set.
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ = sm;
-  uint8_t* sK = sm + AT_TILE;
-  uint8_t* sV = sm + 2 * AT_TILE;
-  uint8_t* sO = sm + 3 * AT_TILE;   // dO
-  uint8_t* sP = sm + 4 * AT_TILE;   // 2 tiles: P, then Pd in place
-  uint8_t* sS = sm + 6 * AT_TILE;   // 2 tiles: dS
-  float* red = reinterpret_cast<float*>(sm + 8 * AT_TILE);  // [2 halves][128 rows]
-  uint64_t* bar = reinterpret_cast<uint64_t*>(red + 256);   // load, mma1, mma2
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 3);
+  uint8_t* sIn = sm;                         // 2 x [Q, K, V, dO, P(2 tiles)]
+  uint8_t* sS = sm + 12 * AT_TILE;           // 2 tiles: dS
+  float* red = reinterpret_cast<float*>(sm + 14 * AT_TILE);  // [2 halves][128 rows]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(red + 256);   // load[2], mma1, mma2
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 4);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int z = blockIdx.x, b = z / a.A, h = z % a.A;
   const int q = warp & 3, hf = warp >> 2;
   const int row = q * 32 + lane;
   const int j0 = hf * 64;
   if (tid == 0) {
-    for (int i = 0; i < 3; ++i) mbar_init(&bar[i], 1);
+    for (int i = 0; i < 4; ++i) mbar_init(&bar[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) tmem_alloc1<256>(tslot);
@@ -274,15 +310,34 @@ __global__ void __launch_bounds__(AT_THREADS) k_attn_bwd(const __grid_constant__
   pdl_wait();
   pdl_trigger();
 
+  auto issue_load = [&](int zz, int buf) {
+    const int bb = zz / a.A, hh = zz % a.A;
+    uint8_t* d = sIn + buf * 6 * AT_TILE;
+    mbar_expect_tx(&bar[buf], 6 * AT_TILE);
+    tma_load_3(d, &m_qkv, &bar[buf], hh * AT_D, 0, bb);
+    tma_load_3(d + AT_TILE, &m_qkv, &bar[buf], a.H + hh * AT_D, 0, bb);
+    tma_load_3(d + 2 * AT_TILE, &m_qkv, &bar[buf], 2 * a.H + hh * AT_D, 0, bb);
+    tma_load_3(d + 3 * AT_TILE, &m_dctx, &bar[buf], hh * AT_D, 0, bb);
+    tma_load_3(d + 4 * AT_TILE, &m_probs, &bar[buf], 0, 0, zz);
+    tma_load_3(d + 5 * AT_TILE, &m_probs, &bar[buf], 64, 0, zz);
+  };
+  if (tid == 0 && int(blockIdx.x) < a.Z) issue_load(blockIdx.x, 0);
+  int it = 0;
+  for (int z = blockIdx.x; z < a.Z; z += gridDim.x, ++it) {
+  const int buf = it & 1;
+  const int b = z / a.A, h = z % a.A;
+  uint8_t* sQ = sIn + buf * 6 * AT_TILE;
+  uint8_t* sK = sQ + AT_TILE;
+  uint8_t* sV = sQ + 2 * AT_TILE;
+  uint8_t* sO = sQ + 3 * AT_TILE;   // dO
+  uint8_t* sP = sQ + 4 * AT_TILE;   // 2 tiles: P, then Pd in place
   if (tid == 0) {
-    mbar_expect_tx(&bar[0], 6 * AT_TILE);
-    tma_load_3(sQ, &m_qkv, &bar[0], h * AT_D, 0, b);
-    tma_load_3(sK, &m_qkv, &bar[0], a.H + h * AT_D, 0, b);
-    tma_load_3(sV, &m_qkv, &bar[0], 2 * a.H + h * AT_D, 0, b);
-    tma_load_3(sO, &m_dctx, &bar[0], h * AT_D, 0, b);
-    tma_load_3(sP, &m_probs, &bar[0], 0, 0, z);
-    tma_load_3(sP + AT_TILE, &m_probs, &bar[0], 64, 0, z);
-    mbar_wait(&bar[0], 0);
+    const int zn = z + int(gridDim.x);
+    if (zn < a.Z) {
+      bulk_wait_read<0>();  // head it-1's output stores have read the other set
+      issue_load(zn, buf ^ 1);
+    }
+    mbar_wait(&bar[buf], (it >> 1) & 1);
     tc_fence_after();
     // dPd = dO V^T  (A = dO K-major, B = V K-major: [key][dh])
     constexpr uint32_t id1 = umma_idesc(128, 128, true, false, false);
@@ -290,12 +345,12 @@ __global__ void __launch_bounds__(AT_THREADS) k_attn_bwd(const __grid_constant__
     for (int k = 0; k < 4; ++k)
       tc_mma<1>(tm, umma_desc(smem_u32(sO) + k * 32, 16, 1024), umma_desc(smem_u32(sV) + k * 32, 16, 1024), id1,
                 k ? 1u : 0u);
-    tc_commit<1>(&bar[1]);
+    tc_commit<1>(&bar[2]);
   }
   uint32_t kb[2];
   keep_bits64(a.d, (uint64_t(z) * a.S + row) * a.S, j0, a.S, kb);
   const float sd = a.d.p > 0.0f ? a.d.scale : 1.0f;
-  mbar_wait(&bar[1], 0);
+  mbar_wait(&bar[2], it & 1);
   tc_fence_after();
 
   const uint32_t trow = tm + (uint32_t(q * 32) << 16) + j0;
@@ -373,9 +428,9 @@ __global__ void __launch_bounds__(AT_THREADS) k_attn_bwd(const __grid_constant__
     for (int k = 0; k < 8; ++k)  // dK = dS^T Q -> cols 64..127
       tc_mma<1>(tm + 64, umma_desc(smem_u32(sS) + k * 2048, AT_TILE, 1024),
                 umma_desc(smem_u32(sQ) + k * 2048, AT_TILE, 1024), id_mm, k ? 1u : 0u);
-    tc_commit<1>(&bar[2]);
+    tc_commit<1>(&bar[3]);
   }
-  mbar_wait(&bar[2], 0);
+  mbar_wait(&bar[3], it & 1);
   tc_fence_after();
   // dQ (query row), dK, dV (key row = TMEM lane): this thread's 32 head-dim
   // columns of each -> bf16 staging in sQ / sK / sV
@@ -405,8 +460,12 @@ __global__ void __launch_bounds__(AT_THREADS) k_attn_bwd(const __grid_constant__
     tma_store_4d(&m_dqkv, sK, a.H + h * AT_D, 0, b, 0);
     tma_store_4d(&m_dqkv, sV, 2 * a.H + h * AT_D, 0, b, 0);
     bulk_commit();
-    bulk_wait_all();
   }
+  tc_fence_before();
+  __syncthreads();
+  }
+  if (tid == 0) bulk_wait_all();
+  tc_fence_before();
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
@@ -415,8 +474,8 @@ __global__ void __launch_bounds__(AT_THREADS) k_attn_bwd(const __grid_constant__
 }
 
 // ------------------------------------------------------------------ host
-constexpr int AT_FWD_SMEM = 1024 + 5 * AT_TILE + 2048 + 64;
-constexpr int AT_BWD_SMEM = 1024 + 8 * AT_TILE + 1024 + 64;
+constexpr int AT_FWD_SMEM = 1024 + 10 * AT_TILE + 2048 + 64;
+constexpr int AT_BWD_SMEM = 1024 + 14 * AT_TILE + 1024 + 64;
 
 bool attn_fused_ok(int dt, int64_t S, int64_t H, int64_t A, bool exact) {
   return !exact && dt == TCB_BF16 && A > 0 && H % A == 0 && H / A == AT_D && S >= 8 && S <= AT_S && S % 8 == 0;
@@ -428,7 +487,7 @@ static CUtensorMap seq_map(const void* p, int64_t cols, int64_t S, int64_t B) {
 }
 
 void launch_attn_fwd(const void* qkv, void* ctx, void* probs, int64_t B, int64_t S, int64_t H, int64_t A, float scale,
-                     int causal, const DropCfg& d, cudaStream_t s) {
+                     int causal, const DropCfg& d, cudaStream_t s, void* trace) {
   static std::once_flag once;
   std::call_once(once, [] {
     TCB_CUDA(cudaFuncSetAttribute(k_attn_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, AT_FWD_SMEM));
@@ -437,8 +496,9 @@ void launch_attn_fwd(const void* qkv, void* ctx, void* probs, int64_t B, int64_t
   const CUtensorMap mc = seq_map(ctx, H, S, B);
   const CUtensorMap mp = encode4(probs, TCB_BF16, S, S, B * A, 1, S, S * S, S * S * B * A, 64, 128,
                                  CU_TENSOR_MAP_SWIZZLE_128B);
-  AttnArgs a{int(S), int(H), int(A), int(H / A), causal, scale, d};
-  launch_k(k_attn_fwd, unsigned(B * A), AT_THREADS, AT_FWD_SMEM, s, mq, mp, mc, a);
+  AttnArgs a{int(S), int(H), int(A), int(H / A), causal, int(B * A), static_cast<unsigned long long*>(trace), scale, d};
+  const int grid = int(B * A < kNumSMs ? B * A : kNumSMs);
+  launch_k(k_attn_fwd, unsigned(grid), AT_THREADS, AT_FWD_SMEM, s, mq, mp, mc, a);
   TCB_CUDA(cudaGetLastError());
 }
 
@@ -453,8 +513,9 @@ void launch_attn_bwd(const void* qkv, const void* probs, const void* dctx, void*
   const CUtensorMap md = seq_map(dqkv, 3 * H, S, B);
   const CUtensorMap mp = encode4(probs, TCB_BF16, S, S, B * A, 1, S, S * S, S * S * B * A, 64, 128,
                                  CU_TENSOR_MAP_SWIZZLE_128B);
-  AttnArgs a{int(S), int(H), int(A), int(H / A), causal, scale, d};
-  launch_k(k_attn_bwd, unsigned(B * A), AT_THREADS, AT_BWD_SMEM, s, mq, mp, mo, md, a);
+  AttnArgs a{int(S), int(H), int(A), int(H / A), causal, int(B * A), nullptr, scale, d};
+  const int grid = int(B * A < kNumSMs ? B * A : kNumSMs);
+  launch_k(k_attn_bwd, unsigned(grid), AT_THREADS, AT_BWD_SMEM, s, mq, mp, mo, md, a);
   TCB_CUDA(cudaGetLastError());
 }
 

@@ -1050,8 +1050,9 @@ static void b_attention(Plan& p) {
   require(p.out[0].numel() == g.B * g.S * g.H, "attention: ctx must be [T, H]");
   require(p.out[1].numel() == g.Z * g.S * g.S, "attention: probs must be [B*A*S, S]");
   if (attn_fused_ok(g.dt, g.S, g.H, g.A, g.exact) && !p.attrs.i("unfused", 0)) {
+    void* trace = reinterpret_cast<void*>(p.attrs.i("tc_trace", 0));  // tooling only
     p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
-      launch_attn_fwd(in[0].ptr, out[0].ptr, out[1].ptr, g.B, g.S, g.H, g.A, g.scale, g.causal, g.d, s);
+      launch_attn_fwd(in[0].ptr, out[0].ptr, out[1].ptr, g.B, g.S, g.H, g.A, g.scale, g.causal, g.d, s, trace);
     };
     return;
   }

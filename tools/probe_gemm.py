@@ -193,6 +193,16 @@ def attention(iters, p=0.1):
     f = Plan("attention", [((T, 3 * H), BF16)], [((T, H), BF16), ((B * A * S, S), BF16)], at)
     b = Plan("attention_dx", [((T, 3 * H), BF16), ((B * A * S, S), BF16), ((T, H), BF16)], [((T, 3 * H), BF16)], at)
     uf = time_plan(f, [qkv.data_ptr()], [ctx.data_ptr(), probs.data_ptr()], iters)
+    tr = torch.zeros(148 * 8, dtype=torch.int64, device="cuda")
+    ft = Plan("attention", [((T, 3 * H), BF16)], [((T, H), BF16), ((B * A * S, S), BF16)], {**at, "tc_trace": tr.data_ptr()})
+    ft.launch([qkv.data_ptr()], [ctx.data_ptr(), probs.data_ptr()], torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    import numpy as np
+    t = tr.view(148, 8).cpu().numpy().astype("float64")
+    t = t[t[:, 0] > 0]
+    d = np.diff(t[:, :6], axis=1) / 1000.0
+    print(json.dumps({"attn_fwd_phase_us(head 2): load_wait, qk_mma, softmax, store+pd+pv, epilogue":
+                      [round(float(np.median(d[:, k])), 2) for k in range(5)]}), flush=True)
     ub = time_plan(b, [qkv.data_ptr(), probs.data_ptr(), ctx.data_ptr()], [dq.data_ptr()], iters)
     fl = 4.0 * B * A * S * S * 64
     return [{"name": "attention_fwd", "us": round(uf, 2), "tflops": round(fl / uf / 1e6, 1)},
