@@ -868,12 +868,17 @@ int orc_exec(const char* op, const orc_tensor* in, int nin, orc_tensor* out, int
     for (int64_t i = 0; i < n; ++i) F(&out[0])[i] = rnd(out[0].dtype, v);
     return 0;
   }
-  if (!strcmp(op, "colsum")) { /* bias gradient: f32 column sums over all leading dims, rows ascending */
+  if (!strcmp(op, "colsum")) { /* bias gradient: f32 column sums over all leading dims, rows ascending;
+                                  with labels, rows labelled ignore_index are skipped */
     NEED(1, 1);
     int64_t C = in[0].shape[in[0].rank - 1], R = numel(&in[0]) / C;
+    const int32_t* lab = nin > 1 ? (const int32_t*)in[1].ptr : NULL;
+    const int64_t ign = aint(A, na, "ignore_index", -100);
     for (int64_t j = 0; j < C; ++j) F(&out[0])[j] = 0.0f;
-    for (int64_t r = 0; r < R; ++r)
+    for (int64_t r = 0; r < R; ++r) {
+      if (lab && lab[r] == ign) continue;
       for (int64_t j = 0; j < C; ++j) F(&out[0])[j] += F(&in[0])[r * C + j];
+    }
     return 0;
   }
   if (!strcmp(op, "mse")) { /* backends.hpp:205-214: sequential acc, then a divide */

@@ -181,7 +181,8 @@ constexpr int CS_ROWS = 32;  // rows per block: 4 per warp, all loads in flight 
 
 template <typename T>
 __global__ void __launch_bounds__(256) k_colsum_partial(const T* __restrict__ x, float* __restrict__ part,
-                                                        int64_t R, int64_t C) {
+                                                        int64_t R, int64_t C, const int32_t* __restrict__ lab,
+                                                        int32_t ign) {
   TCB_PDL_ENTRY();
   __shared__ float red[8][256 + 4];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -198,7 +199,9 @@ __global__ void __launch_bounds__(256) k_colsum_partial(const T* __restrict__ x,
 #pragma unroll
       for (int i = 0; i < RPW; ++i) {
         const int64_t r = r0 + warp + 8 * i;
-        q[i] = r < r1 ? *reinterpret_cast<const uint4*>(x + r * C + c0) : make_uint4(0, 0, 0, 0);
+        // rows labelled ignore_index are skipped (exact zeros of a CE gradient)
+        q[i] = (r < r1 && !(lab && lab[r] == ign)) ? *reinterpret_cast<const uint4*>(x + r * C + c0)
+                                                   : make_uint4(0, 0, 0, 0);
       }
 #pragma unroll
       for (int i = 0; i < RPW; ++i) {
@@ -208,6 +211,7 @@ __global__ void __launch_bounds__(256) k_colsum_partial(const T* __restrict__ x,
       }
     } else {
       for (int64_t r = r0 + warp; r < r1; r += 8) {
+        if (lab && lab[r] == ign) continue;
         float4 a = *reinterpret_cast<const float4*>(x + r * C + c0);
         float4 b = *reinterpret_cast<const float4*>(x + r * C + c0 + 4);
         acc[0] += a.x; acc[1] += a.y; acc[2] += a.z; acc[3] += a.w;
@@ -252,8 +256,14 @@ __global__ void __launch_bounds__(1024) k_colsum_final(const float* __restrict__
 
 // colsum: f32 column sums over all leading dims (bias gradients of [T, N]
 // GEMM outputs); exact row order for f32 input, split-row tree otherwise.
+// With a labels input, rows labelled ignore_index are not read on the split-row
+// path (they are exact zeros of the CE gradient); the other paths add those
+// zeros, which leaves every sum unchanged.
 static void b_colsum(Plan& p) {
-  check_arity(p, 1, 1, 1, 1);
+  check_arity(p, 1, 2, 1, 1);
+  const bool masked = p.in.size() > 1;
+  if (masked) require(p.in[1].dtype == TCB_I32, "colsum: labels must be i32");
+  const int32_t ign = int32_t(p.attrs.i("ignore_index", -100));
   const Spec& X = p.in[0];
   require(is_float(X.dtype), "colsum: float input");
   require(p.out[0].dtype == TCB_F32, "colsum: output is f32");
@@ -280,7 +290,8 @@ static void b_colsum(Plan& p) {
       p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
         if (reinterpret_cast<uintptr_t>(in[0].ptr) % 16) fail(TCB_ERR_ARG, "colsum: input not 16-byte aligned");
         dim3 grid(unsigned((C + 255) / 256), unsigned(nchunk));
-        launch_k(k_colsum_partial<T>, grid, 256, 0, s, (const T*)in[0].ptr, (float*)ws->p, R, C);
+        launch_k(k_colsum_partial<T>, grid, 256, 0, s, (const T*)in[0].ptr, (float*)ws->p, R, C,
+                 masked ? (const int32_t*)in[1].ptr : nullptr, ign);
         launch_k(k_colsum_final, unsigned((C + 31) / 32), 1024, 0, s, (const float*)ws->p, (float*)out[0].ptr, nchunk, C,
                                                                   1.0f);
       };

@@ -1341,9 +1341,16 @@ __global__ void __launch_bounds__(512) k_ce_row(const T* __restrict__ x, const i
   const T* xr = x + t * Vp;
   T* dr = dx ? dx + t * Vp : nullptr;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  if (lab == ign) {
-    if (dr)
-      for (int64_t j = threadIdx.x; j < Vp; j += blockDim.x) dr[j] = from_f<T>(0.0f);
+  if (lab == ign) {  // no loss, zero gradient row (16-byte stores when aligned)
+    if (dr) {
+      if (vec) {
+        constexpr int EPV = 16 / sizeof(T);  // elements per 16-byte store
+        for (int64_t c = threadIdx.x; c < Vp / EPV; c += blockDim.x)
+          reinterpret_cast<uint4*>(dr)[c] = make_uint4(0, 0, 0, 0);
+      } else {
+        for (int64_t j = threadIdx.x; j < Vp; j += blockDim.x) dr[j] = from_f<T>(0.0f);
+      }
+    }
     if (threadIdx.x == 0) row_loss[t] = 0.0f;
     return;
   }

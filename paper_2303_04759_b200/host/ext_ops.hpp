@@ -284,8 +284,16 @@ inline void register_extension_ops(OpRegistry& r) {
     return TensorType{dtype_from(ir::attr_string(a, "dtype", "f32")), opreg::parse_shape_attr(ir::attr_string(a, "shape"))};
   });
   // f32 column sums over all leading dims (bias gradients)
-  reg("colsum", 1, R, [](const V& in, const AttrMap&) -> Type {
+  // colsum(x [, labels]) {ignore_index}: f32 column sums over all leading dims;
+  // with labels, rows whose label is ignore_index are skipped (they are exact
+  // zeros in the cross-entropy gradient this feeds the decoder bias from)
+  reg("colsum", -1, R, [](const V& in, const AttrMap&) -> Type {
+    if (in.size() != 1 && in.size() != 2) throw TypeError("colsum: (x [, labels])");
     auto x = rel::T(in[0], "colsum");
+    if (in.size() == 2) {
+      auto l = rel::T(in[1], "colsum");
+      if (l.dtype != kI32 || numel(l) * x.shape.back() != numel(x)) throw TypeError("colsum: labels i32 [rows]");
+    }
     return TensorType{kF32, {x.shape.back()}};
   });
 }

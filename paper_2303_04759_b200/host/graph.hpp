@@ -395,7 +395,7 @@ inline UseInfo count_uses(const LetSeq& s) {
 }
 
 struct FusionStats {
-  int dact = 0, ln_dy2 = 0, emb_base = 0, ln_bias = 0, pairs = 0, dead = 0;
+  int dact = 0, ln_dy2 = 0, emb_base = 0, ln_bias = 0, pairs = 0, ce_mask = 0, dead = 0;
 };
 
 /// Horizontal fusion (SPEC.md:533-540 applied to GEMMs): a weight-gradient
@@ -576,6 +576,27 @@ inline FusionStats fuse(LetSeq& s, bool patterns = true) {
             ++st.ln_bias;
             continue;
           }
+        }
+      }
+    }
+    // 5. colsum(get(cross_entropy(logits, labels), 1)) -> colsum(dlogits, labels):
+    //    rows with label == ignore_index are exact zeros of dlogits, skip them
+    if (op == "colsum" && b.value->args.size() == 1) {
+      auto src = arg_var(b.value, 0);
+      auto it = src ? def.find(src.get()) : def.end();
+      if (it != def.end() && s.lets[it->second].value->kind == ExprKind::TupleGet &&
+          s.lets[it->second].value->index == 1) {
+        auto& gl = s.lets[it->second];
+        auto tv = gl.value->args[0]->kind == ExprKind::VarRef ? gl.value->args[0]->var : nullptr;
+        auto* cp = producer(tv);
+        if (cp && cp->value->op == "cross_entropy" && cp->value->args.size() == 2) {
+          AttrMap at = b.value->call_attrs;
+          at["ignore_index"] = ir::attr_int(cp->value->call_attrs, "ignore_index", -100);
+          auto call = ir::call("colsum", {b.value->args[0], cp->value->args[1]}, at);
+          call->ty = b.value->ty;
+          b.value = call;
+          ++st.ce_mask;
+          continue;
         }
       }
     }
