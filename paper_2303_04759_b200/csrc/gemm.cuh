@@ -41,6 +41,8 @@ struct GemmArgs {
   int force_splits = 0;            // split-K ways (cluster of CG x splits CTAs, DSMEM reduction)
   void* trace = nullptr;           // optional per-CTA timeline buffer (12 x u64 per CTA, tooling)
   int no_tma_epi = 0;              // force the direct-store epilogue (tooling)
+  const int* sched = nullptr;      // device LPT schedule of a pair launch (gemm_pair_schedule)
+  int sched_rounds = 0;
 };
 
 struct TcChoice {
@@ -56,6 +58,8 @@ bool gemm_tc_supported(const GemmArgs& g, std::string* why);
 void launch_gemm_tc(const GemmArgs& g, cudaStream_t s);
 // two independent problems in one persistent launch (same tile shape)
 void launch_gemm_tc_pair(const GemmArgs& g0, const GemmArgs& g1, cudaStream_t s);
+// host-side longest-processing-time unit schedule for a pair launch
+std::vector<int> gemm_pair_schedule(const GemmArgs& g0, const GemmArgs& g1, int* rounds);
 // cost-model choice of tile shape / CTA pairing / split-K for a problem
 TcChoice gemm_tc_choose(const GemmArgs& g);
 // plan-time: freeze the tile choice and allocate split-K scratch (no-op for the

@@ -150,7 +150,16 @@ static void b_matmul_pair(Plan& p) {
   g0.force_cg = g1.force_cg = int(p.attrs.i("tc_cg", 0));
   const bool exact = want_exact(p) || p.in[n0].dtype != TCB_BF16;
   p.nkernels = exact ? 2 : 1;
-  p.run = [g0, g1, exact, n0](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) mutable {
+  std::shared_ptr<Scratch> sched;
+  if (!exact && !p.attrs.i("static_rr", 0)) {
+    int rounds = 0;
+    std::vector<int> table = gemm_pair_schedule(g0, g1, &rounds);
+    sched = std::make_shared<Scratch>(table.size() * sizeof(int));
+    TCB_CUDA(cudaMemcpy(sched->p, table.data(), table.size() * sizeof(int), cudaMemcpyHostToDevice));
+    g0.sched = static_cast<const int*>(sched->p);
+    g0.sched_rounds = rounds;
+  }
+  p.run = [g0, g1, exact, n0, sched](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) mutable {
     g0.a.ptr = in[0].ptr;
     g0.b.ptr = in[1].ptr;
     if (n0 == 3) g0.aux = in[2].ptr;

@@ -89,8 +89,18 @@ struct TcParams {
   // exchanged through distributed shared memory and reduced in split order
   int splits;
   int64_t num_units;
+  // optional static schedule: cluster c runs units sched[c], sched[c + n_cl],
+  // ... up to the first -1 (longest-processing-time balanced on the host);
+  // without it cluster c runs units c, c + n_cl, ...
+  const int* sched;
+  int sched_rounds;
   unsigned long long* trace;  // optional per-CTA timeline (tools/probe_gemm.py --trace)
 };
+__device__ __forceinline__ int64_t unit_at(const TcParams& P, int64_t cl, int64_t ncl, int64_t i) {
+  if (P.sched) return i < P.sched_rounds ? int64_t(__ldg(P.sched + i * ncl + cl)) : -1;
+  const int64_t u = cl + i * ncl;
+  return u < P.num_units ? u : -1;
+}
 __device__ __forceinline__ int unit_prob(const TcParams& P, int64_t u) {
   return (P.nprob > 1 && u >= P.pr[0].num_tiles) ? 1 : 0;
 }
@@ -317,7 +327,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int64_t u = cl_id; u < P.num_units; u += n_cl) {
+      for (int64_t ui = 0, u; (u = unit_at(P, cl_id, n_cl, ui)) >= 0; ++ui) {
         const int prob = unit_prob(P, u);
         const TcProb& Q = P.pr[prob];
         const CUtensorMap* mA = prob ? &tmA1 : &tmA0;
@@ -365,7 +375,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int64_t u = cl_id; u < P.num_units; u += n_cl) {
+      for (int64_t ui = 0, u; (u = unit_at(P, cl_id, n_cl, ui)) >= 0; ++ui) {
         const TcProb& Q = P.pr[unit_prob(P, u)];
         const int kb0 = split * Q.kps;
         const int kb1 = min(kb0 + Q.kps, Q.k_blocks);
@@ -375,7 +385,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          if (tr && u == cl_id && kb == kb0) tr[2] = gtimer();
+          if (tr && ui == 0 && kb == kb0) tr[2] = gtimer();
           const uint32_t a_addr = smem_u32(sA + stage * C::A_BYTES);
           const uint32_t b_addr = smem_u32(sB + stage * C::B_BYTES);
 #pragma unroll
@@ -421,16 +431,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     uint32_t sidx = 0;    // output slot ring
     uint32_t achunk = 0;  // aux chunk counter: ring slot achunk % RING, phase (achunk / RING) & 1
     // aux prefetch cursor over the same (tile, chunk) order as the consumer
-    int64_t pt = cl_id;
+    int64_t pi = 0;  // iteration index of the next aux box's unit
     int pc = sub;
     uint32_t aissue = 0;
     auto issue_next_aux = [&]() {
-      while (pt < P.num_units) {
+      for (int64_t pt; (pt = unit_at(P, cl_id, n_cl, pi)) >= 0;) {
         const int prob = unit_prob(P, pt);
         const TcProb& Q = P.pr[prob];
         if (!(Q.tma_epi && Q.dact != ACT_NONE)) {  // this problem has no act'(aux): skip its units
           pc = sub;
-          pt += n_cl;
+          ++pi;
           continue;
         }
         int z, mb, nb;
@@ -440,7 +450,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         pc += SPLIT;
         if (pc >= NCH) {
           pc = sub;
-          pt += n_cl;
+          ++pi;
         }
         if (n0 >= Q.N) continue;  // chunk skipped by the consumer too
         if (lane == 0) {
@@ -460,7 +470,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     if (AUX)
       for (int k = 0; k < TC_AUX_RING - 1; ++k) issue_next_aux();
 
-    for (int64_t u = cl_id; u < P.num_units; u += n_cl) {
+    for (int64_t ui = 0, u; (u = unit_at(P, cl_id, n_cl, ui)) >= 0; ++ui) {
       const int prob = unit_prob(P, u);
       const TcProb& Q = P.pr[prob];
       const EpiMaps& EM = prob ? EM1 : EM0;
@@ -541,7 +551,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       if (Q.bias) load_bias();
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      if (tr && ew == 0 && u == cl_id) tr[4] = gtimer();
+      if (tr && ew == 0 && ui == 0) tr[4] = gtimer();
       if (P.splits > 1) {
         // ---- split-K: partial accumulators -> owners through DSMEM.  Chunk c
         // of the tile belongs to split c % S of the same pair rank; an owner's
@@ -603,7 +613,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         for (int j = 0; j < W; ++j) v[j] = __uint_as_float(r[j]);
         finish(v, ci, n0);
       }
-      if (tr && ew == 0 && lane == 0 && u == cl_id) tr[6] = gtimer();
+      if (tr && ew == 0 && lane == 0 && ui == 0) tr[6] = gtimer();
       // release the accumulator to the (leader's) MMA warp
       tc_fence_before();
       __syncwarp();
@@ -611,7 +621,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         if constexpr (CG == 2) mbar_arrive_cluster(tempty_addr0 + acc * 8);
         else mbar_arrive(&tempty[acc]);
       }
-      if (tr && ew == 0 && lane == 0 && u == cl_id) tr[7] = gtimer();
+      if (tr && ew == 0 && lane == 0 && ui == 0) tr[7] = gtimer();
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
@@ -750,6 +760,8 @@ static void launch_cfg(const GemmArgs* gs, int n, cudaStream_t s) {
     em[1] = em[0];
   }
   P.num_units = P.pr[0].num_tiles + (n > 1 ? P.pr[1].num_tiles : 0);
+  P.sched = gs[0].sched;
+  P.sched_rounds = gs[0].sched_rounds;
   const int csz = CG * P.splits;  // cluster: CTA pair x K splits
   int grid;
   if (P.splits > 1) {
@@ -872,16 +884,62 @@ void launch_gemm_tc(const GemmArgs& g, cudaStream_t s) {
 }
 
 // Two independent problems in one grid (same tile shape, no split-K); the
-// problem with more k-blocks per tile goes first so its long tiles start early.
+// problem with more k-blocks per tile goes first.
+static TcChoice pair_choice(const GemmArgs& g0, const GemmArgs& g1) {
+  TcChoice c{g0.force_bn ? g0.force_bn : 256, g0.force_cg ? g0.force_cg : 2, 1};
+  if (c.cg == 2 && (g0.M <= 128 || g1.M <= 128)) c.cg = 1;
+  return c;
+}
 void launch_gemm_tc_pair(const GemmArgs& g0, const GemmArgs& g1, cudaStream_t s) {
   std::string why;
   for (const GemmArgs* g : {&g0, &g1})
     if (!gemm_tc_supported(*g, &why)) fail(TCB_ERR_UNIMPLEMENTED, "tcgen05 gemm pair: " + why);
-  TcChoice c{g0.force_bn ? g0.force_bn : 256, g0.force_cg ? g0.force_cg : 2, 1};
-  if (c.cg == 2 && (g0.M <= 128 || g1.M <= 128)) c.cg = 1;
+  const TcChoice c = pair_choice(g0, g1);
   const bool swap = g1.K > g0.K;
   GemmArgs gs[2] = {swap ? g1 : g0, swap ? g0 : g1};
+  gs[0].sched = g0.sched;
+  gs[0].sched_rounds = g0.sched_rounds;
   dispatch_tc(gs, 2, c, s);
+}
+
+// Longest-processing-time schedule for a pair launch: unit cost = its k-blocks
+// plus an epilogue weight (GELU / act' epilogues cost more), every unit goes to
+// the least-loaded cluster, largest first.  Returns the [rounds][clusters]
+// table (-1 = done) the kernel walks; deterministic (ties by index).
+std::vector<int> gemm_pair_schedule(const GemmArgs& g0, const GemmArgs& g1, int* rounds) {
+  const TcChoice c = pair_choice(g0, g1);
+  const bool swap = g1.K > g0.K;
+  const GemmArgs* gs[2] = {swap ? &g1 : &g0, swap ? &g0 : &g1};
+  std::vector<std::pair<double, int>> units;
+  int64_t base = 0;
+  for (const GemmArgs* g : gs) {
+    const int64_t tiles = ((g->M + 128 * c.cg - 1) / (128 * c.cg)) * ((g->N + c.bn - 1) / c.bn) * g->Z;
+    const double kb = double((g->K + TC_BK - 1) / TC_BK);
+    const double epi = (g->dact != ACT_NONE || g->act == ACT_GELU) ? 6.0 : 2.0;
+    for (int64_t t = 0; t < tiles; ++t) units.push_back({kb + epi, int(base + t)});
+    base += tiles;
+  }
+  const int64_t total = int64_t(units.size()) * c.cg;
+  int grid = int(total < kNumSMs ? total : kNumSMs);
+  grid = (grid / c.cg) * c.cg;
+  const int ncl = grid / c.cg;
+  std::stable_sort(units.begin(), units.end(), [](auto& a, auto& b) { return a.first > b.first; });
+  std::vector<double> load(ncl, 0.0);
+  std::vector<std::vector<int>> lists(ncl);
+  for (auto& [cost, u] : units) {
+    int best = 0;
+    for (int k = 1; k < ncl; ++k)
+      if (load[k] < load[best]) best = k;
+    load[best] += cost;
+    lists[best].push_back(u);
+  }
+  int r = 0;
+  for (auto& l : lists) r = std::max(r, int(l.size()));
+  std::vector<int> table(size_t(r) * ncl, -1);
+  for (int k = 0; k < ncl; ++k)
+    for (size_t i = 0; i < lists[k].size(); ++i) table[i * ncl + k] = lists[k][i];
+  *rounds = r;
+  return table;
 }
 
 }  // namespace tcb

@@ -117,6 +117,38 @@ def trace(iters):
                           "epi_done": q(5), "atomic": q(8), "red_start": q(9), "red_end": q(10)}), flush=True)
 
 
+def pairs(iters):
+    """BERT-base backward GEMM pairs (dgrad [+act'] and wgrad sharing dY): one
+    grouped launch vs the two separate launches."""
+    T = 4096
+    cases = [("qkv", 768, 2304, 0), ("proj", 768, 768, 0), ("ffn1", 768, 3072, 0), ("ffn2_dact", 3072, 768, 1)]
+    for name, Hin, Hout, dact in cases:
+        # linear y = x W (x [T, Hin], W [Hin, Hout]); dY [T, Hout]
+        x = torch.randn(T, Hin, device="cuda").to(torch.bfloat16)
+        w = (0.02 * torch.randn(Hin, Hout, device="cuda")).to(torch.bfloat16)
+        dy = torch.randn(T, Hout, device="cuda").to(torch.bfloat16)
+        u = torch.randn(T, Hin, device="cuda").to(torch.bfloat16)
+        dx = torch.empty(T, Hin, device="cuda", dtype=torch.bfloat16)
+        dw = torch.empty(Hin, Hout, device="cuda")
+        ins0 = [((T, Hout), BF16), ((Hin, Hout), BF16)] + ([((T, Hin), BF16)] if dact else [])
+        p0 = Plan("matmul_dact" if dact else "matmul_t", ins0, [((T, Hin), BF16)],
+                  {"tb": 1, **({"act": "gelu"} if dact else {})})
+        p1 = Plan("matmul_t", [((T, Hin), BF16), ((T, Hout), BF16)], [((Hin, Hout), F32)], {"ta": 1, "out": "f32"})
+        a0 = [dy.data_ptr(), w.data_ptr()] + ([u.data_ptr()] if dact else [])
+        t0 = time_plan(p0, a0, [dx.data_ptr()], iters)
+        t1 = time_plan(p1, [x.data_ptr(), dy.data_ptr()], [dw.data_ptr()], iters)
+        at = {"n0": 3 if dact else 2, "ta0": 0, "tb0": 1, "ta1": 1, "tb1": 0, "out1": "f32"}
+        if dact:
+            at["act0"] = "gelu"
+        pp = Plan("matmul_pair", ins0 + [((T, Hin), BF16), ((T, Hout), BF16)], [((T, Hin), BF16), ((Hin, Hout), F32)], at)
+        tp = time_plan(pp, a0 + [x.data_ptr(), dy.data_ptr()], [dx.data_ptr(), dw.data_ptr()], iters)
+        pr = Plan("matmul_pair", ins0 + [((T, Hin), BF16), ((T, Hout), BF16)], [((T, Hin), BF16), ((Hin, Hout), F32)],
+                  {**at, "static_rr": 1})
+        trr = time_plan(pr, a0 + [x.data_ptr(), dy.data_ptr()], [dx.data_ptr(), dw.data_ptr()], iters)
+        print(json.dumps({"name": name, "dgrad_us": round(t0, 2), "wgrad_us": round(t1, 2), "sum_us": round(t0 + t1, 2),
+                          "pair_lpt_us": round(tp, 2), "pair_round_robin_us": round(trr, 2)}), flush=True)
+
+
 def sweep_splits(iters):
     """Split-K ways on the weight-gradient shapes (few output tiles, K = T);
     the last line per shape is the cost model's own choice."""
@@ -218,7 +250,11 @@ def main():
     ap.add_argument("--sweep", action="store_true")
     ap.add_argument("--splits", action="store_true")
     ap.add_argument("--trace", action="store_true")
+    ap.add_argument("--pairs", action="store_true")
     args = ap.parse_args()
+    if args.pairs:
+        pairs(args.iters)
+        return
     if args.trace:
         trace(args.iters)
         return
