@@ -102,25 +102,29 @@ static void b_adam(Plan& p) {
             p.attrs.f("eps", 1e-8), p.attrs.f("grad_scale", 1.0)};
   const int64_t n = p.in[0].numel();
   const int hd = p.out.size() > 3 ? p.out[3].dtype : -1;
+  const bool small = p.attrs.i("co_resident", 0) != 0;
   if (hd >= 0) require(is_float(hd), "adam_update_ex: 4th output must be a float copy");
   p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
     for (int i = 0; i < 4; ++i)
       if (reinterpret_cast<uintptr_t>(in[i].ptr) % 16 || (i < 3 && reinterpret_cast<uintptr_t>(out[i].ptr) % 16))
         fail(TCB_ERR_ARG, "adam_update: buffers must be 16-byte aligned");
-    const int grid = grid_for((n + 3) / 4, 256, kNumSMs * 4);
+    // co_resident: small CTAs that fit beside a GEMM CTA's 61K registers, for
+    // optimizer chunks the VM overlaps with the backward on a side stream
+    const int bs = small ? 64 : 256;
+    const int grid = grid_for((n + 3) / 4, bs, kNumSMs * (small ? 8 : 4));
     if (hd == TCB_BF16)
-      launch_k(k_adam<__nv_bfloat16>, grid, 256, 0, s, 
+      launch_k(k_adam<__nv_bfloat16>, grid, bs, 0, s, 
           (const float*)in[0].ptr, (const float*)in[1].ptr, (const float*)in[2].ptr,
           (const float*)in[3].ptr, (const float*)in[4].ptr, (float*)out[0].ptr, (float*)out[1].ptr,
           (float*)out[2].ptr, (__nv_bfloat16*)out[3].ptr, n, c);
     else if (hd == TCB_F16)
-      launch_k(k_adam<__half>, grid, 256, 0, s, (const float*)in[0].ptr, (const float*)in[1].ptr,
+      launch_k(k_adam<__half>, grid, bs, 0, s, (const float*)in[0].ptr, (const float*)in[1].ptr,
                                           (const float*)in[2].ptr, (const float*)in[3].ptr,
                                           (const float*)in[4].ptr, (float*)out[0].ptr,
                                           (float*)out[1].ptr, (float*)out[2].ptr,
                                           (__half*)out[3].ptr, n, c);
     else
-      launch_k(k_adam<float>, grid, 256, 0, s, (const float*)in[0].ptr, (const float*)in[1].ptr,
+      launch_k(k_adam<float>, grid, bs, 0, s, (const float*)in[0].ptr, (const float*)in[1].ptr,
                                          (const float*)in[2].ptr, (const float*)in[3].ptr,
                                          (const float*)in[4].ptr, (float*)out[0].ptr,
                                          (float*)out[1].ptr, (float*)out[2].ptr,
