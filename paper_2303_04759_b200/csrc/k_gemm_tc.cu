@@ -37,6 +37,10 @@ constexpr int TC_EW = 16;                             // epilogue chunk width (c
 constexpr int TC_SLOT = 32 * TC_EW * 4;               // per-warp output slot: f32 box or (y, u) 16-bit boxes
 constexpr int TC_AUX_SLOT = 32 * TC_EW * 2;           // per-warp act'(aux) slot (16-bit)
 constexpr int TC_AUX_RING = 3;                        // aux boxes in flight per warp (2 chunks ahead)
+// output staging slots per warp: one (the operand ring gets the smem: +1 stage);
+// the act'(aux) kernels, epilogue-bound, keep two so stores overlap
+template <bool AUX>
+constexpr int out_ring() { return AUX ? 2 : 1; }
 
 template <int BN, int CG, bool AUX>
 struct TcCfg {
@@ -45,7 +49,7 @@ struct TcCfg {
   static constexpr int B_BYTES = B_ROWS * TC_BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int EPI_BYTES =
-      TC_EPI_WARPS * 2 * TC_SLOT + (AUX ? TC_EPI_WARPS * TC_AUX_RING * TC_AUX_SLOT : 0);
+      TC_EPI_WARPS * out_ring<AUX>() * TC_SLOT + (AUX ? TC_EPI_WARPS * TC_AUX_RING * TC_AUX_SLOT : 0);
   static constexpr int BIAS_BYTES = TC_EPI_WARPS * ((BN / TC_EW + TC_EPI_WARPS / 4 - 1) / (TC_EPI_WARPS / 4)) * TC_EW * 4;
   static constexpr int BAR_BYTES = 1024;
   static constexpr int BUDGET = 227 * 1024 - 1024 - BAR_BYTES - EPI_BYTES - BIAS_BYTES;
@@ -258,7 +262,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   uint8_t* sA = smem;
   uint8_t* sB = smem + C::STAGES * C::A_BYTES;
   uint8_t* sEpi = smem + C::STAGES * C::STAGE_BYTES;        // epilogue warps x 2 output slots
-  uint8_t* sAux = sEpi + TC_EPI_WARPS * 2 * TC_SLOT;       // epilogue warps x 2 aux slots (AUX)
+  constexpr int OUT_RING = out_ring<AUX>();
+  uint8_t* sAux = sEpi + TC_EPI_WARPS * OUT_RING * TC_SLOT;  // epilogue warps x aux ring (AUX)
   float* sBias = reinterpret_cast<float*>(sAux + (AUX ? TC_EPI_WARPS * TC_AUX_RING * TC_AUX_SLOT : 0));
   uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sBias) + C::BIAS_BYTES);
   uint64_t* full = bars;
@@ -382,21 +387,24 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + uint32_t(acc * BN);
+        // descriptors of stage 0; stage s and k-step k only move the start
+        // address field (bits 0-13, 16-byte units): + s * stage bytes / 16 and
+        // + k * (K-major: 32 B -> 2, MN-major: 16 k-rows x 128 B -> 128)
+        // LBO = 8 KB between 64-wide MN chunks, SBO = 1 KB between 8-row atoms.
+        const uint64_t a_desc0 = Q.ta ? umma_desc(smem_u32(sA), 8192, 1024) : umma_desc(smem_u32(sA), 16, 1024);
+        const uint64_t b_desc0 = Q.tb ? umma_desc(smem_u32(sB), 16, 1024) : umma_desc(smem_u32(sB), 8192, 1024);
+        const uint32_t a_step = Q.ta ? 128u : 2u, b_step = Q.tb ? 2u : 128u;
+        const uint32_t idesc = Q.idesc;
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           if (tr && ui == 0 && kb == kb0) tr[2] = gtimer();
-          const uint32_t a_addr = smem_u32(sA + stage * C::A_BYTES);
-          const uint32_t b_addr = smem_u32(sB + stage * C::B_BYTES);
+          const uint64_t ad0 = a_desc0 + uint64_t(stage * (C::A_BYTES >> 4));
+          const uint64_t bd0 = b_desc0 + uint64_t(stage * (C::B_BYTES >> 4));
 #pragma unroll
-          for (int k = 0; k < TC_BK / 16; ++k) {
-            // K-major: +32 B per 16-element k step inside the 128 B swizzle row;
-            // MN-major: +2048 B (16 k-rows of 128 B); LBO = 8 KB between 64-wide
-            // MN chunks, SBO = 1 KB between 8-row swizzle atoms.
-            const uint64_t ad = Q.ta ? umma_desc(a_addr + k * 2048, 8192, 1024) : umma_desc(a_addr + k * 32, 16, 1024);
-            const uint64_t bd = Q.tb ? umma_desc(b_addr + k * 32, 16, 1024) : umma_desc(b_addr + k * 2048, 8192, 1024);
-            tc_mma<CG>(tmem_d, ad, bd, Q.idesc, (kb > kb0 || k) ? 1u : 0u);
-          }
+          for (int k = 0; k < TC_BK / 16; ++k)
+            tc_mma<CG>(tmem_d, ad0 + uint64_t(k * a_step), bd0 + uint64_t(k * b_step), idesc,
+                       (kb > kb0 || k) ? 1u : 0u);
           tc_commit<CG>(&empty[stage], mcast);
           if (++stage == C::STAGES) {
             stage = 0;
@@ -421,7 +429,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const int ew = warp - 4;
     const int q = warp & 3;
     const int sub = ew >> 2;
-    uint8_t* slots = sEpi + ew * 2 * TC_SLOT;
+    uint8_t* slots = sEpi + ew * OUT_RING * TC_SLOT;
     uint8_t* aslots = sAux + ew * TC_AUX_RING * TC_AUX_SLOT;
     float* wbias = sBias + ew * CPW * W;
     uint64_t* ab = abar + TC_AUX_RING * ew;
@@ -511,7 +519,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             ++achunk;
           }
           uint8_t* slot = slots + sidx * TC_SLOT;
-          if (lane == 0) bulk_wait_read<1>();  // the store that last used this slot has read it
+          if (lane == 0) bulk_wait_read<OUT_RING - 1>();  // the store that last used this slot has read it
           __syncwarp();
           if (Q.aux_out) stage_row<W>(slot + TC_SLOT / 2, lane, Q.c_dtype, v);
           apply_act<W>(Q.act, v);
@@ -523,7 +531,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             if (Q.aux_out) tma_store_4d(&EM.u, slot + TC_SLOT / 2, int(n0), mrow0, z2, z1);
             bulk_commit();
           }
-          sidx ^= 1;
+          if (++sidx == OUT_RING) sidx = 0;
         } else if (m < Q.M) {
           const int nvalid = int(Q.N - n0 < W ? Q.N - n0 : W);
           const int64_t base = coff + m * Q.ldc + n0;
@@ -795,7 +803,7 @@ static void launch_cfg(const GemmArgs* gs, int n, cudaStream_t s) {
 static int stage_bytes(int bn, int cg) { return TC_BM * TC_BK * 2 + (bn / cg) * TC_BK * 2; }
 static int stages_of(int bn, int cg) {
   const int cpw = (bn / TC_EW + TC_EPI_WARPS / 4 - 1) / (TC_EPI_WARPS / 4);
-  const int budget = 227 * 1024 - 1024 - 512 - TC_EPI_WARPS * 2 * TC_SLOT - TC_EPI_WARPS * cpw * TC_EW * 4;
+  const int budget = 227 * 1024 - 1024 - 1024 - TC_EPI_WARPS * out_ring<false>() * TC_SLOT - TC_EPI_WARPS * cpw * TC_EW * 4;
   return std::min(8, budget / stage_bytes(bn, cg));
 }
 // split-K through DSMEM: pure matmul epilogue, cluster <= 8 CTAs, whole
