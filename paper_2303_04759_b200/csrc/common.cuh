@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <functional>
@@ -209,17 +210,21 @@ __device__ __forceinline__ void philox4x32_10(uint32_t c[4], uint32_t k0, uint32
 struct DropCfg {
   float p = 0.0f, scale = 1.0f;
   uint64_t seed = 0, salt = 0;
+  // keep iff the 16-bit draw h >= thr.  h * 2^-16 is exact in f32, so this is
+  // the oracle's float(h) * (1/65536) >= p exactly, with thr = ceil(p * 65536)
+  uint32_t thr = 0;
 };
 // 8 keep bits for indices (q*8 .. q*8+7): one Philox call, 16 bits per element
-// (identical to oracle.c orc_dropout_keep)
+// (identical to oracle.c orc_dropout_keep); integer compares: the high half of
+// word w is >= thr iff w >= thr << 16
 __device__ __forceinline__ uint32_t dropout_bits8q(const DropCfg& d, uint64_t q) {
   uint32_t c[4] = {uint32_t(q), uint32_t(d.salt), uint32_t(d.salt >> 32), 0u};
   philox4x32_10(c, uint32_t(d.seed), uint32_t(d.seed >> 32));
   uint32_t bits = 0;
 #pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const uint32_t h = (k & 1) ? (c[k >> 1] >> 16) : (c[k >> 1] & 0xFFFFu);
-    bits |= (float(h) * (1.0f / 65536.0f) >= d.p ? 1u : 0u) << k;
+  for (int k = 0; k < 4; ++k) {
+    bits |= ((c[k] & 0xFFFFu) >= d.thr ? 1u : 0u) << (2 * k);
+    bits |= ((c[k] >> 16) >= d.thr ? 1u : 0u) << (2 * k + 1);
   }
   return bits;
 }
@@ -240,6 +245,7 @@ inline DropCfg drop_cfg(const Attrs& a) {
   d.p = float(a.f("p", 0.0));
   d.scale = d.p > 0.0f ? 1.0f / (1.0f - d.p) : 1.0f;
   d.seed = uint64_t(a.i("seed", 0));
+  d.thr = d.p > 0.0f ? uint32_t(std::ceil(double(d.p) * 65536.0)) : 0u;
   d.salt = uint64_t(a.i("salt", 0));
   return d;
 }

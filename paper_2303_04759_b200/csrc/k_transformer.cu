@@ -240,6 +240,9 @@ __global__ void __launch_bounds__(256) k_ln_fwd(const T* __restrict__ x, const T
 // 16-bit vector fast path (bf16/f16, H % 8 == 0, 16-byte rows): two rows per
 // warp with every load of both rows issued up front and kept packed (8
 // elements per uint4), so a 2-CTA/SM wave holds all BERT-base rows in flight.
+// The path is instruction-bound (one wave, ~13 warps/SM), so: gamma / beta as
+// 16-byte vectors, paired f32->16-bit conversions, y = fma(fma(s, rstd,
+// -mean*rstd), g, b), and FULL (H == NC*256) drops the per-chunk guards.
 template <typename T>
 __device__ __forceinline__ void unpack8(const uint4& q, float* f) {
   const T* h = reinterpret_cast<const T*>(&q);
@@ -247,18 +250,35 @@ __device__ __forceinline__ void unpack8(const uint4& q, float* f) {
   for (int k = 0; k < 8; ++k) f[k] = to_f(h[k]);
 }
 template <typename T>
+__device__ __forceinline__ uint32_t pack2(float a, float b) {
+  if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h);
+  } else {
+    __half2 h = __floats2half2_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h);
+  }
+}
+template <typename T>
 __device__ __forceinline__ uint4 pack8(const float* f) {
-  uint4 q;
-  T* h = reinterpret_cast<T*>(&q);
-#pragma unroll
-  for (int k = 0; k < 8; ++k) h[k] = from_f<T>(f[k]);
-  return q;
+  return make_uint4(pack2<T>(f[0], f[1]), pack2<T>(f[2], f[3]), pack2<T>(f[4], f[5]), pack2<T>(f[6], f[7]));
+}
+// 8 per-column parameters (gamma / beta) from j0: f32 or the storage dtype
+template <typename T, bool GF>
+__device__ __forceinline__ void ld_param8(const void* p, int j0, float* f) {
+  if constexpr (GF) {
+    const float4* q = reinterpret_cast<const float4*>(static_cast<const float*>(p) + j0);
+    const float4 a = __ldg(q), b = __ldg(q + 1);
+    f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w;
+    f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
+  } else {
+    unpack8<T>(__ldg(reinterpret_cast<const uint4*>(static_cast<const T*>(p) + j0)), f);
+  }
 }
 
-template <typename T, int NC>
+template <typename T, int NC, bool GF, bool FULL>
 __global__ void __launch_bounds__(256) k_ln_fwd16(const T* __restrict__ x, const T* __restrict__ r,
-                                                  const float* __restrict__ gamma_f, const T* __restrict__ gamma_t,
-                                                  const float* __restrict__ beta_f, const T* __restrict__ beta_t,
+                                                  const void* __restrict__ gamma, const void* __restrict__ beta,
                                                   T* __restrict__ y, T* __restrict__ s_out, float* __restrict__ mean_o,
                                                   float* __restrict__ rstd_o, int64_t rows, int H, float eps,
                                                   DropCfg d) {
@@ -267,14 +287,14 @@ __global__ void __launch_bounds__(256) k_ln_fwd16(const T* __restrict__ x, const
   const int lane = threadIdx.x & 31;
   const int64_t row0 = (blockIdx.x * int64_t(blockDim.x >> 5) + (threadIdx.x >> 5)) * RW;
   if (row0 >= rows) return;
-  const int nch = H / 8;
+  const int nch = FULL ? NC * 32 : H / 8;
   uint4 xq[RW][NC], rq[RW][NC];
 #pragma unroll
   for (int q = 0; q < RW; ++q)
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
       const int ch = lane + c * 32;
-      if (row0 + q < rows && ch < nch) {
+      if (row0 + q < rows && (FULL || ch < nch)) {
         const int64_t i = (row0 + q) * H + ch * 8;
         xq[q][c] = __ldg(reinterpret_cast<const uint4*>(x + i));
         if (r) rq[q][c] = __ldg(reinterpret_cast<const uint4*>(r + i));
@@ -290,19 +310,23 @@ __global__ void __launch_bounds__(256) k_ln_fwd16(const T* __restrict__ x, const
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
       const int ch = lane + c * 32;
-      if (ch < nch) {
-        const int64_t i = row * H + ch * 8;
+      if (FULL || ch < nch) {
         unpack8<T>(xq[q][c], v[c]);
         if (r) {
+          const int64_t i = row * H + ch * 8;
           float rv[8];
           unpack8<T>(rq[q][c], rv);
           const uint32_t bits = d.p > 0.0f ? dropout_bits8q(d, uint64_t(i) >> 3) : 0xFFu;
+          uint4 w;
+          uint32_t* wp = reinterpret_cast<uint32_t*>(&w);
 #pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            const float xv = ((bits >> k) & 1u) ? __fmul_rn(v[c][k], d.scale) : 0.0f;
-            v[c][k] = to_f(from_f<T>(__fadd_rn(xv, rv[k])));  // s rounded to storage dtype
+          for (int k = 0; k < 8; k += 2) {
+            const float x0 = ((bits >> k) & 1u) ? __fmul_rn(v[c][k], d.scale) : 0.0f;
+            const float x1 = ((bits >> (k + 1)) & 1u) ? __fmul_rn(v[c][k + 1], d.scale) : 0.0f;
+            wp[k >> 1] = pack2<T>(__fadd_rn(x0, rv[k]), __fadd_rn(x1, rv[k + 1]));  // s in the storage dtype
           }
-          *reinterpret_cast<uint4*>(s_out + i) = pack8<T>(v[c]);
+          unpack8<T>(w, v[c]);
+          *reinterpret_cast<uint4*>(s_out + i) = w;
         }
 #pragma unroll
         for (int k = 0; k < 8; ++k) sum += v[c][k];
@@ -315,13 +339,14 @@ __global__ void __launch_bounds__(256) k_ln_fwd16(const T* __restrict__ x, const
     float sq = 0.0f;
 #pragma unroll
     for (int c = 0; c < NC; ++c)
-      if (lane + c * 32 < nch)
+      if (FULL || lane + c * 32 < nch)
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
           const float dd = v[c][k] - mean;
-          sq += dd * dd;
+          sq = fmaf(dd, dd, sq);
         }
     const float rstd = 1.0f / sqrtf(warp_sum(sq) * inv + eps);
+    const float nmr = -mean * rstd;
     if (lane == 0) {
       mean_o[row] = mean;
       rstd_o[row] = rstd;
@@ -329,15 +354,12 @@ __global__ void __launch_bounds__(256) k_ln_fwd16(const T* __restrict__ x, const
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
       const int ch = lane + c * 32;
-      if (ch < nch) {
-        float o[8];
+      if (FULL || ch < nch) {
+        float g[8], b[8], o[8];
+        ld_param8<T, GF>(gamma, ch * 8, g);
+        ld_param8<T, GF>(beta, ch * 8, b);
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const int j = ch * 8 + k;
-          const float g = gamma_f ? __ldg(gamma_f + j) : to_f(gamma_t[j]);
-          const float b = beta_f ? __ldg(beta_f + j) : to_f(beta_t[j]);
-          o[k] = (v[c][k] - mean) * rstd * g + b;
-        }
+        for (int k = 0; k < 8; ++k) o[k] = fmaf(fmaf(v[c][k], rstd, nmr), g[k], b[k]);
         *reinterpret_cast<uint4*>(y + row * H + ch * 8) = pack8<T>(o);
       }
     }
@@ -368,12 +390,16 @@ static void build_ln_fwd(Plan& p, bool residual) {
       vec = vec && reinterpret_cast<uintptr_t>(out[0].ptr) % 16 == 0;
       if (residual) vec = vec && reinterpret_cast<uintptr_t>(out[1].ptr) % 16 == 0;
       if constexpr (sizeof(T) == 2) {
+        // parameter vectors need 16-byte alignment too
+        for (int i = gi; i < gi + 2; ++i) vec = vec && reinterpret_cast<uintptr_t>(in[i].ptr) % 16 == 0;
         if (vec) {
-          launch_k(k_ln_fwd16<T, NC>, unsigned((rows + 15) / 16), 256, 0, s, (const T*)in[0].ptr,
-                   residual ? (const T*)in[1].ptr : nullptr, gf ? (const float*)in[gi].ptr : nullptr,
-                   gf ? nullptr : (const T*)in[gi].ptr, gf ? (const float*)in[gi + 1].ptr : nullptr,
-                   gf ? nullptr : (const T*)in[gi + 1].ptr, (T*)out[0].ptr, residual ? (T*)out[1].ptr : nullptr,
-                   (float*)out[residual ? 2 : 1].ptr, (float*)out[residual ? 3 : 2].ptr, rows, H, eps, d);
+          const bool full = H == NC * 256;
+          auto kern = gf ? (full ? k_ln_fwd16<T, NC, true, true> : k_ln_fwd16<T, NC, true, false>)
+                         : (full ? k_ln_fwd16<T, NC, false, true> : k_ln_fwd16<T, NC, false, false>);
+          launch_k(kern, unsigned((rows + 15) / 16), 256, 0, s, (const T*)in[0].ptr,
+                   residual ? (const T*)in[1].ptr : nullptr, (const void*)in[gi].ptr, (const void*)in[gi + 1].ptr,
+                   (T*)out[0].ptr, residual ? (T*)out[1].ptr : nullptr, (float*)out[residual ? 2 : 1].ptr,
+                   (float*)out[residual ? 3 : 2].ptr, rows, H, eps, d);
           return;
         }
       }
@@ -495,117 +521,154 @@ __global__ void __launch_bounds__(256) k_ln_bwd(const T* __restrict__ sx, const 
   }
 }
 
-// 16-bit vector fast path: both rows' loads issued up front (packed), the
-// per-lane column partials (dgamma, dbeta, and with bias_grad the column sum of
-// the outgoing gradient) accumulate in per-warp smem rows, folded per CTA.
-template <typename T, int NC>
-__global__ void __launch_bounds__(256) k_ln_bwd16(const T* __restrict__ sx, const float* __restrict__ gamma_f,
-                                                  const T* __restrict__ gamma_t, const float* __restrict__ mean,
-                                                  const float* __restrict__ rstd, const T* __restrict__ dy,
-                                                  const T* __restrict__ dy2, T* __restrict__ ds_o,
-                                                  T* __restrict__ dx_o, float* __restrict__ ws, int nparts,
-                                                  int64_t rows, int H, DropCfg d) {
+// 16-bit vector fast path: both rows' loads issued up front (packed). Pass 1
+// walks chunk-major over the two rows, so each column's dgamma / dbeta partial
+// (the two rows' sum) is complete in registers and stored once to the warp's
+// smem row [warp][part][H] (no read-modify-write); pass 2 recomputes xh and g
+// from the packed loads, writes ds / dx and the bias-grad partial likewise.
+// The 8 warp rows fold per CTA (16-byte smem reads) into one ws row per part.
+template <typename T, int NC, bool GF, bool FULL>
+__global__ void __launch_bounds__(256, NC <= 3 ? 2 : 1) k_ln_bwd16(const T* __restrict__ sx, const void* __restrict__ gamma,
+                                                  const float* __restrict__ mean, const float* __restrict__ rstd,
+                                                  const T* __restrict__ dy, const T* __restrict__ dy2,
+                                                  T* __restrict__ ds_o, T* __restrict__ dx_o, float* __restrict__ ws,
+                                                  int nparts, int64_t rows, int H, DropCfg d) {
   TCB_PDL_ENTRY();
   constexpr int RW = LNB_ROWS / 8;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int nch = H / 8;
-  extern __shared__ float red[];
-  constexpr int CP = NC * 32;  // chunk pitch
-  float* pp[3];
-#pragma unroll
-  for (int a = 0; a < 3; ++a) pp[a] = red + (warp * 3 + a) * 8 * CP;
-#pragma unroll
-  for (int a = 0; a < 3; ++a)
-#pragma unroll
-    for (int c = 0; c < NC; ++c)
-#pragma unroll
-      for (int k = 0; k < 8; ++k) pp[a][k * CP + c * 32 + lane] = 0.0f;
+  const int nch = FULL ? NC * 32 : H / 8;
+  extern __shared__ float red[];  // [8 warps][3 parts][H]
+  float* prow = red + warp * 3 * H;
   const int64_t row0 = int64_t(blockIdx.x) * LNB_ROWS + warp * RW;
   uint4 sq[RW][NC], dq[RW][NC], d2q[RW][NC];
+  float mu[RW], rs[RW];
+  bool live[RW];
 #pragma unroll
-  for (int q = 0; q < RW; ++q)
+  for (int q = 0; q < RW; ++q) {
+    live[q] = row0 + q < rows;
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
       const int ch = lane + c * 32;
-      if (row0 + q < rows && ch < nch) {
+      if (live[q] && (FULL || ch < nch)) {
         const int64_t i = (row0 + q) * H + ch * 8;
         sq[q][c] = __ldg(reinterpret_cast<const uint4*>(sx + i));
         dq[q][c] = __ldg(reinterpret_cast<const uint4*>(dy + i));
         if (dy2) d2q[q][c] = __ldg(reinterpret_cast<const uint4*>(dy2 + i));
       }
     }
+    mu[q] = live[q] ? mean[row0 + q] : 0.0f;
+    rs[q] = live[q] ? rstd[row0 + q] : 0.0f;
+  }
+  // xh, dv (= dy + dy2) and g = dv * gamma of chunk c of row q
+  auto load_row = [&](int q, int c, const float* gm, float* xh, float* dv, float* g) {
+    float sv[8];
+    unpack8<T>(sq[q][c], sv);
+    unpack8<T>(dq[q][c], dv);
+    if (dy2) {
+      float d2[8];
+      unpack8<T>(d2q[q][c], d2);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) dv[k] = __fadd_rn(dv[k], d2[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      xh[k] = (sv[k] - mu[q]) * rs[q];
+      g[k] = dv[k] * gm[k];
+    }
+  };
   const float inv = 1.0f / float(H);
+  float c1[RW], c2[RW];
+#pragma unroll
+  for (int q = 0; q < RW; ++q) c1[q] = c2[q] = 0.0f;
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    const int ch = lane + c * 32;
+    if (!(FULL || ch < nch)) continue;
+    float gm[8], pg[8], pb[8];
+    ld_param8<T, GF>(gamma, ch * 8, gm);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) pg[k] = pb[k] = 0.0f;
+#pragma unroll
+    for (int q = 0; q < RW; ++q) {
+      if (!live[q]) break;
+      float xh[8], dv[8], g[8];
+      load_row(q, c, gm, xh, dv, g);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        c1[q] = fmaf(g[k], xh[k], c1[q]);
+        c2[q] += g[k];
+        pg[k] = fmaf(dv[k], xh[k], pg[k]);
+        pb[k] += dv[k];
+      }
+    }
+    float4* o0 = reinterpret_cast<float4*>(prow + ch * 8);
+    float4* o1 = reinterpret_cast<float4*>(prow + H + ch * 8);
+    o0[0] = make_float4(pg[0], pg[1], pg[2], pg[3]);
+    o0[1] = make_float4(pg[4], pg[5], pg[6], pg[7]);
+    o1[0] = make_float4(pb[0], pb[1], pb[2], pb[3]);
+    o1[1] = make_float4(pb[4], pb[5], pb[6], pb[7]);
+  }
+  // o = rs * (g - c2 - xh * c1) = fma(rs, g, fma(xh, -rs*c1, -rs*c2))
+  float a1[RW], a0[RW];
 #pragma unroll
   for (int q = 0; q < RW; ++q) {
-    const int64_t row = row0 + q;
-    if (row >= rows) break;
-    const float mu = mean[row], rs = rstd[row];
-    float xh[NC][8], g[NC][8];
-    float c1 = 0.0f, c2 = 0.0f;
+    c1[q] = warp_sum(c1[q]) * inv;
+    c2[q] = warp_sum(c2[q]) * inv;
+    a1[q] = -rs[q] * c1[q];
+    a0[q] = -rs[q] * c2[q];
+  }
 #pragma unroll
-    for (int c = 0; c < NC; ++c) {
-      const int ch = lane + c * 32;
-      if (ch < nch) {
-        float sv[8], dv[8];
-        unpack8<T>(sq[q][c], sv);
-        unpack8<T>(dq[q][c], dv);
-        if (dy2) {
-          float d2[8];
-          unpack8<T>(d2q[q][c], d2);
+  for (int c = 0; c < NC; ++c) {
+    const int ch = lane + c * 32;
+    if (!(FULL || ch < nch)) continue;
+    float gm[8], pz[8];
+    ld_param8<T, GF>(gamma, ch * 8, gm);
 #pragma unroll
-          for (int k = 0; k < 8; ++k) dv[k] = __fadd_rn(dv[k], d2[k]);
-        }
+    for (int k = 0; k < 8; ++k) pz[k] = 0.0f;
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const int j = ch * 8 + k;
-          const float gm = gamma_f ? __ldg(gamma_f + j) : to_f(gamma_t[j]);
-          xh[c][k] = (sv[k] - mu) * rs;
-          g[c][k] = dv[k] * gm;
-          c1 += g[c][k] * xh[c][k];
-          c2 += g[c][k];
-          pp[0][k * CP + c * 32 + lane] += dv[k] * xh[c][k];
-          pp[1][k * CP + c * 32 + lane] += dv[k];
-        }
-      } else {
+    for (int q = 0; q < RW; ++q) {
+      if (!live[q]) break;
+      float xh[8], dv[8], g[8], o[8];
+      load_row(q, c, gm, xh, dv, g);
+      const int64_t i = (row0 + q) * H + ch * 8;
 #pragma unroll
-        for (int k = 0; k < 8; ++k) xh[c][k] = g[c][k] = 0.0f;
+      for (int k = 0; k < 8; ++k) o[k] = fmaf(rs[q], g[k], fmaf(xh[k], a1[q], a0[q]));
+      uint4 w = pack8<T>(o);
+      *reinterpret_cast<uint4*>(ds_o + i) = w;
+      if (dx_o) {
+        const uint32_t bits = d.p > 0.0f ? dropout_bits8q(d, uint64_t(i) >> 3) : 0xFFu;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) o[k] = ((bits >> k) & 1u) ? o[k] * d.scale : 0.0f;
+        w = pack8<T>(o);
+        *reinterpret_cast<uint4*>(dx_o + i) = w;
+      }
+      if (nparts > 2) {  // bias grad: the outgoing gradient as stored
+        float f[8];
+        unpack8<T>(w, f);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) pz[k] += f[k];
       }
     }
-    c1 = warp_sum(c1) * inv;
-    c2 = warp_sum(c2) * inv;
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
-      const int ch = lane + c * 32;
-      if (ch < nch) {
-        const int64_t i = row * H + ch * 8;
-        float o[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) o[k] = rs * (g[c][k] - c2 - xh[c][k] * c1);
-        uint4 w = pack8<T>(o);
-        *reinterpret_cast<uint4*>(ds_o + i) = w;
-        if (dx_o) {
-          const uint32_t bits = d.p > 0.0f ? dropout_bits8q(d, uint64_t(i) >> 3) : 0xFFu;
-#pragma unroll
-          for (int k = 0; k < 8; ++k) o[k] = ((bits >> k) & 1u) ? o[k] * d.scale : 0.0f;
-          w = pack8<T>(o);
-          *reinterpret_cast<uint4*>(dx_o + i) = w;
-        }
-        if (nparts > 2) {  // bias grad: the outgoing gradient as stored
-          float f[8];
-          unpack8<T>(w, f);
-#pragma unroll
-          for (int k = 0; k < 8; ++k) pp[2][k * CP + c * 32 + lane] += f[k];
-        }
-      }
+    if (nparts > 2) {
+      float4* o2 = reinterpret_cast<float4*>(prow + 2 * H + ch * 8);
+      o2[0] = make_float4(pz[0], pz[1], pz[2], pz[3]);
+      o2[1] = make_float4(pz[4], pz[5], pz[6], pz[7]);
     }
   }
+  // warps whose rows are all past the end contribute zeros
+  if (!live[0]) {
+    for (int j = lane * 4; j < 3 * H; j += 128) *reinterpret_cast<float4*>(prow + j) = make_float4(0, 0, 0, 0);
+  }
   __syncthreads();
-  for (int j = threadIdx.x; j < H; j += blockDim.x) {
-    const int off = (j & 7) * CP + (j >> 3);
+  for (int j = threadIdx.x * 4; j < H; j += blockDim.x * 4) {
     for (int a = 0; a < nparts; ++a) {
-      float acc = 0.0f;
-      for (int w = 0; w < 8; ++w) acc += red[(w * 3 + a) * 8 * CP + off];
-      ws[(int64_t(blockIdx.x) * nparts + a) * H + j] = acc;
+      float4 acc = make_float4(0, 0, 0, 0);
+#pragma unroll
+      for (int w = 0; w < 8; ++w) {
+        const float4 t = *reinterpret_cast<const float4*>(red + (w * 3 + a) * H + j);
+        acc.x += t.x; acc.y += t.y; acc.z += t.z; acc.w += t.w;
+      }
+      *reinterpret_cast<float4*>(ws + (int64_t(blockIdx.x) * nparts + a) * H + j) = acc;
     }
   }
 }
@@ -671,7 +734,12 @@ static void b_layer_norm_dx(Plan& p) {
     std::call_once(once, [] {
       constexpr int sm = 8 * 3 * 8 * 32 * NC * 4;
       TCB_CUDA(cudaFuncSetAttribute(k_ln_bwd<T, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-      TCB_CUDA(cudaFuncSetAttribute(k_ln_bwd16<T, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+      if constexpr (sizeof(T) == 2) {
+        TCB_CUDA(cudaFuncSetAttribute(k_ln_bwd16<T, NC, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+        TCB_CUDA(cudaFuncSetAttribute(k_ln_bwd16<T, NC, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+        TCB_CUDA(cudaFuncSetAttribute(k_ln_bwd16<T, NC, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+        TCB_CUDA(cudaFuncSetAttribute(k_ln_bwd16<T, NC, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+      }
     });
     p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
       bool vec = H % 8 == 0;
@@ -684,10 +752,16 @@ static void b_layer_norm_dx(Plan& p) {
       const T* d2 = has_res ? (const T*)in[5].ptr : nullptr;
       T* dxp = has_dx ? (T*)out[3].ptr : nullptr;
       bool fast = false;
-      if constexpr (sizeof(T) == 2) fast = vec;
+      if constexpr (sizeof(T) == 2) fast = vec && reinterpret_cast<uintptr_t>(in[1].ptr) % 16 == 0;
       if (fast) {
-        launch_k(k_ln_bwd16<T, NC>, nblk, 256, smem, s, (const T*)in[0].ptr, gfp, gtp, (const float*)in[2].ptr,
-                 (const float*)in[3].ptr, (const T*)in[4].ptr, d2, (T*)out[0].ptr, dxp, (float*)ws->p, np, rows, H, d);
+        if constexpr (sizeof(T) == 2) {
+          const bool full = H == NC * 256;
+          auto kern = gf ? (full ? k_ln_bwd16<T, NC, true, true> : k_ln_bwd16<T, NC, true, false>)
+                         : (full ? k_ln_bwd16<T, NC, false, true> : k_ln_bwd16<T, NC, false, false>);
+          launch_k(kern, nblk, 256, smem, s, (const T*)in[0].ptr, (const void*)in[1].ptr, (const float*)in[2].ptr,
+                   (const float*)in[3].ptr, (const T*)in[4].ptr, d2, (T*)out[0].ptr, dxp, (float*)ws->p, np, rows, H,
+                   d);
+        }
       } else {
         launch_k(k_ln_bwd<T, NC>, nblk, 256, smem, s, (const T*)in[0].ptr, gfp, gtp, (const float*)in[2].ptr,
                  (const float*)in[3].ptr, (const T*)in[4].ptr, d2, (T*)out[0].ptr, dxp, (float*)ws->p, np, rows, H, d,

@@ -373,6 +373,27 @@ def test_add_layer_norm_and_backward(p):
     assert rel_err(g[3], o[3]) < 1e-4 and rel_err(g[0], o[0]) < 5e-3
 
 
+@pytest.mark.parametrize("H,gdt", [(768, BF16), (1000, F32), (1000, BF16), (256, F32), (2048, F32)])
+def test_layer_norm_fwd_bwd_shapes(H, gdt):
+    # ragged row count (tail CTA with dead warps / a half-filled warp), 16-bit
+    # and f32 gamma/beta, full and partial last chunks, the largest supported H
+    T = 77
+    x, r = rn(T, H), rn(T, H)
+    gm, bt = rn(H, lo=0.5, hi=1.5), rn(H, lo=-0.1, hi=0.1)
+    attrs = {"eps": 1e-12, "p": 0.1, "seed": 3, "salt": 9}
+    g, o = run_both("add_layer_norm", [(x, BF16), (r, BF16), (gm, gdt), (bt, gdt)],
+                    [((T, H), BF16), ((T, H), BF16), ((T,), F32), ((T,), F32)], attrs)
+    assert bits_equal(g[1], o[1])
+    assert rel_err(g[0], o[0]) < BF16_TOL and rel_err(g[2], o[2]) < 1e-5 and rel_err(g[3], o[3]) < 1e-5
+    s, mean, rstd = o[1], o[2], o[3]
+    dy, dy2 = rn(T, H), rn(T, H)
+    outs = [((T, H), BF16), ((H,), F32), ((H,), F32), ((T, H), BF16), ((H,), F32)]
+    g, o = run_both("layer_norm_dx", [(s, BF16), (gm, gdt), (mean, F32), (rstd, F32), (dy, BF16), (dy2, BF16)],
+                    outs, {**attrs, "bias_grad": 1})
+    assert rel_err(g[0], o[0]) < 5e-3 and rel_err(g[3], o[3]) < 5e-3
+    assert rel_err(g[1], o[1]) < 1e-5 and rel_err(g[2], o[2]) < 1e-5 and rel_err(g[4], o[4]) < 1e-4
+
+
 def test_layer_norm_dx_f32():
     T, H = 64, 128
     s, gm = rn(T, H), rn(H, lo=0.5, hi=1.5)
