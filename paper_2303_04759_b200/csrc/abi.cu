@@ -142,6 +142,17 @@ int tcb_plan_create(const char* dialect_op, const tcb_tensor* in, int nin, const
   });
 }
 
+// Profiling knob, never set in tests or the bench: TCB_SKIP_OPS="op1,op2" makes
+// tcb_launch return without launching those ops, so a step's time can be
+// attributed per op class by difference (outputs are then garbage).
+static bool skipped_op(const std::string& op) {
+  static const std::string list = [] {
+    const char* e = std::getenv("TCB_SKIP_OPS");
+    return e ? "," + std::string(e) + "," : std::string();
+  }();
+  return !list.empty() && list.find("," + op + ",") != std::string::npos;
+}
+
 int tcb_launch(tcb_plan plan, const tcb_tensor* in, int nin, tcb_tensor* out, int nout,
                void* stream) {
   TCB_TRY({
@@ -149,6 +160,7 @@ int tcb_launch(tcb_plan plan, const tcb_tensor* in, int nin, tcb_tensor* out, in
     Plan& p = plan->p;
     if (nin != int(p.in.size()) || nout != int(p.out.size()))
       fail(TCB_ERR_ARG, "b200." + p.op + ": launch arity differs from plan");
+    if (skipped_op(p.op)) return TCB_OK;
     p.run(in, out, static_cast<cudaStream_t>(stream));
     TCB_CUDA(cudaGetLastError());
   });

@@ -127,6 +127,19 @@ __device__ __forceinline__ float gelu_grad_f(float x) {
   return __fadd_rn(cdf, __fmul_rn(x, pdf));
 }
 
+// Packed f32x2 arithmetic (sm_100 FADD2 / FMUL2 / FFMA2): one instruction per
+// element pair, each lane IEEE round-to-nearest like the scalar op, so results
+// are bit-identical to the scalar code while issue-bound row kernels halve
+// their FP instruction count.
+__device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ float2 splat2(float a) { return make_float2(a, a); }
+// a 32-bit word of two 16-bit floats <-> float2 (bf16: shifts; f16: cvt)
+__device__ __forceinline__ float2 bf2_to_f2(uint32_t w) {
+  return make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xffff0000u));
+}
+
 // GEMM-epilogue GELU / GELU' on the MUFU path: Phi(x) from the
 // Abramowitz-Stegun 7.1.26 erfc (|err| <= 1.5e-7, with ex2.approx / rcp.approx
 // adding a few ulp) sharing one exponential exp(-x^2/2) with the pdf term.

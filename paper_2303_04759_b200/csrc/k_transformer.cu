@@ -263,17 +263,51 @@ template <typename T>
 __device__ __forceinline__ uint4 pack8(const float* f) {
   return make_uint4(pack2<T>(f[0], f[1]), pack2<T>(f[2], f[3]), pack2<T>(f[4], f[5]), pack2<T>(f[6], f[7]));
 }
-// 8 per-column parameters (gamma / beta) from j0: f32 or the storage dtype
-template <typename T, bool GF>
-__device__ __forceinline__ void ld_param8(const void* p, int j0, float* f) {
-  if constexpr (GF) {
-    const float4* q = reinterpret_cast<const float4*>(static_cast<const float*>(p) + j0);
-    const float4 a = __ldg(q), b = __ldg(q + 1);
-    f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w;
-    f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
-  } else {
-    unpack8<T>(__ldg(reinterpret_cast<const uint4*>(static_cast<const T*>(p) + j0)), f);
+// 8 packed 16-bit values <-> 4 float2 (element pairs for the f32x2 ops)
+template <typename T>
+__device__ __forceinline__ void unpack8x2(const uint4& q, float2* f) {
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(&q);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    if constexpr (std::is_same<T, __nv_bfloat16>::value) f[k] = bf2_to_f2(w[k]);
+    else f[k] = __half22float2(*reinterpret_cast<const __half2*>(&w[k]));
   }
+}
+template <typename T>
+__device__ __forceinline__ uint4 pack8x2(const float2* f) {
+  return make_uint4(pack2<T>(f[0].x, f[0].y), pack2<T>(f[1].x, f[1].y), pack2<T>(f[2].x, f[2].y),
+                    pack2<T>(f[3].x, f[3].y));
+}
+// keep-mask select of a pair: (bit k ? t.x : 0, bit k+1 ? t.y : 0)
+__device__ __forceinline__ float2 keep2(uint32_t bits, int k, float2 t) {
+  return make_float2(((bits >> k) & 1u) ? t.x : 0.0f, ((bits >> (k + 1)) & 1u) ? t.y : 0.0f);
+}
+// per-column f32 parameters staged in smem once per CTA (gamma [, beta]): one
+// 16-byte load per thread, all in flight together (H % 8 == 0, 16-byte aligned)
+template <typename T, bool GF>
+__device__ __forceinline__ void stage_params(const void* g, const void* b, float* sg, float* sb, int H) {
+  const int n8 = H / 8, n = b ? 2 * n8 : n8;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const bool isb = i >= n8;
+    const int c = isb ? i - n8 : i;
+    float4* dst = reinterpret_cast<float4*>((isb ? sb : sg) + c * 8);
+    if constexpr (GF) {
+      const float4* src = reinterpret_cast<const float4*>(static_cast<const float*>(isb ? b : g) + c * 8);
+      const float4 u = __ldg(src), v = __ldg(src + 1);
+      dst[0] = u;
+      dst[1] = v;
+    } else {
+      float f[8];
+      unpack8<T>(__ldg(reinterpret_cast<const uint4*>(static_cast<const T*>(isb ? b : g) + c * 8)), f);
+      dst[0] = make_float4(f[0], f[1], f[2], f[3]);
+      dst[1] = make_float4(f[4], f[5], f[6], f[7]);
+    }
+  }
+}
+__device__ __forceinline__ void lds8x2(const float* p, float2* f) {
+  const float4 a = reinterpret_cast<const float4*>(p)[0], b = reinterpret_cast<const float4*>(p)[1];
+  f[0] = make_float2(a.x, a.y); f[1] = make_float2(a.z, a.w);
+  f[2] = make_float2(b.x, b.y); f[3] = make_float2(b.z, b.w);
 }
 
 template <typename T, int NC, bool GF, bool FULL>
@@ -284,9 +318,9 @@ __global__ void __launch_bounds__(256) k_ln_fwd16(const T* __restrict__ x, const
                                                   DropCfg d) {
   TCB_PDL_ENTRY();
   constexpr int RW = 2;
+  __shared__ __align__(16) float sg[NC * 256], sb[NC * 256];
   const int lane = threadIdx.x & 31;
   const int64_t row0 = (blockIdx.x * int64_t(blockDim.x >> 5) + (threadIdx.x >> 5)) * RW;
-  if (row0 >= rows) return;
   const int nch = FULL ? NC * 32 : H / 8;
   uint4 xq[RW][NC], rq[RW][NC];
 #pragma unroll
@@ -300,53 +334,53 @@ __global__ void __launch_bounds__(256) k_ln_fwd16(const T* __restrict__ x, const
         if (r) rq[q][c] = __ldg(reinterpret_cast<const uint4*>(r + i));
       }
     }
+  stage_params<T, GF>(gamma, beta, sg, sb, H);
+  __syncthreads();
   const float inv = 1.0f / float(H);
+  const float2 sc2 = splat2(d.scale);
 #pragma unroll
   for (int q = 0; q < RW; ++q) {
     const int64_t row = row0 + q;
     if (row >= rows) break;
-    float v[NC][8];
-    float sum = 0.0f;
+    float2 v[NC][4];
+    float2 sum2 = make_float2(0.0f, 0.0f);
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
       const int ch = lane + c * 32;
       if (FULL || ch < nch) {
-        unpack8<T>(xq[q][c], v[c]);
+        unpack8x2<T>(xq[q][c], v[c]);
         if (r) {
           const int64_t i = row * H + ch * 8;
-          float rv[8];
-          unpack8<T>(rq[q][c], rv);
+          float2 rv[4];
+          unpack8x2<T>(rq[q][c], rv);
           const uint32_t bits = d.p > 0.0f ? dropout_bits8q(d, uint64_t(i) >> 3) : 0xFFu;
-          uint4 w;
-          uint32_t* wp = reinterpret_cast<uint32_t*>(&w);
+          float2 sv[4];
 #pragma unroll
-          for (int k = 0; k < 8; k += 2) {
-            const float x0 = ((bits >> k) & 1u) ? __fmul_rn(v[c][k], d.scale) : 0.0f;
-            const float x1 = ((bits >> (k + 1)) & 1u) ? __fmul_rn(v[c][k + 1], d.scale) : 0.0f;
-            wp[k >> 1] = pack2<T>(__fadd_rn(x0, rv[k]), __fadd_rn(x1, rv[k + 1]));  // s in the storage dtype
-          }
-          unpack8<T>(w, v[c]);
+          for (int k = 0; k < 4; ++k) sv[k] = add2(keep2(bits, 2 * k, mul2(v[c][k], sc2)), rv[k]);
+          const uint4 w = pack8x2<T>(sv);  // s in the storage dtype
+          unpack8x2<T>(w, v[c]);
           *reinterpret_cast<uint4*>(s_out + i) = w;
         }
 #pragma unroll
-        for (int k = 0; k < 8; ++k) sum += v[c][k];
+        for (int k = 0; k < 4; ++k) sum2 = add2(sum2, v[c][k]);
       } else {
 #pragma unroll
-        for (int k = 0; k < 8; ++k) v[c][k] = 0.0f;
+        for (int k = 0; k < 4; ++k) v[c][k] = make_float2(0.0f, 0.0f);
       }
     }
-    const float mean = warp_sum(sum) * inv;
-    float sq = 0.0f;
+    const float mean = warp_sum(sum2.x + sum2.y) * inv;
+    const float2 nm2 = splat2(-mean);
+    float2 sq2 = make_float2(0.0f, 0.0f);
 #pragma unroll
     for (int c = 0; c < NC; ++c)
       if (FULL || lane + c * 32 < nch)
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const float dd = v[c][k] - mean;
-          sq = fmaf(dd, dd, sq);
+        for (int k = 0; k < 4; ++k) {
+          const float2 dd = add2(v[c][k], nm2);
+          sq2 = fma2(dd, dd, sq2);
         }
-    const float rstd = 1.0f / sqrtf(warp_sum(sq) * inv + eps);
-    const float nmr = -mean * rstd;
+    const float rstd = 1.0f / sqrtf(warp_sum(sq2.x + sq2.y) * inv + eps);
+    const float2 rs2 = splat2(rstd), nmr2 = splat2(-mean * rstd);
     if (lane == 0) {
       mean_o[row] = mean;
       rstd_o[row] = rstd;
@@ -355,12 +389,12 @@ __global__ void __launch_bounds__(256) k_ln_fwd16(const T* __restrict__ x, const
     for (int c = 0; c < NC; ++c) {
       const int ch = lane + c * 32;
       if (FULL || ch < nch) {
-        float g[8], b[8], o[8];
-        ld_param8<T, GF>(gamma, ch * 8, g);
-        ld_param8<T, GF>(beta, ch * 8, b);
+        float2 g[4], b[4], o[4];
+        lds8x2(sg + ch * 8, g);
+        lds8x2(sb + ch * 8, b);
 #pragma unroll
-        for (int k = 0; k < 8; ++k) o[k] = fmaf(fmaf(v[c][k], rstd, nmr), g[k], b[k]);
-        *reinterpret_cast<uint4*>(y + row * H + ch * 8) = pack8<T>(o);
+        for (int k = 0; k < 4; ++k) o[k] = fma2(fma2(v[c][k], rs2, nmr2), g[k], b[k]);
+        *reinterpret_cast<uint4*>(y + row * H + ch * 8) = pack8x2<T>(o);
       }
     }
   }
@@ -537,11 +571,12 @@ __global__ void __launch_bounds__(256, NC <= 3 ? 2 : 1) k_ln_bwd16(const T* __re
   constexpr int RW = LNB_ROWS / 8;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nch = FULL ? NC * 32 : H / 8;
-  extern __shared__ float red[];  // [8 warps][3 parts][H]
+  extern __shared__ __align__(16) float red[];  // [8 warps][3 parts][H], then gamma (f32) [H]
   float* prow = red + warp * 3 * H;
+  float* sg = red + 8 * 3 * H;
   const int64_t row0 = int64_t(blockIdx.x) * LNB_ROWS + warp * RW;
   uint4 sq[RW][NC], dq[RW][NC], d2q[RW][NC];
-  float mu[RW], rs[RW];
+  float2 rs2[RW], nmr2[RW];
   bool live[RW];
 #pragma unroll
   for (int q = 0; q < RW; ++q) {
@@ -556,103 +591,106 @@ __global__ void __launch_bounds__(256, NC <= 3 ? 2 : 1) k_ln_bwd16(const T* __re
         if (dy2) d2q[q][c] = __ldg(reinterpret_cast<const uint4*>(dy2 + i));
       }
     }
-    mu[q] = live[q] ? mean[row0 + q] : 0.0f;
-    rs[q] = live[q] ? rstd[row0 + q] : 0.0f;
+    const float mu = live[q] ? mean[row0 + q] : 0.0f, rs = live[q] ? rstd[row0 + q] : 0.0f;
+    rs2[q] = splat2(rs);
+    nmr2[q] = splat2(-mu * rs);
   }
-  // xh, dv (= dy + dy2) and g = dv * gamma of chunk c of row q
-  auto load_row = [&](int q, int c, const float* gm, float* xh, float* dv, float* g) {
-    float sv[8];
-    unpack8<T>(sq[q][c], sv);
-    unpack8<T>(dq[q][c], dv);
+  stage_params<T, GF>(gamma, nullptr, sg, nullptr, H);
+  __syncthreads();
+  // xh = s*rs - mu*rs, dv = dy + dy2 and g = dv * gamma of chunk c of row q (pairs)
+  auto load_row = [&](int q, int c, const float2* gm, float2* xh, float2* dv, float2* g) {
+    float2 sv[4];
+    unpack8x2<T>(sq[q][c], sv);
+    unpack8x2<T>(dq[q][c], dv);
     if (dy2) {
-      float d2[8];
-      unpack8<T>(d2q[q][c], d2);
+      float2 d2[4];
+      unpack8x2<T>(d2q[q][c], d2);
 #pragma unroll
-      for (int k = 0; k < 8; ++k) dv[k] = __fadd_rn(dv[k], d2[k]);
+      for (int k = 0; k < 4; ++k) dv[k] = add2(dv[k], d2[k]);
     }
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      xh[k] = (sv[k] - mu[q]) * rs[q];
-      g[k] = dv[k] * gm[k];
+    for (int k = 0; k < 4; ++k) {
+      xh[k] = fma2(sv[k], rs2[q], nmr2[q]);
+      g[k] = mul2(dv[k], gm[k]);
     }
   };
   const float inv = 1.0f / float(H);
-  float c1[RW], c2[RW];
+  float2 c1[RW], c2[RW];
 #pragma unroll
-  for (int q = 0; q < RW; ++q) c1[q] = c2[q] = 0.0f;
+  for (int q = 0; q < RW; ++q) c1[q] = c2[q] = make_float2(0.0f, 0.0f);
 #pragma unroll
   for (int c = 0; c < NC; ++c) {
     const int ch = lane + c * 32;
     if (!(FULL || ch < nch)) continue;
-    float gm[8], pg[8], pb[8];
-    ld_param8<T, GF>(gamma, ch * 8, gm);
+    float2 gm[4], pg[4], pb[4];
+    lds8x2(sg + ch * 8, gm);
 #pragma unroll
-    for (int k = 0; k < 8; ++k) pg[k] = pb[k] = 0.0f;
+    for (int k = 0; k < 4; ++k) pg[k] = pb[k] = make_float2(0.0f, 0.0f);
 #pragma unroll
     for (int q = 0; q < RW; ++q) {
       if (!live[q]) break;
-      float xh[8], dv[8], g[8];
+      float2 xh[4], dv[4], g[4];
       load_row(q, c, gm, xh, dv, g);
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        c1[q] = fmaf(g[k], xh[k], c1[q]);
-        c2[q] += g[k];
-        pg[k] = fmaf(dv[k], xh[k], pg[k]);
-        pb[k] += dv[k];
+      for (int k = 0; k < 4; ++k) {
+        c1[q] = fma2(g[k], xh[k], c1[q]);
+        c2[q] = add2(c2[q], g[k]);
+        pg[k] = fma2(dv[k], xh[k], pg[k]);
+        pb[k] = add2(pb[k], dv[k]);
       }
     }
     float4* o0 = reinterpret_cast<float4*>(prow + ch * 8);
     float4* o1 = reinterpret_cast<float4*>(prow + H + ch * 8);
-    o0[0] = make_float4(pg[0], pg[1], pg[2], pg[3]);
-    o0[1] = make_float4(pg[4], pg[5], pg[6], pg[7]);
-    o1[0] = make_float4(pb[0], pb[1], pb[2], pb[3]);
-    o1[1] = make_float4(pb[4], pb[5], pb[6], pb[7]);
+    o0[0] = make_float4(pg[0].x, pg[0].y, pg[1].x, pg[1].y);
+    o0[1] = make_float4(pg[2].x, pg[2].y, pg[3].x, pg[3].y);
+    o1[0] = make_float4(pb[0].x, pb[0].y, pb[1].x, pb[1].y);
+    o1[1] = make_float4(pb[2].x, pb[2].y, pb[3].x, pb[3].y);
   }
   // o = rs * (g - c2 - xh * c1) = fma(rs, g, fma(xh, -rs*c1, -rs*c2))
-  float a1[RW], a0[RW];
+  float2 a1[RW], a0[RW];
 #pragma unroll
   for (int q = 0; q < RW; ++q) {
-    c1[q] = warp_sum(c1[q]) * inv;
-    c2[q] = warp_sum(c2[q]) * inv;
-    a1[q] = -rs[q] * c1[q];
-    a0[q] = -rs[q] * c2[q];
+    const float m1 = warp_sum(c1[q].x + c1[q].y) * inv, m2 = warp_sum(c2[q].x + c2[q].y) * inv;
+    a1[q] = splat2(-rs2[q].x * m1);
+    a0[q] = splat2(-rs2[q].x * m2);
   }
+  const float2 sc2 = splat2(d.scale);
 #pragma unroll
   for (int c = 0; c < NC; ++c) {
     const int ch = lane + c * 32;
     if (!(FULL || ch < nch)) continue;
-    float gm[8], pz[8];
-    ld_param8<T, GF>(gamma, ch * 8, gm);
+    float2 gm[4], pz[4];
+    lds8x2(sg + ch * 8, gm);
 #pragma unroll
-    for (int k = 0; k < 8; ++k) pz[k] = 0.0f;
+    for (int k = 0; k < 4; ++k) pz[k] = make_float2(0.0f, 0.0f);
 #pragma unroll
     for (int q = 0; q < RW; ++q) {
       if (!live[q]) break;
-      float xh[8], dv[8], g[8], o[8];
+      float2 xh[4], dv[4], g[4], o[4];
       load_row(q, c, gm, xh, dv, g);
       const int64_t i = (row0 + q) * H + ch * 8;
 #pragma unroll
-      for (int k = 0; k < 8; ++k) o[k] = fmaf(rs[q], g[k], fmaf(xh[k], a1[q], a0[q]));
-      uint4 w = pack8<T>(o);
+      for (int k = 0; k < 4; ++k) o[k] = fma2(rs2[q], g[k], fma2(xh[k], a1[q], a0[q]));
+      uint4 w = pack8x2<T>(o);
       *reinterpret_cast<uint4*>(ds_o + i) = w;
       if (dx_o) {
         const uint32_t bits = d.p > 0.0f ? dropout_bits8q(d, uint64_t(i) >> 3) : 0xFFu;
 #pragma unroll
-        for (int k = 0; k < 8; ++k) o[k] = ((bits >> k) & 1u) ? o[k] * d.scale : 0.0f;
-        w = pack8<T>(o);
+        for (int k = 0; k < 4; ++k) o[k] = keep2(bits, 2 * k, mul2(o[k], sc2));
+        w = pack8x2<T>(o);
         *reinterpret_cast<uint4*>(dx_o + i) = w;
       }
       if (nparts > 2) {  // bias grad: the outgoing gradient as stored
-        float f[8];
-        unpack8<T>(w, f);
+        float2 f[4];
+        unpack8x2<T>(w, f);
 #pragma unroll
-        for (int k = 0; k < 8; ++k) pz[k] += f[k];
+        for (int k = 0; k < 4; ++k) pz[k] = add2(pz[k], f[k]);
       }
     }
     if (nparts > 2) {
       float4* o2 = reinterpret_cast<float4*>(prow + 2 * H + ch * 8);
-      o2[0] = make_float4(pz[0], pz[1], pz[2], pz[3]);
-      o2[1] = make_float4(pz[4], pz[5], pz[6], pz[7]);
+      o2[0] = make_float4(pz[0].x, pz[0].y, pz[1].x, pz[1].y);
+      o2[1] = make_float4(pz[2].x, pz[2].y, pz[3].x, pz[3].y);
     }
   }
   // warps whose rows are all past the end contribute zeros
@@ -724,7 +762,7 @@ static void b_layer_norm_dx(Plan& p) {
   const int nblk = int((rows + LNB_ROWS - 1) / LNB_ROWS);
   auto ws = std::make_shared<Scratch>(size_t(nblk) * np * H * sizeof(float));
   const int ncs = (H + 255) / 256;
-  const size_t smem = size_t(8) * 3 * 8 * 32 * ncs * sizeof(float);  // [8 warps][3][8][NC*32]
+  const size_t smem = size_t(8) * 3 * 8 * 32 * ncs * sizeof(float) + size_t(H) * sizeof(float);  // partials + gamma
   p.nkernels = 2;
   dispatch_float(S.dtype, [&](auto* tp) {
    using T = std::remove_pointer_t<decltype(tp)>;
@@ -732,7 +770,7 @@ static void b_layer_norm_dx(Plan& p) {
     constexpr int NC = decltype(nc)::value;
     static std::once_flag once;
     std::call_once(once, [] {
-      constexpr int sm = 8 * 3 * 8 * 32 * NC * 4;
+      constexpr int sm = 8 * 3 * 8 * 32 * NC * 4 + NC * 256 * 4;
       TCB_CUDA(cudaFuncSetAttribute(k_ln_bwd<T, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
       if constexpr (sizeof(T) == 2) {
         TCB_CUDA(cudaFuncSetAttribute(k_ln_bwd16<T, NC, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
