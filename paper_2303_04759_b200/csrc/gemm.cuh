@@ -43,6 +43,7 @@ struct GemmArgs {
   int no_tma_epi = 0;              // force the direct-store epilogue (tooling)
   const int* sched = nullptr;      // device LPT schedule of a pair launch (gemm_pair_schedule)
   int sched_rounds = 0;
+  int wsplit = 1;                  // > 1: c is a [wsplit][M][N] f32 workspace of K-slice partials
 };
 
 struct TcChoice {
@@ -60,6 +61,11 @@ void launch_gemm_tc(const GemmArgs& g, cudaStream_t s);
 void launch_gemm_tc_pair(const GemmArgs& g0, const GemmArgs& g1, cudaStream_t s);
 // host-side longest-processing-time unit schedule for a pair launch
 std::vector<int> gemm_pair_schedule(const GemmArgs& g0, const GemmArgs& g1, int* rounds);
+// K slices for problem idx of a pair (1 = none); partials then need
+// launch_wsplit_reduce into the real output
+int gemm_pair_wsplit(GemmArgs g0, GemmArgs g1, int idx);
+bool gemm_wsplit_ok(const GemmArgs& g, int S);
+void launch_wsplit_reduce(const float* ws, float* out, int64_t n, int S, cudaStream_t s);
 // cost-model choice of tile shape / CTA pairing / split-K for a problem
 TcChoice gemm_tc_choose(const GemmArgs& g);
 // plan-time: freeze the tile choice and allocate split-K scratch (no-op for the

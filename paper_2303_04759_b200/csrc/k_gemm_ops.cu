@@ -150,8 +150,26 @@ static void b_matmul_pair(Plan& p) {
   g0.force_cg = g1.force_cg = int(p.attrs.i("tc_cg", 0));
   const bool exact = want_exact(p) || p.in[n0].dtype != TCB_BF16;
   p.nkernels = exact ? 2 : 1;
-  std::shared_ptr<Scratch> sched;
+  std::shared_ptr<Scratch> sched, wsbuf;
+  int ws_idx = -1, ws_s = 1;
   if (!exact && !p.attrs.i("static_rr", 0)) {
+    // a weight gradient with few long tiles is cut along K into slices
+    // (partials in a plan-owned workspace, reduced in slice order afterwards)
+    const int forced = int(p.attrs.i("wsplit", 0));  // tests / tuning (1 disables)
+    for (int i = 0; i < 2 && ws_s == 1; ++i) {
+      const GemmArgs& g = i ? g1 : g0;
+      const int sp = forced ? forced : gemm_pair_wsplit(g0, g1, i);
+      if (sp > 1 && gemm_wsplit_ok(g, sp)) {
+        ws_idx = i;
+        ws_s = sp;
+      }
+    }
+    if (ws_s > 1) {
+      GemmArgs& g = ws_idx ? g1 : g0;
+      g.wsplit = ws_s;
+      wsbuf = std::make_shared<Scratch>(size_t(ws_s) * size_t(g.M) * size_t(g.N) * sizeof(float));
+      p.nkernels = 2;
+    }
     int rounds = 0;
     std::vector<int> table = gemm_pair_schedule(g0, g1, &rounds);
     sched = std::make_shared<Scratch>(table.size() * sizeof(int));
@@ -159,7 +177,8 @@ static void b_matmul_pair(Plan& p) {
     g0.sched = static_cast<const int*>(sched->p);
     g0.sched_rounds = rounds;
   }
-  p.run = [g0, g1, exact, n0, sched](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) mutable {
+  p.run = [g0, g1, exact, n0, sched, wsbuf, ws_idx, ws_s](const tcb_tensor* in, tcb_tensor* out,
+                                                          cudaStream_t s) mutable {
     g0.a.ptr = in[0].ptr;
     g0.b.ptr = in[1].ptr;
     if (n0 == 3) g0.aux = in[2].ptr;
@@ -168,8 +187,15 @@ static void b_matmul_pair(Plan& p) {
     g1.b.ptr = in[n0 + 1].ptr;
     g1.c = out[1].ptr;
     if (!exact && gemm_tc_supported(g0, nullptr) && gemm_tc_supported(g1, nullptr)) {
+      if (ws_s > 1) (ws_idx ? g1 : g0).c = wsbuf->p;
       launch_gemm_tc_pair(g0, g1, s);
+      if (ws_s > 1) {
+        const GemmArgs& g = ws_idx ? g1 : g0;
+        launch_wsplit_reduce(static_cast<const float*>(wsbuf->p), static_cast<float*>(out[ws_idx].ptr), g.M * g.N,
+                             ws_s, s);
+      }
     } else {
+      g0.wsplit = g1.wsplit = 1;
       launch_gemm(g0, exact, s);
       launch_gemm(g1, exact, s);
     }

@@ -66,6 +66,11 @@ struct TcProb {
   int m_blocks, n_blocks, k_blocks;  // m_blocks counts (128*CG)-row blocks
   int64_t num_tiles;
   int kps;  // k-blocks per K split
+  // > 1: the problem's K is cut into wsplit slices run as separate units; unit
+  // (s, tile) accumulates k-blocks [s*kps, +kps) and stores its f32 partial tile
+  // to slice s of a [wsplit][M][N] workspace (C map Z2 = wsplit), which a fixed-
+  // order reduction kernel sums afterwards (deterministic)
+  int wsplit;
   uint32_t idesc;
   // epilogue
   void* c;
@@ -338,10 +343,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const CUtensorMap* mA = prob ? &tmA1 : &tmA0;
         const CUtensorMap* mB = prob ? &tmB1 : &tmB0;
         const int64_t t = u - (prob ? P.pr[0].num_tiles : 0);
-        const int kb0 = split * Q.kps;
-        const int kb1 = min(kb0 + Q.kps, Q.k_blocks);
         int z, mb, nb;
         decode_tile(Q, t, z, mb, nb);
+        const int kb0 = (Q.wsplit > 1 ? z : split) * Q.kps;
+        const int kb1 = min(kb0 + Q.kps, Q.k_blocks);
+        if (Q.wsplit > 1) z = 0;  // z is the K slice, not a batch index
         const int z1 = int(z / Q.Z2), z2 = int(z % Q.Z2);
         const int m0 = mb * (TC_BM * CG) + int(rank) * TC_BM;
         const int n0 = nb * BN + int(rank) * C::B_ROWS;
@@ -381,8 +387,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       int acc = 0;
       uint32_t acc_phase = 0;
       for (int64_t ui = 0, u; (u = unit_at(P, cl_id, n_cl, ui)) >= 0; ++ui) {
-        const TcProb& Q = P.pr[unit_prob(P, u)];
-        const int kb0 = split * Q.kps;
+        const int prob = unit_prob(P, u);
+        const TcProb& Q = P.pr[prob];
+        int kb0 = split * Q.kps;
+        if (Q.wsplit > 1) {
+          int z, mb, nb;
+          decode_tile(Q, u - (prob ? P.pr[0].num_tiles : 0), z, mb, nb);
+          kb0 = z * Q.kps;
+        }
         const int kb1 = min(kb0 + Q.kps, Q.k_blocks);
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
@@ -486,7 +498,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const int64_t t = u - (prob ? P.pr[0].num_tiles : 0);
       int z, mb, nb;
       decode_tile(Q, t, z, mb, nb);
-      const int z1 = int(z / Q.Z2), z2 = int(z % Q.Z2);
+      const int z1 = Q.wsplit > 1 ? 0 : int(z / Q.Z2), z2 = Q.wsplit > 1 ? z : int(z % Q.Z2);
       const int64_t coff = int64_t(z1) * Q.c_s1 + int64_t(z2) * Q.c_s2;
       const int mrow0 = mb * (TC_BM * CG) + int(rank) * TC_BM + q * 32;  // this warp's 32-row box
       const int64_t m = int64_t(mrow0) + lane;
@@ -707,13 +719,14 @@ static void fill_prob(const GemmArgs& g, int splits, TcProb& P, CUtensorMap& ta,
   P.m_blocks = int((g.M + TC_BM * CG - 1) / (TC_BM * CG));
   P.n_blocks = int((g.N + BN - 1) / BN);
   P.k_blocks = int((g.K + TC_BK - 1) / TC_BK);
-  P.num_tiles = int64_t(P.m_blocks) * P.n_blocks * g.Z;
-  P.kps = (P.k_blocks + splits - 1) / splits;
+  P.wsplit = g.wsplit > 1 ? g.wsplit : 1;
+  P.num_tiles = int64_t(P.m_blocks) * P.n_blocks * g.Z * P.wsplit;
+  P.kps = (P.k_blocks + splits * P.wsplit - 1) / (splits * P.wsplit);
   P.idesc = umma_idesc(TC_BM * CG, BN, g.a.dtype == TCB_BF16, g.ta != 0, g.tb == 0);
   P.c = g.c;
   P.ldc = g.ldc;
   P.c_s1 = g.c_s1;
-  P.c_s2 = g.c_s2;
+  P.c_s2 = P.wsplit > 1 ? g.M * g.ldc : g.c_s2;  // workspace slices
   P.c_dtype = g.c_dtype;
   P.alpha = g.alpha;
   P.bias = g.bias;
@@ -740,7 +753,10 @@ static void fill_prob(const GemmArgs& g, int splits, TcProb& P, CUtensorMap& ta,
                                : CU_TENSOR_MAP_SWIZZLE_32B;
     };
     const CUtensorMapSwizzle csw = sw(TC_EW * dtype_bytes(g.c_dtype));
-    em.c = encode4(g.c, g.c_dtype, g.N, g.M, g.Z2, Z1, g.ldc, g.c_s2, g.c_s1, TC_EW, 32, csw);
+    if (P.wsplit > 1)
+      em.c = encode4(g.c, g.c_dtype, g.N, g.M, P.wsplit, 1, g.ldc, g.M * g.ldc, 0, TC_EW, 32, csw);
+    else
+      em.c = encode4(g.c, g.c_dtype, g.N, g.M, g.Z2, Z1, g.ldc, g.c_s2, g.c_s1, TC_EW, 32, csw);
     if (g.aux_out) em.u = encode4(g.aux_out, g.c_dtype, g.N, g.M, g.Z2, Z1, g.ldc, g.c_s2, g.c_s1, TC_EW, 32, csw);
     if (g.dact != ACT_NONE)
       em.aux = encode4(g.aux, g.aux_dtype, g.N, g.M, g.Z2, Z1, g.ldc, g.c_s2, g.c_s1, TC_EW, 32, sw(TC_EW * 2));
@@ -914,15 +930,17 @@ void launch_gemm_tc_pair(const GemmArgs& g0, const GemmArgs& g1, cudaStream_t s)
 // plus an epilogue weight (GELU / act' epilogues cost more), every unit goes to
 // the least-loaded cluster, largest first.  Returns the [rounds][clusters]
 // table (-1 = done) the kernel walks; deterministic (ties by index).
-std::vector<int> gemm_pair_schedule(const GemmArgs& g0, const GemmArgs& g1, int* rounds) {
+static std::vector<int> lpt_table(const GemmArgs& g0, const GemmArgs& g1, int* rounds, double* max_load) {
   const TcChoice c = pair_choice(g0, g1);
   const bool swap = g1.K > g0.K;
   const GemmArgs* gs[2] = {swap ? &g1 : &g0, swap ? &g0 : &g1};
   std::vector<std::pair<double, int>> units;
   int64_t base = 0;
   for (const GemmArgs* g : gs) {
-    const int64_t tiles = ((g->M + 128 * c.cg - 1) / (128 * c.cg)) * ((g->N + c.bn - 1) / c.bn) * g->Z;
-    const double kb = double((g->K + TC_BK - 1) / TC_BK);
+    const int ws = g->wsplit > 1 ? g->wsplit : 1;
+    const int64_t tiles = ((g->M + 128 * c.cg - 1) / (128 * c.cg)) * ((g->N + c.bn - 1) / c.bn) * g->Z * ws;
+    const int64_t kbt = (g->K + TC_BK - 1) / TC_BK;
+    const double kb = double((kbt + ws - 1) / ws);
     const double epi = (g->dact != ACT_NONE || g->act == ACT_GELU) ? 6.0 : 2.0;
     for (int64_t t = 0; t < tiles; ++t) units.push_back({kb + epi, int(base + t)});
     base += tiles;
@@ -947,7 +965,67 @@ std::vector<int> gemm_pair_schedule(const GemmArgs& g0, const GemmArgs& g1, int*
   for (int k = 0; k < ncl; ++k)
     for (size_t i = 0; i < lists[k].size(); ++i) table[i * ncl + k] = lists[k][i];
   *rounds = r;
+  if (max_load) *max_load = *std::max_element(load.begin(), load.end());
   return table;
+}
+std::vector<int> gemm_pair_schedule(const GemmArgs& g0, const GemmArgs& g1, int* rounds) {
+  return lpt_table(g0, g1, rounds, nullptr);
+}
+
+// K slices for problem `idx` of a pair (a weight gradient whose few long tiles
+// bound the launch): the S in {1, 2, 4, 8} minimising the LPT makespan plus
+// the slice reduction (its launch and (S+1) f32 passes over M x N, in k-block
+// units of ~0.34 us).  Only plain f32 outputs with no epilogue work qualify.
+bool gemm_wsplit_ok(const GemmArgs& g, int S) {
+  const int64_t kbt = (g.K + TC_BK - 1) / TC_BK;
+  const int64_t kps = (kbt + S - 1) / S;
+  return S >= 1 && S <= 16 && (S - 1) * kps < kbt && g.c_dtype == TCB_F32 && !g.bias && g.act == ACT_NONE &&
+         g.dact == ACT_NONE && !g.aux_out && g.Z == 1 && g.ldc == g.N && g.alpha == 1.0f;
+}
+int gemm_pair_wsplit(GemmArgs g0, GemmArgs g1, int idx) {
+  GemmArgs& g = idx ? g1 : g0;
+  const int64_t kbt = (g.K + TC_BK - 1) / TC_BK;
+  if (!gemm_wsplit_ok(g, 1) || kbt < 16) return 1;
+  int best_s = 1;
+  double best = 1e30;
+  for (int S : {1, 2, 4, 8}) {
+    if (kbt / S < 4 || !gemm_wsplit_ok(g, S)) break;
+    g.wsplit = S;
+    int r = 0;
+    double ml = 0.0;
+    lpt_table(g0, g1, &r, &ml);
+    const double red = S > 1 ? (2.0 + double(S + 1) * double(g.M * g.N) * 4.0 / 5e6) / 0.34 : 0.0;
+    if (ml + red < best * 0.95) {
+      best = ml + red;
+      best_s = S;
+    }
+  }
+  return best_s;
+}
+
+// out = sum_s ws[s] in slice order (deterministic), float4 vectorised
+__global__ void k_wsplit_reduce(const float* __restrict__ ws, float* __restrict__ out, int64_t n, int S) {
+  TCB_PDL_ENTRY();
+  const int64_t n4 = n / 4, stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n4; i += stride) {
+    float4 acc = reinterpret_cast<const float4*>(ws)[i];
+    for (int s = 1; s < S; ++s) {
+      const float4 v = reinterpret_cast<const float4*>(ws + s * n)[i];
+      acc.x += v.x;
+      acc.y += v.y;
+      acc.z += v.z;
+      acc.w += v.w;
+    }
+    reinterpret_cast<float4*>(out)[i] = acc;
+  }
+  for (int64_t i = n4 * 4 + blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += stride) {
+    float acc = ws[i];
+    for (int s = 1; s < S; ++s) acc += ws[s * n + i];
+    out[i] = acc;
+  }
+}
+void launch_wsplit_reduce(const float* ws, float* out, int64_t n, int S, cudaStream_t s) {
+  launch_k(k_wsplit_reduce, grid_for((n + 3) / 4, 256, kNumSMs * 4), 256, 0, s, ws, out, n, S);
 }
 
 }  // namespace tcb
