@@ -433,12 +433,13 @@ static void gemm_acc(const float* A, const float* B, float* C, int64_t M, int64_
   free(Bt);
 }
 
-enum { ACT_NONE = 0, ACT_RELU = 1, ACT_TANH = 2, ACT_GELU = 3 };
+enum { ACT_NONE = 0, ACT_RELU = 1, ACT_TANH = 2, ACT_GELU = 3, ACT_DERIV = 4 };
 static int parse_act(const char* s) {
   if (!s || !*s || !strcmp(s, "none")) return ACT_NONE;
   if (!strcmp(s, "relu")) return ACT_RELU;
   if (!strcmp(s, "tanh")) return ACT_TANH;
   if (!strcmp(s, "gelu")) return ACT_GELU;
+  if (!strcmp(s, "deriv")) return ACT_DERIV;
   return -1;
 }
 static inline float act_f(int act, float v) {
@@ -456,6 +457,16 @@ static inline float dact_f(int act, float aux) {
     case ACT_RELU: return aux > 0.0f ? 1.0f : 0.0f;
     case ACT_TANH: return 1.0f - aux * aux;
     case ACT_GELU: return gelu_grad_f(aux);
+    case ACT_DERIV: return aux; /* aux already holds act'(u) (linear save=grad) */
+    default: return 1.0f;
+  }
+}
+/* act'(u) from the pre-activation: what linear(save=grad) stores as u */
+static inline float deriv_of_preact(int act, float u) {
+  switch (act) {
+    case ACT_RELU: return u > 0.0f ? 1.0f : 0.0f;
+    case ACT_TANH: { float y = tanhf(u); return 1.0f - y * y; }
+    case ACT_GELU: return gelu_grad_f(u);
     default: return 1.0f;
   }
 }
@@ -923,11 +934,13 @@ int orc_exec(const char* op, const orc_tensor* in, int nin, orc_tensor* out, int
   }
   /* linear: act(x . W + bias) -- matmul_add_act (backends.hpp:311-324) with the
    * gelu extension; one rounding at the end; tw reads W stored [N,K].
-   * Outputs (y) or (y, u) where u is the rounded pre-activation. */
+   * Outputs (y) or (y, u) where u is the rounded pre-activation, or with
+   * save=grad the rounded derivative act'(pre-activation). */
   if (!strcmp(op, "linear")) {
     NEED(3, 1);
     int act = parse_act(astr(A, na, "act", "none"));
     if (act < 0) return fail("linear: bad act");
+    const int save_grad = !strcmp(astr(A, na, "save", "preact"), "grad");
     int tw = (int)aint(A, na, "tw", 0);
     int64_t M = in[0].shape[0], K = in[0].shape[1];
     int64_t N = tw ? in[1].shape[0] : in[1].shape[1];
@@ -935,7 +948,7 @@ int orc_exec(const char* op, const orc_tensor* in, int nin, orc_tensor* out, int
     for (int64_t i = 0; i < M; ++i)
       for (int64_t j = 0; j < N; ++j) {
         float v = F(&out[0])[i * N + j] + F(&in[2])[j];
-        if (nout > 1) F(&out[1])[i * N + j] = rnd(out[1].dtype, v);
+        if (nout > 1) F(&out[1])[i * N + j] = rnd(out[1].dtype, save_grad ? deriv_of_preact(act, v) : v);
         F(&out[0])[i * N + j] = rnd(out[0].dtype, act_f(act, v));
       }
     return 0;

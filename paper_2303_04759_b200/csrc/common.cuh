@@ -177,9 +177,12 @@ __device__ __forceinline__ float fast_gelu_grad(float x) {
   return fmaf(x * 0.39894228040143268f, e, phi);
 }
 
-enum Act { ACT_NONE = 0, ACT_RELU = 1, ACT_TANH = 2, ACT_GELU = 3 };
+// ACT_DERIV: the aux operand already holds act'(u) (a forward epilogue saved
+// the derivative instead of the pre-activation), so act'(aux) = aux
+enum Act { ACT_NONE = 0, ACT_RELU = 1, ACT_TANH = 2, ACT_GELU = 3, ACT_DERIV = 4 };
 inline int parse_act(const std::string& s) {
   if (s.empty() || s == "none") return ACT_NONE;
+  if (s == "deriv") return ACT_DERIV;
   if (s == "relu") return ACT_RELU;
   if (s == "tanh") return ACT_TANH;
   if (s == "gelu") return ACT_GELU;
@@ -193,11 +196,24 @@ __device__ __forceinline__ float act_f(int act, float v) {
     default: return v;
   }
 }
+// act'(u) from the pre-activation u (what a save_grad epilogue stores)
+__device__ __forceinline__ float deriv_of_preact(int act, float u) {
+  switch (act) {
+    case ACT_RELU: return u > 0.0f ? 1.0f : 0.0f;
+    case ACT_TANH: {
+      const float y = tanhf(u);
+      return __fsub_rn(1.0f, __fmul_rn(y, y));
+    }
+    case ACT_GELU: return gelu_grad_f(u);
+    default: return 1.0f;
+  }
+}
 __device__ __forceinline__ float dact_f(int act, float aux) {
   switch (act) {
     case ACT_RELU: return aux > 0.0f ? 1.0f : 0.0f;
     case ACT_TANH: return __fsub_rn(1.0f, __fmul_rn(aux, aux));
     case ACT_GELU: return gelu_grad_f(aux);
+    case ACT_DERIV: return aux;
     default: return 1.0f;
   }
 }

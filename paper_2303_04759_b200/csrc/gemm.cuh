@@ -37,6 +37,7 @@ struct GemmArgs {
   const void* aux = nullptr;   // same layout as C (ldc, batch strides), aux_dtype
   int aux_dtype = TCB_F32;
   void* aux_out = nullptr;     // pre-activation store, same layout/dtype as C
+  int save_grad = 0;           // aux_out holds act'(pre-activation) instead (consumed with ACT_DERIV)
   int force_bn = 0, force_cg = 0;  // tcgen05 tile override (tests / tuning); 0 = cost model
   int force_splits = 0;            // split-K ways (cluster of CG x splits CTAs, DSMEM reduction)
   void* trace = nullptr;           // optional per-CTA timeline buffer (12 x u64 per CTA, tooling)

@@ -66,7 +66,7 @@ __global__ void __launch_bounds__(XT* XT) k_gemm_exact(GemmArgs g) {
   if (g.bias) v = __fadd_rn(v, ld_g(g.bias, g.bias_dtype, n));
   const int64_t ci = offc + m * g.ldc + n;
   if (g.dact != ACT_NONE) v = __fmul_rn(v, dact_f(g.dact, ld_g(g.aux, g.aux_dtype, ci)));
-  if (g.aux_out) st_g(g.aux_out, g.c_dtype, ci, v);
+  if (g.aux_out) st_g(g.aux_out, g.c_dtype, ci, g.save_grad ? deriv_of_preact(g.act, v) : v);
   if (g.act != ACT_NONE) v = act_f(g.act, v);
   st_g(g.c, g.c_dtype, ci, v);
 }

@@ -96,6 +96,11 @@ static void b_linear(Plan& p) {
                                 "linear: pre-activation output must match y");
   const bool exact = want_exact(p);
   const bool save = p.out.size() > 1;
+  // save=grad: the second output is act'(u) (the backward then multiplies by it)
+  const std::string what = p.attrs.s("save", "preact");
+  require(what == "preact" || what == "grad", "linear: save must be preact or grad");
+  g.save_grad = what == "grad" ? 1 : 0;
+  if (g.save_grad) require(save && g.act != ACT_NONE, "linear: save=grad needs an activation and two outputs");
   auto keep = std::make_shared<GemmWs>();
   gemm_prepare(g, exact, *keep);
   p.run = [g, exact, save, keep](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) mutable {

@@ -83,6 +83,7 @@ struct TcProb {
   const void* aux;
   int aux_dtype;
   void* aux_out;
+  int save_grad;  // aux_out = act'(pre-activation)
   int tma_epi;   // 1: smem + TMA-store epilogue (tensor maps valid); 0: direct stores
   int c_vec_ok;  // direct path: 16-byte aligned rows
 };
@@ -166,8 +167,39 @@ __device__ __forceinline__ void apply_dact(int act, float (&v)[W], const float (
 #pragma unroll
       for (int j = 0; j < W; ++j) v[j] *= fast_gelu_grad(a[j]);
       break;
+    case ACT_DERIV:
+#pragma unroll
+      for (int j = 0; j < W; ++j) v[j] *= a[j];
+      break;
     default:
       break;
+  }
+}
+// y = act(v) in place and d = act'(v) (save_grad epilogue); GELU shares one
+// Phi / exp evaluation between the two
+template <int W>
+__device__ __forceinline__ void act_and_deriv(int act, float (&v)[W], float (&d)[W]) {
+  if (act == ACT_GELU) {
+#pragma unroll
+    for (int j = 0; j < W; ++j) {
+      float phi, e;
+      fast_phi(v[j], phi, e);
+      d[j] = fmaf(v[j] * 0.39894228040143268f, e, phi);
+      v[j] *= phi;
+    }
+    return;
+  }
+#pragma unroll
+  for (int j = 0; j < W; ++j) {
+    if (act == ACT_TANH) {
+      v[j] = tanhf(v[j]);
+      d[j] = __fsub_rn(1.0f, __fmul_rn(v[j], v[j]));
+    } else if (act == ACT_RELU) {
+      d[j] = v[j] > 0.0f ? 1.0f : 0.0f;
+      v[j] = v[j] > 0.0f ? v[j] : 0.0f;
+    } else {
+      d[j] = 1.0f;
+    }
   }
 }
 
@@ -533,8 +565,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           uint8_t* slot = slots + sidx * TC_SLOT;
           if (lane == 0) bulk_wait_read<OUT_RING - 1>();  // the store that last used this slot has read it
           __syncwarp();
-          if (Q.aux_out) stage_row<W>(slot + TC_SLOT / 2, lane, Q.c_dtype, v);
-          apply_act<W>(Q.act, v);
+          if (Q.save_grad) {
+            float dv[W];
+            act_and_deriv<W>(Q.act, v, dv);
+            stage_row<W>(slot + TC_SLOT / 2, lane, Q.c_dtype, dv);
+          } else {
+            if (Q.aux_out) stage_row<W>(slot + TC_SLOT / 2, lane, Q.c_dtype, v);
+            apply_act<W>(Q.act, v);
+          }
           stage_row<W>(slot, lane, Q.c_dtype, v);
           fence_proxy_async();
           __syncwarp();
@@ -553,8 +591,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             for (int j = 0; j < W; ++j) a[j] = j < nvalid ? ld_e(Q.aux, Q.aux_dtype, base + j) : 0.0f;
             apply_dact<W>(Q.dact, v, a);
           }
-          if (Q.aux_out) store_row<W>(Q.aux_out, Q.c_dtype, base, v, nvalid);
-          apply_act<W>(Q.act, v);
+          if (Q.save_grad) {
+            float dv[W];
+            act_and_deriv<W>(Q.act, v, dv);
+            store_row<W>(Q.aux_out, Q.c_dtype, base, dv, nvalid);
+          } else {
+            if (Q.aux_out) store_row<W>(Q.aux_out, Q.c_dtype, base, v, nvalid);
+            apply_act<W>(Q.act, v);
+          }
           store_row<W>(Q.c, Q.c_dtype, base, v, nvalid);
         }
       };
@@ -736,6 +780,7 @@ static void fill_prob(const GemmArgs& g, int splits, TcProb& P, CUtensorMap& ta,
   P.aux = g.aux;
   P.aux_dtype = g.aux_dtype;
   P.aux_out = g.aux_out;
+  P.save_grad = g.aux_out ? g.save_grad : 0;
   const int es = dtype_bytes(g.c_dtype);
   P.c_vec_ok = (reinterpret_cast<uintptr_t>(g.c) % 16 == 0) && ((g.ldc * es) % 16 == 0) &&
                ((g.c_s1 * es) % 16 == 0) && ((g.c_s2 * es) % 16 == 0) &&

@@ -230,7 +230,10 @@ inline void register_default_adjoints() {
       } else {
         if (!c.let.var->ty.is_tuple()) throw NonDifferentiable("linear(act=" + act + ") needs save_preact=1");
         VarPtr u = c.g.get(c.let.var, 1);
-        du = act == "gelu" ? c.g.op("gelu_dx", {u, dy}) : c.g.op("mul", {dy, c.g.op("gtz", {u})});
+        if (ir::attr_string(at, "save", "preact") == "grad")  // u already holds act'(pre-activation)
+          du = c.g.op("mul", {dy, u});
+        else
+          du = act == "gelu" ? c.g.op("gelu_dx", {u, dy}) : c.g.op("mul", {dy, c.g.op("gtz", {u})});
       }
     }
     VarPtr dx = c.g.op("matmul_t", {du, w}, {{"tb", std::int64_t(tw ? 0 : 1)}});
@@ -531,6 +534,30 @@ inline FusionStats fuse(LetSeq& s, bool patterns = true) {
         ++st.dact;
         continue;
       }
+    }
+    // 1b. mul(matmul_t(a, b), d) with d = act'(u) saved by linear(save=grad)
+    //     -> matmul_dact(a, b, d, act=deriv)   (same shape, no broadcast)
+    if (op == "mul" && b.value->args.size() == 2) {
+      bool done = false;
+      for (int side = 0; side < 2 && !done; ++side) {
+        auto src = arg_var(b.value, side), other = arg_var(b.value, 1 - side);
+        auto* p = producer(src);
+        if (!p || !other || p->value->op != "matmul_t" || !single(src) ||
+            ir::attr_double(p->value->call_attrs, "alpha", 1.0) != 1.0 || p->value->call_attrs.count("out"))
+          continue;
+        if (src->ty.is_tuple() || other->ty.is_tuple() || b.var->ty.is_tuple()) continue;
+        const auto &ts = src->ty.tensor(), &to = other->ty.tensor(), &tr = b.var->ty.tensor();
+        if (ts.shape != to.shape || ts.dtype != to.dtype || tr.shape != ts.shape || tr.dtype != ts.dtype) continue;
+        AttrMap at = pick(p->value->call_attrs, {"ta", "tb"});
+        at["act"] = std::string("deriv");
+        auto call = ir::call("matmul_dact", {p->value->args[0], p->value->args[1], b.value->args[1 - side]}, at);
+        call->ty = b.value->ty;
+        b.value = call;
+        removed.insert(def[src.get()]);
+        ++st.dact;
+        done = true;
+      }
+      if (done) continue;
     }
     // 2. layer_norm_dx(s, g, m, r, add(a, b)) -> layer_norm_dx(s, g, m, r, a, b)
     if (op == "layer_norm_dx" && b.value->args.size() == 5) {

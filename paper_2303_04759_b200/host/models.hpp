@@ -30,6 +30,7 @@ struct ModelCfg {
   int64_t world = 1;        // ZeRO-1 data-parallel ranks
   double ln_eps = 1e-12;
   int fuse = 1;             // run the fusion pass
+  int save_deriv = 1;       // act linears save act'(u) for the backward instead of u
   int64_t vocab_pad() const { return ((V + 63) / 64) * 64; }
   int64_t T() const { return B * S; }
   int64_t positions() const { return max_pos ? max_pos : (kind == "bert" ? std::max<int64_t>(512, S) : S); }
@@ -67,6 +68,7 @@ inline ModelCfg parse_cfg(const std::string& s) {
     else if (k == "world") c.world = I();
     else if (k == "ln_eps") c.ln_eps = D();
     else if (k == "fuse") c.fuse = int(I());
+    else if (k == "save_deriv") c.save_deriv = int(I());
     else throw Error("unknown model config key '" + k + "'");
   }
   if (c.H % c.A) throw TypeError("H must be divisible by A");
@@ -227,7 +229,12 @@ inline TrainStep build_train_step(const ModelCfg& c) {
                     int tw = 0) {
     AttrMap a{{"act", actf}};
     if (tw) a["tw"] = std::int64_t(1);
-    if (actf == "gelu" || actf == "relu") a["save_preact"] = std::int64_t(1);
+    // the forward epilogue saves act'(u) (not u): the backward's dgrad epilogue
+    // then multiplies by it instead of re-evaluating the derivative
+    if (actf == "gelu" || actf == "relu") {
+      a["save_preact"] = std::int64_t(1);
+      if (c.save_deriv) a["save"] = std::string("grad");
+    }
     VarPtr y = g.op("linear", {x, W[w], W[b]}, a);
     return y->ty.is_tuple() ? g.get(y, 0) : y;
   };

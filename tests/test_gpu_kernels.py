@@ -239,6 +239,26 @@ def test_matmul_pair(dact, tile):
     assert rel_err(g[1], o[1]) < 1e-5, rel_err(g[1], o[1])
 
 
+@pytest.mark.parametrize("act", ["gelu", "relu"])
+@pytest.mark.parametrize("tile", [(256, 2), (128, 1), None])
+def test_linear_save_grad_and_deriv_dact(act, tile):
+    """linear(save=grad) stores act'(pre-activation) as its second output; the
+    backward's matmul_dact(act=deriv) multiplies by it (both against the
+    oracle); ragged shapes exercise the direct-store fallback too."""
+    m, k, n = 700, 256, 600
+    x, w, bias = rn(m, k), rn(k, n, lo=-0.1, hi=0.1), rn(n)
+    at = {"act": act, "save": "grad"}
+    if tile:
+        at.update({"tc_bn": tile[0], "tc_cg": tile[1]})
+    g, o = run_both("linear", [(x, BF16), (w, BF16), (bias, F32)], [((m, n), BF16), ((m, n), BF16)], at)
+    assert rel_err(g[0], o[0]) < BF16_TOL and rel_err(g[1], o[1]) < BF16_TOL
+    d = o[1]
+    dy, w2 = rn(m, 320), rn(n, 320)
+    at2 = {"tb": 1, "act": "deriv", **({"tc_bn": tile[0], "tc_cg": tile[1]} if tile else {})}
+    g, o = run_both("matmul_dact", [(dy, BF16), (w2, BF16), (d, BF16)], [((m, n), BF16)], at2)
+    assert rel_err(g[0], o[0]) < BF16_TOL
+
+
 @pytest.mark.parametrize("wsplit", [2, 3, 4])
 @pytest.mark.parametrize("dact", [0, 1])
 def test_matmul_pair_wsplit(wsplit, dact):
