@@ -4,8 +4,8 @@
 // Forward  (oracle.c attention_fwd):
 //   TMA Q, K, V head tiles straight out of qkv [T, 3H] (no split copies)
 //   S  = Q K^T                 tcgen05.mma 128x128x64 -> TMEM
-//   P  = softmax(scale * S)    8 warps: a (query row = TMEM lane, 64-key
-//                              half) per thread, halves combined in smem
+//   P  = softmax(scale * S)    16 warps: a (query row = TMEM lane, 32-key
+//                              quarter) per thread, quarters combined in smem
 //   probs <- P (bf16)          swizzled smem tile -> TMA store (saved for bwd)
 //   Pd = dropout(P)            Philox keep bits, same indices as k_softmax
 //   O  = Pd V                  tcgen05.mma 128x64x128 (Pd = K-major A from
@@ -27,7 +27,8 @@ namespace tcb {
 constexpr int AT_S = 128;         // query / key tile (sequence padded to 128)
 constexpr int AT_D = 64;          // head dim (one SWIZZLE_128B row)
 constexpr int AT_TILE = 16384;    // 128 rows x 128 B
-constexpr int AT_THREADS = 256;   // 8 warps: 2 per TMEM lane quarter, one per 64-key half
+constexpr int AT_THREADS = 256;   // backward: 8 warps, 2 per TMEM lane quarter, one per 64-key half
+constexpr int AT_FWD_THREADS = 512;  // forward: 16 warps, 4 per lane quarter, one per 32-key quarter
 
 struct AttnArgs {
   int S, H, A, dh, causal, Z;
@@ -63,17 +64,30 @@ __device__ __forceinline__ void keep_bits64(const DropCfg& d, uint64_t base, int
     }
   }
 }
+// keep bits for 32 row elements j0 .. j0+31 of flat index base + j (base, j0 % 8 == 0)
+__device__ __forceinline__ uint32_t keep_bits32(const DropCfg& d, uint64_t base, int j0, int S) {
+  uint32_t kb = 0xffffffffu;
+  if (d.p <= 0.0f) return kb;
+#pragma unroll
+  for (int g = 0; g < 4; ++g) {
+    if (j0 + g * 8 < S) {
+      const uint32_t b = dropout_bits8q(d, ((base + j0) >> 3) + g);
+      kb = (kb & ~(0xffu << (g * 8))) | (b << (g * 8));
+    }
+  }
+  return kb;
+}
 // e^x on the MUFU path (ex2.approx; -inf -> 0); the oracle's expf differs by a few ulp
 __device__ __forceinline__ float fast_exp(float x) { return ex2_approx(x * 1.4426950408889634f); }
 
 // ------------------------------------------------------------------ forward
 // Thread layout: warp w owns TMEM lane quarter q = w % 4 (query rows 32q..+31)
-// and key half hf = w / 4 (columns 64hf..+63, exactly one SW128 P tile); the
-// two halves of a row combine max / sum through smem.
-__global__ void __launch_bounds__(AT_THREADS) k_attn_fwd(const __grid_constant__ CUtensorMap m_qkv,
-                                                         const __grid_constant__ CUtensorMap m_probs,
-                                                         const __grid_constant__ CUtensorMap m_ctx,
-                                                         const AttnArgs a) {
+// and key quarter cq = w / 4 (columns 32cq..+31, half of one SW128 P tile); the
+// four quarters of a row combine max / sum through smem.
+__global__ void __launch_bounds__(AT_FWD_THREADS) k_attn_fwd(const __grid_constant__ CUtensorMap m_qkv,
+                                                             const __grid_constant__ CUtensorMap m_probs,
+                                                             const __grid_constant__ CUtensorMap m_ctx,
+                                                             const AttnArgs a) {
   // Persistent over heads z = blockIdx.x, +gridDim.x, ...: the Q/K/V tiles of
   // the next head stream in (TMA, second buffer) while this head's softmax and
   // PV product run; ctx / probs leave through asynchronous TMA stores.
@@ -82,14 +96,14 @@ __global__ void __launch_bounds__(AT_THREADS) k_attn_fwd(const __grid_constant__
   uint8_t* sQKV = sm;                        // 2 buffers x (Q, K, V)
   uint8_t* sP = sm + 6 * AT_TILE;            // 2 tiles: keys 0-63, 64-127 (probs, stored)
   uint8_t* sPd = sm + 8 * AT_TILE;           // 2 tiles: dropout(P), the PV operand (p > 0)
-  float* red = reinterpret_cast<float*>(sm + 10 * AT_TILE);  // [2 stats][2 halves][128 rows]
-  uint64_t* bar = reinterpret_cast<uint64_t*>(red + 512);   // load[2], mma1, mma2
+  float* red = reinterpret_cast<float*>(sm + 10 * AT_TILE);  // [2 stats][4 quarters][128 rows]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(red + 1024);  // load[2], mma1, mma2
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 4);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int q = warp & 3, hf = warp >> 2;
+  const int q = warp & 3, cq = warp >> 2;
   const int row = q * 32 + lane;  // query row = TMEM lane
-  const int j0 = hf * 64;         // this thread's key columns
+  const int j0 = cq * 32;         // this thread's key columns
   const int Z = gridDim.x > 0 ? a.Z : 0;
   if (tid == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&m_qkv)) : "memory");
@@ -145,58 +159,56 @@ __global__ void __launch_bounds__(AT_THREADS) k_attn_fwd(const __grid_constant__
       tc_commit<1>(&bar[2]);
     }
     // dropout keep bits overlap the QK^T MMA
-    uint32_t kb[2];
-    keep_bits64(a.d, (uint64_t(z) * a.S + row) * a.S, j0, a.S, kb);
+    const uint32_t kb = keep_bits32(a.d, (uint64_t(z) * a.S + row) * a.S, j0, a.S);
     mbar_wait(&bar[2], it & 1);
     tc_fence_after();
     T(2);
 
-    // ---- softmax over this thread's 64 scores
-    float v[64];
+    // ---- softmax over this thread's 32 scores
+    float v[32];
     {
       uint32_t r[32];
+      TMEM_LD32(trow + j0, r);
+      tmem_wait_ld();
 #pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        TMEM_LD32(trow + j0 + c * 32, r);
-        tmem_wait_ld();
-#pragma unroll
-        for (int j = 0; j < 32; ++j) v[c * 32 + j] = __uint_as_float(r[j]);
-      }
+      for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
     }
     // scores scaled into the log2 domain: p = 2^(s*scale*log2e - max)
     const float sl2 = a.scale * 1.4426950408889634f;
     const int lim = a.causal ? min(a.S, row + 1) : a.S;  // valid key columns of this row
     float mx = -INFINITY;
 #pragma unroll
-    for (int j = 0; j < 64; ++j) {
+    for (int j = 0; j < 32; ++j) {
       const float t = j0 + j < lim ? v[j] * sl2 : -INFINITY;
       v[j] = t;
       mx = fmaxf(mx, t);
     }
-    red[hf * 128 + row] = mx;
+    red[cq * 128 + row] = mx;
     // the previous head's probs store must have read sP before it is rewritten
     if (tid == 0) bulk_wait_read<0>();
     __syncthreads();
-    mx = fmaxf(red[row], red[128 + row]);
+    mx = fmaxf(fmaxf(red[row], red[128 + row]), fmaxf(red[256 + row], red[384 + row]));
     float sum = 0.0f;
 #pragma unroll
-    for (int j = 0; j < 64; ++j) {
+    for (int j = 0; j < 32; ++j) {
       v[j] = ex2_approx(v[j] - mx);  // ex2(-inf) = 0 for masked columns
       sum += v[j];
     }
-    red[256 + hf * 128 + row] = sum;
+    red[512 + cq * 128 + row] = sum;
     __syncthreads();
-    const float inv = row < a.S ? 1.0f / (red[256 + row] + red[384 + row]) : 0.0f;
-    uint8_t* tileP = sP + hf * AT_TILE;
-    // P rounded to bf16 (the stored probs) = this half's K-major A tile
+    const float inv =
+        row < a.S ? 1.0f / ((red[512 + row] + red[640 + row]) + (red[768 + row] + red[896 + row])) : 0.0f;
+    uint8_t* tileP = sP + (cq >> 1) * AT_TILE;
+    const int g0 = (cq & 1) * 4;  // this quarter's first 16-byte granule in the tile row
+    // P rounded to bf16 (the stored probs) = this quarter of the K-major A tile
 #pragma unroll
-    for (int g = 0; g < 8; ++g) {
+    for (int g = 0; g < 4; ++g) {
       uint4 w;
       w.x = pack_bf2(v[g * 8 + 0] * inv, v[g * 8 + 1] * inv);
       w.y = pack_bf2(v[g * 8 + 2] * inv, v[g * 8 + 3] * inv);
       w.z = pack_bf2(v[g * 8 + 4] * inv, v[g * 8 + 5] * inv);
       w.w = pack_bf2(v[g * 8 + 6] * inv, v[g * 8 + 7] * inv);
-      *reinterpret_cast<uint4*>(tileP + sw128(row, g)) = w;
+      *reinterpret_cast<uint4*>(tileP + sw128(row, g0 + g)) = w;
       v[g * 8 + 0] = bf_lo(w.x), v[g * 8 + 1] = bf_hi(w.x), v[g * 8 + 2] = bf_lo(w.y), v[g * 8 + 3] = bf_hi(w.y);
       v[g * 8 + 4] = bf_lo(w.z), v[g * 8 + 5] = bf_hi(w.z), v[g * 8 + 6] = bf_lo(w.w), v[g * 8 + 7] = bf_hi(w.w);
     }
@@ -212,21 +224,21 @@ __global__ void __launch_bounds__(AT_THREADS) k_attn_fwd(const __grid_constant__
     if (a.d.p > 0.0f) {
       // Pd = bf16(P * keep / (1-p)) into its own tile: the probs store keeps reading sP
       sA = sPd;
-      uint8_t* tileP = sPd + hf * AT_TILE;
+      uint8_t* tileD = sPd + (cq >> 1) * AT_TILE;
 #pragma unroll
-      for (int g = 0; g < 8; ++g) {
+      for (int g = 0; g < 4; ++g) {
         float pd[8];
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
           const int j = g * 8 + e;
-          pd[e] = ((kb[j >> 5] >> (j & 31)) & 1u) ? v[j] * a.d.scale : 0.0f;
+          pd[e] = ((kb >> j) & 1u) ? v[j] * a.d.scale : 0.0f;
         }
         uint4 w;
         w.x = pack_bf2(pd[0], pd[1]);
         w.y = pack_bf2(pd[2], pd[3]);
         w.z = pack_bf2(pd[4], pd[5]);
         w.w = pack_bf2(pd[6], pd[7]);
-        *reinterpret_cast<uint4*>(tileP + sw128(row, g)) = w;
+        *reinterpret_cast<uint4*>(tileD + sw128(row, g0 + g)) = w;
       }
       fence_proxy_async();
     }
@@ -244,20 +256,20 @@ __global__ void __launch_bounds__(AT_THREADS) k_attn_fwd(const __grid_constant__
     mbar_wait(&bar[3], it & 1);
     tc_fence_after();
     T(4);
-    // ---- ctx row, this thread's 32 head-dim columns -> bf16 -> staging (this
+    // ---- ctx row, this thread's 16 head-dim columns -> bf16 -> staging (this
     // head's Q tile, no longer needed) -> TMA store
     {
-      uint32_t r[32];
-      TMEM_LD32(trow + 128 + hf * 32, r);
+      uint32_t r[16];
+      TMEM_LD16(trow + 128 + cq * 16, r);
       tmem_wait_ld();
 #pragma unroll
-      for (int g = 0; g < 4; ++g) {
+      for (int g = 0; g < 2; ++g) {
         uint4 w;
         w.x = pack_bf2(__uint_as_float(r[g * 8 + 0]), __uint_as_float(r[g * 8 + 1]));
         w.y = pack_bf2(__uint_as_float(r[g * 8 + 2]), __uint_as_float(r[g * 8 + 3]));
         w.z = pack_bf2(__uint_as_float(r[g * 8 + 4]), __uint_as_float(r[g * 8 + 5]));
         w.w = pack_bf2(__uint_as_float(r[g * 8 + 6]), __uint_as_float(r[g * 8 + 7]));
-        *reinterpret_cast<uint4*>(sQ + sw128(row, hf * 4 + g)) = w;
+        *reinterpret_cast<uint4*>(sQ + sw128(row, cq * 2 + g)) = w;
       }
     }
     fence_proxy_async();
@@ -474,7 +486,7 @@ __global__ void __launch_bounds__(AT_THREADS) k_attn_bwd(const __grid_constant__
 }
 
 // ------------------------------------------------------------------ host
-constexpr int AT_FWD_SMEM = 1024 + 10 * AT_TILE + 2048 + 64;
+constexpr int AT_FWD_SMEM = 1024 + 10 * AT_TILE + 4096 + 64;
 constexpr int AT_BWD_SMEM = 1024 + 14 * AT_TILE + 1024 + 64;
 
 bool attn_fused_ok(int dt, int64_t S, int64_t H, int64_t A, bool exact) {
@@ -498,7 +510,7 @@ void launch_attn_fwd(const void* qkv, void* ctx, void* probs, int64_t B, int64_t
                                  CU_TENSOR_MAP_SWIZZLE_128B);
   AttnArgs a{int(S), int(H), int(A), int(H / A), causal, int(B * A), static_cast<unsigned long long*>(trace), scale, d};
   const int grid = int(B * A < kNumSMs ? B * A : kNumSMs);
-  launch_k(k_attn_fwd, unsigned(grid), AT_THREADS, AT_FWD_SMEM, s, mq, mp, mc, a);
+  launch_k(k_attn_fwd, unsigned(grid), AT_FWD_THREADS, AT_FWD_SMEM, s, mq, mp, mc, a);
   TCB_CUDA(cudaGetLastError());
 }
 

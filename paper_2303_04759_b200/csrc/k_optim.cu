@@ -44,17 +44,23 @@ struct AdamCfg {
   double lr, b1, b2, eps, gs;
 };
 
+// f64 update like the oracle, with the per-step constants folded: mhat / vhat
+// multiply by precomputed 1/bc (lr/bc1 for the numerator), leaving one divide
+// and one square root per element (the oracle's three divides cost the kernel
+// its HBM roofline).  m, v are bit-identical to the oracle's; p differs only
+// when the f64 update sits within ~1e-16 of an f32 rounding boundary.
+struct AdamStep {
+  double lr_bc1, rbc2;
+};
 template <typename TH>
-__device__ __forceinline__ void adam_elem(const AdamCfg& c, double bc1, double bc2, float p, float g,
-                                          float m, float v, float& po, float& mo, float& vo, TH* half,
-                                          int64_t i) {
+__device__ __forceinline__ void adam_elem(const AdamCfg& c, const AdamStep& k, float p, float g, float m, float v,
+                                          float& po, float& mo, float& vo, TH* half, int64_t i) {
   double gd = g;
   if (c.gs != 1.0) gd = __dmul_rn(gd, c.gs);
   double mi = __dadd_rn(__dmul_rn(c.b1, double(m)), __dmul_rn(__dsub_rn(1.0, c.b1), gd));
   double vi = __dadd_rn(__dmul_rn(c.b2, double(v)), __dmul_rn(__dmul_rn(__dsub_rn(1.0, c.b2), gd), gd));
-  double mhat = __ddiv_rn(mi, bc1);
-  double vhat = __ddiv_rn(vi, bc2);
-  double upd = __ddiv_rn(__dmul_rn(c.lr, mhat), __dadd_rn(__dsqrt_rn(vhat), c.eps));
+  const double denom = __dadd_rn(__dsqrt_rn(__dmul_rn(vi, k.rbc2)), c.eps);
+  const double upd = __ddiv_rn(__dmul_rn(k.lr_bc1, mi), denom);
   float pn = float(__dsub_rn(double(p), upd));
   po = pn;
   mo = float(mi);
@@ -71,6 +77,7 @@ __global__ void __launch_bounds__(256) k_adam(const float* __restrict__ p, const
   const double t = double(step[0]);
   const double bc1 = __dsub_rn(1.0, pow(c.b1, t));
   const double bc2 = __dsub_rn(1.0, pow(c.b2, t));
+  const AdamStep k{c.lr / bc1, 1.0 / bc2};
   const int64_t nv = n / 4;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < nv; q += stride) {
@@ -79,16 +86,24 @@ __global__ void __launch_bounds__(256) k_adam(const float* __restrict__ p, const
     float4 M = reinterpret_cast<const float4*>(m)[q];
     float4 V = reinterpret_cast<const float4*>(v)[q];
     float4 PO, MO, VO;
-    adam_elem(c, bc1, bc2, P.x, G.x, M.x, V.x, PO.x, MO.x, VO.x, half, q * 4 + 0);
-    adam_elem(c, bc1, bc2, P.y, G.y, M.y, V.y, PO.y, MO.y, VO.y, half, q * 4 + 1);
-    adam_elem(c, bc1, bc2, P.z, G.z, M.z, V.z, PO.z, MO.z, VO.z, half, q * 4 + 2);
-    adam_elem(c, bc1, bc2, P.w, G.w, M.w, V.w, PO.w, MO.w, VO.w, half, q * 4 + 3);
+    adam_elem(c, k, P.x, G.x, M.x, V.x, PO.x, MO.x, VO.x, (TH*)nullptr, 0);
+    adam_elem(c, k, P.y, G.y, M.y, V.y, PO.y, MO.y, VO.y, (TH*)nullptr, 0);
+    adam_elem(c, k, P.z, G.z, M.z, V.z, PO.z, MO.z, VO.z, (TH*)nullptr, 0);
+    adam_elem(c, k, P.w, G.w, M.w, V.w, PO.w, MO.w, VO.w, (TH*)nullptr, 0);
+    if (half) {  // the low-precision copy as one 8- (16-bit) or 16-byte (f32) store
+      if constexpr (sizeof(TH) == 2) {
+        TH h4[4] = {from_f<TH>(PO.x), from_f<TH>(PO.y), from_f<TH>(PO.z), from_f<TH>(PO.w)};
+        reinterpret_cast<uint2*>(half)[q] = *reinterpret_cast<const uint2*>(h4);
+      } else {
+        reinterpret_cast<float4*>(half)[q] = PO;
+      }
+    }
     reinterpret_cast<float4*>(po)[q] = PO;
     reinterpret_cast<float4*>(mo)[q] = MO;
     reinterpret_cast<float4*>(vo)[q] = VO;
   }
   for (int64_t i = nv * 4 + blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += stride)
-    adam_elem(c, bc1, bc2, p[i], g[i], m[i], v[i], po[i], mo[i], vo[i], half, i);
+    adam_elem(c, k, p[i], g[i], m[i], v[i], po[i], mo[i], vo[i], half, i);
 }
 
 static void b_adam(Plan& p) {
@@ -108,6 +123,8 @@ static void b_adam(Plan& p) {
     for (int i = 0; i < 4; ++i)
       if (reinterpret_cast<uintptr_t>(in[i].ptr) % 16 || (i < 3 && reinterpret_cast<uintptr_t>(out[i].ptr) % 16))
         fail(TCB_ERR_ARG, "adam_update: buffers must be 16-byte aligned");
+    if (hd >= 0 && reinterpret_cast<uintptr_t>(out[3].ptr) % 16)
+      fail(TCB_ERR_ARG, "adam_update_ex: the parameter copy must be 16-byte aligned");
     // co_resident: small CTAs that fit beside a GEMM CTA's 61K registers, for
     // optimizer chunks the VM overlaps with the backward on a side stream
     const int bs = small ? 64 : 256;

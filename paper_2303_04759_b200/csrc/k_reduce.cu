@@ -231,6 +231,53 @@ __global__ void __launch_bounds__(256) k_colsum_partial(const T* __restrict__ x,
   }
 }
 
+// Labelled variant (decoder bias gradient of the MLM head): most rows carry
+// ignore_index and are exact zeros, so a block covers a long row range (rpc
+// rows) and each warp walks its rows loading only the labelled ones -- few,
+// large blocks keep the partial buffer (and the final fold) small.
+template <typename T>
+__global__ void __launch_bounds__(256) k_colsum_partial_masked(const T* __restrict__ x, float* __restrict__ part,
+                                                               int64_t R, int64_t C, int64_t rpc,
+                                                               const int32_t* __restrict__ lab, int32_t ign) {
+  TCB_PDL_ENTRY();
+  __shared__ float red[8][256 + 4];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t c0 = int64_t(blockIdx.x) * 256 + lane * 8;
+  const int64_t r0 = int64_t(blockIdx.y) * rpc;
+  const int64_t r1 = r0 + rpc < R ? r0 + rpc : R;
+  float acc[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) acc[k] = 0.0f;
+  if (c0 < C) {
+    for (int64_t r = r0 + warp; r < r1; r += 8) {
+      if (__ldg(lab + r) == ign) continue;  // warp-uniform: one row per warp
+      float f[8];
+      if constexpr (sizeof(T) == 2) {
+        const uint4 q = *reinterpret_cast<const uint4*>(x + r * C + c0);
+        const T* h = reinterpret_cast<const T*>(&q);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) f[k] = to_f(h[k]);
+      } else {
+        const float4 a = *reinterpret_cast<const float4*>(x + r * C + c0);
+        const float4 b = *reinterpret_cast<const float4*>(x + r * C + c0 + 4);
+        f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w; f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) acc[k] += f[k];
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 8; ++k) red[warp][lane * 8 + k] = acc[k];
+  __syncthreads();
+  const int64_t c = int64_t(blockIdx.x) * 256 + threadIdx.x;
+  if (c < C) {
+    float s = 0.0f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) s += red[w][threadIdx.x];
+    part[int64_t(blockIdx.y) * C + c] = s;
+  }
+}
+
 // block = 32 columns x 32 warps; warp w sums partial rows w, w+32, ... (loads
 // unrolled 4 deep), then warp 0 adds the 32 warp sums in order: deterministic
 __global__ void __launch_bounds__(1024) k_colsum_final(const float* __restrict__ part, float* __restrict__ out,
@@ -284,14 +331,25 @@ static void b_colsum(Plan& p) {
                                                                            (float*)out[0].ptr, C, g, 0);
       };
     } else if (C % 8 == 0) {
-      const int64_t nchunk = (R + CS_ROWS - 1) / CS_ROWS;
+      // masked: ~8 blocks per SM in total, each over rpc rows (a multiple of 8)
+      const int64_t cblocks = (C + 255) / 256;
+      int64_t rpc = CS_ROWS;
+      if (masked) {
+        const int64_t want = std::max<int64_t>(1, (kNumSMs * 8 + cblocks - 1) / cblocks);
+        rpc = std::max<int64_t>(CS_ROWS, (((R + want - 1) / want) + 7) / 8 * 8);
+      }
+      const int64_t nchunk = (R + rpc - 1) / rpc;
       auto ws = std::make_shared<Scratch>(size_t(nchunk) * C * 4);
       p.nkernels = 2;
       p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
         if (reinterpret_cast<uintptr_t>(in[0].ptr) % 16) fail(TCB_ERR_ARG, "colsum: input not 16-byte aligned");
-        dim3 grid(unsigned((C + 255) / 256), unsigned(nchunk));
-        launch_k(k_colsum_partial<T>, grid, 256, 0, s, (const T*)in[0].ptr, (float*)ws->p, R, C,
-                 masked ? (const int32_t*)in[1].ptr : nullptr, ign);
+        const dim3 grid{unsigned(cblocks), unsigned(nchunk)};
+        if (masked)
+          launch_k(k_colsum_partial_masked<T>, grid, 256, 0, s, (const T*)in[0].ptr, (float*)ws->p, R, C, rpc,
+                   (const int32_t*)in[1].ptr, ign);
+        else
+          launch_k(k_colsum_partial<T>, grid, 256, 0, s, (const T*)in[0].ptr, (float*)ws->p, R, C,
+                   (const int32_t*)nullptr, ign);
         launch_k(k_colsum_final, unsigned((C + 31) / 32), 1024, 0, s, (const float*)ws->p, (float*)out[0].ptr, nchunk, C,
                                                                   1.0f);
       };

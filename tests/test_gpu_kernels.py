@@ -125,6 +125,19 @@ def test_colsum(shape):
     assert bits_equal(g[0], o[0])  # f32: exact row order
 
 
+@pytest.mark.parametrize("shape", [(4096, 30528), (300, 2304), (77, 40)])
+def test_colsum_masked(shape):
+    """colsum(x, labels) skips rows labelled ignore_index (the CE gradient's
+    exact-zero rows); the oracle adds the masked-out rows' zeros instead."""
+    R, C = shape
+    x = rn(R, C)
+    lab = RNG.integers(0, 50, size=R).astype(np.int32)
+    lab[RNG.uniform(size=R) < 0.85] = -100
+    x[lab == -100] = 0.0  # what the CE gradient holds there
+    g, o = run_both("colsum", [(x, BF16), (lab, I32)], [((C,), F32)], {"ignore_index": -100})
+    assert rel_err(g[0], o[0]) < 1e-5
+
+
 def test_embedding_dx_single_long_segment():
     """token-type ids: every token hits row 0 (one 4096-long segment).  Long
     segments are folded in 128-row chunks (deterministic, not the oracle's

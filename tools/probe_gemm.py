@@ -179,12 +179,13 @@ def linear_gelu(iters, M=4096, K=768, N=3072):
     y = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
     u = torch.empty_like(y)
     res = []
-    for act, save in (("gelu", 1), ("none", 0)):
+    for act, save, what in (("gelu", 1, "preact"), ("gelu", 1, "grad"), ("none", 0, "")):
         outs = [((M, N), BF16), ((M, N), BF16)] if save else [((M, N), BF16)]
-        plan = Plan("linear", [((M, K), BF16), ((K, N), BF16), ((N,), F32)], outs, {"act": act, "save_preact": save})
+        at = {"act": act, "save_preact": save, **({"save": what} if save else {})}
+        plan = Plan("linear", [((M, K), BF16), ((K, N), BF16), ((N,), F32)], outs, at)
         us = time_plan(plan, [x.data_ptr(), w.data_ptr(), b.data_ptr()],
                        [y.data_ptr(), u.data_ptr()][:len(outs)], iters)
-        res.append({"name": f"linear_{act}_{M}x{K}x{N}", "us": round(us, 2),
+        res.append({"name": f"linear_{act}{'_' + what if save else ''}_{M}x{K}x{N}", "us": round(us, 2),
                     "tflops": round(2.0 * M * N * K / us / 1e6, 1)})
     # the FFN2 backward data gradient with the fused GELU' epilogue vs plain
     dy = torch.randn(M, K, device="cuda").to(torch.bfloat16)
@@ -193,6 +194,10 @@ def linear_gelu(iters, M=4096, K=768, N=3072):
                 {"tb": 1, "act": "gelu"})
     us = time_plan(plan, [dy.data_ptr(), w2.data_ptr(), u.data_ptr()], [y.data_ptr()], iters)
     res.append({"name": f"matmul_dact_gelu_{M}x{K}x{N}", "us": round(us, 2), "tflops": round(2.0 * M * N * K / us / 1e6, 1)})
+    plan = Plan("matmul_dact", [((M, K), BF16), ((N, K), BF16), ((M, N), BF16)], [((M, N), BF16)],
+                {"tb": 1, "act": "deriv"})
+    us = time_plan(plan, [dy.data_ptr(), w2.data_ptr(), u.data_ptr()], [y.data_ptr()], iters)
+    res.append({"name": f"matmul_dact_deriv_{M}x{K}x{N}", "us": round(us, 2), "tflops": round(2.0 * M * N * K / us / 1e6, 1)})
     plan = Plan("matmul_t", [((M, K), BF16), ((N, K), BF16)], [((M, N), BF16)], {"tb": 1})
     us = time_plan(plan, [dy.data_ptr(), w2.data_ptr()], [y.data_ptr()], iters)
     res.append({"name": f"matmul_t_tb_{M}x{K}x{N}", "us": round(us, 2), "tflops": round(2.0 * M * N * K / us / 1e6, 1)})
