@@ -86,6 +86,19 @@ int tcb_launch(tcb_plan plan, const tcb_tensor* in, int nin, tcb_tensor* out, in
 
 void tcb_plan_destroy(tcb_plan plan);
 
+/* Deferred partial-sum folds (backend-internal scheduling; no reference
+ * counterpart).  With deferral on, layer_norm_dx and colsum write their
+ * per-block partials to a per-instance buffer carved from a pool of
+ * pool_bytes and queue the fold; tcb_fold_flush folds every queued job in one
+ * launch on `stream` (tcb_launch flushes by itself before any launch that
+ * reads a pending output).  Results are bit-identical to folding in place.
+ * tcb_fold_defer must be called outside stream capture. */
+int tcb_fold_defer(int on, uint64_t pool_bytes);
+int tcb_fold_flush(void* stream);
+/* Cumulative counts: op launches whose fold kernel was deferred, and fold
+ * kernels the flushes launched (kernels-per-step accounting). */
+int tcb_fold_counters(uint64_t* ops_deferred, uint64_t* flush_launches);
+
 /* Number of kernel launches this plan enqueues per tcb_launch (for the
  * bench's gpu_launches count). */
 int tcb_plan_num_kernels(tcb_plan plan);

@@ -9,6 +9,7 @@
 #include <sstream>
 
 #include "common.cuh"
+#include "fold.cuh"
 
 namespace tcb {
 
@@ -161,12 +162,27 @@ int tcb_launch(tcb_plan plan, const tcb_tensor* in, int nin, tcb_tensor* out, in
     if (nin != int(p.in.size()) || nout != int(p.out.size()))
       fail(TCB_ERR_ARG, "b200." + p.op + ": launch arity differs from plan");
     if (skipped_op(p.op)) return TCB_OK;
+    // a deferred fold whose output this launch reads is folded first
+    for (int i = 0; i < nin; ++i)
+      fold_flush_if_reads(in[i].ptr, size_t(p.in[i].numel()) * dtype_bytes(p.in[i].dtype),
+                          static_cast<cudaStream_t>(stream));
     p.run(in, out, static_cast<cudaStream_t>(stream));
     TCB_CUDA(cudaGetLastError());
   });
 }
 
 void tcb_plan_destroy(tcb_plan plan) { delete plan; }
+
+int tcb_fold_defer(int on, uint64_t pool_bytes) { TCB_TRY(fold_set(on != 0, size_t(pool_bytes))); }
+
+int tcb_fold_flush(void* stream) { TCB_TRY(fold_flush(static_cast<cudaStream_t>(stream))); }
+
+int tcb_fold_counters(uint64_t* ops_deferred, uint64_t* flush_launches) {
+  TCB_TRY({
+    if (!ops_deferred || !flush_launches) fail(TCB_ERR_ARG, "tcb_fold_counters: null output");
+    fold_counters(ops_deferred, flush_launches);
+  });
+}
 
 int tcb_plan_num_kernels(tcb_plan plan) { return plan ? plan->p.nkernels : 0; }
 

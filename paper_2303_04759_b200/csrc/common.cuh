@@ -323,6 +323,13 @@ struct Scratch {
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+// Profiling knob (never set in tests / the bench): TCB_SKIP_FOLDS=1 drops the
+// deterministic partial-sum folds (LN dgamma/dbeta, bias colsums, K-slice
+// reductions) to bound what merging them could save.  Outputs are then wrong.
+inline bool skip_folds() {
+  static const bool v = std::getenv("TCB_SKIP_FOLDS") && std::atoi(std::getenv("TCB_SKIP_FOLDS"));
+  return v;
+}
 inline bool pdl_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("TCB_PDL");

@@ -1070,7 +1070,7 @@ __global__ void k_wsplit_reduce(const float* __restrict__ ws, float* __restrict_
   }
 }
 void launch_wsplit_reduce(const float* ws, float* out, int64_t n, int S, cudaStream_t s) {
-  launch_k(k_wsplit_reduce, grid_for((n + 3) / 4, 256, kNumSMs * 4), 256, 0, s, ws, out, n, S);
+  if (!skip_folds()) launch_k(k_wsplit_reduce, grid_for((n + 3) / 4, 256, kNumSMs * 4), 256, 0, s, ws, out, n, S);
 }
 
 }  // namespace tcb

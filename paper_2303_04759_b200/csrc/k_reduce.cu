@@ -9,6 +9,7 @@
 //    extension; bias gradients of [T, N] GEMM outputs), deterministic but in a
 //    different association order (tolerance-checked).
 #include "common.cuh"
+#include "fold.cuh"
 
 namespace tcb {
 
@@ -344,13 +345,20 @@ static void b_colsum(Plan& p) {
       p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
         if (reinterpret_cast<uintptr_t>(in[0].ptr) % 16) fail(TCB_ERR_ARG, "colsum: input not 16-byte aligned");
         const dim3 grid{unsigned(cblocks), unsigned(nchunk)};
+        float* dws = fold_deferring() ? fold_scratch(out[0].ptr, 0, size_t(nchunk) * C * 4) : nullptr;
+        float* wsp = dws ? dws : (float*)ws->p;
         if (masked)
-          launch_k(k_colsum_partial_masked<T>, grid, 256, 0, s, (const T*)in[0].ptr, (float*)ws->p, R, C, rpc,
+          launch_k(k_colsum_partial_masked<T>, grid, 256, 0, s, (const T*)in[0].ptr, wsp, R, C, rpc,
                    (const int32_t*)in[1].ptr, ign);
         else
-          launch_k(k_colsum_partial<T>, grid, 256, 0, s, (const T*)in[0].ptr, (float*)ws->p, R, C,
+          launch_k(k_colsum_partial<T>, grid, 256, 0, s, (const T*)in[0].ptr, wsp, R, C,
                    (const int32_t*)nullptr, ign);
-        launch_k(k_colsum_final, unsigned((C + 31) / 32), 1024, 0, s, (const float*)ws->p, (float*)out[0].ptr, nchunk, C,
+        if (dws) {
+          fold_defer(FoldJob{dws, C, int(nchunk), int(C), (float*)out[0].ptr, 1.0f});
+          fold_op_deferred();
+          return;
+        }
+        if (!skip_folds()) launch_k(k_colsum_final, unsigned((C + 31) / 32), 1024, 0, s, (const float*)ws->p, (float*)out[0].ptr, nchunk, C,
                                                                   1.0f);
       };
     } else {

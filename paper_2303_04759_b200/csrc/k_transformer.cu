@@ -8,6 +8,7 @@
 // allows, f32 statistics and warp-shuffle reductions; the oracle (oracle.c) has
 // the same formulas with sequential sums (tolerance-checked, not bit-exact).
 #include "gemm.cuh"
+#include "fold.cuh"
 
 namespace tcb {
 
@@ -791,21 +792,30 @@ static void b_layer_norm_dx(Plan& p) {
       T* dxp = has_dx ? (T*)out[3].ptr : nullptr;
       bool fast = false;
       if constexpr (sizeof(T) == 2) fast = vec && reinterpret_cast<uintptr_t>(in[1].ptr) % 16 == 0;
+      // deferred fold: this instance's partials go to its own buffer, folded at the flush
+      float* dws = fold_deferring() ? fold_scratch(out[1].ptr, 0, size_t(nblk) * np * H * sizeof(float)) : nullptr;
+      float* wsp = dws ? dws : (float*)ws->p;
       if (fast) {
         if constexpr (sizeof(T) == 2) {
           const bool full = H == NC * 256;
           auto kern = gf ? (full ? k_ln_bwd16<T, NC, true, true> : k_ln_bwd16<T, NC, true, false>)
                          : (full ? k_ln_bwd16<T, NC, false, true> : k_ln_bwd16<T, NC, false, false>);
           launch_k(kern, nblk, 256, smem, s, (const T*)in[0].ptr, (const void*)in[1].ptr, (const float*)in[2].ptr,
-                   (const float*)in[3].ptr, (const T*)in[4].ptr, d2, (T*)out[0].ptr, dxp, (float*)ws->p, np, rows, H,
+                   (const float*)in[3].ptr, (const T*)in[4].ptr, d2, (T*)out[0].ptr, dxp, wsp, np, rows, H,
                    d);
         }
       } else {
         launch_k(k_ln_bwd<T, NC>, nblk, 256, smem, s, (const T*)in[0].ptr, gfp, gtp, (const float*)in[2].ptr,
-                 (const float*)in[3].ptr, (const T*)in[4].ptr, d2, (T*)out[0].ptr, dxp, (float*)ws->p, np, rows, H, d,
+                 (const float*)in[3].ptr, (const T*)in[4].ptr, d2, (T*)out[0].ptr, dxp, wsp, np, rows, H, d,
                  vec);
       }
-      launch_k(k_ln_colsum, (H + 31) / 32, 1024, 0, s, (const float*)ws->p, (float*)out[1].ptr, (float*)out[2].ptr,
+      if (dws) {
+        float* dst[3] = {(float*)out[1].ptr, (float*)out[2].ptr, bias ? (float*)out[di].ptr : nullptr};
+        for (int a = 0; a < np; ++a) fold_defer(FoldJob{dws + size_t(a) * H, int64_t(np) * H, nblk, H, dst[a], 1.0f});
+        fold_op_deferred();
+        return;
+      }
+      if (!skip_folds()) launch_k(k_ln_colsum, (H + 31) / 32, 1024, 0, s, (const float*)ws->p, (float*)out[1].ptr, (float*)out[2].ptr,
                bias ? (float*)out[di].ptr : nullptr, nblk, H);
     };
    });

@@ -143,6 +143,7 @@ struct Instr {
 struct VMStats {
   int64_t arena_bytes = 0, state_bytes = 0, planner_peak = 0;
   int instructions = 0, kernels = 0, lets = 0;
+  int kernels_static = 0;  // sum of the plans' kernel counts (before fold deferral)
 };
 
 class DeviceVM {
@@ -197,17 +198,34 @@ class DeviceVM {
 
   /// enqueue one step on `stream`; use_graph: capture once, then replay
   void run(void* stream, bool use_graph) {
+    // deferred partial-sum folds for this step's enqueue (pool allocated here,
+    // outside capture); enqueue flushes them before the optimizer
+    tcb_check(tcb_fold_defer(fold_defer_ ? 1 : 0, fold_pool_bytes()), "fold defer");
+    struct Off {
+      ~Off() { tcb_fold_defer(0, 0); }
+    } off;
+    uint64_t d0 = 0, l0 = 0, d1 = 0, l1 = 0;
+    tcb_check(tcb_fold_counters(&d0, &l0), "fold counters");
     if (use_graph) {
       if (!graph_) {
         tcb_check(tcb_graph_capture_begin(stream), "graph capture");
         enqueue(stream);
         tcb_check(tcb_graph_capture_end(stream, &graph_), "graph capture end");
+        tcb_check(tcb_fold_counters(&d1, &l1), "fold counters");
+        stats_.kernels = int(stats_.kernels_static - int64_t(d1 - d0) + int64_t(l1 - l0));
       }
       tcb_check(tcb_graph_launch(graph_, stream), "graph launch");
     } else {
       enqueue(stream);
+      tcb_check(tcb_fold_counters(&d1, &l1), "fold counters");
+      stats_.kernels = int(stats_.kernels_static - int64_t(d1 - d0) + int64_t(l1 - l0));
     }
   }
+  static uint64_t fold_pool_bytes() {
+    const char* e = std::getenv("TCB_FOLD_POOL_MB");
+    return uint64_t(e ? std::atoll(e) : 256) << 20;
+  }
+  void set_fold_defer(bool on) { fold_defer_ = on; }
 
   void set_comm(void* c) {
     comm_ = c;
@@ -276,6 +294,7 @@ class DeviceVM {
       }
       if (ins.kind != OpKind::Launch) ins.nkernels = 1;
       stats_.kernels += ins.nkernels;
+      stats_.kernels_static += ins.nkernels;
       code_.push_back(std::move(ins));
     }
     // returned values bound to a state param but not written in place: copy back
@@ -415,6 +434,7 @@ class DeviceVM {
       for (auto& x : after_of[size_t(i)]) out.push_back(x);
     }
     stats_.kernels += int(ch.size()) - adam.nkernels;
+    stats_.kernels_static += int(ch.size()) - adam.nkernels;
     code_ = std::move(out);
     side_chunks_ = int(ch.size());
   }
@@ -423,9 +443,13 @@ class DeviceVM {
     return c == TCB_F32 ? kF32 : c == TCB_BF16 ? dtype_from("bf16") : c == TCB_I32 ? kI32 : kF16;
   }
 
+  static bool is_optimizer(const std::string& op) {
+    return op == "adam_update" || op == "adam_update_ex" || op == "sgd_update";
+  }
   void enqueue(void* stream) {
     bool forked = false;
     for (auto& x : code_) {
+      if (x.kind != OpKind::Launch || is_optimizer(x.op)) tcb_check(tcb_fold_flush(stream), "fold flush");
       if (x.side) {
         if (!side_) {
           tcb_check(tcb_stream_create(&side_), "side stream");
@@ -464,6 +488,7 @@ class DeviceVM {
           break;
       }
     }
+    tcb_check(tcb_fold_flush(stream), "fold flush");
     if (forked) {  // join: the step ends when the last optimizer chunk is done
       tcb_check(tcb_event_record(ev_join_, side_), "event record");
       tcb_check(tcb_stream_wait_event(stream, ev_join_), "stream wait");
@@ -493,6 +518,8 @@ class DeviceVM {
   }
 
   int device_ = 0;
+  // TCB_FOLD_DEFER=0 folds every partial sum in place (A/B and debugging)
+  bool fold_defer_ = !(std::getenv("TCB_FOLD_DEFER") && std::atoi(std::getenv("TCB_FOLD_DEFER")) == 0);
   FunctionPtr fn_;
   LetSeq seq_;
   std::vector<std::pair<int, int>> sb_;

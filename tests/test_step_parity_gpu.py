@@ -84,3 +84,27 @@ def test_gpt2_tiny_causal_parity():
                       lr=1e-3)
     s, o, gl, ol = run_pair(cfg, steps=3)
     assert np.max(np.abs(gl - ol)) < 2e-2, (gl, ol)
+
+
+def test_deferred_folds_bit_identical(monkeypatch):
+    """Deferring the LayerNorm / bias-grad partial folds to one launch before
+    the optimizer (the default) gives bit-identical losses and parameters to
+    folding in place (TCB_FOLD_DEFER=0): same sums in the same order."""
+    cfg = ModelConfig.tiny(dtype="bf16", opt="adam", lr=1e-3, L=2, p=0.1)
+
+    def run(defer):
+        monkeypatch.setenv("TCB_FOLD_DEFER", "1" if defer else "0")
+        s = Session(cfg)
+        s.init_params()
+        losses = []
+        for k in range(2):
+            ids, labels = synthetic_batch(cfg, seed=cfg.seed_d + k)
+            s.set_batch(ids, labels)
+            s.step(graph=True)
+            losses.append(s.loss())
+        return np.array(losses), s.read("params"), s.info()["kernels_per_step"]
+
+    l1, p1, k1 = run(True)
+    l0, p0, k0 = run(False)
+    assert np.array_equal(l1, l0) and np.array_equal(p1, p0)
+    assert k1 < k0  # the per-op fold kernels became one flush
