@@ -182,7 +182,7 @@ class Events:
 
 def gemm_roofline(stream, peaks, iters=50):
     """Dominant kernel: the tcgen05 GEMM at the BERT-base FFN1 forward shape
-    (linear 4096x768 . 768x3072 + bias + GeLU, pre-activation saved), timed with
+    (linear 4096x768 . 768x3072 + bias + GeLU, GeLU' saved for the backward), timed with
     CUDA events over `iters` launches on the session stream."""
     import ctypes
 
@@ -197,7 +197,7 @@ def gemm_roofline(stream, peaks, iters=50):
     u = torch.empty_like(y)
     torch.cuda.synchronize()
     plan = Plan("linear", [((M, K), BF16), ((K, N), BF16), ((N,), F32)], [((M, N), BF16), ((M, N), BF16)],
-                {"act": "gelu", "save_preact": 1})
+                {"act": "gelu", "save_preact": 1, "save": "grad"})
     ins, outs = [x.data_ptr(), w.data_ptr(), b.data_ptr()], [y.data_ptr(), u.data_ptr()]
     for _ in range(5):
         plan.launch(ins, outs, stream)
@@ -213,9 +213,17 @@ def gemm_roofline(stream, peaks, iters=50):
     flops = 2.0 * M * N * K
     achieved = flops / (ms * 1e-3) / 1e12
     peak = peaks.get("bf16_tflops", FALLBACK_PEAKS["bf16_tflops"])
+    # DRAM bytes per launch of this exact kernel from the committed ncu --set full capture
+    traffic = None
+    try:
+        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
+                               "r01_roofline_kernel_ncu.json")) as f:
+            traffic = json.load(f)["traffic_bytes"]
+    except (OSError, KeyError, ValueError):
+        pass
     return {"bound": "tensor", "achieved": round(achieved, 1), "peak": peak, "unit": "TFLOP/s",
-            "frac": round(achieved / peak, 4), "traffic": None,
-            "kernel": f"b200.linear tcgen05 {M}x{K}x{N} bf16 (+bias+gelu+preact)", "us_per_launch": round(ms * 1e3, 2)}
+            "frac": round(achieved / peak, 4), "traffic": traffic,
+            "kernel": f"b200.linear tcgen05 {M}x{K}x{N} bf16 (+bias+gelu, act' saved)", "us_per_launch": round(ms * 1e3, 2)}
 
 
 def max_batch_report(stream_sync_free_bytes: int):
