@@ -450,6 +450,12 @@ static inline float act_f(int act, float v) {
     default: return v;
   }
 }
+/* linear: act(x . W + bias) -- matmul_add_act (backends.hpp:311-324) with the
+ * gelu extension; one rounding at the end; tw reads W stored [N,K].  u (may be
+ * NULL) receives the rounded pre-activation, or with save_grad the rounded
+ * derivative act'(pre-activation). */
+static void linear_fwd(const orc_tensor* x, const orc_tensor* w, const orc_tensor* bias, orc_tensor* y,
+                       orc_tensor* u, int act, int tw, int save_grad);
 /* derivative given the saved aux value: pre-activation u for relu/gelu, the
  * output y for tanh (tanh_dx semantics, backends.hpp:172-173). */
 static inline float dact_f(int act, float aux) {
@@ -469,6 +475,19 @@ static inline float deriv_of_preact(int act, float u) {
     case ACT_GELU: return gelu_grad_f(u);
     default: return 1.0f;
   }
+}
+
+static void linear_fwd(const orc_tensor* x, const orc_tensor* w, const orc_tensor* bias, orc_tensor* y,
+                       orc_tensor* u, int act, int tw, int save_grad) {
+  int64_t M = x->shape[0], K = x->shape[1];
+  int64_t N = tw ? w->shape[0] : w->shape[1];
+  gemm_acc(F(x), F(w), F(y), M, N, K, 0, tw, 1.0f);
+  for (int64_t i = 0; i < M; ++i)
+    for (int64_t j = 0; j < N; ++j) {
+      float v = F(y)[i * N + j] + F(bias)[j];
+      if (u) F(u)[i * N + j] = rnd(u->dtype, save_grad ? deriv_of_preact(act, v) : v);
+      F(y)[i * N + j] = rnd(y->dtype, act_f(act, v));
+    }
 }
 
 /* ------------------------------------------------------------- attention */
@@ -941,16 +960,21 @@ int orc_exec(const char* op, const orc_tensor* in, int nin, orc_tensor* out, int
     int act = parse_act(astr(A, na, "act", "none"));
     if (act < 0) return fail("linear: bad act");
     const int save_grad = !strcmp(astr(A, na, "save", "preact"), "grad");
-    int tw = (int)aint(A, na, "tw", 0);
-    int64_t M = in[0].shape[0], K = in[0].shape[1];
-    int64_t N = tw ? in[1].shape[0] : in[1].shape[1];
-    gemm_acc(F(&in[0]), F(&in[1]), F(&out[0]), M, N, K, 0, tw, 1.0f);
-    for (int64_t i = 0; i < M; ++i)
-      for (int64_t j = 0; j < N; ++j) {
-        float v = F(&out[0])[i * N + j] + F(&in[2])[j];
-        if (nout > 1) F(&out[1])[i * N + j] = rnd(out[1].dtype, save_grad ? deriv_of_preact(act, v) : v);
-        F(&out[0])[i * N + j] = rnd(out[0].dtype, act_f(act, v));
-      }
+    linear_fwd(&in[0], &in[1], &in[2], &out[0], nout > 1 ? &out[1] : NULL, act, (int)aint(A, na, "tw", 0),
+               save_grad);
+    return 0;
+  }
+  /* linear_chain(x, W1, b1, W2, b2) -> (y1 [, u1], y2): the two linears in
+   * sequence (the device runs them as one chained launch); y2 reads the
+   * ROUNDED y1 exactly like a separate second linear would. */
+  if (!strcmp(op, "linear_chain")) {
+    if (nin != 5 || (nout != 2 && nout != 3)) return fail("linear_chain: 5 inputs, 2-3 outputs");
+    int act = parse_act(astr(A, na, "act", "none")), act2 = parse_act(astr(A, na, "act2", "none"));
+    if (act < 0 || act2 < 0) return fail("linear_chain: bad act");
+    const int save_grad = !strcmp(astr(A, na, "save", "preact"), "grad");
+    linear_fwd(&in[0], &in[1], &in[2], &out[0], nout > 2 ? &out[1] : NULL, act, (int)aint(A, na, "tw", 0),
+               save_grad);
+    linear_fwd(&out[0], &in[3], &in[4], &out[nout - 1], NULL, act2, (int)aint(A, na, "tw2", 0), 0);
     return 0;
   }
   /* matmul_pair(a0, b0 [, aux0], a1, b1): problem 0 is matmul_t (n0 = 2) or

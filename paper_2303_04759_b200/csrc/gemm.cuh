@@ -45,6 +45,9 @@ struct GemmArgs {
   const int* sched = nullptr;      // device LPT schedule of a pair launch (gemm_pair_schedule)
   int sched_rounds = 0;
   int wsplit = 1;                  // > 1: c is a [wsplit][M][N] f32 workspace of K-slice partials
+  int* dep_signal = nullptr;       // chained launch: per-row-block completion counters this problem signals
+  const int* dep_wait = nullptr;   // ... or waits on (>= dep_need) before loading A
+  int dep_need = 0;
 };
 
 struct TcChoice {
@@ -62,6 +65,10 @@ void launch_gemm_tc(const GemmArgs& g, cudaStream_t s);
 void launch_gemm_tc_pair(const GemmArgs& g0, const GemmArgs& g1, cudaStream_t s);
 // host-side longest-processing-time unit schedule for a pair launch
 std::vector<int> gemm_pair_schedule(const GemmArgs& g0, const GemmArgs& g1, int* rounds);
+// chained pair: problem 1 reads problem 0's output as A (row-block counters)
+void launch_gemm_tc_chain(const GemmArgs& g0, const GemmArgs& g1, cudaStream_t s);
+std::vector<int> gemm_chain_schedule(const GemmArgs& g0, const GemmArgs& g1, int* rounds);
+int gemm_chain_need(const GemmArgs& g0, const GemmArgs& g1);
 // K slices for problem idx of a pair (1 = none); partials then need
 // launch_wsplit_reduce into the real output
 int gemm_pair_wsplit(GemmArgs g0, GemmArgs g1, int idx);

@@ -71,6 +71,12 @@ struct TcProb {
   // to slice s of a [wsplit][M][N] workspace (C map Z2 = wsplit), which a fixed-
   // order reduction kernel sums afterwards (deterministic)
   int wsplit;
+  // chained launch (problem 1 reads problem 0's output as its A operand):
+  // problem 0 adds 1 to sig[mb] per epilogue warp once its stores of a tile
+  // of row block mb completed; problem 1's producer waits for dep[mb] >= need
+  int* sig;
+  const int* dep;
+  int dep_need;
   uint32_t idesc;
   // epilogue
   void* c;
@@ -381,6 +387,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const int kb1 = min(kb0 + Q.kps, Q.k_blocks);
         if (Q.wsplit > 1) z = 0;  // z is the K slice, not a batch index
         const int z1 = int(z / Q.Z2), z2 = int(z % Q.Z2);
+        if (Q.dep) dep_wait(Q.dep + mb, Q.dep_need);  // the A rows come from problem 0's tiles
         const int m0 = mb * (TC_BM * CG) + int(rank) * TC_BM;
         const int n0 = nb * BN + int(rank) * C::B_ROWS;
         for (int kb = kb0; kb < kb1; ++kb) {
@@ -678,6 +685,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         finish(v, ci, n0);
       }
       if (tr && ew == 0 && lane == 0 && ui == 0) tr[6] = gtimer();
+      if (Q.sig) {  // publish this warp's part of the tile once its stores landed
+        if (lane == 0) {
+          bulk_wait_all();
+          dep_signal(Q.sig + mb);
+        }
+        __syncwarp();
+      }
       // release the accumulator to the (leader's) MMA warp
       tc_fence_before();
       __syncwarp();
@@ -781,6 +795,9 @@ static void fill_prob(const GemmArgs& g, int splits, TcProb& P, CUtensorMap& ta,
   P.aux_dtype = g.aux_dtype;
   P.aux_out = g.aux_out;
   P.save_grad = g.aux_out ? g.save_grad : 0;
+  P.sig = g.dep_signal;
+  P.dep = g.dep_wait;
+  P.dep_need = g.dep_need;
   const int es = dtype_bytes(g.c_dtype);
   P.c_vec_ok = (reinterpret_cast<uintptr_t>(g.c) % 16 == 0) && ((g.ldc * es) % 16 == 0) &&
                ((g.c_s1 * es) % 16 == 0) && ((g.c_s2 * es) % 16 == 0) &&
@@ -1015,6 +1032,77 @@ static std::vector<int> lpt_table(const GemmArgs& g0, const GemmArgs& g1, int* r
 }
 std::vector<int> gemm_pair_schedule(const GemmArgs& g0, const GemmArgs& g1, int* rounds) {
   return lpt_table(g0, g1, rounds, nullptr);
+}
+
+// Chained launch: problem 1's A operand is problem 0's output (FFN1 -> FFN2).
+// Same tile shape for both; no swap.  Host list schedule over clusters in
+// k-block time units: problem-0 tiles in row-block-major order; a problem-1
+// tile of row block m becomes eligible once all of m's problem-0 tiles are
+// placed, and is ready at their estimated completion (MMA end + epilogue).  A
+// cluster takes a ready problem-1 tile first, else the next problem-0 tile,
+// else the earliest problem-1 tile (waiting for it).  Every unit is appended
+// after all units it depends on were appended somewhere, so with all CTAs
+// co-resident no cluster ever waits on work queued behind itself.
+static std::vector<int> chain_table(const GemmArgs& g0, const GemmArgs& g1, int* rounds, double* max_load) {
+  const TcChoice c = pair_choice(g0, g1);
+  const int64_t mb = (g0.M + 128 * c.cg - 1) / (128 * c.cg);
+  const int64_t nb0 = (g0.N + c.bn - 1) / c.bn, nb1 = (g1.N + c.bn - 1) / c.bn;
+  const int64_t t0 = mb * nb0, t1 = mb * nb1;
+  const double kb0 = double((g0.K + TC_BK - 1) / TC_BK), kb1 = double((g1.K + TC_BK - 1) / TC_BK);
+  const double epi0 = (g0.act == ACT_GELU || g0.dact != ACT_NONE) ? 20.0 : 6.0;  // epilogue length, k-block units
+  const int64_t total = (t0 + t1) * c.cg;
+  int grid = int(total < kNumSMs ? total : kNumSMs);
+  grid = (grid / c.cg) * c.cg;
+  const int ncl = grid / c.cg;
+  std::vector<double> avail(ncl, 0.0), ready(mb, 0.0);
+  std::vector<int> placed(mb, 0);
+  std::vector<std::vector<int>> lists(ncl);
+  std::vector<int64_t> next_nb1(mb, 0);  // next problem-1 tile of each row block
+  int64_t next0 = 0, left1 = t1;
+  while (next0 < t0 || left1 > 0) {
+    int cl = 0;
+    for (int k = 1; k < ncl; ++k)
+      if (avail[k] < avail[cl]) cl = k;
+    // earliest-ready eligible problem-1 row block
+    int64_t best_m = -1;
+    for (int64_t m = 0; m < mb; ++m)
+      if (placed[m] == nb0 && next_nb1[m] < nb1 && (best_m < 0 || ready[m] < ready[best_m])) best_m = m;
+    if (best_m >= 0 && (ready[best_m] <= avail[cl] || next0 >= t0)) {
+      const int64_t u = t0 + best_m * nb1 + next_nb1[best_m]++;
+      avail[cl] = std::max(avail[cl], ready[best_m]) + kb1 + 2.0;
+      lists[cl].push_back(int(u));
+      --left1;
+    } else {
+      const int64_t m = next0 / nb0;
+      avail[cl] += kb0;
+      ready[m] = std::max(ready[m], avail[cl] + epi0);
+      ++placed[m];
+      lists[cl].push_back(int(next0++));
+    }
+  }
+  int r = 0;
+  for (auto& l : lists) r = std::max(r, int(l.size()));
+  std::vector<int> table(size_t(r) * ncl, -1);
+  for (int k = 0; k < ncl; ++k)
+    for (size_t i = 0; i < lists[k].size(); ++i) table[i * ncl + k] = lists[k][i];
+  *rounds = r;
+  if (max_load) *max_load = *std::max_element(avail.begin(), avail.end());
+  return table;
+}
+std::vector<int> gemm_chain_schedule(const GemmArgs& g0, const GemmArgs& g1, int* rounds) {
+  return chain_table(g0, g1, rounds, nullptr);
+}
+int gemm_chain_need(const GemmArgs& g0, const GemmArgs& g1) {
+  const TcChoice c = pair_choice(g0, g1);
+  return int((g0.N + c.bn - 1) / c.bn) * c.cg * TC_EPI_WARPS;
+}
+void launch_gemm_tc_chain(const GemmArgs& g0, const GemmArgs& g1, cudaStream_t s) {
+  std::string why;
+  for (const GemmArgs* g : {&g0, &g1})
+    if (!gemm_tc_supported(*g, &why)) fail(TCB_ERR_UNIMPLEMENTED, "tcgen05 gemm chain: " + why);
+  if (!g0.dep_signal || !g1.dep_wait || !g0.sched) fail(TCB_ERR_ARG, "tcgen05 gemm chain: counters / schedule missing");
+  GemmArgs gs[2] = {g0, g1};
+  dispatch_tc(gs, 2, pair_choice(g0, g1), s);
 }
 
 // K slices for problem `idx` of a pair (a weight gradient whose few long tiles

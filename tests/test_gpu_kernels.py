@@ -566,3 +566,39 @@ def test_unimplemented_is_loud():
         Plan("b200.no_such_op", [((4,), F32)], [((4,), F32)])
     with pytest.raises(UnimplementedOp):
         Plan("ref.add", [((4,), F32), ((4,), F32)], [((4,), F32)])
+
+
+@pytest.mark.parametrize("shape", [(700, 256, 384, 320), (512, 128, 512, 256)])
+@pytest.mark.parametrize("save", ["grad", "preact"])
+def test_linear_chain(shape, save):
+    """FFN1 -> FFN2 as one chained tcgen05 launch (problem 1 waits on problem
+    0's row-block counters), against the oracle's two sequential linears."""
+    m, k, n1, n2 = shape
+    x, w1, b1 = rn(m, k), rn(k, n1, lo=-0.1, hi=0.1), rn(n1)
+    w2, b2 = rn(n1, n2, lo=-0.1, hi=0.1), rn(n2)
+    at = {"act": "gelu", "save_preact": 1, "save": save}
+    outs = [((m, n1), BF16), ((m, n1), BF16), ((m, n2), BF16)]
+    g, o = run_both("linear_chain", [(x, BF16), (w1, BF16), (b1, F32), (w2, BF16), (b2, F32)], outs, at)
+    for a, b in zip(g, o):
+        assert rel_err(a, b) < BF16_TOL, rel_err(a, b)
+
+
+def test_linear_chain_bert_ffn_repeatable():
+    """BERT-base FFN forward (4096x768 -> 3072 -> 768) chained: equal to the
+    two separate linears bit for bit (same tiles, same epilogues), and
+    run-to-run identical."""
+    from gpu_util import from_torch, to_torch
+    from paper_2303_04759_b200.runtime import run_op
+    T, H, F = 4096, 768, 3072
+    x = to_torch(rn(T, H), BF16)
+    w1, b1 = to_torch(rn(H, F, lo=-0.05, hi=0.05), BF16), to_torch(rn(F), F32)
+    w2, b2 = to_torch(rn(F, H, lo=-0.05, hi=0.05), BF16), to_torch(rn(H), F32)
+    at = {"act": "gelu", "save_preact": 1, "save": "grad"}
+    outs = [((T, F), BF16), ((T, F), BF16), ((T, H), BF16)]
+    c1 = [from_torch(t) for t in run_op("linear_chain", [x, w1, b1, w2, b2], outs, at)]
+    c2 = [from_torch(t) for t in run_op("linear_chain", [x, w1, b1, w2, b2], outs, at)]
+    y1, u1 = run_op("linear", [x, w1, b1], outs[:2], at)
+    (y2,) = run_op("linear", [y1, w2, b2], outs[2:], {})
+    sep = [from_torch(t) for t in (y1, u1, y2)]
+    for a, b, c in zip(c1, c2, sep):
+        assert bits_equal(a, b) and bits_equal(a, c)

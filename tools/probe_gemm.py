@@ -204,6 +204,30 @@ def linear_gelu(iters, M=4096, K=768, N=3072):
     return res
 
 
+def chain(iters):
+    """BERT-base FFN forward: linear(gelu, act' saved) then linear, as two
+    launches vs one chained launch (linear_chain)."""
+    T, H, F = 4096, 768, 3072
+    x = torch.randn(T, H, device="cuda").to(torch.bfloat16)
+    w1 = (0.02 * torch.randn(H, F, device="cuda")).to(torch.bfloat16)
+    w2 = (0.02 * torch.randn(F, H, device="cuda")).to(torch.bfloat16)
+    b1, b2 = torch.zeros(F, device="cuda"), torch.zeros(H, device="cuda")
+    y1 = torch.empty(T, F, device="cuda", dtype=torch.bfloat16)
+    u1 = torch.empty_like(y1)
+    y2 = torch.empty(T, H, device="cuda", dtype=torch.bfloat16)
+    at = {"act": "gelu", "save_preact": 1, "save": "grad"}
+    p1 = Plan("linear", [((T, H), BF16), ((H, F), BF16), ((F,), F32)], [((T, F), BF16)] * 2, at)
+    p2 = Plan("linear", [((T, F), BF16), ((F, H), BF16), ((H,), F32)], [((T, H), BF16)], {})
+    t1 = time_plan(p1, [x.data_ptr(), w1.data_ptr(), b1.data_ptr()], [y1.data_ptr(), u1.data_ptr()], iters)
+    t2 = time_plan(p2, [y1.data_ptr(), w2.data_ptr(), b2.data_ptr()], [y2.data_ptr()], iters)
+    pc = Plan("linear_chain", [((T, H), BF16), ((H, F), BF16), ((F,), F32), ((F, H), BF16), ((H,), F32)],
+              [((T, F), BF16), ((T, F), BF16), ((T, H), BF16)], at)
+    tc = time_plan(pc, [x.data_ptr(), w1.data_ptr(), b1.data_ptr(), w2.data_ptr(), b2.data_ptr()],
+                   [y1.data_ptr(), u1.data_ptr(), y2.data_ptr()], iters)
+    print(json.dumps({"name": "ffn_fwd", "ffn1_us": round(t1, 2), "ffn2_us": round(t2, 2),
+                      "sum_us": round(t1 + t2, 2), "chain_us": round(tc, 2)}), flush=True)
+
+
 def time_plan(plan, ins, outs, iters):
     s = torch.cuda.current_stream().cuda_stream
     for _ in range(3):
@@ -256,7 +280,11 @@ def main():
     ap.add_argument("--splits", action="store_true")
     ap.add_argument("--trace", action="store_true")
     ap.add_argument("--pairs", action="store_true")
+    ap.add_argument("--chain", action="store_true")
     args = ap.parse_args()
+    if args.chain:
+        chain(args.iters)
+        return
     if args.pairs:
         pairs(args.iters)
         return
