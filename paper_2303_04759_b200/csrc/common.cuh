@@ -166,6 +166,22 @@ __device__ __forceinline__ void fast_phi(float x, float& phi, float& e) {
   const float half_erfc = 0.5f * (poly * t) * e;                  // 0.5 erfc(z)
   phi = x >= 0.0f ? 1.0f - half_erfc : half_erfc;
 }
+// fast_phi on an element pair with f32x2 arithmetic (same operations, same
+// order per lane as fast_phi -> bit-identical results, half the FP issue slots)
+__device__ __forceinline__ void fast_phi2(float2 x, float2& phi, float2& e) {
+  const float2 ax = make_float2(fabsf(x.x), fabsf(x.y));
+  const float2 q = mul2(mul2(x, x), splat2(-0.72134752044448170f));
+  e = make_float2(ex2_approx(q.x), ex2_approx(q.y));
+  const float2 den = fma2(splat2(0.23164188f), ax, splat2(1.0f));
+  const float2 t = make_float2(rcp_approx(den.x), rcp_approx(den.y));
+  float2 poly = fma2(t, splat2(1.061405429f), splat2(-1.453152027f));
+  poly = fma2(t, poly, splat2(1.421413741f));
+  poly = fma2(t, poly, splat2(-0.284496736f));
+  poly = fma2(t, poly, splat2(0.254829592f));
+  const float2 he = mul2(mul2(splat2(0.5f), mul2(poly, t)), e);
+  const float2 one_m = add2(splat2(1.0f), make_float2(-he.x, -he.y));
+  phi = make_float2(x.x >= 0.0f ? one_m.x : he.x, x.y >= 0.0f ? one_m.y : he.y);
+}
 __device__ __forceinline__ float fast_gelu(float x) {
   float phi, e;
   fast_phi(x, phi, e);

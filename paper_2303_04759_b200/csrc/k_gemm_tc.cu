@@ -152,7 +152,14 @@ __device__ __forceinline__ void apply_act(int act, float (&v)[W]) {
       break;
     case ACT_GELU:
 #pragma unroll
-      for (int j = 0; j < W; ++j) v[j] = fast_gelu(v[j]);
+      for (int j = 0; j < W; j += 2) {
+        const float2 x = make_float2(v[j], v[j + 1]);
+        float2 phi, e;
+        fast_phi2(x, phi, e);
+        const float2 y = mul2(x, phi);
+        v[j] = y.x;
+        v[j + 1] = y.y;
+      }
       break;
     default:
       break;
@@ -171,11 +178,23 @@ __device__ __forceinline__ void apply_dact(int act, float (&v)[W], const float (
       break;
     case ACT_GELU:
 #pragma unroll
-      for (int j = 0; j < W; ++j) v[j] *= fast_gelu_grad(a[j]);
+      for (int j = 0; j < W; j += 2) {
+        const float2 x = make_float2(a[j], a[j + 1]);
+        float2 phi, e;
+        fast_phi2(x, phi, e);
+        const float2 g = fma2(mul2(x, splat2(0.39894228040143268f)), e, phi);
+        const float2 r = mul2(make_float2(v[j], v[j + 1]), g);
+        v[j] = r.x;
+        v[j + 1] = r.y;
+      }
       break;
     case ACT_DERIV:
 #pragma unroll
-      for (int j = 0; j < W; ++j) v[j] *= a[j];
+      for (int j = 0; j < W; j += 2) {
+        const float2 r = mul2(make_float2(v[j], v[j + 1]), make_float2(a[j], a[j + 1]));
+        v[j] = r.x;
+        v[j + 1] = r.y;
+      }
       break;
     default:
       break;
@@ -187,11 +206,16 @@ template <int W>
 __device__ __forceinline__ void act_and_deriv(int act, float (&v)[W], float (&d)[W]) {
   if (act == ACT_GELU) {
 #pragma unroll
-    for (int j = 0; j < W; ++j) {
-      float phi, e;
-      fast_phi(v[j], phi, e);
-      d[j] = fmaf(v[j] * 0.39894228040143268f, e, phi);
-      v[j] *= phi;
+    for (int j = 0; j < W; j += 2) {
+      const float2 x = make_float2(v[j], v[j + 1]);
+      float2 phi, e;
+      fast_phi2(x, phi, e);
+      const float2 g = fma2(mul2(x, splat2(0.39894228040143268f)), e, phi);
+      const float2 y = mul2(x, phi);
+      d[j] = g.x;
+      d[j + 1] = g.y;
+      v[j] = y.x;
+      v[j + 1] = y.y;
     }
     return;
   }
@@ -240,6 +264,27 @@ struct Box {
     return (g ^ ((row * row_bytes >> 7) & (ng - 1)));
   }
 };
+template <int W, typename H>
+__device__ __forceinline__ void stage_row16(uint8_t* box, int lane, const float (&v)[W]) {
+  constexpr int RB = W * 2;
+#pragma unroll
+  for (int g = 0; g < RB / 16; ++g) {
+    uint4 q;
+    if constexpr (std::is_same<H, __nv_bfloat16>::value) {
+      q.x = pack2(v[8 * g], v[8 * g + 1], TCB_BF16);
+      q.y = pack2(v[8 * g + 2], v[8 * g + 3], TCB_BF16);
+      q.z = pack2(v[8 * g + 4], v[8 * g + 5], TCB_BF16);
+      q.w = pack2(v[8 * g + 6], v[8 * g + 7], TCB_BF16);
+    } else {
+      q.x = pack2(v[8 * g], v[8 * g + 1], TCB_F16);
+      q.y = pack2(v[8 * g + 2], v[8 * g + 3], TCB_F16);
+      q.z = pack2(v[8 * g + 4], v[8 * g + 5], TCB_F16);
+      q.w = pack2(v[8 * g + 6], v[8 * g + 7], TCB_F16);
+    }
+    *reinterpret_cast<uint4*>(box + lane * RB + (Box<W>::sw(lane, g, RB) << 4)) = q;
+  }
+}
+// one uniform dtype branch per row (the 16-bit packs are then single-path)
 template <int W>
 __device__ __forceinline__ void stage_row(uint8_t* box, int lane, int dt, const float (&v)[W]) {
   if (dt == TCB_F32) {
@@ -249,29 +294,33 @@ __device__ __forceinline__ void stage_row(uint8_t* box, int lane, int dt, const 
       float4 q = make_float4(v[4 * g], v[4 * g + 1], v[4 * g + 2], v[4 * g + 3]);
       *reinterpret_cast<float4*>(box + lane * RB + (Box<W>::sw(lane, g, RB) << 4)) = q;
     }
+  } else if (dt == TCB_BF16) {
+    stage_row16<W, __nv_bfloat16>(box, lane, v);
   } else {
-    constexpr int RB = W * 2;
-#pragma unroll
-    for (int g = 0; g < RB / 16; ++g) {
-      uint4 q;
-      q.x = pack2(v[8 * g], v[8 * g + 1], dt);
-      q.y = pack2(v[8 * g + 2], v[8 * g + 3], dt);
-      q.z = pack2(v[8 * g + 4], v[8 * g + 5], dt);
-      q.w = pack2(v[8 * g + 6], v[8 * g + 7], dt);
-      *reinterpret_cast<uint4*>(box + lane * RB + (Box<W>::sw(lane, g, RB) << 4)) = q;
-    }
+    stage_row16<W, __half>(box, lane, v);
   }
 }
 template <int W>
 __device__ __forceinline__ void unstage_row16(const uint8_t* box, int lane, int dt, float (&a)[W]) {
   constexpr int RB = W * 2;
+  if (dt == TCB_BF16) {
 #pragma unroll
-  for (int g = 0; g < RB / 16; ++g) {
-    uint4 q = *reinterpret_cast<const uint4*>(box + lane * RB + (Box<W>::sw(lane, g, RB) << 4));
-    unpack2(q.x, dt, a[8 * g], a[8 * g + 1]);
-    unpack2(q.y, dt, a[8 * g + 2], a[8 * g + 3]);
-    unpack2(q.z, dt, a[8 * g + 4], a[8 * g + 5]);
-    unpack2(q.w, dt, a[8 * g + 6], a[8 * g + 7]);
+    for (int g = 0; g < RB / 16; ++g) {
+      uint4 q = *reinterpret_cast<const uint4*>(box + lane * RB + (Box<W>::sw(lane, g, RB) << 4));
+      unpack2(q.x, TCB_BF16, a[8 * g], a[8 * g + 1]);
+      unpack2(q.y, TCB_BF16, a[8 * g + 2], a[8 * g + 3]);
+      unpack2(q.z, TCB_BF16, a[8 * g + 4], a[8 * g + 5]);
+      unpack2(q.w, TCB_BF16, a[8 * g + 6], a[8 * g + 7]);
+    }
+  } else {
+#pragma unroll
+    for (int g = 0; g < RB / 16; ++g) {
+      uint4 q = *reinterpret_cast<const uint4*>(box + lane * RB + (Box<W>::sw(lane, g, RB) << 4));
+      unpack2(q.x, TCB_F16, a[8 * g], a[8 * g + 1]);
+      unpack2(q.y, TCB_F16, a[8 * g + 2], a[8 * g + 3]);
+      unpack2(q.z, TCB_F16, a[8 * g + 4], a[8 * g + 5]);
+      unpack2(q.w, TCB_F16, a[8 * g + 6], a[8 * g + 7]);
+    }
   }
 }
 
@@ -552,10 +601,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 #pragma unroll
           for (int j = 0; j < W / 4; ++j) {
             const float4 b4 = bb[j];
-            v[4 * j] += b4.x;
-            v[4 * j + 1] += b4.y;
-            v[4 * j + 2] += b4.z;
-            v[4 * j + 3] += b4.w;
+            const float2 lo = add2(make_float2(v[4 * j], v[4 * j + 1]), make_float2(b4.x, b4.y));
+            const float2 hi = add2(make_float2(v[4 * j + 2], v[4 * j + 3]), make_float2(b4.z, b4.w));
+            v[4 * j] = lo.x;
+            v[4 * j + 1] = lo.y;
+            v[4 * j + 2] = hi.x;
+            v[4 * j + 3] = hi.y;
           }
         }
         if (Q.tma_epi) {
