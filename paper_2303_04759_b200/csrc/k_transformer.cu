@@ -1351,17 +1351,18 @@ __global__ void __launch_bounds__(256) k_embed_fold(const int32_t* __restrict__ 
                                                     const int32_t* __restrict__ sorted,
                                                     const int32_t* __restrict__ seg_len,
                                                     const float* __restrict__ part, float* __restrict__ out,
-                                                    int64_t H) {
+                                                    int64_t T, int64_t H) {
   TCB_PDL_ENTRY();
-  const int64_t pos = blockIdx.x;
-  const int32_t len = seg_len[pos];
-  if (len <= EMB_CHUNK) return;
-  const int32_t id = ids[sorted[pos]];
   const int64_t j = int64_t(blockIdx.y) * blockDim.x + threadIdx.x;
-  if (j >= H) return;
-  float acc = out[int64_t(id) * H + j];
-  for (int64_t c = pos; c < pos + len; c += EMB_CHUNK) acc = __fadd_rn(acc, part[c * H + j]);
-  out[int64_t(id) * H + j] = acc;
+  // grid-stride over sorted positions: only heads of long segments do work
+  for (int64_t pos = blockIdx.x; pos < T; pos += gridDim.x) {
+    const int32_t len = seg_len[pos];
+    if (len <= EMB_CHUNK || j >= H) continue;
+    const int32_t id = ids[sorted[pos]];
+    float acc = out[int64_t(id) * H + j];
+    for (int64_t c = pos; c < pos + len; c += EMB_CHUNK) acc = __fadd_rn(acc, part[c * H + j]);
+    out[int64_t(id) * H + j] = acc;
+  }
 }
 
 // block (pos, column tile): if sorted position `pos` starts a segment of equal
@@ -1376,27 +1377,37 @@ __global__ void __launch_bounds__(256) k_embed_accum(const int32_t* __restrict__
                                                      const TD* __restrict__ dy, float* __restrict__ out,
                                                      float* __restrict__ part, int64_t T, int64_t H) {
   TCB_PDL_ENTRY();
-  const int64_t pos = blockIdx.x;
-  const int64_t head = seg_head[pos];
-  if ((pos - head) % EMB_CHUNK) return;  // not a chunk start
-  const int32_t len = seg_len[head];
-  const bool single = len <= EMB_CHUNK;
-  const int64_t end = (head + len) < (pos + EMB_CHUNK) ? (head + len) : (pos + EMB_CHUNK);
-  const int32_t id = ids[sorted[pos]];
   const int64_t j = int64_t(blockIdx.y) * blockDim.x + threadIdx.x;
-  if (j >= H) return;
-  float acc = single ? out[int64_t(id) * H + j] : 0.0f;
-  int64_t q = pos;
-  for (; q + 4 <= end; q += 4) {
-    float v0 = to_f(dy[int64_t(sorted[q]) * H + j]);
-    float v1 = to_f(dy[int64_t(sorted[q + 1]) * H + j]);
-    float v2 = to_f(dy[int64_t(sorted[q + 2]) * H + j]);
-    float v3 = to_f(dy[int64_t(sorted[q + 3]) * H + j]);
-    acc = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(acc, v0), v1), v2), v3);
+  // grid-stride over sorted positions (most are not chunk starts and skip at once)
+  for (int64_t pos = blockIdx.x; pos < T; pos += gridDim.x) {
+    const int64_t head = seg_head[pos];
+    if ((pos - head) % EMB_CHUNK || j >= H) continue;  // not a chunk start
+    const int32_t len = seg_len[head];
+    const bool single = len <= EMB_CHUNK;
+    const int64_t end = (head + len) < (pos + EMB_CHUNK) ? (head + len) : (pos + EMB_CHUNK);
+    const int32_t id = ids[sorted[pos]];
+    float acc = single ? out[int64_t(id) * H + j] : 0.0f;
+    int64_t q = pos;
+    // 16 row loads in flight per round (long segments are latency chains);
+    // the adds stay in ascending t
+    for (; q + 16 <= end; q += 16) {
+      float v[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) v[k] = to_f(dy[int64_t(sorted[q + k]) * H + j]);
+#pragma unroll
+      for (int k = 0; k < 16; ++k) acc = __fadd_rn(acc, v[k]);
+    }
+    for (; q + 4 <= end; q += 4) {
+      float v0 = to_f(dy[int64_t(sorted[q]) * H + j]);
+      float v1 = to_f(dy[int64_t(sorted[q + 1]) * H + j]);
+      float v2 = to_f(dy[int64_t(sorted[q + 2]) * H + j]);
+      float v3 = to_f(dy[int64_t(sorted[q + 3]) * H + j]);
+      acc = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(acc, v0), v1), v2), v3);
+    }
+    for (; q < end; ++q) acc = __fadd_rn(acc, to_f(dy[int64_t(sorted[q]) * H + j]));
+    if (single) out[int64_t(id) * H + j] = acc;
+    else part[pos * H + j] = acc;
   }
-  for (; q < end; ++q) acc = __fadd_rn(acc, to_f(dy[int64_t(sorted[q]) * H + j]));
-  if (single) out[int64_t(id) * H + j] = acc;
-  else part[pos * H + j] = acc;
 }
 
 static void b_embedding_dx(Plan& p) {
@@ -1424,11 +1435,14 @@ static void b_embedding_dx(Plan& p) {
       int32_t* hd = seg + T;
       TCB_CUDA(cudaMemsetAsync(seg, 0, size_t(T) * 4, s));
       const int32_t* ids = (const int32_t*)in[0].ptr;
-      const dim3 g2(unsigned(T), unsigned((H + 255) / 256));
+      // persistent-ish grids: ~8 CTAs per SM in total over the column tiles
+      const int64_t ct = (H + 255) / 256;
+      const int64_t gx = std::max<int64_t>(1, std::min<int64_t>(T, (kNumSMs * 8 + ct - 1) / ct));
+      const dim3 g2{unsigned(gx), unsigned(ct)};
       launch_k(k_embed_rank, unsigned((T + 7) / 8), 256, 0, s, ids, srt, seg, hd, T);
       launch_k(k_embed_accum<TD>, g2, 256, 0, s, ids, srt, seg, hd, (const TD*)in[1].ptr, (float*)out[0].ptr,
                                           (float*)part->p, T, H);
-      launch_k(k_embed_fold, g2, 256, 0, s, ids, srt, seg, (const float*)part->p, (float*)out[0].ptr, H);
+      launch_k(k_embed_fold, g2, 256, 0, s, ids, srt, seg, (const float*)part->p, (float*)out[0].ptr, T, H);
     };
   });
 }
