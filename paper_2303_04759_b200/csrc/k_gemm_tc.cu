@@ -45,8 +45,11 @@ constexpr int out_ring() { return AUX ? 2 : 1; }
 template <int BN, int CG, bool AUX>
 struct TcCfg {
   static constexpr int B_ROWS = BN / CG;  // B rows (N) staged by each CTA
+  // MN-major B arrives in 64-column boxes; a 96-row half (BN=192 pair) takes two,
+  // the second over-fetching 32 columns the MMA never reads
+  static constexpr int B_CHUNKS = (B_ROWS + 63) / 64;
   static constexpr int A_BYTES = TC_BM * TC_BK * 2;
-  static constexpr int B_BYTES = B_ROWS * TC_BK * 2;
+  static constexpr int B_BYTES = B_CHUNKS * 64 * TC_BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int EPI_BYTES =
       TC_EPI_WARPS * out_ring<AUX>() * TC_SLOT + (AUX ? TC_EPI_WARPS * TC_AUX_RING * TC_AUX_SLOT : 0);
@@ -443,7 +446,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           mbar_wait(&empty[stage], phase ^ 1);
           // both CTAs' bytes complete on the leader's barrier
           const uint32_t fb = CG == 2 ? mapa(smem_u32(&full[stage]), lead) : smem_u32(&full[stage]);
-          if (rank == 0) mbar_expect_tx(&full[stage], CG * C::STAGE_BYTES);
+          if (rank == 0)
+            mbar_expect_tx(&full[stage], CG * (C::A_BYTES + (Q.tb ? C::B_ROWS * TC_BK * 2 : C::B_BYTES)));
           uint8_t* a_dst = sA + stage * C::A_BYTES;
           uint8_t* b_dst = sB + stage * C::B_BYTES;
           const int k0 = kb * TC_BK;
@@ -457,7 +461,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             tma_load_4d<CG>(b_dst, mB, fb, k0, n0, z2, z1);
           } else {
 #pragma unroll
-            for (int c = 0; c < C::B_ROWS / 64; ++c)
+            for (int c = 0; c < C::B_CHUNKS; ++c)
               tma_load_4d<CG>(b_dst + c * 8192, mB, fb, n0 + c * 64, k0, z2, z1);
           }
           if (++stage == C::STAGES) {
@@ -929,7 +933,7 @@ static void launch_cfg(const GemmArgs* gs, int n, cudaStream_t s) {
 // rounds = ceil(units / concurrent units), a CTA pair is one unit of 74;
 // K_FIX k-blocks model the per-unit fill/drain; eff(.) is the relative
 // mainloop throughput per SM of each tile shape.
-static int stage_bytes(int bn, int cg) { return TC_BM * TC_BK * 2 + (bn / cg) * TC_BK * 2; }
+static int stage_bytes(int bn, int cg) { return TC_BM * TC_BK * 2 + ((bn / cg + 63) / 64) * 64 * TC_BK * 2; }
 static int stages_of(int bn, int cg) {
   const int cpw = (bn / TC_EW + TC_EPI_WARPS / 4 - 1) / (TC_EPI_WARPS / 4);
   const int budget = 227 * 1024 - 1024 - 1024 - TC_EPI_WARPS * out_ring<false>() * TC_SLOT - TC_EPI_WARPS * cpw * TC_EW * 4;
@@ -951,7 +955,7 @@ static TcChoice choose(const GemmArgs& g, bool allow_split) {
     int bn, cg;
     double eff;
   };
-  const Cand cands[] = {{256, 2, 1.0}, {128, 2, 0.6}, {256, 1, 0.75}, {192, 1, 0.7}, {128, 1, 0.55}};
+  const Cand cands[] = {{256, 2, 1.0}, {192, 2, 0.85}, {128, 2, 0.6}, {256, 1, 0.75}, {192, 1, 0.7}, {128, 1, 0.55}};
   const int64_t kblocks = (g.K + TC_BK - 1) / TC_BK;
   constexpr double K_FIX = 6.0, K_RED = 2.0;
   TcChoice best{128, 1, 1};
@@ -1003,6 +1007,7 @@ static void dispatch_tc(const GemmArgs* gs, int n, const TcChoice& c, cudaStream
     return;                                                \
   }
   TC_CASE(256, 2)
+  TC_CASE(192, 2)
   TC_CASE(128, 2)
   TC_CASE(256, 1)
   TC_CASE(192, 1)

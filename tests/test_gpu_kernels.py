@@ -182,7 +182,7 @@ def test_matmul_t_tcgen05(mnk, ta, tb):
     assert rel_err(g[0], o[0]) < BF16_TOL
 
 
-TILES = [(256, 2), (128, 2), (256, 1), (192, 1), (128, 1)]
+TILES = [(256, 2), (192, 2), (128, 2), (256, 1), (192, 1), (128, 1)]
 
 
 @pytest.mark.parametrize("bn,cg", TILES)

@@ -167,7 +167,7 @@ def sweep_splits(iters):
 def sweep(iters):
     """Every tile configuration on every BERT-base shape (cost-model calibration)."""
     for sh in SHAPES[:-1]:
-        for tile in [(256, 2), (128, 2), (256, 1), (192, 1), (128, 1)]:
+        for tile in [(256, 2), (192, 2), (128, 2), (256, 1), (192, 1), (128, 1)]:
             print(json.dumps(run(*sh, iters=iters, tile=tile, cublas=False)), flush=True)
 
 
