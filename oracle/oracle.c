@@ -640,9 +640,11 @@ static void ln_row(const float* x, int64_t H, float eps, float* mean_o, float* r
   *rstd_o = 1.0f / sqrtf(sq * inv + eps);
 }
 
+/* mask (may be NULL): add_layer_norm save_mask -- the residual-branch keep
+ * bits, byte i holding elements 8i..8i+7 (bit k = element 8i+k) */
 static int layer_norm_fwd(const orc_tensor* x, const orc_tensor* r, const orc_tensor* g,
                           const orc_tensor* bta, orc_tensor* y, orc_tensor* s_out,
-                          orc_tensor* mean_t, orc_tensor* rstd_t, const orc_attr* a, int na) {
+                          orc_tensor* mean_t, orc_tensor* rstd_t, orc_tensor* mask, const orc_attr* a, int na) {
   const int64_t H = x->shape[x->rank - 1];
   const int64_t T = numel(x) / H;
   const float eps = (float)adbl(a, na, "eps", 1e-12);
@@ -656,7 +658,13 @@ static int layer_norm_fwd(const orc_tensor* x, const orc_tensor* r, const orc_te
       float v = X[t * H + j];
       if (r) {
         uint64_t idx = (uint64_t)(t * H + j);
-        v = (orc_dropout_keep(seed, salt, idx, p) ? v * sp : 0.0f) + F(r)[t * H + j];
+        const int keep = orc_dropout_keep(seed, salt, idx, p);
+        if (mask) {
+          uint8_t* mb = (uint8_t*)mask->ptr;
+          if ((idx & 7) == 0) mb[idx >> 3] = 0;
+          mb[idx >> 3] |= (uint8_t)(keep << (idx & 7));
+        }
+        v = (keep ? v * sp : 0.0f) + F(r)[t * H + j];
         v = rnd(x->dtype, v);
         F(s_out)[t * H + j] = v;
       }
@@ -720,7 +728,9 @@ static int layer_norm_bwd(const orc_tensor* const* in, int nin, orc_tensor* out,
       if (has_dx) {
         uint64_t idx = (uint64_t)(t * H + j);
         F(&out[3])[t * H + j] =
-            rnd(out[3].dtype, orc_dropout_keep(seed, salt, idx, p) ? dsv * sp : 0.0f);
+            rnd(out[3].dtype, (in[6] ? (((const uint8_t*)in[6]->ptr)[idx >> 3] >> (idx & 7)) & 1
+                                      : orc_dropout_keep(seed, salt, idx, p))
+                                  ? dsv * sp : 0.0f);
       }
       dg[j] += dyv * xh;
       db[j] += dyv;
@@ -1084,16 +1094,21 @@ int orc_exec(const char* op, const orc_tensor* in, int nin, orc_tensor* out, int
   if (!strcmp(op, "attention_dx")) { NEED(3, 1); return attention_bwd(&in[0], &in[1], &in[2], &out[0], A, na); }
   if (!strcmp(op, "layer_norm")) {
     NEED(3, 3);
-    return layer_norm_fwd(&in[0], NULL, &in[1], &in[2], &out[0], NULL, &out[1], &out[2], A, na);
+    return layer_norm_fwd(&in[0], NULL, &in[1], &in[2], &out[0], NULL, &out[1], &out[2], NULL, A, na);
   }
   if (!strcmp(op, "add_layer_norm")) {
     NEED(4, 4);
-    return layer_norm_fwd(&in[0], &in[1], &in[2], &in[3], &out[0], &out[1], &out[2], &out[3], A, na);
+    return layer_norm_fwd(&in[0], &in[1], &in[2], &in[3], &out[0], &out[1], &out[2], &out[3], nout > 4 ? &out[4] : NULL,
+                          A, na);
   }
   if (!strcmp(op, "layer_norm_dx")) {
     NEED(5, 3);
-    const orc_tensor* ins[6] = {&in[0], &in[1], &in[2], &in[3], &in[4], nin > 5 ? &in[5] : NULL};
-    return layer_norm_bwd(ins, nin, out, nout, A, na);
+    /* mask_in: the last input is add_layer_norm's saved keep bits */
+    const int mask_in = (int)aint(A, na, "mask_in", 0) != 0;
+    const int nd = nin - mask_in;
+    const orc_tensor* ins[7] = {&in[0], &in[1], &in[2], &in[3], &in[4], nd > 5 ? &in[5] : NULL,
+                                mask_in ? &in[nin - 1] : NULL};
+    return layer_norm_bwd(ins, nd, out, nout, A, na);
   }
   if (!strcmp(op, "embedding")) { /* out[t,:] = table[ids[t],:] */
     NEED(2, 1);

@@ -258,6 +258,11 @@ struct DropCfg {
   // keep iff the 16-bit draw h >= thr.  h * 2^-16 is exact in f32, so this is
   // the oracle's float(h) * (1/65536) >= p exactly, with thr = ceil(p * 65536)
   uint32_t thr = 0;
+  // optional saved keep bits, one byte per 8 consecutive elements (bit k =
+  // element 8i+k): a forward site writes them, its backward reads them
+  // instead of re-running Philox (add_layer_norm save_mask / layer_norm_dx mask_in)
+  uint8_t* mask_out = nullptr;
+  const uint8_t* mask_in = nullptr;
 };
 // 8 keep bits for indices (q*8 .. q*8+7): one Philox call, 16 bits per element
 // (identical to oracle.c orc_dropout_keep); integer compares: the high half of

@@ -174,6 +174,7 @@ __global__ void __launch_bounds__(256) k_ln_fwd(const T* __restrict__ x, const T
         const int64_t i = row * H + ch * 8;
         if (r) {
           const uint32_t bits = drop_bits8(d, uint64_t(i));
+          if (d.mask_out && (i & 7) == 0) d.mask_out[i >> 3] = uint8_t(bits);
 #pragma unroll
           for (int k = 0; k < 8; ++k) {
             float xv = ((bits >> k) & 1u) ? __fmul_rn(v[q][c][k], d.scale) : 0.0f;
@@ -355,6 +356,7 @@ __global__ void __launch_bounds__(256) k_ln_fwd16(const T* __restrict__ x, const
           float2 rv[4];
           unpack8x2<T>(rq[q][c], rv);
           const uint32_t bits = d.p > 0.0f ? dropout_bits8q(d, uint64_t(i) >> 3) : 0xFFu;
+          if (d.mask_out) d.mask_out[i >> 3] = uint8_t(bits);
           float2 sv[4];
 #pragma unroll
           for (int k = 0; k < 4; ++k) sv[k] = add2(keep2(bits, 2 * k, mul2(v[c][k], sc2)), rv[k]);
@@ -402,8 +404,10 @@ __global__ void __launch_bounds__(256) k_ln_fwd16(const T* __restrict__ x, const
 }
 
 static void build_ln_fwd(Plan& p, bool residual) {
-  if (residual) check_arity(p, 4, 4, 4, 4);
+  if (residual) check_arity(p, 4, 4, 4, 5);
   else check_arity(p, 3, 3, 3, 3);
+  // add_layer_norm save_mask: a 5th output holds the residual-branch keep bits
+  const bool save_mask = residual && p.out.size() == 5;
   const Spec& X = p.in[0];
   const int H = int(X.dim(-1));
   const int64_t rows = X.numel() / H;
@@ -413,12 +417,17 @@ static void build_ln_fwd(Plan& p, bool residual) {
   require(G.dtype == TCB_F32 || G.dtype == X.dtype, p.op + ": gamma dtype");
   const bool gf = G.dtype == TCB_F32;
   const float eps = float(p.attrs.f("eps", 1e-12));
-  const DropCfg d = drop_cfg(p.attrs);
+  const DropCfg d0 = drop_cfg(p.attrs);
+  if (save_mask)
+    require(H % 8 == 0 && d0.p > 0.0f && p.out[4].numel() * dtype_bytes(p.out[4].dtype) * 8 >= X.numel(),
+            p.op + ": save_mask needs p > 0, H % 8 == 0 and a T*H/8-byte mask output");
   dispatch_float(X.dtype, [&](auto* tp) {
    using T = std::remove_pointer_t<decltype(tp)>;
    dispatch_nc(H, [&](auto nc) {
     constexpr int NC = decltype(nc)::value;
     p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
+      DropCfg d = d0;
+      if (save_mask) d.mask_out = static_cast<uint8_t*>(out[4].ptr);
       const int gi = residual ? 2 : 1;
       bool vec = (H % 8 == 0);
       for (int i = 0; i < (residual ? 2 : 1); ++i) vec = vec && reinterpret_cast<uintptr_t>(in[i].ptr) % 16 == 0;
@@ -531,7 +540,7 @@ __global__ void __launch_bounds__(256) k_ln_bwd(const T* __restrict__ sx, const 
         for (int k = 0; k < 8; ++k) o[k] = rs * (g[c][k] - c2 - xh[c][k] * c1);
         st8(ds_o, i, (row + 1) * int64_t(H), vec, o);
         if (dx_o) {
-          const uint32_t bits = drop_bits8(d, uint64_t(i));
+          const uint32_t bits = d.mask_in ? uint32_t(d.mask_in[i >> 3]) : drop_bits8(d, uint64_t(i));
 #pragma unroll
           for (int k = 0; k < 8; ++k) o[k] = ((bits >> k) & 1u) ? o[k] * d.scale : 0.0f;
           st8(dx_o, i, (row + 1) * int64_t(H), vec, o);
@@ -675,7 +684,8 @@ __global__ void __launch_bounds__(256, NC <= 3 ? 2 : 1) k_ln_bwd16(const T* __re
       uint4 w = pack8x2<T>(o);
       *reinterpret_cast<uint4*>(ds_o + i) = w;
       if (dx_o) {
-        const uint32_t bits = d.p > 0.0f ? dropout_bits8q(d, uint64_t(i) >> 3) : 0xFFu;
+        const uint32_t bits = d.mask_in ? uint32_t(d.mask_in[i >> 3])
+                              : d.p > 0.0f ? dropout_bits8q(d, uint64_t(i) >> 3) : 0xFFu;
 #pragma unroll
         for (int k = 0; k < 4; ++k) o[k] = keep2(bits, 2 * k, mul2(o[k], sc2));
         w = pack8x2<T>(o);
@@ -746,16 +756,20 @@ __global__ void __launch_bounds__(1024) k_ln_colsum(const float* __restrict__ ws
 }
 
 static void b_layer_norm_dx(Plan& p) {
-  check_arity(p, 5, 6, 3, 5);
+  // mask_in: the last input holds the forward's saved keep bits
+  const bool mask_in = p.attrs.i("mask_in", 0) != 0;
+  check_arity(p, 5 + int(mask_in), 6 + int(mask_in), 3, 5);
   const Spec& S = p.in[0];
   const int H = int(S.dim(-1));
   const int64_t rows = S.numel() / H;
   require(H <= LN_MAXC * 8 * 32, "layer_norm_dx: hidden size > 2048 unsupported");
   require(p.out[1].dtype == TCB_F32 && p.out[2].dtype == TCB_F32, "layer_norm_dx: dgamma/dbeta are f32");
   const bool gf = p.in[1].dtype == TCB_F32;
-  const DropCfg d = drop_cfg(p.attrs);
+  const DropCfg d0 = drop_cfg(p.attrs);
   const bool bias = p.attrs.i("bias_grad", 0) != 0;
-  const bool has_res = p.in.size() > 5, has_dx = int(p.out.size()) - int(bias) > 3;
+  const bool has_res = int(p.in.size()) - int(mask_in) > 5, has_dx = int(p.out.size()) - int(bias) > 3;
+  const int nin = int(p.in.size());
+  if (mask_in) require(H % 8 == 0, "layer_norm_dx: mask_in needs H % 8 == 0");
   const int di = has_dx ? 4 : 3;  // index of the fused bias-grad output
   require(int(p.out.size()) - int(bias) >= 3, "layer_norm_dx: outputs (ds, dg, db [, dx] [, dbias])");
   if (bias) require(p.out[di].dtype == TCB_F32 && p.out[di].numel() == H, "layer_norm_dx: dbias is f32 [H]");
@@ -781,6 +795,8 @@ static void b_layer_norm_dx(Plan& p) {
       }
     });
     p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
+      DropCfg d = d0;
+      if (mask_in) d.mask_in = static_cast<const uint8_t*>(in[nin - 1].ptr);
       bool vec = H % 8 == 0;
       for (int i : {0, 4}) vec = vec && reinterpret_cast<uintptr_t>(in[i].ptr) % 16 == 0;
       if (has_res) vec = vec && reinterpret_cast<uintptr_t>(in[5].ptr) % 16 == 0;

@@ -235,16 +235,24 @@ inline void register_extension_ops(OpRegistry& r) {
     return TupleType{{x, TensorType{kF32, {Tn}}, TensorType{kF32, {Tn}}}};
   });
   // add_layer_norm(x, r, gamma, beta) -> (y, s = dropout(x) + r, mean, rstd)
-  reg("add_layer_norm", 4, O, [](const V& in, const AttrMap&) -> Type {
+  //   [, keep bits as i32 [T*H/32] (byte i = elements 8i..8i+7) with save_mask and p > 0]
+  reg("add_layer_norm", 4, O, [](const V& in, const AttrMap& a) -> Type {
     auto x = rel::T(in[0], "add_layer_norm"), r = rel::T(in[1], "add_layer_norm");
     if (!(x == r)) throw TypeError("add_layer_norm: x and residual differ");
     int64_t H = x.shape.back(), Tn = numel(x) / H;
-    return TupleType{{x, x, TensorType{kF32, {Tn}}, TensorType{kF32, {Tn}}}};
+    TupleType t{{x, x, TensorType{kF32, {Tn}}, TensorType{kF32, {Tn}}}};
+    if (rel::a_int(a, "save_mask", 0) && ir::attr_double(a, "p", 0.0) > 0.0) {
+      if (H % 8 || numel(x) % 32) throw TypeError("add_layer_norm: save_mask needs H % 8 == 0, T*H % 32 == 0");
+      t.fields.push_back(TensorType{kI32, {numel(x) / 32}});
+    }
+    return t;
   });
   // layer_norm_dx(s, gamma, mean, rstd, dy [, dy2]) -> (ds, dgamma, dbeta [, dx if p > 0]
   //   [, dbias = column sums of the outgoing gradient if bias_grad])
+  //   (mask_in: a last input holds add_layer_norm's saved keep bits)
   reg("layer_norm_dx", -1, O, [](const V& in, const AttrMap& a) -> Type {
-    if (in.size() != 5 && in.size() != 6) throw TypeError("layer_norm_dx: 5 or 6 inputs");
+    const size_t nm = rel::a_int(a, "mask_in", 0) ? 1 : 0;
+    if (in.size() != 5 + nm && in.size() != 6 + nm) throw TypeError("layer_norm_dx: 5 or 6 inputs (+ mask)");
     auto s = rel::T(in[0], "layer_norm_dx");
     TensorType g{kF32, {s.shape.back()}};
     TupleType t{{s, g, g}};

@@ -258,8 +258,13 @@ inline void register_default_adjoints() {
     if (!c.dout[0]) return {nullptr, nullptr, nullptr, nullptr};
     auto gm = arg_var(c.let.value, 2);
     const auto& at = c.let.value->call_attrs;
-    auto t = c.g.op("layer_norm_dx", {c.g.get(c.let.var, 1), gm, c.g.get(c.let.var, 2), c.g.get(c.let.var, 3), c.dout[0]},
-                    pick(at, {"p", "seed", "salt"}));
+    std::vector<VarPtr> args{c.g.get(c.let.var, 1), gm, c.g.get(c.let.var, 2), c.g.get(c.let.var, 3), c.dout[0]};
+    AttrMap la = pick(at, {"p", "seed", "salt"});
+    if (c.let.var->ty.is_tuple() && c.let.var->ty.tuple().fields.size() > 4) {  // saved keep bits
+      args.push_back(c.g.get(c.let.var, 4));
+      la["mask_in"] = std::int64_t(1);
+    }
+    auto t = c.g.op("layer_norm_dx", args, la);
     VarPtr ds = c.g.get(t, 0);
     VarPtr dx = ir::attr_double(at, "p", 0.0) > 0.0 ? c.g.get(t, 3) : ds;
     return {dx, ds, c.g.get(t, 1), c.g.get(t, 2)};
@@ -560,16 +565,17 @@ inline FusionStats fuse(LetSeq& s, bool patterns = true) {
       if (done) continue;
     }
     // 2. layer_norm_dx(s, g, m, r, add(a, b)) -> layer_norm_dx(s, g, m, r, a, b)
-    if (op == "layer_norm_dx" && b.value->args.size() == 5) {
+    const size_t lnm = op == "layer_norm_dx" && ir::attr_int(b.value->call_attrs, "mask_in", 0) ? 1 : 0;
+    if (op == "layer_norm_dx" && b.value->args.size() == 5 + lnm) {
       auto src = arg_var(b.value, 4);
       auto* p = producer(src);
       if (p && p->value->op == "add" && single(src)) {
         auto a = arg_var(p->value, 0), c = arg_var(p->value, 1);
         if (a && c && a->ty == src->ty && c->ty == src->ty) {
-          auto call = ir::call("layer_norm_dx",
-                               {b.value->args[0], b.value->args[1], b.value->args[2], b.value->args[3],
-                                p->value->args[0], p->value->args[1]},
-                               b.value->call_attrs);
+          std::vector<ExprPtr> nargs{b.value->args[0], b.value->args[1], b.value->args[2], b.value->args[3],
+                                     p->value->args[0], p->value->args[1]};
+          if (lnm) nargs.push_back(b.value->args[5]);  // the mask stays last
+          auto call = ir::call("layer_norm_dx", nargs, b.value->call_attrs);
           call->ty = b.value->ty;
           b.value = call;
           removed.insert(def[src.get()]);

@@ -239,6 +239,12 @@ inline TrainStep build_train_step(const ModelCfg& c) {
     return y->ty.is_tuple() ? g.get(y, 0) : y;
   };
   AttrMap attn_attrs{{"heads", c.A}, {"seq", c.S}, {"causal", std::int64_t(c.kind == "gpt2")}};
+  // residual LayerNorms save their dropout keep bits for the backward (no Philox re-run)
+  auto ln_attrs = [&]() {
+    AttrMap a{{"eps", c.ln_eps}};
+    if (c.p > 0.0 && c.H % 8 == 0 && (c.T() * c.H) % 32 == 0) a["save_mask"] = std::int64_t(1);
+    return a;
+  };
 
   // ---- embeddings
   VarPtr h;
@@ -260,11 +266,11 @@ inline TrainStep build_train_step(const ModelCfg& c) {
       VarPtr qkv = linear(h, p + "qkv.w", p + "qkv.b");
       VarPtr at = g.op("attention", {qkv}, drop_attrs(attn_attrs));
       VarPtr ao = linear(g.get(at, 0), p + "proj.w", p + "proj.b");
-      VarPtr l1 = g.op("add_layer_norm", {ao, h, W[p + "ln1.g"], W[p + "ln1.b"]}, drop_attrs({{"eps", c.ln_eps}}));
+      VarPtr l1 = g.op("add_layer_norm", {ao, h, W[p + "ln1.g"], W[p + "ln1.b"]}, drop_attrs(ln_attrs()));
       VarPtr h1 = g.get(l1, 0);
       VarPtr f = linear(h1, p + "ffn1.w", p + "ffn1.b", "gelu");
       VarPtr f2 = linear(f, p + "ffn2.w", p + "ffn2.b");
-      VarPtr l2 = g.op("add_layer_norm", {f2, h1, W[p + "ln2.g"], W[p + "ln2.b"]}, drop_attrs({{"eps", c.ln_eps}}));
+      VarPtr l2 = g.op("add_layer_norm", {f2, h1, W[p + "ln2.g"], W[p + "ln2.b"]}, drop_attrs(ln_attrs()));
       h = g.get(l2, 0);
     } else {  // GPT-2 pre-LN: h = h + drop(attn(ln1(h))); h = h + drop(mlp(ln2(h)))
       VarPtr x1 = g.get(g.op("layer_norm", {h, W[p + "ln1.g"], W[p + "ln1.b"]}, {{"eps", 1e-5}}), 0);

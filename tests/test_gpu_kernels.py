@@ -471,6 +471,34 @@ def test_layer_norm_fwd_bwd_shapes(H, gdt):
     assert rel_err(g[1], o[1]) < 1e-5 and rel_err(g[2], o[2]) < 1e-5 and rel_err(g[4], o[4]) < 1e-4
 
 
+@pytest.mark.parametrize("T", [77, 300])
+def test_layer_norm_saved_dropout_mask(T):
+    """add_layer_norm(save_mask) writes the residual-branch keep bits (one byte
+    per 8 elements, bit-exact vs the oracle's Philox draws); layer_norm_dx
+    (mask_in) reading them gives bit-identical gradients to re-running Philox."""
+    H = 768
+    x, r = rn(T, H), rn(T, H)
+    gm, bt = rn(H, lo=0.5, hi=1.5), rn(H, lo=-0.1, hi=0.1)
+    attrs = {"eps": 1e-12, "p": 0.1, "seed": 5, "salt": 17}
+    n32 = T * H // 32
+    g, o = run_both("add_layer_norm", [(x, BF16), (r, BF16), (gm, BF16), (bt, BF16)],
+                    [((T, H), BF16), ((T, H), BF16), ((T,), F32), ((T,), F32), ((n32,), I32)],
+                    {**attrs, "save_mask": 1})
+    assert bits_equal(g[1], o[1]) and np.array_equal(g[4].view(np.uint8), o[4].view(np.uint8))
+    keep = np.unpackbits(g[4].view(np.uint8), bitorder="little")[: T * H]
+    from oracle import oracle_py as O
+    assert np.array_equal(keep, O.dropout_keep_mask(5, 17, T * H, 0.1))
+    s, mean, rstd, mask = o[1], o[2], o[3], g[4]
+    dy, dy2 = rn(T, H), rn(T, H)
+    outs = [((T, H), BF16), ((H,), F32), ((H,), F32), ((T, H), BF16)]
+    ins = [(s, BF16), (gm, BF16), (mean, F32), (rstd, F32), (dy, BF16), (dy2, BF16)]
+    g1, o1 = run_both("layer_norm_dx", ins + [(mask, I32)], outs, {**attrs, "mask_in": 1})
+    g0, _ = run_both("layer_norm_dx", ins, outs, attrs)
+    for a, b in zip(g1, g0):
+        assert bits_equal(a, b)
+    assert rel_err(g1[3], o1[3]) < 5e-3 and rel_err(g1[1], o1[1]) < 1e-5
+
+
 def test_layer_norm_dx_f32():
     T, H = 64, 128
     s, gm = rn(T, H), rn(H, lo=0.5, hi=1.5)
