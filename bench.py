@@ -235,9 +235,14 @@ def max_batch_report(stream_sync_free_bytes: int):
     import torch
     from paper_2303_04759_b200.session import ModelConfig, Session, max_batch_under_remat, synthetic_batch
     budget = int(stream_sync_free_bytes * 0.92) - (2 << 30)
-    b_remat, gi = max_batch_under_remat(ModelConfig.bert_base, budget)
-    b_plain, _ = max_batch_under_remat(ModelConfig.bert_base, budget, remat=False)
-    out = {"model": "bert-base seq128 bf16 Adam", "budget_gb": round(budget / 1e9, 1), "max_batch": b_remat,
+    # kernels' batch-proportional scratch outside the planned arena (BERT-base,
+    # per token: embedding_dx chunk partials 3 KB, LayerNorm-backward partials
+    # ~2.3 KB over its plans, bias-grad colsum partials ~0.8 KB, sort buffers)
+    reserve = 128 * 6656
+    b_remat, gi = max_batch_under_remat(ModelConfig.bert_base, budget, reserve_per_sample=reserve)
+    b_plain, _ = max_batch_under_remat(ModelConfig.bert_base, budget, remat=False, reserve_per_sample=reserve)
+    out = {"model": "bert-base seq128 bf16 Adam", "budget_gb": round(budget / 1e9, 1),
+           "scratch_reserve_gb": round(b_remat * reserve / 1e9, 1), "max_batch": b_remat,
            "max_batch_no_remat": b_plain, "remat_replays": gi.get("remat_replays"),
            "planned_bytes_gb": round((gi.get("arena_plan_bytes", 0) + gi.get("state_bytes", 0)) / 1e9, 1)}
     try:

@@ -1426,6 +1426,24 @@ __global__ void __launch_bounds__(256) k_embed_accum(const int32_t* __restrict__
   }
 }
 
+static std::shared_ptr<Scratch> emb_part_scratch(size_t bytes) {
+  struct Dev {
+    std::vector<std::shared_ptr<Scratch>> all;  // kept alive: captured graphs may hold old ones
+    size_t cap = 0;
+  };
+  static std::mutex mu;
+  static std::map<int, Dev> per_dev;  // per device (a process may drive several)
+  int dev = 0;
+  TCB_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> g(mu);
+  Dev& d = per_dev[dev];
+  if (d.all.empty() || bytes > d.cap) {
+    d.all.push_back(std::make_shared<Scratch>(bytes));
+    d.cap = bytes;
+  }
+  return d.all.back();
+}
+
 static void b_embedding_dx(Plan& p) {
   check_arity(p, 2, 3, 1, 1);
   require(p.in[0].dtype == TCB_I32, "embedding_dx: ids must be i32");
@@ -1435,7 +1453,10 @@ static void b_embedding_dx(Plan& p) {
   const bool has_base = p.in.size() > 2;
   if (has_base) require(p.in[2].dtype == TCB_F32 && p.in[2].numel() == V * H, "embedding_dx: base is f32 [V,H]");
   auto sorted = std::make_shared<Scratch>(size_t(T) * 12);  // sorted[T] ++ seg_len[T] ++ seg_head[T]
-  auto part = std::make_shared<Scratch>(size_t(T) * H * 4);  // chunk partials of long segments
+  // chunk partials of long segments: one buffer shared by every embedding_dx
+  // plan of the process (they run one after another on the step's stream),
+  // grown at plan creation -- before any graph capture -- and never freed
+  auto part = emb_part_scratch(size_t(T) * H * 4);
   p.nkernels = 4;
   dispatch_float(p.in[1].dtype, [&](auto* tp) {
     using TD = std::remove_pointer_t<decltype(tp)>;

@@ -537,7 +537,9 @@ inline std::pair<FunctionPtr, RematPlan> rematerialize(const ir::FunctionIR& fn,
       if (x.param >= 0 || x.parent >= 0 || x.producer < 0 || x.def >= i || x.last <= i || x.last >= n) continue;
       if (needed.count(int(u))) continue;
       const auto& pe = seq.lets[x.producer].value;
-      if (!replayable(pe) || seq.lets[x.producer].var->ty.is_tuple()) continue;
+      // tuple producers are replayed whole (every field recomputed; field uses
+      // after the split are redirected to the replay, see below)
+      if (!replayable(pe)) continue;
       // next use after i
       int next = -1, uses_after = 0;
       for (int k = i + 1; k < n; ++k)
@@ -578,19 +580,43 @@ inline std::pair<FunctionPtr, RematPlan> rematerialize(const ir::FunctionIR& fn,
     auto ne = std::make_shared<ir::Expr>(*pb.value);
     ne->serial = ir::detail::next_serial();
     const ir::Var* old = pb.var.get();
+    // a tuple producer's fields are read through get-lets; those defined before
+    // the split whose vars are used after it get a twin on the replay
+    std::unordered_map<const ir::Var*, ir::VarPtr> twin;
+    std::vector<std::pair<ir::VarPtr, ir::ExprPtr>> twin_lets;
+    if (pb.var->ty.is_tuple())
+      for (int k = 0; k < best_next; ++k) {
+        const auto& g = seq.lets[k];
+        if (g.value->kind != ExprKind::TupleGet || g.value->args[0]->kind != ExprKind::VarRef ||
+            g.value->args[0]->var.get() != old)
+          continue;
+        auto tv = ir::make_var(g.var->id + "_r" + std::to_string(plan.replays), g.var->ty, g.var->attrs);
+        auto te = ir::tuple_get(ir::var_ref(nv), g.value->index);
+        te->ty = g.value->ty;
+        twin[g.var.get()] = tv;
+        twin_lets.push_back({tv, te});
+      }
     LetSeq out;
     out.ret = seq.ret;
     for (int k = 0; k < n; ++k) {
-      if (k == best_next) out.lets.push_back({nv, ne});
+      if (k == best_next) {
+        out.lets.push_back({nv, ne});
+        for (auto& t : twin_lets) out.lets.push_back({t.first, t.second});
+      }
       auto b = seq.lets[k];
       if (k >= best_next) {
         bool touched = false;
         auto e2 = std::make_shared<ir::Expr>(*b.value);
-        for (auto& a : e2->args)
-          if (a->kind == ExprKind::VarRef && a->var.get() == old) {
+        for (auto& a : e2->args) {
+          if (a->kind != ExprKind::VarRef) continue;
+          if (a->var.get() == old) {
             a = ir::var_ref(nv);
             touched = true;
+          } else if (auto it = twin.find(a->var.get()); it != twin.end()) {
+            a = ir::var_ref(it->second);
+            touched = true;
           }
+        }
         if (touched) b.value = e2;
       }
       out.lets.push_back(b);

@@ -151,7 +151,9 @@ def plan_fits(cfg: ModelConfig, budget: int, remat: bool) -> tuple[bool, dict]:
     c = ModelConfig(**{f.name: getattr(cfg, f.name) for f in fields(cfg) if f.name != "extra"})
     c.extra = dict(cfg.extra)
     if remat:
-        c.extra["budget"] = int(budget)
+        # the remat pass bounds the liveness peak; address packing of the arena
+        # adds fragmentation on top, so it aims 1.5% below the budget
+        c.extra["budget"] = int(budget * 0.985)
     try:
         gi = graph_info(c)
     except RuntimeError:
@@ -159,23 +161,28 @@ def plan_fits(cfg: ModelConfig, budget: int, remat: bool) -> tuple[bool, dict]:
     return gi["arena_plan_bytes"] + gi["state_bytes"] <= budget, gi
 
 
-def max_batch_under_remat(factory, budget: int, b0: int = 32, remat: bool = True) -> tuple[int, dict]:
+def max_batch_under_remat(factory, budget: int, b0: int = 32, remat: bool = True,
+                          reserve_per_sample: int = 0) -> tuple[int, dict]:
     """Largest per-GPU batch the planner fits in `budget` bytes: doubling from
     b0, then bisection ('double B until BudgetInfeasible,
-    then bisect').  Returns (B, graph_info at B)."""
-    ok, gi = plan_fits(factory(B=b0), budget, remat)
+    then bisect').  reserve_per_sample: bytes per sample kept outside the
+    planned arena for the kernels' own batch-proportional scratch (partial
+    sums, sort buffers), so the arena budget at batch B is budget - B * reserve.
+    Returns (B, graph_info at B)."""
+    fits = lambda B: plan_fits(factory(B=B), budget - B * reserve_per_sample, remat)  # noqa: E731
+    ok, gi = fits(b0)
     if not ok:
         return 0, {}
     lo, hi, best = b0, None, gi
     while hi is None:
-        ok, g = plan_fits(factory(B=lo * 2), budget, remat)
+        ok, g = fits(lo * 2)
         if ok:
             lo, best = lo * 2, g
         else:
             hi = lo * 2
     while hi - lo > 1:
         mid = (lo + hi) // 2
-        ok, g = plan_fits(factory(B=mid), budget, remat)
+        ok, g = fits(mid)
         if ok:
             lo, best = mid, g
         else:

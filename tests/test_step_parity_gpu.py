@@ -108,3 +108,32 @@ def test_deferred_folds_bit_identical(monkeypatch):
     l0, p0, k0 = run(False)
     assert np.array_equal(l1, l0) and np.array_equal(p1, p0)
     assert k1 < k0  # the per-op fold kernels became one flush
+
+
+def test_remat_with_tuple_replays_bit_identical():
+    """Rematerialisation under a budget of 75% of the unremat plan
+    replays multi-output producers too (add_layer_norm with its saved dropout
+    mask, attention, the GELU linear) -- losses and parameters stay
+    bit-identical to the run without remat."""
+    from paper_2303_04759_b200.session import graph_info
+    cfg = ModelConfig.tiny(dtype="bf16", opt="adam", lr=1e-3, L=2, p=0.1)
+    gi = graph_info(cfg)
+    budget = int(0.75 * (gi["arena_plan_bytes"] + gi["state_bytes"]))
+    cfg_r = ModelConfig.tiny(dtype="bf16", opt="adam", lr=1e-3, L=2, p=0.1)
+    cfg_r.extra["budget"] = budget
+
+    def run(c):
+        s = Session(c)
+        s.init_params()
+        losses = []
+        for k in range(2):
+            ids, labels = synthetic_batch(c, seed=c.seed_d + k)
+            s.set_batch(ids, labels)
+            s.step(graph=True)
+            losses.append(s.loss())
+        return np.array(losses), s.read("params"), s.info()
+
+    l0, p0, _ = run(cfg)
+    l1, p1, info = run(cfg_r)
+    assert info["remat_replays"] > 0
+    assert np.array_equal(l0, l1) and np.array_equal(p0, p1)
