@@ -1457,7 +1457,7 @@ static void b_embedding_dx(Plan& p) {
   // plan of the process (they run one after another on the step's stream),
   // grown at plan creation -- before any graph capture -- and never freed
   auto part = emb_part_scratch(size_t(T) * H * 4);
-  p.nkernels = 4;
+  p.nkernels = 3;  // rank, accumulate, fold (+ a memset / memcpy node)
   dispatch_float(p.in[1].dtype, [&](auto* tp) {
     using TD = std::remove_pointer_t<decltype(tp)>;
     p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
