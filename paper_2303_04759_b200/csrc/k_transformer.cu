@@ -1503,8 +1503,11 @@ __global__ void k_ce_count(const int32_t* __restrict__ labels, int64_t T, int64_
 }
 
 template <typename T>
-__global__ void __launch_bounds__(512) k_ce_row(const T* __restrict__ x, const int32_t* __restrict__ labels,
-                                                T* __restrict__ dx, float* __restrict__ row_loss,
+// dx may alias x (the planner runs cross_entropy in place, logits -> dlogits):
+// every element is read by the thread that later overwrites it, and the label
+// logit is read before the block barrier that precedes any write
+__global__ void __launch_bounds__(512) k_ce_row(const T* x, const int32_t* __restrict__ labels,
+                                                T* dx, float* __restrict__ row_loss,
                                                 const float* __restrict__ inv_n_p, int64_t Vp, int64_t V,
                                                 int64_t ign, float gscale, int* __restrict__ err, bool vec) {
   TCB_PDL_ENTRY();
@@ -1531,6 +1534,7 @@ __global__ void __launch_bounds__(512) k_ce_row(const T* __restrict__ x, const i
     if (threadIdx.x == 0) atomicExch(err, 1);
     return;
   }
+  const float xlab = threadIdx.x == 0 ? to_f(xr[lab]) : 0.0f;  // before any thread may overwrite it
   // pass 1: online max / sum
   float m = -INFINITY, s = 0.0f;
   const int64_t nch = V / 8;
@@ -1569,7 +1573,7 @@ __global__ void __launch_bounds__(512) k_ce_row(const T* __restrict__ x, const i
   float S = 0.0f;
   for (int w = 0; w < nw; ++w) S += ss[w] * expf(sm[w] - M);
   const float lse = M + logf(S);
-  if (threadIdx.x == 0) row_loss[t] = lse - to_f(xr[lab]);
+  if (threadIdx.x == 0) row_loss[t] = lse - xlab;
   if (!dr) return;
   // pass 2: gradient
   const float inv_s = 1.0f / S;

@@ -15,6 +15,8 @@
 #pragma once
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <limits>
 #include <map>
 #include <numeric>
@@ -61,6 +63,7 @@ inline bool inplace_safe(const std::string& base, int in_idx, int out_idx) {
   if (base == "sgd_update") return in_idx == 0 && out_idx == 0;
   if (base == "add_scalar") return in_idx == 0 && out_idx == 0;
   if (base == "embedding_dx") return in_idx == 2 && out_idx == 0;  // base + scatter
+  if (base == "cross_entropy") return in_idx == 0 && out_idx == 1;  // logits -> dlogits (k_ce_row)
   return false;
 }
 
@@ -202,10 +205,26 @@ inline Layout build_layout(const ir::FunctionIR& fn, const std::vector<std::pair
     if (b.var->ty.is_tuple()) {
       const auto& fields = b.var->ty.tuple().fields;
       auto tf = tuple_fields.find(b.var.get());
+      std::set<int> taken;  // input units already handed to an earlier field
       for (size_t k = 0; k < fields.size(); ++k) {
         int pu = -1;
-        if (tf != tuple_fields.end() && tf->second.count(int(k)))
-          pu = try_bind(tf->second.at(int(k)), i, e, int(k));
+        const ir::Var* fv = (tf != tuple_fields.end() && tf->second.count(int(k))) ? tf->second.at(int(k)) : nullptr;
+        if (fv) pu = try_bind(fv, i, e, int(k));
+        // plain in-place reuse for a field (same rules as single-output ops)
+        if (pu < 0 && !(fv && bind.count(fv))) {
+          for (size_t a = 0; a < e->args.size() && pu < 0; ++a) {
+            if (e->args[a]->kind != ExprKind::VarRef || !inplace_safe(base, int(a), int(k))) continue;
+            const ir::Var* av = e->args[a]->var.get();
+            const auto& rs = L.refs.at(av);
+            if (rs.size() != 1) continue;
+            const Ref& r = rs[0];
+            const Unit& cu = L.units[r.unit];
+            if (cu.param < 0 && cu.parent < 0 && r.off == 0 && r.bytes == cu.bytes && cu.bytes == nbytes(fields[k]) &&
+                unit_refs[r.unit] == 1 && last_use[av] == i && !ret_index.count(av) && !taken.count(r.unit))
+              pu = r.unit;
+          }
+          if (pu >= 0) taken.insert(pu);
+        }
         if (pu >= 0) outs.push_back(Ref{pu, 0, nbytes(fields[k])});
         else {
           int u = new_unit(nbytes(fields[k]), i, i);
@@ -531,6 +550,7 @@ inline std::pair<FunctionPtr, RematPlan> rematerialize(const ir::FunctionIR& fn,
     std::unordered_map<const ir::Var*, int> def;
     for (int k = 0; k < n; ++k) def[seq.lets[k].var.get()] = k;
     int best_u = -1, best_next = -1;
+    std::vector<std::pair<const ir::Var*, int>> best_chain;  // (dead input var, its producer let)
     double best_score = std::numeric_limits<double>::infinity();
     for (size_t u = 0; u < L.units.size(); ++u) {
       const Unit& x = L.units[u];
@@ -551,21 +571,62 @@ inline std::pair<FunctionPtr, RematPlan> rematerialize(const ir::FunctionIR& fn,
                 ++uses_after;
               }
       if (next < 0) continue;
-      // replay inputs must be live at `next` (params, or units whose last >= next)
+      // replay inputs must be live at `next` (params, or units whose last >=
+      // next); an input that is dead there may itself be replayed first when
+      // its producer is a single-output replayable op whose inputs are live
+      // (a depth-2 chain; SPEC.md:485 allows up to 3)
       bool ok = true;
+      double cost = op_cost(pe);
+      std::vector<std::pair<const ir::Var*, int>> chain;
       for (auto& a : pe->args) {
-        if (a->kind != ExprKind::VarRef) continue;
+        if (a->kind != ExprKind::VarRef || !ok) continue;
+        bool dead = false;
         for (auto& r : L.refs.at(a->var.get())) {
           const Unit& iu = L.units[L.root(r.unit).first];
-          if (iu.param < 0 && iu.last < next) ok = false;
+          if (iu.param < 0 && iu.last < next) dead = true;
+        }
+        if (!dead) continue;
+        auto dit = def.find(a->var.get());
+        if (dit == def.end()) {
+          ok = false;
+          continue;
+        }
+        const auto& p2 = seq.lets[dit->second];
+        if (p2.value->kind != ExprKind::Call || p2.var->ty.is_tuple() || !replayable(p2.value)) {
+          ok = false;
+          continue;
+        }
+        for (auto& a2 : p2.value->args) {
+          if (a2->kind != ExprKind::VarRef) continue;
+          for (auto& r2 : L.refs.at(a2->var.get())) {
+            const Unit& iu2 = L.units[L.root(r2.unit).first];
+            if (iu2.param < 0 && iu2.last < next) ok = false;
+          }
+        }
+        if (ok) {
+          chain.push_back({a->var.get(), dit->second});
+          cost += op_cost(p2.value);
         }
       }
       if (!ok) continue;
-      double score = op_cost(pe) * uses_after / double(std::max<int64_t>(1, x.bytes));
+      double score = cost * uses_after / double(std::max<int64_t>(1, x.bytes));
       if (score < best_score) {
         best_score = score;
         best_u = int(u);
         best_next = next;
+        best_chain = chain;
+      }
+    }
+    if (best_u < 0 && std::getenv("TB_REMAT_DEBUG")) {  // why nothing is evictable here
+      std::fprintf(stderr, "remat: peak %lld at %d (%s), floor %lld, budget %lld\n", (long long)mp.peak, i,
+                   seq.lets[i].value->op.c_str(), (long long)floor_i, (long long)budget);
+      for (size_t u = 0; u < L.units.size(); ++u) {
+        const Unit& x = L.units[u];
+        if (x.param >= 0 || x.parent >= 0 || x.def >= i || x.last <= i || x.bytes < (int64_t(256) << 20)) continue;
+        const char* why = needed.count(int(u)) ? "needed" : x.producer < 0 ? "no producer"
+                          : !replayable(seq.lets[x.producer].value) ? "not replayable" : "inputs dead / no next";
+        std::fprintf(stderr, "  unit %zu %lld MB def %d last %d %s: %s\n", u, (long long)(x.bytes >> 20), x.def,
+                     x.last, x.producer >= 0 ? seq.lets[x.producer].value->op.c_str() : "-", why);
       }
     }
     if (best_u < 0) {
@@ -579,6 +640,18 @@ inline std::pair<FunctionPtr, RematPlan> rematerialize(const ir::FunctionIR& fn,
     auto nv = ir::make_var(pb.var->id + "_r" + std::to_string(plan.replays), pb.var->ty, pb.var->attrs);
     auto ne = std::make_shared<ir::Expr>(*pb.value);
     ne->serial = ir::detail::next_serial();
+    // depth-2 chain: replay the dead inputs' producers first, feed the replay
+    std::vector<std::pair<ir::VarPtr, ir::ExprPtr>> chain_lets;
+    for (auto& [cv, cl] : best_chain) {
+      const auto& cb = seq.lets[cl];
+      auto cv2 = ir::make_var(cb.var->id + "_r" + std::to_string(plan.replays), cb.var->ty, cb.var->attrs);
+      auto ce = std::make_shared<ir::Expr>(*cb.value);
+      ce->serial = ir::detail::next_serial();
+      chain_lets.push_back({cv2, ce});
+      for (auto& a : ne->args)
+        if (a->kind == ExprKind::VarRef && a->var.get() == cv) a = ir::var_ref(cv2);
+      plan.replays++;
+    }
     const ir::Var* old = pb.var.get();
     // a tuple producer's fields are read through get-lets; those defined before
     // the split whose vars are used after it get a twin on the replay
@@ -600,6 +673,7 @@ inline std::pair<FunctionPtr, RematPlan> rematerialize(const ir::FunctionIR& fn,
     out.ret = seq.ret;
     for (int k = 0; k < n; ++k) {
       if (k == best_next) {
+        for (auto& c : chain_lets) out.lets.push_back({c.first, c.second});
         out.lets.push_back({nv, ne});
         for (auto& t : twin_lets) out.lets.push_back({t.first, t.second});
       }

@@ -588,6 +588,27 @@ def test_cross_entropy(dt):
     assert np.all(g[1][:, V:] == 0) and np.all(g[1][::7] == 0)
 
 
+@pytest.mark.parametrize("dt", [F32, BF16])
+def test_cross_entropy_in_place(dt):
+    """The planner runs cross_entropy in place (dlogits overwrite the logits):
+    bit-identical to separate buffers, label logits included."""
+    import torch
+    from gpu_util import from_torch, to_torch
+    from paper_2303_04759_b200.runtime import run_op
+    T, V, Vp = 300, 1000, 1024
+    x = rn(T, Vp, lo=-4, hi=4)
+    lab = RNG.integers(0, V, size=T).astype(np.int32)
+    lab[::5] = -100
+    attrs = {"classes": V, "ignore_index": -100}
+    xs, ls = to_torch(x, dt), to_torch(lab, I32)
+    sep = [from_torch(t) for t in run_op("cross_entropy", [xs, ls], [((1,), F32), ((T, Vp), dt)], attrs)]
+    xi = xs.clone()
+    loss = torch.empty(1, device=xi.device, dtype=torch.float32)
+    run_op("cross_entropy", [xi, ls], [((1,), F32), ((T, Vp), dt)], attrs, outs=[loss, xi])
+    torch.cuda.synchronize()
+    assert bits_equal(from_torch(loss), sep[0]) and bits_equal(from_torch(xi), sep[1])
+
+
 def test_unimplemented_is_loud():
     from paper_2303_04759_b200.runtime import Plan, UnimplementedOp
     with pytest.raises(UnimplementedOp):
