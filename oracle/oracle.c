@@ -516,7 +516,8 @@ static void attn_heads(const orc_tensor* qkv, attn_t* at, const orc_attr* a, int
 /* Fused attention forward (extension op).  Rounding points
  * mirror the b200 pipeline: scores f32, P and dropout(P) and ctx rounded to the
  * activation dtype. */
-static int attention_fwd(const orc_tensor* qkv, orc_tensor* ctx, orc_tensor* probs,
+/* mask (may be NULL): the dropout keep bits, word (z*S + i)*4 + (j >> 5), bit j & 31 */
+static int attention_fwd(const orc_tensor* qkv, orc_tensor* ctx, orc_tensor* probs, orc_tensor* mask,
                          const orc_attr* a, int na) {
   attn_t at;
   attn_heads(qkv, &at, a, na);
@@ -550,7 +551,13 @@ static int attention_fwd(const orc_tensor* qkv, orc_tensor* ctx, orc_tensor* pro
           float pv = rnd(at.dt, s[j] / sum);
           P[(z * S + i) * S + j] = pv;
           uint64_t idx = (uint64_t)((z * S + i) * S + j);
-          float dv = orc_dropout_keep(at.seed, at.salt, idx, at.p) ? pv * sp : 0.0f;
+          const int keep = orc_dropout_keep(at.seed, at.salt, idx, at.p);
+          if (mask) {
+            uint32_t* mw = (uint32_t*)mask->ptr + (z * S + i) * 4 + (j >> 5);
+            if ((j & 31) == 0) *mw = 0xffffffffu;
+            if (!keep) *mw &= ~(1u << (j & 31));
+          }
+          float dv = keep ? pv * sp : 0.0f;
           pd[i * S + j] = rnd(at.dt, dv);
         }
       }
@@ -567,7 +574,7 @@ static int attention_fwd(const orc_tensor* qkv, orc_tensor* ctx, orc_tensor* pro
 }
 
 static int attention_bwd(const orc_tensor* qkv, const orc_tensor* probs, const orc_tensor* dctx,
-                         orc_tensor* dqkv, const orc_attr* a, int na) {
+                         const orc_tensor* mask, orc_tensor* dqkv, const orc_attr* a, int na) {
   attn_t at;
   attn_heads(qkv, &at, a, na);
   const int64_t S = at.S, dh = at.dh, H = at.H, H3 = 3 * at.H;
@@ -589,7 +596,8 @@ static int attention_bwd(const orc_tensor* qkv, const orc_tensor* probs, const o
           for (int64_t d = 0; d < dh; ++d)
             acc += dC[(b * S + i) * H + h * dh + d] * X[(b * S + j) * H3 + 2 * H + h * dh + d];
           uint64_t idx = (uint64_t)((z * S + i) * S + j);
-          int keep = orc_dropout_keep(at.seed, at.salt, idx, at.p);
+          int keep = mask ? (int)((((const uint32_t*)mask->ptr)[(z * S + i) * 4 + (j >> 5)] >> (j & 31)) & 1u)
+                          : orc_dropout_keep(at.seed, at.salt, idx, at.p);
           float pv = P[(z * S + i) * S + j];
           dp[j] = keep ? acc * sp : 0.0f;
           pd[i * S + j] = rnd(at.dt, keep ? pv * sp : 0.0f);
@@ -1090,8 +1098,14 @@ int orc_exec(const char* op, const orc_tensor* in, int nin, orc_tensor* out, int
     }
     return 0;
   }
-  if (!strcmp(op, "attention")) { NEED(1, 2); return attention_fwd(&in[0], &out[0], &out[1], A, na); }
-  if (!strcmp(op, "attention_dx")) { NEED(3, 1); return attention_bwd(&in[0], &in[1], &in[2], &out[0], A, na); }
+  if (!strcmp(op, "attention")) {
+    NEED(1, 2);
+    return attention_fwd(&in[0], &out[0], &out[1], nout > 2 ? &out[2] : NULL, A, na);
+  }
+  if (!strcmp(op, "attention_dx")) {
+    NEED(3, 1);
+    return attention_bwd(&in[0], &in[1], &in[2], nin > 3 ? &in[3] : NULL, &out[0], A, na);
+  }
   if (!strcmp(op, "layer_norm")) {
     NEED(3, 3);
     return layer_norm_fwd(&in[0], NULL, &in[1], &in[2], &out[0], NULL, &out[1], &out[2], NULL, A, na);

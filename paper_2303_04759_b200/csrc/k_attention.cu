@@ -158,8 +158,10 @@ __global__ void __launch_bounds__(AT_FWD_THREADS) k_attn_fwd(const __grid_consta
                   k ? 1u : 0u);
       tc_commit<1>(&bar[2]);
     }
-    // dropout keep bits overlap the QK^T MMA
+    // dropout keep bits overlap the QK^T MMA (and are saved for the backward)
     const uint32_t kb = keep_bits32(a.d, (uint64_t(z) * a.S + row) * a.S, j0, a.S);
+    if (a.d.mask_out && row < a.S)
+      reinterpret_cast<uint32_t*>(a.d.mask_out)[(uint64_t(z) * a.S + row) * 4 + cq] = kb;
     mbar_wait(&bar[2], it & 1);
     tc_fence_after();
     T(2);
@@ -360,7 +362,13 @@ __global__ void __launch_bounds__(AT_THREADS) k_attn_bwd(const __grid_constant__
     tc_commit<1>(&bar[2]);
   }
   uint32_t kb[2];
-  keep_bits64(a.d, (uint64_t(z) * a.S + row) * a.S, j0, a.S, kb);
+  if (a.d.mask_in) {  // the forward's saved keep bits (no Philox re-run)
+    const uint32_t* mw = reinterpret_cast<const uint32_t*>(a.d.mask_in) + (uint64_t(z) * a.S + row) * 4 + 2 * hf;
+    kb[0] = row < a.S ? mw[0] : 0xffffffffu;
+    kb[1] = row < a.S ? mw[1] : 0xffffffffu;
+  } else {
+    keep_bits64(a.d, (uint64_t(z) * a.S + row) * a.S, j0, a.S, kb);
+  }
   const float sd = a.d.p > 0.0f ? a.d.scale : 1.0f;
   mbar_wait(&bar[2], it & 1);
   tc_fence_after();

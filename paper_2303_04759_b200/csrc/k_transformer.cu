@@ -1183,14 +1183,24 @@ static void set_c(GemmArgs& r, void* c, int64_t ld, int64_t s1, int64_t s2, int 
 
 // attention(qkv) -> (ctx [T,H], probs [Z*S, S])
 static void b_attention(Plan& p) {
-  check_arity(p, 1, 1, 2, 2);
+  check_arity(p, 1, 1, 2, 3);
   const AttnGeom g = attn_geom(p);
   require(p.out[0].numel() == g.B * g.S * g.H, "attention: ctx must be [T, H]");
   require(p.out[1].numel() == g.Z * g.S * g.S, "attention: probs must be [B*A*S, S]");
-  if (attn_fused_ok(g.dt, g.S, g.H, g.A, g.exact) && !p.attrs.i("unfused", 0)) {
+  // save_mask: a third output keeps the dropout bits, 4 words per query row
+  const bool save_mask = p.out.size() > 2;
+  const bool fused = attn_fused_ok(g.dt, g.S, g.H, g.A, g.exact) && !p.attrs.i("unfused", 0);
+  if (save_mask) {
+    if (!fused) fail(TCB_ERR_UNIMPLEMENTED, "attention: save_mask needs the fused kernel");
+    require(g.d.p > 0.0f && p.out[2].numel() * dtype_bytes(p.out[2].dtype) >= g.Z * g.S * 16,
+            "attention: save_mask needs p > 0 and a Z*S*4-word mask");
+  }
+  if (fused) {
     void* trace = reinterpret_cast<void*>(p.attrs.i("tc_trace", 0));  // tooling only
     p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
-      launch_attn_fwd(in[0].ptr, out[0].ptr, out[1].ptr, g.B, g.S, g.H, g.A, g.scale, g.causal, g.d, s, trace);
+      DropCfg d = g.d;
+      if (save_mask) d.mask_out = static_cast<uint8_t*>(out[2].ptr);
+      launch_attn_fwd(in[0].ptr, out[0].ptr, out[1].ptr, g.B, g.S, g.H, g.A, g.scale, g.causal, d, s, trace);
     };
     return;
   }
@@ -1226,12 +1236,17 @@ TCB_REGISTER("attention", b_attention);
 
 // attention_dx(qkv, probs, dctx) -> dqkv [T, 3H]
 static void b_attention_dx(Plan& p) {
-  check_arity(p, 3, 3, 1, 1);
+  check_arity(p, 3, 4, 1, 1);
   const AttnGeom g = attn_geom(p);
   require(p.out[0].numel() == p.in[0].numel(), "attention_dx: dqkv must be [T, 3H]");
-  if (attn_fused_ok(g.dt, g.S, g.H, g.A, g.exact) && !p.attrs.i("unfused", 0)) {
+  const bool mask_in = p.in.size() > 3;  // the forward's saved keep bits
+  const bool fused = attn_fused_ok(g.dt, g.S, g.H, g.A, g.exact) && !p.attrs.i("unfused", 0);
+  if (mask_in && !fused) fail(TCB_ERR_UNIMPLEMENTED, "attention_dx: a saved mask needs the fused kernel");
+  if (fused) {
     p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
-      launch_attn_bwd(in[0].ptr, in[1].ptr, in[2].ptr, out[0].ptr, g.B, g.S, g.H, g.A, g.scale, g.causal, g.d, s);
+      DropCfg d = g.d;
+      if (mask_in) d.mask_in = static_cast<const uint8_t*>(in[3].ptr);
+      launch_attn_bwd(in[0].ptr, in[1].ptr, in[2].ptr, out[0].ptr, g.B, g.S, g.H, g.A, g.scale, g.causal, d, s);
     };
     return;
   }

@@ -224,9 +224,19 @@ inline void register_extension_ops(OpRegistry& r) {
     int64_t H = q.shape[1] / 3, A = rel::a_int(a, "heads", 1), S = rel::a_int(a, "seq", q.shape[0]);
     if (q.shape[1] % 3 || H % A || q.shape[0] % S) throw TypeError("attention: bad qkv/heads/seq");
     int64_t B = q.shape[0] / S;
-    return TupleType{{TensorType{q.dtype, {q.shape[0], H}}, TensorType{q.dtype, {B * A * S, S}}}};
+    TupleType t{{TensorType{q.dtype, {q.shape[0], H}}, TensorType{q.dtype, {B * A * S, S}}}};
+    // save_mask (p > 0): the dropout keep bits, 4 i32 words per query row (S <= 128)
+    if (rel::a_int(a, "save_mask", 0) && ir::attr_double(a, "p", 0.0) > 0.0) {
+      if (S > 128) throw TypeError("attention: save_mask needs seq <= 128");
+      t.fields.push_back(TensorType{kI32, {B * A * S * 4}});
+    }
+    return t;
   });
-  reg("attention_dx", 3, O, [](const V& in, const AttrMap&) -> Type { return rel::T(in[0], "attention_dx"); });
+  // attention_dx(qkv, probs, dctx [, saved keep bits]) -> dqkv
+  reg("attention_dx", -1, O, [](const V& in, const AttrMap&) -> Type {
+    if (in.size() != 3 && in.size() != 4) throw TypeError("attention_dx: (qkv, probs, dctx [, mask])");
+    return rel::T(in[0], "attention_dx");
+  });
   // layer_norm(x, gamma, beta) -> (y, mean f32[T], rstd f32[T])
   reg("layer_norm", 3, O, [](const V& in, const AttrMap&) -> Type {
     auto x = rel::T(in[0], "layer_norm");

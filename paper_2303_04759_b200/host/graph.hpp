@@ -246,7 +246,9 @@ inline void register_default_adjoints() {
     if (!c.dout[0]) return {nullptr};
     auto qkv = arg_var(c.let.value, 0);
     VarPtr probs = c.g.get(c.let.var, 1);
-    return {c.g.op("attention_dx", {qkv, probs, c.dout[0]}, c.let.value->call_attrs)};
+    std::vector<VarPtr> args{qkv, probs, c.dout[0]};
+    if (c.let.var->ty.tuple().fields.size() > 2) args.push_back(c.g.get(c.let.var, 2));  // saved keep bits
+    return {c.g.op("attention_dx", args, c.let.value->call_attrs)};
   };
   A["layer_norm"] = [](AdjointCtx& c) -> std::vector<VarPtr> {
     if (!c.dout[0]) return {nullptr, nullptr, nullptr};

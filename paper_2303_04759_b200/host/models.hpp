@@ -239,6 +239,9 @@ inline TrainStep build_train_step(const ModelCfg& c) {
     return y->ty.is_tuple() ? g.get(y, 0) : y;
   };
   AttrMap attn_attrs{{"heads", c.A}, {"seq", c.S}, {"causal", std::int64_t(c.kind == "gpt2")}};
+  // the fused attention saves its dropout keep bits for the backward
+  if (c.p > 0.0 && c.dtype == "bf16" && c.H / c.A == 64 && c.S <= 128 && c.S % 8 == 0)
+    attn_attrs["save_mask"] = std::int64_t(1);
   // residual LayerNorms save their dropout keep bits for the backward (no Philox re-run)
   auto ln_attrs = [&]() {
     AttrMap a{{"eps", c.ln_eps}};

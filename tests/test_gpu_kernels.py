@@ -559,6 +559,33 @@ def test_attention_fused_tcgen05(S, p, causal):
     assert rel_err(g[0], gu[0]) < 2e-2, rel_err(g[0], gu[0])
 
 
+@pytest.mark.parametrize("S,causal", [(128, 0), (64, 1)])
+def test_attention_saved_dropout_mask(S, causal):
+    """attention(save_mask) writes the keep bits of its P dropout (4 words per
+    query row, bit-exact vs the oracle); attention_dx reading them equals the
+    Philox re-run bit for bit."""
+    B, A, dh = 2, 2, 64
+    H, T = A * dh, B * S
+    qkv = rn(T, 3 * H, lo=-2, hi=2)
+    at = {"heads": A, "seq": S, "p": 0.1, "seed": 9, "salt": 4, "causal": causal}
+    outs = [((T, H), BF16), ((B * A * S, S), BF16)]
+    nw = B * A * S * 4
+    g, o = run_both("attention", [(qkv, BF16)], outs + [((nw,), I32)], {**at, "save_mask": 1})
+    g0, _ = run_both("attention", [(qkv, BF16)], outs, at)
+    assert bits_equal(g[0], g0[0]) and bits_equal(g[1], g0[1])
+    # words hold bits for keys 0..127; only keys < S are meaningful
+    gw, ow = g[2].view(np.uint32).reshape(-1, 4), o[2].view(np.uint32).reshape(-1, 4)
+    keymask = np.array([(1 << 32) - 1 if (w + 1) * 32 <= S else ((1 << max(0, S - 32 * w)) - 1)
+                        for w in range(4)], dtype=np.uint64).astype(np.uint32)
+    assert np.array_equal(gw & keymask, ow & keymask)
+    probs, dctx = o[1], rn(T, H)
+    ins = [(qkv, BF16), (probs, BF16), (dctx, BF16)]
+    g1, o1 = run_both("attention_dx", ins + [(g[2], I32)], [((T, 3 * H), BF16)], at)
+    g2, _ = run_both("attention_dx", ins, [((T, 3 * H), BF16)], at)
+    assert bits_equal(g1[0], g2[0])
+    assert rel_err(g1[0], o1[0]) < 3e-2
+
+
 def test_embedding_bit_exact():
     V, H, T = 1000, 96, 513
     ids = RNG.integers(0, V, size=T).astype(np.int32)
