@@ -16,8 +16,10 @@ struct FoldState {
   std::vector<FoldJob> jobs;
   uint64_t ops_deferred = 0, flush_launches = 0;  // cumulative (launch accounting)
 };
+// per thread: one VM (rank) per thread may run concurrently,
+// each with its own queue and pool on its own device
 FoldState& st() {
-  static FoldState s;
+  thread_local FoldState s;
   return s;
 }
 }  // namespace
