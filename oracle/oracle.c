@@ -985,6 +985,21 @@ int orc_exec(const char* op, const orc_tensor* in, int nin, orc_tensor* out, int
   /* linear_chain(x, W1, b1, W2, b2) -> (y1 [, u1], y2): the two linears in
    * sequence (the device runs them as one chained launch); y2 reads the
    * ROUNDED y1 exactly like a separate second linear would. */
+  /* embedding_sum(ids.., tables..): gathers added in table order, each sum
+   * rounded to the tables' dtype (= the embedding / add chain it replaces) */
+  if (!strcmp(op, "embedding_sum")) {
+    const int n = nin / 2;
+    if (nin != 2 * n || n < 2 || nout != 1) return fail("embedding_sum: (ids.., tables..) -> 1 output");
+    const int64_t Tn = numel(&in[0]), H = in[n].shape[1];
+    for (int64_t t = 0; t < Tn; ++t)
+      for (int64_t j = 0; j < H; ++j) {
+        float acc = F(&in[n])[(int64_t)((const int32_t*)in[0].ptr)[t] * H + j];
+        for (int k = 1; k < n; ++k)
+          acc = rnd(out[0].dtype, acc + F(&in[n + k])[(int64_t)((const int32_t*)in[k].ptr)[t] * H + j]);
+        F(&out[0])[t * H + j] = rnd(out[0].dtype, acc);
+      }
+    return 0;
+  }
   if (!strcmp(op, "linear_chain")) {
     if (nin != 5 || (nout != 2 && nout != 3)) return fail("linear_chain: 5 inputs, 2-3 outputs");
     int act = parse_act(astr(A, na, "act", "none")), act2 = parse_act(astr(A, na, "act2", "none"));

@@ -1326,6 +1326,91 @@ static void b_embedding(Plan& p) {
 }
 TCB_REGISTER("embedding", b_embedding);
 
+// embedding_sum(ids_0..ids_{n-1}, table_0..table_{n-1}) = (e_0 + e_1) + e_2 ...
+// with the sum rounded to the tables' dtype after every add -- exactly the
+// embedding / add chain it replaces (BERT: word + position + token type), one
+// warp per token, 16-byte row chunks.
+struct EmbSumArgs {
+  const int32_t* ids[4];
+  const void* tab[4];
+  int64_t V[4];
+  int n;
+};
+template <typename T>
+__global__ void __launch_bounds__(256) k_embed_sum(const EmbSumArgs a, T* __restrict__ out, int64_t Tn, int64_t H,
+                                                   int* __restrict__ err, bool vec) {
+  TCB_PDL_ENTRY();
+  const int64_t t = blockIdx.x * int64_t(blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (t >= Tn) return;
+  int64_t row[4];
+  for (int k = 0; k < a.n; ++k) {
+    const int32_t id = a.ids[k][t];
+    if (id < 0 || id >= a.V[k]) {
+      if (lane == 0) atomicExch(err, 1);
+      return;
+    }
+    row[k] = int64_t(id) * H;
+  }
+  if (vec) {
+    for (int64_t c = lane; c < H / 8; c += 32) {
+      float acc[8];
+      unpack8<T>(*reinterpret_cast<const uint4*>(static_cast<const T*>(a.tab[0]) + row[0] + c * 8), acc);
+      for (int k = 1; k < a.n; ++k) {
+        float f[8];
+        unpack8<T>(*reinterpret_cast<const uint4*>(static_cast<const T*>(a.tab[k]) + row[k] + c * 8), f);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[e] = to_f(from_f<T>(__fadd_rn(acc[e], f[e])));
+      }
+      *reinterpret_cast<uint4*>(out + t * H + c * 8) = pack8<T>(acc);
+    }
+  } else {
+    for (int64_t j = lane; j < H; j += 32) {
+      float acc = to_f(static_cast<const T*>(a.tab[0])[row[0] + j]);
+      for (int k = 1; k < a.n; ++k) acc = to_f(from_f<T>(__fadd_rn(acc, to_f(static_cast<const T*>(a.tab[k])[row[k] + j]))));
+      out[t * H + j] = from_f<T>(acc);
+    }
+  }
+}
+
+static void b_embedding_sum(Plan& p) {
+  const int n = int(p.in.size()) / 2;
+  require(int(p.in.size()) == 2 * n && n >= 2 && n <= 4, "embedding_sum: (ids_0.., table_0..), 2 to 4 tables");
+  check_arity(p, 2 * n, 2 * n, 1, 1);
+  const int64_t Tn = p.in[0].numel(), H = p.in[n].shape[1];
+  const int dt = p.in[n].dtype;
+  for (int k = 0; k < n; ++k) {
+    require(p.in[k].dtype == TCB_I32 && p.in[k].numel() == Tn, "embedding_sum: ids must be i32 of one shape");
+    require(p.in[n + k].rank == 2 && p.in[n + k].shape[1] == H && p.in[n + k].dtype == dt,
+            "embedding_sum: tables must be [V_k, H] of one dtype");
+  }
+  require(p.out[0].dtype == dt && p.out[0].numel() == Tn * H, "embedding_sum: output is [T, H] in the tables' dtype");
+  require(dt == TCB_BF16 || dt == TCB_F16, "embedding_sum: 16-bit tables");
+  auto err = std::make_shared<Scratch>(4);
+  TCB_CUDA(cudaMemset(err->p, 0, 4));
+  std::vector<int64_t> V(n);
+  for (int k = 0; k < n; ++k) V[k] = p.in[n + k].shape[0];
+  auto launch = [=](auto* tp, const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
+    using T = std::remove_pointer_t<decltype(tp)>;
+    EmbSumArgs a{};
+    a.n = n;
+    bool vec = H % 8 == 0 && reinterpret_cast<uintptr_t>(out[0].ptr) % 16 == 0;
+    for (int k = 0; k < n; ++k) {
+      a.ids[k] = static_cast<const int32_t*>(in[k].ptr);
+      a.tab[k] = in[n + k].ptr;
+      a.V[k] = V[k];
+      vec = vec && reinterpret_cast<uintptr_t>(in[n + k].ptr) % 16 == 0;
+    }
+    launch_k(k_embed_sum<T>, unsigned((Tn + 7) / 8), 256, 0, s, a, static_cast<T*>(out[0].ptr), Tn, H, (int*)err->p,
+             vec);
+  };
+  p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
+    if (dt == TCB_BF16) launch(static_cast<__nv_bfloat16*>(nullptr), in, out, s);
+    else launch(static_cast<__half*>(nullptr), in, out, s);
+  };
+}
+TCB_REGISTER("embedding_sum", b_embedding_sum);
+
 // Deterministic scatter-add: stable rank of (id, t) pairs, then one warp per
 // distinct id accumulates its rows in ascending t onto base -- the oracle's
 // order exactly, so f32 results are bit-identical.

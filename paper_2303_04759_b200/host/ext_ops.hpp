@@ -284,6 +284,23 @@ inline void register_extension_ops(OpRegistry& r) {
     shape.push_back(tab.shape[1]);
     return TensorType{rel::out_dtype(a, tab.dtype), shape};
   });
+  // embedding_sum(ids_0..ids_{n-1}, table_0..table_{n-1}) -> [..., H]: the
+  // rounded chain (e_0 + e_1) + e_2 ... of n embedding lookups
+  reg("embedding_sum", -1, I, [](const V& in, const AttrMap&) -> Type {
+    const size_t n = in.size() / 2;
+    if (in.size() != 2 * n || n < 2 || n > 4) throw TypeError("embedding_sum: (ids.., tables..), 2 to 4 tables");
+    auto ids = rel::T(in[0], "embedding_sum"), tab = rel::T(in[n], "embedding_sum");
+    rel::need_rank(tab, 2, "embedding_sum");
+    for (size_t k = 0; k < n; ++k) {
+      auto ik = rel::T(in[k], "embedding_sum"), tk = rel::T(in[n + k], "embedding_sum");
+      if (ik.dtype != kI32 || !(ik == ids)) throw TypeError("embedding_sum: ids must be i32 of one shape");
+      rel::need_rank(tk, 2, "embedding_sum");
+      if (tk.shape[1] != tab.shape[1] || tk.dtype != tab.dtype) throw TypeError("embedding_sum: tables differ");
+    }
+    auto shape = ids.shape;
+    shape.push_back(tab.shape[1]);
+    return TensorType{tab.dtype, shape};
+  });
   // embedding_dx(ids, dy [, base]) {rows} -> f32 [rows, H]
   reg("embedding_dx", -1, O, [](const V& in, const AttrMap& a) -> Type {
     if (in.size() != 2 && in.size() != 3) throw TypeError("embedding_dx: 2 or 3 inputs");

@@ -271,6 +271,16 @@ inline void register_default_adjoints() {
     VarPtr dx = ir::attr_double(at, "p", 0.0) > 0.0 ? c.g.get(t, 3) : ds;
     return {dx, ds, c.g.get(t, 1), c.g.get(t, 2)};
   };
+  A["embedding_sum"] = [](AdjointCtx& c) -> std::vector<VarPtr> {
+    const size_t n = c.let.value->args.size() / 2;
+    std::vector<VarPtr> g(2 * n, nullptr);
+    if (!c.dout[0]) return g;
+    for (size_t k = 0; k < n; ++k) {
+      auto ids = arg_var(c.let.value, k), tab = arg_var(c.let.value, n + k);
+      g[n + k] = c.g.op("embedding_dx", {ids, c.dout[0]}, {{"rows", tab->ty.tensor().shape[0]}});
+    }
+    return g;
+  };
   A["embedding"] = [](AdjointCtx& c) -> std::vector<VarPtr> {
     auto ids = arg_var(c.let.value, 0), tab = arg_var(c.let.value, 1);
     return {nullptr, c.g.op("embedding_dx", {ids, c.dout[0]}, {{"rows", tab->ty.tensor().shape[0]}})};

@@ -253,8 +253,13 @@ inline TrainStep build_train_step(const ModelCfg& c) {
   VarPtr h;
   if (c.kind == "bert") {
     VarPtr type_ids = par(ts.i_type);
-    VarPtr e = g.op("add", {g.op("embedding", {ids, W["word_emb"]}), g.op("embedding", {pos_ids, W["pos_emb"]})});
-    e = g.op("add", {e, g.op("embedding", {type_ids, W["type_emb"]})});
+    VarPtr e;
+    if (c.dtype == "bf16") {  // one fused gather-and-add kernel (same roundings)
+      e = g.op("embedding_sum", {ids, pos_ids, type_ids, W["word_emb"], W["pos_emb"], W["type_emb"]});
+    } else {
+      e = g.op("add", {g.op("embedding", {ids, W["word_emb"]}), g.op("embedding", {pos_ids, W["pos_emb"]})});
+      e = g.op("add", {e, g.op("embedding", {type_ids, W["type_emb"]})});
+    }
     VarPtr ln = g.op("layer_norm", {e, W["emb_ln.g"], W["emb_ln.b"]}, {{"eps", c.ln_eps}});
     h = g.get(ln, 0);
     if (c.p > 0) h = g.op("dropout", {h}, drop_attrs());

@@ -678,3 +678,15 @@ def test_linear_chain_bert_ffn_repeatable():
     sep = [from_torch(t) for t in (y1, u1, y2)]
     for a, b, c in zip(c1, c2, sep):
         assert bits_equal(a, b) and bits_equal(a, c)
+
+
+@pytest.mark.parametrize("H", [768, 100])
+def test_embedding_sum_bit_exact(H):
+    """embedding_sum (word + position + token type, rounded after each add)
+    equals the oracle's chain bit for bit; H=100 takes the scalar path."""
+    T = 300
+    ids = [RNG.integers(0, v, size=T).astype(np.int32) for v in (1000, 512, 2)]
+    tabs = [rn(v, H) for v in (1000, 512, 2)]
+    ins = [(i, I32) for i in ids] + [(t, BF16) for t in tabs]
+    g, o = run_both("embedding_sum", ins, [((T, H), BF16)])
+    assert bits_equal(g[0], o[0])
