@@ -659,6 +659,7 @@ static int layer_norm_fwd(const orc_tensor* x, const orc_tensor* r, const orc_te
   const float p = (float)adbl(a, na, "p", 0.0);
   const uint64_t seed = (uint64_t)aint(a, na, "seed", 0), salt = (uint64_t)aint(a, na, "salt", 0);
   const float sp = p > 0.0f ? 1.0f / (1.0f - p) : 1.0f;
+  const int post_drop = !r && p > 0.0f && aint(a, na, "post_dropout", 0);
   float* row = (float*)malloc(sizeof(float) * H);
   const float* X = F(x);
   for (int64_t t = 0; t < T; ++t) {
@@ -682,8 +683,12 @@ static int layer_norm_fwd(const orc_tensor* x, const orc_tensor* r, const orc_te
     ln_row(row, H, eps, &mean, &rstd);
     F(mean_t)[t] = mean;
     F(rstd_t)[t] = rstd;
-    for (int64_t j = 0; j < H; ++j)
-      F(y)[t * H + j] = rnd(y->dtype, (row[j] - mean) * rstd * F(g)[j] + F(bta)[j]);
+    for (int64_t j = 0; j < H; ++j) {
+      float o = rnd(y->dtype, (row[j] - mean) * rstd * F(g)[j] + F(bta)[j]);
+      if (post_drop) /* layer_norm post_dropout = the dropout op on the rounded output */
+        o = rnd(y->dtype, orc_dropout_keep(seed, salt, (uint64_t)(t * H + j), p) ? o * sp : 0.0f);
+      F(y)[t * H + j] = o;
+    }
   }
   free(row);
   return 0;
@@ -702,6 +707,15 @@ static int layer_norm_bwd(const orc_tensor* const* in, int nin, orc_tensor* out,
   const uint64_t seed = (uint64_t)aint(a, na, "seed", 0), salt = (uint64_t)aint(a, na, "salt", 0);
   const float sp = p > 0.0f ? 1.0f / (1.0f - p) : 1.0f;
   const float inv = 1.0f / (float)H;
+  /* in_p: the forward layer_norm's post_dropout folded in -- dy is first the
+   * dropout op's output round(keep ? dy * scale : 0) */
+  const float in_p = (float)adbl(a, na, "in_p", 0.0);
+  const uint64_t in_seed = (uint64_t)aint(a, na, "in_seed", 0), in_salt = (uint64_t)aint(a, na, "in_salt", 0);
+  const float in_sp = in_p > 0.0f ? 1.0f / (1.0f - in_p) : 1.0f;
+#define LN_DY(t, j)                                                                                     \
+  (in_p > 0.0f ? rnd(dy->dtype, orc_dropout_keep(in_seed, in_salt, (uint64_t)((t) * H + (j)), in_p)    \
+                                     ? F(dy)[(t) * H + (j)] * in_sp : 0.0f)                          \
+               : F(dy)[(t) * H + (j)])
   float* dg = F(&out[1]);
   float* db = F(&out[2]);
   /* bias_grad: column sums (row order) of the outgoing gradient as stored --
@@ -718,7 +732,7 @@ static int layer_norm_bwd(const orc_tensor* const* in, int nin, orc_tensor* out,
     float c1 = 0.0f, c2 = 0.0f;
     for (int64_t j = 0; j < H; ++j) {
       float xh = (F(s)[t * H + j] - mean) * rstd;
-      float dyv = F(dy)[t * H + j];
+      float dyv = LN_DY(t, j);
       if (dy2) dyv += F(dy2)[t * H + j];
       float gg = dyv * F(g)[j];
       c1 += gg * xh;
@@ -728,7 +742,7 @@ static int layer_norm_bwd(const orc_tensor* const* in, int nin, orc_tensor* out,
     c2 *= inv;
     for (int64_t j = 0; j < H; ++j) {
       float xh = (F(s)[t * H + j] - mean) * rstd;
-      float dyv = F(dy)[t * H + j];
+      float dyv = LN_DY(t, j);
       if (dy2) dyv += F(dy2)[t * H + j];
       float gg = dyv * F(g)[j];
       float dsv = rstd * (gg - c2 - xh * c1);
@@ -746,6 +760,7 @@ static int layer_norm_bwd(const orc_tensor* const* in, int nin, orc_tensor* out,
     }
   }
   return 0;
+#undef LN_DY
 }
 
 /* ----------------------------------------------------------- cross entropy */

@@ -397,7 +397,15 @@ __global__ void __launch_bounds__(256) k_ln_fwd16(const T* __restrict__ x, const
         lds8x2(sb + ch * 8, b);
 #pragma unroll
         for (int k = 0; k < 4; ++k) o[k] = fma2(fma2(v[c][k], rs2, nmr2), g[k], b[k]);
-        *reinterpret_cast<uint4*>(y + row * H + ch * 8) = pack8x2<T>(o);
+        uint4 w = pack8x2<T>(o);
+        if (!r && d.p > 0.0f) {  // post_dropout: dropout(LN(x)) as the separate op rounds it
+          const uint32_t bits = dropout_bits8q(d, uint64_t(row * H + ch * 8) >> 3);
+          unpack8x2<T>(w, o);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) o[k] = keep2(bits, 2 * k, mul2(o[k], sc2));
+          w = pack8x2<T>(o);
+        }
+        *reinterpret_cast<uint4*>(y + row * H + ch * 8) = w;
       }
     }
   }
@@ -417,7 +425,11 @@ static void build_ln_fwd(Plan& p, bool residual) {
   require(G.dtype == TCB_F32 || G.dtype == X.dtype, p.op + ": gamma dtype");
   const bool gf = G.dtype == TCB_F32;
   const float eps = float(p.attrs.f("eps", 1e-12));
-  const DropCfg d0 = drop_cfg(p.attrs);
+  DropCfg d0 = drop_cfg(p.attrs);
+  // plain layer_norm: dropout on the OUTPUT only with attr post_dropout (16-bit path)
+  const bool post_drop = !residual && p.attrs.i("post_dropout", 0) != 0 && d0.p > 0.0f;
+  if (!residual && !post_drop) d0 = DropCfg{};
+  if (post_drop) require(X.dtype != TCB_F32 && H % 8 == 0, p.op + ": post_dropout needs a 16-bit input, H % 8 == 0");
   if (save_mask)
     require(H % 8 == 0 && d0.p > 0.0f && p.out[4].numel() * dtype_bytes(p.out[4].dtype) * 8 >= X.numel(),
             p.op + ": save_mask needs p > 0, H % 8 == 0 and a T*H/8-byte mask output");
@@ -447,6 +459,7 @@ static void build_ln_fwd(Plan& p, bool residual) {
           return;
         }
       }
+      if (post_drop) fail(TCB_ERR_UNIMPLEMENTED, p.op + ": post_dropout needs aligned 16-bit rows");
       constexpr int RW = NC <= 2 ? 2 : 1;
       launch_k(k_ln_fwd<T, NC>, unsigned((rows + 8 * RW - 1) / (8 * RW)), 256, 0, s, 
           (const T*)in[0].ptr, residual ? (const T*)in[1].ptr : nullptr,
@@ -576,7 +589,7 @@ __global__ void __launch_bounds__(256, NC <= 3 ? 2 : 1) k_ln_bwd16(const T* __re
                                                   const float* __restrict__ mean, const float* __restrict__ rstd,
                                                   const T* __restrict__ dy, const T* __restrict__ dy2,
                                                   T* __restrict__ ds_o, T* __restrict__ dx_o, float* __restrict__ ws,
-                                                  int nparts, int64_t rows, int H, DropCfg d) {
+                                                  int nparts, int64_t rows, int H, DropCfg d, DropCfg din) {
   TCB_PDL_ENTRY();
   constexpr int RW = LNB_ROWS / 8;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -607,11 +620,28 @@ __global__ void __launch_bounds__(256, NC <= 3 ? 2 : 1) k_ln_bwd16(const T* __re
   }
   stage_params<T, GF>(gamma, nullptr, sg, nullptr, H);
   __syncthreads();
+  // in_dropout (the output dropout of a plain layer_norm folded in): the incoming
+  // gradient is the separate dropout op's result, round(keep ? dy * scale : 0)
+  uint32_t inb[RW][NC];
+  if (din.p > 0.0f) {
+#pragma unroll
+    for (int q = 0; q < RW; ++q)
+#pragma unroll
+      for (int c = 0; c < NC; ++c)
+        inb[q][c] = live[q] ? dropout_bits8q(din, uint64_t((row0 + q) * H + (lane + c * 32) * 8) >> 3) : 0u;
+  }
+  const float2 isc2 = splat2(din.scale);
   // xh = s*rs - mu*rs, dv = dy + dy2 and g = dv * gamma of chunk c of row q (pairs)
   auto load_row = [&](int q, int c, const float2* gm, float2* xh, float2* dv, float2* g) {
     float2 sv[4];
     unpack8x2<T>(sq[q][c], sv);
     unpack8x2<T>(dq[q][c], dv);
+    if (din.p > 0.0f) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) dv[k] = keep2(inb[q][c], 2 * k, mul2(dv[k], isc2));
+      const uint4 w = pack8x2<T>(dv);
+      unpack8x2<T>(w, dv);
+    }
     if (dy2) {
       float2 d2[4];
       unpack8x2<T>(d2q[q][c], d2);
@@ -766,6 +796,13 @@ static void b_layer_norm_dx(Plan& p) {
   require(p.out[1].dtype == TCB_F32 && p.out[2].dtype == TCB_F32, "layer_norm_dx: dgamma/dbeta are f32");
   const bool gf = p.in[1].dtype == TCB_F32;
   const DropCfg d0 = drop_cfg(p.attrs);
+  // in_p / in_seed / in_salt: the forward layer_norm's post_dropout, applied to dy
+  DropCfg din;
+  din.p = float(p.attrs.f("in_p", 0.0));
+  din.scale = din.p > 0.0f ? 1.0f / (1.0f - din.p) : 1.0f;
+  din.seed = uint64_t(p.attrs.i("in_seed", 0));
+  din.salt = uint64_t(p.attrs.i("in_salt", 0));
+  din.thr = din.p > 0.0f ? uint32_t(std::ceil(double(din.p) * 65536.0)) : 0u;
   const bool bias = p.attrs.i("bias_grad", 0) != 0;
   const bool has_res = int(p.in.size()) - int(mask_in) > 5, has_dx = int(p.out.size()) - int(bias) > 3;
   const int nin = int(p.in.size());
@@ -811,6 +848,8 @@ static void b_layer_norm_dx(Plan& p) {
       // deferred fold: this instance's partials go to its own buffer, folded at the flush
       float* dws = fold_deferring() ? fold_scratch(out[1].ptr, 0, size_t(nblk) * np * H * sizeof(float)) : nullptr;
       float* wsp = dws ? dws : (float*)ws->p;
+      if (din.p > 0.0f && (!fast || has_res))
+        fail(TCB_ERR_UNIMPLEMENTED, "layer_norm_dx: in_p needs the 16-bit path and a single dy");
       if (fast) {
         if constexpr (sizeof(T) == 2) {
           const bool full = H == NC * 256;
@@ -818,7 +857,7 @@ static void b_layer_norm_dx(Plan& p) {
                          : (full ? k_ln_bwd16<T, NC, false, true> : k_ln_bwd16<T, NC, false, false>);
           launch_k(kern, nblk, 256, smem, s, (const T*)in[0].ptr, (const void*)in[1].ptr, (const float*)in[2].ptr,
                    (const float*)in[3].ptr, (const T*)in[4].ptr, d2, (T*)out[0].ptr, dxp, wsp, np, rows, H,
-                   d);
+                   d, din);
         }
       } else {
         launch_k(k_ln_bwd<T, NC>, nblk, 256, smem, s, (const T*)in[0].ptr, gfp, gtp, (const float*)in[2].ptr,

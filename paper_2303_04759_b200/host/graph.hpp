@@ -415,7 +415,7 @@ inline UseInfo count_uses(const LetSeq& s) {
 }
 
 struct FusionStats {
-  int dact = 0, ln_dy2 = 0, emb_base = 0, ln_bias = 0, pairs = 0, ce_mask = 0, dead = 0;
+  int dact = 0, ln_dy2 = 0, emb_base = 0, ln_bias = 0, pairs = 0, ce_mask = 0, dead = 0, ln_drop = 0;
 };
 
 /// Horizontal fusion (SPEC.md:533-540 applied to GEMMs): a weight-gradient
@@ -575,6 +575,51 @@ inline FusionStats fuse(LetSeq& s, bool patterns = true) {
         done = true;
       }
       if (done) continue;
+    }
+    // 6a. dropout(get(layer_norm(x, g, b), 0)) -> layer_norm {post_dropout} (16-bit):
+    //     the LN kernel applies the output dropout (same roundings, one pass)
+    if (op == "dropout" && b.value->args.size() == 1) {
+      auto src = arg_var(b.value, 0);
+      auto it = src ? def.find(src.get()) : def.end();
+      if (it != def.end() && !removed.count(it->second) && s.lets[it->second].value->kind == ExprKind::TupleGet &&
+          single(src) && s.lets[it->second].value->index == 0) {
+        auto& gl = s.lets[it->second];
+        auto tv = gl.value->args[0]->kind == ExprKind::VarRef ? gl.value->args[0]->var : nullptr;
+        auto* lp = producer(tv);
+        const auto& ty = b.var->ty;
+        if (lp && lp->value->op == "layer_norm" && !lp->value->call_attrs.count("post_dropout") && !ty.is_tuple() &&
+            (ty.tensor().dtype == kBF16 || ty.tensor().dtype == kF16) && ty.tensor().shape.back() % 8 == 0) {
+          for (const char* k : {"p", "seed", "salt"})
+            if (b.value->call_attrs.count(k)) lp->value->call_attrs[k] = b.value->call_attrs.at(k);
+          lp->value->call_attrs["post_dropout"] = std::int64_t(1);
+          auto e = ir::tuple_get(ir::var_ref(tv), 0);
+          e->ty = b.value->ty;
+          b.value = e;
+          removed.insert(it->second);  // the old get is now unused
+          ++st.ln_drop;
+          continue;
+        }
+      }
+    }
+    // 6b. layer_norm_dx(s, g, m, r, dropout(dy)) -> layer_norm_dx {in_p, in_seed, in_salt}
+    if (op == "layer_norm_dx" && b.value->args.size() == 5 && !b.value->call_attrs.count("in_p")) {
+      auto src = arg_var(b.value, 4);
+      auto* p = producer(src);
+      const auto& ty = src ? src->ty : b.var->ty;
+      if (p && p->value->op == "dropout" && single(src) && !ty.is_tuple() &&
+          (ty.tensor().dtype == kBF16 || ty.tensor().dtype == kF16) && ty.tensor().shape.back() % 8 == 0) {
+        AttrMap at = b.value->call_attrs;
+        at["in_p"] = ir::attr_double(p->value->call_attrs, "p", 0.0);
+        at["in_seed"] = ir::attr_int(p->value->call_attrs, "seed", 0);
+        at["in_salt"] = ir::attr_int(p->value->call_attrs, "salt", 0);
+        auto call = ir::call("layer_norm_dx", {b.value->args[0], b.value->args[1], b.value->args[2],
+                                               b.value->args[3], p->value->args[0]}, at);
+        call->ty = b.value->ty;
+        b.value = call;
+        removed.insert(def[src.get()]);
+        ++st.ln_drop;
+        continue;
+      }
     }
     // 2. layer_norm_dx(s, g, m, r, add(a, b)) -> layer_norm_dx(s, g, m, r, a, b)
     const size_t lnm = op == "layer_norm_dx" && ir::attr_int(b.value->call_attrs, "mask_in", 0) ? 1 : 0;

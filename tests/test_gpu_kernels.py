@@ -690,3 +690,27 @@ def test_embedding_sum_bit_exact(H):
     ins = [(i, I32) for i in ids] + [(t, BF16) for t in tabs]
     g, o = run_both("embedding_sum", ins, [((T, H), BF16)])
     assert bits_equal(g[0], o[0])
+
+
+def test_layer_norm_post_dropout_fused():
+    """Embedding LayerNorm with its output dropout folded in (layer_norm
+    post_dropout) and the backward's incoming-gradient dropout folded into
+    layer_norm_dx (in_p): bit-identical to the separate dropout ops."""
+    T, H = 300, 768
+    x, gm, bt = rn(T, H), rn(H, lo=0.5, hi=1.5), rn(H, lo=-0.1, hi=0.1)
+    dat = {"p": 0.1, "seed": 21, "salt": 3}
+    outs = [((T, H), BF16), ((T,), F32), ((T,), F32)]
+    g, o = run_both("layer_norm", [(x, BF16), (gm, BF16), (bt, BF16)], outs, {"eps": 1e-12, "post_dropout": 1, **dat})
+    g0, _ = run_both("layer_norm", [(x, BF16), (gm, BF16), (bt, BF16)], outs, {"eps": 1e-12})
+    gd, _ = run_both("dropout", [(g0[0], BF16)], [((T, H), BF16)], dat)
+    assert bits_equal(g[0], gd[0]) and bits_equal(g[1], g0[1])
+    assert rel_err(g[0], o[0]) < BF16_TOL
+    dy = rn(T, H)
+    ins = [(x, BF16), (gm, BF16), (g[1], F32), (g[2], F32)]
+    lo = [((T, H), BF16), ((H,), F32), ((H,), F32)]
+    gf, of = run_both("layer_norm_dx", ins + [(dy, BF16)], lo, {"in_p": 0.1, "in_seed": 21, "in_salt": 3})
+    dd, _ = run_both("dropout", [(dy, BF16)], [((T, H), BF16)], dat)
+    gu, _ = run_both("layer_norm_dx", ins + [(dd[0], BF16)], lo, {})
+    for a, b in zip(gf, gu):
+        assert bits_equal(a, b)
+    assert rel_err(gf[0], of[0]) < 5e-3 and rel_err(gf[1], of[1]) < 1e-5
