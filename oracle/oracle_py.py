@@ -157,3 +157,55 @@ def dropout_keep_mask(seed: int, salt: int, n: int, p: float) -> np.ndarray:
 
 __all__ = ["run", "HostTensor", "rng_uniform", "rng_below", "ref_available", "lib", "ref",
            "F32", "F16", "BF16", "I32", "U8", "dropout_keep_mask"]
+
+
+# --- TNSR format restatement (tensor.hpp:76-139), numpy ------------------------
+# "TNSR", u8 code, u8 rank, u64 LE dims, raw LE data.  Codes 0 f32 / 1 f16 are
+# the reference's (save_tensor tensor.hpp:80-99, load_tensor :108-133); 2 bf16
+# (uint16 bits) and 3 i32 are the backend's extension.
+TNSR_NP = {0: "<f4", 1: "<f2", 2: "<u2", 3: "<i4"}
+
+
+def tnsr_bytes(arr: np.ndarray, code: int) -> bytes:
+    a = np.require(arr, TNSR_NP[code], "C")
+    head = b"TNSR" + bytes([code, a.ndim]) + np.asarray(a.shape, "<u8").tobytes()
+    return head + a.tobytes()
+
+
+def tnsr_parse(buf: bytes) -> tuple[np.ndarray, int]:
+    if buf[:4] != b"TNSR":
+        raise ValueError("bad tensor file magic")
+    code, rank = buf[4], buf[5]
+    if code not in TNSR_NP:
+        raise ValueError("bad tensor file header")
+    shape = tuple(int(d) for d in np.frombuffer(buf, "<u8", rank, 6))
+    off = 6 + 8 * rank
+    n = int(np.prod(shape, dtype=np.int64))
+    dt = np.dtype(TNSR_NP[code])
+    if len(buf) < off + n * dt.itemsize:
+        raise ValueError("truncated tensor file")
+    return np.frombuffer(buf, dt, n, off).reshape(shape).copy(), code
+
+
+def ref_tnsr_save(path: str, data: np.ndarray, code: int):
+    """The reference's own save_tensor (oracle/_ref) on float data."""
+    r = ref()
+    a = np.require(data, np.float32, "C")
+    shape = (ctypes.c_int64 * max(a.ndim, 1))(*a.shape)
+    rc = r.ref_tnsr_save(os.fsencode(path), ctypes.c_void_p(a.ctypes.data), code, a.ndim, shape)
+    if rc != 0:
+        raise RuntimeError(r.ref_last_error().decode())
+
+
+def ref_tnsr_load(path: str, cap: int) -> tuple[np.ndarray, int]:
+    """The reference's own load_tensor (oracle/_ref): values widened to float."""
+    r = ref()
+    out = np.empty(cap, np.float32)
+    code, rank = ctypes.c_int(), ctypes.c_int()
+    shape = (ctypes.c_int64 * 8)()
+    rc = r.ref_tnsr_load(os.fsencode(path), ctypes.c_void_p(out.ctypes.data), ctypes.c_int64(cap),
+                         ctypes.byref(code), ctypes.byref(rank), shape)
+    if rc != 0:
+        raise RuntimeError(r.ref_last_error().decode())
+    shp = tuple(shape[:rank.value])
+    return out[:int(np.prod(shp, dtype=np.int64))].reshape(shp), code.value

@@ -134,4 +134,37 @@ int ref_infer(const char* op, const orc_tensor* in, int nin, const orc_attr* att
   }
 }
 
+// trainc::save_tensor / load_tensor (tensor.hpp:80-133) on float host data:
+// f16 tensors are passed as floats and rounded by the reference on save.
+int ref_tnsr_save(const char* path, const float* data, int code, int rank, const int64_t* shape) {
+  try {
+    TensorType ty;
+    ty.dtype = code == 1 ? DType::F16 : DType::F32;
+    for (int i = 0; i < rank; ++i) ty.shape.push_back(shape[i]);
+    Tensor t(ty);
+    for (size_t i = 0; i < t.data.size(); ++i) t.data[i] = data[i];
+    save_tensor(t, std::string(path));
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
+/// out must hold cap floats; *code/*rank/shape[0..rank) describe the file
+int ref_tnsr_load(const char* path, float* out, int64_t cap, int* code, int* rank, int64_t* shape) {
+  try {
+    Tensor t = load_tensor(std::string(path));
+    *code = t.ty.dtype == DType::F32 ? 0 : 1;
+    *rank = t.ty.rank();
+    for (int i = 0; i < *rank && i < 8; ++i) shape[i] = t.ty.shape[size_t(i)];
+    if (int64_t(t.data.size()) > cap) throw Error("ref_tnsr_load: buffer too small");
+    std::memcpy(out, t.data.data(), t.data.size() * 4);
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
 }  // extern "C"

@@ -9,6 +9,7 @@
 #include <sstream>
 
 #include "models.hpp"
+#include "tnsr.hpp"
 #include "vm.hpp"
 
 namespace tb {
@@ -344,6 +345,19 @@ int tb_session_set_comm(void* h, void* comm) {
   TB_TRY(static_cast<Session*>(h)->vm.set_comm(comm));
 }
 
+/// KernelCache::clear (backends.hpp:356-361) plus the plans (and their device
+/// scratch) behind it.  Only valid while no session is alive: a live VM holds
+/// plan handles.
+int tb_cache_clear(void) {
+  TB_TRY({
+    std::lock_guard<std::mutex> g(PlanTable::global().mu);
+    for (auto& kv : PlanTable::global().plans)
+      if (kv.second) tcb_plan_destroy(kv.second);
+    PlanTable::global().plans.clear();
+    backends::KernelCache::global().clear();
+  });
+}
+
 /// KernelCache counters (backends.hpp:363-368): compiles, hits, size
 int tb_cache_stats(int64_t* out3) {
   TB_TRY({
@@ -351,6 +365,82 @@ int tb_cache_stats(int64_t* out3) {
     out3[0] = int64_t(c.compiles());
     out3[1] = int64_t(c.hits());
     out3[2] = int64_t(c.size());
+  });
+}
+
+// --- TNSR tensor files (tensor.hpp:76-139; host/tnsr.hpp) -------------------
+
+/// Write `data` (host memory, stored element bytes) as a TNSR file.
+/// code: 0 f32, 1 f16 (the reference's), 2 bf16, 3 i32 (extension).
+int tb_tnsr_save(const char* path, const void* data, int code, int rank, const int64_t* shape) {
+  TB_TRY({
+    tnsr::Header h;
+    h.code = code;
+    tnsr::code_bytes(code);
+    if (rank < 0) throw Error("bad tensor file header");
+    h.shape.assign(shape, shape + rank);
+    tnsr::save(path, h, data);
+  });
+}
+
+/// Header of a TNSR file: *code, *rank, shape[0..min(rank, cap)).
+int tb_tnsr_header(const char* path, int* code, int* rank, int64_t* shape, int cap) {
+  TB_TRY({
+    tnsr::Header h = tnsr::load_header(path);
+    *code = h.code;
+    *rank = int(h.shape.size());
+    for (int i = 0; i < cap && i < int(h.shape.size()); ++i) shape[i] = h.shape[size_t(i)];
+  });
+}
+
+/// Read the data section of a TNSR file into host memory (bytes must match).
+int tb_tnsr_load(const char* path, void* data, int64_t bytes) {
+  TB_TRY(tnsr::load(path, data, bytes));
+}
+
+static const ir::Var& session_param(Session* s, const char* name, int* index) {
+  const auto& ps = s->vm.fn().params;
+  for (size_t i = 0; i < ps.size(); ++i)
+    if (ps[i]->id == name) {
+      *index = int(i);
+      return *ps[i];
+    }
+  throw Error(std::string("no parameter ") + name);
+}
+
+/// Checkpoint one device-resident step parameter (params, p16, m, v, step, ...)
+/// to a TNSR file: stream-ordered D2H on the session stream, then the write.
+int tb_session_save_param(void* h, const char* name, const char* path) {
+  TB_TRY({
+    auto* s = static_cast<Session*>(h);
+    int idx = 0;
+    const auto& v = session_param(s, name, &idx);
+    const auto& tt = v.ty.tensor();
+    std::vector<char> buf(size_t(nbytes(tt)));
+    tcb_check(tcb_memcpy(buf.data(), s->vm.param_ptr(idx), uint64_t(buf.size()), 1, s->stream), "d2h");
+    tcb_check(tcb_stream_sync(s->stream), "sync");
+    tnsr::Header hd;
+    hd.code = int(tt.dtype);
+    hd.shape = tt.shape;
+    tnsr::save(path, hd, buf.data());
+  });
+}
+
+/// Restore a step parameter from a TNSR file written for the same graph: the
+/// dtype code and shape must equal the parameter's (no implicit conversion).
+int tb_session_load_param(void* h, const char* name, const char* path) {
+  TB_TRY({
+    auto* s = static_cast<Session*>(h);
+    int idx = 0;
+    const auto& v = session_param(s, name, &idx);
+    const auto& tt = v.ty.tensor();
+    tnsr::Header hd = tnsr::load_header(path);
+    if (hd.code != int(tt.dtype) || hd.shape != tt.shape)
+      throw TypeError(std::string("TNSR file ") + path + " does not match parameter " + name);
+    std::vector<char> buf(size_t(nbytes(tt)));
+    tnsr::load(path, buf.data(), int64_t(buf.size()));
+    tcb_check(tcb_memcpy(s->vm.param_ptr(idx), buf.data(), uint64_t(buf.size()), 0, s->stream), "h2d");
+    tcb_check(tcb_stream_sync(s->stream), "sync");
   });
 }
 

@@ -61,6 +61,14 @@ def lib():
         L.tb_synthetic_batch.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p,
                                          ctypes.c_void_p, ctypes.c_int]
         L.tb_cache_stats.argtypes = [ctypes.POINTER(ctypes.c_int64)]
+        L.tb_cache_clear.argtypes = []
+        L.tb_tnsr_save.argtypes = [ctypes.c_char_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
+                                   ctypes.POINTER(ctypes.c_int64)]
+        L.tb_tnsr_header.argtypes = [ctypes.c_char_p, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int),
+                                     ctypes.POINTER(ctypes.c_int64), ctypes.c_int]
+        L.tb_tnsr_load.argtypes = [ctypes.c_char_p, ctypes.c_void_p, ctypes.c_int64]
+        L.tb_session_save_param.argtypes = [ctypes.c_void_p, ctypes.c_char_p, ctypes.c_char_p]
+        L.tb_session_load_param.argtypes = [ctypes.c_void_p, ctypes.c_char_p, ctypes.c_char_p]
         _lib = L
     return _lib
 
@@ -300,6 +308,45 @@ class Session:
     def set_comm(self, comm: int):
         _check(lib().tb_session_set_comm(self.h, comm))
 
+    STATE = ("params", "p16", "m", "v", "step")
+
+    def state_names(self) -> list[str]:
+        """Training-state parameters of this step graph (master weights, the
+        bf16 compute copy, Adam moments, step counter) -- what a checkpoint holds."""
+        out = []
+        for n in self.STATE:
+            try:
+                self.param_ptr(n)
+            except RuntimeError:
+                continue
+            out.append(n)
+        return out
+
+    def save_param(self, name: str, path: str):
+        """One step parameter -> TNSR file (tensor.hpp:80-104 layout; bf16 code 2)."""
+        _check(lib().tb_session_save_param(self.h, name.encode(), os.fsencode(path)))
+
+    def load_param(self, name: str, path: str):
+        """TNSR file -> step parameter (dtype code and shape must match)."""
+        _check(lib().tb_session_load_param(self.h, name.encode(), os.fsencode(path)))
+
+    def save_checkpoint(self, directory: str) -> list[str]:
+        """Write the training state as <directory>/<name>.tnsr, one file per state
+        parameter; on ZeRO ranks each rank writes its own shard (name.rank<r>)."""
+        os.makedirs(directory, exist_ok=True)
+        names = self.state_names()
+        sfx = f".rank{self.cfg.extra.get('rank', 0)}" if self.cfg.world > 1 else ""
+        for n in names:
+            self.save_param(n, os.path.join(directory, f"{n}{sfx}.tnsr"))
+        return names
+
+    def load_checkpoint(self, directory: str) -> list[str]:
+        names = self.state_names()
+        sfx = f".rank{self.cfg.extra.get('rank', 0)}" if self.cfg.world > 1 else ""
+        for n in names:
+            self.load_param(n, os.path.join(directory, f"{n}{sfx}.tnsr"))
+        return names
+
     def close(self):
         if getattr(self, "h", None):
             lib().tb_session_destroy(self.h)
@@ -312,7 +359,39 @@ class Session:
             pass
 
 
+TNSR_CODES = {np.dtype(np.float32): 0, np.dtype(np.float16): 1, np.dtype(np.int32): 3}
+TNSR_DTYPES = {0: np.float32, 1: np.float16, 2: np.uint16, 3: np.int32}  # 2 = bf16 bits
+
+
+def tnsr_save(path: str, arr: np.ndarray, code: int | None = None):
+    """Host array -> TNSR file through the native writer (host/tnsr.hpp).
+    bf16 is passed as uint16 bit patterns with code=2."""
+    arr = np.require(arr, requirements="C")  # keeps rank 0 (ascontiguousarray would not)
+    if code is None:
+        code = TNSR_CODES[arr.dtype]
+    if np.dtype(TNSR_DTYPES[code]).itemsize != arr.itemsize:
+        raise TypeError(f"array dtype {arr.dtype} does not match TNSR code {code}")
+    shape = (ctypes.c_int64 * max(arr.ndim, 1))(*arr.shape)
+    _check(lib().tb_tnsr_save(os.fsencode(path), arr.ctypes.data, code, arr.ndim, shape))
+
+
+def tnsr_load(path: str) -> tuple[np.ndarray, int]:
+    """TNSR file -> (array, code) through the native reader."""
+    code, rank = ctypes.c_int(), ctypes.c_int()
+    shape = (ctypes.c_int64 * 255)()
+    _check(lib().tb_tnsr_header(os.fsencode(path), ctypes.byref(code), ctypes.byref(rank), shape, 255))
+    out = np.empty(tuple(shape[:rank.value]), TNSR_DTYPES[code.value])
+    _check(lib().tb_tnsr_load(os.fsencode(path), out.ctypes.data, out.nbytes))
+    return out, code.value
+
+
 def cache_stats() -> dict:
     out = (ctypes.c_int64 * 3)()
     _check(lib().tb_cache_stats(out))
     return {"compiles": out[0], "hits": out[1], "size": out[2]}
+
+
+def cache_clear():
+    """Drop every compiled plan and its device scratch (KernelCache::clear,
+    backends.hpp:356-361).  Call only with no Session alive."""
+    _check(lib().tb_cache_clear())
