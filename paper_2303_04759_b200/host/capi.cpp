@@ -10,6 +10,7 @@
 
 #include "models.hpp"
 #include "tnsr.hpp"
+#include "trainc_b200.h"
 #include "vm.hpp"
 
 namespace tb {

@@ -20,7 +20,7 @@ CXXFLAGS = ["-std=c++20", "-O2", "-fPIC", "-Wall", "-Wno-unused-variable", "-Wno
 
 def _sources():
     hs = [os.path.join(PKG, "host", f) for f in os.listdir(os.path.join(PKG, "host"))]
-    return hs + [os.path.join(ROOT, "include", "tcb200.h")]
+    return hs + [os.path.join(ROOT, "include", h) for h in ("tcb200.h", "trainc_b200.h")]
 
 
 def build_host(force: bool = False) -> str:
