@@ -16,6 +16,7 @@
  *   tb_session_save_param / load_param
  *                       <- the TNSR parameter dumps of `trainc train` (checkpoint /
  *                          resume of params, bf16 copy, Adam m/v, step)
+ *   tb_autocast_info    <- the autocast + place_casts passes
  *   tb_cache_stats/clear <- KernelCache::compiles/hits/size/clear
  *                          (backends.hpp:356-368)
  *
@@ -55,6 +56,9 @@ int tb_session_param(void* h, const char* name, void** ptr, int64_t* bytes);
 const char* tb_session_segments(void* h);
 const char* tb_session_text(void* h, const char* what);
 int tb_session_set_comm(void* h, void* comm);
+
+/* AutoCast pass census on the all-f32 step (CPU only; host/autocast.hpp) */
+int tb_autocast_info(const char* cfg, const char* policy, const char* placement, int64_t* out, int n);
 
 /* KernelCache */
 int tb_cache_clear(void); /* only with no session alive */

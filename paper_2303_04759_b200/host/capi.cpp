@@ -8,6 +8,7 @@
 #include <memory>
 #include <sstream>
 
+#include "autocast.hpp"
 #include "models.hpp"
 #include "tnsr.hpp"
 #include "trainc_b200.h"
@@ -101,15 +102,22 @@ static void prepare(Session& s, const char* cfg_c) {
   std::istringstream is(all);
   std::string kv;
   int do_schedule = 0;
+  std::string amp;
   while (std::getline(is, kv, ';')) {
     if (kv.rfind("budget=", 0) == 0) s.budget = std::stoll(kv.substr(7));
     else if (kv.rfind("schedule=", 0) == 0) do_schedule = std::stoi(kv.substr(9));
+    else if (kv.rfind("autocast=", 0) == 0) amp = kv.substr(9);
     else if (kv.rfind("rank=", 0) == 0) s.rank = std::stoi(kv.substr(5));
     else if (!kv.empty()) model += kv + ";";
   }
   s.cfg = parse_cfg(model);
   s.ts = build_train_step(s.cfg);
   FunctionPtr fn = s.ts.fn;
+  if (!amp.empty()) {  // graph-generation pass: AutoCast the all-f32 step (SPEC.md:721 phase order)
+    if (s.cfg.dtype != "f32") throw Error("autocast: expects the all-f32 step (dtype=f32)");
+    PrecisionPolicy pol = amp == "b200" ? b200_policy() : amp == "default" ? default_policy() : all_f32_policy();
+    fn = autocast(*fn, pol);
+  }
   if (do_schedule) fn = ir::make_fn(fn->name, fn->params, schedule(*fn, s.ts.state_binding));
   if (s.budget > 0) {
     auto [rf, plan] = rematerialize(*fn, s.budget, s.ts.state_binding);
@@ -344,6 +352,28 @@ const char* tb_session_text(void* h, const char* what) {
 
 int tb_session_set_comm(void* h, void* comm) {
   TB_TRY(static_cast<Session*>(h)->vm.set_comm(comm));
+}
+
+/// CPU-only: run the AutoCast pass (host/autocast.hpp) on the all-f32 training
+/// step of `cfg` under policy "default", "b200" or "f32", with
+/// placement "auto" (exclusive/shared) or "shared".  out: sites, casts,
+/// exclusive, shared, low_ops, f32_violations, standalone_casts, param_casts, lets
+int tb_autocast_info(const char* cfg, const char* policy, const char* placement, int64_t* out, int n) {
+  TB_TRY({
+    ensure_registered(split_ws(tcb_supported_ops()));
+    ModelCfg c = parse_cfg(cfg ? cfg : "");
+    if (c.dtype != "f32") throw Error("autocast: expects the all-f32 step (dtype=f32)");
+    TrainStep ts = build_train_step(c);
+    const std::string pn = policy ? policy : "default";
+    PrecisionPolicy pol = pn == "b200" ? b200_policy() : pn == "f32" ? all_f32_policy() : default_policy();
+    if (pn != "default" && pn != "b200" && pn != "f32") throw Error("autocast: unknown policy " + pn);
+    const std::string pl = placement ? placement : "auto";
+    CastReport r;
+    FunctionPtr fn = autocast(*ts.fn, pol, &r, pl == "shared" ? Placement::AllShared : Placement::Auto);
+    int64_t v[] = {r.sites, r.casts, r.exclusive, r.shared, r.low_ops, r.f32_violations, r.standalone_casts,
+                   r.param_casts, int64_t(ir::flatten(*fn).lets.size())};
+    for (int i = 0; i < n && i < int(sizeof v / sizeof v[0]); ++i) out[i] = v[i];
+  });
 }
 
 /// KernelCache::clear (backends.hpp:356-361) plus the plans (and their device

@@ -62,6 +62,8 @@ def lib():
                                          ctypes.c_void_p, ctypes.c_int]
         L.tb_cache_stats.argtypes = [ctypes.POINTER(ctypes.c_int64)]
         L.tb_cache_clear.argtypes = []
+        L.tb_autocast_info.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p,
+                                       ctypes.POINTER(ctypes.c_int64), ctypes.c_int]
         L.tb_tnsr_save.argtypes = [ctypes.c_char_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
                                    ctypes.POINTER(ctypes.c_int64)]
         L.tb_tnsr_header.argtypes = [ctypes.c_char_p, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int),
@@ -395,3 +397,16 @@ def cache_clear():
     """Drop every compiled plan and its device scratch (KernelCache::clear,
     backends.hpp:356-361).  Call only with no Session alive."""
     _check(lib().tb_cache_clear())
+
+
+AUTOCAST_FIELDS = ("sites", "casts", "exclusive", "shared", "low_ops", "f32_violations", "standalone_casts",
+                   "param_casts", "lets")
+
+
+def autocast_info(cfg: "ModelConfig", policy: str = "b200", placement: str = "auto") -> dict:
+    """Run the AutoCast pass on the all-f32 training step of `cfg` (CPU only)
+    and return its cast census (host/autocast.hpp)."""
+    out = (ctypes.c_int64 * len(AUTOCAST_FIELDS))()
+    _check(lib().tb_autocast_info(cfg.cfg_string(model_only=True).encode(), policy.encode(), placement.encode(),
+                                  out, len(AUTOCAST_FIELDS)))
+    return dict(zip(AUTOCAST_FIELDS, list(out)))
