@@ -1,3 +1,4 @@
+#include <sstream>
 // interp.cpp -- the reference ANF interpreter, "the universal oracle"
 // (SPEC.md:636), over the CPU restatement of exec_base (oracle.c).
 // TEST INFRASTRUCTURE: loaded only by tests/, smoke() and bench.py's CPU legs.
@@ -10,6 +11,7 @@
 #include <cstring>
 #include <memory>
 
+#include "autocast.hpp"
 #include "models.hpp"
 #include "oracle.h"
 
@@ -210,7 +212,16 @@ void run_world_step(std::vector<Interp>& R) {
 std::unique_ptr<Interp> make_interp(const std::string& cfg, int rank) {
   ensure_registered({});
   auto I = std::make_unique<Interp>();
-  I->ts = build_train_step(parse_cfg(cfg));
+  // optional "autocast=<policy>" key: interpret the AutoCast'd f32 step
+  std::string model, amp, kv;
+  std::istringstream is(cfg);
+  while (std::getline(is, kv, ';')) {
+    if (kv.rfind("autocast=", 0) == 0) amp = kv.substr(9);
+    else if (!kv.empty()) model += kv + ";";
+  }
+  I->ts = build_train_step(parse_cfg(model));
+  if (!amp.empty())
+    I->ts.fn = autocast(*I->ts.fn, amp == "b200" ? b200_policy() : amp == "default" ? default_policy() : all_f32_policy());
   const auto& ps = I->ts.fn->params;
   for (auto& p : ps) I->state.push_back(std::make_shared<std::vector<uint32_t>>(size_t(numel(p->ty.tensor())), 0u));
   // params (this rank's shard under ZeRO) / half copy from the shared

@@ -807,6 +807,10 @@ static void b_layer_norm_dx(Plan& p) {
   const bool has_res = int(p.in.size()) - int(mask_in) > 5, has_dx = int(p.out.size()) - int(bias) > 3;
   const int nin = int(p.in.size());
   if (mask_in) require(H % 8 == 0, "layer_norm_dx: mask_in needs H % 8 == 0");
+  // the kernels read every activation-shaped input (dy, x, the residual dy2) as S's dtype
+  for (int i = 1; i < nin - int(mask_in); ++i)
+    if (p.in[i].numel() == S.numel())
+      require(p.in[i].dtype == S.dtype, "layer_norm_dx: activation-shaped inputs must share one dtype");
   const int di = has_dx ? 4 : 3;  // index of the fused bias-grad output
   require(int(p.out.size()) - int(bias) >= 3, "layer_norm_dx: outputs (ds, dg, db [, dx] [, dbias])");
   if (bias) require(p.out[di].dtype == TCB_F32 && p.out[di].numel() == H, "layer_norm_dx: dbias is f32 [H]");

@@ -38,8 +38,9 @@ namespace tb {
 
 /// F32Math: the op computes in f32 but its b200 kernel loads low-precision
 /// inputs and widens them in registers -- the cast-up lives inside the
-/// consumer's kernel.  Its inputs are unified to the low dtype when any of them
-/// is low (the b200 kernels take one storage dtype), else stay f32.
+/// consumer's kernel.  Activation-shaped f32 inputs next to a low one are cast
+/// down (the b200 kernels read one activation storage dtype); statistics,
+/// gamma and beta keep theirs.
 enum class Prec { Low, F32, Follow, F32Math };
 
 struct PrecisionPolicy {
@@ -156,17 +157,26 @@ inline FunctionPtr autocast(const ir::FunctionIR& fn, const PrecisionPolicy& pol
       const Prec pr = pol.of(base);
       DType target = kF32;
       if (pr == Prec::F32Math) {
-        // inputs as they are when the b200 relation takes the mix (e.g. bf16
-        // activations with f32 LayerNorm statistics); else unify to low
-        try {
-          let_ty[i] = opreg::registry().type_rel_of(e->op)(in, e->call_attrs);
-          ty[b.var.get()] = let_ty[i];
-          continue;
-        } catch (const TypeError&) {
-          target = kF32;
-          for (auto& t : in)
-            if (t.is_tensor() && t.tensor().dtype == pol.low) target = pol.low;
+        // the b200 kernels read all activation-shaped inputs (those shaped like
+        // a low-precision input) in one storage dtype and widen on load; the
+        // statistics / gamma / beta keep their own dtype
+        std::set<std::vector<int64_t>> low_shapes;
+        for (auto& t : in)
+          if (t.is_tensor() && t.tensor().dtype == pol.low) low_shapes.insert(t.tensor().shape);
+        // f32 accumulators by contract (embedding_dx's base gradient)
+        static const std::map<std::string, std::set<size_t>> pinned_f32 = {{"embedding_dx", {2}}};
+        auto pin = pinned_f32.find(base);
+        for (size_t k = 0; k < in.size(); ++k) {
+          if (!in[k].is_tensor() || in[k].tensor().dtype != kF32 || !low_shapes.count(in[k].tensor().shape)) continue;
+          if (pin != pinned_f32.end() && pin->second.count(k)) continue;
+          sites.push_back({e->args[k]->var.get(), i, k, pol.low});
+          auto t = in[k].tensor();
+          t.dtype = pol.low;
+          in[k] = Type(t);
         }
+        let_ty[i] = opreg::registry().type_rel_of(e->op)(in, e->call_attrs);
+        ty[b.var.get()] = let_ty[i];
+        continue;
       } else if (pr == Prec::Low) {
         target = pol.low;
       }

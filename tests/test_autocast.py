@@ -95,3 +95,36 @@ def test_amp_verify_autocast_step_on_device():
     assert np.all(np.isfinite(amp))
     assert amp[-1] < amp[0]  # it trains
     assert float(np.max(np.abs(amp - f32))) <= 5e-2, (f32, amp)
+
+
+@pytest.mark.gpu
+def test_autocast_step_matches_oracle_interpreter():
+    """The device run of the AutoCast'd step against the CPU oracle interpreter
+    of the same graph: first loss within 1e-5 relative, and every parameter
+    segment's Adam update within 2e-2 relative (bf16 GEMM accumulation order)."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import numpy as np
+    from oracle.interp_py import Interp
+    from paper_2303_04759_b200.session import Session, synthetic_batch
+    cfg = ModelConfig.tiny(opt="adam", lr=1e-3)
+    cfg.extra["autocast"] = "b200"
+    ids, labels = synthetic_batch(cfg)
+    s = Session(cfg)
+    s.init_params()
+    p0 = s.read("params")
+    s.set_batch(ids, labels)
+    s.step(graph=False)
+    ld = s.loss()
+    pd = s.read("params")
+    o = Interp(cfg.cfg_string(model_only=True) + ";autocast=b200")
+    lo = o.step(ids, labels)
+    po = o.read("params", pd.size)
+    assert abs(ld - lo) <= 1e-5 * abs(lo)
+    for name, off, n in s.segments():
+        d = pd[off:off + n] - p0[off:off + n]
+        r = po[off:off + n] - p0[off:off + n]
+        err = np.linalg.norm(d - r) / max(np.linalg.norm(r), 1e-30)
+        assert err <= 2e-2, (name, err)
+    s.close()
