@@ -11,6 +11,8 @@
  *                          [schedule] -> [remat under budget] -> dispatch to b200
  *   tb_session_step     <- vm::run of the all-in-one step function
  *   tb_graph_info/text  <- `trainc inspect` (IR, bytecode, memory curve) on CPU
+ *   tb_text_reprint     <- parse_text / print_text (text.hpp:156-160, :620) with
+ *                          bf16 / i32 parameter tokens (host/text_ext.hpp)
  *   tb_tnsr_*           <- save_tensor / load_tensor (tensor.hpp:76-139), with the
  *                          bf16 (2) and i32 (3) extension codes
  *   tb_session_save_param / load_param
@@ -36,7 +38,8 @@ const char* tb_last_error(void);
 
 /* CPU-only graph inspection (no device): cfg is "kind=bert;L=12;H=768;..." */
 int tb_graph_info(const char* cfg, int64_t* out, int n);
-const char* tb_graph_text(const char* cfg, const char* what);
+const char* tb_graph_text(const char* cfg, const char* what); /* "ir" | "text" | "mem" */
+const char* tb_text_reprint(const char* text); /* parse (text.hpp + bf16/i32) -> print */
 
 /* device session: compiled step + static arena + state on `device` */
 void* tb_session_create(const char* cfg, int device);

@@ -10,6 +10,7 @@
 
 #include "autocast.hpp"
 #include "models.hpp"
+#include "text_ext.hpp"
 #include "tnsr.hpp"
 #include "trainc_b200.h"
 #include "vm.hpp"
@@ -163,6 +164,8 @@ const char* tb_graph_text(const char* cfg, const char* what) {
       os << "index,live_bytes\n";
       for (size_t i = 0; i < mp.curve.size(); ++i) os << i << "," << mp.curve[i] << "\n";
       g_text = os.str();
+    } else if (w == "text") {
+      g_text = print_text_ext(*s.fn);  // the reference's text IR (text.hpp) + bf16/i32 tokens
     } else {
       g_text = print_fn(*s.fn);
     }
@@ -352,6 +355,22 @@ const char* tb_session_text(void* h, const char* what) {
 
 int tb_session_set_comm(void* h, void* comm) {
   TB_TRY(static_cast<Session*>(h)->vm.set_comm(comm));
+}
+
+/// Parse text IR (text_ext.hpp: the reference's format plus bf16/i32
+/// parameter tokens), re-infer every type, and print it again.  Returns NULL
+/// with tb_last_error() on a parse or type error.
+const char* tb_text_reprint(const char* text) {
+  try {
+    ensure_registered(split_ws(tcb_supported_ops()));
+    ir::ModuleIR m = parse_text_ext(text ? text : "");
+    if (m.functions.size() != 1) throw Error("tb_text_reprint: expects one function");
+    g_text = print_text_ext(*m.functions[0].second);
+    return g_text.c_str();
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
 }
 
 /// CPU-only: run the AutoCast pass (host/autocast.hpp) on the all-f32 training

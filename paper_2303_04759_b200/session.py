@@ -62,6 +62,8 @@ def lib():
                                          ctypes.c_void_p, ctypes.c_int]
         L.tb_cache_stats.argtypes = [ctypes.POINTER(ctypes.c_int64)]
         L.tb_cache_clear.argtypes = []
+        L.tb_text_reprint.restype = ctypes.c_char_p
+        L.tb_text_reprint.argtypes = [ctypes.c_char_p]
         L.tb_autocast_info.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p,
                                        ctypes.POINTER(ctypes.c_int64), ctypes.c_int]
         L.tb_tnsr_save.argtypes = [ctypes.c_char_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
@@ -410,3 +412,11 @@ def autocast_info(cfg: "ModelConfig", policy: str = "b200", placement: str = "au
     _check(lib().tb_autocast_info(cfg.cfg_string(model_only=True).encode(), policy.encode(), placement.encode(),
                                   out, len(AUTOCAST_FIELDS)))
     return dict(zip(AUTOCAST_FIELDS, list(out)))
+
+
+def text_reprint(text: str) -> str:
+    """Parse text IR (the reference format + bf16/i32 tokens) and print it again."""
+    t = lib().tb_text_reprint(text.encode())
+    if t is None:
+        raise RuntimeError(lib().tb_last_error().decode())
+    return t.decode()
