@@ -420,3 +420,44 @@ def text_reprint(text: str) -> str:
     if t is None:
         raise RuntimeError(lib().tb_last_error().decode())
     return t.decode()
+
+
+def train_report(cfg: "ModelConfig", steps: int, path: str | None = None, seed: int | None = None,
+                 graph: bool = True) -> list[tuple[int, float, float, int]]:
+    """`trainc train --report out.csv`: run `steps` training
+    steps on synthetic data from `seed` and return / write rows of
+    (step, loss, iter_time, peak_pool_bytes).  iter_time is the step's device
+    time in seconds (CUDA events on the session stream); peak_pool_bytes is the
+    static arena + state the memory planner reserved (the VM never allocates
+    inside a step).  Same seed -> identical loss column."""
+    from . import runtime as R
+    s = Session(cfg)
+    rows = []
+    try:
+        s.init_params()
+        info = s.info()
+        pool = int(info["arena_bytes"]) + int(info["state_bytes"])
+        L = R.lib()
+        ev0, ev1 = ctypes.c_void_p(), ctypes.c_void_p()
+        R.check(L.tcb_event_create(ctypes.byref(ev0)))
+        R.check(L.tcb_event_create(ctypes.byref(ev1)))
+        for k in range(steps):
+            ids, labels = synthetic_batch(cfg, seed=(cfg.seed_d if seed is None else seed) + k)
+            s.set_batch(ids, labels)
+            R.check(L.tcb_event_record(ev0, ctypes.c_void_p(s.stream)))
+            s.step(graph=graph)
+            R.check(L.tcb_event_record(ev1, ctypes.c_void_p(s.stream)))
+            loss = s.loss()
+            ms = ctypes.c_float()
+            R.check(L.tcb_event_elapsed_ms(ev0, ev1, ctypes.byref(ms)))
+            rows.append((k, loss, ms.value * 1e-3, pool))
+        L.tcb_event_destroy(ev0)
+        L.tcb_event_destroy(ev1)
+    finally:
+        s.close()
+    if path is not None:
+        with open(path, "w") as f:
+            f.write("step,loss,iter_time,peak_pool_bytes\n")
+            for k, loss, t, pool in rows:
+                f.write(f"{k},{float(loss):.9g},{t:.6e},{pool}\n")  # 9 digits round-trip an f32
+    return rows

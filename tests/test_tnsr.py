@@ -180,3 +180,20 @@ def test_checkpoint_resume_bit_identical(tmp_path):
         b.load_param("params", str(tmp_path / "wrong.tnsr"))
     a.close()
     b.close()
+
+
+@pytest.mark.gpu
+def test_train_report_csv_deterministic(tmp_path):
+    """`trainc train --report`: header-only for 0 steps; the
+    same seed twice gives identical CSVs except the timing column."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    cfg = S.ModelConfig.tiny(dtype="bf16", opt="adam", lr=1e-3)
+    S.train_report(cfg, 0, str(tmp_path / "r0.csv"))
+    assert open(tmp_path / "r0.csv").read() == "step,loss,iter_time,peak_pool_bytes\n"
+    a = S.train_report(cfg, 5, str(tmp_path / "a.csv"), seed=11)
+    b = S.train_report(cfg, 5, str(tmp_path / "b.csv"), seed=11)
+    strip = lambda p: [l.split(",")[:2] + l.split(",")[3:] for l in open(p).read().splitlines()]
+    assert strip(tmp_path / "a.csv") == strip(tmp_path / "b.csv")
+    assert len(a) == 5 and all(r[2] > 0 for r in a) and all(r[3] > 0 for r in a)
