@@ -137,3 +137,25 @@ def test_remat_with_tuple_replays_bit_identical():
     l1, p1, info = run(cfg_r)
     assert info["remat_replays"] > 0
     assert np.array_equal(l0, l1) and np.array_equal(p0, p1)
+
+
+def test_fusion_launches_strictly_fewer_kernels():
+    """`inspect --kernels` before vs after fusion: the fused step
+    launches strictly fewer kernels, and the unfused step still matches the
+    oracle (fusion changes launches, not the training result's tolerance)."""
+    def run(fuse):
+        cfg = ModelConfig.tiny(dtype="bf16", opt="adam", lr=1e-3, fuse=fuse)
+        s = Session(cfg)
+        s.init_params()
+        ids, labels = synthetic_batch(cfg)
+        s.set_batch(ids, labels)
+        s.step()
+        k = s.info()["kernels_per_step"]
+        loss = s.loss()
+        s.close()
+        return k, loss
+
+    k0, l0 = run(0)
+    k1, l1 = run(1)
+    assert k1 < k0, (k0, k1)
+    assert abs(l0 - l1) <= 2e-2, (l0, l1)
