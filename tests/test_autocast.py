@@ -69,7 +69,7 @@ def test_rejects_non_f32_step():
 def test_amp_verify_autocast_step_on_device():
     """amp_verify: the AutoCast'd f32 step runs on the b200
     device VM and its loss trajectory stays within 5e-2 of the f32 step's over
-    30 Adam steps on identical data and init (SPEC.md:788 threshold)."""
+    50 Adam steps on identical data and init (SPEC.md:788 threshold)."""
     torch = pytest.importorskip("torch")
     if not torch.cuda.is_available():
         pytest.skip("no GPU")
@@ -83,7 +83,7 @@ def test_amp_verify_autocast_step_on_device():
         s.init_params()
         ids, labels = synthetic_batch(cfg)
         out = []
-        for _ in range(30):
+        for _ in range(50):
             s.set_batch(ids, labels)
             s.step()
             out.append(s.loss())
@@ -94,7 +94,10 @@ def test_amp_verify_autocast_step_on_device():
     amp = losses({"autocast": "b200"})
     assert np.all(np.isfinite(amp))
     assert amp[-1] < amp[0]  # it trains
-    assert float(np.max(np.abs(amp - f32))) <= 5e-2, (f32, amp)
+    dmax = float(np.max(np.abs(amp - f32)))
+    print(f"amp_verify: 50 steps, max |dloss| = {dmax:.4g}; loss {f32[0]:.4f} -> {f32[-1]:.4f} (f32), "
+          f"{amp[-1]:.4f} (autocast)")
+    assert dmax <= 5e-2, (f32, amp)
 
 
 @pytest.mark.gpu
