@@ -220,8 +220,13 @@ std::unique_ptr<Interp> make_interp(const std::string& cfg, int rank) {
     else if (!kv.empty()) model += kv + ";";
   }
   I->ts = build_train_step(parse_cfg(model));
-  if (!amp.empty())
-    I->ts.fn = autocast(*I->ts.fn, amp == "b200" ? b200_policy() : amp == "default" ? default_policy() : all_f32_policy());
+  if (!amp.empty()) {
+    const bool fold = amp.size() > 5 && amp.compare(amp.size() - 5, 5, "+fold") == 0;
+    const std::string pn = fold ? amp.substr(0, amp.size() - 5) : amp;
+    I->ts.fn = autocast(*I->ts.fn, pn == "b200" ? b200_policy() : pn == "default" ? default_policy() : all_f32_policy());
+    if (fold)
+      I->ts.fn = fold_param_casts(*I->ts.fn, I->ts.i_params, I->ts.P_pad, &I->ts.i_p16, I->ts.state_binding);
+  }
   const auto& ps = I->ts.fn->params;
   for (auto& p : ps) I->state.push_back(std::make_shared<std::vector<uint32_t>>(size_t(numel(p->ty.tensor())), 0u));
   // params (this rank's shard under ZeRO) / half copy from the shared

@@ -332,4 +332,89 @@ inline FunctionPtr autocast(const ir::FunctionIR& fn, const PrecisionPolicy& pol
   return ir::make_fn(fn.name, fn.params, out);
 }
 
+/// After AutoCast: fold the per-step parameter casts into the optimizer's
+/// compute copy.  Every `convert(view(params){offset,shape}) -> bf16` becomes
+/// `view(p16){offset,shape}` of a new bf16 [P] state parameter, and the
+/// optimizer (`adam_update_ex`) emits that copy (half=bf16) as a new state
+/// output bound to p16.  p16 = bf16_rne(params) holds at step entry (the
+/// initialiser and the previous step's Adam both round the same master
+/// weights), so the result is bit-identical to the AutoCast'd step with the
+/// convert launches gone -- the structure of the hand-built bf16 graph.
+/// Returns the new function; *i_p16 and state_binding are updated.  World 1,
+/// Adam only (returns the input when there is nothing to fold).
+inline FunctionPtr fold_param_casts(const ir::FunctionIR& fn, int i_params, int64_t P_pad, int* i_p16,
+                                    std::vector<std::pair<int, int>>& state_binding, int* folded = nullptr) {
+  LetSeq seq = ir::flatten(fn);
+  const ir::Var* params = fn.params.at(size_t(i_params)).get();
+  std::map<const ir::Var*, const ExprPtr*> view_of;  // let var -> its view(params) call
+  for (auto& b : seq.lets)
+    if (b.value->kind == ExprKind::Call && base_name(b.value->op) == "view" &&
+        b.value->args.at(0)->var.get() == params)
+      view_of[b.var.get()] = &b.value;
+  size_t adam = seq.lets.size();
+  for (size_t i = 0; i < seq.lets.size(); ++i)
+    if (seq.lets[i].value->kind == ExprKind::Call && base_name(seq.lets[i].value->op) == "adam_update_ex") adam = i;
+  int n = 0;
+  for (auto& b : seq.lets)
+    if (b.value->kind == ExprKind::Call && base_name(b.value->op) == "convert" &&
+        ir::attr_string(b.value->call_attrs, "to", "") == "bf16" && view_of.count(b.value->args.at(0)->var.get()))
+      ++n;
+  if (folded) *folded = n;
+  if (n == 0 || adam == seq.lets.size()) return ir::make_fn(fn.name, fn.params, seq);
+
+  std::vector<VarPtr> ps = fn.params;
+  auto p16 = ir::make_var("p16", Type(TensorType{kBF16, {P_pad}}));
+  ps.push_back(p16);
+  *i_p16 = int(ps.size()) - 1;
+  LetSeq out;
+  VarPtr copy;
+  for (size_t i = 0; i < seq.lets.size(); ++i) {
+    auto b = seq.lets[i];
+    const auto& e = b.value;
+    if (e->kind == ExprKind::Call && base_name(e->op) == "convert" &&
+        ir::attr_string(e->call_attrs, "to", "") == "bf16" && view_of.count(e->args.at(0)->var.get())) {
+      const ExprPtr& vcall = *view_of[e->args[0]->var.get()];
+      auto nv = ir::call(vcall->op, {ir::var_ref(p16)}, vcall->call_attrs);
+      std::vector<Type> in{p16->ty};
+      nv->ty = opreg::registry().type_rel_of(vcall->op)(in, vcall->call_attrs);
+      out.lets.push_back({b.var, nv});
+      continue;
+    }
+    if (i == adam) {
+      AttrMap a = e->call_attrs;
+      a["half"] = std::string("bf16");
+      auto ne = ir::call(e->op, e->args, a);
+      std::vector<Type> in;
+      for (auto& x : e->args) in.push_back(x->var->ty);
+      ne->ty = opreg::registry().type_rel_of(e->op)(in, a);
+      auto v = ir::make_var(b.var->id, ne->ty, b.var->attrs);
+      out.lets.push_back({v, ne});
+      // later tuple_gets of the optimizer refer to the new var
+      for (size_t j = i + 1; j < seq.lets.size(); ++j) {
+        auto& ej = seq.lets[j].value;
+        if (ej->kind == ExprKind::TupleGet && ej->args[0]->var.get() == b.var.get()) {
+          auto g = ir::tuple_get(ir::var_ref(v), ej->index);
+          g->ty = ne->ty.tuple().fields.at(size_t(ej->index));
+          seq.lets[j].value = g;
+          seq.lets[j].var->ty = g->ty;
+        }
+      }
+      auto g = ir::tuple_get(ir::var_ref(v), 3);
+      g->ty = ne->ty.tuple().fields.at(3);
+      copy = ir::make_var("p16_next", g->ty);
+      out.lets.push_back({copy, g});
+      continue;
+    }
+    out.lets.push_back(b);
+  }
+  std::vector<ExprPtr> xs = seq.ret->args;
+  xs.push_back(ir::var_ref(copy));
+  TupleType tt;
+  for (auto& x : xs) tt.fields.push_back(x->var->ty.tensor());
+  out.ret = ir::tuple(xs);
+  out.ret->ty = tt;
+  state_binding.push_back({int(xs.size()) - 1, *i_p16});
+  return ir::make_fn(fn.name, ps, out);
+}
+
 }  // namespace tb

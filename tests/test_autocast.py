@@ -135,3 +135,35 @@ def test_autocast_step_matches_oracle_interpreter(policy):
         err = np.linalg.norm(d - r) / max(np.linalg.norm(r), 1e-30)
         assert err <= 2e-2, (name, err)
     s.close()
+
+
+@pytest.mark.gpu
+def test_fold_param_casts_bit_identical():
+    """fold_param_casts: the AutoCast'd step with its parameter converts folded
+    into the optimizer's bf16 compute copy is bit-identical to the unfolded
+    one (loss and master weights over 3 Adam steps) and launches fewer kernels."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import numpy as np
+    from paper_2303_04759_b200.session import Session, synthetic_batch
+
+    def run(key):
+        cfg = ModelConfig.tiny(opt="adam", lr=1e-3)
+        cfg.extra["autocast"] = key
+        s = Session(cfg)
+        s.init_params()
+        losses = []
+        for k in range(3):
+            s.set_batch(*synthetic_batch(cfg, seed=cfg.seed_d + k))
+            s.step()
+            losses.append(s.loss())
+        out = (np.array(losses, np.float32), s.read("params"), s.info()["kernels_per_step"])
+        s.close()
+        return out
+
+    l0, p0, k0 = run("b200")
+    l1, p1, k1 = run("b200+fold")
+    assert l0.tobytes() == l1.tobytes()
+    assert p0.tobytes() == p1.tobytes()
+    assert k1 < k0, (k0, k1)

@@ -37,4 +37,7 @@ direct = rate(ModelConfig.bert_base())
 c = ModelConfig.bert_base(dtype="f32")
 c.extra["autocast"] = "b200"
 amp = rate(c)
-print(json.dumps({"direct_bf16": direct, "autocast_b200": amp}))
+c = ModelConfig.bert_base(dtype="f32")
+c.extra["autocast"] = "b200+fold"
+fold = rate(c)
+print(json.dumps({"direct_bf16": direct, "autocast_b200": amp, "autocast_b200_fold": fold}))
