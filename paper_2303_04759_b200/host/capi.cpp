@@ -116,13 +116,29 @@ static void prepare(Session& s, const char* cfg_c) {
   FunctionPtr fn = s.ts.fn;
   if (!amp.empty()) {  // graph-generation pass: AutoCast the all-f32 step (SPEC.md:721 phase order)
     if (s.cfg.dtype != "f32") throw Error("autocast: expects the all-f32 step (dtype=f32)");
-    const bool fold = amp.size() > 5 && amp.compare(amp.size() - 5, 5, "+fold") == 0;
-    const std::string pn = fold ? amp.substr(0, amp.size() - 5) : amp;
+    // "<policy>[+fold[+fuse]]"
+    std::vector<std::string> parts;
+    {
+      std::istringstream ps(amp);
+      std::string t;
+      while (std::getline(ps, t, '+')) parts.push_back(t);
+    }
+    const std::string pn = parts.empty() ? "" : parts[0];
+    const bool fold = std::find(parts.begin(), parts.end(), "fold") != parts.end();
+    const bool refuse = std::find(parts.begin(), parts.end(), "fuse") != parts.end();
     PrecisionPolicy pol = pn == "b200" ? b200_policy() : pn == "default" ? default_policy() : all_f32_policy();
     fn = autocast(*fn, pol);
     if (fold) {  // parameter casts -> the optimizer's bf16 compute copy
       if (s.cfg.world != 1 || s.cfg.opt != "adam") throw Error("autocast +fold: world 1 Adam steps only");
       fn = fold_param_casts(*fn, s.ts.i_params, s.ts.P_pad, &s.ts.i_p16, s.ts.state_binding);
+      s.ts.fn = fn;
+    }
+    if (refuse) {
+      // fusion again on the now-bf16 graph: dgrad+wgrad pairs (K-sliced wgrad,
+      // a different f32 summation order) and the other bf16-only patterns
+      LetSeq fs = ir::flatten(*fn);
+      fuse(fs, s.cfg.fuse != 0);
+      fn = ir::make_fn(fn->name, fn->params, fs);
       s.ts.fn = fn;
     }
   }

@@ -33,11 +33,15 @@ def rate(cfg, steps=20, warm=5):
             "kernels_per_step": info["kernels_per_step"], "loss": round(loss, 4)}
 
 
-direct = rate(ModelConfig.bert_base())
-c = ModelConfig.bert_base(dtype="f32")
-c.extra["autocast"] = "b200"
-amp = rate(c)
-c = ModelConfig.bert_base(dtype="f32")
-c.extra["autocast"] = "b200+fold"
-fold = rate(c)
-print(json.dumps({"direct_bf16": direct, "autocast_b200": amp, "autocast_b200_fold": fold}))
+import sys
+
+keys = sys.argv[1:] or ["direct", "b200", "b200+fold", "b200+fold+fuse"]
+out = {}
+for k in keys:
+    if k == "direct":
+        out["direct_bf16"] = rate(ModelConfig.bert_base())
+    else:
+        c = ModelConfig.bert_base(dtype="f32")
+        c.extra["autocast"] = k
+        out["autocast_" + k] = rate(c)
+print(json.dumps(out))
