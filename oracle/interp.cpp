@@ -11,8 +11,7 @@
 #include <cstring>
 #include <memory>
 
-#include "autocast.hpp"
-#include "models.hpp"
+#include "pipeline.hpp"
 #include "oracle.h"
 
 namespace {
@@ -30,6 +29,7 @@ struct Interp {
   TrainStep ts;
   std::vector<std::shared_ptr<std::vector<uint32_t>>> state;  // one per fn param
   double last_loss = 0;
+  std::vector<uint32_t> last_grad;  // the optimizer's gradient input of the last step (f32 slots)
 };
 
 orc_tensor odesc(std::vector<uint32_t>& buf, const TensorType& t) {
@@ -148,6 +148,11 @@ void run_step(Interp& I, CollFn coll = nullptr, int rank = 0) {
       env[b.var.get()] = std::move(out);
       continue;
     }
+    if (e->kind == ExprKind::Call) {
+      const std::string base = base_name(e->op);
+      if (base == "sgd_update" || base == "adam_update" || base == "adam_update_ex")
+        I.last_grad = *env.at(e->args.at(1)->var.get()).fields[0];
+    }
     exec_let(env, b);
   }
   finish_step(I, env, seq);
@@ -220,13 +225,7 @@ std::unique_ptr<Interp> make_interp(const std::string& cfg, int rank) {
     else if (!kv.empty()) model += kv + ";";
   }
   I->ts = build_train_step(parse_cfg(model));
-  if (!amp.empty()) {
-    const bool fold = amp.size() > 5 && amp.compare(amp.size() - 5, 5, "+fold") == 0;
-    const std::string pn = fold ? amp.substr(0, amp.size() - 5) : amp;
-    I->ts.fn = autocast(*I->ts.fn, pn == "b200" ? b200_policy() : pn == "default" ? default_policy() : all_f32_policy());
-    if (fold)
-      I->ts.fn = fold_param_casts(*I->ts.fn, I->ts.i_params, I->ts.P_pad, &I->ts.i_p16, I->ts.state_binding);
-  }
+  if (!amp.empty()) apply_autocast(I->ts, amp);  // same parser and phases as the session
   const auto& ps = I->ts.fn->params;
   for (auto& p : ps) I->state.push_back(std::make_shared<std::vector<uint32_t>>(size_t(numel(p->ty.tensor())), 0u));
   // params (this rank's shard under ZeRO) / half copy from the shared
@@ -345,6 +344,32 @@ int orc_interp_read(void* h, const char* name, void* dst, int64_t nelem) {
     }
   g_err = std::string("no parameter ") + name;
   return 1;
+}
+
+/// overwrite function parameter `name` (f32 slots / i32) from host memory
+int orc_interp_write(void* h, const char* name, const void* src, int64_t nelem) {
+  auto* I = static_cast<Interp*>(h);
+  const auto& ps = I->ts.fn->params;
+  for (size_t i = 0; i < ps.size(); ++i)
+    if (ps[i]->id == name) {
+      if (nelem != int64_t(I->state[i]->size())) {
+        g_err = std::string("write ") + name + ": size mismatch";
+        return 1;
+      }
+      std::memcpy(I->state[i]->data(), src, size_t(nelem) * 4);
+      return 0;
+    }
+  g_err = std::string("no parameter ") + name;
+  return 1;
+}
+
+/// the flat gradient the optimizer consumed in the last step (before any
+/// ZeRO grad_scale), f32; returns its element count when dst is NULL
+int64_t orc_interp_read_grad(void* h, float* dst, int64_t nelem) {
+  auto* I = static_cast<Interp*>(h);
+  const int64_t n = int64_t(I->last_grad.size());
+  if (dst) std::memcpy(dst, I->last_grad.data(), size_t(std::min(n, nelem)) * 4);
+  return n;
 }
 
 }  // extern "C"

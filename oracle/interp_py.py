@@ -29,6 +29,9 @@ def lib():
         L.orc_interp_create_rank.argtypes = [ctypes.c_char_p, ctypes.c_int]
         L.orc_interp_step_coll.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                            ctypes.POINTER(ctypes.c_float), COLL_FN, ctypes.c_int]
+        L.orc_interp_write.argtypes = [ctypes.c_void_p, ctypes.c_char_p, ctypes.c_void_p, ctypes.c_int64]
+        L.orc_interp_read_grad.restype = ctypes.c_int64
+        L.orc_interp_read_grad.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64]
         L.orc_world_create.restype = ctypes.c_void_p
         L.orc_world_create.argtypes = [ctypes.c_char_p, ctypes.c_int]
         L.orc_world_destroy.argtypes = [ctypes.c_void_p]
@@ -111,6 +114,19 @@ class Interp:
         out = np.empty(n, np.float32)
         if lib().orc_interp_read(self.h, name.encode(), out.ctypes.data, n):
             raise RuntimeError(lib().orc_interp_last_error().decode())
+        return out
+
+    def write(self, name: str, arr: np.ndarray):
+        arr = np.ascontiguousarray(arr)
+        assert arr.itemsize == 4
+        if lib().orc_interp_write(self.h, name.encode(), arr.ctypes.data, arr.size):
+            raise RuntimeError(lib().orc_interp_last_error().decode())
+
+    def grad(self) -> np.ndarray:
+        """The flat f32 gradient the optimizer consumed in the last step."""
+        n = lib().orc_interp_read_grad(self.h, None, 0)
+        out = np.empty(n, np.float32)
+        lib().orc_interp_read_grad(self.h, out.ctypes.data, n)
         return out
 
     def __del__(self):

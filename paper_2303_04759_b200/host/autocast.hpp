@@ -417,4 +417,41 @@ inline FunctionPtr fold_param_casts(const ir::FunctionIR& fn, int i_params, int6
   return ir::make_fn(fn.name, ps, out);
 }
 
+/// The session key `autocast=<policy>[+fold][+fuse]`, parsed in ONE place for
+/// the device session (capi.cpp) and the oracle interpreter (oracle/interp.cpp)
+/// so both build the same graph.  Unknown policies and unknown '+' tokens are
+/// errors (never a silent all-f32 fallback).
+struct AutocastKey {
+  std::string policy;  // "b200" | "default" | "f32"
+  bool fold = false;   // fold_param_casts
+  bool fuse = false;   // fusion re-run on the bf16 graph
+};
+
+inline PrecisionPolicy policy_by_name(const std::string& pn) {
+  if (pn == "b200") return b200_policy();
+  if (pn == "default") return default_policy();
+  if (pn == "f32") return all_f32_policy();
+  throw Error("autocast: unknown policy '" + pn + "' (b200 | default | f32)");
+}
+
+inline AutocastKey parse_autocast_key(const std::string& key) {
+  AutocastKey k;
+  std::vector<std::string> parts;
+  size_t a = 0;
+  while (true) {
+    size_t b = key.find('+', a);
+    parts.push_back(key.substr(a, b == std::string::npos ? std::string::npos : b - a));
+    if (b == std::string::npos) break;
+    a = b + 1;
+  }
+  k.policy = parts[0];
+  (void)policy_by_name(k.policy);  // validates
+  for (size_t i = 1; i < parts.size(); ++i) {
+    if (parts[i] == "fold") k.fold = true;
+    else if (parts[i] == "fuse") k.fuse = true;
+    else throw Error("autocast: unknown key token '+" + parts[i] + "' in '" + key + "'");
+  }
+  return k;
+}
+
 }  // namespace tb

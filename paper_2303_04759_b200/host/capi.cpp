@@ -8,8 +8,7 @@
 #include <memory>
 #include <sstream>
 
-#include "autocast.hpp"
-#include "models.hpp"
+#include "pipeline.hpp"
 #include "text_ext.hpp"
 #include "tnsr.hpp"
 #include "trainc_b200.h"
@@ -115,32 +114,8 @@ static void prepare(Session& s, const char* cfg_c) {
   s.ts = build_train_step(s.cfg);
   FunctionPtr fn = s.ts.fn;
   if (!amp.empty()) {  // graph-generation pass: AutoCast the all-f32 step (SPEC.md:721 phase order)
-    if (s.cfg.dtype != "f32") throw Error("autocast: expects the all-f32 step (dtype=f32)");
-    // "<policy>[+fold[+fuse]]"
-    std::vector<std::string> parts;
-    {
-      std::istringstream ps(amp);
-      std::string t;
-      while (std::getline(ps, t, '+')) parts.push_back(t);
-    }
-    const std::string pn = parts.empty() ? "" : parts[0];
-    const bool fold = std::find(parts.begin(), parts.end(), "fold") != parts.end();
-    const bool refuse = std::find(parts.begin(), parts.end(), "fuse") != parts.end();
-    PrecisionPolicy pol = pn == "b200" ? b200_policy() : pn == "default" ? default_policy() : all_f32_policy();
-    fn = autocast(*fn, pol);
-    if (fold) {  // parameter casts -> the optimizer's bf16 compute copy
-      if (s.cfg.world != 1 || s.cfg.opt != "adam") throw Error("autocast +fold: world 1 Adam steps only");
-      fn = fold_param_casts(*fn, s.ts.i_params, s.ts.P_pad, &s.ts.i_p16, s.ts.state_binding);
-      s.ts.fn = fn;
-    }
-    if (refuse) {
-      // fusion again on the now-bf16 graph: dgrad+wgrad pairs (K-sliced wgrad,
-      // a different f32 summation order) and the other bf16-only patterns
-      LetSeq fs = ir::flatten(*fn);
-      fuse(fs, s.cfg.fuse != 0);
-      fn = ir::make_fn(fn->name, fn->params, fs);
-      s.ts.fn = fn;
-    }
+    apply_autocast(s.ts, amp);
+    fn = s.ts.fn;
   }
   if (do_schedule) fn = ir::make_fn(fn->name, fn->params, schedule(*fn, s.ts.state_binding));
   if (s.budget > 0) {
@@ -406,9 +381,7 @@ int tb_autocast_info(const char* cfg, const char* policy, const char* placement,
     ModelCfg c = parse_cfg(cfg ? cfg : "");
     if (c.dtype != "f32") throw Error("autocast: expects the all-f32 step (dtype=f32)");
     TrainStep ts = build_train_step(c);
-    const std::string pn = policy ? policy : "default";
-    PrecisionPolicy pol = pn == "b200" ? b200_policy() : pn == "f32" ? all_f32_policy() : default_policy();
-    if (pn != "default" && pn != "b200" && pn != "f32") throw Error("autocast: unknown policy " + pn);
+    const PrecisionPolicy pol = policy_by_name(policy ? policy : "default");
     const std::string pl = placement ? placement : "auto";
     CastReport r;
     FunctionPtr fn = autocast(*ts.fn, pol, &r, pl == "shared" ? Placement::AllShared : Placement::Auto);
