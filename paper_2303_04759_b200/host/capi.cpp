@@ -162,6 +162,10 @@ const char* tb_graph_text(const char* cfg, const char* what) {
       os << "index,live_bytes\n";
       for (size_t i = 0; i < mp.curve.size(); ++i) os << i << "," << mp.curve[i] << "\n";
       g_text = os.str();
+    } else if (w == "segments") {  // flat parameter layout: "name offset numel" per line
+      std::ostringstream os;
+      for (auto& g : s.ts.segs) os << g.name << " " << g.offset << " " << g.numel << "\n";
+      g_text = os.str();
     } else if (w == "text") {
       g_text = print_text_ext(*s.fn);  // the reference's text IR (text.hpp) + bf16/i32 tokens
     } else {

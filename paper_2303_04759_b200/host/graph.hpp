@@ -293,8 +293,21 @@ inline void register_default_adjoints() {
   };
 }
 
+/// dependency_report: per forward op, which forward tensors
+/// its ADJOINT retains -- its inputs x (by argument position) and its output y
+/// (for a tuple op: any field) -- read off the lets the adjoint emitted.
+/// tanh keeps only y (NeedsY), matmul both inputs, add nothing (NeedsNeither).
+struct DepEntry {
+  int let = -1;              // forward let index
+  std::string op;
+  std::vector<int> inputs;   // argument positions the adjoint reads
+  bool output = false;       // y (or a field of it) read by the adjoint
+};
+
 struct GradResult {
-  VarPtr flat_grad;  // f32 [P] in leaf-offset order
+  VarPtr flat_grad;             // f32 [P] in leaf-offset order
+  size_t n_forward = 0;         // lets before the backward
+  std::vector<DepEntry> deps;   // dependency_report, forward order
 };
 
 /// Reverse-mode AD of `loss` w.r.t. the leaves (which must tile [0, P) of the
@@ -332,6 +345,7 @@ inline GradResult autodiff(Graph& g, const VarPtr& loss, std::vector<Leaf> leave
     tgrad[{src.get(), 0}] = loss;  // placeholder: d loss = 1 (consumed by the CE adjoint)
   }
 
+  std::vector<DepEntry> deps_rev;
   for (size_t ii = fwd.lets.size(); ii-- > 0;) {
     const LetBinding& lb = fwd.lets[ii];
     const ExprPtr& e = lb.value;
@@ -364,7 +378,21 @@ inline GradResult autodiff(Graph& g, const VarPtr& loss, std::vector<Leaf> leave
     auto rule = adjoints().find(e->op);
     if (rule == adjoints().end()) throw NonDifferentiable("no adjoint registered for op " + e->op);
     AdjointCtx ctx{g, lb, dout};
+    const size_t mark = g.seq().lets.size();
     auto dins = rule->second(ctx);
+    {  // dependency_report: what this adjoint's lets read from the forward
+      DepEntry de;
+      de.let = int(ii);
+      de.op = e->op;
+      std::set<const ir::Var*> read;
+      for (size_t k = mark; k < g.seq().lets.size(); ++k)
+        for (auto& a : g.seq().lets[k].value->args)
+          if (a->kind == ExprKind::VarRef) read.insert(a->var.get());
+      for (size_t k = 0; k < e->args.size(); ++k)
+        if (e->args[k]->kind == ExprKind::VarRef && read.count(e->args[k]->var.get())) de.inputs.push_back(int(k));
+      de.output = read.count(lb.var.get()) > 0;
+      deps_rev.push_back(de);
+    }
     for (size_t j = 0; j < dins.size() && j < e->args.size(); ++j) {
       auto av = arg_var(e, j);
       if (av && dins[j]) accumulate(av, dins[j]);
@@ -380,17 +408,27 @@ inline GradResult autodiff(Graph& g, const VarPtr& loss, std::vector<Leaf> leave
   };
   for (auto& lf : leaves) {
     if (lf.offset < pos) throw Error("autodiff: parameter leaves overlap");
-    if (lf.offset > pos) parts.push_back(zeros(lf.offset - pos));  // alignment gap
+    if (lf.offset > pos) {  // alignment gap
+      parts.push_back(zeros(lf.offset - pos));
+      pos = lf.offset;
+    }
     auto it = grad.find(lf.view.get());
     if (it == grad.end()) throw NonDifferentiable("no gradient reaches parameter %" + lf.view->id);
     VarPtr d = it->second;
     if (d->ty.tensor().dtype != kF32) d = g.op("convert", {d}, {{"to", std::string("f32")}});
+    if (numel(d->ty.tensor()) != lf.numel)
+      throw Error("autodiff: gradient of %" + lf.view->id + " has " + std::to_string(numel(d->ty.tensor())) +
+                  " elements, the parameter " + std::to_string(lf.numel));
     parts.push_back(d);
     pos += lf.numel;
   }
   if (pos > P) throw Error("autodiff: leaves exceed the flat buffer");
   if (pos < P) parts.push_back(zeros(P - pos));
-  return {g.op("concat", parts, {}, "grad")};
+  GradResult r;
+  r.flat_grad = g.op("concat", parts, {}, "grad");
+  r.n_forward = fwd.lets.size();
+  r.deps.assign(deps_rev.rbegin(), deps_rev.rend());
+  return r;
 }
 
 // -------------------------------------------------------------------- fusion

@@ -317,6 +317,9 @@ inline TrainStep build_train_step(const ModelCfg& c) {
   // (SPEC.md:513,566 zero-padded shards)
   GradResult gr = autodiff(g, loss, leaves, ts.P_pad);
   VarPtr grad = gr.flat_grad;
+  if (numel(grad->ty.tensor()) != ts.P_pad)
+    throw Error("build_train_step: flat gradient has " + std::to_string(numel(grad->ty.tensor())) +
+                " elements, expected P_pad " + std::to_string(ts.P_pad));
 
   // ---- optimizer (+ ZeRO-1)
   std::vector<VarPtr> rets{loss};

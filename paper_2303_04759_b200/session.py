@@ -224,6 +224,15 @@ def graph_text(cfg: ModelConfig, what: str = "ir") -> str:
     return t
 
 
+def graph_segments(cfg: ModelConfig) -> list[tuple[str, int, int]]:
+    """CPU-only: the flat parameter segments (name, offset, numel) of cfg's step."""
+    out = []
+    for line in graph_text(cfg, "segments").splitlines():
+        n, o, k = line.split()
+        out.append((n, int(o), int(k)))
+    return out
+
+
 class Session:
     def __init__(self, cfg: ModelConfig, device: int = 0):
         self.cfg = cfg
