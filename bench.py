@@ -232,6 +232,7 @@ def _verify_step(batch: int, budget: int):
     import torch
     from paper_2303_04759_b200.session import ModelConfig, Session, cache_clear, synthetic_batch
     cfg = ModelConfig.bert_base(B=batch)
+    cfg.extra["schedule"] = 1  # p-c list schedule first: -0.26% peak at B~3k
     cfg.extra["budget"] = budget
     s = Session(cfg)
     try:

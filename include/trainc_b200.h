@@ -63,6 +63,12 @@ int tb_session_set_comm(void* h, void* comm);
 /* AutoCast pass census on the all-f32 step (CPU only; host/autocast.hpp) */
 int tb_autocast_info(const char* cfg, const char* policy, const char* placement, int64_t* out, int n);
 
+/* memsched on a text-IR function (CPU only; host/memsched.hpp):
+ * what = "liveness" | "curve" | "schedule" | "remat" (under budget bytes);
+ * transient_inputs: inputs die at their last use (SPEC.md example accounting).
+ * Returns NULL on error (tb_last_error). */
+const char* tb_memsched_text(const char* text, const char* what, int64_t budget, int transient_inputs);
+
 /* KernelCache */
 int tb_cache_clear(void); /* only with no session alive */
 int tb_cache_stats(int64_t* out3);

@@ -11,6 +11,7 @@
 #include <cstring>
 #include <memory>
 
+#include "memsched.hpp"
 #include "pipeline.hpp"
 #include "oracle.h"
 
@@ -219,13 +220,21 @@ std::unique_ptr<Interp> make_interp(const std::string& cfg, int rank) {
   auto I = std::make_unique<Interp>();
   // optional "autocast=<policy>" key: interpret the AutoCast'd f32 step
   std::string model, amp, kv;
+  int64_t budget = 0;
+  int sched = 0;
   std::istringstream is(cfg);
   while (std::getline(is, kv, ';')) {
     if (kv.rfind("autocast=", 0) == 0) amp = kv.substr(9);
+    else if (kv.rfind("budget=", 0) == 0) budget = std::stoll(kv.substr(7));
+    else if (kv.rfind("schedule=", 0) == 0) sched = std::stoi(kv.substr(9));
     else if (!kv.empty()) model += kv + ";";
   }
   I->ts = build_train_step(parse_cfg(model));
   if (!amp.empty()) apply_autocast(I->ts, amp);  // same parser and phases as the session
+  // the memsched phases in the session's order (capi.cpp prepare): the
+  // interpreter then executes the scheduled / rematerialised let sequence
+  if (sched) I->ts.fn = ir::make_fn(I->ts.fn->name, I->ts.fn->params, schedule(*I->ts.fn, I->ts.state_binding));
+  if (budget > 0) I->ts.fn = rematerialize(*I->ts.fn, budget, I->ts.state_binding).first;
   const auto& ps = I->ts.fn->params;
   for (auto& p : ps) I->state.push_back(std::make_shared<std::vector<uint32_t>>(size_t(numel(p->ty.tensor())), 0u));
   // params (this rank's shard under ZeRO) / half copy from the shared

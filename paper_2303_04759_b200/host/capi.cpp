@@ -162,6 +162,13 @@ const char* tb_graph_text(const char* cfg, const char* what) {
       os << "index,live_bytes\n";
       for (size_t i = 0; i < mp.curve.size(); ++i) os << i << "," << mp.curve[i] << "\n";
       g_text = os.str();
+    } else if (w == "remat") {  // the remat plan of cfg (needs budget=): one split per line
+      std::ostringstream os;
+      os << "replays " << s.remat.replays << "\npeak_before " << s.remat.peak_before << "\npeak_after "
+         << s.remat.peak_after << "\n";
+      for (auto& sp : s.remat.splits)
+        os << "split " << sp.victim << " " << sp.evict_index << " " << sp.replay_before << "\n";
+      g_text = os.str();
     } else if (w == "segments") {  // flat parameter layout: "name offset numel" per line
       std::ostringstream os;
       for (auto& g : s.ts.segs) os << g.name << " " << g.offset << " " << g.numel << "\n";
@@ -368,6 +375,70 @@ const char* tb_text_reprint(const char* text) {
     ir::ModuleIR m = parse_text_ext(text ? text : "");
     if (m.functions.size() != 1) throw Error("tb_text_reprint: expects one function");
     g_text = print_text_ext(*m.functions[0].second);
+    return g_text.c_str();
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
+
+/// CPU-only memsched on one text-IR function (text.hpp
+/// syntax + bf16/i32 parameter tokens).  transient_inputs: function inputs die
+/// at their last use (the accounting of SPEC.md's examples) instead of living
+/// throughout (the device VM).  what:
+///   "liveness"  one line per var field: "id field unit def last bytes" (unit =
+///               root storage unit; aliases share their source's unit)
+///   "curve"     "peak <bytes> <index>" then "i <live bytes>" per let
+///   "schedule"  p-c list schedule: "peak_before B", "peak_after B",
+///               "order id id ...", then the scheduled function's text
+///   "remat"     rematerialise under `budget`: "replays N", "peak_before B",
+///               "peak_after B", "split victim evict_index replay_before" per
+///               split, then the transformed function's text
+/// Returns NULL (tb_last_error) on parse/type errors or BudgetInfeasible.
+const char* tb_memsched_text(const char* text, const char* what, int64_t budget, int transient_inputs) {
+  try {
+    ensure_registered(split_ws(tcb_supported_ops()));
+    ir::ModuleIR m = parse_text_ext(text ? text : "");
+    if (m.functions.size() != 1) throw Error("tb_memsched_text: expects one function");
+    FunctionPtr fn = m.functions[0].second;
+    const bool tr = transient_inputs != 0;
+    const std::string w = what ? what : "";
+    std::ostringstream os;
+    if (w == "liveness") {
+      Layout L = build_layout(*fn, {}, true, tr);
+      auto line = [&](const ir::Var* v) {
+        const auto& rs = L.refs.at(v);
+        for (size_t k = 0; k < rs.size(); ++k) {
+          int u = L.root(rs[k].unit).first;
+          os << v->id << " " << k << " " << u << " " << L.units[u].def << " " << L.units[u].last << " "
+             << rs[k].bytes << "\n";
+        }
+      };
+      for (auto& p : fn->params) line(p.get());
+      for (auto& b : ir::flatten(*fn).lets) line(b.var.get());
+    } else if (w == "curve") {
+      MemProfile mp = peak_memory(*fn, {}, tr);
+      os << "peak " << mp.peak << " " << mp.peak_index << "\n";
+      for (size_t i = 0; i < mp.curve.size(); ++i) os << i << " " << mp.curve[i] << "\n";
+    } else if (w == "schedule") {
+      LetSeq sq = schedule(*fn, {}, tr);
+      FunctionPtr f2 = ir::make_fn(fn->name, fn->params, sq);
+      os << "peak_before " << peak_memory(*fn, {}, tr).peak << "\n";
+      os << "peak_after " << peak_memory(*f2, {}, tr).peak << "\n";
+      os << "order";
+      for (auto& b : sq.lets) os << " " << b.var->id;
+      os << "\n" << print_text_ext(*f2);
+    } else if (w == "remat") {
+      auto [f2, plan] = rematerialize(*fn, budget, {}, tr);
+      os << "replays " << plan.replays << "\npeak_before " << plan.peak_before << "\npeak_after "
+         << plan.peak_after << "\n";
+      for (auto& sp : plan.splits)
+        os << "split " << sp.victim << " " << sp.evict_index << " " << sp.replay_before << "\n";
+      os << print_text_ext(*f2);
+    } else {
+      throw Error("tb_memsched_text: unknown query '" + w + "'");
+    }
+    g_text = os.str();
     return g_text.c_str();
   } catch (const std::exception& e) {
     g_err = e.what();

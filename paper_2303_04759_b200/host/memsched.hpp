@@ -33,6 +33,7 @@ struct Unit {
   int64_t sub_off = 0;
   int param = -1;         // >= 0: a function parameter (persistent state / input)
   int producer = -1;      // let index that writes it (-1 for params)
+  bool pinned = true;     // params: live over the whole function
 };
 
 struct Ref {
@@ -57,6 +58,13 @@ struct Layout {
   }
 };
 
+/// the returned expressions of a let sequence: a tuple's fields or one var
+inline std::vector<ExprPtr> ret_exprs(const LetSeq& seq) {
+  if (!seq.ret) return {};
+  if (seq.ret->kind == ExprKind::Tuple) return seq.ret->args;
+  return {seq.ret};
+}
+
 inline bool inplace_safe(const std::string& base, int in_idx, int out_idx) {
   if (base == "adam_update" || base == "adam_update_ex")
     return (out_idx == 0 && in_idx == 0) || (out_idx == 1 && in_idx == 2) || (out_idx == 2 && in_idx == 3);
@@ -69,8 +77,14 @@ inline bool inplace_safe(const std::string& base, int in_idx, int out_idx) {
 
 /// state_binding: (ret index, param index) pairs; params listed are written in
 /// place when liveness allows (otherwise the VM copies back after the step).
+///
+/// transient_inputs: the accounting of SPEC.md's memsched EXAMPLES (:454-458,
+/// "predecessor freed after each step"), where a function input that is not
+/// bound state occupies memory only until its last use; the default is the
+/// invariant of SPEC.md:431 ("params ... live over the whole function"), which
+/// is also what the device VM does (inputs are persistent buffers).
 inline Layout build_layout(const ir::FunctionIR& fn, const std::vector<std::pair<int, int>>& state_binding,
-                           bool elide_concat = true) {
+                           bool elide_concat = true, bool transient_inputs = false) {
   Layout L;
   auto seq = ir::flatten(fn);
   L.n = int(seq.lets.size());
@@ -265,10 +279,9 @@ inline Layout build_layout(const ir::FunctionIR& fn, const std::vector<std::pair
     for (auto& a : seq.lets[i].value->args)
       if (a->kind == ExprKind::VarRef)
         for (auto& r : L.refs.at(a->var.get())) L.units[r.unit].last = std::max(L.units[r.unit].last, i);
-  if (seq.ret)
-    for (auto& a : seq.ret->args)
-      if (a->kind == ExprKind::VarRef)
-        for (auto& r : L.refs.at(a->var.get())) L.units[r.unit].last = L.n;
+  for (auto& a : ret_exprs(seq))
+    if (a->kind == ExprKind::VarRef)
+      for (auto& r : L.refs.at(a->var.get())) L.units[r.unit].last = L.n;
   // concat children: the parent covers them
   for (size_t u = 0; u < L.units.size(); ++u) {
     if (L.units[u].parent < 0) continue;
@@ -276,6 +289,28 @@ inline Layout build_layout(const ir::FunctionIR& fn, const std::vector<std::pair
     (void)off;
     L.units[root].def = std::min(L.units[root].def, L.units[u].def);
     L.units[root].last = std::max(L.units[root].last, L.units[u].last);
+  }
+  if (transient_inputs) {
+    std::set<int> bound;
+    for (auto& [rj, pi] : state_binding) bound.insert(pi);
+    std::vector<int> lastp(L.units.size(), -1);
+    for (int i = 0; i < L.n; ++i)
+      for (auto& a : seq.lets[i].value->args)
+        if (a->kind == ExprKind::VarRef)
+          for (auto& r : L.refs.at(a->var.get())) {
+            int ru = L.root(r.unit).first;
+            lastp[ru] = std::max(lastp[ru], i);
+          }
+    for (auto& a : ret_exprs(seq))
+      if (a->kind == ExprKind::VarRef)
+        for (auto& r : L.refs.at(a->var.get())) lastp[L.root(r.unit).first] = L.n;
+    for (size_t u = 0; u < L.units.size(); ++u) {
+      Unit& x = L.units[u];
+      if (x.param < 0 || bound.count(x.param)) continue;
+      x.pinned = false;
+      x.def = 0;
+      x.last = std::max(lastp[u], 0);
+    }
   }
   return L;
 }
@@ -296,7 +331,7 @@ inline MemProfile peak_memory(const Layout& L) {
   for (size_t u = 0; u < L.units.size(); ++u) {
     const Unit& x = L.units[u];
     if (x.parent >= 0) continue;
-    if (x.param >= 0) {
+    if (x.param >= 0 && x.pinned) {
       m.state_bytes += x.bytes;
       for (auto& c : m.curve) c += x.bytes;
       continue;
@@ -311,8 +346,9 @@ inline MemProfile peak_memory(const Layout& L) {
   return m;
 }
 
-inline MemProfile peak_memory(const ir::FunctionIR& fn, const std::vector<std::pair<int, int>>& sb = {}) {
-  return peak_memory(build_layout(fn, sb));
+inline MemProfile peak_memory(const ir::FunctionIR& fn, const std::vector<std::pair<int, int>>& sb = {},
+                             bool transient_inputs = false) {
+  return peak_memory(build_layout(fn, sb, true, transient_inputs));
 }
 
 // ----------------------------------------------------------- arena plan
@@ -423,8 +459,9 @@ inline double op_cost(const ir::ExprPtr& call) {
 // ------------------------------------------------------------------ schedule
 /// p - c greedy list scheduling: among ready lets pick the
 /// one with minimum (bytes produced - bytes freed), ties by original order.
-inline LetSeq schedule(const ir::FunctionIR& fn, const std::vector<std::pair<int, int>>& sb = {}) {
-  Layout L = build_layout(fn, sb);
+inline LetSeq schedule(const ir::FunctionIR& fn, const std::vector<std::pair<int, int>>& sb = {},
+                       bool transient_inputs = false) {
+  Layout L = build_layout(fn, sb, true, transient_inputs);
   LetSeq seq = ir::flatten(fn);
   const int n = int(seq.lets.size());
   std::unordered_map<const ir::Var*, int> def;
@@ -450,7 +487,7 @@ inline LetSeq schedule(const ir::FunctionIR& fn, const std::vector<std::pair<int
         for (int u : roots_of(a->var.get())) remaining[u]++;
   std::vector<char> pinned(L.units.size(), 0);
   for (size_t u = 0; u < L.units.size(); ++u)
-    if (L.units[u].param >= 0 || L.units[u].last >= n) pinned[u] = 1;
+    if ((L.units[u].param >= 0 && L.units[u].pinned) || L.units[u].last >= n) pinned[u] = 1;
   std::vector<int> indeg(n);
   for (int i = 0; i < n; ++i) indeg[i] = int(deps[i].size());
   std::vector<int> ready;
@@ -524,11 +561,12 @@ inline bool replayable(const ir::ExprPtr& e) {
 /// allows <= 3; deeper chains are not evicted).  Throws BudgetInfeasible when
 /// the floor (state + max single-op working set) exceeds the budget.
 inline std::pair<FunctionPtr, RematPlan> rematerialize(const ir::FunctionIR& fn, int64_t budget,
-                                                        const std::vector<std::pair<int, int>>& sb = {}) {
+                                                        const std::vector<std::pair<int, int>>& sb = {},
+                                                        bool transient_inputs = false) {
   RematPlan plan;
   auto cur = std::make_shared<ir::FunctionIR>(fn);
   for (int iter = 0; iter < 100000; ++iter) {
-    Layout L = build_layout(*cur, sb);
+    Layout L = build_layout(*cur, sb, true, transient_inputs);
     MemProfile mp = peak_memory(L);
     if (iter == 0) plan.peak_before = mp.peak;
     plan.peak_after = mp.peak;
@@ -544,7 +582,7 @@ inline std::pair<FunctionPtr, RematPlan> rematerialize(const ir::FunctionIR& fn,
       if (a->kind == ExprKind::VarRef)
         for (auto& r : L.refs.at(a->var.get())) needed.insert(L.root(r.unit).first);
     for (int u : needed)
-      if (L.units[u].param < 0) floor_i += L.units[u].bytes;
+      if (L.units[u].param < 0 || !L.units[u].pinned) floor_i += L.units[u].bytes;
     // candidates: units live across i, not used at i, produced by a replayable
     // single-output op whose inputs are params or still live at the next use
     std::unordered_map<const ir::Var*, int> def;
@@ -583,7 +621,7 @@ inline std::pair<FunctionPtr, RematPlan> rematerialize(const ir::FunctionIR& fn,
         bool dead = false;
         for (auto& r : L.refs.at(a->var.get())) {
           const Unit& iu = L.units[L.root(r.unit).first];
-          if (iu.param < 0 && iu.last < next) dead = true;
+          if ((iu.param < 0 || !iu.pinned) && iu.last < next) dead = true;
         }
         if (!dead) continue;
         auto dit = def.find(a->var.get());
@@ -600,7 +638,7 @@ inline std::pair<FunctionPtr, RematPlan> rematerialize(const ir::FunctionIR& fn,
           if (a2->kind != ExprKind::VarRef) continue;
           for (auto& r2 : L.refs.at(a2->var.get())) {
             const Unit& iu2 = L.units[L.root(r2.unit).first];
-            if (iu2.param < 0 && iu2.last < next) ok = false;
+            if ((iu2.param < 0 || !iu2.pinned) && iu2.last < next) ok = false;
           }
         }
         if (ok) {

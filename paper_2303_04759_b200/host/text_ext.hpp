@@ -50,6 +50,30 @@ inline std::string print_text_ext(const ir::FunctionIR& fn) {
   return head + body;
 }
 
+/// The reference parser creates a fresh Var object per `%id` occurrence; the
+/// passes here (memsched, the VM) identify values by Var pointer, so every
+/// reference is relinked to its definition (param or let) by id.
+inline void relink_vars(ir::FunctionIR& fn) {
+  std::unordered_map<std::string, VarPtr> def;
+  for (auto& p : fn.params) def[p->id] = p;
+  auto seq = ir::flatten(fn);
+  std::function<void(const ExprPtr&)> fix = [&](const ExprPtr& e) {
+    if (!e) return;
+    if (e->kind == ExprKind::VarRef) {
+      auto it = def.find(e->var->id);
+      if (it == def.end()) throw Error("text: %" + e->var->id + " used before its definition");
+      e->var = it->second;
+      return;
+    }
+    for (auto& a : e->args) fix(a);
+  };
+  for (auto& b : seq.lets) {
+    fix(b.value);
+    def[b.var->id] = b.var;
+  }
+  fix(seq.ret);
+}
+
 inline ir::ModuleIR parse_text_ext(const std::string& src) {
   std::map<std::string, DType> ext;  // param id -> dtype outside the reference format
   static const std::regex tok(R"(%([A-Za-z0-9_.]+): (bf16|i32)\[)");
@@ -71,6 +95,7 @@ inline ir::ModuleIR parse_text_ext(const std::string& src) {
       t.dtype = e->second;
       p->ty = Type(t);
     }
+    relink_vars(*fn);
     ir::infer_types(*fn);
   }
   return mod;

@@ -73,6 +73,8 @@ def lib():
         L.tb_tnsr_load.argtypes = [ctypes.c_char_p, ctypes.c_void_p, ctypes.c_int64]
         L.tb_session_save_param.argtypes = [ctypes.c_void_p, ctypes.c_char_p, ctypes.c_char_p]
         L.tb_session_load_param.argtypes = [ctypes.c_void_p, ctypes.c_char_p, ctypes.c_char_p]
+        L.tb_memsched_text.restype = ctypes.c_char_p
+        L.tb_memsched_text.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_int64, ctypes.c_int]
         _lib = L
     return _lib
 
@@ -162,6 +164,7 @@ def plan_fits(cfg: ModelConfig, budget: int, remat: bool) -> tuple[bool, dict]:
     (no evictable tensor) does not fit."""
     c = ModelConfig(**{f.name: getattr(cfg, f.name) for f in fields(cfg) if f.name != "extra"})
     c.extra = dict(cfg.extra)
+    c.extra.setdefault("schedule", 1)  # p-c list schedule before remat (SPEC.md:459-466)
     if remat:
         # the remat pass bounds the liveness peak; address packing of the arena
         # adds fragmentation on top, so it aims 1.5% below the budget
@@ -231,6 +234,14 @@ def graph_segments(cfg: ModelConfig) -> list[tuple[str, int, int]]:
         n, o, k = line.split()
         out.append((n, int(o), int(k)))
     return out
+
+
+def memsched_text(text: str, what: str, budget: int = 0, transient_inputs: bool = False) -> str:
+    """CPU-only memsched queries on a text-IR function (tb_memsched_text)."""
+    t = lib().tb_memsched_text(text.encode(), what.encode(), budget, int(transient_inputs))
+    if t is None:
+        raise RuntimeError(lib().tb_last_error().decode())
+    return t.decode()
 
 
 class Session:

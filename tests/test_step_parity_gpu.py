@@ -159,3 +159,29 @@ def test_fusion_launches_strictly_fewer_kernels():
     k1, l1 = run(1)
     assert k1 < k0, (k0, k1)
     assert abs(l0 - l1) <= 2e-2, (l0, l1)
+
+
+def test_scheduled_step_bit_identical():
+    """The p-c list schedule (session key schedule=1, used by
+    the max-batch search) only reorders independent lets: losses and
+    parameters bit-identical to the written order on the device."""
+    cfg = ModelConfig.tiny(dtype="bf16", opt="adam", lr=1e-3, L=2, p=0.1)
+    cfg_s = ModelConfig.tiny(dtype="bf16", opt="adam", lr=1e-3, L=2, p=0.1)
+    cfg_s.extra["schedule"] = 1
+
+    def run(c):
+        s = Session(c)
+        s.init_params()
+        losses = []
+        for k in range(2):
+            ids, labels = synthetic_batch(c, seed=c.seed_d + k)
+            s.set_batch(ids, labels)
+            s.step(graph=True)
+            losses.append(s.loss())
+        out = np.array(losses), s.read("params")
+        s.close()
+        return out
+
+    l0, p0 = run(cfg)
+    l1, p1 = run(cfg_s)
+    assert np.array_equal(l0, l1) and np.array_equal(p0, p1)
