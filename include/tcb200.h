@@ -84,6 +84,15 @@ int tcb_plan_create(const char* dialect_op, const tcb_tensor* in, int nin,
 int tcb_launch(tcb_plan plan, const tcb_tensor* in, int nin, tcb_tensor* out, int nout,
                void* stream);
 
+/* Launch with a caller-owned device WORKSPACE (>= tcb_plan_workspace_bytes).
+ * Plans own no mutable device memory: every launch context (a VM, a rank
+ * thread) passes its own workspace, so a plan shared through the process-wide
+ * KernelCache is safe under concurrent launches on different streams.  Plain
+ * tcb_launch uses a plan-owned fallback workspace (allocated on first use;
+ * not for concurrent or captured use). */
+int tcb_launch_ws(tcb_plan plan, const tcb_tensor* in, int nin, tcb_tensor* out, int nout, void* ws,
+                  uint64_t ws_bytes, void* stream);
+int tcb_plan_workspace_bytes(tcb_plan plan, uint64_t* bytes);
 void tcb_plan_destroy(tcb_plan plan);
 
 /* Deferred partial-sum folds (backend-internal scheduling; no reference
@@ -95,6 +104,12 @@ void tcb_plan_destroy(tcb_plan plan);
  * tcb_fold_defer must be called outside stream capture. */
 int tcb_fold_defer(int on, uint64_t pool_bytes);
 int tcb_fold_flush(void* stream);
+/* Per-launch-context fold pools: a VM creates one context (its partial-sum
+ * slots live and die with it) and activates it on its thread before enqueueing
+ * a step (tcb_fold_use(NULL) turns deferral off). */
+int tcb_fold_ctx_create(uint64_t pool_bytes, void** ctx);
+void tcb_fold_ctx_destroy(void* ctx);
+int tcb_fold_use(void* ctx);
 /* Cumulative counts: op launches whose fold kernel was deferred, and fold
  * kernels the flushes launched (kernels-per-step accounting). */
 int tcb_fold_counters(uint64_t* ops_deferred, uint64_t* flush_launches);

@@ -54,7 +54,18 @@ static std::string spec_str(const Spec& s) {
 
 struct tcb_plan_ {
   tcb::Plan p;
+  // fallback workspace for callers of plain tcb_launch (tests, one-off ops):
+  // allocated on first such launch (never during capture), serialised by mu
+  std::mutex mu;
+  std::unique_ptr<tcb::Scratch> own_ws;
 };
+
+namespace tcb {
+char*& launch_ws() {
+  thread_local char* w = nullptr;
+  return w;
+}
+}  // namespace tcb
 
 using namespace tcb;
 
@@ -154,26 +165,69 @@ static bool skipped_op(const std::string& op) {
   return !list.empty() && list.find("," + op + ",") != std::string::npos;
 }
 
+static void launch_with(tcb_plan plan, const tcb_tensor* in, int nin, tcb_tensor* out, int nout, void* ws,
+                        uint64_t ws_bytes, void* stream) {
+  if (!plan) fail(TCB_ERR_ARG, "null plan");
+  Plan& p = plan->p;
+  if (nin != int(p.in.size()) || nout != int(p.out.size()))
+    fail(TCB_ERR_ARG, "b200." + p.op + ": launch arity differs from plan");
+  if (p.ws_bytes && ws && ws_bytes < p.ws_bytes)
+    fail(TCB_ERR_ARG, "b200." + p.op + ": workspace of " + std::to_string(ws_bytes) + " B < the plan's " +
+                          std::to_string(p.ws_bytes) + " B");
+  if (skipped_op(p.op)) return;
+  // a deferred fold whose output this launch reads is folded first
+  for (int i = 0; i < nin; ++i)
+    fold_flush_if_reads(in[i].ptr, size_t(p.in[i].numel()) * dtype_bytes(p.in[i].dtype),
+                        static_cast<cudaStream_t>(stream));
+  struct Reset {
+    ~Reset() { launch_ws() = nullptr; }
+  } reset;
+  launch_ws() = static_cast<char*>(ws);
+  p.run(in, out, static_cast<cudaStream_t>(stream));
+  TCB_CUDA(cudaGetLastError());
+}
+
+int tcb_launch_ws(tcb_plan plan, const tcb_tensor* in, int nin, tcb_tensor* out, int nout, void* ws,
+                  uint64_t ws_bytes, void* stream) {
+  TCB_TRY({
+    if (plan && plan->p.ws_bytes && !ws) fail(TCB_ERR_ARG, "b200." + plan->p.op + ": needs a workspace");
+    launch_with(plan, in, nin, out, nout, ws, ws_bytes, stream);
+  });
+}
+
 int tcb_launch(tcb_plan plan, const tcb_tensor* in, int nin, tcb_tensor* out, int nout,
                void* stream) {
   TCB_TRY({
     if (!plan) fail(TCB_ERR_ARG, "null plan");
-    Plan& p = plan->p;
-    if (nin != int(p.in.size()) || nout != int(p.out.size()))
-      fail(TCB_ERR_ARG, "b200." + p.op + ": launch arity differs from plan");
-    if (skipped_op(p.op)) return TCB_OK;
-    // a deferred fold whose output this launch reads is folded first
-    for (int i = 0; i < nin; ++i)
-      fold_flush_if_reads(in[i].ptr, size_t(p.in[i].numel()) * dtype_bytes(p.in[i].dtype),
-                          static_cast<cudaStream_t>(stream));
-    p.run(in, out, static_cast<cudaStream_t>(stream));
-    TCB_CUDA(cudaGetLastError());
+    void* ws = nullptr;
+    if (plan->p.ws_bytes) {
+      std::lock_guard<std::mutex> g(plan->mu);
+      if (!plan->own_ws) plan->own_ws = std::make_unique<Scratch>(plan->p.ws_bytes);
+      ws = plan->own_ws->p;
+    }
+    launch_with(plan, in, nin, out, nout, ws, plan->p.ws_bytes, stream);
+  });
+}
+
+int tcb_plan_workspace_bytes(tcb_plan plan, uint64_t* bytes) {
+  TCB_TRY({
+    if (!plan || !bytes) fail(TCB_ERR_ARG, "tcb_plan_workspace_bytes: null argument");
+    *bytes = plan->p.ws_bytes;
   });
 }
 
 void tcb_plan_destroy(tcb_plan plan) { delete plan; }
 
 int tcb_fold_defer(int on, uint64_t pool_bytes) { TCB_TRY(fold_set(on != 0, size_t(pool_bytes))); }
+
+int tcb_fold_ctx_create(uint64_t pool_bytes, void** ctx) {
+  TCB_TRY({
+    if (!ctx) fail(TCB_ERR_ARG, "tcb_fold_ctx_create: null output");
+    *ctx = fold_ctx_create(size_t(pool_bytes));
+  });
+}
+void tcb_fold_ctx_destroy(void* ctx) { fold_ctx_destroy(static_cast<FoldCtx*>(ctx)); }
+int tcb_fold_use(void* ctx) { TCB_TRY(fold_use(static_cast<FoldCtx*>(ctx))); }
 
 int tcb_fold_flush(void* stream) { TCB_TRY(fold_flush(static_cast<cudaStream_t>(stream))); }
 

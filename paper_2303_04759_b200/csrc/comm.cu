@@ -128,6 +128,23 @@ int tcb_comm_destroy(void* comm) {
   });
 }
 
+// NCCL moves one flat buffer per call: the segments of a bucket must be
+// contiguous in memory and cover exactly world * shard elements (the zero pad
+// materialised), or the call would read / write past them
+static void check_bucket(const tcb_tensor* segs, int nseg, int64_t want, const char* what) {
+  int64_t total = 0;
+  const char* next = static_cast<const char*>(segs[0].ptr);
+  for (int i = 0; i < nseg; ++i) {
+    require(segs[i].dtype == segs[0].dtype, std::string(what) + ": segments of one bucket share a dtype");
+    require(static_cast<const char*>(segs[i].ptr) == next, std::string(what) + ": bucket segments are not contiguous");
+    const int64_t n = numel_of(segs[i]);
+    next += n * dtype_bytes(segs[i].dtype);
+    total += n;
+  }
+  require(total == want, std::string(what) + ": bucket has " + std::to_string(total) + " elements, world x shard = " +
+                             std::to_string(want));
+}
+
 int tcb_reduce_scatter(void* comm, const tcb_tensor* segs, int nseg, tcb_tensor* shard, void* stream) {
   TCB_TRY_C({
     require(nseg >= 1, "reduce_scatter: no segments");
@@ -138,6 +155,8 @@ int tcb_reduce_scatter(void* comm, const tcb_tensor* segs, int nseg, tcb_tensor*
       const int es = dtype_bytes(shard->dtype);
       for (int i = 0; i < nseg; ++i) {
         const int64_t n = numel_of(segs[i]);
+        require(off + n <= shard_n, "reduce_scatter: segments exceed the shard (a world > 1 step without a "
+                                    "communicator?)");
         TCB_CUDA(cudaMemcpyAsync(static_cast<char*>(shard->ptr) + off * es, segs[i].ptr, n * es,
                                  cudaMemcpyDeviceToDevice, s));
         off += n;
@@ -147,6 +166,9 @@ int tcb_reduce_scatter(void* comm, const tcb_tensor* segs, int nseg, tcb_tensor*
       return TCB_OK;
     }
     ncclComm_t c = static_cast<ncclComm_t>(comm);
+    int world = 0;
+    TCB_NCCL(nccl().commCount(c, &world));
+    check_bucket(segs, nseg, shard_n * world, "reduce_scatter");
     TCB_NCCL(nccl().groupStart());
     TCB_NCCL(nccl().reduceScatter(segs[0].ptr, shard->ptr, size_t(shard_n), nccl_dtype(shard->dtype), ncclSum,
                                   c, s));
@@ -164,6 +186,8 @@ int tcb_all_gather(void* comm, const tcb_tensor* shard, tcb_tensor* segs, int ns
       const int es = dtype_bytes(shard->dtype);
       for (int i = 0; i < nseg; ++i) {
         const int64_t n = numel_of(segs[i]);
+        require(off + n <= shard_n, "all_gather: segments exceed the shard (a world > 1 step without a "
+                                    "communicator?)");
         TCB_CUDA(cudaMemcpyAsync(segs[i].ptr, static_cast<const char*>(shard->ptr) + off * es, n * es,
                                  cudaMemcpyDeviceToDevice, s));
         off += n;
@@ -171,6 +195,9 @@ int tcb_all_gather(void* comm, const tcb_tensor* shard, tcb_tensor* segs, int ns
       return TCB_OK;
     }
     ncclComm_t c = static_cast<ncclComm_t>(comm);
+    int world = 0;
+    TCB_NCCL(nccl().commCount(c, &world));
+    check_bucket(segs, nseg, shard_n * world, "all_gather");
     TCB_NCCL(nccl().groupStart());
     TCB_NCCL(nccl().allGather(shard->ptr, segs[0].ptr, size_t(shard_n), nccl_dtype(shard->dtype), c, s));
     TCB_NCCL(nccl().groupEnd());

@@ -318,8 +318,8 @@ void dispatch_float(int dtype, Fn&& f) {
   fail(TCB_ERR_TYPE, std::string("unsupported dtype ") + dtype_name(dtype));
 }
 
-// Plan-owned device scratch (allocated once at plan creation, freed with the
-// plan).  Launches of one plan are stream-ordered, so reuse is race-free.
+// Device allocation owned by a plan: only for READ-ONLY plan data (schedule
+// tables) -- mutable scratch comes from the launch workspace (Plan::ws_take).
 struct Scratch {
   void* p = nullptr;
   explicit Scratch(size_t bytes) { TCB_CUDA(cudaMalloc(&p, bytes ? bytes : 16)); }
@@ -388,7 +388,26 @@ struct Plan {
   Attrs attrs;
   RunFn run;
   int nkernels = 1;
+  // Mutable device scratch is NOT owned by the plan (plans are shared through
+  // the process-wide KernelCache by VMs that may run concurrently): a builder
+  // reserves a byte range of the per-launch WORKSPACE with ws_take() and the
+  // run function addresses it with ws_at(offset).  The caller of the launch
+  // (a VM) supplies one workspace for its whole stream (tcb_launch_ws).
+  size_t ws_bytes = 0;
+  size_t ws_take(size_t bytes) {
+    const size_t off = (ws_bytes + 255) & ~size_t(255);
+    ws_bytes = off + ((bytes + 255) & ~size_t(255));
+    return off;
+  }
 };
+
+// the workspace of the launch in progress on this thread (set by tcb_launch_ws)
+char*& launch_ws();
+inline void* ws_at(size_t off) {
+  char* b = launch_ws();
+  if (!b) fail(TCB_ERR_ARG, "launch without a workspace for a plan that needs one");
+  return b + off;
+}
 
 using Builder = void (*)(Plan&);
 void register_builder(const char* op, Builder b);

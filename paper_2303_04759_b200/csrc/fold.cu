@@ -7,17 +7,25 @@
 
 namespace tcb {
 
+// A pool of per-op-instance partial buffers.  One context per launch context
+// (the device VM owns one; its slots die with it), so sessions never share
+// slots and a later session cannot be handed a smaller slot of an earlier one.
+struct FoldCtx {
+  std::unique_ptr<Scratch> pool;
+  size_t pool_bytes = 0, used = 0;
+  std::map<std::pair<const void*, int>, std::pair<size_t, size_t>> slots;  // (key, tag) -> (offset, bytes)
+};
+
 namespace {
 struct FoldState {
   bool on = false;
-  std::unique_ptr<Scratch> pool;
-  size_t pool_bytes = 0, used = 0;
-  std::map<std::pair<const void*, int>, size_t> slots;  // (key, tag) -> pool offset
+  FoldCtx* ctx = nullptr;  // active context (a VM's, or `own` for tcb_fold_defer)
+  FoldCtx own;
   std::vector<FoldJob> jobs;
   uint64_t ops_deferred = 0, flush_launches = 0;  // cumulative (launch accounting)
 };
 // per thread: one VM (rank) per thread may run concurrently,
-// each with its own queue and pool on its own device
+// each with its own queue and context on its own device
 FoldState& st() {
   thread_local FoldState s;
   return s;
@@ -28,15 +36,40 @@ bool fold_deferring() { return st().on; }
 
 float* fold_scratch(const void* key, int tag, size_t bytes) {
   FoldState& s = st();
-  if (!s.on || !s.pool) return nullptr;
+  if (!s.on || !s.ctx || !s.ctx->pool) return nullptr;
+  FoldCtx& c = *s.ctx;
   bytes = (bytes + 255) & ~size_t(255);
-  auto it = s.slots.find({key, tag});
-  if (it != s.slots.end()) return reinterpret_cast<float*>(static_cast<char*>(s.pool->p) + it->second);
-  if (s.used + bytes > s.pool_bytes) return nullptr;  // pool exhausted: the op folds in place
-  s.slots[{key, tag}] = s.used;
-  float* p = reinterpret_cast<float*>(static_cast<char*>(s.pool->p) + s.used);
-  s.used += bytes;
+  auto it = c.slots.find({key, tag});
+  if (it != c.slots.end() && it->second.second >= bytes)
+    return reinterpret_cast<float*>(static_cast<char*>(c.pool->p) + it->second.first);
+  // new key, or a larger request than the slot holds: carve a fresh region
+  if (c.used + bytes > c.pool_bytes) return nullptr;  // pool exhausted: the op folds in place
+  c.slots[{key, tag}] = {c.used, bytes};
+  float* p = reinterpret_cast<float*>(static_cast<char*>(c.pool->p) + c.used);
+  c.used += bytes;
   return p;
+}
+
+FoldCtx* fold_ctx_create(size_t pool_bytes) {
+  auto* c = new FoldCtx;
+  if (pool_bytes) {
+    c->pool = std::make_unique<Scratch>(pool_bytes);
+    c->pool_bytes = pool_bytes;
+  }
+  return c;
+}
+void fold_ctx_destroy(FoldCtx* c) {
+  FoldState& s = st();
+  if (s.ctx == c) {
+    s.ctx = nullptr;
+    s.on = false;
+  }
+  delete c;
+}
+void fold_use(FoldCtx* c) {
+  FoldState& s = st();
+  s.ctx = c;
+  s.on = c && c->pool;
 }
 
 void fold_defer(const FoldJob& j) { st().jobs.push_back(j); }
@@ -161,14 +194,16 @@ void fold_flush_if_reads(const void* ptr, size_t bytes, cudaStream_t s) {
 
 void fold_set(bool on, size_t pool_bytes) {
   FoldState& s = st();
-  if (on && pool_bytes && (!s.pool || s.pool_bytes < pool_bytes)) {
-    s.pool.reset();
-    s.slots.clear();
-    s.used = 0;
-    s.pool = std::make_unique<Scratch>(pool_bytes);
-    s.pool_bytes = pool_bytes;
+  FoldCtx& c = s.own;
+  if (on && pool_bytes && (!c.pool || c.pool_bytes < pool_bytes)) {
+    c.pool.reset();
+    c.slots.clear();
+    c.used = 0;
+    c.pool = std::make_unique<Scratch>(pool_bytes);
+    c.pool_bytes = pool_bytes;
   }
-  s.on = on && s.pool != nullptr;
+  s.ctx = &c;
+  s.on = on && c.pool != nullptr;
 }
 
 }  // namespace tcb

@@ -26,6 +26,10 @@ struct FoldJob {
   float scale;
 };
 
+struct FoldCtx;
+FoldCtx* fold_ctx_create(size_t pool_bytes);  // outside stream capture
+void fold_ctx_destroy(FoldCtx* c);
+void fold_use(FoldCtx* c);  // this thread's deferral uses c (nullptr: off)
 bool fold_deferring();
 // deferral on/off; on allocates (once, eagerly) a pool of pool_bytes for the
 // per-instance partial buffers.  Must be called outside stream capture.

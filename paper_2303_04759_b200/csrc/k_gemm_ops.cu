@@ -137,18 +137,17 @@ static void b_linear_chain(Plan& p) {
   require(what == "preact" || what == "grad", "linear_chain: save must be preact or grad");
   g0.save_grad = (save && what == "grad") ? 1 : 0;
   const bool exact = want_exact(p) || p.in[0].dtype != TCB_BF16;
-  std::shared_ptr<Scratch> sched, counters;
+  std::shared_ptr<Scratch> sched;  // read-only schedule table
+  size_t counters = 0;             // row-block counters (workspace)
   const int64_t mbl = (g0.M + 255) / 256 + 1;
   if (!exact) {
     int rounds = 0;
     std::vector<int> table = gemm_chain_schedule(g0, g1, &rounds);
     sched = std::make_shared<Scratch>(table.size() * sizeof(int));
     TCB_CUDA(cudaMemcpy(sched->p, table.data(), table.size() * sizeof(int), cudaMemcpyHostToDevice));
-    counters = std::make_shared<Scratch>(size_t(mbl) * sizeof(int));
+    counters = p.ws_take(size_t(mbl) * sizeof(int));
     g0.sched = static_cast<const int*>(sched->p);
     g0.sched_rounds = rounds;
-    g0.dep_signal = static_cast<int*>(counters->p);
-    g1.dep_wait = static_cast<const int*>(counters->p);
     g1.dep_need = gemm_chain_need(g0, g1);
   }
   p.nkernels = exact ? 2 : 1;  // the chained GEMM (its counter reset is a memset node), or two linears
@@ -169,7 +168,9 @@ static void b_linear_chain(Plan& p) {
     g1.bias = in[4].ptr;
     g1.c = out[save ? 2 : 1].ptr;
     if (!exact && gemm_tc_supported(g0, nullptr) && gemm_tc_supported(g1, nullptr)) {
-      TCB_CUDA(cudaMemsetAsync(counters->p, 0, size_t(mbl) * sizeof(int), s));
+      g0.dep_signal = static_cast<int*>(ws_at(counters));
+      g1.dep_wait = static_cast<const int*>(ws_at(counters));
+      TCB_CUDA(cudaMemsetAsync(ws_at(counters), 0, size_t(mbl) * sizeof(int), s));
       launch_gemm_tc_chain(g0, g1, s);
     } else {
       g0.dep_signal = nullptr;
@@ -223,7 +224,8 @@ static void b_matmul_pair(Plan& p) {
   g0.force_cg = g1.force_cg = int(p.attrs.i("tc_cg", 0));
   const bool exact = want_exact(p) || p.in[n0].dtype != TCB_BF16;
   p.nkernels = exact ? 2 : 1;
-  std::shared_ptr<Scratch> sched, wsbuf;
+  std::shared_ptr<Scratch> sched;  // read-only schedule table
+  size_t wsbuf = 0;                // K-slice partials (workspace)
   int ws_idx = -1, ws_s = 1;
   if (!exact && !p.attrs.i("static_rr", 0)) {
     // a weight gradient with few long tiles is cut along K into slices
@@ -240,7 +242,7 @@ static void b_matmul_pair(Plan& p) {
     if (ws_s > 1) {
       GemmArgs& g = ws_idx ? g1 : g0;
       g.wsplit = ws_s;
-      wsbuf = std::make_shared<Scratch>(size_t(ws_s) * size_t(g.M) * size_t(g.N) * sizeof(float));
+      wsbuf = p.ws_take(size_t(ws_s) * size_t(g.M) * size_t(g.N) * sizeof(float));
       p.nkernels = 2;
     }
     int rounds = 0;
@@ -260,11 +262,11 @@ static void b_matmul_pair(Plan& p) {
     g1.b.ptr = in[n0 + 1].ptr;
     g1.c = out[1].ptr;
     if (!exact && gemm_tc_supported(g0, nullptr) && gemm_tc_supported(g1, nullptr)) {
-      if (ws_s > 1) (ws_idx ? g1 : g0).c = wsbuf->p;
+      if (ws_s > 1) (ws_idx ? g1 : g0).c = ws_at(wsbuf);
       launch_gemm_tc_pair(g0, g1, s);
       if (ws_s > 1) {
         const GemmArgs& g = ws_idx ? g1 : g0;
-        launch_wsplit_reduce(static_cast<const float*>(wsbuf->p), static_cast<float*>(out[ws_idx].ptr), g.M * g.N,
+        launch_wsplit_reduce(static_cast<const float*>(ws_at(wsbuf)), static_cast<float*>(out[ws_idx].ptr), g.M * g.N,
                              ws_s, s);
       }
     } else {

@@ -340,13 +340,13 @@ static void b_colsum(Plan& p) {
         rpc = std::max<int64_t>(CS_ROWS, (((R + want - 1) / want) + 7) / 8 * 8);
       }
       const int64_t nchunk = (R + rpc - 1) / rpc;
-      auto ws = std::make_shared<Scratch>(size_t(nchunk) * C * 4);
+      const size_t ws = p.ws_take(size_t(nchunk) * C * 4);
       p.nkernels = 2;
       p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
         if (reinterpret_cast<uintptr_t>(in[0].ptr) % 16) fail(TCB_ERR_ARG, "colsum: input not 16-byte aligned");
         const dim3 grid{unsigned(cblocks), unsigned(nchunk)};
         float* dws = fold_deferring() ? fold_scratch(out[0].ptr, 0, size_t(nchunk) * C * 4) : nullptr;
-        float* wsp = dws ? dws : (float*)ws->p;
+        float* wsp = dws ? dws : (float*)ws_at(ws);
         if (masked)
           launch_k(k_colsum_partial_masked<T>, grid, 256, 0, s, (const T*)in[0].ptr, wsp, R, C, rpc,
                    (const int32_t*)in[1].ptr, ign);
@@ -358,7 +358,7 @@ static void b_colsum(Plan& p) {
           fold_op_deferred();
           return;
         }
-        if (!skip_folds()) launch_k(k_colsum_final, unsigned((C + 31) / 32), 1024, 0, s, (const float*)ws->p, (float*)out[0].ptr, nchunk, C,
+        if (!skip_folds()) launch_k(k_colsum_final, unsigned((C + 31) / 32), 1024, 0, s, (const float*)ws_at(ws), (float*)out[0].ptr, nchunk, C,
                                                                   1.0f);
       };
     } else {

@@ -816,7 +816,7 @@ static void b_layer_norm_dx(Plan& p) {
   if (bias) require(p.out[di].dtype == TCB_F32 && p.out[di].numel() == H, "layer_norm_dx: dbias is f32 [H]");
   const int np = bias ? 3 : 2;
   const int nblk = int((rows + LNB_ROWS - 1) / LNB_ROWS);
-  auto ws = std::make_shared<Scratch>(size_t(nblk) * np * H * sizeof(float));
+  const size_t ws = p.ws_take(size_t(nblk) * np * H * sizeof(float));
   const int ncs = (H + 255) / 256;
   const size_t smem = size_t(8) * 3 * 8 * 32 * ncs * sizeof(float) + size_t(H) * sizeof(float);  // partials + gamma
   p.nkernels = 2;
@@ -851,7 +851,7 @@ static void b_layer_norm_dx(Plan& p) {
       if constexpr (sizeof(T) == 2) fast = vec && reinterpret_cast<uintptr_t>(in[1].ptr) % 16 == 0;
       // deferred fold: this instance's partials go to its own buffer, folded at the flush
       float* dws = fold_deferring() ? fold_scratch(out[1].ptr, 0, size_t(nblk) * np * H * sizeof(float)) : nullptr;
-      float* wsp = dws ? dws : (float*)ws->p;
+      float* wsp = dws ? dws : (float*)ws_at(ws);
       if (din.p > 0.0f && (!fast || has_res))
         fail(TCB_ERR_UNIMPLEMENTED, "layer_norm_dx: in_p needs the 16-bit path and a single dy");
       if (fast) {
@@ -874,7 +874,7 @@ static void b_layer_norm_dx(Plan& p) {
         fold_op_deferred();
         return;
       }
-      if (!skip_folds()) launch_k(k_ln_colsum, (H + 31) / 32, 1024, 0, s, (const float*)ws->p, (float*)out[1].ptr, (float*)out[2].ptr,
+      if (!skip_folds()) launch_k(k_ln_colsum, (H + 31) / 32, 1024, 0, s, (const float*)ws_at(ws), (float*)out[1].ptr, (float*)out[2].ptr,
                bias ? (float*)out[di].ptr : nullptr, nblk, H);
     };
    });
@@ -1248,8 +1248,8 @@ static void b_attention(Plan& p) {
     return;
   }
   const size_t nsq = size_t(g.Z) * g.S * g.S;
-  auto scores = std::make_shared<Scratch>(nsq * 4);
-  auto pd = std::make_shared<Scratch>(g.d.p > 0.0f ? nsq * dtype_bytes(g.dt) : 0);
+  const size_t scores = p.ws_take(nsq * 4);
+  const size_t pd = p.ws_take(g.d.p > 0.0f ? nsq * dtype_bytes(g.dt) : 0);
   p.nkernels = 3;
   dispatch_float(g.dt, [&](auto* tp) {
     using T = std::remove_pointer_t<decltype(tp)>;
@@ -1257,14 +1257,14 @@ static void b_attention(Plan& p) {
       // 1. scores = scale * Q K^T (f32)
       GemmArgs q = attn_gemm(g, g.S, g.S, g.dh, qkv_view(g, in[0].ptr, 0), 0, qkv_view(g, in[0].ptr, 1), 1);
       q.alpha = g.scale;
-      set_c(q, scores->p, g.S, g.A * g.S * g.S, g.S * g.S, TCB_F32);
+      set_c(q, ws_at(scores), g.S, g.A * g.S * g.S, g.S * g.S, TCB_F32);
       launch_gemm(q, g.exact, s);
       // 2. P = softmax(scores) (+ dropout copy)
       const int64_t rows = g.Z * g.S;
-      T* Pd = g.d.p > 0.0f ? (T*)pd->p : nullptr;
+      T* Pd = g.d.p > 0.0f ? (T*)ws_at(pd) : nullptr;
       dispatch_nq(int(g.S), [&](auto nq) {
         launch_k(k_softmax<float, T, decltype(nq)::value>, sm_grid<decltype(nq)::value>(rows), 256, 0, s, 
-            (const float*)scores->p, (T*)out[1].ptr, Pd, rows, int(g.S), int(g.S), 1.0f, g.causal, g.d,
+            (const float*)ws_at(scores), (T*)out[1].ptr, Pd, rows, int(g.S), int(g.S), 1.0f, g.causal, g.d,
             g.S % 4 == 0 && reinterpret_cast<uintptr_t>(out[1].ptr) % 16 == 0);
       });
       // 3. ctx = Pd V
@@ -1294,9 +1294,9 @@ static void b_attention_dx(Plan& p) {
     return;
   }
   const size_t nsq = size_t(g.Z) * g.S * g.S;
-  auto dpd = std::make_shared<Scratch>(nsq * 4);
-  auto ds = std::make_shared<Scratch>(nsq * dtype_bytes(g.dt));
-  auto pd = std::make_shared<Scratch>(g.d.p > 0.0f ? nsq * dtype_bytes(g.dt) : 0);
+  const size_t dpd = p.ws_take(nsq * 4);
+  const size_t ds = p.ws_take(nsq * dtype_bytes(g.dt));
+  const size_t pd = p.ws_take(g.d.p > 0.0f ? nsq * dtype_bytes(g.dt) : 0);
   p.nkernels = 5;
   dispatch_float(g.dt, [&](auto* tp) {
     using T = std::remove_pointer_t<decltype(tp)>;
@@ -1304,24 +1304,24 @@ static void b_attention_dx(Plan& p) {
       const void* qkv = in[0].ptr;
       // 1. dPd = dctx V^T (f32)
       GemmArgs a = attn_gemm(g, g.S, g.S, g.dh, ctx_view(g, in[2].ptr), 0, qkv_view(g, qkv, 2), 1);
-      set_c(a, dpd->p, g.S, g.A * g.S * g.S, g.S * g.S, TCB_F32);
+      set_c(a, ws_at(dpd), g.S, g.A * g.S * g.S, g.S * g.S, TCB_F32);
       launch_gemm(a, g.exact, s);
       // 2. dS = P (dP - rowdot) * scale ; Pd
       const int64_t rows = g.Z * g.S;
-      T* Pd = g.d.p > 0.0f ? (T*)pd->p : nullptr;
+      T* Pd = g.d.p > 0.0f ? (T*)ws_at(pd) : nullptr;
       dispatch_nq(int(g.S), [&](auto nq) {
         launch_k(k_softmax_bwd<T, float, T, decltype(nq)::value>, sm_grid<decltype(nq)::value>(rows), 256, 0, s, 
-            (const T*)in[1].ptr, (const float*)dpd->p, (T*)ds->p, Pd, rows, int(g.S), g.scale, g.d,
+            (const T*)in[1].ptr, (const float*)ws_at(dpd), (T*)ws_at(ds), Pd, rows, int(g.S), g.scale, g.d,
             g.S % 4 == 0 && reinterpret_cast<uintptr_t>(in[1].ptr) % 16 == 0);
       });
       char* dq = static_cast<char*>(out[0].ptr);
       const size_t part = size_t(g.H) * dtype_bytes(g.dt);
       // 3. dQ = dS K
-      GemmArgs b = attn_gemm(g, g.S, g.dh, g.S, sq_view(g, ds->p, g.dt), 0, qkv_view(g, qkv, 1), 0);
+      GemmArgs b = attn_gemm(g, g.S, g.dh, g.S, sq_view(g, ws_at(ds), g.dt), 0, qkv_view(g, qkv, 1), 0);
       set_c(b, dq, 3 * g.H, g.S * 3 * g.H, g.dh, g.dt);
       launch_gemm(b, g.exact, s);
       // 4. dK = dS^T Q
-      GemmArgs c = attn_gemm(g, g.S, g.dh, g.S, sq_view(g, ds->p, g.dt), 1, qkv_view(g, qkv, 0), 0);
+      GemmArgs c = attn_gemm(g, g.S, g.dh, g.S, sq_view(g, ws_at(ds), g.dt), 1, qkv_view(g, qkv, 0), 0);
       set_c(c, dq + part, 3 * g.H, g.S * 3 * g.H, g.dh, g.dt);
       launch_gemm(c, g.exact, s);
       // 5. dV = Pd^T dctx
@@ -1569,24 +1569,6 @@ __global__ void __launch_bounds__(256) k_embed_accum(const int32_t* __restrict__
   }
 }
 
-static std::shared_ptr<Scratch> emb_part_scratch(size_t bytes) {
-  struct Dev {
-    std::vector<std::shared_ptr<Scratch>> all;  // kept alive: captured graphs may hold old ones
-    size_t cap = 0;
-  };
-  static std::mutex mu;
-  static std::map<int, Dev> per_dev;  // per device (a process may drive several)
-  int dev = 0;
-  TCB_CUDA(cudaGetDevice(&dev));
-  std::lock_guard<std::mutex> g(mu);
-  Dev& d = per_dev[dev];
-  if (d.all.empty() || bytes > d.cap) {
-    d.all.push_back(std::make_shared<Scratch>(bytes));
-    d.cap = bytes;
-  }
-  return d.all.back();
-}
-
 static void b_embedding_dx(Plan& p) {
   check_arity(p, 2, 3, 1, 1);
   require(p.in[0].dtype == TCB_I32, "embedding_dx: ids must be i32");
@@ -1595,11 +1577,9 @@ static void b_embedding_dx(Plan& p) {
   require(p.in[1].numel() == T * H, "embedding_dx: dy must be [T, H]");
   const bool has_base = p.in.size() > 2;
   if (has_base) require(p.in[2].dtype == TCB_F32 && p.in[2].numel() == V * H, "embedding_dx: base is f32 [V,H]");
-  auto sorted = std::make_shared<Scratch>(size_t(T) * 12);  // sorted[T] ++ seg_len[T] ++ seg_head[T]
-  // chunk partials of long segments: one buffer shared by every embedding_dx
-  // plan of the process (they run one after another on the step's stream),
-  // grown at plan creation -- before any graph capture -- and never freed
-  auto part = emb_part_scratch(size_t(T) * H * 4);
+  const size_t sorted = p.ws_take(size_t(T) * 12);  // sorted[T] ++ seg_len[T] ++ seg_head[T]
+  // chunk partials of long segments (launch workspace)
+  const size_t part = p.ws_take(size_t(T) * H * 4);
   p.nkernels = 3;  // rank, accumulate, fold (+ a memset / memcpy node)
   dispatch_float(p.in[1].dtype, [&](auto* tp) {
     using TD = std::remove_pointer_t<decltype(tp)>;
@@ -1610,7 +1590,7 @@ static void b_embedding_dx(Plan& p) {
       } else {
         TCB_CUDA(cudaMemsetAsync(out[0].ptr, 0, nb, s));
       }
-      int32_t* srt = (int32_t*)sorted->p;
+      int32_t* srt = (int32_t*)ws_at(sorted);
       int32_t* seg = srt + T;
       int32_t* hd = seg + T;
       TCB_CUDA(cudaMemsetAsync(seg, 0, size_t(T) * 4, s));
@@ -1621,8 +1601,8 @@ static void b_embedding_dx(Plan& p) {
       const dim3 g2{unsigned(gx), unsigned(ct)};
       launch_k(k_embed_rank, unsigned((T + 7) / 8), 256, 0, s, ids, srt, seg, hd, T);
       launch_k(k_embed_accum<TD>, g2, 256, 0, s, ids, srt, seg, hd, (const TD*)in[1].ptr, (float*)out[0].ptr,
-                                          (float*)part->p, T, H);
-      launch_k(k_embed_fold, g2, 256, 0, s, ids, srt, seg, (const float*)part->p, (float*)out[0].ptr, T, H);
+                                          (float*)ws_at(part), T, H);
+      launch_k(k_embed_fold, g2, 256, 0, s, ids, srt, seg, (const float*)ws_at(part), (float*)out[0].ptr, T, H);
     };
   });
 }
@@ -1769,14 +1749,14 @@ static void b_cross_entropy(Plan& p) {
   const float gscale = float(p.attrs.f("grad_scale", 1.0));
   const bool grad = p.out.size() > 1;
   if (grad) require(same_shape(p.out[1], X) && p.out[1].dtype == X.dtype, "cross_entropy: dlogits like logits");
-  auto ws = std::make_shared<Scratch>(size_t(T + 4) * 4);
-  auto err = std::make_shared<Scratch>(4);
+  const size_t ws = p.ws_take(size_t(T + 4) * 4);
+  auto err = std::make_shared<Scratch>(4);  // sticky error flag (label out of range), write-only
   TCB_CUDA(cudaMemset(err->p, 0, 4));
   p.nkernels = 3;
   dispatch_float(X.dtype, [&](auto* tp) {
     using T_ = std::remove_pointer_t<decltype(tp)>;
     p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
-      float* inv_n = (float*)ws->p;
+      float* inv_n = (float*)ws_at(ws);
       float* rows = inv_n + 4;
       const bool vec = Vp % 8 == 0 && reinterpret_cast<uintptr_t>(in[0].ptr) % 16 == 0 &&
                        (!grad || reinterpret_cast<uintptr_t>(out[1].ptr) % 16 == 0);

@@ -192,6 +192,7 @@ void* tb_session_create(const char* cfg_c, int device) {
     s->device = device;
     prepare(*s, cfg_c);
     s->vm.set_device(device);
+    s->vm.set_world(int(s->cfg.world));
     s->vm.compile(s->fn, s->ts.state_binding);
     tcb_check(tcb_stream_create(&s->stream), "stream");
     const int64_t T = s->cfg.T();

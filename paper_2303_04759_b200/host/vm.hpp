@@ -40,10 +40,11 @@ inline tcb_tensor desc(void* ptr, const TensorType& t) {
 }
 
 /// KernelCacheKey: dialect op, input shapes + dtypes,
-/// attributes (the closure-hash slot carries the attribute string).
+/// attributes (the closure-hash slot carries the attribute string), plus the
+/// device the plan was compiled for (plans hold read-only device data).
 inline std::string cache_key(const std::string& op, const std::vector<TensorType>& in,
-                             const std::vector<TensorType>& out, const AttrMap& attrs) {
-  std::string k = op + "|";
+                             const std::vector<TensorType>& out, const AttrMap& attrs, int device = 0) {
+  std::string k = "dev" + std::to_string(device) + "|" + op + "|";
   for (auto& t : in) k += type_str(t) + ",";
   k += "->";
   for (auto& t : out) k += type_str(t) + ",";
@@ -97,8 +98,8 @@ struct PlanTable {
 };
 
 inline tcb_plan get_plan(const std::string& op, const std::vector<TensorType>& in, const std::vector<TensorType>& out,
-                         const AttrMap& attrs) {
-  const std::string key = cache_key(op, in, out, attrs);
+                         const AttrMap& attrs, int device = 0) {
+  const std::string key = cache_key(op, in, out, attrs, device);
   backends::KernelCache::global().get(key, [&]() -> backends::KernelPtr {
     std::vector<tcb_tensor> di, dout;
     for (auto& t : in) di.push_back(desc(nullptr, t));
@@ -110,10 +111,13 @@ inline tcb_plan get_plan(const std::string& op, const std::vector<TensorType>& i
                               int(at.size()), nullptr, &p),
               "compile " + op);
     {
+      // a plan already published under this key may be held by a running VM:
+      // it is never destroyed -- a concurrent duplicate compile is dropped
+      // (the KernelCache entry itself stays last-writer-wins, backends.hpp:335-337)
       std::lock_guard<std::mutex> g(PlanTable::global().mu);
       auto& slot = PlanTable::global().plans[key];
-      if (slot) tcb_plan_destroy(slot);  // last writer wins (backends.hpp:335-337)
-      slot = p;
+      if (slot) tcb_plan_destroy(p);
+      else slot = p;
     }
     auto k = std::make_shared<backends::Kernel>();
     k->key = key;
@@ -141,7 +145,7 @@ struct Instr {
 };
 
 struct VMStats {
-  int64_t arena_bytes = 0, state_bytes = 0, planner_peak = 0;
+  int64_t arena_bytes = 0, state_bytes = 0, planner_peak = 0, workspace_bytes = 0;
   int instructions = 0, kernels = 0, lets = 0;
   int kernels_static = 0;  // sum of the plans' kernel counts (before fold deferral)
 };
@@ -200,9 +204,13 @@ class DeviceVM {
   void run(void* stream, bool use_graph) {
     // deferred partial-sum folds for this step's enqueue (pool allocated here,
     // outside capture); enqueue flushes them before the optimizer
-    tcb_check(tcb_fold_defer(fold_defer_ ? 1 : 0, fold_pool_bytes()), "fold defer");
+    if (has_collectives_ && !comm_ && world_ > 1)
+      throw ProtocolError("device VM: a world-" + std::to_string(world_) +
+                          " step needs a communicator (set_comm) before it runs");
+    if (fold_defer_ && !fold_ctx_) tcb_check(tcb_fold_ctx_create(fold_pool_bytes(), &fold_ctx_), "fold context");
+    tcb_check(tcb_fold_use(fold_defer_ ? fold_ctx_ : nullptr), "fold use");
     struct Off {
-      ~Off() { tcb_fold_defer(0, 0); }
+      ~Off() { tcb_fold_use(nullptr); }
     } off;
     uint64_t d0 = 0, l0 = 0, d1 = 0, l1 = 0;
     tcb_check(tcb_fold_counters(&d0, &l0), "fold counters");
@@ -229,14 +237,13 @@ class DeviceVM {
 
   void set_comm(void* c) {
     comm_ = c;
-    for (auto& ins : code_)
-      (void)ins;
     if (graph_) {
       tcb_graph_destroy(graph_);
       graph_ = nullptr;
     }
   }
   void set_device(int d) { device_ = d; }
+  void set_world(int w) { world_ = w; }
   const VMStats& stats() const { return stats_; }
   const Layout& layout() const { return layout_; }
   const std::vector<Instr>& code() const { return code_; }
@@ -289,7 +296,7 @@ class DeviceVM {
       else if (base == "all_gather") ins.kind = OpKind::AllGather;
       else if (base == "allreduce") ins.kind = OpKind::AllReduce;
       else {
-        ins.plan = get_plan(b.value->op, tin, tout, b.value->call_attrs);
+        ins.plan = get_plan(b.value->op, tin, tout, b.value->call_attrs, device_);
         ins.nkernels = tcb_plan_num_kernels(ins.plan);
       }
       if (ins.kind != OpKind::Launch) ins.nkernels = 1;
@@ -315,6 +322,25 @@ class DeviceVM {
     }
     overlap_optimizer();
     stats_.instructions = int(code_.size());
+    // one launch workspace for the whole (stream-ordered) step: the largest
+    // any plan asks for (plans own no mutable device memory)
+    uint64_t ws = 0;
+    for (auto& x : code_) {
+      if (!x.plan) continue;
+      uint64_t b = 0;
+      tcb_check(tcb_plan_workspace_bytes(x.plan, &b), "workspace size");
+      ws = std::max(ws, b);
+    }
+    if (ws) {
+      void* w = nullptr;
+      tcb_check(tcb_init(device_, ws, &w), "tcb_init(workspace)");
+      ws_ = w;
+      ws_bytes_ = ws;
+    }
+    stats_.workspace_bytes = int64_t(ws);
+    for (auto& x : code_)
+      if (x.kind == OpKind::ReduceScatter || x.kind == OpKind::AllGather || x.kind == OpKind::AllReduce)
+        has_collectives_ = true;
   }
 
   // Early optimizer (world 1): the flat Adam over [P] is split into chunks of
@@ -423,7 +449,7 @@ class DeviceVM {
         x.out[k].ptr = static_cast<char*>(x.out[k].ptr) + c.a * es;
         tout.push_back(TensorType{code_dtype(x.out[k].dtype), {n}});
       }
-      x.plan = get_plan(adam.op, tin, tout, at);
+      x.plan = get_plan(adam.op, tin, tout, at, device_);
       x.nkernels = tcb_plan_num_kernels(x.plan);
       if (x.after < 0) out.push_back(x);  // ready from the start: plain side launch after the hoisted step
       else after_of[size_t(x.after)].push_back(x);
@@ -464,13 +490,15 @@ class DeviceVM {
         ev = ev_pool_[ev_pool_used_++];
         tcb_check(tcb_event_record(ev, stream), "event record");
         tcb_check(tcb_stream_wait_event(side_, ev), "stream wait");
-        tcb_check(tcb_launch(x.plan, x.in.data(), int(x.in.size()), x.out.data(), int(x.out.size()), side_), x.op);
+        tcb_check(tcb_launch_ws(x.plan, x.in.data(), int(x.in.size()), x.out.data(), int(x.out.size()), side_ws(),
+                                ws_bytes_, side_), x.op);
         forked = true;
         continue;
       }
       switch (x.kind) {
         case OpKind::Launch:
-          tcb_check(tcb_launch(x.plan, x.in.data(), int(x.in.size()), x.out.data(), int(x.out.size()), stream),
+          tcb_check(tcb_launch_ws(x.plan, x.in.data(), int(x.in.size()), x.out.data(), int(x.out.size()), ws_,
+                                  ws_bytes_, stream),
                     x.op);
           break;
         case OpKind::ReduceScatter:
@@ -513,7 +541,13 @@ class DeviceVM {
     graph_ = nullptr;
     if (arena_base_) tcb_free_arena(arena_base_);
     if (state_base_) tcb_free_arena(state_base_);
+    if (ws_) tcb_free_arena(ws_);
+    if (side_ws_) tcb_free_arena(side_ws_);
+    if (fold_ctx_) tcb_fold_ctx_destroy(fold_ctx_);
     arena_base_ = state_base_ = nullptr;
+    ws_ = side_ws_ = fold_ctx_ = nullptr;
+    ws_bytes_ = 0;
+    has_collectives_ = false;
     code_.clear();
   }
 
@@ -536,6 +570,17 @@ class DeviceVM {
   std::vector<void*> ev_pool_;
   size_t ev_pool_used_ = 0;
   int side_chunks_ = 0;
+  void* ws_ = nullptr;        // launch workspace of the compute stream
+  void* side_ws_ = nullptr;   // ... and of the optimizer side stream
+  uint64_t ws_bytes_ = 0;
+  void* fold_ctx_ = nullptr;  // this VM's deferred-fold pool
+  bool has_collectives_ = false;
+  int world_ = 1;
+  void* side_ws() {
+    if (!ws_bytes_) return nullptr;
+    if (!side_ws_) tcb_check(tcb_init(device_, ws_bytes_, &side_ws_), "tcb_init(side workspace)");
+    return side_ws_;
+  }
   VMStats stats_;
 };
 
