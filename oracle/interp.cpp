@@ -25,6 +25,9 @@ struct HVal {
 };
 
 thread_local std::string g_err;
+// the dropout step of the step being interpreted (rng_step state after its
+// increment), or -1 for a graph without dropout
+thread_local int64_t g_rng_step = -1;
 
 struct Interp {
   TrainStep ts;
@@ -111,7 +114,9 @@ void exec_let(Env& env, const ir::LetBinding& b) {
   }
   for (size_t k = 0; k < out.fields.size(); ++k) outs.push_back(odesc(*out.fields[k], out.types[k]));
   std::vector<std::string> keep;
-  auto at = oattrs(e->call_attrs, keep);
+  AttrMap am = e->call_attrs;
+  if (g_rng_step >= 0) am["rng_step"] = std::int64_t(g_rng_step);  // Philox counter word 3
+  auto at = oattrs(am, keep);
   const std::string base = base_name(e->op);
   if (orc_exec(base.c_str(), ins.data(), int(ins.size()), outs.data(), int(outs.size()), at.data(),
                int(at.size())) != 0)
@@ -132,9 +137,17 @@ void finish_step(Interp& I, Env& env, const ir::LetSeq& seq) {
 
 /// single rank; collectives with world > 1 go through `coll` (e.g. gloo from
 /// Python) -- without it the oracle refuses them like exec_base does.
+int64_t next_rng_step(const Interp& I) {
+  if (I.ts.i_rng < 0) return -1;
+  float v;
+  std::memcpy(&v, I.state[size_t(I.ts.i_rng)]->data(), 4);
+  return int64_t(v + 1.0f);  // the step's add_scalar(rng_step, 1)
+}
+
 void run_step(Interp& I, CollFn coll = nullptr, int rank = 0) {
   auto seq = ir::flatten(*I.ts.fn);
   Env env = init_env(I);
+  g_rng_step = next_rng_step(I);
   for (auto& b : seq.lets) {
     const auto& e = b.value;
     if (e->kind == ExprKind::Call && is_collective(base_name(e->op)) &&
@@ -165,6 +178,7 @@ void run_step(Interp& I, CollFn coll = nullptr, int rank = 0) {
 /// mismatched op across ranks raises ProtocolError.
 void run_world_step(std::vector<Interp>& R) {
   const int N = int(R.size());
+  g_rng_step = next_rng_step(R[0]);
   auto seq = ir::flatten(*R[0].ts.fn);
   std::vector<ir::LetSeq> seqs;
   for (auto& I : R) seqs.push_back(ir::flatten(*I.ts.fn));

@@ -145,9 +145,24 @@ static void philox4x32_10(uint32_t c[4], uint32_t k0, uint32_t k1) {
   }
 }
 
+/* Counter word 3 is the training step's dropout step (the step graph's
+ * rng_step state, incremented once per step; attr "rng_step" of the op being
+ * executed), so masks differ from step to step; 0 outside a step. */
+static __thread uint32_t g_rng_step;
+
+int orc_dropout_keep_step(uint64_t seed, uint64_t salt, uint64_t index, float p, uint32_t step) {
+  if (p <= 0.0f) return 1;
+  uint32_t c[4] = {(uint32_t)(index >> 3), (uint32_t)salt, (uint32_t)(salt >> 32), step};
+  philox4x32_10(c, (uint32_t)seed, (uint32_t)(seed >> 32));
+  uint32_t w = c[(index & 7) >> 1];
+  uint32_t h = (index & 1) ? (w >> 16) : (w & 0xFFFFu);
+  float u = (float)h * (1.0f / 65536.0f);
+  return u >= p;
+}
+
 int orc_dropout_keep(uint64_t seed, uint64_t salt, uint64_t index, float p) {
   if (p <= 0.0f) return 1;
-  uint32_t c[4] = {(uint32_t)(index >> 3), (uint32_t)salt, (uint32_t)(salt >> 32), 0u};
+  uint32_t c[4] = {(uint32_t)(index >> 3), (uint32_t)salt, (uint32_t)(salt >> 32), g_rng_step};
   philox4x32_10(c, (uint32_t)seed, (uint32_t)(seed >> 32));
   uint32_t w = c[(index & 7) >> 1];
   uint32_t h = (index & 1) ? (w >> 16) : (w & 0xFFFFu);
@@ -853,6 +868,7 @@ int orc_exec(const char* op, const orc_tensor* in, int nin, orc_tensor* out, int
              const orc_attr* attrs, int na) {
   g_err[0] = 0;
   const orc_attr* A = attrs;
+  g_rng_step = (uint32_t)aint(A, na, "rng_step", 0);
   /* exec_base if-chain, backends.hpp:168-273 */
   if (!strcmp(op, "add")) { NEED(2, 1); return elemwise_binary(OP_ADD, &in[0], &in[1], &out[0]); }
   if (!strcmp(op, "sub")) { NEED(2, 1); return elemwise_binary(OP_SUB, &in[0], &in[1], &out[0]); }

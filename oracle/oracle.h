@@ -60,6 +60,7 @@ float orc_bf16_bits_to_float(uint16_t h);
 float orc_quantize_bf16(float f);
 
 /* Philox4x32-10 keep-mask draw used by dropout: 1 = keep. */
+int orc_dropout_keep_step(uint64_t seed, uint64_t salt, uint64_t index, float p, uint32_t step);
 int orc_dropout_keep(uint64_t seed, uint64_t salt, uint64_t index, float p);
 
 /* mt19937-backed generator restating Rng (tensor.hpp:145-176) so synthetic

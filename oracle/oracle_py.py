@@ -46,6 +46,9 @@ def lib():
                                               ctypes.c_float, ctypes.c_float]
         _lib.orc_rng_fill_below.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
                                             ctypes.c_uint32]
+        _lib.orc_dropout_keep_step.restype = ctypes.c_int
+        _lib.orc_dropout_keep_step.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
+                                               ctypes.c_float, ctypes.c_uint32]
         _lib.orc_dropout_keep.restype = ctypes.c_int
         _lib.orc_dropout_keep.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
                                           ctypes.c_float]
@@ -150,9 +153,11 @@ def rng_below(seed: int, n: int, bound: int, impl="oracle") -> np.ndarray:
     return out
 
 
-def dropout_keep_mask(seed: int, salt: int, n: int, p: float) -> np.ndarray:
+def dropout_keep_mask(seed: int, salt: int, n: int, p: float, step: int = 0) -> np.ndarray:
+    """keep bits of elements 0..n-1 of a dropout site (step: the Philox
+    counter's rng_step word)"""
     L = lib()
-    return np.array([L.orc_dropout_keep(seed, salt, i, p) for i in range(n)], dtype=np.uint8)
+    return np.array([L.orc_dropout_keep_step(seed, salt, i, p, step) for i in range(n)], dtype=np.uint8)
 
 
 __all__ = ["run", "HostTensor", "rng_uniform", "rng_below", "ref_available", "lib", "ref",

@@ -54,6 +54,7 @@ static std::string spec_str(const Spec& s) {
 
 struct tcb_plan_ {
   tcb::Plan p;
+  bool rng_in = false;  // launches carry a trailing rng_step input
   // fallback workspace for callers of plain tcb_launch (tests, one-off ops):
   // allocated on first such launch (never during capture), serialised by mu
   std::mutex mu;
@@ -64,6 +65,10 @@ namespace tcb {
 char*& launch_ws() {
   thread_local char* w = nullptr;
   return w;
+}
+const float*& launch_rng() {
+  thread_local const float* r = nullptr;
+  return r;
 }
 }  // namespace tcb
 
@@ -144,6 +149,14 @@ int tcb_plan_create(const char* dialect_op, const tcb_tensor* in, int nin, const
       }
       if (closure_hash) key << "|" << closure_hash;
       p.key = key.str();
+      // rng_in=1: the caller appends the training step's rng_step (f32[1]) as
+      // the last input of every launch; kernels key their dropout masks on it
+      if (p.attrs.i("rng_in", 0)) {
+        require(!p.in.empty() && p.in.back().numel() == 1 && p.in.back().dtype == TCB_F32,
+                "b200." + base + ": rng_in expects a trailing f32[1] rng_step input");
+        p.in.pop_back();
+        pl->rng_in = true;
+      }
       it->second(p);
       if (!p.run) fail(TCB_ERR_UNIMPLEMENTED, "b200." + base + ": no kernel for this configuration");
     } catch (...) {
@@ -169,20 +182,24 @@ static void launch_with(tcb_plan plan, const tcb_tensor* in, int nin, tcb_tensor
                         uint64_t ws_bytes, void* stream) {
   if (!plan) fail(TCB_ERR_ARG, "null plan");
   Plan& p = plan->p;
-  if (nin != int(p.in.size()) || nout != int(p.out.size()))
+  if (nin != int(p.in.size()) + int(plan->rng_in) || nout != int(p.out.size()))
     fail(TCB_ERR_ARG, "b200." + p.op + ": launch arity differs from plan");
   if (p.ws_bytes && ws && ws_bytes < p.ws_bytes)
     fail(TCB_ERR_ARG, "b200." + p.op + ": workspace of " + std::to_string(ws_bytes) + " B < the plan's " +
                           std::to_string(p.ws_bytes) + " B");
   if (skipped_op(p.op)) return;
   // a deferred fold whose output this launch reads is folded first
-  for (int i = 0; i < nin; ++i)
+  for (int i = 0; i < int(p.in.size()); ++i)
     fold_flush_if_reads(in[i].ptr, size_t(p.in[i].numel()) * dtype_bytes(p.in[i].dtype),
                         static_cast<cudaStream_t>(stream));
   struct Reset {
-    ~Reset() { launch_ws() = nullptr; }
+    ~Reset() {
+      launch_ws() = nullptr;
+      launch_rng() = nullptr;
+    }
   } reset;
   launch_ws() = static_cast<char*>(ws);
+  launch_rng() = plan->rng_in ? static_cast<const float*>(in[nin - 1].ptr) : nullptr;
   p.run(in, out, static_cast<cudaStream_t>(stream));
   TCB_CUDA(cudaGetLastError());
 }

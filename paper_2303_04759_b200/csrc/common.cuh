@@ -263,12 +263,20 @@ struct DropCfg {
   // instead of re-running Philox (add_layer_norm save_mask / layer_norm_dx mask_in)
   uint8_t* mask_out = nullptr;
   const uint8_t* mask_in = nullptr;
+  // Philox counter word 3: the training step's dropout step (rng_step state,
+  // f32, incremented once per step), so masks differ from step to step.
+  // Read on the device once per kernel (drop_resolve, after griddepcontrol.wait)
+  uint32_t step = 0;
+  const float* step_ptr = nullptr;
 };
+__device__ __forceinline__ void drop_resolve(DropCfg& d) {
+  if (d.step_ptr) d.step = uint32_t(*d.step_ptr);
+}
 // 8 keep bits for indices (q*8 .. q*8+7): one Philox call, 16 bits per element
 // (identical to oracle.c orc_dropout_keep); integer compares: the high half of
 // word w is >= thr iff w >= thr << 16
 __device__ __forceinline__ uint32_t dropout_bits8q(const DropCfg& d, uint64_t q) {
-  uint32_t c[4] = {uint32_t(q), uint32_t(d.salt), uint32_t(d.salt >> 32), 0u};
+  uint32_t c[4] = {uint32_t(q), uint32_t(d.salt), uint32_t(d.salt >> 32), d.step};
   philox4x32_10(c, uint32_t(d.seed), uint32_t(d.seed >> 32));
   uint32_t bits = 0;
 #pragma unroll
@@ -289,6 +297,13 @@ __device__ __forceinline__ uint32_t dropout_bits4(const DropCfg& d, uint64_t i0)
   uint32_t b = 0;
   for (int k = 0; k < 4; ++k) b |= uint32_t(dropout_keep(d, i0 + k)) << k;
   return b;
+}
+// the rng_step input of the launch in progress (tcb_launch appends it when the
+// plan was created with rng_in=1); nullptr: step 0
+const float*& launch_rng();
+inline DropCfg with_step(DropCfg d) {
+  d.step_ptr = launch_rng();
+  return d;
 }
 inline DropCfg drop_cfg(const Attrs& a) {
   DropCfg d;

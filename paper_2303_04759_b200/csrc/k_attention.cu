@@ -117,6 +117,8 @@ __global__ void __launch_bounds__(AT_FWD_THREADS) k_attn_fwd(const __grid_consta
   const uint32_t tm = *tslot;
   pdl_wait();
   pdl_trigger();
+  DropCfg dd = a.d;
+  drop_resolve(dd);
 
   auto issue_load = [&](int zz, int buf) {
     const int bb = zz / a.A, hh = zz % a.A;
@@ -159,9 +161,9 @@ __global__ void __launch_bounds__(AT_FWD_THREADS) k_attn_fwd(const __grid_consta
       tc_commit<1>(&bar[2]);
     }
     // dropout keep bits overlap the QK^T MMA (and are saved for the backward)
-    const uint32_t kb = keep_bits32(a.d, (uint64_t(z) * a.S + row) * a.S, j0, a.S);
-    if (a.d.mask_out && row < a.S)
-      reinterpret_cast<uint32_t*>(a.d.mask_out)[(uint64_t(z) * a.S + row) * 4 + cq] = kb;
+    const uint32_t kb = keep_bits32(dd, (uint64_t(z) * a.S + row) * a.S, j0, a.S);
+    if (dd.mask_out && row < a.S)
+      reinterpret_cast<uint32_t*>(dd.mask_out)[(uint64_t(z) * a.S + row) * 4 + cq] = kb;
     mbar_wait(&bar[2], it & 1);
     tc_fence_after();
     T(2);
@@ -223,7 +225,7 @@ __global__ void __launch_bounds__(AT_FWD_THREADS) k_attn_fwd(const __grid_consta
       bulk_commit();
     }
     uint8_t* sA = sP;
-    if (a.d.p > 0.0f) {
+    if (dd.p > 0.0f) {
       // Pd = bf16(P * keep / (1-p)) into its own tile: the probs store keeps reading sP
       sA = sPd;
       uint8_t* tileD = sPd + (cq >> 1) * AT_TILE;
@@ -233,7 +235,7 @@ __global__ void __launch_bounds__(AT_FWD_THREADS) k_attn_fwd(const __grid_consta
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
           const int j = g * 8 + e;
-          pd[e] = ((kb >> j) & 1u) ? v[j] * a.d.scale : 0.0f;
+          pd[e] = ((kb >> j) & 1u) ? v[j] * dd.scale : 0.0f;
         }
         uint4 w;
         w.x = pack_bf2(pd[0], pd[1]);
@@ -323,6 +325,8 @@ __global__ void __launch_bounds__(AT_THREADS) k_attn_bwd(const __grid_constant__
   const uint32_t tm = *tslot;
   pdl_wait();
   pdl_trigger();
+  DropCfg dd = a.d;
+  drop_resolve(dd);
 
   auto issue_load = [&](int zz, int buf) {
     const int bb = zz / a.A, hh = zz % a.A;
@@ -362,14 +366,14 @@ __global__ void __launch_bounds__(AT_THREADS) k_attn_bwd(const __grid_constant__
     tc_commit<1>(&bar[2]);
   }
   uint32_t kb[2];
-  if (a.d.mask_in) {  // the forward's saved keep bits (no Philox re-run)
-    const uint32_t* mw = reinterpret_cast<const uint32_t*>(a.d.mask_in) + (uint64_t(z) * a.S + row) * 4 + 2 * hf;
+  if (dd.mask_in) {  // the forward's saved keep bits (no Philox re-run)
+    const uint32_t* mw = reinterpret_cast<const uint32_t*>(dd.mask_in) + (uint64_t(z) * a.S + row) * 4 + 2 * hf;
     kb[0] = row < a.S ? mw[0] : 0xffffffffu;
     kb[1] = row < a.S ? mw[1] : 0xffffffffu;
   } else {
-    keep_bits64(a.d, (uint64_t(z) * a.S + row) * a.S, j0, a.S, kb);
+    keep_bits64(dd, (uint64_t(z) * a.S + row) * a.S, j0, a.S, kb);
   }
-  const float sd = a.d.p > 0.0f ? a.d.scale : 1.0f;
+  const float sd = dd.p > 0.0f ? dd.scale : 1.0f;
   mbar_wait(&bar[2], it & 1);
   tc_fence_after();
 
@@ -420,7 +424,7 @@ __global__ void __launch_bounds__(AT_THREADS) k_attn_bwd(const __grid_constant__
     o.z = pack_bf2(ds[4], ds[5]);
     o.w = pack_bf2(ds[6], ds[7]);
     *reinterpret_cast<uint4*>(tileS + sw128(row, g)) = o;
-    if (a.d.p > 0.0f) {
+    if (dd.p > 0.0f) {
       o.x = pack_bf2(pd[0], pd[1]);
       o.y = pack_bf2(pd[2], pd[3]);
       o.z = pack_bf2(pd[4], pd[5]);

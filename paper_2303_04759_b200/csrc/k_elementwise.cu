@@ -342,6 +342,7 @@ TCB_REGISTER("concat", b_concat);
 template <typename T>
 __global__ void k_dropout(const T* __restrict__ x, T* __restrict__ y, int64_t n, DropCfg d) {
   TCB_PDL_ENTRY();
+  drop_resolve(d);
   const int64_t nq = (n + 7) / 8;
   for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < nq;
        q += int64_t(gridDim.x) * blockDim.x) {
@@ -361,7 +362,7 @@ static void b_dropout(Plan& p) {
   dispatch_float(p.out[0].dtype, [&](auto* tp) {
     using T = std::remove_pointer_t<decltype(tp)>;
     p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
-      launch_k(k_dropout<T>, grid_for((n + 7) / 8, 256), 256, 0, s, (const T*)in[0].ptr, (T*)out[0].ptr, n, d);
+      launch_k(k_dropout<T>, grid_for((n + 7) / 8, 256), 256, 0, s, (const T*)in[0].ptr, (T*)out[0].ptr, n, with_step(d));
     };
   });
 }

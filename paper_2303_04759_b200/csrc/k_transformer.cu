@@ -142,6 +142,7 @@ __global__ void __launch_bounds__(256) k_ln_fwd(const T* __restrict__ x, const T
                                                 float* __restrict__ rstd_o, int64_t rows, int H, float eps,
                                                 DropCfg d, bool vec) {
   TCB_PDL_ENTRY();
+  drop_resolve(d);
   // RW rows per warp, every global load of both rows issued before the first
   // reduction so enough bytes are in flight to cover DRAM latency
   constexpr int RW = NC <= 2 ? 2 : 1;
@@ -319,6 +320,7 @@ __global__ void __launch_bounds__(256) k_ln_fwd16(const T* __restrict__ x, const
                                                   float* __restrict__ rstd_o, int64_t rows, int H, float eps,
                                                   DropCfg d) {
   TCB_PDL_ENTRY();
+  drop_resolve(d);
   constexpr int RW = 2;
   __shared__ __align__(16) float sg[NC * 256], sb[NC * 256];
   const int lane = threadIdx.x & 31;
@@ -438,7 +440,7 @@ static void build_ln_fwd(Plan& p, bool residual) {
    dispatch_nc(H, [&](auto nc) {
     constexpr int NC = decltype(nc)::value;
     p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
-      DropCfg d = d0;
+      DropCfg d = with_step(d0);
       if (save_mask) d.mask_out = static_cast<uint8_t*>(out[4].ptr);
       const int gi = residual ? 2 : 1;
       bool vec = (H % 8 == 0);
@@ -490,6 +492,7 @@ __global__ void __launch_bounds__(256) k_ln_bwd(const T* __restrict__ sx, const 
                                                 T* __restrict__ dx_o, float* __restrict__ ws, int nparts,
                                                 int64_t rows, int H, DropCfg d, bool vec) {
   TCB_PDL_ENTRY();
+  drop_resolve(d);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nch = (H + 7) / 8;
   // per-warp dgamma/dbeta partials live in smem (not registers), laid out
@@ -591,6 +594,8 @@ __global__ void __launch_bounds__(256, NC <= 3 ? 2 : 1) k_ln_bwd16(const T* __re
                                                   T* __restrict__ ds_o, T* __restrict__ dx_o, float* __restrict__ ws,
                                                   int nparts, int64_t rows, int H, DropCfg d, DropCfg din) {
   TCB_PDL_ENTRY();
+  drop_resolve(d);
+  drop_resolve(din);
   constexpr int RW = LNB_ROWS / 8;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nch = FULL ? NC * 32 : H / 8;
@@ -836,7 +841,7 @@ static void b_layer_norm_dx(Plan& p) {
       }
     });
     p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
-      DropCfg d = d0;
+      DropCfg d = with_step(d0);
       if (mask_in) d.mask_in = static_cast<const uint8_t*>(in[nin - 1].ptr);
       bool vec = H % 8 == 0;
       for (int i : {0, 4}) vec = vec && reinterpret_cast<uintptr_t>(in[i].ptr) % 16 == 0;
@@ -861,7 +866,7 @@ static void b_layer_norm_dx(Plan& p) {
                          : (full ? k_ln_bwd16<T, NC, false, true> : k_ln_bwd16<T, NC, false, false>);
           launch_k(kern, nblk, 256, smem, s, (const T*)in[0].ptr, (const void*)in[1].ptr, (const float*)in[2].ptr,
                    (const float*)in[3].ptr, (const T*)in[4].ptr, d2, (T*)out[0].ptr, dxp, wsp, np, rows, H,
-                   d, din);
+                   d, with_step(din));
         }
       } else {
         launch_k(k_ln_bwd<T, NC>, nblk, 256, smem, s, (const T*)in[0].ptr, gfp, gtp, (const float*)in[2].ptr,
@@ -931,6 +936,7 @@ __global__ void __launch_bounds__(256) k_softmax(const TI* __restrict__ x, TO* _
                                                  TO* __restrict__ Pd, int64_t rows, int C, int Sq,
                                                  float scale, int causal, DropCfg d, bool vec) {
   TCB_PDL_ENTRY();
+  drop_resolve(d);
   constexpr int RW = NQ == 1 ? 4 : NQ == 2 ? 2 : 1;  // rows per warp, loads batched
   const int lane = threadIdx.x & 31;
   const int64_t row0 = (blockIdx.x * int64_t(blockDim.x >> 5) + (threadIdx.x >> 5)) * RW;
@@ -1003,6 +1009,7 @@ __global__ void __launch_bounds__(256) k_softmax_bwd(const TP* __restrict__ P, c
                                                      TO* __restrict__ dS, TO* __restrict__ Pd_o, int64_t rows,
                                                      int C, float scale, DropCfg d, bool vec) {
   TCB_PDL_ENTRY();
+  drop_resolve(d);
   constexpr int RW = NQ == 1 ? 4 : NQ == 2 ? 2 : 1;
   const int lane = threadIdx.x & 31;
   const int64_t row0 = (blockIdx.x * int64_t(blockDim.x >> 5) + (threadIdx.x >> 5)) * RW;
@@ -1104,7 +1111,7 @@ static void b_softmax(Plan& p) {
                        reinterpret_cast<uintptr_t>(out[0].ptr) % 16 == 0 &&
                        (!pd || reinterpret_cast<uintptr_t>(out[1].ptr) % 16 == 0);
       launch_k(k_softmax<TI, TO, NQ>, sm_grid<NQ>(rows), 256, 0, s, 
-          (const TI*)in[0].ptr, (TO*)out[0].ptr, pd ? (TO*)out[1].ptr : nullptr, rows, C, Sq, scale, causal, d, vec);
+          (const TI*)in[0].ptr, (TO*)out[0].ptr, pd ? (TO*)out[1].ptr : nullptr, rows, C, Sq, scale, causal, with_step(d), vec);
     };
    });
   });
@@ -1241,7 +1248,7 @@ static void b_attention(Plan& p) {
   if (fused) {
     void* trace = reinterpret_cast<void*>(p.attrs.i("tc_trace", 0));  // tooling only
     p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
-      DropCfg d = g.d;
+      DropCfg d = with_step(g.d);
       if (save_mask) d.mask_out = static_cast<uint8_t*>(out[2].ptr);
       launch_attn_fwd(in[0].ptr, out[0].ptr, out[1].ptr, g.B, g.S, g.H, g.A, g.scale, g.causal, d, s, trace);
     };
@@ -1264,7 +1271,7 @@ static void b_attention(Plan& p) {
       T* Pd = g.d.p > 0.0f ? (T*)ws_at(pd) : nullptr;
       dispatch_nq(int(g.S), [&](auto nq) {
         launch_k(k_softmax<float, T, decltype(nq)::value>, sm_grid<decltype(nq)::value>(rows), 256, 0, s, 
-            (const float*)ws_at(scores), (T*)out[1].ptr, Pd, rows, int(g.S), int(g.S), 1.0f, g.causal, g.d,
+            (const float*)ws_at(scores), (T*)out[1].ptr, Pd, rows, int(g.S), int(g.S), 1.0f, g.causal, with_step(g.d),
             g.S % 4 == 0 && reinterpret_cast<uintptr_t>(out[1].ptr) % 16 == 0);
       });
       // 3. ctx = Pd V
@@ -1287,7 +1294,7 @@ static void b_attention_dx(Plan& p) {
   if (mask_in && !fused) fail(TCB_ERR_UNIMPLEMENTED, "attention_dx: a saved mask needs the fused kernel");
   if (fused) {
     p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
-      DropCfg d = g.d;
+      DropCfg d = with_step(g.d);
       if (mask_in) d.mask_in = static_cast<const uint8_t*>(in[3].ptr);
       launch_attn_bwd(in[0].ptr, in[1].ptr, in[2].ptr, out[0].ptr, g.B, g.S, g.H, g.A, g.scale, g.causal, d, s);
     };
@@ -1311,7 +1318,7 @@ static void b_attention_dx(Plan& p) {
       T* Pd = g.d.p > 0.0f ? (T*)ws_at(pd) : nullptr;
       dispatch_nq(int(g.S), [&](auto nq) {
         launch_k(k_softmax_bwd<T, float, T, decltype(nq)::value>, sm_grid<decltype(nq)::value>(rows), 256, 0, s, 
-            (const T*)in[1].ptr, (const float*)ws_at(dpd), (T*)ws_at(ds), Pd, rows, int(g.S), g.scale, g.d,
+            (const T*)in[1].ptr, (const float*)ws_at(dpd), (T*)ws_at(ds), Pd, rows, int(g.S), g.scale, with_step(g.d),
             g.S % 4 == 0 && reinterpret_cast<uintptr_t>(in[1].ptr) % 16 == 0);
       });
       char* dq = static_cast<char*>(out[0].ptr);

@@ -91,7 +91,7 @@ struct TrainStep {
   std::vector<ParamSeg> segs;
   // function parameter roles (indices into fn->params)
   int i_ids = -1, i_labels = -1, i_pos = -1, i_type = -1, i_params = -1, i_p16 = -1, i_m = -1, i_v = -1,
-      i_step = -1;
+      i_step = -1, i_rng = -1;
   std::vector<std::pair<int, int>> state_binding;  // (ret index, param index): in-place state update
   FusionStats fusion;
   int64_t shard() const { return P_pad / cfg.world; }
@@ -207,7 +207,11 @@ inline TrainStep build_train_step(const ModelCfg& c) {
     ts.i_v = P("v", {kF32, {pstate}});
     ts.i_step = P("step", {kF32, {1}});
   }
+  // dropout step counter (f32[1] state, +1 per step): the Philox counter's
+  // 4th word, so the dropout masks change every step (device and oracle alike)
+  if (c.p > 0.0) ts.i_rng = P("rng_step", {kF32, {1}});
   auto par = [&](int i) { return g.params()[i]; };
+  VarPtr rng_next = c.p > 0.0 ? g.op("add_scalar", {par(ts.i_rng)}, {{"value", 1.0}}, "rng") : nullptr;
   VarPtr ids = par(ts.i_ids), labels = par(ts.i_labels), pos_ids = par(ts.i_pos);
   VarPtr wsrc = copy ? par(ts.i_p16) : par(ts.i_params);
 
@@ -356,6 +360,10 @@ inline TrainStep build_train_step(const ModelCfg& c) {
       rets.push_back(nh);
       ts.state_binding.push_back({5, ts.i_p16});
     }
+  }
+  if (rng_next) {
+    rets.push_back(rng_next);
+    ts.state_binding.push_back({int(rets.size()) - 1, ts.i_rng});
   }
   FunctionPtr raw = g.finish(rets);
   LetSeq seq = ir::flatten(*raw);

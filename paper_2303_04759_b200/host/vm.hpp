@@ -266,6 +266,9 @@ class DeviceVM {
  private:
   void emit_bytecode() {
     code_.clear();
+    rng_ptr_ = nullptr;
+    for (size_t p = 0; p < fn_->params.size(); ++p)
+      if (fn_->params[p]->id == "rng_step") rng_ptr_ = param_ptr_[p];
     std::set<int> copy_concat(layout_.concat_copy.begin(), layout_.concat_copy.end());
     for (size_t i = 0; i < seq_.lets.size(); ++i) {
       const auto& b = seq_.lets[i];
@@ -292,11 +295,21 @@ class DeviceVM {
         tout.push_back(b.var->ty.tensor());
         ins.out.push_back(desc(ptr_of(b.var.get()), b.var->ty.tensor()));
       }
+      // dropout sites read the step's rng_step state as a trailing launch input
+      // (plan attr rng_in=1): their Philox masks change every step
+      AttrMap pattrs = b.value->call_attrs;
+      if (rng_ptr_ && pattrs.count("seed") &&
+          (ir::attr_double(pattrs, "p", 0.0) > 0.0 || ir::attr_double(pattrs, "in_p", 0.0) > 0.0)) {
+        pattrs["rng_in"] = std::int64_t(1);
+        TensorType rt{kF32, {1}};
+        tin.push_back(rt);
+        ins.in.push_back(desc(rng_ptr_, rt));
+      }
       if (base == "reduce_scatter") ins.kind = OpKind::ReduceScatter;
       else if (base == "all_gather") ins.kind = OpKind::AllGather;
       else if (base == "allreduce") ins.kind = OpKind::AllReduce;
       else {
-        ins.plan = get_plan(b.value->op, tin, tout, b.value->call_attrs, device_);
+        ins.plan = get_plan(b.value->op, tin, tout, pattrs, device_);
         ins.nkernels = tcb_plan_num_kernels(ins.plan);
       }
       if (ins.kind != OpKind::Launch) ins.nkernels = 1;
@@ -576,6 +589,7 @@ class DeviceVM {
   void* fold_ctx_ = nullptr;  // this VM's deferred-fold pool
   bool has_collectives_ = false;
   int world_ = 1;
+  void* rng_ptr_ = nullptr;   // the rng_step state (dropout step counter)
   void* side_ws() {
     if (!ws_bytes_) return nullptr;
     if (!side_ws_) tcb_check(tcb_init(device_, ws_bytes_, &side_ws_), "tcb_init(side workspace)");

@@ -332,7 +332,7 @@ class Session:
     def set_comm(self, comm: int):
         _check(lib().tb_session_set_comm(self.h, comm))
 
-    STATE = ("params", "p16", "m", "v", "step")
+    STATE = ("params", "p16", "m", "v", "step", "rng_step")
 
     def state_names(self) -> list[str]:
         """Training-state parameters of this step graph (master weights, the

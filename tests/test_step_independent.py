@@ -204,3 +204,19 @@ def test_fused_vs_unfused_interpreter(kind, dtype, p):
     worst = max((rel(g1[o:o + n], g0[o:o + n]), name) for name, o, n in graph_segments(cfg1))
     print(kind, dtype, p, "loss", l1, l0, "worst segment", worst)
     assert worst[0] <= tol, worst
+
+
+# ------------------------------------------------------- 4. dropout per step
+def test_dropout_masks_change_every_step():
+    """The Philox key carries the step graph's rng_step state (counter word 3,
+    +1 per step): with the parameters frozen (SGD lr=0) and the same batch,
+    p > 0 gives a different loss each step (new masks) while p = 0 gives the
+    same loss; the counter is part of the training state."""
+    for p, differ in ((0.1, True), (0.0, False)):
+        cfg = tiny("bert", p=p, H=64, F=128, V=128, S=16, B=2)
+        ids, labels = synthetic_batch(cfg)
+        o = Interp(cfg.cfg_string(model_only=True))
+        l1, l2, l3 = o.step(ids, labels), o.step(ids, labels), o.step(ids, labels)
+        assert (l1 != l2 and l2 != l3) if differ else (l1 == l2 == l3), (p, l1, l2, l3)
+        if p > 0:
+            assert o.read("rng_step", 1)[0] == 3.0

@@ -185,3 +185,13 @@ def test_scheduled_step_bit_identical():
     l0, p0 = run(cfg)
     l1, p1 = run(cfg_s)
     assert np.array_equal(l0, l1) and np.array_equal(p0, p1)
+
+
+def test_dropout_masks_change_per_step_device_matches_oracle():
+    """Dropout keyed on the rng_step state: with frozen parameters (SGD lr=0)
+    and one batch, each step draws new masks on the device exactly as the
+    oracle does (losses differ step to step and agree with the oracle)."""
+    cfg = ModelConfig.tiny(dtype="bf16", opt="sgd", lr=0.0, L=1, p=0.1)
+    s, o, gl, ol = run_pair(cfg, steps=3)
+    assert len(set(gl.tolist())) == 3, gl
+    assert np.max(np.abs(gl - ol)) < 2e-2, (gl, ol)
