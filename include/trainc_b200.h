@@ -59,6 +59,9 @@ int tb_session_param(void* h, const char* name, void** ptr, int64_t* bytes);
 const char* tb_session_segments(void* h);
 const char* tb_session_text(void* h, const char* what);
 int tb_session_set_comm(void* h, void* comm);
+/* vm.profile: per-instruction median device time over `repeats` eager steps
+ * (CSV idx,op,let,median_us,bytes_in,bytes_out,kernels); NULL on error */
+const char* tb_session_profile(void* h, int repeats);
 
 /* AutoCast pass census on the all-f32 step (CPU only; host/autocast.hpp) */
 int tb_autocast_info(const char* cfg, const char* policy, const char* placement, int64_t* out, int n);

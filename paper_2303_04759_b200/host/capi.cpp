@@ -363,6 +363,19 @@ const char* tb_session_text(void* h, const char* what) {
   return s->text.c_str();
 }
 
+/// vm.profile: `repeats` eager steps with CUDA events around
+/// every instruction; CSV idx,op,let,median_us,bytes_in,bytes_out,kernels.
+const char* tb_session_profile(void* h, int repeats) {
+  auto* s = static_cast<Session*>(h);
+  try {
+    s->text = s->vm.profile(s->stream, repeats);
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+  return s->text.c_str();
+}
+
 int tb_session_set_comm(void* h, void* comm) {
   TB_TRY(static_cast<Session*>(h)->vm.set_comm(comm));
 }

@@ -298,7 +298,7 @@ class DeviceVM {
       // dropout sites read the step's rng_step state as a trailing launch input
       // (plan attr rng_in=1): their Philox masks change every step
       AttrMap pattrs = b.value->call_attrs;
-      if (rng_ptr_ && pattrs.count("seed") &&
+      if (rng_ptr_ && (pattrs.count("seed") || pattrs.count("in_seed")) &&
           (ir::attr_double(pattrs, "p", 0.0) > 0.0 || ir::attr_double(pattrs, "in_p", 0.0) > 0.0)) {
         pattrs["rng_in"] = std::int64_t(1);
         TensorType rt{kF32, {1}};
@@ -485,10 +485,92 @@ class DeviceVM {
   static bool is_optimizer(const std::string& op) {
     return op == "adam_update" || op == "adam_update_ex" || op == "sgd_update";
   }
+  // vm.profile: events around every main-stream instruction
+  // and every fold flush of an eager step
+  struct ProfMark {
+    int instr;  // index into code_, -1: a deferred-fold flush
+    void *e0, *e1;
+  };
+  std::vector<ProfMark>* prof_ = nullptr;
+  std::vector<void*> prof_events_;
+  size_t prof_used_ = 0;
+  void* prof_rec(void* stream) {
+    if (prof_used_ >= prof_events_.size()) {
+      void* e = nullptr;
+      tcb_check(tcb_event_create(&e), "event");
+      prof_events_.push_back(e);
+    }
+    void* e = prof_events_[prof_used_++];
+    tcb_check(tcb_event_record(e, stream), "event record");
+    return e;
+  }
+  void flush_folds(void* stream) {
+    void* e0 = prof_ ? prof_rec(stream) : nullptr;
+    tcb_check(tcb_fold_flush(stream), "fold flush");
+    if (prof_) prof_->push_back({-1, e0, prof_rec(stream)});
+  }
+
+ public:
+  /// vm.profile: `repeats` eager steps with CUDA events around every
+  /// instruction; one CSV row per instruction (and per deferred-fold flush):
+  /// idx,op,let,median_us,bytes_in,bytes_out,kernels.  Compile time is not in
+  /// here (it happened at session creation: the one-time bucket).
+  std::string profile(void* stream, int repeats) {
+    std::vector<std::vector<float>> times;
+    std::vector<ProfMark> marks;
+    std::vector<ProfMark> first;
+    for (int r = 0; r < std::max(1, repeats); ++r) {
+      marks.clear();
+      prof_used_ = 0;
+      prof_ = &marks;
+      struct Off {
+        DeviceVM* v;
+        ~Off() { v->prof_ = nullptr; }
+      } off{this};
+      run(stream, false);
+      tcb_check(tcb_stream_sync(stream), "sync");
+      if (r == 0) {
+        first = marks;
+        times.assign(marks.size(), {});
+      }
+      if (marks.size() != first.size()) throw Error("profile: instruction stream changed between repeats");
+      for (size_t i = 0; i < marks.size(); ++i) {
+        float ms = 0;
+        tcb_check(tcb_event_elapsed_ms(marks[i].e0, marks[i].e1, &ms), "elapsed");
+        times[i].push_back(ms);
+      }
+    }
+    std::string out = "idx,op,let,median_us,bytes_in,bytes_out,kernels\n";
+    for (size_t i = 0; i < first.size(); ++i) {
+      auto v = times[i];
+      std::sort(v.begin(), v.end());
+      const double med = 1000.0 * v[v.size() / 2];
+      const int k = first[i].instr;
+      int64_t bi = 0, bo = 0;
+      std::string op = "fold_flush";
+      int let = -1, nk = 1;
+      if (k >= 0) {
+        const Instr& x = code_[size_t(k)];
+        for (auto& t : x.in) bi += nbytes_desc(t);
+        for (auto& t : x.out) bo += nbytes_desc(t);
+        op = x.op;
+        let = x.let;
+        nk = x.nkernels;
+      }
+      char buf[256];
+      std::snprintf(buf, sizeof buf, "%zu,%s,%d,%.3f,%lld,%lld,%d\n", i, op.c_str(), let, med, (long long)bi,
+                    (long long)bo, nk);
+      out += buf;
+    }
+    return out;
+  }
+
+ private:
   void enqueue(void* stream) {
     bool forked = false;
-    for (auto& x : code_) {
-      if (x.kind != OpKind::Launch || is_optimizer(x.op)) tcb_check(tcb_fold_flush(stream), "fold flush");
+    for (size_t xi = 0; xi < code_.size(); ++xi) {
+      auto& x = code_[xi];
+      if (x.kind != OpKind::Launch || is_optimizer(x.op)) flush_folds(stream);
       if (x.side) {
         if (!side_) {
           tcb_check(tcb_stream_create(&side_), "side stream");
@@ -508,6 +590,7 @@ class DeviceVM {
         forked = true;
         continue;
       }
+      void* pe0 = prof_ ? prof_rec(stream) : nullptr;
       switch (x.kind) {
         case OpKind::Launch:
           tcb_check(tcb_launch_ws(x.plan, x.in.data(), int(x.in.size()), x.out.data(), int(x.out.size()), ws_,
@@ -528,8 +611,9 @@ class DeviceVM {
           tcb_check(tcb_memcpy(x.out[0].ptr, x.in[0].ptr, uint64_t(x.copy_bytes), 2, stream), "copy_back");
           break;
       }
+      if (prof_) prof_->push_back({int(xi), pe0, prof_rec(stream)});
     }
-    tcb_check(tcb_fold_flush(stream), "fold flush");
+    flush_folds(stream);
     if (forked) {  // join: the step ends when the last optimizer chunk is done
       tcb_check(tcb_event_record(ev_join_, side_), "event record");
       tcb_check(tcb_stream_wait_event(stream, ev_join_), "stream wait");
@@ -546,6 +630,8 @@ class DeviceVM {
   void release() {
     for (void* e : ev_pool_) tcb_event_destroy(e);
     ev_pool_.clear();
+    for (void* e : prof_events_) tcb_event_destroy(e);
+    prof_events_.clear();
     if (ev_join_) tcb_event_destroy(ev_join_);
     ev_join_ = nullptr;
     if (side_) tcb_stream_destroy(side_);

@@ -73,6 +73,8 @@ def lib():
         L.tb_tnsr_load.argtypes = [ctypes.c_char_p, ctypes.c_void_p, ctypes.c_int64]
         L.tb_session_save_param.argtypes = [ctypes.c_void_p, ctypes.c_char_p, ctypes.c_char_p]
         L.tb_session_load_param.argtypes = [ctypes.c_void_p, ctypes.c_char_p, ctypes.c_char_p]
+        L.tb_session_profile.restype = ctypes.c_char_p
+        L.tb_session_profile.argtypes = [ctypes.c_void_p, ctypes.c_int]
         L.tb_memsched_text.restype = ctypes.c_char_p
         L.tb_memsched_text.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_int64, ctypes.c_int]
         _lib = L
@@ -328,6 +330,20 @@ class Session:
 
     def text(self, what: str) -> str:
         return lib().tb_session_text(self.h, what.encode()).decode()
+
+    def profile(self, repeats: int = 5) -> list[dict]:
+        """vm.profile: per-instruction median device time of
+        eager steps (CUDA events around every instruction and fold flush)."""
+        t = lib().tb_session_profile(self.h, repeats)
+        if t is None:
+            raise RuntimeError(lib().tb_last_error().decode())
+        rows = []
+        lines = t.decode().splitlines()
+        for line in lines[1:]:
+            i, op, let, us, bi, bo, k = line.split(",")
+            rows.append({"idx": int(i), "op": op, "let": int(let), "us": float(us), "bytes_in": int(bi),
+                         "bytes_out": int(bo), "kernels": int(k)})
+        return rows
 
     def set_comm(self, comm: int):
         _check(lib().tb_session_set_comm(self.h, comm))
