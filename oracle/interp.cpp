@@ -253,9 +253,9 @@ std::unique_ptr<Interp> make_interp(const std::string& cfg, int rank) {
   for (auto& p : ps) I->state.push_back(std::make_shared<std::vector<uint32_t>>(size_t(numel(p->ty.tensor())), 0u));
   // params (this rank's shard under ZeRO) / half copy from the shared
   // initialiser; m, v, step = 0
-  std::vector<float> p = init_params(I->ts);
-  const int64_t sh = int64_t(I->state[I->ts.i_params]->size());
-  std::memcpy(I->state[I->ts.i_params]->data(), p.data() + size_t(rank) * size_t(sh), size_t(sh) * 4);
+  std::vector<float> p = shard_of(I->ts, init_params(I->ts), rank);  // ZeRO: slice `rank` of every bucket
+  if (int64_t(p.size()) != int64_t(I->state[I->ts.i_params]->size())) throw Error("interp: shard size mismatch");
+  std::memcpy(I->state[I->ts.i_params]->data(), p.data(), p.size() * 4);
   if (I->ts.i_p16 >= 0) {
     const DType cd = I->ts.fn->params[I->ts.i_p16]->ty.tensor().dtype;
     for (size_t i = 0; i < p.size(); ++i) {

@@ -8,6 +8,7 @@
 #include <memory>
 #include <sstream>
 
+#include "distpar.hpp"
 #include "pipeline.hpp"
 #include "text_ext.hpp"
 #include "tnsr.hpp"
@@ -118,6 +119,9 @@ static void prepare(Session& s, const char* cfg_c) {
     fn = s.ts.fn;
   }
   if (do_schedule) fn = ir::make_fn(fn->name, fn->params, schedule(*fn, s.ts.state_binding));
+  // ZeRO: overlap_schedule -- every collective starts as soon
+  // as its bucket exists (the VM runs them on its comm stream)
+  if (s.cfg.zero_on()) fn = ir::make_fn(fn->name, fn->params, hoist_collectives(ir::flatten(*fn)));
   if (s.budget > 0) {
     auto [rf, plan] = rematerialize(*fn, s.budget, s.ts.state_binding);
     fn = rf;
@@ -168,6 +172,16 @@ const char* tb_graph_text(const char* cfg, const char* what) {
          << s.remat.peak_after << "\n";
       for (auto& sp : s.remat.splits)
         os << "split " << sp.victim << " " << sp.evict_index << " " << sp.replay_before << "\n";
+      g_text = os.str();
+    } else if (w == "buckets") {  // ZeRO buckets: "offset numel shard" per line
+      std::ostringstream os;
+      for (auto [o, n] : s.ts.buckets) os << o << " " << n << " " << (n + s.cfg.world - 1) / s.cfg.world << "\n";
+      g_text = os.str();
+    } else if (w == "timeline") {  // two-stream cost simulation of the step (distpar.hpp)
+      Timeline t = timeline(ir::flatten(*s.fn));
+      std::ostringstream os;
+      os << "serial " << t.serial << "\noverlap " << t.overlap << "\nevents " << t.events << "\ncollectives "
+         << t.collectives << "\n";
       g_text = os.str();
     } else if (w == "segments") {  // flat parameter layout: "name offset numel" per line
       std::ostringstream os;
@@ -242,10 +256,10 @@ int tb_session_info(void* h, int64_t* out, int n) {
 int tb_session_init_params(void* h) {
   TB_TRY({
     auto* s = static_cast<Session*>(h);
-    std::vector<float> p = init_params(s->ts);
-    const int64_t sh = s->cfg.world > 1 ? s->ts.shard() : s->ts.P_pad;
-    const float* mine = p.data() + size_t(s->cfg.world > 1 ? s->rank * sh : 0);
-    tcb_check(tcb_memcpy(s->vm.param_ptr(s->ts.i_params), mine, uint64_t(sh) * 4, 0, nullptr), "params");
+    // the rank's ZeRO shard (slice `rank` of every bucket), or all of it
+    std::vector<float> p = shard_of(s->ts, init_params(s->ts), s->rank);
+    const int64_t sh = int64_t(p.size());
+    tcb_check(tcb_memcpy(s->vm.param_ptr(s->ts.i_params), p.data(), uint64_t(sh) * 4, 0, nullptr), "params");
     if (s->ts.i_p16 >= 0) {
       const DType cd = s->ts.fn->params[s->ts.i_p16]->ty.tensor().dtype;
       if (cd == kF32) {
@@ -442,6 +456,15 @@ const char* tb_memsched_text(const char* text, const char* what, int64_t budget,
       os << "order";
       for (auto& b : sq.lets) os << " " << b.var->id;
       os << "\n" << print_text_ext(*f2);
+    } else if (w == "overlap") {  // hoist_collectives + timeline: per let "id stream start end wait"
+      LetSeq h = hoist_collectives(ir::flatten(*fn));
+      Timeline t = timeline(h);
+      os << "serial " << t.serial << "\noverlap " << t.overlap << "\nevents " << t.events << "\n";
+      for (size_t i = 0; i < h.lets.size(); ++i) {
+        const auto& e = t.ops[i];
+        os << "op " << h.lets[i].var->id << " " << e.stream << " " << e.start << " " << e.end << " "
+           << (e.wait_on >= 0 ? h.lets[size_t(e.wait_on)].var->id : std::string("-")) << "\n";
+      }
     } else if (w == "remat") {
       auto [f2, plan] = rematerialize(*fn, budget, {}, tr);
       os << "replays " << plan.replays << "\npeak_before " << plan.peak_before << "\npeak_after "

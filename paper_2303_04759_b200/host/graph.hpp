@@ -305,7 +305,8 @@ struct DepEntry {
 };
 
 struct GradResult {
-  VarPtr flat_grad;             // f32 [P] in leaf-offset order
+  VarPtr flat_grad;             // f32 [P] in leaf-offset order (null with make_flat=false)
+  std::vector<std::pair<int64_t, VarPtr>> parts;  // (flat offset, f32 piece): leaf grads and zero gaps
   size_t n_forward = 0;         // lets before the backward
   std::vector<DepEntry> deps;   // dependency_report, forward order
 };
@@ -313,7 +314,8 @@ struct GradResult {
 /// Reverse-mode AD of `loss` w.r.t. the leaves (which must tile [0, P) of the
 /// flat master buffer).  Appends the backward lets to `g` and returns the flat
 /// gradient var.
-inline GradResult autodiff(Graph& g, const VarPtr& loss, std::vector<Leaf> leaves, int64_t P) {
+inline GradResult autodiff(Graph& g, const VarPtr& loss, std::vector<Leaf> leaves, int64_t P,
+                           bool make_flat = true) {
   register_default_adjoints();
   LetSeq fwd = g.seq();  // snapshot of the forward lets
   std::unordered_map<const ir::Var*, VarPtr> grad;
@@ -402,6 +404,7 @@ inline GradResult autodiff(Graph& g, const VarPtr& loss, std::vector<Leaf> leave
   // leaf gradients -> one flat f32 buffer in offset order
   std::sort(leaves.begin(), leaves.end(), [](const Leaf& a, const Leaf& b) { return a.offset < b.offset; });
   std::vector<VarPtr> parts;
+  std::vector<std::pair<int64_t, VarPtr>> placed;
   int64_t pos = 0;
   auto zeros = [&](int64_t n) {
     return g.op("fill", {}, {{"shape", std::to_string(n)}, {"dtype", std::string("f32")}, {"value", 0.0}});
@@ -410,6 +413,7 @@ inline GradResult autodiff(Graph& g, const VarPtr& loss, std::vector<Leaf> leave
     if (lf.offset < pos) throw Error("autodiff: parameter leaves overlap");
     if (lf.offset > pos) {  // alignment gap
       parts.push_back(zeros(lf.offset - pos));
+      placed.push_back({pos, parts.back()});
       pos = lf.offset;
     }
     auto it = grad.find(lf.view.get());
@@ -420,12 +424,17 @@ inline GradResult autodiff(Graph& g, const VarPtr& loss, std::vector<Leaf> leave
       throw Error("autodiff: gradient of %" + lf.view->id + " has " + std::to_string(numel(d->ty.tensor())) +
                   " elements, the parameter " + std::to_string(lf.numel));
     parts.push_back(d);
+    placed.push_back({pos, d});
     pos += lf.numel;
   }
   if (pos > P) throw Error("autodiff: leaves exceed the flat buffer");
-  if (pos < P) parts.push_back(zeros(P - pos));
+  if (pos < P) {
+    parts.push_back(zeros(P - pos));
+    placed.push_back({pos, parts.back()});
+  }
   GradResult r;
-  r.flat_grad = g.op("concat", parts, {}, "grad");
+  if (make_flat) r.flat_grad = g.op("concat", parts, {}, "grad");
+  r.parts = std::move(placed);
   r.n_forward = fwd.lets.size();
   r.deps.assign(deps_rev.rbegin(), deps_rev.rend());
   return r;

@@ -31,6 +31,9 @@ struct ModelCfg {
   double ln_eps = 1e-12;
   int fuse = 1;             // run the fusion pass
   int save_deriv = 1;       // act linears save act'(u) for the backward instead of u
+  double bucket_mb = 25.0;  // ZeRO gradient bucket size (f32 MB; 0: one bucket per segment)
+  int zero = 0;             // force the ZeRO data plane at world 1 (identity collectives)
+  bool zero_on() const { return world > 1 || zero; }
   int64_t vocab_pad() const { return ((V + 63) / 64) * 64; }
   int64_t T() const { return B * S; }
   int64_t positions() const { return max_pos ? max_pos : (kind == "bert" ? std::max<int64_t>(512, S) : S); }
@@ -69,6 +72,8 @@ inline ModelCfg parse_cfg(const std::string& s) {
     else if (k == "ln_eps") c.ln_eps = D();
     else if (k == "fuse") c.fuse = int(I());
     else if (k == "save_deriv") c.save_deriv = int(I());
+    else if (k == "bucket_mb") c.bucket_mb = D();
+    else if (k == "zero") c.zero = int(I());
     else throw Error("unknown model config key '" + k + "'");
   }
   if (c.H % c.A) throw TypeError("H must be divisible by A");
@@ -94,7 +99,12 @@ struct TrainStep {
       i_step = -1, i_rng = -1;
   std::vector<std::pair<int, int>> state_binding;  // (ret index, param index): in-place state update
   FusionStats fusion;
-  int64_t shard() const { return P_pad / cfg.world; }
+  // ZeRO: gradient / parameter buckets (flat offset, numel) covering [0, P_pad);
+  // rank r owns slice r (ceil(numel / world) elements) of every bucket, and
+  // its shard state is the concatenation of those slices in bucket order
+  std::vector<std::pair<int64_t, int64_t>> buckets;
+  int64_t shard_n = 0;
+  int64_t shard() const { return shard_n ? shard_n : P_pad / cfg.world; }
 };
 
 class ParamTable {
@@ -171,6 +181,47 @@ inline ParamTable param_table(const ModelCfg& c) {
   return t;
 }
 
+/// horizontal_fuse_collectives.  The per-parameter
+/// collectives of partition_zero are merged into buckets
+/// BEFORE the shard layout is fixed (a rank's shard is a function of the
+/// bucket table, so merging afterwards would move elements between ranks):
+/// consecutive cut candidates (parameter segment starts, 64-element aligned)
+/// are merged greedily until a bucket holds >= bucket_elems; bucket_elems <= 0
+/// keeps one bucket per segment (no fusion).  Returns (offset, numel) buckets
+/// tiling [0, P).
+inline std::vector<std::pair<int64_t, int64_t>> hfuse_buckets(const std::vector<int64_t>& starts, int64_t P,
+                                                              int64_t bucket_elems) {
+  std::vector<std::pair<int64_t, int64_t>> out;
+  int64_t a = 0;
+  for (int64_t c : starts) {
+    if (c <= a || c >= P) continue;
+    if (c - a >= std::max<int64_t>(bucket_elems, 1)) {
+      out.push_back({a, c - a});
+      a = c;
+    }
+  }
+  if (P > a) out.push_back({a, P - a});
+  return out;
+}
+
+/// rank r's ZeRO shard of a flat [P_pad] vector: slice r of every bucket
+/// (zero padded to ceil(numel / world)), in bucket order -- what
+/// reduce_scatter delivers and all_gather reassembles.
+inline std::vector<float> shard_of(const TrainStep& ts, const std::vector<float>& full, int64_t rank) {
+  if (ts.buckets.empty()) return full;
+  const int64_t W = ts.cfg.world;
+  std::vector<float> out;
+  out.reserve(size_t(ts.shard()));
+  for (auto [o, n] : ts.buckets) {
+    const int64_t sh = (n + W - 1) / W;
+    for (int64_t j = 0; j < sh; ++j) {
+      const int64_t k = rank * sh + j;
+      out.push_back(k < n ? full[size_t(o + k)] : 0.0f);
+    }
+  }
+  return out;
+}
+
 /// Build the training step.  Inputs: ids, labels, pos_ids (+ type_ids for
 /// BERT), params (f32 master, sharded under ZeRO), [p16 (half copy, full)],
 /// [m, v (sharded), step].  Outputs: (loss, new states...) with in-place
@@ -188,7 +239,14 @@ inline TrainStep build_train_step(const ModelCfg& c) {
   const bool adam = c.opt == "adam";
   // a full compute copy of the parameters exists under AutoCast (bf16) and
   // under ZeRO (the master is sharded; the gathered copy feeds the forward)
-  const bool copy = amp || c.world > 1;
+  const bool zero = c.zero_on();
+  const bool copy = amp || zero;
+  if (zero) {
+    std::vector<int64_t> starts;
+    for (auto& sg : ts.segs) starts.push_back(sg.offset);
+    ts.buckets = hfuse_buckets(starts, ts.P_pad, int64_t(c.bucket_mb * 1e6 / 4.0));
+    for (auto [o, n] : ts.buckets) ts.shard_n += (n + c.world - 1) / c.world;
+  }
 
   Graph g;
   auto P = [&](const std::string& n, TensorType t) {
@@ -199,9 +257,12 @@ inline TrainStep build_train_step(const ModelCfg& c) {
   ts.i_labels = P("labels", {kI32, {T}});
   ts.i_pos = P("pos_ids", {kI32, {T}});
   if (c.kind == "bert") ts.i_type = P("type_ids", {kI32, {T}});
-  const int64_t pstate = c.world > 1 ? ts.shard() : ts.P_pad;
+  const int64_t pstate = zero ? ts.shard() : ts.P_pad;
   ts.i_params = P("params", {kF32, {pstate}});
-  if (copy) ts.i_p16 = P("p16", {act, {ts.P_pad}});
+  // the compute copy: full under AutoCast; under ZeRO the rank keeps its
+  // SHARD of it and the step all-gathers the full copy first (f32 steps
+  // gather the master shard itself)
+  if (amp) ts.i_p16 = P("p16", {act, {zero ? ts.shard() : ts.P_pad}});
   if (adam) {
     ts.i_m = P("m", {kF32, {pstate}});
     ts.i_v = P("v", {kF32, {pstate}});
@@ -213,7 +274,22 @@ inline TrainStep build_train_step(const ModelCfg& c) {
   auto par = [&](int i) { return g.params()[i]; };
   VarPtr rng_next = c.p > 0.0 ? g.op("add_scalar", {par(ts.i_rng)}, {{"value", 1.0}}, "rng") : nullptr;
   VarPtr ids = par(ts.i_ids), labels = par(ts.i_labels), pos_ids = par(ts.i_pos);
-  VarPtr wsrc = copy ? par(ts.i_p16) : par(ts.i_params);
+  VarPtr wsrc = amp ? par(ts.i_p16) : par(ts.i_params);
+  if (zero) {
+    // ZeRO-1 all-gather of the compute copy, one collective per bucket at the
+    // top of the step: the forward's first layers wait only for their own
+    // bucket, the rest of the gather overlaps the forward (comm stream)
+    VarPtr src = wsrc;
+    std::vector<VarPtr> full;
+    int64_t so = 0;
+    for (auto [o, n] : ts.buckets) {
+      const int64_t sh = (n + c.world - 1) / c.world;
+      VarPtr v = g.op("view", {src}, {{"offset", so}, {"shape", std::to_string(sh)}}, "psh");
+      full.push_back(g.op("all_gather", {v}, {{"world", c.world}, {"shape", std::to_string(n)}}, "pag"));
+      so += sh;
+    }
+    wsrc = full.size() == 1 ? full[0] : g.op("concat", full, {}, "pfull");
+  }
 
   std::vector<Leaf> leaves;
   std::map<std::string, VarPtr> W;
@@ -319,9 +395,9 @@ inline TrainStep build_train_step(const ModelCfg& c) {
   // ---- backward (autodiff) -> flat f32 gradient [P]
   // gaps between aligned segments and the tail up to P_pad get zero gradients
   // (SPEC.md:513,566 zero-padded shards)
-  GradResult gr = autodiff(g, loss, leaves, ts.P_pad);
+  GradResult gr = autodiff(g, loss, leaves, ts.P_pad, /*make_flat=*/!zero);
   VarPtr grad = gr.flat_grad;
-  if (numel(grad->ty.tensor()) != ts.P_pad)
+  if (grad && numel(grad->ty.tensor()) != ts.P_pad)
     throw Error("build_train_step: flat gradient has " + std::to_string(numel(grad->ty.tensor())) +
                 " elements, expected P_pad " + std::to_string(ts.P_pad));
 
@@ -329,16 +405,32 @@ inline TrainStep build_train_step(const ModelCfg& c) {
   std::vector<VarPtr> rets{loss};
   const std::string full_shape = std::to_string(ts.P_pad);
   VarPtr gsh = grad;
-  if (c.world > 1)  // sum-reduce-scatter of one flat bucket
-    gsh = g.op("reduce_scatter", {grad}, {{"world", c.world}});
+  if (zero) {
+    // one sum-reduce-scatter per bucket over the
+    // bucket's own gradient pieces -- so in the IR each collective depends
+    // only on its bucket and overlap_schedule can start it as soon as those
+    // pieces exist; the shard is the concatenation of the bucket shards
+    std::vector<VarPtr> shards;
+    size_t pi = 0;
+    for (auto [o, n] : ts.buckets) {
+      std::vector<VarPtr> pieces;
+      while (pi < gr.parts.size() && gr.parts[pi].first < o + n) {
+        if (gr.parts[pi].first < o) throw Error("ZeRO: a gradient piece straddles a bucket boundary");
+        pieces.push_back(gr.parts[pi++].second);
+      }
+      VarPtr gb = pieces.size() == 1 ? pieces[0] : g.op("concat", pieces, {}, "gbkt");
+      if (numel(gb->ty.tensor()) != n) throw Error("ZeRO: bucket pieces do not tile the bucket");
+      shards.push_back(g.op("reduce_scatter", {gb}, {{"world", c.world}}, "gsh"));
+    }
+    gsh = shards.size() == 1 ? shards[0] : g.op("concat", shards, {}, "gshard");
+  }
   if (!adam) {
     // mean over ranks folded into the step size: lr / N
     VarPtr np = g.op("sgd_update", {par(ts.i_params), gsh}, {{"lr", c.lr / double(c.world)}});
     rets.push_back(np);
     ts.state_binding.push_back({1, ts.i_params});
-    if (copy) {  // refresh the compute copy (cast, then gather under ZeRO)
-      VarPtr nh = amp ? g.op("convert", {np}, {{"to", c.dtype}}) : np;
-      if (c.world > 1) nh = g.op("all_gather", {nh}, {{"world", c.world}, {"shape", full_shape}});
+    if (amp) {  // refresh the compute copy (its shard under ZeRO: gathered next step)
+      VarPtr nh = g.op("convert", {np}, {{"to", c.dtype}});
       rets.push_back(nh);
       ts.state_binding.push_back({2, ts.i_p16});
     }
@@ -349,14 +441,12 @@ inline TrainStep build_train_step(const ModelCfg& c) {
                {"grad_scale", 1.0 / double(c.world)}, {"half", c.dtype}};
     VarPtr up = g.op("adam_update_ex", {par(ts.i_params), gsh, par(ts.i_m), par(ts.i_v), step1}, aa);
     VarPtr np = g.get(up, 0), nm = g.get(up, 1), nv = g.get(up, 2), nh = g.get(up, 3);
-    if (c.world > 1)
-      nh = g.op("all_gather", {nh}, {{"world", c.world}, {"shape", full_shape}});
     rets.insert(rets.end(), {np, nm, nv, step1});
     ts.state_binding.push_back({1, ts.i_params});
     ts.state_binding.push_back({2, ts.i_m});
     ts.state_binding.push_back({3, ts.i_v});
     ts.state_binding.push_back({4, ts.i_step});
-    if (copy) {
+    if (amp) {  // the bf16 compute copy (its shard under ZeRO: gathered next step)
       rets.push_back(nh);
       ts.state_binding.push_back({5, ts.i_p16});
     }

@@ -590,6 +590,11 @@ class DeviceVM {
         forked = true;
         continue;
       }
+      if (x.kind == OpKind::ReduceScatter || x.kind == OpKind::AllGather || x.kind == OpKind::AllReduce) {
+        enqueue_collective(x, stream);
+        continue;
+      }
+      wait_comm_hazards(x, stream);
       void* pe0 = prof_ ? prof_rec(stream) : nullptr;
       switch (x.kind) {
         case OpKind::Launch:
@@ -614,11 +619,94 @@ class DeviceVM {
       if (prof_) prof_->push_back({int(xi), pe0, prof_rec(stream)});
     }
     flush_folds(stream);
+    if (!inflight_.empty()) {  // join: the step ends when the last collective is done
+      tcb_check(tcb_stream_wait_event(stream, inflight_.back().done), "stream wait");
+      ++comm_waits_;
+      inflight_.clear();
+    }
+    comm_ev_used_ = 0;
     if (forked) {  // join: the step ends when the last optimizer chunk is done
       tcb_check(tcb_event_record(ev_join_, side_), "event record");
       tcb_check(tcb_stream_wait_event(stream, ev_join_), "stream wait");
     }
     ev_pool_used_ = 0;
+  }
+
+  // ---- the comm stream (distpar overlap_schedule) ----
+  // Collectives run on their own stream: each one waits for everything the
+  // compute stream enqueued before it (its inputs were hoisted right behind
+  // their producers by hoist_collectives), and a compute instruction waits on
+  // the latest in-flight collective whose buffers it touches (RAW on the
+  // collective's output, WAR on its input's arena space): one signal/wait
+  // pair per cross-stream edge.
+  struct Inflight {
+    void* done;
+    std::vector<std::pair<const char*, const char*>> ranges;
+  };
+  std::vector<Inflight> inflight_;
+  void* comm_stream_ = nullptr;
+  std::vector<void*> comm_ev_;
+  size_t comm_ev_used_ = 0;
+  int comm_waits_ = 0;
+  void* comm_event() {
+    if (comm_ev_used_ >= comm_ev_.size()) {
+      void* e = nullptr;
+      tcb_check(tcb_event_create(&e), "event");
+      comm_ev_.push_back(e);
+    }
+    return comm_ev_[comm_ev_used_++];
+  }
+  static std::pair<const char*, const char*> range_of(const tcb_tensor& t) {
+    const char* a = static_cast<const char*>(t.ptr);
+    return {a, a + nbytes_desc(t)};
+  }
+  void enqueue_collective(Instr& x, void* stream) {
+    flush_folds(stream);  // deferred gradient folds of this bucket land first
+    if (!comm_stream_) tcb_check(tcb_stream_create(&comm_stream_), "comm stream");
+    void* go = comm_event();
+    tcb_check(tcb_event_record(go, stream), "event record");
+    tcb_check(tcb_stream_wait_event(comm_stream_, go), "stream wait");
+    void* pe0 = prof_ ? prof_rec(comm_stream_) : nullptr;
+    switch (x.kind) {
+      case OpKind::ReduceScatter:
+        tcb_check(tcb_reduce_scatter(comm_, x.in.data(), int(x.in.size()), &x.out[0], comm_stream_), x.op);
+        break;
+      case OpKind::AllGather:
+        tcb_check(tcb_all_gather(comm_, &x.in[0], x.out.data(), int(x.out.size()), comm_stream_), x.op);
+        break;
+      default:
+        tcb_check(tcb_memcpy(x.out[0].ptr, x.in[0].ptr, uint64_t(nbytes_desc(x.in[0])), 2, comm_stream_), x.op);
+        tcb_check(tcb_all_reduce(comm_, &x.out[0], comm_stream_), x.op);
+        break;
+    }
+    if (prof_) prof_->push_back({int(&x - code_.data()), pe0, prof_rec(comm_stream_)});
+    Inflight f;
+    f.done = comm_event();
+    tcb_check(tcb_event_record(f.done, comm_stream_), "event record");
+    for (auto& t : x.in) f.ranges.push_back(range_of(t));
+    for (auto& t : x.out) f.ranges.push_back(range_of(t));
+    inflight_.push_back(std::move(f));
+  }
+  void wait_comm_hazards(const Instr& x, void* stream) {
+    if (inflight_.empty()) return;
+    int last = -1;
+    for (int k = int(inflight_.size()) - 1; k >= 0 && last < 0; --k)
+      for (auto& r : inflight_[size_t(k)].ranges) {
+        bool hit = false;
+        for (auto* ts : {&x.in, &x.out})
+          for (auto& t : *ts) {
+            auto q = range_of(t);
+            if (q.first < r.second && r.first < q.second) hit = true;
+          }
+        if (hit) {
+          last = k;
+          break;
+        }
+      }
+    if (last < 0) return;
+    tcb_check(tcb_stream_wait_event(stream, inflight_[size_t(last)].done), "stream wait");
+    ++comm_waits_;
+    inflight_.erase(inflight_.begin(), inflight_.begin() + last + 1);  // the comm stream is FIFO
   }
 
   static int64_t nbytes_desc(const tcb_tensor& t) {
@@ -632,6 +720,11 @@ class DeviceVM {
     ev_pool_.clear();
     for (void* e : prof_events_) tcb_event_destroy(e);
     prof_events_.clear();
+    for (void* e : comm_ev_) tcb_event_destroy(e);
+    comm_ev_.clear();
+    if (comm_stream_) tcb_stream_destroy(comm_stream_);
+    comm_stream_ = nullptr;
+    inflight_.clear();
     if (ev_join_) tcb_event_destroy(ev_join_);
     ev_join_ = nullptr;
     if (side_) tcb_stream_destroy(side_);

@@ -109,6 +109,8 @@ class ModelConfig:
     seed_drop: int = 7
     world: int = 1
     fuse: int = 1
+    bucket_mb: float = 25.0  # ZeRO gradient bucket (f32 MB; 0: one per parameter segment)
+    zero: int = 0            # ZeRO data plane at world 1 (identity collectives, comm stream)
     extra: dict = field(default_factory=dict)  # runtime keys: budget, schedule, rank
 
     def cfg_string(self, model_only: bool = False) -> str:

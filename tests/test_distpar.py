@@ -13,7 +13,7 @@ import numpy as np
 import pytest
 
 from oracle.interp_py import Interp, World
-from paper_2303_04759_b200.session import ModelConfig, graph_info, synthetic_batch
+from paper_2303_04759_b200.session import ModelConfig, graph_info, graph_text, synthetic_batch
 
 SMALL = dict(kind="bert", L=1, H=64, A=2, F=128, V=256, S=32, B=2, p=0.0)
 
@@ -35,12 +35,35 @@ def test_zero_partition_shapes(n):
     cn = graph_info(cfg(dtype="bf16", opt="adam", world=n))
     assert cn["P"] == c1["P"]
     assert cn["P_pad"] % (64 * n) == 0 and cn["P_pad"] >= cn["P"]
-    shard = cn["P_pad"] // n
-    assert shard == -(-cn["P_pad"] // n)  # ceil(total / N)
+    bk = buckets(cfg(dtype="bf16", opt="adam", world=n))
+    shard = sum(sh for _, _, sh in bk)
+    # every bucket is split into N equal slices of ceil(numel / N)
+    assert all(sh == -(-nb // n) for _, nb, sh in bk)
+    assert sum(nb for _, nb, _ in bk) == cn["P_pad"]
     # optimizer state (params, m, v) per rank is exactly one shard each
     full_state = c1["state_bytes"] - 3 * c1["P_pad"] * 4
     part_state = cn["state_bytes"] - 3 * shard * 4
-    assert part_state - full_state == (cn["P_pad"] - c1["P_pad"]) * 2  # only the bf16 copy grows with padding
+    # the bf16 compute copy is sharded too (all-gathered at the top of the step)
+    assert part_state - full_state == shard * 2 - c1["P_pad"] * 2
+
+
+def buckets(c: ModelConfig):
+    """ZeRO bucket table (offset, numel, shard) of the step graph"""
+    return [tuple(int(x) for x in line.split()) for line in graph_text(c, "buckets").splitlines()]
+
+
+def unshard(c: ModelConfig, shards, P_pad: int) -> np.ndarray:
+    """flat [P_pad] vector from the per-rank shards: rank r holds slice r of
+    every bucket, bucket after bucket"""
+    out = np.zeros(P_pad, shards[0].dtype)
+    so = 0
+    for o, n, sh in buckets(c):
+        for r, x in enumerate(shards):
+            k = min(sh, n - r * sh)
+            if k > 0:
+                out[o + r * sh:o + r * sh + k] = x[so:so + k]
+        so += sh
+    return out
 
 
 def _single_vs_world(c1: ModelConfig, cn: ModelConfig, n: int, steps: int):
@@ -53,8 +76,9 @@ def _single_vs_world(c1: ModelConfig, cn: ModelConfig, n: int, steps: int):
         lw.append(world.step(ids, labels))
     P = graph_info(c1)["P"]
     Pn = graph_info(cn)["P_pad"]
+    shard = sum(sh for _, _, sh in buckets(cn))
     p_single = single.read("params", P)
-    p_world = np.concatenate([world.read(r, "params", Pn // n) for r in range(n)])[:P]
+    p_world = unshard(cn, [world.read(r, "params", shard) for r in range(n)], Pn)[:P]
     return np.array(ls), np.array(lw), p_single, p_world, world
 
 
@@ -88,7 +112,8 @@ def test_bus_is_deterministic():
         w = World(cn.cfg_string(model_only=True), 3)
         ids, labels = batches(cn, 3, 7)
         w.step(ids, labels)
-        outs.append(np.concatenate([w.read(r, "params", graph_info(cn)["P_pad"] // 3) for r in range(3)]))
+        sh = sum(x for _, _, x in buckets(cn))
+        outs.append(np.concatenate([w.read(r, "params", sh) for r in range(3)]))
     assert np.array_equal(outs[0].view(np.uint32), outs[1].view(np.uint32))
 
 
@@ -128,7 +153,7 @@ def _gloo_rank(rank, world, port, cfg_string, steps, out_path):
     for k in range(steps):
         ids, labels = batches(c, world, k)
         losses.append(it.step(ids[rank], labels[rank], coll=coll))
-    shard = graph_info(c)["P_pad"] // world
+    shard = sum(sh for _, _, sh in buckets(c))
     np.save(out_path + f".{rank}.npy", np.concatenate([it.read("params", shard), np.array(losses, np.float32)]))
     dist.barrier()
     dist.destroy_process_group()
@@ -151,7 +176,7 @@ def test_gloo_two_process_matches_bus(tmp_path):
     for k in range(steps):
         ids, labels = batches(c, world, k)
         bl.append(bus.step(ids, labels))
-    shard = graph_info(c)["P_pad"] // world
+    shard = sum(sh for _, _, sh in buckets(c))
     for r in range(world):
         got = np.load(out + f".{r}.npy")
         ref = np.concatenate([bus.read(r, "params", shard), np.array([x[r] for x in bl], np.float32)])
