@@ -75,6 +75,7 @@ class ClockSampler:
             self.idx = gpu_index
         self.sm, self.reasons, self.mx = [], set(), None
         self.stop_ev = threading.Event()
+        self.active = threading.Event()  # samples are kept only while set (the timed regions)
         self.thread = None
         self.nvml = None
 
@@ -88,6 +89,9 @@ class ClockSampler:
         get_r = getattr(N, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
             getattr(N, "nvmlDeviceGetCurrentClocksThrottleReasons")
         while not self.stop_ev.is_set():
+            if not self.active.is_set():
+                time.sleep(0.001)
+                continue
             try:
                 self.sm.append(float(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)))
                 r = int(get_r(h))
@@ -399,35 +403,43 @@ def run_ours(args):
     if world > 1:
         s.set_comm(make_comm(world, rank))
     s.init_params()
-    ids, labels = synthetic_batch(cfg, seed=cfg.seed_d + rank)
+    # one global synthetic batch of B x world samples; each rank takes its shard
+    # ("every rank generates the global batch and takes its shard")
+    from paper_2303_04759_b200.session import ModelConfig
+    gcfg = ModelConfig.bert_base(B=cfg.B * world)
+    gids, glabels = synthetic_batch(gcfg)
+    ids, labels = gids[rank * cfg.T:(rank + 1) * cfg.T], glabels[rank * cfg.T:(rank + 1) * cfg.T]
     h_ids, h_lab = s.staging()
     h_ids[:] = ids
     h_lab[:] = labels
     s.set_batch_from_staging()
     stream = s.stream
+    clocks = ClockSampler(local)
+    clocks.start()  # NVML up before the timed regions; samples kept only inside them
     for _ in range(args.warmup):
         s.step(graph=True)
     s.sync()
     info = s.info()  # after the first capture: kernel count with deferred folds
     first_loss = s.loss()
 
-    clocks = ClockSampler(local)
-    clocks.start()
     # --- device-resident timed region
     ev = Events()
     barrier(world)
     s.sync()
+    clocks.active.set()
     ev.start(stream)
     for _ in range(args.steps):
         s.step(graph=True)
     ev.stop(stream)
     s.sync()
+    clocks.active.clear()
     barrier(world)
     ms = max_over_ranks(ev.ms() / args.steps, world)
     # --- end-to-end timed region: H2D batch + step + D2H loss every step
     ev2 = Events()
     barrier(world)
     s.sync()
+    clocks.active.set()
     ev2.start(stream)
     for _ in range(args.steps):
         s.set_batch_from_staging()
@@ -435,6 +447,7 @@ def run_ours(args):
         s.fetch_loss()
     ev2.stop(stream)
     s.sync()
+    clocks.active.clear()
     barrier(world)
     ms_e2e = max_over_ranks(ev2.ms() / args.steps, world)
     clk = clocks.stop()
