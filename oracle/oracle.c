@@ -646,6 +646,127 @@ static int attention_bwd(const orc_tensor* qkv, const orc_tensor* probs, const o
   return 0;
 }
 
+/* attention lse=1 (the flash kernels): exact f32 softmax P (no intermediate
+ * rounding), Pd = P keep / (1-p), ctx = round(Pd V); the second output is the
+ * per-row log-sum-exp of the scaled scores, lse = log sum_j exp(scale s_j)
+ * (causal: j <= i).  Keep bits of (z, i, j): Philox index (z*S + i)*S + j;
+ * mask (may be NULL): ceil(S/32) words per query row, word (z*S+i)*nw + j/32. */
+static int attention_fwd_lse(const orc_tensor* qkv, orc_tensor* ctx, orc_tensor* lse_t, orc_tensor* mask,
+                             const orc_attr* a, int na) {
+  attn_t at;
+  attn_heads(qkv, &at, a, na);
+  const int64_t S = at.S, dh = at.dh, H = at.H, H3 = 3 * at.H, nw = (S + 31) / 32;
+  const float* X = F(qkv);
+  float* C = F(ctx);
+  float* L = F(lse_t);
+  float* s = (float*)malloc(sizeof(float) * S);
+  float* pd = (float*)malloc(sizeof(float) * S * S);
+  const float sp = at.p > 0.0f ? 1.0f / (1.0f - at.p) : 1.0f;
+  for (int64_t b = 0; b < at.B; ++b)
+    for (int64_t h = 0; h < at.A; ++h) {
+      const int64_t z = b * at.A + h;
+      for (int64_t i = 0; i < S; ++i) {
+        float m = -INFINITY;
+        for (int64_t j = 0; j < S; ++j) {
+          float acc = 0.0f;
+          for (int64_t d = 0; d < dh; ++d)
+            acc += X[(b * S + i) * H3 + h * dh + d] * X[(b * S + j) * H3 + H + h * dh + d];
+          float v = acc * at.scale;
+          if (at.causal && j > i) v = -INFINITY;
+          s[j] = v;
+          if (v > m) m = v;
+        }
+        float sum = 0.0f;
+        for (int64_t j = 0; j < S; ++j) {
+          s[j] = expf(s[j] - m);
+          sum += s[j];
+        }
+        L[z * S + i] = m + logf(sum);
+        for (int64_t j = 0; j < S; ++j) {
+          const int keep = orc_dropout_keep(at.seed, at.salt, (uint64_t)((z * S + i) * S + j), at.p);
+          if (mask) {
+            uint32_t* mw = (uint32_t*)mask->ptr + (z * S + i) * nw + (j >> 5);
+            if ((j & 31) == 0) *mw = 0xffffffffu;
+            if (!keep) *mw &= ~(1u << (j & 31));
+          }
+          pd[i * S + j] = keep ? s[j] / sum * sp : 0.0f;
+        }
+      }
+      for (int64_t i = 0; i < S; ++i)
+        for (int64_t d = 0; d < dh; ++d) {
+          float acc = 0.0f;
+          for (int64_t j = 0; j < S; ++j) acc += pd[i * S + j] * X[(b * S + j) * H3 + 2 * H + h * dh + d];
+          C[(b * S + i) * H + h * dh + d] = rnd(at.dt, acc);
+        }
+    }
+  free(s);
+  free(pd);
+  return 0;
+}
+
+/* attention_dx lse=1 (qkv, ctx, lse, dctx [, mask]) -> dqkv: P recomputed
+ * from the scores and lse, D_i = sum_d dO O (O = the stored ctx), dP = keep
+ * (dO . V_j) / (1-p), dS = round(P (dP - D) scale), Pd = round(P keep / (1-p))
+ * (the MMA operands are activation-dtype tiles); dQ = dS K, dK = dS^T Q,
+ * dV = Pd^T dO, each rounded once. */
+static int attention_bwd_lse(const orc_tensor* qkv, const orc_tensor* ctx, const orc_tensor* lse_t,
+                             const orc_tensor* dctx, const orc_tensor* mask, orc_tensor* dqkv, const orc_attr* a,
+                             int na) {
+  attn_t at;
+  attn_heads(qkv, &at, a, na);
+  const int64_t S = at.S, dh = at.dh, H = at.H, H3 = 3 * at.H, nw = (S + 31) / 32;
+  const float* X = F(qkv);
+  const float* O = F(ctx);
+  const float* L = F(lse_t);
+  const float* dC = F(dctx);
+  float* dX = F(dqkv);
+  float* ds = (float*)malloc(sizeof(float) * S * S);
+  float* pd = (float*)malloc(sizeof(float) * S * S);
+  const float sp = at.p > 0.0f ? 1.0f / (1.0f - at.p) : 1.0f;
+  for (int64_t b = 0; b < at.B; ++b)
+    for (int64_t h = 0; h < at.A; ++h) {
+      const int64_t z = b * at.A + h;
+      for (int64_t i = 0; i < S; ++i) {
+        float D = 0.0f;
+        for (int64_t d = 0; d < dh; ++d) D += dC[(b * S + i) * H + h * dh + d] * O[(b * S + i) * H + h * dh + d];
+        for (int64_t j = 0; j < S; ++j) {
+          float acc = 0.0f, dpd = 0.0f;
+          for (int64_t d = 0; d < dh; ++d) {
+            acc += X[(b * S + i) * H3 + h * dh + d] * X[(b * S + j) * H3 + H + h * dh + d];
+            dpd += dC[(b * S + i) * H + h * dh + d] * X[(b * S + j) * H3 + 2 * H + h * dh + d];
+          }
+          const int valid = !(at.causal && j > i);
+          const float p = valid ? expf(acc * at.scale - L[z * S + i]) : 0.0f;
+          const uint64_t idx = (uint64_t)((z * S + i) * S + j);
+          const int keep = mask ? (int)((((const uint32_t*)mask->ptr)[(z * S + i) * nw + (j >> 5)] >> (j & 31)) & 1u)
+                                : orc_dropout_keep(at.seed, at.salt, idx, at.p);
+          const float dp = keep ? dpd * sp : 0.0f;
+          ds[i * S + j] = rnd(at.dt, p * (dp - D) * at.scale);
+          pd[i * S + j] = rnd(at.dt, keep ? p * sp : 0.0f);
+        }
+      }
+      for (int64_t i = 0; i < S; ++i)
+        for (int64_t d = 0; d < dh; ++d) {
+          float acc = 0.0f;
+          for (int64_t j = 0; j < S; ++j) acc += ds[i * S + j] * X[(b * S + j) * H3 + H + h * dh + d];
+          dX[(b * S + i) * H3 + h * dh + d] = rnd(at.dt, acc);
+        }
+      for (int64_t j = 0; j < S; ++j)
+        for (int64_t d = 0; d < dh; ++d) {
+          float acck = 0.0f, accv = 0.0f;
+          for (int64_t i = 0; i < S; ++i) {
+            acck += ds[i * S + j] * X[(b * S + i) * H3 + h * dh + d];
+            accv += pd[i * S + j] * dC[(b * S + i) * H + h * dh + d];
+          }
+          dX[(b * S + j) * H3 + H + h * dh + d] = rnd(at.dt, acck);
+          dX[(b * S + j) * H3 + 2 * H + h * dh + d] = rnd(at.dt, accv);
+        }
+    }
+  free(ds);
+  free(pd);
+  return 0;
+}
+
 /* ------------------------------------------------------------- layernorm */
 /* Row statistics: left-to-right f32 sums; mean = sum * (1/H); two-pass
  * variance; rstd = 1/sqrtf(var + eps). */
@@ -1143,6 +1264,14 @@ int orc_exec(const char* op, const orc_tensor* in, int nin, orc_tensor* out, int
       for (int64_t j = 0; j < C; ++j) F(&out[0])[r * C + j] = rnd(out[0].dtype, y[j] * (dy[j] - dot) * scale);
     }
     return 0;
+  }
+  if (!strcmp(op, "attention") && aint(A, na, "lse", 0)) {
+    NEED(1, 2);
+    return attention_fwd_lse(&in[0], &out[0], &out[1], nout > 2 ? &out[2] : NULL, A, na);
+  }
+  if (!strcmp(op, "attention_dx") && aint(A, na, "lse", 0)) {
+    NEED(4, 1);
+    return attention_bwd_lse(&in[0], &in[1], &in[2], &in[3], nin > 4 ? &in[4] : NULL, &out[0], A, na);
   }
   if (!strcmp(op, "attention")) {
     NEED(1, 2);

@@ -87,6 +87,14 @@ void launch_attn_fwd(const void* qkv, void* ctx, void* probs, int64_t B, int64_t
 void launch_attn_bwd(const void* qkv, const void* probs, const void* dctx, void* dqkv, int64_t B, int64_t S, int64_t H,
                      int64_t A, float scale, int causal, const DropCfg& d, cudaStream_t s);
 
+// Flash attention (k_flash.cu): any seq % 8 == 0, head dim 64, bf16; saves lse
+bool flash_ok(int dt, int64_t S, int64_t H, int64_t A);
+void launch_flash_fwd(const void* qkv, void* ctx, float* lse, int64_t B, int64_t S, int64_t H, int64_t A,
+                      float scale, int causal, const DropCfg& d, cudaStream_t s);
+void launch_flash_bwd(const void* qkv, const void* ctx, const float* lse, const void* dctx, void* dqkv,
+                      float* dq_ws, int64_t B, int64_t S, int64_t H, int64_t A, float scale, int causal,
+                      const DropCfg& d, cudaStream_t s);
+
 // Picks the kernel: tcgen05 for f16/bf16 operands unless exact is requested or
 // the shape is unsupported (then the exact SIMT kernel; never a CPU path).
 inline void launch_gemm(const GemmArgs& g, bool exact, cudaStream_t s) {

@@ -1160,7 +1160,7 @@ struct AttnGeom {
   bool exact;
 };
 
-static AttnGeom attn_geom(const Plan& p) {
+static AttnGeom attn_geom(const Plan& p, bool any_len = false) {
   const Spec& X = p.in[0];
   require(X.rank == 2 && X.shape[1] % 3 == 0, p.op + ": qkv must be [T, 3H]");
   AttnGeom g;
@@ -1169,7 +1169,7 @@ static AttnGeom attn_geom(const Plan& p) {
   g.S = p.attrs.i("seq", X.shape[0]);
   require(g.A >= 1 && g.H % g.A == 0, p.op + ": heads must divide H");
   require(g.S >= 1 && X.shape[0] % g.S == 0, p.op + ": seq must divide T");
-  require(g.S <= SM_MAXV * 32, p.op + ": seq > 1024 unsupported");
+  require(any_len || g.S <= SM_MAXV * 32, p.op + ": seq > 1024 unsupported");
   g.B = X.shape[0] / g.S;
   g.dh = g.H / g.A;
   g.Z = g.B * g.A;
@@ -1231,8 +1231,53 @@ static void set_c(GemmArgs& r, void* c, int64_t ld, int64_t s1, int64_t s2, int 
   r.c_dtype = dt;
 }
 
+// attention(qkv) {lse=1} -> (ctx [T,H], lse f32 [Z*S] [, keep bits i32 [Z*S*ceil(S/32)]]):
+// the flash kernels of k_flash.cu (any S % 8 == 0, head dim 64, bf16)
+static void b_attention_lse(Plan& p) {
+  check_arity(p, 1, 1, 2, 3);
+  const AttnGeom g = attn_geom(p, true);
+  if (!flash_ok(g.dt, g.S, g.H, g.A) || g.exact)
+    fail(TCB_ERR_UNIMPLEMENTED, "attention lse=1: needs bf16, head dim 64, seq % 8 == 0");
+  require(p.out[0].numel() == g.B * g.S * g.H && p.out[0].dtype == g.dt, "attention: ctx must be [T, H]");
+  require(p.out[1].numel() == g.Z * g.S && p.out[1].dtype == TCB_F32, "attention lse=1: lse must be f32 [B*A*S]");
+  const bool save_mask = p.out.size() > 2;
+  const int64_t nw = (g.S + 31) / 32;
+  if (save_mask)
+    require(g.d.p > 0.0f && p.out[2].numel() * dtype_bytes(p.out[2].dtype) >= g.Z * g.S * nw * 4,
+            "attention: save_mask needs p > 0 and ceil(S/32) words per query row");
+  p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
+    DropCfg d = with_step(g.d);
+    if (save_mask) d.mask_out = static_cast<uint8_t*>(out[2].ptr);
+    launch_flash_fwd(in[0].ptr, out[0].ptr, static_cast<float*>(out[1].ptr), g.B, g.S, g.H, g.A, g.scale,
+                     g.causal, d, s);
+  };
+}
+
+// attention_dx(qkv, ctx, lse, dctx [, keep bits]) {lse=1} -> dqkv
+static void b_attention_dx_lse(Plan& p) {
+  check_arity(p, 4, 5, 1, 1);
+  const AttnGeom g = attn_geom(p, true);
+  if (!flash_ok(g.dt, g.S, g.H, g.A) || g.exact)
+    fail(TCB_ERR_UNIMPLEMENTED, "attention_dx lse=1: needs bf16, head dim 64, seq % 8 == 0");
+  require(p.in[1].numel() == g.B * g.S * g.H && p.in[1].dtype == g.dt, "attention_dx: ctx must be [T, H]");
+  require(p.in[2].numel() == g.Z * g.S && p.in[2].dtype == TCB_F32, "attention_dx: lse must be f32 [B*A*S]");
+  require(p.in[3].numel() == g.B * g.S * g.H && p.in[3].dtype == g.dt, "attention_dx: dctx must be [T, H]");
+  require(p.out[0].numel() == p.in[0].numel(), "attention_dx: dqkv must be [T, 3H]");
+  const bool mask_in = p.in.size() > 4;
+  const int64_t nt = (g.S + 127) / 128;
+  const size_t dq = p.ws_take(nt > 1 ? size_t(g.B * g.S * g.H) * sizeof(float) : 0);
+  p.nkernels = nt > 1 ? 2 : 1;  // (+ a memset node) the dQ f32 -> bf16 store
+  p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
+    DropCfg d = with_step(g.d);
+    if (mask_in) d.mask_in = static_cast<const uint8_t*>(in[4].ptr);
+    launch_flash_bwd(in[0].ptr, in[1].ptr, static_cast<const float*>(in[2].ptr), in[3].ptr, out[0].ptr,
+                     nt > 1 ? static_cast<float*>(ws_at(dq)) : nullptr, g.B, g.S, g.H, g.A, g.scale, g.causal, d, s);
+  };
+}
+
 // attention(qkv) -> (ctx [T,H], probs [Z*S, S])
 static void b_attention(Plan& p) {
+  if (p.attrs.i("lse", 0)) return b_attention_lse(p);
   check_arity(p, 1, 1, 2, 3);
   const AttnGeom g = attn_geom(p);
   require(p.out[0].numel() == g.B * g.S * g.H, "attention: ctx must be [T, H]");
@@ -1286,6 +1331,7 @@ TCB_REGISTER("attention", b_attention);
 
 // attention_dx(qkv, probs, dctx) -> dqkv [T, 3H]
 static void b_attention_dx(Plan& p) {
+  if (p.attrs.i("lse", 0)) return b_attention_dx_lse(p);
   check_arity(p, 3, 4, 1, 1);
   const AttnGeom g = attn_geom(p);
   require(p.out[0].numel() == p.in[0].numel(), "attention_dx: dqkv must be [T, 3H]");

@@ -224,6 +224,14 @@ inline void register_extension_ops(OpRegistry& r) {
     int64_t H = q.shape[1] / 3, A = rel::a_int(a, "heads", 1), S = rel::a_int(a, "seq", q.shape[0]);
     if (q.shape[1] % 3 || H % A || q.shape[0] % S) throw TypeError("attention: bad qkv/heads/seq");
     int64_t B = q.shape[0] / S;
+    if (rel::a_int(a, "lse", 0)) {
+      // lse=1 (flash): (ctx, per-row log-sum-exp f32 [B*A*S] [, keep bits,
+      // ceil(S/32) i32 words per query row])
+      TupleType t{{TensorType{q.dtype, {q.shape[0], H}}, TensorType{kF32, {B * A * S}}}};
+      if (rel::a_int(a, "save_mask", 0) && ir::attr_double(a, "p", 0.0) > 0.0)
+        t.fields.push_back(TensorType{kI32, {B * A * S * ((S + 31) / 32)}});
+      return t;
+    }
     TupleType t{{TensorType{q.dtype, {q.shape[0], H}}, TensorType{q.dtype, {B * A * S, S}}}};
     // save_mask (p > 0): the dropout keep bits, 4 i32 words per query row (S <= 128)
     if (rel::a_int(a, "save_mask", 0) && ir::attr_double(a, "p", 0.0) > 0.0) {
@@ -233,7 +241,12 @@ inline void register_extension_ops(OpRegistry& r) {
     return t;
   });
   // attention_dx(qkv, probs, dctx [, saved keep bits]) -> dqkv
-  reg("attention_dx", -1, O, [](const V& in, const AttrMap&) -> Type {
+  // lse=1: attention_dx(qkv, ctx, lse, dctx [, keep bits]) -> dqkv
+  reg("attention_dx", -1, O, [](const V& in, const AttrMap& a) -> Type {
+    if (rel::a_int(a, "lse", 0)) {
+      if (in.size() != 4 && in.size() != 5) throw TypeError("attention_dx lse=1: (qkv, ctx, lse, dctx [, mask])");
+      return rel::T(in[0], "attention_dx");
+    }
     if (in.size() != 3 && in.size() != 4) throw TypeError("attention_dx: (qkv, probs, dctx [, mask])");
     return rel::T(in[0], "attention_dx");
   });

@@ -245,6 +245,11 @@ inline void register_default_adjoints() {
   A["attention"] = [](AdjointCtx& c) -> std::vector<VarPtr> {
     if (!c.dout[0]) return {nullptr};
     auto qkv = arg_var(c.let.value, 0);
+    if (ir::attr_int(c.let.value->call_attrs, "lse", 0)) {  // flash: P recomputed from (ctx, lse)
+      std::vector<VarPtr> args{qkv, c.g.get(c.let.var, 0), c.g.get(c.let.var, 1), c.dout[0]};
+      if (c.let.var->ty.tuple().fields.size() > 2) args.push_back(c.g.get(c.let.var, 2));
+      return {c.g.op("attention_dx", args, c.let.value->call_attrs)};
+    }
     VarPtr probs = c.g.get(c.let.var, 1);
     std::vector<VarPtr> args{qkv, probs, c.dout[0]};
     if (c.let.var->ty.tuple().fields.size() > 2) args.push_back(c.g.get(c.let.var, 2));  // saved keep bits

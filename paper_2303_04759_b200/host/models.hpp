@@ -33,6 +33,7 @@ struct ModelCfg {
   int save_deriv = 1;       // act linears save act'(u) for the backward instead of u
   double bucket_mb = 25.0;  // ZeRO gradient bucket size (f32 MB; 0: one bucket per segment)
   int zero = 0;             // force the ZeRO data plane at world 1 (identity collectives)
+  int flash = 1;            // bf16 attention: flash kernels (lse saved) instead of the stored-P path
   bool zero_on() const { return world > 1 || zero; }
   int64_t vocab_pad() const { return ((V + 63) / 64) * 64; }
   int64_t T() const { return B * S; }
@@ -74,6 +75,7 @@ inline ModelCfg parse_cfg(const std::string& s) {
     else if (k == "save_deriv") c.save_deriv = int(I());
     else if (k == "bucket_mb") c.bucket_mb = D();
     else if (k == "zero") c.zero = int(I());
+    else if (k == "flash") c.flash = int(I());
     else throw Error("unknown model config key '" + k + "'");
   }
   if (c.H % c.A) throw TypeError("H must be divisible by A");
@@ -319,8 +321,11 @@ inline TrainStep build_train_step(const ModelCfg& c) {
     return y->ty.is_tuple() ? g.get(y, 0) : y;
   };
   AttrMap attn_attrs{{"heads", c.A}, {"seq", c.S}, {"causal", std::int64_t(c.kind == "gpt2")}};
-  // the fused attention saves its dropout keep bits for the backward
-  if (c.p > 0.0 && c.dtype == "bf16" && c.H / c.A == 64 && c.S <= 128 && c.S % 8 == 0)
+  // bf16, head dim 64: the flash kernels (any S % 8 == 0) keep only the
+  // per-row log-sum-exp for the backward (not P), and the dropout keep bits
+  const bool flash = c.dtype == "bf16" && c.H / c.A == 64 && c.S % 8 == 0 && c.flash;
+  if (flash) attn_attrs["lse"] = std::int64_t(1);
+  if (c.p > 0.0 && c.dtype == "bf16" && c.H / c.A == 64 && c.S % 8 == 0 && (flash || c.S <= 128))
     attn_attrs["save_mask"] = std::int64_t(1);
   // residual LayerNorms save their dropout keep bits for the backward (no Philox re-run)
   auto ln_attrs = [&]() {

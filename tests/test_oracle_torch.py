@@ -262,3 +262,31 @@ def test_dropout_rate_and_scale(p):
     rate = kept.mean()
     sigma = np.sqrt(p * (1 - p) / n)
     assert abs(rate - (1 - p)) < 4 * sigma, rate
+
+
+@pytest.mark.parametrize("seed", SEEDS[:3])
+@pytest.mark.parametrize("p,causal,S", [(0.0, 0, 12), (0.25, 0, 12), (0.0, 1, 40), (0.25, 1, 40)])
+def test_attention_lse_fwd_bwd_vs_torch(seed, p, causal, S):
+    """attention lse=1 (the flash formulation): ctx and the per-row
+    log-sum-exp vs torch; attention_dx(qkv, ctx, lse, dctx) vs torch autograd
+    (f32: the dS / Pd roundings are identities)."""
+    rng = np.random.default_rng(seed)
+    B, A, dh = 2, 3, 8
+    H, T = A * dh, B * S
+    qkv, dctx = rn(rng, T, 3 * H, lo=-2, hi=2), rn(rng, T, H)
+    at = {"heads": A, "seq": S, "p": p, "seed": 21 + seed, "salt": 4, "causal": causal, "lse": 1}
+    ctx, lse = O.run("attention", [qkv], [((T, H), F32), ((B * A * S,), F32)], at)
+    keep = O.dropout_keep_mask(21 + seed, 4, B * A * S * S, p).reshape(B, A, S, S).astype(np.float64)
+    qt = t64(qkv, True)
+    ct, pt = torch_attention(qt, B, S, A, p, t64(keep), causal)
+    assert rel(ctx, ct.detach()) < 1e-5
+    q_, k_ = qt.detach()[:, :H], qt.detach()[:, H:2 * H]
+    sh = lambda t: t.reshape(B, S, A, dh).permute(0, 2, 1, 3)  # noqa: E731
+    sc = sh(q_) @ sh(k_).transpose(-1, -2) / np.sqrt(dh)
+    if causal:
+        sc = sc.masked_fill(torch.triu(torch.ones(S, S, dtype=torch.bool), 1), float("-inf"))
+    assert rel(lse, torch.logsumexp(sc, -1).reshape(-1)) < 1e-6
+    ct.backward(t64(dctx))
+    (dqkv,) = O.run("attention_dx", [qkv, ctx, lse, dctx], [((T, 3 * H), F32)], at)
+    # D uses the stored (f32) ctx: exact here
+    assert rel(dqkv, qt.grad) < 1e-4, rel(dqkv, qt.grad)
