@@ -205,7 +205,9 @@ __global__ void __launch_bounds__(FA_FWD_THREADS) k_flash_fwd(const __grid_const
       w.w = pack_bf2(pd[6], pd[7]);
       *reinterpret_cast<uint4*>(tileP + sw128(row, g0 + g)) = w;
     }
-    if (j > 0 && alpha != 1.0f) {  // O *= alpha (this thread's 16 of the row's 64 columns)
+    // O *= alpha (this thread's 16 of the row's 64 columns); tcgen05.ld/st are
+    // warp-collective, so the skip test must be warp-uniform
+    if (j > 0 && __any_sync(0xffffffffu, alpha != 1.0f)) {
       uint32_t r[16];
       TMEM_LD16(trow + 128 + cq * 16, r);
       tmem_wait_ld();
