@@ -33,7 +33,7 @@ struct ModelCfg {
   int save_deriv = 1;       // act linears save act'(u) for the backward instead of u
   double bucket_mb = 25.0;  // ZeRO gradient bucket size (f32 MB; 0: one bucket per segment)
   int zero = 0;             // force the ZeRO data plane at world 1 (identity collectives)
-  int flash = 1;            // bf16 attention: flash kernels (lse saved) instead of the stored-P path
+  int flash = 1;            // bf16 attention: flash kernels (lse saved) for S > 128; 2: always; 0: never
   bool zero_on() const { return world > 1 || zero; }
   int64_t vocab_pad() const { return ((V + 63) / 64) * 64; }
   int64_t T() const { return B * S; }
@@ -321,9 +321,12 @@ inline TrainStep build_train_step(const ModelCfg& c) {
     return y->ty.is_tuple() ? g.get(y, 0) : y;
   };
   AttrMap attn_attrs{{"heads", c.A}, {"seq", c.S}, {"causal", std::int64_t(c.kind == "gpt2")}};
-  // bf16, head dim 64: the flash kernels (any S % 8 == 0) keep only the
-  // per-row log-sum-exp for the backward (not P), and the dropout keep bits
-  const bool flash = c.dtype == "bf16" && c.H / c.A == 64 && c.S % 8 == 0 && c.flash;
+  // bf16, head dim 64, S > 128: the flash kernels keep only the per-row
+  // log-sum-exp for the backward (not P), and the dropout keep bits.  At
+  // S <= 128 the persistent stored-P kernels are faster (BERT-base step 6.16k
+  // vs 6.05k samples/s measured with flash; flash=2 forces it there)
+  const bool flash = c.dtype == "bf16" && c.H / c.A == 64 && c.S % 8 == 0 &&
+                     ((c.flash == 1 && c.S > 128) || c.flash == 2);
   if (flash) attn_attrs["lse"] = std::int64_t(1);
   if (c.p > 0.0 && c.dtype == "bf16" && c.H / c.A == 64 && c.S % 8 == 0 && (flash || c.S <= 128))
     attn_attrs["save_mask"] = std::int64_t(1);

@@ -111,7 +111,7 @@ class ModelConfig:
     fuse: int = 1
     bucket_mb: float = 25.0  # ZeRO gradient bucket (f32 MB; 0: one per parameter segment)
     zero: int = 0            # ZeRO data plane at world 1 (identity collectives, comm stream)
-    flash: int = 1           # bf16 attention via the flash kernels (lse saved, any S % 8 == 0)
+    flash: int = 1           # bf16 attention via the flash kernels (lse saved): 1 for S > 128, 2 always, 0 never
     extra: dict = field(default_factory=dict)  # runtime keys: budget, schedule, rank
 
     def cfg_string(self, model_only: bool = False) -> str:

@@ -52,10 +52,18 @@ def test_flash_fwd_bwd_vs_oracle(S, causal, p):
         nw = (S + 31) // 32
         at_m = {**at, "save_mask": 1}
         g, o = run_both("attention", [(qkv, BF16)], outs + [((B * A * S * nw,), I32)], at_m)
-        assert np.array_equal(g[2], o[2])
+        # causal: a query tile never visits the key tiles past its diagonal, so
+        # their words are not written (and never read by the backward)
+        rows = np.arange(B * A * S) % S
+        words = np.arange(nw)
+        used = (words[None, :] * 32 // 128 <= rows[:, None] // 128) if causal else np.ones((B * A * S, nw), bool)
+        gw, ow = g[2].reshape(B * A * S, nw), o[2].reshape(B * A * S, nw)
+        assert np.array_equal(gw[used], ow[used])
         keep = np.unpackbits(g[2].view(np.uint8), bitorder="little").reshape(B * A * S, nw * 32)[:, :S]
         ref = O.dropout_keep_mask(5, 11, B * A * S * S, p).reshape(B * A * S, S)
-        assert np.array_equal(keep, ref)
+        cols = np.arange(S)
+        kused = (cols[None, :] // 128 <= rows[:, None] // 128) if causal else np.ones((B * A * S, S), bool)
+        assert np.array_equal(keep[kused], ref[kused])
         gm, _ = run_both("attention_dx", ins + [(g[2], I32)], [((T, 3 * H), BF16)], at_m)
         g0, _ = run_both("attention_dx", ins, [((T, 3 * H), BF16)], at)
         assert np.array_equal(gm[0], g0[0])
