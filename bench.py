@@ -238,12 +238,12 @@ def gemm_roofline(stream, peaks, iters=50):
             "kernel": f"b200.linear tcgen05 {M}x{K}x{N} bf16 (+bias+gelu, act' saved)", "us_per_launch": round(ms * 1e3, 2)}
 
 
-def _verify_step(batch: int, budget: int):
-    """One untimed + one timed (CUDA events) BERT-base step at `batch` under the
-    remat budget; returns (ms, loss)."""
+def _verify_step(batch: int, budget: int, factory=None):
+    """One untimed + one timed (CUDA events) step of `factory` (BERT-base by
+    default) at `batch` under the remat budget; returns (ms, loss)."""
     import torch
     from paper_2303_04759_b200.session import ModelConfig, Session, cache_clear, synthetic_batch
-    cfg = ModelConfig.bert_base(B=batch)
+    cfg = (factory or ModelConfig.bert_base)(B=batch)
     cfg.extra["schedule"] = 1  # p-c list schedule first (SPEC.md:459-466): -0.26% peak at B~3k
     cfg.extra["budget"] = budget
     s = Session(cfg)
@@ -308,6 +308,44 @@ def max_batch_report(stream_sync_free_bytes: int):
         out["refused"] = attempts
     out["max_batch"] = out.get("verified_batch", b_remat) if out.get("verified_on_gpu") else b_remat
     out["planner_max_batch"] = b_remat
+    return out
+
+
+def c3_report(free_bytes: int):
+    """BASELINE configs[2] (C3): GPT-2 medium (345M) causal LM, S = 512, bf16
+    Adam, dropout 0.1 (flash attention: lse saved, P recomputed) -- the largest
+    trainable batch under rematerialisation (planner: doubling + bisection
+    under the device budget) and without it, then ONE
+    verified GPU step at the found batch (timed with CUDA events)."""
+    import torch
+    from paper_2303_04759_b200.session import ModelConfig, cache_clear, max_batch_under_remat
+    cache_clear()
+    budget = int(free_bytes * 0.92) - (2 << 30)
+    reserve = 512 * 6656
+    b_remat, gi = max_batch_under_remat(ModelConfig.gpt2_medium, budget, b0=8, reserve_per_sample=reserve)
+    b_plain, _ = max_batch_under_remat(ModelConfig.gpt2_medium, budget, b0=8, remat=False,
+                                       reserve_per_sample=reserve)
+    out = {"model": "gpt2-medium (L24 H1024 A16 F4096 V50257) seq512 causal bf16 Adam, flash attention",
+           "budget_gb": round(budget / 1e9, 1), "max_batch": b_remat, "max_batch_no_remat": b_plain,
+           "remat_replays": gi.get("remat_replays"), "planner_max_batch": b_remat}
+    b, attempts = b_remat, []
+    for _ in range(4):
+        try:
+            ms, loss = _verify_step(b, budget, ModelConfig.gpt2_medium)
+            out.update({"verified_on_gpu": bool(np.isfinite(loss)), "verified_batch": b, "step_ms": round(ms, 1),
+                        "samples_per_s": round(b / (ms * 1e-3), 2), "tokens_per_s": round(b * 512 / (ms * 1e-3)),
+                        "loss": round(loss, 4)})
+            break
+        except Exception as e:
+            attempts.append({"batch": b, "error": str(e)[:160]})
+            cache_clear()
+            torch.cuda.empty_cache()
+            b = int(b * 0.985)
+    else:
+        out["verified_on_gpu"] = False
+    if attempts:
+        out["refused"] = attempts
+    out["max_batch"] = out.get("verified_batch", b_remat) if out.get("verified_on_gpu") else b_remat
     return out
 
 
@@ -503,6 +541,9 @@ def run_ours(args):
         import torch
         free, total = torch.cuda.mem_get_info()
         out["config"]["max_batch_under_remat"] = max_batch_report(free)
+        torch.cuda.empty_cache()
+        free, total = torch.cuda.mem_get_info()
+        out["config"]["c3_gpt2_medium_max_batch_under_remat"] = c3_report(free)
     if world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline_port()
     print(json.dumps(out), flush=True)
