@@ -82,10 +82,11 @@ void gemm_prepare(GemmArgs& g, bool exact, GemmWs& keep);
 
 // Fused short-sequence attention (k_attention.cu): bf16, head dim 64, S <= 128
 bool attn_fused_ok(int dt, int64_t S, int64_t H, int64_t A, bool exact);
+// lse != nullptr: lse mode (no P stored / loaded; per-row log-sum-exp written / read)
 void launch_attn_fwd(const void* qkv, void* ctx, void* probs, int64_t B, int64_t S, int64_t H, int64_t A, float scale,
-                     int causal, const DropCfg& d, cudaStream_t s, void* trace = nullptr);
+                     int causal, const DropCfg& d, cudaStream_t s, void* trace = nullptr, float* lse = nullptr);
 void launch_attn_bwd(const void* qkv, const void* probs, const void* dctx, void* dqkv, int64_t B, int64_t S, int64_t H,
-                     int64_t A, float scale, int causal, const DropCfg& d, cudaStream_t s);
+                     int64_t A, float scale, int causal, const DropCfg& d, cudaStream_t s, const float* lse = nullptr);
 
 // Flash attention (k_flash.cu): any seq % 8 == 0, head dim 64, bf16; saves lse
 bool flash_ok(int dt, int64_t S, int64_t H, int64_t A);

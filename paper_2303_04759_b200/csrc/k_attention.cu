@@ -35,6 +35,11 @@ struct AttnArgs {
   unsigned long long* trace;
   float scale;
   DropCfg d;
+  // lse mode (attention lse=1): the forward writes the per-row log-sum-exp
+  // instead of storing P; the backward recomputes P = 2^(S log2e scale - lse
+  // log2e) from a QK^T MMA instead of loading it
+  float* lse_out;
+  const float* lse_in;
 };
 
 // byte offset of granule g (8 bf16) of row r in a [128 rows x 128 B] SW128 tile
@@ -219,7 +224,12 @@ __global__ void __launch_bounds__(AT_FWD_THREADS) k_attn_fwd(const __grid_consta
     fence_proxy_async();
     __syncthreads();
     T(3);
-    if (tid == 0) {
+    if (a.lse_out) {  // lse mode: no P store; the row's log-sum-exp instead
+      if (cq == 0 && row < a.S) {
+        const float tot = (red[512 + row] + red[640 + row]) + (red[768 + row] + red[896 + row]);
+        a.lse_out[uint64_t(z) * a.S + row] = (mx + __log2f(tot)) * 0.6931471805599453f;
+      }
+    } else if (tid == 0) {
       tma_store_4d(&m_probs, sP, 0, 0, z, 0);
       if (a.S > 64) tma_store_4d(&m_probs, sP + AT_TILE, 64, 0, z, 0);
       bulk_commit();
@@ -318,7 +328,7 @@ __global__ void __launch_bounds__(AT_THREADS) k_attn_bwd(const __grid_constant__
     for (int i = 0; i < 4; ++i) mbar_init(&bar[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 1) tmem_alloc1<256>(tslot);
+  if (warp == 1) tmem_alloc1<512>(tslot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -331,13 +341,15 @@ __global__ void __launch_bounds__(AT_THREADS) k_attn_bwd(const __grid_constant__
   auto issue_load = [&](int zz, int buf) {
     const int bb = zz / a.A, hh = zz % a.A;
     uint8_t* d = sIn + buf * 6 * AT_TILE;
-    mbar_expect_tx(&bar[buf], 6 * AT_TILE);
+    mbar_expect_tx(&bar[buf], (a.lse_in ? 4 : 6) * AT_TILE);
     tma_load_3(d, &m_qkv, &bar[buf], hh * AT_D, 0, bb);
     tma_load_3(d + AT_TILE, &m_qkv, &bar[buf], a.H + hh * AT_D, 0, bb);
     tma_load_3(d + 2 * AT_TILE, &m_qkv, &bar[buf], 2 * a.H + hh * AT_D, 0, bb);
     tma_load_3(d + 3 * AT_TILE, &m_dctx, &bar[buf], hh * AT_D, 0, bb);
-    tma_load_3(d + 4 * AT_TILE, &m_probs, &bar[buf], 0, 0, zz);
-    tma_load_3(d + 5 * AT_TILE, &m_probs, &bar[buf], 64, 0, zz);
+    if (!a.lse_in) {  // lse mode: P is recomputed from a QK^T MMA, not loaded
+      tma_load_3(d + 4 * AT_TILE, &m_probs, &bar[buf], 0, 0, zz);
+      tma_load_3(d + 5 * AT_TILE, &m_probs, &bar[buf], 64, 0, zz);
+    }
   };
   if (tid == 0 && int(blockIdx.x) < a.Z) issue_load(blockIdx.x, 0);
   int it = 0;
@@ -363,6 +375,12 @@ __global__ void __launch_bounds__(AT_THREADS) k_attn_bwd(const __grid_constant__
     for (int k = 0; k < 4; ++k)
       tc_mma<1>(tm, umma_desc(smem_u32(sO) + k * 32, 16, 1024), umma_desc(smem_u32(sV) + k * 32, 16, 1024), id1,
                 k ? 1u : 0u);
+    if (a.lse_in) {  // S = Q K^T -> TMEM columns 256..383 (P recomputed from it and lse)
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        tc_mma<1>(tm + 256, umma_desc(smem_u32(sQ) + k * 32, 16, 1024),
+                  umma_desc(smem_u32(sK) + k * 32, 16, 1024), id1, k ? 1u : 0u);
+    }
     tc_commit<1>(&bar[2]);
   }
   uint32_t kb[2];
@@ -383,10 +401,33 @@ __global__ void __launch_bounds__(AT_THREADS) k_attn_bwd(const __grid_constant__
   // pass 1: rowdot = sum_j P_j * dP_j (this half), combined through smem
   float dp[64];
   float rowdot = 0.0f;
+  const float lse2 = (a.lse_in && row < a.S) ? a.lse_in[uint64_t(z) * a.S + row] * 1.4426950408889634f : 0.0f;
+  const float sl2 = a.scale * 1.4426950408889634f;
+  const int lim = row >= a.S ? 0 : a.causal ? min(a.S, row + 1) : a.S;
 #pragma unroll
   for (int c = 0; c < 2; ++c) {
     uint32_t r[32];
     TMEM_LD32(trow + c * 32, r);
+    if (a.lse_in) {  // P = 2^(s*scale*log2e - lse*log2e), rounded to bf16 into the P tile
+      uint32_t rs[32];
+      TMEM_LD32(trow + 256 + c * 32, rs);
+      tmem_wait_ld();
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        float pf[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const int col = j0 + c * 32 + g * 8 + e;
+          pf[e] = col < lim ? ex2_approx(__uint_as_float(rs[g * 8 + e]) * sl2 - lse2) : 0.0f;
+        }
+        uint4 w;
+        w.x = pack_bf2(pf[0], pf[1]);
+        w.y = pack_bf2(pf[2], pf[3]);
+        w.z = pack_bf2(pf[4], pf[5]);
+        w.w = pack_bf2(pf[6], pf[7]);
+        *reinterpret_cast<uint4*>(tileP + sw128(row, c * 4 + g)) = w;
+      }
+    }
     tmem_wait_ld();
 #pragma unroll
     for (int g = 0; g < 4; ++g) {
@@ -493,7 +534,7 @@ __global__ void __launch_bounds__(AT_THREADS) k_attn_bwd(const __grid_constant__
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_free1<256>(tm);
+    tmem_free1<512>(tm);
   }
 }
 
@@ -511,23 +552,25 @@ static CUtensorMap seq_map(const void* p, int64_t cols, int64_t S, int64_t B) {
 }
 
 void launch_attn_fwd(const void* qkv, void* ctx, void* probs, int64_t B, int64_t S, int64_t H, int64_t A, float scale,
-                     int causal, const DropCfg& d, cudaStream_t s, void* trace) {
+                     int causal, const DropCfg& d, cudaStream_t s, void* trace, float* lse) {
   static std::once_flag once;
   std::call_once(once, [] {
     TCB_CUDA(cudaFuncSetAttribute(k_attn_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, AT_FWD_SMEM));
   });
   const CUtensorMap mq = seq_map(qkv, 3 * H, S, B);
   const CUtensorMap mc = seq_map(ctx, H, S, B);
-  const CUtensorMap mp = encode4(probs, TCB_BF16, S, S, B * A, 1, S, S * S, S * S * B * A, 64, 128,
-                                 CU_TENSOR_MAP_SWIZZLE_128B);
-  AttnArgs a{int(S), int(H), int(A), int(H / A), causal, int(B * A), static_cast<unsigned long long*>(trace), scale, d};
+  // lse mode: no probs tensor (the map is never used; point it at ctx)
+  const CUtensorMap mp = lse ? mc : encode4(probs, TCB_BF16, S, S, B * A, 1, S, S * S, S * S * B * A, 64, 128,
+                                            CU_TENSOR_MAP_SWIZZLE_128B);
+  AttnArgs a{int(S), int(H), int(A), int(H / A), causal, int(B * A), static_cast<unsigned long long*>(trace), scale, d,
+             lse, nullptr};
   const int grid = int(B * A < kNumSMs ? B * A : kNumSMs);
   launch_k(k_attn_fwd, unsigned(grid), AT_FWD_THREADS, AT_FWD_SMEM, s, mq, mp, mc, a);
   TCB_CUDA(cudaGetLastError());
 }
 
 void launch_attn_bwd(const void* qkv, const void* probs, const void* dctx, void* dqkv, int64_t B, int64_t S, int64_t H,
-                     int64_t A, float scale, int causal, const DropCfg& d, cudaStream_t s) {
+                     int64_t A, float scale, int causal, const DropCfg& d, cudaStream_t s, const float* lse) {
   static std::once_flag once;
   std::call_once(once, [] {
     TCB_CUDA(cudaFuncSetAttribute(k_attn_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, AT_BWD_SMEM));
@@ -535,9 +578,9 @@ void launch_attn_bwd(const void* qkv, const void* probs, const void* dctx, void*
   const CUtensorMap mq = seq_map(qkv, 3 * H, S, B);
   const CUtensorMap mo = seq_map(dctx, H, S, B);
   const CUtensorMap md = seq_map(dqkv, 3 * H, S, B);
-  const CUtensorMap mp = encode4(probs, TCB_BF16, S, S, B * A, 1, S, S * S, S * S * B * A, 64, 128,
-                                 CU_TENSOR_MAP_SWIZZLE_128B);
-  AttnArgs a{int(S), int(H), int(A), int(H / A), causal, int(B * A), nullptr, scale, d};
+  const CUtensorMap mp = lse ? mo : encode4(probs, TCB_BF16, S, S, B * A, 1, S, S * S, S * S * B * A, 64, 128,
+                                            CU_TENSOR_MAP_SWIZZLE_128B);
+  AttnArgs a{int(S), int(H), int(A), int(H / A), causal, int(B * A), nullptr, scale, d, nullptr, lse};
   const int grid = int(B * A < kNumSMs ? B * A : kNumSMs);
   launch_k(k_attn_bwd, unsigned(grid), AT_THREADS, AT_BWD_SMEM, s, mq, mp, mo, md, a);
   TCB_CUDA(cudaGetLastError());

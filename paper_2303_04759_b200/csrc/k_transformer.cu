@@ -1245,11 +1245,18 @@ static void b_attention_lse(Plan& p) {
   if (save_mask)
     require(g.d.p > 0.0f && p.out[2].numel() * dtype_bytes(p.out[2].dtype) >= g.Z * g.S * nw * 4,
             "attention: save_mask needs p > 0 and ceil(S/32) words per query row");
+  // S <= 128: the persistent per-head kernels (k_attention.cu) in lse mode --
+  // measured faster there than the flash grid; longer sequences: flash
+  const bool persistent = attn_fused_ok(g.dt, g.S, g.H, g.A, g.exact) && !p.attrs.i("flash_kernel", 0);
   p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
     DropCfg d = with_step(g.d);
     if (save_mask) d.mask_out = static_cast<uint8_t*>(out[2].ptr);
-    launch_flash_fwd(in[0].ptr, out[0].ptr, static_cast<float*>(out[1].ptr), g.B, g.S, g.H, g.A, g.scale,
-                     g.causal, d, s);
+    if (persistent)
+      launch_attn_fwd(in[0].ptr, out[0].ptr, nullptr, g.B, g.S, g.H, g.A, g.scale, g.causal, d, s, nullptr,
+                      static_cast<float*>(out[1].ptr));
+    else
+      launch_flash_fwd(in[0].ptr, out[0].ptr, static_cast<float*>(out[1].ptr), g.B, g.S, g.H, g.A, g.scale,
+                       g.causal, d, s);
   };
 }
 
@@ -1267,9 +1274,15 @@ static void b_attention_dx_lse(Plan& p) {
   const int64_t nt = (g.S + 127) / 128;
   const size_t dq = p.ws_take(nt > 1 ? size_t(g.B * g.S * g.H) * sizeof(float) : 0);
   p.nkernels = nt > 1 ? 2 : 1;  // (+ a memset node) the dQ f32 -> bf16 store
+  const bool persistent = attn_fused_ok(g.dt, g.S, g.H, g.A, g.exact) && !p.attrs.i("flash_kernel", 0);
   p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
     DropCfg d = with_step(g.d);
     if (mask_in) d.mask_in = static_cast<const uint8_t*>(in[4].ptr);
+    if (persistent) {
+      launch_attn_bwd(in[0].ptr, nullptr, in[3].ptr, out[0].ptr, g.B, g.S, g.H, g.A, g.scale, g.causal, d, s,
+                      static_cast<const float*>(in[2].ptr));
+      return;
+    }
     launch_flash_bwd(in[0].ptr, in[1].ptr, static_cast<const float*>(in[2].ptr), in[3].ptr, out[0].ptr,
                      nt > 1 ? static_cast<float*>(ws_at(dq)) : nullptr, g.B, g.S, g.H, g.A, g.scale, g.causal, d, s);
   };

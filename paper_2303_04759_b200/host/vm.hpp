@@ -540,7 +540,15 @@ class DeviceVM {
         times[i].push_back(ms);
       }
     }
-    std::string out = "idx,op,let,median_us,bytes_in,bytes_out,kernels\n";
+    std::string out = "idx,op,let,median_us,bytes_in,bytes_out,kernels,shapes\n";
+    auto shp = [](const std::vector<tcb_tensor>& ts) {
+      std::string r;
+      for (size_t i = 0; i < ts.size(); ++i) {
+        if (i) r += ";";
+        for (int d = 0; d < ts[i].rank; ++d) r += (d ? "x" : "") + std::to_string(ts[i].shape[d]);
+      }
+      return r;
+    };
     for (size_t i = 0; i < first.size(); ++i) {
       auto v = times[i];
       std::sort(v.begin(), v.end());
@@ -549,8 +557,10 @@ class DeviceVM {
       int64_t bi = 0, bo = 0;
       std::string op = "fold_flush";
       int let = -1, nk = 1;
+      std::string shapes;
       if (k >= 0) {
         const Instr& x = code_[size_t(k)];
+        shapes = shp(x.in) + ">" + shp(x.out);
         for (auto& t : x.in) bi += nbytes_desc(t);
         for (auto& t : x.out) bo += nbytes_desc(t);
         op = x.op;
@@ -558,9 +568,9 @@ class DeviceVM {
         nk = x.nkernels;
       }
       char buf[256];
-      std::snprintf(buf, sizeof buf, "%zu,%s,%d,%.3f,%lld,%lld,%d\n", i, op.c_str(), let, med, (long long)bi,
+      std::snprintf(buf, sizeof buf, "%zu,%s,%d,%.3f,%lld,%lld,%d,", i, op.c_str(), let, med, (long long)bi,
                     (long long)bo, nk);
-      out += buf;
+      out += buf + shapes + "\n";
     }
     return out;
   }

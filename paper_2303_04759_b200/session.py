@@ -111,7 +111,7 @@ class ModelConfig:
     fuse: int = 1
     bucket_mb: float = 25.0  # ZeRO gradient bucket (f32 MB; 0: one per parameter segment)
     zero: int = 0            # ZeRO data plane at world 1 (identity collectives, comm stream)
-    flash: int = 1           # bf16 attention via the flash kernels (lse saved): 1 for S > 128, 2 always, 0 never
+    flash: int = 1           # bf16 attention in lse mode (P recomputed in the backward); 0: stored-P path
     extra: dict = field(default_factory=dict)  # runtime keys: budget, schedule, rank
 
     def cfg_string(self, model_only: bool = False) -> str:
@@ -343,9 +343,11 @@ class Session:
         rows = []
         lines = t.decode().splitlines()
         for line in lines[1:]:
-            i, op, let, us, bi, bo, k = line.split(",")
+            i, op, let, us, bi, bo, k, shapes = line.split(",")
+            ins, _, outs = shapes.partition(">")
+            parse = lambda t: [tuple(int(d) for d in x.split("x")) for x in t.split(";") if x]  # noqa: E731
             rows.append({"idx": int(i), "op": op, "let": int(let), "us": float(us), "bytes_in": int(bi),
-                         "bytes_out": int(bo), "kernels": int(k)})
+                         "bytes_out": int(bo), "kernels": int(k), "in": parse(ins), "out": parse(outs)})
         return rows
 
     def set_comm(self, comm: int):

@@ -30,16 +30,20 @@ def rn(*shape, lo=-1.0, hi=1.0):
     return RNG.uniform(lo, hi, size=shape).astype(np.float32)
 
 
-CASES = [(128, 0, 0.0), (128, 1, 0.1), (72, 0, 0.1), (40, 1, 0.0), (256, 1, 0.0), (256, 0, 0.1),
-         (200, 1, 0.1), (512, 1, 0.1), (1024, 1, 0.0)]
+CASES = [(128, 0, 0.0, 0), (128, 1, 0.1, 0), (72, 0, 0.1, 0), (40, 1, 0.0, 0), (128, 0, 0.1, 1), (72, 1, 0.1, 1),
+         (256, 1, 0.0, 0), (256, 0, 0.1, 0), (200, 1, 0.1, 0), (512, 1, 0.1, 0), (1024, 1, 0.0, 0)]
 
 
-@pytest.mark.parametrize("S,causal,p", CASES)
-def test_flash_fwd_bwd_vs_oracle(S, causal, p):
+@pytest.mark.parametrize("S,causal,p,flash_kernel", CASES)
+def test_flash_fwd_bwd_vs_oracle(S, causal, p, flash_kernel):
+    """lse mode: S <= 128 runs the persistent per-head kernels (flash_kernel=1
+    forces the flash grid there too), longer sequences the flash kernels."""
     B, A, dh = (2, 2, 64) if S <= 512 else (1, 1, 64)
     H, T = A * dh, B * S
     qkv = rn(T, 3 * H, lo=-2, hi=2)
     at = {"heads": A, "seq": S, "p": p, "seed": 5, "salt": 11, "causal": causal, "lse": 1}
+    if flash_kernel:
+        at["flash_kernel"] = 1
     outs = [((T, H), BF16), ((B * A * S,), F32)]
     g, o = run_both("attention", [(qkv, BF16)], outs, at)
     assert rel_err(g[0], o[0]) < 2e-2, rel_err(g[0], o[0])
