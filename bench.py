@@ -311,6 +311,31 @@ def max_batch_report(stream_sync_free_bytes: int):
     return out
 
 
+def c5_report(free_bytes: int):
+    """BASELINE configs[4] (C5) on ONE B200: GPT-2 XL (1.5B) S = 1024 bf16
+    Adam with remat -- max batch under remat (planner) and one verified GPU
+    step (the configured 8-GPU ZeRO-1 run needs a multi-GPU node)."""
+    import torch
+    from paper_2303_04759_b200.session import ModelConfig, cache_clear, max_batch_under_remat
+    cache_clear()
+    budget = int(free_bytes * 0.92) - (2 << 30)
+    reserve = 1024 * 8 * 1024
+    b_remat, gi = max_batch_under_remat(ModelConfig.gpt2_xl, budget, b0=32, reserve_per_sample=reserve)
+    b_plain, _ = max_batch_under_remat(ModelConfig.gpt2_xl, budget, b0=4, remat=False, reserve_per_sample=reserve)
+    out = {"model": "gpt2-xl (L48 H1600 A25 F6400 V50257) seq1024 causal bf16 Adam, flash attention, 1 GPU",
+           "budget_gb": round(budget / 1e9, 1), "max_batch": b_remat, "max_batch_no_remat": b_plain,
+           "remat_replays": gi.get("remat_replays")}
+    try:
+        ms, loss = _verify_step(b_remat, budget, ModelConfig.gpt2_xl)
+        out.update({"verified_on_gpu": bool(np.isfinite(loss)), "step_ms": round(ms, 1),
+                    "tokens_per_s": round(b_remat * 1024 / (ms * 1e-3)), "loss": round(loss, 4)})
+    except Exception as e:
+        out.update({"verified_on_gpu": False, "error": str(e)[:200]})
+        cache_clear()
+        torch.cuda.empty_cache()
+    return out
+
+
 def c3_report(free_bytes: int):
     """BASELINE configs[2] (C3): GPT-2 medium (345M) causal LM, S = 512, bf16
     Adam, dropout 0.1 (flash attention: lse saved, P recomputed) -- the largest
@@ -544,6 +569,9 @@ def run_ours(args):
         torch.cuda.empty_cache()
         free, total = torch.cuda.mem_get_info()
         out["config"]["c3_gpt2_medium_max_batch_under_remat"] = c3_report(free)
+        torch.cuda.empty_cache()
+        free, total = torch.cuda.mem_get_info()
+        out["config"]["c5_gpt2_xl_1gpu_max_batch_under_remat"] = c5_report(free)
     if world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline_port()
     print(json.dumps(out), flush=True)

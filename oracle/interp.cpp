@@ -235,12 +235,13 @@ std::unique_ptr<Interp> make_interp(const std::string& cfg, int rank) {
   // optional "autocast=<policy>" key: interpret the AutoCast'd f32 step
   std::string model, amp, kv;
   int64_t budget = 0;
-  int sched = 0;
+  int sched = 0, remat_chain = 1;
   std::istringstream is(cfg);
   while (std::getline(is, kv, ';')) {
     if (kv.rfind("autocast=", 0) == 0) amp = kv.substr(9);
     else if (kv.rfind("budget=", 0) == 0) budget = std::stoll(kv.substr(7));
     else if (kv.rfind("schedule=", 0) == 0) sched = std::stoi(kv.substr(9));
+    else if (kv.rfind("remat_chain=", 0) == 0) remat_chain = std::stoi(kv.substr(12));
     else if (!kv.empty()) model += kv + ";";
   }
   I->ts = build_train_step(parse_cfg(model));
@@ -248,7 +249,7 @@ std::unique_ptr<Interp> make_interp(const std::string& cfg, int rank) {
   // the memsched phases in the session's order (capi.cpp prepare): the
   // interpreter then executes the scheduled / rematerialised let sequence
   if (sched) I->ts.fn = ir::make_fn(I->ts.fn->name, I->ts.fn->params, schedule(*I->ts.fn, I->ts.state_binding));
-  if (budget > 0) I->ts.fn = rematerialize(*I->ts.fn, budget, I->ts.state_binding).first;
+  if (budget > 0) I->ts.fn = rematerialize(*I->ts.fn, budget, I->ts.state_binding, false, remat_chain != 0).first;
   const auto& ps = I->ts.fn->params;
   for (auto& p : ps) I->state.push_back(std::make_shared<std::vector<uint32_t>>(size_t(numel(p->ty.tensor())), 0u));
   // params (this rank's shard under ZeRO) / half copy from the shared

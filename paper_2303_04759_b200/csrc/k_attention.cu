@@ -40,6 +40,7 @@ struct AttnArgs {
   // log2e) from a QK^T MMA instead of loading it
   float* lse_out;
   const float* lse_in;
+  int nw;  // saved keep-bit words per query row: 4 (stored-P mode), ceil(S/32) (lse mode)
 };
 
 // byte offset of granule g (8 bf16) of row r in a [128 rows x 128 B] SW128 tile
@@ -167,8 +168,8 @@ __global__ void __launch_bounds__(AT_FWD_THREADS) k_attn_fwd(const __grid_consta
     }
     // dropout keep bits overlap the QK^T MMA (and are saved for the backward)
     const uint32_t kb = keep_bits32(dd, (uint64_t(z) * a.S + row) * a.S, j0, a.S);
-    if (dd.mask_out && row < a.S)
-      reinterpret_cast<uint32_t*>(dd.mask_out)[(uint64_t(z) * a.S + row) * 4 + cq] = kb;
+    if (dd.mask_out && row < a.S && cq < a.nw)
+      reinterpret_cast<uint32_t*>(dd.mask_out)[(uint64_t(z) * a.S + row) * a.nw + cq] = kb;
     mbar_wait(&bar[2], it & 1);
     tc_fence_after();
     T(2);
@@ -385,9 +386,9 @@ __global__ void __launch_bounds__(AT_THREADS) k_attn_bwd(const __grid_constant__
   }
   uint32_t kb[2];
   if (dd.mask_in) {  // the forward's saved keep bits (no Philox re-run)
-    const uint32_t* mw = reinterpret_cast<const uint32_t*>(dd.mask_in) + (uint64_t(z) * a.S + row) * 4 + 2 * hf;
-    kb[0] = row < a.S ? mw[0] : 0xffffffffu;
-    kb[1] = row < a.S ? mw[1] : 0xffffffffu;
+    const uint32_t* mw = reinterpret_cast<const uint32_t*>(dd.mask_in) + (uint64_t(z) * a.S + row) * a.nw + 2 * hf;
+    kb[0] = row < a.S && 2 * hf < a.nw ? mw[0] : 0xffffffffu;
+    kb[1] = row < a.S && 2 * hf + 1 < a.nw ? mw[1] : 0xffffffffu;
   } else {
     keep_bits64(dd, (uint64_t(z) * a.S + row) * a.S, j0, a.S, kb);
   }
@@ -563,7 +564,7 @@ void launch_attn_fwd(const void* qkv, void* ctx, void* probs, int64_t B, int64_t
   const CUtensorMap mp = lse ? mc : encode4(probs, TCB_BF16, S, S, B * A, 1, S, S * S, S * S * B * A, 64, 128,
                                             CU_TENSOR_MAP_SWIZZLE_128B);
   AttnArgs a{int(S), int(H), int(A), int(H / A), causal, int(B * A), static_cast<unsigned long long*>(trace), scale, d,
-             lse, nullptr};
+             lse, nullptr, lse ? int((S + 31) / 32) : 4};
   const int grid = int(B * A < kNumSMs ? B * A : kNumSMs);
   launch_k(k_attn_fwd, unsigned(grid), AT_FWD_THREADS, AT_FWD_SMEM, s, mq, mp, mc, a);
   TCB_CUDA(cudaGetLastError());
@@ -580,7 +581,8 @@ void launch_attn_bwd(const void* qkv, const void* probs, const void* dctx, void*
   const CUtensorMap md = seq_map(dqkv, 3 * H, S, B);
   const CUtensorMap mp = lse ? mo : encode4(probs, TCB_BF16, S, S, B * A, 1, S, S * S, S * S * B * A, 64, 128,
                                             CU_TENSOR_MAP_SWIZZLE_128B);
-  AttnArgs a{int(S), int(H), int(A), int(H / A), causal, int(B * A), nullptr, scale, d, nullptr, lse};
+  AttnArgs a{int(S), int(H), int(A), int(H / A), causal, int(B * A), nullptr, scale, d, nullptr, lse,
+             lse ? int((S + 31) / 32) : 4};
   const int grid = int(B * A < kNumSMs ? B * A : kNumSMs);
   launch_k(k_attn_bwd, unsigned(grid), AT_THREADS, AT_BWD_SMEM, s, mq, mp, mo, md, a);
   TCB_CUDA(cudaGetLastError());

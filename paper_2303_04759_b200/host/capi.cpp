@@ -103,11 +103,13 @@ static void prepare(Session& s, const char* cfg_c) {
   std::istringstream is(all);
   std::string kv;
   int do_schedule = 0;
+  int remat_chain = 1;  // remat: depth-2 chains through tuple producers (memsched.hpp)
   std::string amp;
   while (std::getline(is, kv, ';')) {
     if (kv.rfind("budget=", 0) == 0) s.budget = std::stoll(kv.substr(7));
     else if (kv.rfind("schedule=", 0) == 0) do_schedule = std::stoi(kv.substr(9));
     else if (kv.rfind("autocast=", 0) == 0) amp = kv.substr(9);
+    else if (kv.rfind("remat_chain=", 0) == 0) remat_chain = std::stoi(kv.substr(12));
     else if (kv.rfind("rank=", 0) == 0) s.rank = std::stoi(kv.substr(5));
     else if (!kv.empty()) model += kv + ";";
   }
@@ -123,7 +125,7 @@ static void prepare(Session& s, const char* cfg_c) {
   // as its bucket exists (the VM runs them on its comm stream)
   if (s.cfg.zero_on()) fn = ir::make_fn(fn->name, fn->params, hoist_collectives(ir::flatten(*fn)));
   if (s.budget > 0) {
-    auto [rf, plan] = rematerialize(*fn, s.budget, s.ts.state_binding);
+    auto [rf, plan] = rematerialize(*fn, s.budget, s.ts.state_binding, false, remat_chain != 0);
     fn = rf;
     s.remat = plan;
   }

@@ -560,9 +560,12 @@ inline bool replayable(const ir::ExprPtr& e) {
 /// split).  Replay inputs must be live there; depth-1 victims only (the spec
 /// allows <= 3; deeper chains are not evicted).  Throws BudgetInfeasible when
 /// the floor (state + max single-op working set) exceeds the budget.
+/// tuple_chains: a dead input that is a FIELD of a replayable tuple producer
+/// (a LayerNorm output feeding a linear, as in pre-LN GPT-2) may be re-created
+/// by replaying that producer whole (depth-2 chain through a twin get-let).
 inline std::pair<FunctionPtr, RematPlan> rematerialize(const ir::FunctionIR& fn, int64_t budget,
                                                         const std::vector<std::pair<int, int>>& sb = {},
-                                                        bool transient_inputs = false) {
+                                                        bool transient_inputs = false, bool tuple_chains = true) {
   RematPlan plan;
   auto cur = std::make_shared<ir::FunctionIR>(fn);
   for (int iter = 0; iter < 100000; ++iter) {
@@ -588,7 +591,15 @@ inline std::pair<FunctionPtr, RematPlan> rematerialize(const ir::FunctionIR& fn,
     std::unordered_map<const ir::Var*, int> def;
     for (int k = 0; k < n; ++k) def[seq.lets[k].var.get()] = k;
     int best_u = -1, best_next = -1;
-    std::vector<std::pair<const ir::Var*, int>> best_chain;  // (dead input var, its producer let)
+    // depth-2 chain entries: a dead input of the replayed producer, re-created
+    // by replaying ITS producer let `prod` (a tuple producer when the input is
+    // a field of it: `field` >= 0, re-read through a twin get-let)
+    struct ChainEnt {
+      const ir::Var* dead;
+      int prod;
+      int field;
+    };
+    std::vector<ChainEnt> best_chain;
     double best_score = std::numeric_limits<double>::infinity();
     for (size_t u = 0; u < L.units.size(); ++u) {
       const Unit& x = L.units[u];
@@ -615,7 +626,7 @@ inline std::pair<FunctionPtr, RematPlan> rematerialize(const ir::FunctionIR& fn,
       // (a depth-2 chain; SPEC.md:485 allows up to 3)
       bool ok = true;
       double cost = op_cost(pe);
-      std::vector<std::pair<const ir::Var*, int>> chain;
+      std::vector<ChainEnt> chain;
       for (auto& a : pe->args) {
         if (a->kind != ExprKind::VarRef || !ok) continue;
         bool dead = false;
@@ -629,8 +640,19 @@ inline std::pair<FunctionPtr, RematPlan> rematerialize(const ir::FunctionIR& fn,
           ok = false;
           continue;
         }
-        const auto& p2 = seq.lets[dit->second];
-        if (p2.value->kind != ExprKind::Call || p2.var->ty.is_tuple() || !replayable(p2.value)) {
+        int prod = dit->second, field = -1;
+        if (seq.lets[prod].value->kind == ExprKind::TupleGet && tuple_chains) {  // a field of a tuple producer
+          const auto& tg = seq.lets[prod].value;
+          auto tit = tg->args[0]->kind == ExprKind::VarRef ? def.find(tg->args[0]->var.get()) : def.end();
+          if (tit == def.end()) {
+            ok = false;
+            continue;
+          }
+          field = int(tg->index);
+          prod = tit->second;
+        }
+        const auto& p2 = seq.lets[prod];
+        if (p2.value->kind != ExprKind::Call || (field < 0 && p2.var->ty.is_tuple()) || !replayable(p2.value)) {
           ok = false;
           continue;
         }
@@ -642,7 +664,7 @@ inline std::pair<FunctionPtr, RematPlan> rematerialize(const ir::FunctionIR& fn,
           }
         }
         if (ok) {
-          chain.push_back({a->var.get(), dit->second});
+          chain.push_back({a->var.get(), prod, field});
           cost += op_cost(p2.value);
         }
       }
@@ -680,14 +702,23 @@ inline std::pair<FunctionPtr, RematPlan> rematerialize(const ir::FunctionIR& fn,
     ne->serial = ir::detail::next_serial();
     // depth-2 chain: replay the dead inputs' producers first, feed the replay
     std::vector<std::pair<ir::VarPtr, ir::ExprPtr>> chain_lets;
-    for (auto& [cv, cl] : best_chain) {
-      const auto& cb = seq.lets[cl];
+    for (auto& ce_ : best_chain) {
+      const auto& cb = seq.lets[ce_.prod];
       auto cv2 = ir::make_var(cb.var->id + "_r" + std::to_string(plan.replays), cb.var->ty, cb.var->attrs);
       auto ce = std::make_shared<ir::Expr>(*cb.value);
       ce->serial = ir::detail::next_serial();
       chain_lets.push_back({cv2, ce});
+      ir::VarPtr feed = cv2;
+      if (ce_.field >= 0) {  // twin get-let of the replayed tuple's field
+        const Type ft = cb.var->ty.tuple().fields.at(size_t(ce_.field));
+        auto gv = ir::make_var(ce_.dead->id + "_r" + std::to_string(plan.replays), ft, ce_.dead->attrs);
+        auto ge = ir::tuple_get(ir::var_ref(cv2), ce_.field);
+        ge->ty = ft;
+        chain_lets.push_back({gv, ge});
+        feed = gv;
+      }
       for (auto& a : ne->args)
-        if (a->kind == ExprKind::VarRef && a->var.get() == cv) a = ir::var_ref(cv2);
+        if (a->kind == ExprKind::VarRef && a->var.get() == ce_.dead) a = ir::var_ref(feed);
       plan.replays++;
     }
     const ir::Var* old = pb.var.get();

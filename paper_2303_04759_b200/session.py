@@ -111,7 +111,7 @@ class ModelConfig:
     fuse: int = 1
     bucket_mb: float = 25.0  # ZeRO gradient bucket (f32 MB; 0: one per parameter segment)
     zero: int = 0            # ZeRO data plane at world 1 (identity collectives, comm stream)
-    flash: int = 1           # bf16 attention in lse mode (P recomputed in the backward); 0: stored-P path
+    flash: int = 1           # bf16 attention lse mode (P recomputed in the bwd): 1 for S > 128, 2 always, 0 never
     extra: dict = field(default_factory=dict)  # runtime keys: budget, schedule, rank
 
     def cfg_string(self, model_only: bool = False) -> str:
@@ -174,11 +174,19 @@ def plan_fits(cfg: ModelConfig, budget: int, remat: bool) -> tuple[bool, dict]:
         # the remat pass bounds the liveness peak; address packing of the arena
         # adds fragmentation on top, so it aims 1.5% below the budget
         c.extra["budget"] = int(budget * 0.985)
-    try:
-        gi = graph_info(c)
-    except RuntimeError:
-        return False, {}
-    return gi["arena_plan_bytes"] + gi["state_bytes"] <= budget, gi
+    # the greedy remat pass is not monotone in its candidate set: plan with
+    # depth-2 chains through tuple producers, and without them if that fails
+    tries = [1, 0] if remat and "remat_chain" not in c.extra else [c.extra.get("remat_chain", 1)]
+    gi = {}
+    for rc in tries:
+        c.extra["remat_chain"] = rc
+        try:
+            gi = graph_info(c)
+        except RuntimeError:
+            continue
+        if gi["arena_plan_bytes"] + gi["state_bytes"] <= budget:
+            return True, gi
+    return False, gi
 
 
 def max_batch_under_remat(factory, budget: int, b0: int = 32, remat: bool = True,
