@@ -48,9 +48,6 @@ struct GemmArgs {
   int* dep_signal = nullptr;       // chained launch: per-row-block completion counters this problem signals
   const int* dep_wait = nullptr;   // ... or waits on (>= dep_need) before loading A
   int dep_need = 0;
-  // B is read-only state written before the previous kernel started (a
-  // weight view): its first k-blocks may be loaded before griddepcontrol.wait
-  int b_ready = 0;
 };
 
 struct TcChoice {

@@ -75,7 +75,6 @@ static void b_matmul_t(Plan& p) {
   g.alpha = float(p.attrs.f("alpha", 1.0));
   const bool exact = want_exact(p);
   auto keep = std::make_shared<GemmWs>();
-  g.b_ready = int(p.attrs.i("b_state", 0));
   gemm_prepare(g, exact, *keep);
   p.run = [g, exact, keep](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) mutable {
     g.a.ptr = in[0].ptr;
@@ -89,7 +88,6 @@ TCB_REGISTER("matmul_t", b_matmul_t);
 static void b_linear(Plan& p) {
   check_arity(p, 3, 3, 1, 2);
   GemmArgs g = gemm2d(p.in[0], p.in[1], 0, int(p.attrs.i("tw", 0)), p.out[0], "linear");
-  g.b_ready = int(p.attrs.i("b_state", 0));  // B is a weight view: staged before the PDL wait
   tile_attrs(g, p);
   require(p.in[2].numel() == g.N, "linear: bias must have N elements");
   g.bias_dtype = p.in[2].dtype;
@@ -195,7 +193,6 @@ static void b_matmul_dact(Plan& p) {
   g.aux_dtype = p.in[2].dtype;
   const bool exact = want_exact(p);
   auto keep = std::make_shared<GemmWs>();
-  g.b_ready = int(p.attrs.i("b_state", 0));
   gemm_prepare(g, exact, *keep);
   p.run = [g, exact, keep](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) mutable {
     g.a.ptr = in[0].ptr;
@@ -216,8 +213,6 @@ static void b_matmul_pair(Plan& p) {
   GemmArgs g0 = gemm2d(p.in[0], p.in[1], int(p.attrs.i("ta0", 0)), int(p.attrs.i("tb0", 0)), p.out[0], "matmul_pair");
   GemmArgs g1 = gemm2d(p.in[n0], p.in[n0 + 1], int(p.attrs.i("ta1", 0)), int(p.attrs.i("tb1", 0)), p.out[1],
                        "matmul_pair");
-  g0.b_ready = int(p.attrs.i("b_state0", 0));
-  g1.b_ready = int(p.attrs.i("b_state1", 0));
   g0.alpha = float(p.attrs.f("alpha0", 1.0));
   g1.alpha = float(p.attrs.f("alpha1", 1.0));
   if (n0 == 3) {

@@ -80,7 +80,6 @@ struct TcProb {
   int* sig;
   const int* dep;
   int dep_need;
-  int b_ready;  // B k-blocks of the first unit may be staged before griddepcontrol.wait
   uint32_t idesc;
   // epilogue
   void* c;
@@ -417,43 +416,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  // B prologue: when B is read-only state (a weight view, b_ready), the
-  // producer stages the B half of the first unit's first k-blocks BEFORE
-  // griddepcontrol.wait -- kernels up to the previous-but-one have completed
-  // by the time this grid runs (every kernel waits before it triggers), so
-  // only the previous kernel's outputs (A) must wait
-  int pre_kb = 0;  // k-blocks whose B half is already in flight
-  if (warp == 0 && lane == 0) {
-    const int64_t u0 = unit_at(P, cl_id, n_cl, 0);
-    if (u0 >= 0) {
-      const int prob = unit_prob(P, u0);
-      const TcProb& Q = P.pr[prob];
-      if (Q.b_ready && !Q.dep && Q.wsplit <= 1) {
-        const CUtensorMap* mB = prob ? &tmB1 : &tmB0;
-        int z, mb, nb;
-        decode_tile(Q, u0 - (prob ? P.pr[0].num_tiles : 0), z, mb, nb);
-        const int kb0 = split * Q.kps, kb1 = min(kb0 + Q.kps, Q.k_blocks);
-        const int z1 = int(z / Q.Z2), z2 = int(z % Q.Z2);
-        const int n0 = nb * BN + int(rank) * C::B_ROWS;
-        pre_kb = min(kb1 - kb0, C::STAGES);
-        for (int i = 0; i < pre_kb; ++i) {
-          const uint32_t fb = CG == 2 ? mapa(smem_u32(&full[i]), lead) : smem_u32(&full[i]);
-          if (rank == 0)
-            mbar_expect_tx(&full[i], CG * (C::A_BYTES + (Q.tb ? C::B_ROWS * TC_BK * 2 : C::B_BYTES)));
-          uint8_t* b_dst = sB + i * C::B_BYTES;
-          const int k0 = (kb0 + i) * TC_BK;
-          if (Q.tb) {
-            tma_load_4d<CG>(b_dst, mB, fb, k0, n0, z2, z1);
-          } else {
-#pragma unroll
-            for (int c = 0; c < C::B_CHUNKS; ++c) tma_load_4d<CG>(b_dst + c * 8192, mB, fb, n0 + c * 64, k0, z2, z1);
-          }
-        }
-      }
-    }
-  }
-  // everything above (barriers, TMEM, descriptor prefetch, the B prologue)
-  // overlapped the previous kernel's tail; from here on we read its outputs
+  // everything above (barriers, TMEM, descriptor prefetch) overlapped the
+  // previous kernel's tail; from here on we read its outputs
   pdl_wait();
   pdl_trigger();
   if (tr && threadIdx.x == 0) tr[1] = gtimer();
@@ -479,12 +443,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const int m0 = mb * (TC_BM * CG) + int(rank) * TC_BM;
         const int n0 = nb * BN + int(rank) * C::B_ROWS;
         for (int kb = kb0; kb < kb1; ++kb) {
-          // B half of this k-block issued by the prologue (first unit only)
-          const bool pre = ui == 0 && kb - kb0 < pre_kb;
-          if (!pre) mbar_wait(&empty[stage], phase ^ 1);
+          mbar_wait(&empty[stage], phase ^ 1);
           // both CTAs' bytes complete on the leader's barrier
           const uint32_t fb = CG == 2 ? mapa(smem_u32(&full[stage]), lead) : smem_u32(&full[stage]);
-          if (rank == 0 && !pre)
+          if (rank == 0)
             mbar_expect_tx(&full[stage], CG * (C::A_BYTES + (Q.tb ? C::B_ROWS * TC_BK * 2 : C::B_BYTES)));
           uint8_t* a_dst = sA + stage * C::A_BYTES;
           uint8_t* b_dst = sB + stage * C::B_BYTES;
@@ -495,9 +457,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 #pragma unroll
             for (int c = 0; c < TC_BM / 64; ++c) tma_load_4d<CG>(a_dst + c * 8192, mA, fb, m0 + c * 64, k0, z2, z1);
           }
-          if (pre) {
-            // B already in flight
-          } else if (Q.tb) {
+          if (Q.tb) {
             tma_load_4d<CG>(b_dst, mB, fb, k0, n0, z2, z1);
           } else {
 #pragma unroll
@@ -893,7 +853,6 @@ static void fill_prob(const GemmArgs& g, int splits, TcProb& P, CUtensorMap& ta,
   P.sig = g.dep_signal;
   P.dep = g.dep_wait;
   P.dep_need = g.dep_need;
-  P.b_ready = g.b_ready;
   const int es = dtype_bytes(g.c_dtype);
   P.c_vec_ok = (reinterpret_cast<uintptr_t>(g.c) % 16 == 0) && ((g.ldc * es) % 16 == 0) &&
                ((g.c_s1 * es) % 16 == 0) && ((g.c_s2 * es) % 16 == 0) &&

@@ -305,20 +305,6 @@ class DeviceVM {
         tin.push_back(rt);
         ins.in.push_back(desc(rng_ptr_, rt));
       }
-      // GEMM B operands that are parameter state (weight views) may be staged
-      // before the kernel's griddepcontrol.wait (k_gemm_tc B prologue)
-      auto in_state = [&](const tcb_tensor& t) {
-        const char* q = static_cast<const char*>(t.ptr);
-        return q >= state_base_ && q < state_base_ + stats_.state_bytes;
-      };
-      if ((base == "linear" || base == "matmul_t" || base == "matmul_dact") && ins.in.size() > 1 &&
-          in_state(ins.in[1]) && !std::getenv("TCB_NO_B_PROLOGUE"))
-        pattrs["b_state"] = std::int64_t(1);
-      if (base == "matmul_pair" && !std::getenv("TCB_NO_B_PROLOGUE")) {
-        const int n0 = int(ir::attr_int(pattrs, "n0", 2));
-        if (in_state(ins.in.at(1))) pattrs["b_state0"] = std::int64_t(1);
-        if (int(ins.in.size()) > n0 + 1 && in_state(ins.in.at(size_t(n0) + 1))) pattrs["b_state1"] = std::int64_t(1);
-      }
       if (base == "reduce_scatter") ins.kind = OpKind::ReduceScatter;
       else if (base == "all_gather") ins.kind = OpKind::AllGather;
       else if (base == "allreduce") ins.kind = OpKind::AllReduce;
