@@ -72,6 +72,10 @@ int tb_autocast_info(const char* cfg, const char* policy, const char* placement,
  * Returns NULL on error (tb_last_error). */
 const char* tb_memsched_text(const char* text, const char* what, int64_t budget, int transient_inputs);
 
+/* backends::derive_priorities over "dialect op shape_class median_us" lines
+ * (e.g. from tb_session_profile); returns "dialect.op priority" lines */
+const char* tb_derive_priorities(const char* samples);
+
 /* KernelCache */
 int tb_cache_clear(void); /* only with no session alive */
 int tb_cache_stats(int64_t* out3);

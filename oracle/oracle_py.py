@@ -131,6 +131,15 @@ def run(op: str, inputs, out_specs, attrs=None, impl: str = "oracle"):
     return [o.arr for o in outs]
 
 
+def ref_opt_matmul(a: np.ndarray, b: np.ndarray) -> np.ndarray:
+    """The reference's opt dialect matmul (matmul_blocked, backends.hpp:280-304)."""
+    A, B = HostTensor(a), HostTensor(b)
+    C = HostTensor(np.zeros((a.shape[0], b.shape[1]), np.float32))
+    if ref().ref_exec_opt(ctypes.byref(A.desc()), ctypes.byref(B.desc()), None, 0, ctypes.byref(C.desc())) != 0:
+        raise RuntimeError(ref().ref_last_error().decode())
+    return C.arr
+
+
 def rng_uniform(seed: int, n: int, lo=-1.0, hi=1.0, impl="oracle") -> np.ndarray:
     out = np.empty(n, dtype=np.float32)
     if impl == "oracle":

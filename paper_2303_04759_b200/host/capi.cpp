@@ -485,6 +485,30 @@ const char* tb_memsched_text(const char* text, const char* what, int64_t budget,
   }
 }
 
+/// backends::derive_priorities (backends.hpp:387-419) over vm.profile-style
+/// latency samples, one per line "dialect op shape_class median_us"; returns
+/// "dialect.op priority" lines (lower median -> higher priority).
+const char* tb_derive_priorities(const char* samples) {
+  try {
+    std::vector<backends::LatencySample> v;
+    std::istringstream is(samples ? samples : "");
+    std::string line;
+    while (std::getline(is, line)) {
+      std::istringstream ls(line);
+      backends::LatencySample x;
+      if (ls >> x.dialect >> x.op >> x.shape_class >> x.median_us) v.push_back(x);
+    }
+    auto t = backends::derive_priorities(v);
+    std::ostringstream os;
+    for (auto& [k, pr] : t.priorities) os << k << " " << pr << "\n";
+    g_text = os.str();
+    return g_text.c_str();
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
+
 /// CPU-only: run the AutoCast pass (host/autocast.hpp) on the all-f32 training
 /// step of `cfg` under policy "default", "b200" or "f32", with
 /// placement "auto" (exclusive/shared) or "shared".  out: sites, casts,

@@ -75,6 +75,8 @@ def lib():
         L.tb_session_load_param.argtypes = [ctypes.c_void_p, ctypes.c_char_p, ctypes.c_char_p]
         L.tb_session_profile.restype = ctypes.c_char_p
         L.tb_session_profile.argtypes = [ctypes.c_void_p, ctypes.c_int]
+        L.tb_derive_priorities.restype = ctypes.c_char_p
+        L.tb_derive_priorities.argtypes = [ctypes.c_char_p]
         L.tb_memsched_text.restype = ctypes.c_char_p
         L.tb_memsched_text.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_int64, ctypes.c_int]
         _lib = L
@@ -247,6 +249,16 @@ def graph_segments(cfg: ModelConfig) -> list[tuple[str, int, int]]:
         n, o, k = line.split()
         out.append((n, int(o), int(k)))
     return out
+
+
+def derive_priorities(samples: list[tuple[str, str, str, float]]) -> dict:
+    """backends::derive_priorities (backends.hpp:387-419): (dialect, op,
+    shape_class, median_us) samples -> {"dialect.op": priority}."""
+    text = "".join(f"{d} {o} {c} {us!r}\n" for d, o, c, us in samples)
+    t = lib().tb_derive_priorities(text.encode())
+    if t is None:
+        raise RuntimeError(lib().tb_last_error().decode())
+    return {k: int(v) for k, v in (line.split() for line in t.decode().splitlines())}
 
 
 def memsched_text(text: str, what: str, budget: int = 0, transient_inputs: bool = False) -> str:
