@@ -246,6 +246,7 @@ std::unique_ptr<Interp> make_interp(const std::string& cfg, int rank) {
   }
   I->ts = build_train_step(parse_cfg(model));
   if (!amp.empty()) apply_autocast(I->ts, amp);  // same parser and phases as the session
+  finalize_graph(I->ts);  // rule-based fusion, as the session does
   // the memsched phases in the session's order (capi.cpp prepare): the
   // interpreter then executes the scheduled / rematerialised let sequence
   if (sched) I->ts.fn = ir::make_fn(I->ts.fn->name, I->ts.fn->params, schedule(*I->ts.fn, I->ts.state_binding));

@@ -979,6 +979,62 @@ static int adam(const orc_tensor* const* in, orc_tensor* out, int nout, const or
   return 0;
 }
 
+/* ew_closure: a rule-fused elementwise group (host/graph.hpp rule_fuse).
+ * Registers 0..nin-1 are the inputs ([1]-element inputs broadcast); each
+ * instruction "op dst a b dtype imm" computes one exec_base elementwise op in
+ * f32 and rounds to its dtype (backends.hpp:59-61, :67-93) -- the same value
+ * the op would store unfused; outs = the output registers. */
+static int ew_closure(const orc_tensor* in, int nin, orc_tensor* out, int nout, const orc_attr* a, int na) {
+  const char* prog = astr(a, na, "prog", "");
+  const char* outs = astr(a, na, "outs", "");
+  enum { MAXI = 16 };
+  char opn[MAXI][16];
+  int dst[MAXI], ra[MAXI], rb[MAXI], dt[MAXI], ni = 0, oreg[8], no = 0;
+  float imm[MAXI];
+  const char* q = prog;
+  while (*q && ni < MAXI) {
+    int used = 0;
+    if (sscanf(q, "%15s %d %d %d %d %f%n", opn[ni], &dst[ni], &ra[ni], &rb[ni], &dt[ni], &imm[ni], &used) != 6)
+      return fail("ew_closure: bad program");
+    ++ni;
+    q += used;
+    while (*q == ';' || *q == ' ') ++q;
+  }
+  q = outs;
+  while (*q && no < 8) {
+    oreg[no++] = (int)strtol(q, (char**)&q, 10);
+    while (*q == ',') ++q;
+  }
+  if (no != nout) return fail("ew_closure: %d output registers for %d outputs", no, nout);
+  const int64_t n = numel(&out[0]);
+  float r[8 + MAXI];
+  for (int64_t i = 0; i < n; ++i) {
+    for (int k = 0; k < nin; ++k) r[k] = F(&in[k])[numel(&in[k]) == 1 ? 0 : i];
+    for (int k = 0; k < ni; ++k) {
+      const float x = r[ra[k]], y = r[rb[k]];
+      float v;
+      const char* o = opn[k];
+      if (!strcmp(o, "add")) v = x + y;
+      else if (!strcmp(o, "sub")) v = x - y;
+      else if (!strcmp(o, "mul")) v = x * y;
+      else if (!strcmp(o, "div")) v = x / y;
+      else if (!strcmp(o, "tanh_dx")) v = y * (1.0f - x * x);
+      else if (!strcmp(o, "gelu_dx")) v = y * gelu_grad_f(x);
+      else if (!strcmp(o, "neg")) v = -x;
+      else if (!strcmp(o, "tanh")) v = tanhf(x);
+      else if (!strcmp(o, "relu")) v = x > 0.0f ? x : 0.0f;
+      else if (!strcmp(o, "gtz")) v = x > 0.0f ? 1.0f : 0.0f;
+      else if (!strcmp(o, "gelu")) v = gelu_f(x);
+      else if (!strcmp(o, "add_scalar")) v = x + imm[k];
+      else if (!strcmp(o, "copy")) v = x;
+      else return fail("ew_closure: no op %s", o);
+      r[dst[k]] = rnd(dt[k], v);
+    }
+    for (int k = 0; k < nout; ++k) F(&out[k])[i] = rnd(out[k].dtype, r[oreg[k]]);
+  }
+  return 0;
+}
+
 /* --------------------------------------------------------------- dispatch */
 #define NEED(ni, no)                                                              \
   do {                                                                            \
@@ -1265,6 +1321,7 @@ int orc_exec(const char* op, const orc_tensor* in, int nin, orc_tensor* out, int
     }
     return 0;
   }
+  if (!strcmp(op, "ew_closure")) return ew_closure(in, nin, out, nout, A, na);
   if (!strcmp(op, "attention") && aint(A, na, "lse", 0)) {
     NEED(1, 2);
     return attention_fwd_lse(&in[0], &out[0], &out[1], nout > 2 ? &out[2] : NULL, A, na);

@@ -120,6 +120,9 @@ static void prepare(Session& s, const char* cfg_c) {
     apply_autocast(s.ts, amp);
     fn = s.ts.fn;
   }
+  s.ts.fn = fn;
+  finalize_graph(s.ts);  // rule-based fusion (ew_closure)
+  fn = s.ts.fn;
   if (do_schedule) fn = ir::make_fn(fn->name, fn->params, schedule(*fn, s.ts.state_binding));
   // ZeRO: overlap_schedule -- every collective starts as soon
   // as its bucket exists (the VM runs them on its comm stream)

@@ -338,6 +338,28 @@ inline void register_extension_ops(OpRegistry& r) {
     TensorType h{dtype_from(ir::attr_string(a, "half", "bf16")), p.shape};
     return TupleType{{p, p, p, h}};
   });
+  // rule-fused elementwise group (graph.hpp rule_fuse): inputs -> the group's
+  // externally used values; otypes = "dtype:d0,d1;dtype:..." one per output
+  reg("ew_closure", -1, O, [](const V& in, const AttrMap& a) -> Type {
+    if (in.empty()) throw TypeError("ew_closure: no inputs");
+    std::vector<TensorType> outs;
+    std::string spec = ir::attr_string(a, "otypes", ""), item;
+    size_t pos = 0;
+    while (pos <= spec.size()) {
+      size_t e = spec.find(';', pos);
+      item = spec.substr(pos, e == std::string::npos ? std::string::npos : e - pos);
+      if (!item.empty()) {
+        const size_t c = item.find(':');
+        if (c == std::string::npos) throw TypeError("ew_closure: bad otypes");
+        outs.push_back(TensorType{dtype_from(item.substr(0, c)), opreg::parse_shape_attr(item.substr(c + 1))});
+      }
+      if (e == std::string::npos) break;
+      pos = e + 1;
+    }
+    if (outs.empty()) throw TypeError("ew_closure: no outputs");
+    if (outs.size() == 1) return outs[0];
+    return TupleType{outs};
+  });
   // x + value (a scalar attribute): the optimizer step counter
   reg("add_scalar", 1, E, [](const V& in, const AttrMap&) -> Type { return rel::T(in[0], "add_scalar"); });
   // constant fill (zero gradients of alignment gaps / pads)

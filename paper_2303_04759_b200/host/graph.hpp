@@ -445,6 +445,166 @@ inline GradResult autodiff(Graph& g, const VarPtr& loss, std::vector<Leaf> leave
   return r;
 }
 
+/// materialization_set: the forward tensors a training
+/// graph's backward reads -- the union of what the adjoints retained
+/// (dependency_report): every forward op input they read and every output
+/// (or output field) they read.  Empty for an inference-only graph.
+inline std::set<const ir::Var*> materialization_set(const LetSeq& fwd, const GradResult& gr) {
+  std::set<const ir::Var*> m;
+  for (auto& d : gr.deps) {
+    const auto& b = fwd.lets.at(size_t(d.let));
+    for (int k : d.inputs)
+      if (b.value->args.at(size_t(k))->kind == ExprKind::VarRef) m.insert(b.value->args[size_t(k)]->var.get());
+    if (d.output) m.insert(b.var.get());
+  }
+  return m;
+}
+
+// ---------------------------------------------------------- rule fusion
+/// Rule-based fusion: after the pattern rewrites,
+/// maximal runs of consecutive Elemwise lets of one element count (inputs of
+/// that size or [1] scalars, float) become one multi-output `ew_closure`
+/// (SPEC.md:359-362): its inputs are the values the run reads from outside,
+/// its outputs every member value used after the run -- so forward tensors the
+/// backward needs (the materialization set) escape as outputs instead of
+/// blocking fusion.  A consecutive run contracts to a node without creating a
+/// cycle.  Groups are capped at 16 ops (and 8 inputs / 8 outputs); a run of
+/// one op stays a bare op.  The closure's program rounds every member's result
+/// to its dtype, so values are bit-identical to the unfused ops.
+inline std::string base_name(const std::string& op);
+
+struct RuleFuseStats {
+  int closures = 0, fused_ops = 0;
+};
+
+inline bool rule_fusible_op(const std::string& base) {
+  static const std::set<std::string> ops = {"add",  "sub",  "mul",  "div",  "tanh_dx", "gelu_dx", "neg",
+                                            "tanh", "relu", "gtz",  "gelu", "convert", "cast",    "add_scalar"};
+  return ops.count(base) > 0;
+}
+
+inline RuleFuseStats rule_fuse(LetSeq& s, int max_group = 16) {
+  RuleFuseStats st;
+  const int n = int(s.lets.size());
+  auto is_fl = [](DType d) { return d == kF32 || d == kF16 || d == kBF16; };
+  auto elig = [&](int i, int64_t& cnt) {
+    const auto& b = s.lets[size_t(i)];
+    if (b.value->kind != ExprKind::Call || !b.var->ty.is_tensor()) return false;
+    if (!rule_fusible_op(base_name(b.value->op))) return false;
+    const auto& o = b.var->ty.tensor();
+    if (!is_fl(o.dtype)) return false;
+    cnt = numel(o);
+    for (auto& a : b.value->args) {
+      if (a->kind != ExprKind::VarRef || !a->var->ty.is_tensor()) return false;
+      const auto& t = a->var->ty.tensor();
+      if (!is_fl(t.dtype) || (numel(t) != cnt && numel(t) != 1)) return false;
+    }
+    return true;
+  };
+  // uses after position i of each var (and returned vars)
+  std::unordered_map<const ir::Var*, int> last_use;
+  for (int i = 0; i < n; ++i)
+    for (auto& a : s.lets[size_t(i)].value->args)
+      if (a->kind == ExprKind::VarRef) last_use[a->var.get()] = i;
+  std::set<const ir::Var*> returned;
+  if (s.ret) {
+    if (s.ret->kind == ExprKind::VarRef) returned.insert(s.ret->var.get());
+    for (auto& a : s.ret->args)
+      if (a->kind == ExprKind::VarRef) returned.insert(a->var.get());
+  }
+  LetSeq out;
+  out.ret = s.ret;
+  auto emit_group = [&](int g0, int g1) {  // lets [g0, g1)
+    if (g1 - g0 < 2) {
+      for (int i = g0; i < g1; ++i) out.lets.push_back(s.lets[size_t(i)]);
+      return;
+    }
+    std::map<const ir::Var*, int> reg;
+    std::vector<VarPtr> ins;
+    std::set<const ir::Var*> members;
+    for (int i = g0; i < g1; ++i) members.insert(s.lets[size_t(i)].var.get());
+    for (int i = g0; i < g1; ++i)
+      for (auto& a : s.lets[size_t(i)].value->args)
+        if (!members.count(a->var.get()) && !reg.count(a->var.get())) {
+          reg[a->var.get()] = int(ins.size());
+          ins.push_back(a->var);
+        }
+    std::vector<int> outm;  // member indices used after the run
+    for (int i = g0; i < g1; ++i) {
+      const ir::Var* v = s.lets[size_t(i)].var.get();
+      auto it = last_use.find(v);
+      if (returned.count(v) || (it != last_use.end() && it->second >= g1)) outm.push_back(i);
+    }
+    if (ins.size() > 8 || outm.size() > 8 || outm.empty()) {
+      for (int i = g0; i < g1; ++i) out.lets.push_back(s.lets[size_t(i)]);
+      return;
+    }
+    std::string prog, outs, otypes;
+    int next = int(ins.size());
+    for (int i = g0; i < g1; ++i) {
+      const auto& b = s.lets[size_t(i)];
+      std::string base = base_name(b.value->op);
+      const int ra = reg.at(b.value->args[0]->var.get());
+      const int rb = b.value->args.size() > 1 ? reg.at(b.value->args[1]->var.get()) : ra;
+      double imm = 0.0;
+      if (base == "convert" || base == "cast") base = "copy";
+      if (base == "add_scalar") imm = ir::attr_double(b.value->call_attrs, "value", 0.0);
+      char buf[96];
+      std::snprintf(buf, sizeof buf, "%s %d %d %d %d %.9g;", base.c_str(), next, ra, rb,
+                    dtype_code(b.var->ty.tensor().dtype), imm);
+      prog += buf;
+      reg[b.var.get()] = next++;
+    }
+    for (size_t k = 0; k < outm.size(); ++k) {
+      const auto& b = s.lets[size_t(outm[k])];
+      outs += (k ? "," : "") + std::to_string(reg.at(b.var.get()));
+      const auto& t = b.var->ty.tensor();
+      otypes += (k ? ";" : "") + std::string(dtype_str(t.dtype)) + ":" + opreg::shape_attr(t.shape);
+    }
+    AttrMap at{{"prog", prog}, {"outs", outs}, {"otypes", otypes}};
+    std::vector<ExprPtr> xs;
+    std::vector<Type> tys;
+    for (auto& v : ins) {
+      xs.push_back(ir::var_ref(v));
+      tys.push_back(v->ty);
+    }
+    auto call = ir::call("ew_closure", std::move(xs), at);
+    call->ty = opreg::registry().type_rel_of("ew_closure")(tys, at);
+    if (outm.size() == 1) {
+      out.lets.push_back({s.lets[size_t(outm[0])].var, call});  // the member's var now names the closure
+    } else {
+      auto cv = ir::make_var(s.lets[size_t(g0)].var->id + "_clo", call->ty);
+      out.lets.push_back({cv, call});
+      for (size_t k = 0; k < outm.size(); ++k) {
+        const auto& b = s.lets[size_t(outm[k])];
+        auto g = ir::tuple_get(ir::var_ref(cv), int(k));
+        g->ty = b.var->ty;
+        out.lets.push_back({b.var, g});
+      }
+    }
+    ++st.closures;
+    st.fused_ops += g1 - g0;
+  };
+  int g0 = -1;
+  int64_t gcnt = 0;
+  for (int i = 0; i < n; ++i) {
+    int64_t cnt = 0;
+    const bool e = elig(i, cnt);
+    if (g0 >= 0 && e && cnt == gcnt && i - g0 < max_group) continue;
+    if (g0 >= 0) emit_group(g0, i);
+    g0 = -1;
+    if (e) {
+      g0 = i;
+      gcnt = cnt;
+    } else {
+      out.lets.push_back(s.lets[size_t(i)]);
+    }
+  }
+  if (g0 >= 0) emit_group(g0, n);
+  s = std::move(out);
+  return st;
+}
+
 // -------------------------------------------------------------------- fusion
 
 struct UseInfo {

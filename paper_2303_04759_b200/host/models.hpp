@@ -33,6 +33,7 @@ struct ModelCfg {
   int save_deriv = 1;       // act linears save act'(u) for the backward instead of u
   double bucket_mb = 25.0;  // ZeRO gradient bucket size (f32 MB; 0: one bucket per segment)
   int zero = 0;             // force the ZeRO data plane at world 1 (identity collectives)
+  int rules = 1;            // rule-based fusion of elementwise runs (ew_closure)
   int flash = 1;            // bf16 attention lse mode: 1 for S > 128, 2 always, 0 never (stored-P path)
   bool zero_on() const { return world > 1 || zero; }
   int64_t vocab_pad() const { return ((V + 63) / 64) * 64; }
@@ -76,6 +77,7 @@ inline ModelCfg parse_cfg(const std::string& s) {
     else if (k == "bucket_mb") c.bucket_mb = D();
     else if (k == "zero") c.zero = int(I());
     else if (k == "flash") c.flash = int(I());
+    else if (k == "rules") c.rules = int(I());
     else throw Error("unknown model config key '" + k + "'");
   }
   if (c.H % c.A) throw TypeError("H must be divisible by A");
@@ -106,6 +108,7 @@ struct TrainStep {
   // its shard state is the concatenation of those slices in bucket order
   std::vector<std::pair<int64_t, int64_t>> buckets;
   int64_t shard_n = 0;
+  int rule_closures = 0;  // ew_closure groups made by finalize_graph
   int64_t shard() const { return shard_n ? shard_n : P_pad / cfg.world; }
 };
 

@@ -28,4 +28,17 @@ inline void apply_autocast(TrainStep& ts, const std::string& key) {
   }
 }
 
+/// The last graph-generation phase (after AutoCast, before memsched and
+/// dispatch): rule-based fusion of elementwise runs into ew_closures
+/// (graph.hpp rule_fuse; key rules=0 disables it).
+inline RuleFuseStats finalize_graph(TrainStep& ts) {
+  RuleFuseStats st;
+  if (!ts.cfg.fuse || !ts.cfg.rules) return st;
+  LetSeq s = ir::flatten(*ts.fn);
+  st = rule_fuse(s);
+  ts.fn = ir::make_fn(ts.fn->name, ts.fn->params, s);
+  ts.rule_closures = st.closures;
+  return st;
+}
+
 }  // namespace tb

@@ -129,6 +129,40 @@ int main() {
     CHECK(p_y.peak <= p_both.peak, "peak %lld vs %lld", (long long)p_y.peak, (long long)p_both.peak);
   }
 
+  // --- materialization_set: tanh's y is in it (NeedsY), its
+  // input u is not; it is exactly the forward tensors the backward lets read;
+  // an inference-only graph has none
+  {
+    const int64_t B = 4, D = 8, C = 16;
+    Graph g;
+    auto x = g.param("x", TensorType{kF32, {B, D}});
+    auto labels = g.param("labels", TensorType{kI32, {B}});
+    auto params = g.param("params", TensorType{kF32, {D * D + D * C}});
+    auto w1 = g.op("view", {params}, {{"offset", std::int64_t(0)}, {"shape", std::string("8,8")}}, "w");
+    auto w2 = g.op("view", {params}, {{"offset", D * D}, {"shape", std::string("8,16")}}, "w");
+    auto u = g.op("matmul", {x, w1}, {}, "u");
+    auto t = g.op("tanh", {u}, {}, "t");
+    auto logits = g.op("matmul", {t, w2}, {}, "logits");
+    auto ce = g.op("cross_entropy", {logits, labels}, {{"classes", C}, {"grad", std::int64_t(1)}});
+    auto loss = g.get(ce, 0, "loss");
+    LetSeq fwd = g.seq();
+    GradResult gr = autodiff(g, loss, {{w1, 0, D * D}, {w2, D * D, D * C}}, D * D + D * C);
+    auto ms = materialization_set(fwd, gr);
+    CHECK(ms.count(t.get()) && !ms.count(u.get()), "tanh: y materialized, x not");
+    CHECK(ms.count(x.get()) && ms.count(w1.get()) && ms.count(w2.get()), "matmul inputs materialized");
+    // dynamic check: exactly the forward vars the backward lets reference
+    std::set<const ir::Var*> fwdv, read;
+    for (auto& b : fwd.lets) fwdv.insert(b.var.get());
+    for (auto& p : {x, labels, params}) fwdv.insert(p.get());
+    auto all = g.seq();
+    for (size_t i = fwd.lets.size(); i < all.lets.size(); ++i)
+      for (auto& a : all.lets[i].value->args)
+        if (a->kind == ExprKind::VarRef && fwdv.count(a->var.get())) read.insert(a->var.get());
+    for (auto* v : ms) CHECK(read.count(v), "materialized var %s is read by the backward", v->id.c_str());
+    GradResult none;
+    CHECK(materialization_set(fwd, none).empty(), "inference-only graph: empty set");
+  }
+
   // --- determinism: two runs, byte-identical text
   {
     std::string t1 = print_text_ext(*build_mlp(true).fn), t2 = print_text_ext(*build_mlp(true).fn);
