@@ -178,6 +178,12 @@ const char* tb_graph_text(const char* cfg, const char* what) {
       for (auto& sp : s.remat.splits)
         os << "split " << sp.victim << " " << sp.evict_index << " " << sp.replay_before << "\n";
       g_text = os.str();
+    } else if (w == "fusion") {  // pattern census: "name priority root matches"
+      std::ostringstream os;
+      for (auto& fp : b200_patterns())
+        os << fp.name << " " << fp.priority << " " << fp.root << " " << s.ts.fusion.by_pattern[fp.name] << "\n";
+      os << "rule.ew_closure 0 - " << s.ts.rule_closures << "\n";
+      g_text = os.str();
     } else if (w == "buckets") {  // ZeRO buckets: "offset numel shard" per line
       std::ostringstream os;
       for (auto [o, n] : s.ts.buckets) os << o << " " << n << " " << (n + s.cfg.world - 1) / s.cfg.world << "\n";

@@ -628,7 +628,35 @@ inline UseInfo count_uses(const LetSeq& s) {
 
 struct FusionStats {
   int dact = 0, ln_dy2 = 0, emb_base = 0, ln_bias = 0, pairs = 0, ce_mask = 0, dead = 0, ln_drop = 0;
+  std::map<std::string, int> by_pattern;  // matches per FusionPattern name
 };
+
+/// The b200 dialect's fusion patterns: a name, a
+/// priority (applied in descending order where roots coincide), the root op
+/// the rooted DAG template starts from, and the template.  Each rewrite lands
+/// on a hand-written b200 fused kernel (the paper's "GEMM + activation"
+/// library-pattern analog).  `disable_patterns` (model cfg key) switches
+/// patterns off by name.
+struct FusionPattern {
+  const char* name;
+  int priority;
+  const char* root;
+  const char* tmpl;
+};
+inline const std::vector<FusionPattern>& b200_patterns() {
+  static const std::vector<FusionPattern> p = {
+      {"b200.dgrad_gelu_epilogue", 30, "gelu_dx", "gelu_dx(u, matmul_t(a, b)) -> matmul_dact(a, b, u){act=gelu}"},
+      {"b200.dgrad_saved_deriv_epilogue", 29, "mul", "mul(matmul_t(a, b), d) -> matmul_dact(a, b, d){act=deriv}"},
+      {"b200.ln_post_dropout", 28, "dropout", "dropout(layer_norm(x, g, b).0) -> layer_norm{post_dropout}.0"},
+      {"b200.ln_dx_in_dropout", 27, "layer_norm_dx", "layer_norm_dx(.., dropout(dy)) -> layer_norm_dx{in_p}(.., dy)"},
+      {"b200.ln_dx_residual_dy2", 26, "layer_norm_dx", "layer_norm_dx(.., add(a, b)) -> layer_norm_dx(.., a, b)"},
+      {"b200.ln_dx_bias_grad", 25, "colsum", "colsum(layer_norm_dx(..).k) -> layer_norm_dx{bias_grad}.last"},
+      {"b200.ce_masked_colsum", 24, "colsum", "colsum(cross_entropy(x, l).1) -> colsum(dlogits, l){ignore_index}"},
+      {"b200.tied_embedding_base", 23, "add", "add(embedding_dx(ids, dy), X) -> embedding_dx(ids, dy, X)"},
+      {"b200.dgrad_wgrad_pair", 20, "matmul_t", "matmul_t(dY, W) ~ matmul_t(X, dY){ta} -> matmul_pair"},
+  };
+  return p;
+}
 
 /// Horizontal fusion (SPEC.md:533-540 applied to GEMMs): a weight-gradient
 /// matmul_t and the nearest bf16 GEMM sharing an operand with it within
@@ -729,8 +757,13 @@ inline int fuse_gemm_pairs(LetSeq& s, int window = 6) {
 
 /// Pattern fusion + dead-let elimination.  Each rewrite needs the absorbed
 /// producer to have exactly one use (SPEC.md:381-388 materialization rule).
-inline FusionStats fuse(LetSeq& s, bool patterns = true) {
+inline FusionStats fuse(LetSeq& s, bool patterns = true, const std::set<std::string>& disabled = {}) {
   FusionStats st;
+  for (auto& fp : b200_patterns()) {
+    if (!opreg::registry().has_base(fp.root)) throw RegistryError(std::string("pattern root op unknown: ") + fp.root);
+    st.by_pattern[fp.name] = 0;
+  }
+  auto on = [&](const char* name) { return !disabled.count(name); };
   UseInfo u = count_uses(s);
   std::unordered_map<const ir::Var*, size_t> def;
   for (size_t i = 0; i < s.lets.size(); ++i) def[s.lets[i].var.get()] = i;
@@ -749,7 +782,7 @@ inline FusionStats fuse(LetSeq& s, bool patterns = true) {
     if (b.value->kind != ExprKind::Call) continue;
     const std::string op = b.value->op;
     // 1. gelu_dx(u, matmul_t(a, b)) -> matmul_dact(a, b, u)   (dact in the dgrad epilogue)
-    if (op == "gelu_dx") {
+    if (op == "gelu_dx" && on("b200.dgrad_gelu_epilogue")) {
       auto src = arg_var(b.value, 1);
       auto* p = producer(src);
       if (p && p->value->op == "matmul_t" && single(src) && ir::attr_double(p->value->call_attrs, "alpha", 1.0) == 1.0 &&
@@ -761,12 +794,13 @@ inline FusionStats fuse(LetSeq& s, bool patterns = true) {
         b.value = call;
         removed.insert(def[src.get()]);
         ++st.dact;
+        ++st.by_pattern["b200.dgrad_gelu_epilogue"];
         continue;
       }
     }
     // 1b. mul(matmul_t(a, b), d) with d = act'(u) saved by linear(save=grad)
     //     -> matmul_dact(a, b, d, act=deriv)   (same shape, no broadcast)
-    if (op == "mul" && b.value->args.size() == 2) {
+    if (op == "mul" && b.value->args.size() == 2 && on("b200.dgrad_saved_deriv_epilogue")) {
       bool done = false;
       for (int side = 0; side < 2 && !done; ++side) {
         auto src = arg_var(b.value, side), other = arg_var(b.value, 1 - side);
@@ -784,13 +818,14 @@ inline FusionStats fuse(LetSeq& s, bool patterns = true) {
         b.value = call;
         removed.insert(def[src.get()]);
         ++st.dact;
+        ++st.by_pattern["b200.dgrad_saved_deriv_epilogue"];
         done = true;
       }
       if (done) continue;
     }
     // 6a. dropout(get(layer_norm(x, g, b), 0)) -> layer_norm {post_dropout} (16-bit):
     //     the LN kernel applies the output dropout (same roundings, one pass)
-    if (op == "dropout" && b.value->args.size() == 1) {
+    if (op == "dropout" && b.value->args.size() == 1 && on("b200.ln_post_dropout")) {
       auto src = arg_var(b.value, 0);
       auto it = src ? def.find(src.get()) : def.end();
       if (it != def.end() && !removed.count(it->second) && s.lets[it->second].value->kind == ExprKind::TupleGet &&
@@ -809,12 +844,14 @@ inline FusionStats fuse(LetSeq& s, bool patterns = true) {
           b.value = e;
           removed.insert(it->second);  // the old get is now unused
           ++st.ln_drop;
+          ++st.by_pattern["b200.ln_post_dropout"];
           continue;
         }
       }
     }
     // 6b. layer_norm_dx(s, g, m, r, dropout(dy)) -> layer_norm_dx {in_p, in_seed, in_salt}
-    if (op == "layer_norm_dx" && b.value->args.size() == 5 && !b.value->call_attrs.count("in_p")) {
+    if (op == "layer_norm_dx" && b.value->args.size() == 5 && !b.value->call_attrs.count("in_p") &&
+        on("b200.ln_dx_in_dropout")) {
       auto src = arg_var(b.value, 4);
       auto* p = producer(src);
       const auto& ty = src ? src->ty : b.var->ty;
@@ -830,12 +867,13 @@ inline FusionStats fuse(LetSeq& s, bool patterns = true) {
         b.value = call;
         removed.insert(def[src.get()]);
         ++st.ln_drop;
+        ++st.by_pattern["b200.ln_dx_in_dropout"];
         continue;
       }
     }
     // 2. layer_norm_dx(s, g, m, r, add(a, b)) -> layer_norm_dx(s, g, m, r, a, b)
     const size_t lnm = op == "layer_norm_dx" && ir::attr_int(b.value->call_attrs, "mask_in", 0) ? 1 : 0;
-    if (op == "layer_norm_dx" && b.value->args.size() == 5 + lnm) {
+    if (op == "layer_norm_dx" && b.value->args.size() == 5 + lnm && on("b200.ln_dx_residual_dy2")) {
       auto src = arg_var(b.value, 4);
       auto* p = producer(src);
       if (p && p->value->op == "add" && single(src)) {
@@ -849,6 +887,7 @@ inline FusionStats fuse(LetSeq& s, bool patterns = true) {
           b.value = call;
           removed.insert(def[src.get()]);
           ++st.ln_dy2;
+          ++st.by_pattern["b200.ln_dx_residual_dy2"];
           continue;
         }
       }
@@ -857,7 +896,7 @@ inline FusionStats fuse(LetSeq& s, bool patterns = true) {
     //    LayerNorm (dx when p > 0, else ds) -> an extra f32 [H] output of
     //    layer_norm_dx (attr bias_grad): the bias gradient of the linear that
     //    fed the LayerNorm, summed in the same row order, with no extra pass
-    if (op == "colsum") {
+    if (op == "colsum" && on("b200.ln_dx_bias_grad")) {
       auto src = arg_var(b.value, 0);
       auto it = src ? def.find(src.get()) : def.end();
       if (it != def.end() && !removed.count(it->second) && s.lets[it->second].value->kind == ExprKind::TupleGet) {
@@ -876,6 +915,7 @@ inline FusionStats fuse(LetSeq& s, bool patterns = true) {
             e->ty = b.value->ty;
             b.value = e;
             ++st.ln_bias;
+            ++st.by_pattern["b200.ln_dx_bias_grad"];
             continue;
           }
         }
@@ -883,7 +923,7 @@ inline FusionStats fuse(LetSeq& s, bool patterns = true) {
     }
     // 5. colsum(get(cross_entropy(logits, labels), 1)) -> colsum(dlogits, labels):
     //    rows with label == ignore_index are exact zeros of dlogits, skip them
-    if (op == "colsum" && b.value->args.size() == 1) {
+    if (op == "colsum" && b.value->args.size() == 1 && on("b200.ce_masked_colsum")) {
       auto src = arg_var(b.value, 0);
       auto it = src ? def.find(src.get()) : def.end();
       if (it != def.end() && s.lets[it->second].value->kind == ExprKind::TupleGet &&
@@ -898,12 +938,13 @@ inline FusionStats fuse(LetSeq& s, bool patterns = true) {
           call->ty = b.value->ty;
           b.value = call;
           ++st.ce_mask;
+          ++st.by_pattern["b200.ce_masked_colsum"];
           continue;
         }
       }
     }
     // 3. add(embedding_dx(ids, dy), X) -> embedding_dx(ids, dy, X)  (tied embeddings)
-    if (op == "add") {
+    if (op == "add" && on("b200.tied_embedding_base")) {
       for (int side = 0; side < 2; ++side) {
         auto src = arg_var(b.value, side), other = arg_var(b.value, 1 - side);
         auto* p = producer(src);
@@ -915,6 +956,7 @@ inline FusionStats fuse(LetSeq& s, bool patterns = true) {
           b.value = call;
           removed.insert(def[src.get()]);
           ++st.emb_base;
+          ++st.by_pattern["b200.tied_embedding_base"];
           break;
         }
       }
@@ -943,7 +985,8 @@ inline FusionStats fuse(LetSeq& s, bool patterns = true) {
     out = std::move(keep);
   }
   s = std::move(out);
-  if (patterns) st.pairs = fuse_gemm_pairs(s);
+  if (patterns && on("b200.dgrad_wgrad_pair")) st.pairs = fuse_gemm_pairs(s);
+  st.by_pattern["b200.dgrad_wgrad_pair"] = st.pairs;
   return st;
 }
 

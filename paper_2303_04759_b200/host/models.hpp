@@ -34,6 +34,7 @@ struct ModelCfg {
   double bucket_mb = 25.0;  // ZeRO gradient bucket size (f32 MB; 0: one bucket per segment)
   int zero = 0;             // force the ZeRO data plane at world 1 (identity collectives)
   int rules = 1;            // rule-based fusion of elementwise runs (ew_closure)
+  std::string disable_patterns;  // comma list of FusionPattern names switched off
   int flash = 1;            // bf16 attention lse mode: 1 for S > 128, 2 always, 0 never (stored-P path)
   bool zero_on() const { return world > 1 || zero; }
   int64_t vocab_pad() const { return ((V + 63) / 64) * 64; }
@@ -78,10 +79,26 @@ inline ModelCfg parse_cfg(const std::string& s) {
     else if (k == "zero") c.zero = int(I());
     else if (k == "flash") c.flash = int(I());
     else if (k == "rules") c.rules = int(I());
+    else if (k == "disable_patterns") c.disable_patterns = v;
     else throw Error("unknown model config key '" + k + "'");
   }
   if (c.H % c.A) throw TypeError("H must be divisible by A");
   return c;
+}
+
+/// the `disable_patterns` key: FusionPattern names (graph.hpp) switched off
+inline std::set<std::string> disabled_patterns(const ModelCfg& c) {
+  std::set<std::string> off;
+  std::istringstream ps(c.disable_patterns);
+  std::string n;
+  while (std::getline(ps, n, ',')) {
+    if (n.empty()) continue;
+    bool known = false;
+    for (auto& fp : b200_patterns()) known = known || n == fp.name;
+    if (!known) throw RegistryError("disable_patterns: no fusion pattern " + n);
+    off.insert(n);
+  }
+  return off;
 }
 
 enum class Init { Uniform, Ones, Zeros };
@@ -468,7 +485,7 @@ inline TrainStep build_train_step(const ModelCfg& c) {
   }
   FunctionPtr raw = g.finish(rets);
   LetSeq seq = ir::flatten(*raw);
-  ts.fusion = fuse(seq, c.fuse != 0);
+  ts.fusion = fuse(seq, c.fuse != 0, disabled_patterns(c));
   ts.fn = ir::make_fn(raw->name, raw->params, seq);
   return ts;
 }

@@ -23,7 +23,7 @@ inline void apply_autocast(TrainStep& ts, const std::string& key) {
   }
   if (k.fuse) {
     LetSeq fs = ir::flatten(*ts.fn);
-    fuse(fs, ts.cfg.fuse != 0);
+    fuse(fs, ts.cfg.fuse != 0, disabled_patterns(ts.cfg));
     ts.fn = ir::make_fn(ts.fn->name, ts.fn->params, fs);
   }
 }

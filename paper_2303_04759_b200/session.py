@@ -114,6 +114,7 @@ class ModelConfig:
     bucket_mb: float = 25.0  # ZeRO gradient bucket (f32 MB; 0: one per parameter segment)
     zero: int = 0            # ZeRO data plane at world 1 (identity collectives, comm stream)
     rules: int = 1           # rule-based fusion of elementwise runs into ew_closure kernels
+    disable_patterns: str = ""  # comma list of b200 FusionPattern names switched off
     flash: int = 1           # bf16 attention lse mode (P recomputed in the bwd): 1 for S > 128, 2 always, 0 never
     extra: dict = field(default_factory=dict)  # runtime keys: budget, schedule, rank
 
