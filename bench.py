@@ -523,8 +523,10 @@ def run_ours(args):
     if rank != 0:
         return
     step_flops = model_flops_per_sample(cfg) * cfg.B
-    prof = step_profile_report(s, peaks, step_flops)
-    prof["roofline_frac_of_replay"] = round(prof["additive_roofline_ms"] / ms, 3)
+    prof = None
+    if world == 1:  # eager profiled steps: at N > 1 every rank would have to join their collectives
+        prof = step_profile_report(s, peaks, step_flops)
+        prof["roofline_frac_of_replay"] = round(prof["additive_roofline_ms"] / ms, 3)
     roof["peak_source"] = peak_kind
     out = {
         "metric": METRIC,
