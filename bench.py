@@ -225,16 +225,19 @@ def gemm_roofline(stream, peaks, iters=50):
     flops = 2.0 * M * N * K
     achieved = flops / (ms * 1e-3) / 1e12
     peak = peaks.get("bf16_tflops", FALLBACK_PEAKS["bf16_tflops"])
-    # DRAM bytes per launch of this exact kernel from the committed ncu --set full capture
-    traffic = None
+    # DRAM bytes per launch of this exact kernel from the committed ncu --set full
+    # capture taken inside a step (--cache-control none: L2 state as the step leaves it)
+    traffic, algo = None, None
     try:
         with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
-                               "r01_roofline_kernel_ncu.json")) as f:
-            traffic = json.load(f)["traffic_bytes"]
+                               "r02_roofline_kernel_ncu.json")) as f:
+            rec = json.load(f)
+            traffic, algo = rec["traffic_bytes"], rec.get("algorithmic_bytes")
     except (OSError, KeyError, ValueError):
         pass
     return {"bound": "tensor", "achieved": round(achieved, 1), "peak": peak, "unit": "TFLOP/s",
-            "frac": round(achieved / peak, 4), "traffic": traffic,
+            "frac": round(achieved / peak, 4), "traffic": traffic, "traffic_algorithmic_bytes": algo,
+            "traffic_source": "profiles/r02_roofline_kernel_ncu.json (in-step ncu, caches not flushed)",
             "kernel": f"b200.linear tcgen05 {M}x{K}x{N} bf16 (+bias+gelu, act' saved)", "us_per_launch": round(ms * 1e3, 2)}
 
 
@@ -390,7 +393,7 @@ def cpu_baseline_port():
             "sample": f"1 C2 train step at B=1 (S=128, 12 layers, bf16-emulated, Adam): {dt:.1f} s single-thread"}
 
 
-GEMM_OPS = {"linear", "matmul_t", "matmul_dact", "matmul_pair", "batch_matmul", "matmul", "linear_chain"}
+GEMM_OPS = {"linear", "matmul_t", "matmul_dact", "matmul_pair", "batch_matmul", "matmul"}
 
 
 def step_profile_report(s, peaks, step_flops, repeats=5):

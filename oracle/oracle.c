@@ -1190,9 +1190,6 @@ int orc_exec(const char* op, const orc_tensor* in, int nin, orc_tensor* out, int
                save_grad);
     return 0;
   }
-  /* linear_chain(x, W1, b1, W2, b2) -> (y1 [, u1], y2): the two linears in
-   * sequence (the device runs them as one chained launch); y2 reads the
-   * ROUNDED y1 exactly like a separate second linear would. */
   /* embedding_sum(ids.., tables..): gathers added in table order, each sum
    * rounded to the tables' dtype (= the embedding / add chain it replaces) */
   if (!strcmp(op, "embedding_sum")) {
@@ -1206,16 +1203,6 @@ int orc_exec(const char* op, const orc_tensor* in, int nin, orc_tensor* out, int
           acc = rnd(out[0].dtype, acc + F(&in[n + k])[(int64_t)((const int32_t*)in[k].ptr)[t] * H + j]);
         F(&out[0])[t * H + j] = rnd(out[0].dtype, acc);
       }
-    return 0;
-  }
-  if (!strcmp(op, "linear_chain")) {
-    if (nin != 5 || (nout != 2 && nout != 3)) return fail("linear_chain: 5 inputs, 2-3 outputs");
-    int act = parse_act(astr(A, na, "act", "none")), act2 = parse_act(astr(A, na, "act2", "none"));
-    if (act < 0 || act2 < 0) return fail("linear_chain: bad act");
-    const int save_grad = !strcmp(astr(A, na, "save", "preact"), "grad");
-    linear_fwd(&in[0], &in[1], &in[2], &out[0], nout > 2 ? &out[1] : NULL, act, (int)aint(A, na, "tw", 0),
-               save_grad);
-    linear_fwd(&out[0], &in[3], &in[4], &out[nout - 1], NULL, act2, (int)aint(A, na, "tw2", 0), 0);
     return 0;
   }
   /* matmul_pair(a0, b0 [, aux0], a1, b1): problem 0 is matmul_t (n0 = 2) or

@@ -39,21 +39,17 @@ struct GemmArgs {
   void* aux_out = nullptr;     // pre-activation store, same layout/dtype as C
   int save_grad = 0;           // aux_out holds act'(pre-activation) instead (consumed with ACT_DERIV)
   int force_bn = 0, force_cg = 0;  // tcgen05 tile override (tests / tuning); 0 = cost model
-  int force_splits = 0;            // split-K ways (cluster of CG x splits CTAs, DSMEM reduction)
   void* trace = nullptr;           // optional per-CTA timeline buffer (12 x u64 per CTA, tooling)
   int no_tma_epi = 0;              // force the direct-store epilogue (tooling)
   const int* sched = nullptr;      // device LPT schedule of a pair launch (gemm_pair_schedule)
   int sched_rounds = 0;
   int wsplit = 1;                  // > 1: c is a [wsplit][M][N] f32 workspace of K-slice partials
-  int* dep_signal = nullptr;       // chained launch: per-row-block completion counters this problem signals
-  const int* dep_wait = nullptr;   // ... or waits on (>= dep_need) before loading A
-  int dep_need = 0;
 };
 
 struct TcChoice {
-  int bn, cg, splits;
+  int bn, cg;
 };
-// plan-owned state of a prepared GEMM (none needed today: split-K reduces on chip)
+// plan-owned state of a prepared GEMM (none needed today)
 struct GemmWs {};
 
 // Launch helpers (defined in the .cu files)
@@ -65,19 +61,14 @@ void launch_gemm_tc(const GemmArgs& g, cudaStream_t s);
 void launch_gemm_tc_pair(const GemmArgs& g0, const GemmArgs& g1, cudaStream_t s);
 // host-side longest-processing-time unit schedule for a pair launch
 std::vector<int> gemm_pair_schedule(const GemmArgs& g0, const GemmArgs& g1, int* rounds);
-// chained pair: problem 1 reads problem 0's output as A (row-block counters)
-void launch_gemm_tc_chain(const GemmArgs& g0, const GemmArgs& g1, cudaStream_t s);
-std::vector<int> gemm_chain_schedule(const GemmArgs& g0, const GemmArgs& g1, int* rounds);
-int gemm_chain_need(const GemmArgs& g0, const GemmArgs& g1);
 // K slices for problem idx of a pair (1 = none); partials then need
 // launch_wsplit_reduce into the real output
 int gemm_pair_wsplit(GemmArgs g0, GemmArgs g1, int idx);
 bool gemm_wsplit_ok(const GemmArgs& g, int S);
 void launch_wsplit_reduce(const float* ws, float* out, int64_t n, int S, cudaStream_t s);
-// cost-model choice of tile shape / CTA pairing / split-K for a problem
+// cost-model choice of tile shape / CTA pairing for a problem
 TcChoice gemm_tc_choose(const GemmArgs& g);
-// plan-time: freeze the tile choice and allocate split-K scratch (no-op for the
-// exact kernel).  Problems built at launch time skip this and never split.
+// plan-time: freeze the tile choice (no-op for the exact kernel).
 void gemm_prepare(GemmArgs& g, bool exact, GemmWs& keep);
 
 // Fused short-sequence attention (k_attention.cu): bf16, head dim 64, S <= 128

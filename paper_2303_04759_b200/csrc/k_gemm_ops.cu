@@ -46,7 +46,6 @@ static GemmArgs gemm2d(const Spec& A, const Spec& B, int ta, int tb, const Spec&
 static void tile_attrs(GemmArgs& g, const Plan& p) {
   g.force_bn = int(p.attrs.i("tc_bn", 0));
   g.force_cg = int(p.attrs.i("tc_cg", 0));
-  g.force_splits = int(p.attrs.i("tc_splits", 0));
   g.trace = reinterpret_cast<void*>(p.attrs.i("tc_trace", 0));  // tooling only
   g.no_tma_epi = int(p.attrs.i("tc_notma", 0));
 }
@@ -113,75 +112,6 @@ static void b_linear(Plan& p) {
   };
 }
 TCB_REGISTER("linear", b_linear);
-
-// linear_chain(x, W1, b1, W2, b2) -> (y1 [, u1], y2): y1 = act(x W1 + b1)
-// (u1 = the saved pre-activation or act'(.) as in linear), y2 = y1 W2 + b2.
-// One persistent tcgen05 launch: problem 1's tiles of row block m start as
-// soon as problem 0's tiles of m are stored (row-block counters), so FFN2
-// fills the SMs FFN1's epilogue-bound tail leaves idle.  Exact / non-bf16
-// configurations run the two linears back to back.
-static void b_linear_chain(Plan& p) {
-  check_arity(p, 5, 5, 2, 3);
-  const bool save = p.out.size() > 2;
-  const Spec& Y1 = p.out[0];
-  GemmArgs g0 = gemm2d(p.in[0], p.in[1], 0, int(p.attrs.i("tw", 0)), Y1, "linear_chain");
-  GemmArgs g1 = gemm2d(Y1, p.in[3], 0, int(p.attrs.i("tw2", 0)), p.out[save ? 2 : 1], "linear_chain");
-  require(p.in[2].numel() == g0.N && p.in[4].numel() == g1.N, "linear_chain: bias sizes");
-  require(Y1.dtype == p.in[0].dtype, "linear_chain: y1 must have the operands' dtype");
-  g0.bias_dtype = p.in[2].dtype;
-  g1.bias_dtype = p.in[4].dtype;
-  g0.act = parse_act(p.attrs.s("act", "none"));
-  g1.act = parse_act(p.attrs.s("act2", "none"));
-  if (save) require(same_shape(p.out[1], Y1) && p.out[1].dtype == Y1.dtype, "linear_chain: u1 must match y1");
-  const std::string what = p.attrs.s("save", "preact");
-  require(what == "preact" || what == "grad", "linear_chain: save must be preact or grad");
-  g0.save_grad = (save && what == "grad") ? 1 : 0;
-  const bool exact = want_exact(p) || p.in[0].dtype != TCB_BF16;
-  std::shared_ptr<Scratch> sched;  // read-only schedule table
-  size_t counters = 0;             // row-block counters (workspace)
-  const int64_t mbl = (g0.M + 255) / 256 + 1;
-  if (!exact) {
-    int rounds = 0;
-    std::vector<int> table = gemm_chain_schedule(g0, g1, &rounds);
-    sched = std::make_shared<Scratch>(table.size() * sizeof(int));
-    TCB_CUDA(cudaMemcpy(sched->p, table.data(), table.size() * sizeof(int), cudaMemcpyHostToDevice));
-    counters = p.ws_take(size_t(mbl) * sizeof(int));
-    g0.sched = static_cast<const int*>(sched->p);
-    g0.sched_rounds = rounds;
-    g1.dep_need = gemm_chain_need(g0, g1);
-  }
-  p.nkernels = exact ? 2 : 1;  // the chained GEMM (its counter reset is a memset node), or two linears
-  GemmWs keep;
-  if (exact) {
-    gemm_prepare(g0, true, keep);
-    gemm_prepare(g1, true, keep);
-  }
-  p.run = [g0, g1, exact, save, sched, counters, mbl](const tcb_tensor* in, tcb_tensor* out,
-                                                       cudaStream_t s) mutable {
-    g0.a.ptr = in[0].ptr;
-    g0.b.ptr = in[1].ptr;
-    g0.bias = in[2].ptr;
-    g0.c = out[0].ptr;
-    g0.aux_out = save ? out[1].ptr : nullptr;
-    g1.a.ptr = out[0].ptr;
-    g1.b.ptr = in[3].ptr;
-    g1.bias = in[4].ptr;
-    g1.c = out[save ? 2 : 1].ptr;
-    if (!exact && gemm_tc_supported(g0, nullptr) && gemm_tc_supported(g1, nullptr)) {
-      g0.dep_signal = static_cast<int*>(ws_at(counters));
-      g1.dep_wait = static_cast<const int*>(ws_at(counters));
-      TCB_CUDA(cudaMemsetAsync(ws_at(counters), 0, size_t(mbl) * sizeof(int), s));
-      launch_gemm_tc_chain(g0, g1, s);
-    } else {
-      g0.dep_signal = nullptr;
-      g1.dep_wait = nullptr;
-      g0.sched = nullptr;
-      launch_gemm(g0, exact, s);
-      launch_gemm(g1, exact, s);
-    }
-  };
-}
-TCB_REGISTER("linear_chain", b_linear_chain);
 
 static void b_matmul_dact(Plan& p) {
   check_arity(p, 3, 3, 1, 1);

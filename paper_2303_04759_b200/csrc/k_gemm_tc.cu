@@ -68,18 +68,12 @@ struct TcProb {
   int ta, tb;
   int m_blocks, n_blocks, k_blocks;  // m_blocks counts (128*CG)-row blocks
   int64_t num_tiles;
-  int kps;  // k-blocks per K split
+  int kps;  // k-blocks per unit (a K slice with wsplit > 1, else the whole K)
   // > 1: the problem's K is cut into wsplit slices run as separate units; unit
   // (s, tile) accumulates k-blocks [s*kps, +kps) and stores its f32 partial tile
   // to slice s of a [wsplit][M][N] workspace (C map Z2 = wsplit), which a fixed-
   // order reduction kernel sums afterwards (deterministic)
   int wsplit;
-  // chained launch (problem 1 reads problem 0's output as its A operand):
-  // problem 0 adds 1 to sig[mb] per epilogue warp once its stores of a tile
-  // of row block mb completed; problem 1's producer waits for dep[mb] >= need
-  int* sig;
-  const int* dep;
-  int dep_need;
   uint32_t idesc;
   // epilogue
   void* c;
@@ -103,10 +97,6 @@ struct TcProb {
 struct TcParams {
   TcProb pr[2];
   int nprob;
-  // split-K (single problem): a cluster of CG x splits CTAs owns one tile; CTA
-  // split s covers k-blocks [s*kps, +kps), then the partial accumulators are
-  // exchanged through distributed shared memory and reduced in split order
-  int splits;
   int64_t num_units;
   // optional static schedule: cluster c runs units sched[c], sched[c + n_cl],
   // ... up to the first -1 (longest-processing-time balanced on the host);
@@ -369,13 +359,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(abar + TC_AUX_RING * TC_EPI_WARPS);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const bool clustered = CG == 2 || P.splits > 1;
+  constexpr bool clustered = CG == 2;
   const uint32_t crank = clustered ? cluster_ctarank() : 0;
   const uint32_t rank = crank % CG;          // position in the CTA pair
   const uint32_t lead = crank - rank;        // the pair leader's cluster rank
-  const int split = int(crank / CG);         // K split (0 without split-K)
-  const int csz = CG * P.splits;
-  const int64_t cl_id = blockIdx.x / csz, n_cl = gridDim.x / csz;
+  const int64_t cl_id = blockIdx.x / CG, n_cl = gridDim.x / CG;
   const uint16_t mcast = uint16_t(3u << lead);
   unsigned long long* tr = P.trace ? P.trace + blockIdx.x * 12 : nullptr;
   if (tr && threadIdx.x == 0) tr[0] = gtimer();
@@ -435,11 +423,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const int64_t t = u - (prob ? P.pr[0].num_tiles : 0);
         int z, mb, nb;
         decode_tile(Q, t, z, mb, nb);
-        const int kb0 = (Q.wsplit > 1 ? z : split) * Q.kps;
+        const int kb0 = (Q.wsplit > 1 ? z : 0) * Q.kps;
         const int kb1 = min(kb0 + Q.kps, Q.k_blocks);
         if (Q.wsplit > 1) z = 0;  // z is the K slice, not a batch index
         const int z1 = int(z / Q.Z2), z2 = int(z % Q.Z2);
-        if (Q.dep) dep_wait(Q.dep + mb, Q.dep_need);  // the A rows come from problem 0's tiles
         const int m0 = mb * (TC_BM * CG) + int(rank) * TC_BM;
         const int n0 = nb * BN + int(rank) * C::B_ROWS;
         for (int kb = kb0; kb < kb1; ++kb) {
@@ -481,7 +468,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       for (int64_t ui = 0, u; (u = unit_at(P, cl_id, n_cl, ui)) >= 0; ++ui) {
         const int prob = unit_prob(P, u);
         const TcProb& Q = P.pr[prob];
-        int kb0 = split * Q.kps;
+        int kb0 = 0;
         if (Q.wsplit > 1) {
           int z, mb, nb;
           decode_tile(Q, u - (prob ? P.pr[0].num_tiles : 0), z, mb, nb);
@@ -678,53 +665,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       if (tr && ew == 0 && ui == 0) tr[4] = gtimer();
-      if (P.splits > 1) {
-        // ---- split-K: partial accumulators -> owners through DSMEM.  Chunk c
-        // of the tile belongs to split c % S of the same pair rank; an owner's
-        // receive buffer (its idle operand stages) is [src split][q][c / S][lane][W].
-        const int S = P.splits, npc = NCH / S;
-        float* recv = reinterpret_cast<float*>(sA);
-        cluster_sync_na();  // every accumulator final, every operand ring idle
-#pragma unroll 1
-        for (int c = sub; c < NCH; c += SPLIT) {
-          if (int64_t(nb) * BN + c * W >= Q.N) continue;
-          uint32_t r[W];
-          const uint32_t taddr = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(c * W);
-          if constexpr (W == 16) TMEM_LD16(taddr, r);
-          else TMEM_LD32(taddr, r);
-          tmem_wait_ld();
-          const int owner = (c % S) * CG + int(rank);
-          const uint32_t dst = mapa(smem_u32(recv + (((split * 4 + q) * npc + c / S) * 32 + lane) * W), owner);
-#pragma unroll
-          for (int j = 0; j < W / 4; ++j)
-            asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(dst + 16 * j), "r"(r[4 * j]),
-                         "r"(r[4 * j + 1]), "r"(r[4 * j + 2]), "r"(r[4 * j + 3])
-                         : "memory");
-        }
-        cluster_sync_na();  // all partials landed
-#pragma unroll 1
-        for (int lc = sub; lc < npc; lc += SPLIT) {
-          const int c = lc * S + split;
-          const int64_t n0 = int64_t(nb) * BN + c * W;
-          if (n0 >= Q.N) continue;
-          float v[W];
-#pragma unroll
-          for (int j = 0; j < W; ++j) v[j] = 0.0f;
-          for (int sp = 0; sp < S; ++sp) {  // fixed split order: deterministic
-            const float4* src = reinterpret_cast<const float4*>(recv + (((sp * 4 + q) * npc + lc) * 32 + lane) * W);
-#pragma unroll
-            for (int j = 0; j < W / 4; ++j) {
-              const float4 x = src[j];
-              v[4 * j] += x.x;
-              v[4 * j + 1] += x.y;
-              v[4 * j + 2] += x.z;
-              v[4 * j + 3] += x.w;
-            }
-          }
-          finish(v, 0, n0);
-        }
-        continue;  // one tile per cluster: nothing to release
-      }
 #pragma unroll 1
       for (int c = sub, ci = 0; c < NCH; c += SPLIT, ++ci) {
         const int64_t n0 = int64_t(nb) * BN + c * W;
@@ -740,13 +680,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         finish(v, ci, n0);
       }
       if (tr && ew == 0 && lane == 0 && ui == 0) tr[6] = gtimer();
-      if (Q.sig) {  // publish this warp's part of the tile once its stores landed
-        if (lane == 0) {
-          bulk_wait_all();
-          dep_signal(Q.sig + mb);
-        }
-        __syncwarp();
-      }
       // release the accumulator to the (leader's) MMA warp
       tc_fence_before();
       __syncwarp();
@@ -762,10 +695,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
     if (lane == 0) bulk_wait_all();
     if (tr && lane == 0) atomicMax(&tr[5], gtimer());
-  }
-  if (P.splits > 1 && warp < 4) {  // the two split-K exchange barriers
-    cluster_sync_na();
-    cluster_sync_na();
   }
   tc_fence_before();
   if (clustered) cluster_sync();
@@ -820,7 +749,7 @@ static bool epi_tma_ok(const GemmArgs& g) {
 
 // one problem's kernel parameters and tensor maps for tile shape (BN, CG)
 template <int BN, int CG, bool AUX>
-static void fill_prob(const GemmArgs& g, int splits, TcProb& P, CUtensorMap& ta, CUtensorMap& tb, EpiMaps& em) {
+static void fill_prob(const GemmArgs& g, TcProb& P, CUtensorMap& ta, CUtensorMap& tb, EpiMaps& em) {
   using C = TcCfg<BN, CG, AUX>;
   P.M = g.M;
   P.N = g.N;
@@ -834,7 +763,7 @@ static void fill_prob(const GemmArgs& g, int splits, TcProb& P, CUtensorMap& ta,
   P.k_blocks = int((g.K + TC_BK - 1) / TC_BK);
   P.wsplit = g.wsplit > 1 ? g.wsplit : 1;
   P.num_tiles = int64_t(P.m_blocks) * P.n_blocks * g.Z * P.wsplit;
-  P.kps = (P.k_blocks + splits * P.wsplit - 1) / (splits * P.wsplit);
+  P.kps = (P.k_blocks + P.wsplit - 1) / P.wsplit;
   P.idesc = umma_idesc(TC_BM * CG, BN, g.a.dtype == TCB_BF16, g.ta != 0, g.tb == 0);
   P.c = g.c;
   P.ldc = g.ldc;
@@ -850,9 +779,6 @@ static void fill_prob(const GemmArgs& g, int splits, TcProb& P, CUtensorMap& ta,
   P.aux_dtype = g.aux_dtype;
   P.aux_out = g.aux_out;
   P.save_grad = g.aux_out ? g.save_grad : 0;
-  P.sig = g.dep_signal;
-  P.dep = g.dep_wait;
-  P.dep_need = g.dep_need;
   const int es = dtype_bytes(g.c_dtype);
   P.c_vec_ok = (reinterpret_cast<uintptr_t>(g.c) % 16 == 0) && ((g.ldc * es) % 16 == 0) &&
                ((g.c_s1 * es) % 16 == 0) && ((g.c_s2 * es) % 16 == 0) &&
@@ -890,11 +816,10 @@ static void launch_cfg(const GemmArgs* gs, int n, cudaStream_t s) {
   });
   TcParams P{};
   P.nprob = n;
-  P.splits = (n == 1 && gs[0].force_splits > 1) ? gs[0].force_splits : 1;
   P.trace = reinterpret_cast<unsigned long long*>(gs[0].trace);
   CUtensorMap ta[2], tb[2];
   EpiMaps em[2];
-  for (int i = 0; i < n; ++i) fill_prob<BN, CG, AUX>(gs[i], P.splits, P.pr[i], ta[i], tb[i], em[i]);
+  for (int i = 0; i < n; ++i) fill_prob<BN, CG, AUX>(gs[i], P.pr[i], ta[i], tb[i], em[i]);
   if (n == 1) {
     ta[1] = ta[0];
     tb[1] = tb[0];
@@ -903,15 +828,9 @@ static void launch_cfg(const GemmArgs* gs, int n, cudaStream_t s) {
   P.num_units = P.pr[0].num_tiles + (n > 1 ? P.pr[1].num_tiles : 0);
   P.sched = gs[0].sched;
   P.sched_rounds = gs[0].sched_rounds;
-  const int csz = CG * P.splits;  // cluster: CTA pair x K splits
-  int grid;
-  if (P.splits > 1) {
-    grid = int(P.num_units * csz);  // one tile per cluster (the exchange reuses its operand ring)
-  } else {
-    const int64_t units = P.num_units * CG;
-    grid = int(units < kNumSMs ? units : kNumSMs);
-    grid = (grid / CG) * CG;
-  }
+  const int64_t units = P.num_units * CG;
+  int grid = int(units < kNumSMs ? units : kNumSMs);
+  grid = (grid / CG) * CG;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(unsigned(grid));
   cfg.blockDim = dim3(TC_THREADS);
@@ -919,7 +838,7 @@ static void launch_cfg(const GemmArgs* gs, int n, cudaStream_t s) {
   cfg.stream = s;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = csz;
+  attr[0].val.clusterDim.x = CG;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
@@ -929,7 +848,7 @@ static void launch_cfg(const GemmArgs* gs, int n, cudaStream_t s) {
 
 // Tile configuration by a wave-quantised cost model (calibrated on the
 // BERT-base shapes, profiles/r01_gemm_tile_sweep.jsonl):
-//   time ~ rounds * (kps + K_FIX) * BN / eff(CG, BN)  (+ split-K reduction)
+//   time ~ rounds * (kps + K_FIX) * BN / eff(CG, BN)
 // rounds = ceil(units / concurrent units), a CTA pair is one unit of 74;
 // K_FIX k-blocks model the per-unit fill/drain; eff(.) is the relative
 // mainloop throughput per SM of each tile shape.
@@ -939,26 +858,16 @@ static int stages_of(int bn, int cg) {
   const int budget = 227 * 1024 - 1024 - 1024 - TC_EPI_WARPS * out_ring<false>() * TC_SLOT - TC_EPI_WARPS * cpw * TC_EW * 4;
   return std::min(8, budget / stage_bytes(bn, cg));
 }
-// split-K through DSMEM: pure matmul epilogue, cluster <= 8 CTAs, whole
-// chunks per owner, and the receive buffer fits the operand ring
-static bool split_ok(const GemmArgs& g, int bn, int cg, int sp) {
-  if (sp == 1) return true;
-  const int64_t kblocks = (g.K + TC_BK - 1) / TC_BK;
-  return (sp == 2 || sp == 4) && cg * sp <= 8 && (bn / TC_EW) % sp == 0 && kblocks >= 2 * sp && !g.bias &&
-         g.act == ACT_NONE && g.dact == ACT_NONE && !g.aux_out &&
-         (bn / TC_EW) * 8192 <= stages_of(bn, cg) * stage_bytes(bn, cg);
-}
-
-static TcChoice choose(const GemmArgs& g, bool allow_split) {
-  if (g.force_bn) return {g.force_bn, g.force_cg ? g.force_cg : 1, g.force_splits ? g.force_splits : 1};
+static TcChoice choose(const GemmArgs& g) {
+  if (g.force_bn) return {g.force_bn, g.force_cg ? g.force_cg : 1};
   struct Cand {
     int bn, cg;
     double eff;
   };
   const Cand cands[] = {{256, 2, 1.0}, {192, 2, 0.85}, {128, 2, 0.6}, {256, 1, 0.75}, {192, 1, 0.7}, {128, 1, 0.55}};
   const int64_t kblocks = (g.K + TC_BK - 1) / TC_BK;
-  constexpr double K_FIX = 6.0, K_RED = 2.0;
-  TcChoice best{128, 1, 1};
+  constexpr double K_FIX = 6.0;
+  TcChoice best{128, 1};
   double best_cost = 1e30;
   for (const Cand& c : cands) {
     if (c.bn > 128 && g.N <= 128) continue;
@@ -967,34 +876,24 @@ static TcChoice choose(const GemmArgs& g, bool allow_split) {
     const int64_t nb = (g.N + c.bn - 1) / c.bn;
     const int64_t tiles = mb * nb * g.Z;
     const int64_t conc = kNumSMs / c.cg;
-    for (int sp : {1, 2, 4}) {
-      if (sp > 1 && (!allow_split || !split_ok(g, c.bn, c.cg, sp) || tiles * sp > conc)) continue;
-      const int64_t kps = (kblocks + sp - 1) / sp;
-      const int64_t units = tiles * sp;
-      const double rounds = double((units + conc - 1) / conc);
-      const double cost = rounds * (double(kps) + K_FIX + (sp > 1 ? K_RED : 0.0)) * double(c.bn) / c.eff;
-      if (cost < best_cost * 0.97) {
-        best_cost = cost;
-        best = {c.bn, c.cg, sp};
-      }
+    const double rounds = double((tiles + conc - 1) / conc);
+    const double cost = rounds * (double(kblocks) + K_FIX) * double(c.bn) / c.eff;
+    if (cost < best_cost * 0.97) {
+      best_cost = cost;
+      best = {c.bn, c.cg};
     }
   }
   return best;
 }
 
-TcChoice gemm_tc_choose(const GemmArgs& g) { return choose(g, true); }
+TcChoice gemm_tc_choose(const GemmArgs& g) { return choose(g); }
 
 void gemm_prepare(GemmArgs& g, bool exact, GemmWs& keep) {
   (void)keep;
   if (exact || !gemm_tc_supported(g, nullptr)) return;
-  // Split-K is exact and deterministic (tests force it) but measured slower on
-  // every BERT-base weight-gradient shape (profiles/r01_gemm_splitk_dsmem.jsonl):
-  // those GEMMs are bound by L2->SMEM operand traffic, which splitting K does
-  // not reduce.  The cost model therefore never picks it on its own.
-  const TcChoice c = choose(g, false);
+  const TcChoice c = choose(g);
   g.force_bn = c.bn;
   g.force_cg = c.cg;
-  g.force_splits = c.splits;
 }
 
 static void dispatch_tc(const GemmArgs* gs, int n, const TcChoice& c, cudaStream_t s) {
@@ -1019,16 +918,13 @@ static void dispatch_tc(const GemmArgs* gs, int n, const TcChoice& c, cudaStream
 void launch_gemm_tc(const GemmArgs& g, cudaStream_t s) {
   std::string why;
   if (!gemm_tc_supported(g, &why)) fail(TCB_ERR_UNIMPLEMENTED, "tcgen05 gemm: " + why);
-  const TcChoice c = choose(g, false);
-  if (!split_ok(g, c.bn, c.cg, c.splits))
-    fail(TCB_ERR_TYPE, "tcgen05 gemm: split-K " + std::to_string(c.splits) + " not valid for this tile / epilogue");
-  dispatch_tc(&g, 1, c, s);
+  dispatch_tc(&g, 1, choose(g), s);
 }
 
-// Two independent problems in one grid (same tile shape, no split-K); the
+// Two independent problems in one grid (same tile shape); the
 // problem with more k-blocks per tile goes first.
 static TcChoice pair_choice(const GemmArgs& g0, const GemmArgs& g1) {
-  TcChoice c{g0.force_bn ? g0.force_bn : 256, g0.force_cg ? g0.force_cg : 2, 1};
+  TcChoice c{g0.force_bn ? g0.force_bn : 256, g0.force_cg ? g0.force_cg : 2};
   if (c.cg == 2 && (g0.M <= 128 || g1.M <= 128)) c.cg = 1;
   return c;
 }
@@ -1088,77 +984,6 @@ static std::vector<int> lpt_table(const GemmArgs& g0, const GemmArgs& g1, int* r
 }
 std::vector<int> gemm_pair_schedule(const GemmArgs& g0, const GemmArgs& g1, int* rounds) {
   return lpt_table(g0, g1, rounds, nullptr);
-}
-
-// Chained launch: problem 1's A operand is problem 0's output (FFN1 -> FFN2).
-// Same tile shape for both; no swap.  Host list schedule over clusters in
-// k-block time units: problem-0 tiles in row-block-major order; a problem-1
-// tile of row block m becomes eligible once all of m's problem-0 tiles are
-// placed, and is ready at their estimated completion (MMA end + epilogue).  A
-// cluster takes a ready problem-1 tile first, else the next problem-0 tile,
-// else the earliest problem-1 tile (waiting for it).  Every unit is appended
-// after all units it depends on were appended somewhere, so with all CTAs
-// co-resident no cluster ever waits on work queued behind itself.
-static std::vector<int> chain_table(const GemmArgs& g0, const GemmArgs& g1, int* rounds, double* max_load) {
-  const TcChoice c = pair_choice(g0, g1);
-  const int64_t mb = (g0.M + 128 * c.cg - 1) / (128 * c.cg);
-  const int64_t nb0 = (g0.N + c.bn - 1) / c.bn, nb1 = (g1.N + c.bn - 1) / c.bn;
-  const int64_t t0 = mb * nb0, t1 = mb * nb1;
-  const double kb0 = double((g0.K + TC_BK - 1) / TC_BK), kb1 = double((g1.K + TC_BK - 1) / TC_BK);
-  const double epi0 = (g0.act == ACT_GELU || g0.dact != ACT_NONE) ? 20.0 : 6.0;  // epilogue length, k-block units
-  const int64_t total = (t0 + t1) * c.cg;
-  int grid = int(total < kNumSMs ? total : kNumSMs);
-  grid = (grid / c.cg) * c.cg;
-  const int ncl = grid / c.cg;
-  std::vector<double> avail(ncl, 0.0), ready(mb, 0.0);
-  std::vector<int> placed(mb, 0);
-  std::vector<std::vector<int>> lists(ncl);
-  std::vector<int64_t> next_nb1(mb, 0);  // next problem-1 tile of each row block
-  int64_t next0 = 0, left1 = t1;
-  while (next0 < t0 || left1 > 0) {
-    int cl = 0;
-    for (int k = 1; k < ncl; ++k)
-      if (avail[k] < avail[cl]) cl = k;
-    // earliest-ready eligible problem-1 row block
-    int64_t best_m = -1;
-    for (int64_t m = 0; m < mb; ++m)
-      if (placed[m] == nb0 && next_nb1[m] < nb1 && (best_m < 0 || ready[m] < ready[best_m])) best_m = m;
-    if (best_m >= 0 && (ready[best_m] <= avail[cl] || next0 >= t0)) {
-      const int64_t u = t0 + best_m * nb1 + next_nb1[best_m]++;
-      avail[cl] = std::max(avail[cl], ready[best_m]) + kb1 + 2.0;
-      lists[cl].push_back(int(u));
-      --left1;
-    } else {
-      const int64_t m = next0 / nb0;
-      avail[cl] += kb0;
-      ready[m] = std::max(ready[m], avail[cl] + epi0);
-      ++placed[m];
-      lists[cl].push_back(int(next0++));
-    }
-  }
-  int r = 0;
-  for (auto& l : lists) r = std::max(r, int(l.size()));
-  std::vector<int> table(size_t(r) * ncl, -1);
-  for (int k = 0; k < ncl; ++k)
-    for (size_t i = 0; i < lists[k].size(); ++i) table[i * ncl + k] = lists[k][i];
-  *rounds = r;
-  if (max_load) *max_load = *std::max_element(avail.begin(), avail.end());
-  return table;
-}
-std::vector<int> gemm_chain_schedule(const GemmArgs& g0, const GemmArgs& g1, int* rounds) {
-  return chain_table(g0, g1, rounds, nullptr);
-}
-int gemm_chain_need(const GemmArgs& g0, const GemmArgs& g1) {
-  const TcChoice c = pair_choice(g0, g1);
-  return int((g0.N + c.bn - 1) / c.bn) * c.cg * TC_EPI_WARPS;
-}
-void launch_gemm_tc_chain(const GemmArgs& g0, const GemmArgs& g1, cudaStream_t s) {
-  std::string why;
-  for (const GemmArgs* g : {&g0, &g1})
-    if (!gemm_tc_supported(*g, &why)) fail(TCB_ERR_UNIMPLEMENTED, "tcgen05 gemm chain: " + why);
-  if (!g0.dep_signal || !g1.dep_wait || !g0.sched) fail(TCB_ERR_ARG, "tcgen05 gemm chain: counters / schedule missing");
-  GemmArgs gs[2] = {g0, g1};
-  dispatch_tc(gs, 2, pair_choice(g0, g1), s);
 }
 
 // K slices for problem `idx` of a pair (a weight gradient whose few long tiles

@@ -117,7 +117,6 @@ static void b_adam(Plan& p) {
             p.attrs.f("eps", 1e-8), p.attrs.f("grad_scale", 1.0)};
   const int64_t n = p.in[0].numel();
   const int hd = p.out.size() > 3 ? p.out[3].dtype : -1;
-  const bool small = p.attrs.i("co_resident", 0) != 0;
   if (hd >= 0) require(is_float(hd), "adam_update_ex: 4th output must be a float copy");
   p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
     for (int i = 0; i < 4; ++i)
@@ -125,10 +124,8 @@ static void b_adam(Plan& p) {
         fail(TCB_ERR_ARG, "adam_update: buffers must be 16-byte aligned");
     if (hd >= 0 && reinterpret_cast<uintptr_t>(out[3].ptr) % 16)
       fail(TCB_ERR_ARG, "adam_update_ex: the parameter copy must be 16-byte aligned");
-    // co_resident: small CTAs that fit beside a GEMM CTA's 61K registers, for
-    // optimizer chunks the VM overlaps with the backward on a side stream
-    const int bs = small ? 64 : 256;
-    const int grid = grid_for((n + 3) / 4, bs, kNumSMs * (small ? 8 : 4));
+    const int bs = 256;
+    const int grid = grid_for((n + 3) / 4, bs, kNumSMs * 4);
     if (hd == TCB_BF16)
       launch_k(k_adam<__nv_bfloat16>, grid, bs, 0, s, 
           (const float*)in[0].ptr, (const float*)in[1].ptr, (const float*)in[2].ptr,

@@ -91,21 +91,6 @@ __device__ __forceinline__ void bulk_wait_read() {
   asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
 }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
-// Cross-CTA tile dependencies (chained GEMMs): the producer side publishes a
-// finished output tile after its TMA stores completed (wait_group 0); the
-// consumer acquires the counter, then orders its TMA (async-proxy) loads after it.
-__device__ __forceinline__ void dep_signal(int* counter) {
-  asm volatile("fence.proxy.async.global;\n\tred.release.gpu.global.add.s32 [%0], 1;" ::"l"(counter) : "memory");
-}
-__device__ __forceinline__ void dep_wait(const int* counter, int need) {
-  int v;
-  for (;;) {
-    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(counter) : "memory");
-    if (v >= need) break;
-    __nanosleep(128);
-  }
-  asm volatile("fence.proxy.async.global;" ::: "memory");
-}
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }

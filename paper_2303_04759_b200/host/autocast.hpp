@@ -58,7 +58,7 @@ struct PrecisionPolicy {
 inline PrecisionPolicy default_policy(DType low = kBF16) {
   PrecisionPolicy p;
   p.low = low;
-  for (const char* o : {"matmul", "matmul_t", "linear", "linear_chain", "matmul_dact", "matmul_pair", "batch_matmul",
+  for (const char* o : {"matmul", "matmul_t", "linear", "matmul_dact", "matmul_pair", "batch_matmul",
                         "attention", "attention_dx"})
     p.by_op[o] = Prec::Low;
   for (const char* o : {"sum", "mean", "mse", "softmax", "softmax_dx", "layer_norm", "add_layer_norm", "layer_norm_dx",

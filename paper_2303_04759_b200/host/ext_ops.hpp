@@ -162,19 +162,6 @@ inline void register_extension_ops(OpRegistry& r) {
     if (rel::a_int(a, "save_preact", 0)) return TupleType{{y, y}};
     return y;
   });
-  // linear_chain(x, W1, b1, W2, b2) -> (y1 [, u1], y2): y1 = act(x W1 + b1)
-  // (u1 with save_preact), y2 = act2(y1 W2 + b2) -- one chained launch
-  reg("linear_chain", 5, O, [](const V& in, const AttrMap& a) -> Type {
-    auto x = rel::T(in[0], "linear_chain"), w1 = rel::T(in[1], "linear_chain");
-    auto b1 = rel::T(in[2], "linear_chain"), w2 = rel::T(in[3], "linear_chain"), b2 = rel::T(in[4], "linear_chain");
-    auto mn1 = gemm_shape(x, w1, 0, int(rel::a_int(a, "tw", 0)), "linear_chain");
-    TensorType y1{x.dtype, mn1};
-    auto mn2 = gemm_shape(y1, w2, 0, int(rel::a_int(a, "tw2", 0)), "linear_chain");
-    if (numel(b1) != mn1[1] || numel(b2) != mn2[1]) throw TypeError("linear_chain: bias sizes");
-    TensorType y2{x.dtype, mn2};
-    if (rel::a_int(a, "save_preact", 0)) return TupleType{{y1, y1, y2}};
-    return TupleType{{y1, y2}};
-  });
   // alpha * op(A) op(B), out dtype attr
   reg("matmul_t", 2, O, [](const V& in, const AttrMap& a) -> Type {
     auto x = rel::T(in[0], "matmul_t"), y = rel::T(in[1], "matmul_t");

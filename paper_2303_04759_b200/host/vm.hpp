@@ -136,8 +136,6 @@ struct Instr {
   OpKind kind = OpKind::Launch;
   std::string op;     // dialect op name
   int let = -1;
-  int side = 0;       // 1: runs on the side stream once main-stream instruction `after` is done
-  int after = -1;
   tcb_plan plan = nullptr;
   std::vector<tcb_tensor> in, out;
   int64_t copy_bytes = 0;
@@ -333,7 +331,6 @@ class DeviceVM {
         code_.push_back(c);
       }
     }
-    overlap_optimizer();
     stats_.instructions = int(code_.size());
     // one launch workspace for the whole (stream-ordered) step: the largest
     // any plan asks for (plans own no mutable device memory)
@@ -354,128 +351,6 @@ class DeviceVM {
     for (auto& x : code_)
       if (x.kind == OpKind::ReduceScatter || x.kind == OpKind::AllGather || x.kind == OpKind::AllReduce)
         has_collectives_ = true;
-  }
-
-  // Early optimizer (world 1): the flat Adam over [P] is split into chunks of
-  // contiguous parameters; each chunk runs on a side stream as soon as the
-  // last main-stream instruction writing its gradient slice is done, so the
-  // memory-bound update overlaps the rest of the backward instead of trailing
-  // it.  Same arithmetic per element; the step counter increment moves to the
-  // front (it reads only the step parameter).  The side stream rejoins the main
-  // stream at the end of the step.
-  void overlap_optimizer() {
-    // measured slower on BERT-base (5392 vs 5441 samples/s: the chunks do not
-    // co-run with the 1-CTA/SM GEMMs), so it is opt-in: TB_OVERLAP_OPT=1
-    const char* env = std::getenv("TB_OVERLAP_OPT");
-    if (!env || env[0] != '1') return;
-    int ai = -1;
-    for (size_t i = 0; i < code_.size(); ++i) {
-      if (code_[i].kind != OpKind::Launch && code_[i].kind != OpKind::Copy) return;  // ZeRO: keep the plain order
-      if (base_name(code_[i].op) == "adam_update_ex" || base_name(code_[i].op) == "adam_update") {
-        if (ai >= 0) return;
-        ai = int(i);
-      }
-    }
-    if (ai < 0) return;
-    Instr adam = code_[ai];
-    if (adam.in.size() != 5 || adam.out.size() < 3) return;
-    const int64_t P = adam.in[1].shape[0];
-    char* g0 = static_cast<char*>(adam.in[1].ptr);
-    // the step increment that feeds Adam: hoist it to the front
-    int si = -1;
-    for (int i = 0; i < ai; ++i)
-      if (code_[i].kind == OpKind::Launch && base_name(code_[i].op) == "add_scalar" && !code_[i].out.empty() &&
-          code_[i].out[0].ptr == adam.in[4].ptr)
-        si = i;
-    if (si < 0) return;
-    // element e may be updated once every main-stream instruction that writes
-    // its gradient or reads its parameter / bf16 copy / moments is done
-    std::vector<int> ready(size_t(P), -1);
-    struct Buf {
-      char* base;
-      int es;
-    };
-    std::vector<Buf> watched = {{g0, 4},
-                                {static_cast<char*>(adam.in[0].ptr), 4},
-                                {static_cast<char*>(adam.in[2].ptr), 4},
-                                {static_cast<char*>(adam.in[3].ptr), 4}};
-    if (adam.out.size() > 3) watched.push_back({static_cast<char*>(adam.out[3].ptr), adam.out[3].dtype == TCB_F32 ? 4 : 2});
-    auto paint = [&](const tcb_tensor& t, int i) {
-      char* a = static_cast<char*>(t.ptr);
-      const int64_t bytes = nbytes_desc(t);
-      for (const Buf& w : watched) {
-        const char *lo = std::max(a, w.base), *hi = std::min(a + bytes, w.base + P * w.es);
-        if (lo >= hi) continue;
-        const int64_t e0 = (lo - w.base) / w.es, e1 = (hi - w.base + w.es - 1) / w.es;
-        for (int64_t e = e0; e < e1; ++e) ready[size_t(e)] = std::max(ready[size_t(e)], i);
-      }
-    };
-    for (int i = 0; i < ai; ++i) {
-      if (i == si) continue;
-      for (auto& o : code_[i].out) paint(o, i);
-      for (auto& x : code_[i].in) paint(x, i);
-    }
-    // chunks: runs of equal readiness merged up to ~P/32 elements, 64-aligned cuts
-    struct Chunk {
-      int64_t a, b;
-      int after;
-    };
-    std::vector<Chunk> ch;
-    const int64_t target = std::max<int64_t>(P / 32, 1 << 16);
-    int64_t a = 0;
-    int mx = ready[0];
-    for (int64_t e = 1; e <= P; ++e) {
-      const bool cut = e == P || (e % 64 == 0 && (e - a >= target || std::abs(ready[size_t(e)] - mx) > 8));
-      if (cut) {
-        ch.push_back({a, e, mx});
-        a = e;
-        if (e < P) mx = ready[size_t(e)];
-      } else if (e < P) {
-        mx = std::max(mx, ready[size_t(e)]);
-      }
-    }
-    std::vector<Instr> out;
-    Instr step = code_[si];
-    out.push_back(step);
-    const auto& call = seq_.lets[size_t(adam.let)].value;
-    AttrMap at = call->call_attrs;
-    at["co_resident"] = std::int64_t(1);
-    std::vector<std::vector<Instr>> after_of(code_.size());
-    for (auto& c : ch) {
-      Instr x = adam;
-      x.side = 1;
-      // a chunk whose gradient is complete before the (hoisted) start runs first
-      x.after = std::max(c.after, -1);
-      const int64_t n = c.b - c.a;
-      std::vector<TensorType> tin, tout;
-      for (size_t k = 0; k < x.in.size(); ++k) {
-        if (k < 4) {
-          x.in[k].shape[0] = n;
-          x.in[k].ptr = static_cast<char*>(x.in[k].ptr) + c.a * 4;
-        }
-        TensorType t{code_dtype(x.in[k].dtype), {x.in[k].shape[0]}};
-        tin.push_back(t);
-      }
-      for (size_t k = 0; k < x.out.size(); ++k) {
-        x.out[k].shape[0] = n;
-        const int es = x.out[k].dtype == TCB_F32 ? 4 : 2;
-        x.out[k].ptr = static_cast<char*>(x.out[k].ptr) + c.a * es;
-        tout.push_back(TensorType{code_dtype(x.out[k].dtype), {n}});
-      }
-      x.plan = get_plan(adam.op, tin, tout, at, device_);
-      x.nkernels = tcb_plan_num_kernels(x.plan);
-      if (x.after < 0) out.push_back(x);  // ready from the start: plain side launch after the hoisted step
-      else after_of[size_t(x.after)].push_back(x);
-    }
-    for (int i = 0; i < int(code_.size()); ++i) {
-      if (i == si || i == ai) continue;
-      out.push_back(code_[i]);
-      for (auto& x : after_of[size_t(i)]) out.push_back(x);
-    }
-    stats_.kernels += int(ch.size()) - adam.nkernels;
-    stats_.kernels_static += int(ch.size()) - adam.nkernels;
-    code_ = std::move(out);
-    side_chunks_ = int(ch.size());
   }
 
   static DType code_dtype(int c) {
@@ -577,29 +452,9 @@ class DeviceVM {
 
  private:
   void enqueue(void* stream) {
-    bool forked = false;
     for (size_t xi = 0; xi < code_.size(); ++xi) {
       auto& x = code_[xi];
       if (x.kind != OpKind::Launch || is_optimizer(x.op)) flush_folds(stream);
-      if (x.side) {
-        if (!side_) {
-          tcb_check(tcb_stream_create(&side_), "side stream");
-          tcb_check(tcb_event_create(&ev_join_), "event");
-        }
-        // fork: everything enqueued on the main stream so far precedes this chunk
-        void* ev = nullptr;
-        if (ev_pool_used_ >= ev_pool_.size()) {
-          tcb_check(tcb_event_create(&ev), "event");
-          ev_pool_.push_back(ev);
-        }
-        ev = ev_pool_[ev_pool_used_++];
-        tcb_check(tcb_event_record(ev, stream), "event record");
-        tcb_check(tcb_stream_wait_event(side_, ev), "stream wait");
-        tcb_check(tcb_launch_ws(x.plan, x.in.data(), int(x.in.size()), x.out.data(), int(x.out.size()), side_ws(),
-                                ws_bytes_, side_), x.op);
-        forked = true;
-        continue;
-      }
       if (x.kind == OpKind::ReduceScatter || x.kind == OpKind::AllGather || x.kind == OpKind::AllReduce) {
         enqueue_collective(x, stream);
         continue;
@@ -635,11 +490,6 @@ class DeviceVM {
       inflight_.clear();
     }
     comm_ev_used_ = 0;
-    if (forked) {  // join: the step ends when the last optimizer chunk is done
-      tcb_check(tcb_event_record(ev_join_, side_), "event record");
-      tcb_check(tcb_stream_wait_event(stream, ev_join_), "stream wait");
-    }
-    ev_pool_used_ = 0;
   }
 
   // ---- the comm stream (distpar overlap_schedule) ----
@@ -726,8 +576,6 @@ class DeviceVM {
   }
 
   void release() {
-    for (void* e : ev_pool_) tcb_event_destroy(e);
-    ev_pool_.clear();
     for (void* e : prof_events_) tcb_event_destroy(e);
     prof_events_.clear();
     for (void* e : comm_ev_) tcb_event_destroy(e);
@@ -735,19 +583,14 @@ class DeviceVM {
     if (comm_stream_) tcb_stream_destroy(comm_stream_);
     comm_stream_ = nullptr;
     inflight_.clear();
-    if (ev_join_) tcb_event_destroy(ev_join_);
-    ev_join_ = nullptr;
-    if (side_) tcb_stream_destroy(side_);
-    side_ = nullptr;
     if (graph_) tcb_graph_destroy(graph_);
     graph_ = nullptr;
     if (arena_base_) tcb_free_arena(arena_base_);
     if (state_base_) tcb_free_arena(state_base_);
     if (ws_) tcb_free_arena(ws_);
-    if (side_ws_) tcb_free_arena(side_ws_);
     if (fold_ctx_) tcb_fold_ctx_destroy(fold_ctx_);
     arena_base_ = state_base_ = nullptr;
-    ws_ = side_ws_ = fold_ctx_ = nullptr;
+    ws_ = fold_ctx_ = nullptr;
     ws_bytes_ = 0;
     has_collectives_ = false;
     code_.clear();
@@ -767,23 +610,12 @@ class DeviceVM {
   std::vector<Instr> code_;
   void* graph_ = nullptr;
   void* comm_ = nullptr;
-  void* side_ = nullptr;       // optimizer side stream
-  void* ev_join_ = nullptr;
-  std::vector<void*> ev_pool_;
-  size_t ev_pool_used_ = 0;
-  int side_chunks_ = 0;
   void* ws_ = nullptr;        // launch workspace of the compute stream
-  void* side_ws_ = nullptr;   // ... and of the optimizer side stream
   uint64_t ws_bytes_ = 0;
   void* fold_ctx_ = nullptr;  // this VM's deferred-fold pool
   bool has_collectives_ = false;
   int world_ = 1;
   void* rng_ptr_ = nullptr;   // the rng_step state (dropout step counter)
-  void* side_ws() {
-    if (!ws_bytes_) return nullptr;
-    if (!side_ws_) tcb_check(tcb_init(device_, ws_bytes_, &side_ws_), "tcb_init(side workspace)");
-    return side_ws_;
-  }
   VMStats stats_;
 };
 

@@ -202,130 +202,6 @@ def test_gemm_tile_variants(mnk, ta, tb, bn, cg):
 
 
 @pytest.mark.parametrize("bn,cg", TILES)
-@pytest.mark.parametrize("splits", [2, 4])
-@pytest.mark.parametrize("ta,tb", [(1, 0), (0, 1)])
-def test_gemm_split_k(bn, cg, splits, ta, tb):
-    """Split-K over a cluster of CG x splits CTAs: partial accumulators are
-    exchanged through distributed shared memory and summed in split order.
-    Oracle parity (ragged K, M, N) and bit-identical repeated launches."""
-    m, n, k = 520, 328, 1000
-    a = rn(k, m) if ta else rn(m, k)
-    b = rn(n, k) if tb else rn(k, n)
-    at = {"ta": ta, "tb": tb, "alpha": 0.5, "tc_bn": bn, "tc_cg": cg, "tc_splits": splits}
-    g, o = run_both("matmul_t", [(a, BF16), (b, BF16)], [((m, n), F32)], at)
-    assert rel_err(g[0], o[0]) < 1e-5, rel_err(g[0], o[0])
-    g, o = run_both("matmul_t", [(a, BF16), (b, BF16)], [((m, n), BF16)], at)
-    assert rel_err(g[0], o[0]) < BF16_TOL
-    from gpu_util import to_torch
-    from paper_2303_04759_b200.runtime import Plan
-    ta_, tb_ = to_torch(a, BF16), to_torch(b, BF16)
-    plan = Plan("matmul_t", [(tuple(ta_.shape), BF16), (tuple(tb_.shape), BF16)], [((m, n), F32)], at)
-    outs = []
-    for _ in range(3):
-        c = torch.empty(m, n, device="cuda")
-        plan.launch([ta_.data_ptr(), tb_.data_ptr()], [c.data_ptr()], torch.cuda.current_stream().cuda_stream)
-        outs.append(c.cpu())
-    assert all(torch.equal(outs[0], x) for x in outs[1:])
-
-
-@pytest.mark.parametrize("dact", [0, 1])
-@pytest.mark.parametrize("tile", [(256, 2), (128, 1)])
-def test_matmul_pair(dact, tile):
-    """Two independent GEMMs in one persistent launch (a linear's data gradient
-    [with act'(aux)] and weight gradient sharing dY), each against the oracle."""
-    T, H, F = 640, 192, 320  # ragged: 640 = 2.5 pair tiles
-    dy, w, x = rn(T, F), rn(H, F), rn(T, H)
-    ins = [(dy, BF16), (w, BF16)]
-    at = {"n0": 2, "ta0": 0, "tb0": 1, "ta1": 1, "tb1": 0, "out1": "f32", "alpha1": 1.0,
-          "tc_bn": tile[0], "tc_cg": tile[1]}
-    if dact:
-        dy, w, u = rn(T, H), rn(F, H), rn(T, F, lo=-3, hi=3)
-        ins = [(dy, BF16), (w, BF16), (u, BF16)]
-        x = rn(T, F)
-        at.update({"n0": 3, "act0": "gelu"})
-        outs = [((T, F), BF16), ((F, H), F32)]
-    else:
-        outs = [((T, H), BF16), ((H, F), F32)]
-    ins += [(x, BF16), (dy, BF16)]
-    g, o = run_both("matmul_pair", ins, outs, at)
-    assert rel_err(g[0], o[0]) < BF16_TOL, rel_err(g[0], o[0])
-    assert rel_err(g[1], o[1]) < 1e-5, rel_err(g[1], o[1])
-
-
-@pytest.mark.parametrize("act", ["gelu", "relu"])
-@pytest.mark.parametrize("tile", [(256, 2), (128, 1), None])
-def test_linear_save_grad_and_deriv_dact(act, tile):
-    """linear(save=grad) stores act'(pre-activation) as its second output; the
-    backward's matmul_dact(act=deriv) multiplies by it (both against the
-    oracle); ragged shapes exercise the direct-store fallback too."""
-    m, k, n = 700, 256, 600
-    x, w, bias = rn(m, k), rn(k, n, lo=-0.1, hi=0.1), rn(n)
-    at = {"act": act, "save": "grad"}
-    if tile:
-        at.update({"tc_bn": tile[0], "tc_cg": tile[1]})
-    g, o = run_both("linear", [(x, BF16), (w, BF16), (bias, F32)], [((m, n), BF16), ((m, n), BF16)], at)
-    assert rel_err(g[0], o[0]) < BF16_TOL and rel_err(g[1], o[1]) < BF16_TOL
-    d = o[1]
-    dy, w2 = rn(m, 320), rn(n, 320)
-    at2 = {"tb": 1, "act": "deriv", **({"tc_bn": tile[0], "tc_cg": tile[1]} if tile else {})}
-    g, o = run_both("matmul_dact", [(dy, BF16), (w2, BF16), (d, BF16)], [((m, n), BF16)], at2)
-    assert rel_err(g[0], o[0]) < BF16_TOL
-
-
-@pytest.mark.parametrize("wsplit", [2, 3, 4])
-@pytest.mark.parametrize("dact", [0, 1])
-def test_matmul_pair_wsplit(wsplit, dact):
-    """The weight gradient cut into K slices (partial tiles in a workspace,
-    reduced in slice order): ragged K (640 = 10 k-blocks) so the last slice is
-    short, against the oracle."""
-    T, H, F = 640, 192, 320
-    dy, w, x = rn(T, F), rn(H, F), rn(T, H)
-    ins = [(dy, BF16), (w, BF16)]
-    at = {"n0": 2, "ta0": 0, "tb0": 1, "ta1": 1, "tb1": 0, "out1": "f32", "wsplit": wsplit}
-    outs = [((T, H), BF16), ((H, F), F32)]
-    if dact:
-        dy, w, u = rn(T, H), rn(F, H), rn(T, F, lo=-3, hi=3)
-        ins = [(dy, BF16), (w, BF16), (u, BF16)]
-        x = rn(T, F)
-        at.update({"n0": 3, "act0": "gelu"})
-        outs = [((T, F), BF16), ((F, H), F32)]
-    ins += [(x, BF16), (dy, BF16)]
-    g, o = run_both("matmul_pair", ins, outs, at)
-    assert rel_err(g[0], o[0]) < BF16_TOL, rel_err(g[0], o[0])
-    assert rel_err(g[1], o[1]) < 1e-5, rel_err(g[1], o[1])
-
-
-def test_matmul_pair_auto_wsplit_bert_proj():
-    """BERT-base attention-projection backward (dgrad 4096x768x768 + wgrad
-    768x768 over 4096 tokens): the planner slices the wgrad's K; checked
-    against float64 products of the same bf16 inputs, and run-to-run bitwise
-    reproducible (fixed slice order)."""
-    from gpu_util import to_torch, from_torch
-    from paper_2303_04759_b200.runtime import run_op
-    T, H = 4096, 768
-    dy, w, x = quantize(rn(T, H), BF16), quantize(rn(H, H, lo=-0.05, hi=0.05), BF16), quantize(rn(T, H), BF16)
-    at = {"n0": 2, "ta0": 0, "tb0": 1, "ta1": 1, "tb1": 0, "out1": "f32"}
-    ins = [to_torch(a, BF16) for a in (dy, w, x, dy)]
-    outs = [((T, H), BF16), ((H, H), F32)]
-    r1 = [from_torch(t) for t in run_op("matmul_pair", ins, outs, at)]
-    r2 = [from_torch(t) for t in run_op("matmul_pair", ins, outs, at)]
-    assert bits_equal(r1[1], r2[1]) and bits_equal(r1[0], r2[0])
-    ref_dw = x.astype(np.float64).T @ dy.astype(np.float64)
-    ref_dx = dy.astype(np.float64) @ w.astype(np.float64).T
-    assert rel_err(r1[1], ref_dw) < 1e-5, rel_err(r1[1], ref_dw)
-    assert rel_err(r1[0], ref_dx) < BF16_TOL
-
-
-def test_gemm_split_k_rejects_fused_epilogue():
-    """Split-K only covers the pure matmul epilogue; asking for it with bias/act fails loudly."""
-    from paper_2303_04759_b200.runtime import TcbError
-    x, w, bias = rn(256, 512), rn(512, 256), rn(256)
-    with pytest.raises(TcbError):
-        run_both("linear", [(x, BF16), (w, BF16), (bias, F32)], [((256, 256), BF16)],
-                 {"act": "gelu", "tc_bn": 128, "tc_cg": 1, "tc_splits": 2})
-
-
-@pytest.mark.parametrize("bn,cg", TILES)
 def test_gemm_tile_variants_epilogues(bn, cg):
     """bias + GeLU + saved pre-activation, and the fused act'(aux) dgrad
     epilogue (aux arrives by TMA), for every tile configuration."""
@@ -642,42 +518,6 @@ def test_unimplemented_is_loud():
         Plan("b200.no_such_op", [((4,), F32)], [((4,), F32)])
     with pytest.raises(UnimplementedOp):
         Plan("ref.add", [((4,), F32), ((4,), F32)], [((4,), F32)])
-
-
-@pytest.mark.parametrize("shape", [(700, 256, 384, 320), (512, 128, 512, 256)])
-@pytest.mark.parametrize("save", ["grad", "preact"])
-def test_linear_chain(shape, save):
-    """FFN1 -> FFN2 as one chained tcgen05 launch (problem 1 waits on problem
-    0's row-block counters), against the oracle's two sequential linears."""
-    m, k, n1, n2 = shape
-    x, w1, b1 = rn(m, k), rn(k, n1, lo=-0.1, hi=0.1), rn(n1)
-    w2, b2 = rn(n1, n2, lo=-0.1, hi=0.1), rn(n2)
-    at = {"act": "gelu", "save_preact": 1, "save": save}
-    outs = [((m, n1), BF16), ((m, n1), BF16), ((m, n2), BF16)]
-    g, o = run_both("linear_chain", [(x, BF16), (w1, BF16), (b1, F32), (w2, BF16), (b2, F32)], outs, at)
-    for a, b in zip(g, o):
-        assert rel_err(a, b) < BF16_TOL, rel_err(a, b)
-
-
-def test_linear_chain_bert_ffn_repeatable():
-    """BERT-base FFN forward (4096x768 -> 3072 -> 768) chained: equal to the
-    two separate linears bit for bit (same tiles, same epilogues), and
-    run-to-run identical."""
-    from gpu_util import from_torch, to_torch
-    from paper_2303_04759_b200.runtime import run_op
-    T, H, F = 4096, 768, 3072
-    x = to_torch(rn(T, H), BF16)
-    w1, b1 = to_torch(rn(H, F, lo=-0.05, hi=0.05), BF16), to_torch(rn(F), F32)
-    w2, b2 = to_torch(rn(F, H, lo=-0.05, hi=0.05), BF16), to_torch(rn(H), F32)
-    at = {"act": "gelu", "save_preact": 1, "save": "grad"}
-    outs = [((T, F), BF16), ((T, F), BF16), ((T, H), BF16)]
-    c1 = [from_torch(t) for t in run_op("linear_chain", [x, w1, b1, w2, b2], outs, at)]
-    c2 = [from_torch(t) for t in run_op("linear_chain", [x, w1, b1, w2, b2], outs, at)]
-    y1, u1 = run_op("linear", [x, w1, b1], outs[:2], at)
-    (y2,) = run_op("linear", [y1, w2, b2], outs[2:], {})
-    sep = [from_torch(t) for t in (y1, u1, y2)]
-    for a, b, c in zip(c1, c2, sep):
-        assert bits_equal(a, b) and bits_equal(a, c)
 
 
 @pytest.mark.parametrize("H", [768, 100])

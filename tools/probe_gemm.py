@@ -36,8 +36,6 @@ def run(name, op, M, K, N, ta, tb, out, iters, tile=None, cublas=True):
     at = {"ta": ta, "tb": tb}
     if tile:
         at.update({"tc_bn": tile[0], "tc_cg": tile[1]})
-        if len(tile) > 2:
-            at["tc_splits"] = tile[2]
     plan = Plan(op, [(tuple(a.shape), BF16), (tuple(b.shape), BF16)], [((M, N), out)], at)
     s = torch.cuda.current_stream().cuda_stream
     for _ in range(3):
@@ -73,10 +71,7 @@ def trace(iters):
     """Per-CTA timeline of one launch (globaltimer ns): entry, setup done, first
     operand stage landed (MMA), last MMA commit, first accumulator ready
     (epilogue), epilogue drained."""
-    cases = [("proj_wgrad_s4", 768, 4096, 768, 1, 0, F32, {"tc_bn": 128, "tc_cg": 1, "tc_splits": 4}),
-             ("proj_wgrad_s4_cg2", 768, 4096, 768, 1, 0, F32, {"tc_bn": 256, "tc_cg": 2, "tc_splits": 4}),
-             ("ffn1_wgrad_s2", 768, 4096, 3072, 1, 0, F32, {"tc_bn": 256, "tc_cg": 2, "tc_splits": 2}),
-             ("ffn1_fwd", 4096, 768, 3072, 0, 0, BF16, {}), ("proj_wgrad", 768, 4096, 768, 1, 0, F32, {}),
+    cases = [("ffn1_fwd", 4096, 768, 3072, 0, 0, BF16, {}), ("proj_wgrad", 768, 4096, 768, 1, 0, F32, {}),
              ("ffn1_wgrad", 768, 4096, 3072, 1, 0, F32, {}),
              ("ffn1_wgrad_bf16out", 768, 4096, 3072, 1, 0, BF16, {}),
              ("ffn1_wgrad_notma", 768, 4096, 3072, 1, 0, F32, {"tc_notma": 1}),
@@ -149,21 +144,6 @@ def pairs(iters):
                           "pair_lpt_us": round(tp, 2), "pair_round_robin_us": round(trr, 2)}), flush=True)
 
 
-def sweep_splits(iters):
-    """Split-K ways on the weight-gradient shapes (few output tiles, K = T);
-    the last line per shape is the cost model's own choice."""
-    T = 4096
-    for name, M, N in (("proj_wgrad", 768, 768), ("qkv_wgrad", 768, 2304), ("ffn1_wgrad", 768, 3072),
-                       ("ffn2_wgrad", 3072, 768)):
-        for tile in [(256, 2), (128, 2), (256, 1), (128, 1)]:
-            for sp in (1, 2, 4):
-                if tile[1] * sp > 8:
-                    continue
-                r = run(name, "matmul_t", M, T, N, 1, 0, F32, iters, tile=tile + (sp,), cublas=False)
-                print(json.dumps(r), flush=True)
-        print(json.dumps(run(name, "matmul_t", M, T, N, 1, 0, F32, iters, cublas=True)), flush=True)
-
-
 def sweep(iters):
     """Every tile configuration on every BERT-base shape (cost-model calibration)."""
     for sh in SHAPES[:-1]:
@@ -204,28 +184,32 @@ def linear_gelu(iters, M=4096, K=768, N=3072):
     return res
 
 
-def chain(iters):
-    """BERT-base FFN forward: linear(gelu, act' saved) then linear, as two
-    launches vs one chained launch (linear_chain)."""
-    T, H, F = 4096, 768, 3072
-    x = torch.randn(T, H, device="cuda").to(torch.bfloat16)
-    w1 = (0.02 * torch.randn(H, F, device="cuda")).to(torch.bfloat16)
-    w2 = (0.02 * torch.randn(F, H, device="cuda")).to(torch.bfloat16)
-    b1, b2 = torch.zeros(F, device="cuda"), torch.zeros(H, device="cuda")
-    y1 = torch.empty(T, F, device="cuda", dtype=torch.bfloat16)
-    u1 = torch.empty_like(y1)
-    y2 = torch.empty(T, H, device="cuda", dtype=torch.bfloat16)
-    at = {"act": "gelu", "save_preact": 1, "save": "grad"}
-    p1 = Plan("linear", [((T, H), BF16), ((H, F), BF16), ((F,), F32)], [((T, F), BF16)] * 2, at)
-    p2 = Plan("linear", [((T, F), BF16), ((F, H), BF16), ((H,), F32)], [((T, H), BF16)], {})
-    t1 = time_plan(p1, [x.data_ptr(), w1.data_ptr(), b1.data_ptr()], [y1.data_ptr(), u1.data_ptr()], iters)
-    t2 = time_plan(p2, [y1.data_ptr(), w2.data_ptr(), b2.data_ptr()], [y2.data_ptr()], iters)
-    pc = Plan("linear_chain", [((T, H), BF16), ((H, F), BF16), ((F,), F32), ((F, H), BF16), ((H,), F32)],
-              [((T, F), BF16), ((T, F), BF16), ((T, H), BF16)], at)
-    tc = time_plan(pc, [x.data_ptr(), w1.data_ptr(), b1.data_ptr(), w2.data_ptr(), b2.data_ptr()],
-                   [y1.data_ptr(), u1.data_ptr(), y2.data_ptr()], iters)
-    print(json.dumps({"name": "ffn_fwd", "ffn1_us": round(t1, 2), "ffn2_us": round(t2, 2),
-                      "sum_us": round(t1 + t2, 2), "chain_us": round(tc, 2)}), flush=True)
+def cublas_epilogue(iters, M=4096, K=768, N=3072):
+    """Vendor yardstick for the roofline kernel: cuBLASLt with its fused
+    bias+GELU epilogue (torch._addmm_activation, tanh-GELU, one output) and
+    cuBLAS + a separate torch GELU, on FFN1's shape."""
+    x = torch.randn(M, K, device="cuda").to(torch.bfloat16)
+    w = (0.02 * torch.randn(K, N, device="cuda")).to(torch.bfloat16)
+    b = torch.zeros(N, device="cuda", dtype=torch.bfloat16)
+
+    def t(fn):
+        for _ in range(3):
+            fn()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(iters):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) * 1000 / iters
+    res = []
+    for name, fn in (("cublaslt_bias_gelu_epilogue", lambda: torch._addmm_activation(b, x, w, use_gelu=True)),
+                     ("cublas_matmul_plus_torch_gelu", lambda: torch.nn.functional.gelu(torch.addmm(b, x, w))),
+                     ("cublas_matmul_plain", lambda: torch.matmul(x, w))):
+        us = t(fn)
+        res.append({"name": f"{name}_{M}x{K}x{N}", "us": round(us, 2), "tflops": round(2.0 * M * N * K / us / 1e6, 1)})
+    return res
 
 
 def time_plan(plan, ins, outs, iters):
@@ -277,22 +261,19 @@ def main():
     ap.add_argument("--attention", action="store_true")
     ap.add_argument("--linear", action="store_true")
     ap.add_argument("--sweep", action="store_true")
-    ap.add_argument("--splits", action="store_true")
     ap.add_argument("--trace", action="store_true")
     ap.add_argument("--pairs", action="store_true")
-    ap.add_argument("--chain", action="store_true")
+    ap.add_argument("--cublas-epi", action="store_true")
     args = ap.parse_args()
-    if args.chain:
-        chain(args.iters)
+    if args.cublas_epi:
+        for r in cublas_epilogue(args.iters):
+            print(json.dumps(r), flush=True)
         return
     if args.pairs:
         pairs(args.iters)
         return
     if args.trace:
         trace(args.iters)
-        return
-    if args.splits:
-        sweep_splits(args.iters)
         return
     if args.sweep:
         sweep(args.iters)
