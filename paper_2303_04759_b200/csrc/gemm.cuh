@@ -39,7 +39,7 @@ struct GemmArgs {
   void* aux_out = nullptr;     // pre-activation store, same layout/dtype as C
   int save_grad = 0;           // aux_out holds act'(pre-activation) instead (consumed with ACT_DERIV)
   int force_bn = 0, force_cg = 0;  // tcgen05 tile override (tests / tuning); 0 = cost model
-  void* trace = nullptr;           // optional per-CTA timeline buffer (12 x u64 per CTA, tooling)
+  void* trace = nullptr;           // optional per-CTA timeline buffer (16 x u64 per CTA, tooling)
   int no_tma_epi = 0;              // force the direct-store epilogue (tooling)
   const int* sched = nullptr;      // device LPT schedule of a pair launch (gemm_pair_schedule)
   int sched_rounds = 0;

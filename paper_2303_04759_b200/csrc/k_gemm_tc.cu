@@ -113,6 +113,22 @@ __device__ __forceinline__ int64_t unit_at(const TcParams& P, int64_t cl, int64_
 __device__ __forceinline__ int unit_prob(const TcParams& P, int64_t u) {
   return (P.nprob > 1 && u >= P.pr[0].num_tiles) ? 1 : 0;
 }
+// compile-time epilogue variants (see finish_fast in the kernel)
+enum EpiKind { EK_GENERIC = 0, EK_PLAIN = 1, EK_BIAS = 2, EK_GELU_SAVE = 3, EK_DERIV = 4, EK_F32 = 5 };
+template <bool AUX>
+__device__ __forceinline__ int epi_kind(const TcProb& Q) {
+  if (!Q.tma_epi || Q.alpha != 1.0f) return EK_GENERIC;
+  if (Q.c_dtype == TCB_F32)  // weight gradients (and their K-slice partials)
+    return (!Q.bias && Q.act == ACT_NONE && Q.dact == ACT_NONE && !Q.aux_out) ? EK_F32 : EK_GENERIC;
+  if (Q.c_dtype != TCB_BF16) return EK_GENERIC;
+  if (Q.dact != ACT_NONE)
+    return (AUX && Q.dact == ACT_DERIV && Q.aux_dtype == TCB_BF16 && !Q.bias && Q.act == ACT_NONE && !Q.aux_out)
+               ? EK_DERIV
+               : EK_GENERIC;
+  if (Q.save_grad) return (Q.act == ACT_GELU && Q.bias && Q.aux_out) ? EK_GELU_SAVE : EK_GENERIC;
+  if (Q.act != ACT_NONE || Q.aux_out) return EK_GENERIC;
+  return Q.bias ? EK_BIAS : EK_PLAIN;
+}
 
 
 __device__ __forceinline__ float ld_e(const void* p, int dt, int64_t i) {
@@ -358,14 +374,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   uint64_t* abar = tempty + 2;  // TC_AUX_RING per epilogue warp
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(abar + TC_AUX_RING * TC_EPI_WARPS);
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // the warp index broadcast from lane 0: the compiler then treats it (and the
+  // tile coordinates derived from it) as warp-uniform, so TMA / tcgen05 issue
+  // takes uniform registers directly instead of a per-lane R2UR loop
+  const int warp = __shfl_sync(0xffffffffu, int(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   constexpr bool clustered = CG == 2;
   const uint32_t crank = clustered ? cluster_ctarank() : 0;
   const uint32_t rank = crank % CG;          // position in the CTA pair
   const uint32_t lead = crank - rank;        // the pair leader's cluster rank
   const int64_t cl_id = blockIdx.x / CG, n_cl = gridDim.x / CG;
   const uint16_t mcast = uint16_t(3u << lead);
-  unsigned long long* tr = P.trace ? P.trace + blockIdx.x * 12 : nullptr;
+  unsigned long long* tr = P.trace ? P.trace + blockIdx.x * 16 : nullptr;
   if (tr && threadIdx.x == 0) tr[0] = gtimer();
 
   if (warp == 0 && lane == 0) {
@@ -503,7 +522,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           }
         }
         tc_commit<CG>(&tfull[acc], mcast);
-        if (tr) tr[3] = gtimer();
+        if (tr) {
+          tr[3] = gtimer();
+          if (ui < 3) tr[12 + ui] = tr[3];
+        }
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
@@ -552,14 +574,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           ++pi;
         }
         if (n0 >= Q.N) continue;  // chunk skipped by the consumer too
+        // warp-uniform operands (broadcast from lane 0): no per-lane issue loop
+        const CUtensorMap* am = uniform_ptr(prob ? &EM1.aux : &EM0.aux);
+        const int ax = __shfl_sync(0xffffffffu, int(n0), 0), ay = __shfl_sync(0xffffffffu, mrow, 0);
+        const int az2 = __shfl_sync(0xffffffffu, int(z % Q.Z2), 0), az1 = __shfl_sync(0xffffffffu, int(z / Q.Z2), 0);
         if (lane == 0) {
           uint64_t* bar = &ab[aissue % TC_AUX_RING];
           mbar_expect_tx(bar, 32 * W * 2);
           asm volatile(
               "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
               " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(aslots + (aissue % TC_AUX_RING) * TC_AUX_SLOT)),
-              "l"(reinterpret_cast<uint64_t>(prob ? &EM1.aux : &EM0.aux)), "r"(int(n0)), "r"(mrow), "r"(int(z % Q.Z2)),
-              "r"(int(z / Q.Z2)), "r"(smem_u32(bar))
+              "l"(reinterpret_cast<uint64_t>(am)), "r"(ax), "r"(ay), "r"(az2), "r"(az1), "r"(smem_u32(bar))
               : "memory");
         }
         ++aissue;
@@ -624,10 +649,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           }
           stage_row<W>(slot, lane, Q.c_dtype, v);
           fence_proxy_async();
-          __syncwarp();
+          // coordinates broadcast from lane 0: provably warp-uniform, so the
+          // store below issues from uniform registers (no per-lane R2UR loop)
+          const int sx = __shfl_sync(0xffffffffu, int(n0), 0), sy = __shfl_sync(0xffffffffu, mrow0, 0);
+          const int sz2 = __shfl_sync(0xffffffffu, z2, 0), sz1 = __shfl_sync(0xffffffffu, z1, 0);
+          const CUtensorMap* mc = uniform_ptr(&EM.c);
+          const CUtensorMap* mu = uniform_ptr(&EM.u);
           if (lane == 0) {
-            tma_store_4d(&EM.c, slot, int(n0), mrow0, z2, z1);
-            if (Q.aux_out) tma_store_4d(&EM.u, slot + TC_SLOT / 2, int(n0), mrow0, z2, z1);
+            tma_store_4d(mc, slot, sx, sy, sz2, sz1);
+            if (Q.aux_out) tma_store_4d(mu, slot + TC_SLOT / 2, sx, sy, sz2, sz1);
             bulk_commit();
           }
           if (++sidx == OUT_RING) sidx = 0;
@@ -651,6 +681,64 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           store_row<W>(Q.c, Q.c_dtype, base, v, nvalid);
         }
       };
+      // The step's hot epilogues with every choice fixed at compile time (TMA
+      // path, bf16 output, alpha 1): no per-chunk branches on the problem's
+      // fields, constant-folded activation / dtype switches.
+      //   EK_BIAS: + bias;  EK_GELU_SAVE: + bias, y = GELU(u) and GELU'(u)
+      //   stored (FFN1 forward);  EK_DERIV: * act'(aux) from the aux ring
+      //   (FFN2 backward data gradient);  EK_F32: plain f32 output (weight
+      //   gradients, K-slice partials).  Anything else: `finish` above.
+      auto finish_fast = [&](auto kind, float (&v)[W], int ci, int64_t n0) {
+        constexpr int K = decltype(kind)::value;
+        if constexpr (K == EK_BIAS || K == EK_GELU_SAVE) {
+          const float4* bb = reinterpret_cast<const float4*>(wbias + ci * W);
+#pragma unroll
+          for (int j = 0; j < W / 4; ++j) {
+            const float4 b4 = bb[j];
+            const float2 lo = add2(make_float2(v[4 * j], v[4 * j + 1]), make_float2(b4.x, b4.y));
+            const float2 hi = add2(make_float2(v[4 * j + 2], v[4 * j + 3]), make_float2(b4.z, b4.w));
+            v[4 * j] = lo.x;
+            v[4 * j + 1] = lo.y;
+            v[4 * j + 2] = hi.x;
+            v[4 * j + 3] = hi.y;
+          }
+        }
+        if constexpr (K == EK_DERIV && AUX) {
+          const uint32_t s = achunk % TC_AUX_RING, ph = (achunk / TC_AUX_RING) & 1;
+          issue_next_aux();
+          mbar_wait(&ab[s], ph);
+          float a[W];
+          unstage_row16<W>(aslots + s * TC_AUX_SLOT, lane, TCB_BF16, a);
+          apply_dact<W>(ACT_DERIV, v, a);
+          ++achunk;
+        }
+        uint8_t* slot = slots + sidx * TC_SLOT;
+        if (lane == 0) bulk_wait_read<OUT_RING - 1>();
+        __syncwarp();
+        if constexpr (K == EK_GELU_SAVE) {
+          float dv[W];
+          act_and_deriv<W>(ACT_GELU, v, dv);
+          stage_row16<W, __nv_bfloat16>(slot + TC_SLOT / 2, lane, dv);
+        }
+        if constexpr (K == EK_F32) stage_row<W>(slot, lane, TCB_F32, v);
+        else stage_row16<W, __nv_bfloat16>(slot, lane, v);
+        fence_proxy_async();
+        const int sx = __shfl_sync(0xffffffffu, int(n0), 0), sy = __shfl_sync(0xffffffffu, mrow0, 0);
+        const int sz2 = __shfl_sync(0xffffffffu, z2, 0), sz1 = __shfl_sync(0xffffffffu, z1, 0);
+        const CUtensorMap* mc = uniform_ptr(&EM.c);
+        if constexpr (K == EK_GELU_SAVE) {
+          const CUtensorMap* mu = uniform_ptr(&EM.u);
+          if (lane == 0) {
+            tma_store_4d(mc, slot, sx, sy, sz2, sz1);
+            tma_store_4d(mu, slot + TC_SLOT / 2, sx, sy, sz2, sz1);
+            bulk_commit();
+          }
+        } else if (lane == 0) {
+          tma_store_4d(mc, slot, sx, sy, sz2, sz1);
+          bulk_commit();
+        }
+        if (++sidx == OUT_RING) sidx = 0;
+      };
       auto load_bias = [&]() {
         // this warp's bias columns for the tile -> smem (read back as broadcasts)
         __syncwarp();
@@ -665,21 +753,35 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       if (tr && ew == 0 && ui == 0) tr[4] = gtimer();
+      if (tr && ew == 0 && lane == 0 && ui >= 1 && ui < 3) tr[8 + 2 * (ui - 1)] = gtimer();
+      auto chunks = [&](auto kind) {
+        constexpr int K = decltype(kind)::value;
 #pragma unroll 1
-      for (int c = sub, ci = 0; c < NCH; c += SPLIT, ++ci) {
-        const int64_t n0 = int64_t(nb) * BN + c * W;
-        if (n0 >= Q.N) continue;
-        uint32_t r[W];
-        const uint32_t taddr = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * BN + c * W);
-        if constexpr (W == 16) TMEM_LD16(taddr, r);
-        else TMEM_LD32(taddr, r);
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        float v[W];
+        for (int c = sub, ci = 0; c < NCH; c += SPLIT, ++ci) {
+          const int64_t n0 = int64_t(nb) * BN + c * W;
+          if (n0 >= Q.N) continue;
+          uint32_t r[W];
+          const uint32_t taddr = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * BN + c * W);
+          if constexpr (W == 16) TMEM_LD16(taddr, r);
+          else TMEM_LD32(taddr, r);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          float v[W];
 #pragma unroll
-        for (int j = 0; j < W; ++j) v[j] = __uint_as_float(r[j]);
-        finish(v, ci, n0);
+          for (int j = 0; j < W; ++j) v[j] = __uint_as_float(r[j]);
+          if constexpr (K == EK_GENERIC) finish(v, ci, n0);
+          else finish_fast(kind, v, ci, n0);
+        }
+      };
+      switch (epi_kind<AUX>(Q)) {
+        case EK_BIAS: chunks(std::integral_constant<int, EK_BIAS>{}); break;
+        case EK_GELU_SAVE: chunks(std::integral_constant<int, EK_GELU_SAVE>{}); break;
+        case EK_DERIV: chunks(std::integral_constant<int, EK_DERIV>{}); break;
+        case EK_PLAIN: chunks(std::integral_constant<int, EK_PLAIN>{}); break;
+        case EK_F32: chunks(std::integral_constant<int, EK_F32>{}); break;
+        default: chunks(std::integral_constant<int, EK_GENERIC>{}); break;
       }
       if (tr && ew == 0 && lane == 0 && ui == 0) tr[6] = gtimer();
+      if (tr && ew == 0 && lane == 0 && ui >= 1 && ui < 3) tr[9 + 2 * (ui - 1)] = gtimer();
       // release the accumulator to the (leader's) MMA warp
       tc_fence_before();
       __syncwarp();

@@ -78,6 +78,13 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, u
         : "memory");
   }
 }
+// a pointer broadcast from lane 0 (all lanes must call): provably warp-uniform
+template <typename T>
+__device__ __forceinline__ const T* uniform_ptr(const T* p) {
+  const uint64_t v = reinterpret_cast<uint64_t>(p);
+  const uint32_t lo = __shfl_sync(0xffffffffu, uint32_t(v), 0), hi = __shfl_sync(0xffffffffu, uint32_t(v >> 32), 0);
+  return reinterpret_cast<const T*>((uint64_t(hi) << 32) | lo);
+}
 __device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, const void* src, int c0, int c1, int c2,
                                              int c3) {
   asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(

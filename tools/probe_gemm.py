@@ -67,49 +67,81 @@ def run(name, op, M, K, N, ta, tb, out, iters, tile=None, cublas=True):
             "cublas_us": round(ucb, 2), "cublas_tflops": round(2.0 * M * N * K / (ucb * 1e-6) / 1e12, 1)}
 
 
-def trace(iters):
-    """Per-CTA timeline of one launch (globaltimer ns): entry, setup done, first
-    operand stage landed (MMA), last MMA commit, first accumulator ready
-    (epilogue), epilogue drained."""
-    cases = [("ffn1_fwd", 4096, 768, 3072, 0, 0, BF16, {}), ("proj_wgrad", 768, 4096, 768, 1, 0, F32, {}),
-             ("ffn1_wgrad", 768, 4096, 3072, 1, 0, F32, {}),
-             ("ffn1_wgrad_bf16out", 768, 4096, 3072, 1, 0, BF16, {}),
-             ("ffn1_wgrad_notma", 768, 4096, 3072, 1, 0, F32, {"tc_notma": 1}),
-             ("ffn1_wgrad_cg1", 768, 4096, 3072, 1, 0, F32, {"tc_bn": 128, "tc_cg": 1}),
-             ("ffn1_wgrad_cg2_128", 768, 4096, 3072, 1, 0, F32, {"tc_bn": 128, "tc_cg": 2}),
-             ("ffn1_wgrad_cg2_256", 768, 4096, 3072, 1, 0, F32, {"tc_bn": 256, "tc_cg": 2}),
-             ("ffn1_wgrad_kmaj", 768, 4096, 3072, 0, 1, F32, {}),
-             ("decoder_fwd", 4096, 768, 30528, 0, 1, BF16, {}),
-             ("ffn2_fwd", 4096, 3072, 768, 0, 0, BF16, {})]
-    for name, M, K, N, ta, tb, out, extra in cases:
+def trace(iters, only=None):
+    """Per-CTA timeline of one launch (globaltimer ns, 16 slots per CTA):
+    entry, setup done, first operand stage landed (MMA), last MMA commit,
+    accumulator ready / chunks done for tiles 0-2 (epilogue warp 0), MMA
+    commit of tiles 0-2, epilogue drained."""
+    cases = [("ffn1_fwd", "matmul_t", 4096, 768, 3072, 0, 0, BF16, {}),
+             ("ffn1_fwd_gelu_grad", "linear", 4096, 768, 3072, 0, 0, BF16, {"act": "gelu", "save_preact": 1, "save": "grad"}),
+             ("ffn1_fwd_gelu_grad_notma", "linear", 4096, 768, 3072, 0, 0, BF16,
+              {"act": "gelu", "save_preact": 1, "save": "grad", "tc_notma": 1}),
+             ("ffn1_fwd_bias", "linear", 4096, 768, 3072, 0, 0, BF16, {}),
+             ("ffn1_fwd_preact", "linear", 4096, 768, 3072, 0, 0, BF16, {"act": "gelu", "save_preact": 1}),
+             ("ffn1_fwd_gelu_only", "linear", 4096, 768, 3072, 0, 0, BF16, {"act": "gelu"}),
+             ("ffn2_dgrad_deriv", "matmul_dact", 4096, 768, 3072, 0, 1, BF16, {"act": "deriv"}),
+             ("proj_fwd", "matmul_t", 4096, 768, 768, 0, 0, BF16, {}),
+             ("qkv_fwd", "matmul_t", 4096, 768, 2304, 0, 0, BF16, {}),
+             ("ffn2_fwd", "matmul_t", 4096, 3072, 768, 0, 0, BF16, {}),
+             ("proj_wgrad", "matmul_t", 768, 4096, 768, 1, 0, F32, {}),
+             ("ffn1_wgrad", "matmul_t", 768, 4096, 3072, 1, 0, F32, {}),
+             ("decoder_fwd", "matmul_t", 4096, 768, 30528, 0, 1, BF16, {})]
+    import numpy as np
+    for name, op, M, K, N, ta, tb, out, extra in cases:
+        if only and name not in only:
+            continue
         a = torch.randn(K, M, device="cuda") if ta else torch.randn(M, K, device="cuda")
         b = torch.randn(N, K, device="cuda") if tb else torch.randn(K, N, device="cuda")
-        a, b = a.to(torch.bfloat16).contiguous(), b.to(torch.bfloat16).contiguous()
+        a, b = a.to(torch.bfloat16).contiguous(), (0.05 * b).to(torch.bfloat16).contiguous()
         c = torch.empty(M, N, device="cuda", dtype=torch.float32 if out == F32 else torch.bfloat16)
-        tr = torch.zeros(148 * 12, dtype=torch.int64, device="cuda")
-        plan = Plan("matmul_t", [(tuple(a.shape), BF16), (tuple(b.shape), BF16)], [((M, N), out)],
-                    {"ta": ta, "tb": tb, "tc_trace": tr.data_ptr(), **extra})
+        tr = torch.zeros(148 * 16, dtype=torch.int64, device="cuda")
+        at = {"ta": ta, "tb": tb, "tc_trace": tr.data_ptr(), **extra}
+        ins, ptrs, outs, optrs = [(tuple(a.shape), BF16), (tuple(b.shape), BF16)], [a.data_ptr(), b.data_ptr()], \
+            [((M, N), out)], [c.data_ptr()]
+        keep = []
+        if op == "linear":
+            bias = torch.zeros(N, device="cuda")
+            u = torch.empty_like(c)
+            keep += [bias, u]
+            ins.append(((N,), F32))
+            ptrs.append(bias.data_ptr())
+            if extra.get("save_preact"):
+                outs.append(((M, N), out))
+                optrs.append(u.data_ptr())
+            at.pop("ta"), at.pop("tb")
+        elif op == "matmul_dact":
+            aux = torch.randn(M, N, device="cuda").to(torch.bfloat16)
+            keep.append(aux)
+            ins.append(((M, N), BF16))
+            ptrs.append(aux.data_ptr())
+            at.pop("ta")
+        plan = Plan(op, ins, outs, at)
         s = torch.cuda.current_stream().cuda_stream
         for _ in range(3):
-            plan.launch([a.data_ptr(), b.data_ptr()], [c.data_ptr()], s)
+            plan.launch(ptrs, optrs, s)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         for _ in range(10):
-            plan.launch([a.data_ptr(), b.data_ptr()], [c.data_ptr()], s)
+            plan.launch(ptrs, optrs, s)
         e1.record()
         torch.cuda.synchronize()
         us = e0.elapsed_time(e1) * 100
-        t = tr.view(148, 12).cpu().numpy().astype("float64")
+        tr.zero_()
+        plan.launch(ptrs, optrs, s)  # the traced launch runs alone
+        torch.cuda.synchronize()
+        t = tr.view(148, 16).cpu().numpy().astype("float64")
         t = t[t[:, 0] > 0]
         base = t[:, 0].min()
-        rel = (t[:, :11] - base) / 1000.0
-        rel[t[:, :11] == 0] = float("nan")
-        import numpy as np
-        q = lambda col: [round(float(np.nanpercentile(rel[:, col], p)), 2) for p in (0, 50, 100)]
-        print(json.dumps({"name": name, "us": round(us, 2), "ctas": len(t), "entry": q(0), "setup": q(1), "first_stage": q(2),
-                          "last_commit": q(3), "first_acc": q(4), "chunks_done": q(6), "released": q(7),
-                          "epi_done": q(5), "atomic": q(8), "red_start": q(9), "red_end": q(10)}), flush=True)
+        rel = (t[:, :16] - base) / 1000.0
+        rel[t[:, :16] == 0] = float("nan")
+        q = lambda col: [round(float(np.nanpercentile(rel[:, col], p)), 2) if np.isfinite(rel[:, col]).any() else None
+                         for p in (0, 50, 100)]
+        print(json.dumps({"name": name, "us": round(us, 2), "ctas": len(t), "entry": q(0), "setup": q(1),
+                          "first_stage": q(2), "commit_t0": q(12), "acc_t0": q(4), "chunks_t0": q(6),
+                          "released_t0": q(7), "commit_t1": q(13), "acc_t1": q(8), "chunks_t1": q(9),
+                          "commit_t2": q(14), "acc_t2": q(10), "chunks_t2": q(11), "last_commit": q(3),
+                          "epi_done": q(5)}), flush=True)
 
 
 def pairs(iters):
@@ -273,7 +305,7 @@ def main():
         pairs(args.iters)
         return
     if args.trace:
-        trace(args.iters)
+        trace(args.iters, os.environ.get("TRACE_ONLY", "").split(",") if os.environ.get("TRACE_ONLY") else None)
         return
     if args.sweep:
         sweep(args.iters)
