@@ -605,6 +605,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const int z1 = Q.wsplit > 1 ? 0 : int(z / Q.Z2), z2 = Q.wsplit > 1 ? z : int(z % Q.Z2);
       const int64_t coff = int64_t(z1) * Q.c_s1 + int64_t(z2) * Q.c_s2;
       const int mrow0 = mb * (TC_BM * CG) + int(rank) * TC_BM + q * 32;  // this warp's 32-row box
+      // per-tile TMA-store operands broadcast from lane 0 once (warp-uniform:
+      // the stores issue from uniform registers, no per-lane R2UR loop)
+      const int un0 = __shfl_sync(0xffffffffu, int(nb) * BN, 0), sy = __shfl_sync(0xffffffffu, mrow0, 0);
+      const int sz2 = __shfl_sync(0xffffffffu, z2, 0), sz1 = __shfl_sync(0xffffffffu, z1, 0);
+      const CUtensorMap* mc = uniform_ptr(&EM.c);
+      const CUtensorMap* mu = uniform_ptr(&EM.u);
       const int64_t m = int64_t(mrow0) + lane;
       // finishes one W-column chunk: v holds the f32 accumulator row segment
       auto finish = [&](float (&v)[W], int ci, int64_t n0) {
@@ -649,12 +655,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           }
           stage_row<W>(slot, lane, Q.c_dtype, v);
           fence_proxy_async();
-          // coordinates broadcast from lane 0: provably warp-uniform, so the
-          // store below issues from uniform registers (no per-lane R2UR loop)
-          const int sx = __shfl_sync(0xffffffffu, int(n0), 0), sy = __shfl_sync(0xffffffffu, mrow0, 0);
-          const int sz2 = __shfl_sync(0xffffffffu, z2, 0), sz1 = __shfl_sync(0xffffffffu, z1, 0);
-          const CUtensorMap* mc = uniform_ptr(&EM.c);
-          const CUtensorMap* mu = uniform_ptr(&EM.u);
+          const int sx = un0 + (sub + ci * SPLIT) * W;  // = n0, from uniform values
           if (lane == 0) {
             tma_store_4d(mc, slot, sx, sy, sz2, sz1);
             if (Q.aux_out) tma_store_4d(mu, slot + TC_SLOT / 2, sx, sy, sz2, sz1);
@@ -723,11 +724,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         if constexpr (K == EK_F32) stage_row<W>(slot, lane, TCB_F32, v);
         else stage_row16<W, __nv_bfloat16>(slot, lane, v);
         fence_proxy_async();
-        const int sx = __shfl_sync(0xffffffffu, int(n0), 0), sy = __shfl_sync(0xffffffffu, mrow0, 0);
-        const int sz2 = __shfl_sync(0xffffffffu, z2, 0), sz1 = __shfl_sync(0xffffffffu, z1, 0);
-        const CUtensorMap* mc = uniform_ptr(&EM.c);
+        const int sx = un0 + (sub + ci * SPLIT) * W;  // = n0, from uniform values
         if constexpr (K == EK_GELU_SAVE) {
-          const CUtensorMap* mu = uniform_ptr(&EM.u);
           if (lane == 0) {
             tma_store_4d(mc, slot, sx, sy, sz2, sz1);
             tma_store_4d(mu, slot + TC_SLOT / 2, sx, sy, sz2, sz1);
