@@ -176,6 +176,45 @@ def pairs(iters):
                           "pair_lpt_us": round(tp, 2), "pair_round_robin_us": round(trr, 2)}), flush=True)
 
 
+def pair_trace(iters):
+    """The step's four backward pairs (FFN2 with the saved-derivative act'):
+    time and per-CTA end spread for the planner's K-slice choice and for
+    forced wsplit 1 / 2 / 4 (tuning data for gemm_pair_wsplit)."""
+    import numpy as np
+    T = 4096
+    cases = [("qkv", 768, 2304, 0), ("proj", 768, 768, 0), ("ffn1", 768, 3072, 0), ("ffn2_deriv", 3072, 768, 1)]
+    for name, Hin, Hout, dact in cases:
+        x = torch.randn(T, Hin, device="cuda").to(torch.bfloat16)
+        w = (0.02 * torch.randn(Hin, Hout, device="cuda")).to(torch.bfloat16)
+        dy = torch.randn(T, Hout, device="cuda").to(torch.bfloat16)
+        u = torch.randn(T, Hin, device="cuda").to(torch.bfloat16)
+        dx = torch.empty(T, Hin, device="cuda", dtype=torch.bfloat16)
+        dw = torch.empty(Hin, Hout, device="cuda")
+        ins0 = [((T, Hout), BF16), ((Hin, Hout), BF16)] + ([((T, Hin), BF16)] if dact else [])
+        a0 = [dy.data_ptr(), w.data_ptr()] + ([u.data_ptr()] if dact else [])
+        for bn, ws in [tuple(int(v) for v in c.split(':')) for c in os.environ.get('PAIR_CFGS', '256:0,256:1,256:2,192:0,192:1,192:2,128:0,128:1,128:2').split(',')]:
+            tr = torch.zeros(148 * 16, dtype=torch.int64, device="cuda")
+            at = {"n0": 3 if dact else 2, "ta0": 0, "tb0": 1, "ta1": 1, "tb1": 0, "out1": "f32", "tc_trace": tr.data_ptr(),
+                  "tc_bn": bn, "tc_cg": 2}
+            if dact:
+                at["act0"] = "deriv"
+            if ws:
+                at["wsplit"] = ws
+            pp = Plan("matmul_pair", ins0 + [((T, Hin), BF16), ((T, Hout), BF16)],
+                      [((T, Hin), BF16), ((Hin, Hout), F32)], at)
+            args = (a0 + [x.data_ptr(), dy.data_ptr()], [dx.data_ptr(), dw.data_ptr()])
+            us = time_plan(pp, *args, iters)
+            tr.zero_()
+            pp.launch(*args, torch.cuda.current_stream().cuda_stream)
+            torch.cuda.synchronize()
+            t = tr.view(148, 16).cpu().numpy().astype("float64")
+            t = t[t[:, 0] > 0]
+            rel = (t[:, 5] - t[:, 0].min()) / 1000.0
+            print(json.dumps({"pair": name, "bn": bn, "wsplit": ws or "planner", "us": round(us, 2), "ctas": len(t),
+                              "epi_done_min_med_max": [round(float(np.percentile(rel, p)), 2) for p in (0, 50, 100)]}),
+                  flush=True)
+
+
 def sweep(iters):
     """Every tile configuration on every BERT-base shape (cost-model calibration)."""
     for sh in SHAPES[:-1]:
@@ -295,6 +334,7 @@ def main():
     ap.add_argument("--sweep", action="store_true")
     ap.add_argument("--trace", action="store_true")
     ap.add_argument("--pairs", action="store_true")
+    ap.add_argument("--pair-trace", action="store_true")
     ap.add_argument("--cublas-epi", action="store_true")
     args = ap.parse_args()
     if args.cublas_epi:
@@ -303,6 +343,9 @@ def main():
         return
     if args.pairs:
         pairs(args.iters)
+        return
+    if args.pair_trace:
+        pair_trace(args.iters)
         return
     if args.trace:
         trace(args.iters, os.environ.get("TRACE_ONLY", "").split(",") if os.environ.get("TRACE_ONLY") else None)
