@@ -41,6 +41,7 @@ struct GemmArgs {
   int force_bn = 0, force_cg = 0;  // tcgen05 tile override (tests / tuning); 0 = cost model
   void* trace = nullptr;           // optional per-CTA timeline buffer (16 x u64 per CTA, tooling)
   int no_tma_epi = 0;              // force the direct-store epilogue (tooling)
+  int generic_epi = 0;             // force the runtime-dispatched epilogue (parity tests of the variants)
   const int* sched = nullptr;      // device LPT schedule of a pair launch (gemm_pair_schedule)
   int sched_rounds = 0;
   int wsplit = 1;                  // > 1: c is a [wsplit][M][N] f32 workspace of K-slice partials

@@ -48,6 +48,7 @@ static void tile_attrs(GemmArgs& g, const Plan& p) {
   g.force_cg = int(p.attrs.i("tc_cg", 0));
   g.trace = reinterpret_cast<void*>(p.attrs.i("tc_trace", 0));  // tooling only
   g.no_tma_epi = int(p.attrs.i("tc_notma", 0));
+  g.generic_epi = int(p.attrs.i("tc_generic_epi", 0));
 }
 
 static void b_matmul(Plan& p) {
@@ -153,6 +154,7 @@ static void b_matmul_pair(Plan& p) {
   g0.force_bn = g1.force_bn = int(p.attrs.i("tc_bn", 0));
   g0.force_cg = g1.force_cg = int(p.attrs.i("tc_cg", 0));
   g0.trace = g1.trace = reinterpret_cast<void*>(p.attrs.i("tc_trace", 0));  // tooling only
+  g0.generic_epi = g1.generic_epi = int(p.attrs.i("tc_generic_epi", 0));
   const bool exact = want_exact(p) || p.in[n0].dtype != TCB_BF16;
   p.nkernels = exact ? 2 : 1;
   std::shared_ptr<Scratch> sched;  // read-only schedule table

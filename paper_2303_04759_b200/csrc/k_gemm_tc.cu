@@ -88,6 +88,7 @@ struct TcProb {
   void* aux_out;
   int save_grad;  // aux_out = act'(pre-activation)
   int tma_epi;   // 1: smem + TMA-store epilogue (tensor maps valid); 0: direct stores
+  int generic_epi;  // 1: never a compile-time epilogue variant (tests)
   int c_vec_ok;  // direct path: 16-byte aligned rows
 };
 // One launch runs one or two GEMM problems with the same tile shape (a
@@ -117,7 +118,7 @@ __device__ __forceinline__ int unit_prob(const TcParams& P, int64_t u) {
 enum EpiKind { EK_GENERIC = 0, EK_PLAIN = 1, EK_BIAS = 2, EK_GELU_SAVE = 3, EK_DERIV = 4, EK_F32 = 5 };
 template <bool AUX>
 __device__ __forceinline__ int epi_kind(const TcProb& Q) {
-  if (!Q.tma_epi || Q.alpha != 1.0f) return EK_GENERIC;
+  if (!Q.tma_epi || Q.alpha != 1.0f || Q.generic_epi) return EK_GENERIC;
   if (Q.c_dtype == TCB_F32)  // weight gradients (and their K-slice partials)
     return (!Q.bias && Q.act == ACT_NONE && Q.dact == ACT_NONE && !Q.aux_out) ? EK_F32 : EK_GENERIC;
   if (Q.c_dtype != TCB_BF16) return EK_GENERIC;
@@ -884,6 +885,7 @@ static void fill_prob(const GemmArgs& g, TcProb& P, CUtensorMap& ta, CUtensorMap
                ((g.c_s1 * es) % 16 == 0) && ((g.c_s2 * es) % 16 == 0) &&
                (!g.aux_out || reinterpret_cast<uintptr_t>(g.aux_out) % 16 == 0);
   P.tma_epi = epi_tma_ok(g) && (g.dact == ACT_NONE || AUX) && !g.no_tma_epi;
+  P.generic_epi = g.generic_epi;
   const int64_t Z1 = (g.Z + g.Z2 - 1) / g.Z2;
   ta = g.ta ? make_map(g.a, g.M, g.K, g.Z2, Z1, 64) : make_map(g.a, g.K, g.M, g.Z2, Z1, TC_BM);
   tb = g.tb ? make_map(g.b, g.K, g.N, g.Z2, Z1, C::B_ROWS) : make_map(g.b, g.N, g.K, g.Z2, Z1, 64);

@@ -218,6 +218,41 @@ def test_gemm_tile_variants_epilogues(bn, cg):
     assert rel_err(g[0], o[0]) < BF16_TOL
 
 
+EPI_VARIANTS = [
+    # (op, inputs (shape, dtype), outputs, attrs): the compile-time epilogue variants of k_gemm_tc
+    ("matmul_t", [((700, 256), BF16), ((256, 600), BF16)], [((700, 600), BF16)], {}),  # plain bf16
+    ("matmul_t", [((256, 700), BF16), ((256, 600), BF16)], [((700, 600), F32)], {"ta": 1, "out": "f32"}),  # f32
+    ("linear", [((700, 256), BF16), ((256, 600), BF16), ((600,), F32)], [((700, 600), BF16)], {}),  # + bias
+    ("linear", [((700, 256), BF16), ((256, 600), BF16), ((600,), F32)], [((700, 600), BF16)] * 2,
+     {"act": "gelu", "save_preact": 1, "save": "grad"}),  # + bias + GELU + GELU' saved
+    ("matmul_dact", [((700, 256), BF16), ((600, 256), BF16), ((700, 600), BF16)], [((700, 600), BF16)],
+     {"tb": 1, "act": "deriv"}),  # * act'(aux)
+    ("matmul_pair", [((512, 768), BF16), ((3072, 768), BF16), ((512, 3072), BF16), ((512, 3072), BF16),
+                     ((512, 768), BF16)], [((512, 3072), BF16), ((3072, 768), F32)],
+     {"n0": 3, "act0": "deriv", "ta0": 0, "tb0": 1, "ta1": 1, "tb1": 0, "out1": "f32", "wsplit": 2}),
+]
+
+
+@pytest.mark.parametrize("case", range(len(EPI_VARIANTS)))
+def test_gemm_epilogue_variants_bit_identical_to_generic(case):
+    """Each compile-time epilogue variant (plain, f32, bias, bias+GELU+GELU',
+    act'(aux), and a grouped pair with K-slice partials) gives exactly the
+    bits of the runtime-dispatched epilogue it replaces (tc_generic_epi=1),
+    on ragged shapes; both against the oracle within bf16 rounding."""
+    from gpu_util import from_torch, to_torch
+    from paper_2303_04759_b200.runtime import run_op
+    op, ins, outs, at = EPI_VARIANTS[case]
+    xs = [rn(*shp, lo=-1, hi=1) for shp, _ in ins]
+    tin = [to_torch(quantize(x, d), d) for x, (_, d) in zip(xs, ins)]
+    fast = [from_torch(t) for t in run_op(op, tin, outs, at)]
+    slow = [from_torch(t) for t in run_op(op, tin, outs, {**at, "tc_generic_epi": 1})]
+    for a, b in zip(fast, slow):
+        assert bits_equal(a, b)
+    _, o = run_both(op, [(x, d) for x, (_, d) in zip(xs, ins)], outs, at)
+    for a, b in zip(fast, o):
+        assert rel_err(a, b) < 1e-2, rel_err(a, b)
+
+
 def test_matmul_t_exact_flag_bit_exact():
     a, b = rn(70, 40), rn(40, 50)
     g, o = run_both("matmul_t", [(a, BF16), (b, BF16)], [((70, 50), BF16)], {"exact": 1})
