@@ -396,14 +396,16 @@ def cpu_baseline_port():
 GEMM_OPS = {"linear", "matmul_t", "matmul_dact", "matmul_pair", "batch_matmul", "matmul"}
 
 
-def step_profile_report(s, peaks, step_flops, repeats=5):
+def step_profile_report(s, peaks, step_flops, repeats=3, inner=10):
     """vm.profile of the benchmarked step (eager, CUDA events around every
-    instruction): per op class the in-step device time per step, the bytes its
-    launches move (their input + output tensors: the algorithmic bytes of a
+    instruction, each launch run `inner` times back to back between its events
+    and averaged, so a short kernel's time is its in-stream cost rather than an
+    event round trip): per op class the in-step device time per step, the bytes
+    its launches move (their input + output tensors: the algorithmic bytes of a
     memory-bound op) and the achieved fraction of measured HBM bandwidth; the
-    GEMM classes against the dense bf16 peak.  Events between launches cost the
-    step its PDL overlap, so these times are a little above the graph replay's."""
-    rows = s.profile(repeats)
+    GEMM classes against the dense bf16 peak.  Runs last on the timed session
+    (the repeated launches advance its training state)."""
+    rows = s.profile(repeats, inner)
     hbm = peaks.get("hbm_gbs", FALLBACK_PEAKS["hbm_gbs"])
     cls = {}
     for r in rows:
@@ -428,7 +430,8 @@ def step_profile_report(s, peaks, step_flops, repeats=5):
     return {"classes": out, "profiled_step_ms": round(total_us / 1e3, 3), "gemm_ms": round(gemm_us / 1e3, 3),
             "memory_bound_ms": round(mem_us / 1e3, 3), "memory_bound_bytes": mem_bytes,
             "memory_bound_hbm_frac": round(mem_bytes / (mem_us * 1e-6) / 1e9 / hbm, 3) if mem_us else None,
-            "additive_roofline_ms": round(t_roof_ms, 3), "hbm_gbs_peak": hbm, "repeats": repeats}
+            "additive_roofline_ms": round(t_roof_ms, 3), "hbm_gbs_peak": hbm, "repeats": repeats,
+            "inner_launches": inner}
 
 
 def autocast_graph_rate(steps=20):

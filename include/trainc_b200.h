@@ -62,6 +62,9 @@ int tb_session_set_comm(void* h, void* comm);
 /* vm.profile: per-instruction median device time over `repeats` eager steps
  * (CSV idx,op,let,median_us,bytes_in,bytes_out,kernels); NULL on error */
 const char* tb_session_profile(void* h, int repeats);
+/* ... each launch instruction run `inner` times back to back between its
+ * events (the per-launch mean); advances the training state `inner` updates */
+const char* tb_session_profile_inner(void* h, int repeats, int inner);
 
 /* AutoCast pass census on the all-f32 step (CPU only; host/autocast.hpp) */
 int tb_autocast_info(const char* cfg, const char* policy, const char* placement, int64_t* out, int n);

@@ -72,7 +72,16 @@ void fold_use(FoldCtx* c) {
   s.on = c && c->pool;
 }
 
-void fold_defer(const FoldJob& j) { st().jobs.push_back(j); }
+void fold_defer(const FoldJob& j) {
+  // an identical job already queued (the same plan relaunched on the same
+  // buffers, e.g. vm.profile's repeated launches) folds the same partials
+  // into the same output: once is enough
+  for (const FoldJob& q : st().jobs)
+    if (q.src == j.src && q.out == j.out && q.ld == j.ld && q.nrows == j.nrows && q.ncols == j.ncols &&
+        q.scale == j.scale)
+      return;
+  st().jobs.push_back(j);
+}
 void fold_op_deferred() { ++st().ops_deferred; }
 void fold_counters(uint64_t* ops, uint64_t* launches) {
   *ops = st().ops_deferred;

@@ -390,10 +390,15 @@ const char* tb_session_text(void* h, const char* what) {
 
 /// vm.profile: `repeats` eager steps with CUDA events around
 /// every instruction; CSV idx,op,let,median_us,bytes_in,bytes_out,kernels.
-const char* tb_session_profile(void* h, int repeats) {
+const char* tb_session_profile(void* h, int repeats) { return tb_session_profile_inner(h, repeats, 1); }
+
+/// ... with every launch instruction run `inner` times back to back between
+/// its events (per-launch mean: no event round trip per launch).  Advances the
+/// session's training state `inner` updates per profiled step.
+const char* tb_session_profile_inner(void* h, int repeats, int inner) {
   auto* s = static_cast<Session*>(h);
   try {
-    s->text = s->vm.profile(s->stream, repeats);
+    s->text = s->vm.profile(s->stream, repeats, inner);
   } catch (const std::exception& e) {
     g_err = e.what();
     return nullptr;

@@ -367,6 +367,7 @@ class DeviceVM {
     void *e0, *e1;
   };
   std::vector<ProfMark>* prof_ = nullptr;
+  int prof_inner_ = 1;
   std::vector<void*> prof_events_;
   size_t prof_used_ = 0;
   void* prof_rec(void* stream) {
@@ -389,8 +390,18 @@ class DeviceVM {
   /// vm.profile: `repeats` eager steps with CUDA events around every
   /// instruction; one CSV row per instruction (and per deferred-fold flush):
   /// idx,op,let,median_us,bytes_in,bytes_out,kernels.  Compile time is not in
-  /// here (it happened at session creation: the one-time bucket).
-  std::string profile(void* stream, int repeats) {
+  /// here (it happened at session creation: the one-time bucket).  inner > 1:
+  /// each launch instruction runs `inner` times back to back between its
+  /// events and its time is the mean -- the in-stream cost of a launch without
+  /// the event round trip, the way the graph replay sees it.  It leaves the
+  /// session's training state advanced `inner` optimizer updates per step
+  /// (profile on a session whose state does not matter).
+  std::string profile(void* stream, int repeats, int inner = 1) {
+    prof_inner_ = std::max(1, inner);
+    struct InnerOff {
+      DeviceVM* v;
+      ~InnerOff() { v->prof_inner_ = 1; }
+    } inner_off{this};
     std::vector<std::vector<float>> times;
     std::vector<ProfMark> marks;
     std::vector<ProfMark> first;
@@ -412,7 +423,8 @@ class DeviceVM {
       for (size_t i = 0; i < marks.size(); ++i) {
         float ms = 0;
         tcb_check(tcb_event_elapsed_ms(marks[i].e0, marks[i].e1, &ms), "elapsed");
-        times[i].push_back(ms);
+        const bool launch = marks[i].instr >= 0 && code_[size_t(marks[i].instr)].kind == OpKind::Launch;
+        times[i].push_back(launch ? ms / float(prof_inner_) : ms);
       }
     }
     std::string out = "idx,op,let,median_us,bytes_in,bytes_out,kernels,shapes\n";
@@ -463,9 +475,12 @@ class DeviceVM {
       void* pe0 = prof_ ? prof_rec(stream) : nullptr;
       switch (x.kind) {
         case OpKind::Launch:
-          tcb_check(tcb_launch_ws(x.plan, x.in.data(), int(x.in.size()), x.out.data(), int(x.out.size()), ws_,
-                                  ws_bytes_, stream),
-                    x.op);
+          // vm.profile with inner > 1 relaunches each instruction back to back
+          // (data-independent timing; in-place ops see their own outputs)
+          for (int rep = 0; rep < (prof_ ? prof_inner_ : 1); ++rep)
+            tcb_check(tcb_launch_ws(x.plan, x.in.data(), int(x.in.size()), x.out.data(), int(x.out.size()), ws_,
+                                    ws_bytes_, stream),
+                      x.op);
           break;
         case OpKind::ReduceScatter:
           tcb_check(tcb_reduce_scatter(comm_, x.in.data(), int(x.in.size()), &x.out[0], stream), x.op);

@@ -75,6 +75,8 @@ def lib():
         L.tb_session_load_param.argtypes = [ctypes.c_void_p, ctypes.c_char_p, ctypes.c_char_p]
         L.tb_session_profile.restype = ctypes.c_char_p
         L.tb_session_profile.argtypes = [ctypes.c_void_p, ctypes.c_int]
+        L.tb_session_profile_inner.restype = ctypes.c_char_p
+        L.tb_session_profile_inner.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int]
         L.tb_derive_priorities.restype = ctypes.c_char_p
         L.tb_derive_priorities.argtypes = [ctypes.c_char_p]
         L.tb_memsched_text.restype = ctypes.c_char_p
@@ -356,10 +358,13 @@ class Session:
     def text(self, what: str) -> str:
         return lib().tb_session_text(self.h, what.encode()).decode()
 
-    def profile(self, repeats: int = 5) -> list[dict]:
+    def profile(self, repeats: int = 5, inner: int = 1) -> list[dict]:
         """vm.profile: per-instruction median device time of
-        eager steps (CUDA events around every instruction and fold flush)."""
-        t = lib().tb_session_profile(self.h, repeats)
+        eager steps (CUDA events around every instruction and fold flush).
+        inner > 1 runs each launch that many times back to back between its
+        events and reports the mean (no per-launch event round trip); it
+        advances the training state `inner` updates per profiled step."""
+        t = lib().tb_session_profile_inner(self.h, repeats, inner)
         if t is None:
             raise RuntimeError(lib().tb_last_error().decode())
         rows = []
