@@ -1520,50 +1520,112 @@ static void b_embedding_sum(Plan& p) {
 }
 TCB_REGISTER("embedding_sum", b_embedding_sum);
 
-// Deterministic scatter-add: stable rank of (id, t) pairs, then one warp per
-// distinct id accumulates its rows in ascending t onto base -- the oracle's
-// order exactly, so f32 results are bit-identical.
-// Stable counting rank of token t among all T ids (ids staged through smem in
-// tiles); the first occurrence of each id also records its segment length at
-// the segment's head position (seg_len is zeroed beforehand).
-// Stable rank of every token by (id, t): rank = #{u : id_u < id_t} +
-// #{u < t : id_u == id_t}.  One warp per token, lanes split the scan of a
-// shared-memory id tile and combine with shuffles (O(T^2 / 32) per warp, spread
-// over the whole GPU: T = 4096 is ~2 us).  Writes the sorted order and, per
-// sorted position, its segment head and (at heads) the segment length.
-constexpr int RANK_TILE = 4096;
-__global__ void __launch_bounds__(256) k_embed_rank(const int32_t* __restrict__ ids, int32_t* __restrict__ sorted,
-                                                    int32_t* __restrict__ seg_len, int32_t* __restrict__ seg_head,
-                                                    int64_t T) {
+// Deterministic scatter-add: the tokens are stably sorted by id (LSD radix
+// sort, 8-bit digits, ties in ascending t), then every chunk of <= EMB_CHUNK
+// equal ids accumulates its rows in ascending t onto base -- the oracle's
+// order exactly for segments of <= EMB_CHUNK rows, so f32 results are
+// bit-identical; longer segments fold their chunk sums in chunk order.
+// O(T) work per pass (the earlier pairwise rank was O(T^2): 0.56 s per launch
+// at T = 1.1M tokens, the remat max batch).
+constexpr int RDX_TILE = 2048;  // keys per block: 8 warps x 8 rounds x 32 lanes
+constexpr int RDX_WARPS = 8, RDX_ROUNDS = RDX_TILE / (RDX_WARPS * 32);
+
+// per-tile histogram of digit (key >> shift) & 255 -> counts[digit][tile]
+__global__ void __launch_bounds__(256) k_radix_count(const int32_t* __restrict__ keys, int64_t T, int shift,
+                                                     int32_t* __restrict__ counts, int ntiles) {
   TCB_PDL_ENTRY();
-  __shared__ int32_t tile[RANK_TILE];
-  const int lane = threadIdx.x & 31;
-  const int64_t t = blockIdx.x * 8 + (threadIdx.x >> 5);
-  const int32_t my = t < T ? ids[t] : 0;
-  int less = 0, eq_before = 0, eq = 0;
-  for (int64_t u0 = 0; u0 < T; u0 += RANK_TILE) {
-    const int n = int(T - u0 < RANK_TILE ? T - u0 : RANK_TILE);
+  __shared__ int32_t h[256];
+  h[threadIdx.x] = 0;
+  __syncthreads();
+  const int64_t t0 = int64_t(blockIdx.x) * RDX_TILE;
+  for (int e = threadIdx.x; e < RDX_TILE; e += 256)
+    if (t0 + e < T) atomicAdd(&h[(keys[t0 + e] >> shift) & 255], 1);
+  __syncthreads();
+  counts[int64_t(threadIdx.x) * ntiles + blockIdx.x] = h[threadIdx.x];
+}
+
+// exclusive scan of n counts in place (digit-major, tile-minor): one block
+__global__ void __launch_bounds__(1024) k_radix_scan(int32_t* __restrict__ c, int64_t n) {
+  TCB_PDL_ENTRY();
+  __shared__ int32_t part[1024];
+  const int64_t per = (n + 1023) / 1024, lo = threadIdx.x * per, hi = lo + per < n ? lo + per : n;
+  int32_t sum = 0;
+  for (int64_t i = lo; i < hi; ++i) sum += c[i];
+  part[threadIdx.x] = sum;
+  __syncthreads();
+  for (int off = 1; off < 1024; off <<= 1) {  // inclusive Hillis-Steele over the thread sums
+    const int32_t v = threadIdx.x >= unsigned(off) ? part[threadIdx.x - off] : 0;
     __syncthreads();
-    for (int k = threadIdx.x; k < n; k += blockDim.x) tile[k] = ids[u0 + k];
+    part[threadIdx.x] += v;
     __syncthreads();
-#pragma unroll 8
-    for (int k = lane; k < n; k += 32) {
-      const int32_t o = tile[k];
-      less += o < my;
-      eq += o == my;
-      eq_before += (o == my) & (u0 + k < t);
+  }
+  int32_t run = threadIdx.x ? part[threadIdx.x - 1] : 0;
+  for (int64_t i = lo; i < hi; ++i) {
+    const int32_t v = c[i];
+    c[i] = run;
+    run += v;
+  }
+}
+
+// stable scatter of one tile: element e = warp * 256 + round * 32 + lane (t
+// order); its rank among equal digits of the tile = equal digits in earlier
+// warps + earlier rounds of its warp + lower lanes of its round
+__global__ void __launch_bounds__(256) k_radix_scatter(const int32_t* __restrict__ kin,
+                                                       const int32_t* __restrict__ vin, int32_t* __restrict__ kout,
+                                                       int32_t* __restrict__ vout, int64_t T, int shift,
+                                                       const int32_t* __restrict__ offs, int ntiles) {
+  TCB_PDL_ENTRY();
+  __shared__ int32_t wc[RDX_WARPS][256];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < RDX_WARPS * 256; i += 256) (&wc[0][0])[i] = 0;
+  __syncthreads();
+  const int64_t t0 = int64_t(blockIdx.x) * RDX_TILE;
+  const uint32_t lt = (1u << lane) - 1u;
+  int32_t key[RDX_ROUNDS], val[RDX_ROUNDS], rk[RDX_ROUNDS];
+#pragma unroll
+  for (int r = 0; r < RDX_ROUNDS; ++r) {
+    const int64_t t = t0 + w * (RDX_ROUNDS * 32) + r * 32 + lane;
+    const bool ok = t < T;
+    key[r] = ok ? kin[t] : 0;
+    val[r] = ok ? (vin ? vin[t] : int32_t(t)) : 0;
+    const int d = ok ? (key[r] >> shift) & 255 : 256 + lane;  // tail lanes: unique non-digits
+    const uint32_t peers = __match_any_sync(0xffffffffu, d);
+    rk[r] = ok ? wc[w][d] + __popc(peers & lt) : 0;
+    __syncwarp();
+    if (ok && (peers & lt) == 0) wc[w][d] += __popc(peers);  // lowest lane of the group
+    __syncwarp();
+  }
+  __syncthreads();
+  {  // exclusive prefix over the warps, per digit (thread = digit)
+    int32_t run = 0;
+    for (int ww = 0; ww < RDX_WARPS; ++ww) {
+      const int32_t v = wc[ww][threadIdx.x];
+      wc[ww][threadIdx.x] = run;
+      run += v;
     }
   }
+  __syncthreads();
 #pragma unroll
-  for (int m = 16; m; m >>= 1) {
-    less += __shfl_xor_sync(0xffffffffu, less, m);
-    eq += __shfl_xor_sync(0xffffffffu, eq, m);
-    eq_before += __shfl_xor_sync(0xffffffffu, eq_before, m);
+  for (int r = 0; r < RDX_ROUNDS; ++r) {
+    const int64_t t = t0 + w * (RDX_ROUNDS * 32) + r * 32 + lane;
+    if (t >= T) continue;
+    const int d = (key[r] >> shift) & 255;
+    const int64_t pos = int64_t(offs[int64_t(d) * ntiles + blockIdx.x]) + wc[w][d] + rk[r];
+    kout[pos] = key[r];
+    vout[pos] = val[r];
   }
-  if (t >= T || lane) return;
-  sorted[less + eq_before] = int32_t(t);
-  seg_head[less + eq_before] = int32_t(less);
-  if (eq_before == 0) seg_len[less] = int32_t(eq);
+}
+
+// segment bounds by id from the sorted ids: start[id] = first position,
+// end[id] = one past the last (only ids that occur are written and read)
+__global__ void __launch_bounds__(256) k_embed_segments(const int32_t* __restrict__ sid, int64_t T,
+                                                        int32_t* __restrict__ start, int32_t* __restrict__ end) {
+  TCB_PDL_ENTRY();
+  for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < T; p += int64_t(gridDim.x) * blockDim.x) {
+    const int32_t id = sid[p];
+    if (p == 0 || sid[p - 1] != id) start[id] = int32_t(p);
+    if (p + 1 == T || sid[p + 1] != id) end[id] = int32_t(p + 1);
+  }
 }
 
 constexpr int EMB_CHUNK = 128;  // rows per partial sum of a long segment
@@ -1572,18 +1634,18 @@ constexpr int EMB_CHUNK = 128;  // rows per partial sum of a long segment
 // ascending t into part[chunk_start]) and folded here in chunk order onto
 // base: deterministic; for segments <= EMB_CHUNK rows k_embed_accum writes the
 // oracle's exact sequential sum directly.
-__global__ void __launch_bounds__(256) k_embed_fold(const int32_t* __restrict__ ids,
-                                                    const int32_t* __restrict__ sorted,
-                                                    const int32_t* __restrict__ seg_len,
+__global__ void __launch_bounds__(256) k_embed_fold(const int32_t* __restrict__ sid,
+                                                    const int32_t* __restrict__ start,
+                                                    const int32_t* __restrict__ end,
                                                     const float* __restrict__ part, float* __restrict__ out,
                                                     int64_t T, int64_t H) {
   TCB_PDL_ENTRY();
   const int64_t j = int64_t(blockIdx.y) * blockDim.x + threadIdx.x;
   // grid-stride over sorted positions: only heads of long segments do work
   for (int64_t pos = blockIdx.x; pos < T; pos += gridDim.x) {
-    const int32_t len = seg_len[pos];
-    if (len <= EMB_CHUNK || j >= H) continue;
-    const int32_t id = ids[sorted[pos]];
+    const int32_t id = sid[pos];
+    const int32_t head = start[id], len = end[id] - head;
+    if (pos != head || len <= EMB_CHUNK || j >= H) continue;
     float acc = out[int64_t(id) * H + j];
     for (int64_t c = pos; c < pos + len; c += EMB_CHUNK) acc = __fadd_rn(acc, part[c * H + j]);
     out[int64_t(id) * H + j] = acc;
@@ -1595,22 +1657,22 @@ __global__ void __launch_bounds__(256) k_embed_fold(const int32_t* __restrict__ 
 // (loads batched 4 deep; the adds keep the oracle's order).  Column-parallel,
 // so one id covering every token (token-type ids) is 256x wider than a warp.
 template <typename TD>
-__global__ void __launch_bounds__(256) k_embed_accum(const int32_t* __restrict__ ids,
+__global__ void __launch_bounds__(256) k_embed_accum(const int32_t* __restrict__ sid,
                                                      const int32_t* __restrict__ sorted,
-                                                     const int32_t* __restrict__ seg_len,
-                                                     const int32_t* __restrict__ seg_head,
+                                                     const int32_t* __restrict__ start,
+                                                     const int32_t* __restrict__ send,
                                                      const TD* __restrict__ dy, float* __restrict__ out,
                                                      float* __restrict__ part, int64_t T, int64_t H) {
   TCB_PDL_ENTRY();
   const int64_t j = int64_t(blockIdx.y) * blockDim.x + threadIdx.x;
   // grid-stride over sorted positions (most are not chunk starts and skip at once)
   for (int64_t pos = blockIdx.x; pos < T; pos += gridDim.x) {
-    const int64_t head = seg_head[pos];
+    const int32_t id = sid[pos];
+    const int64_t head = start[id];
     if ((pos - head) % EMB_CHUNK || j >= H) continue;  // not a chunk start
-    const int32_t len = seg_len[head];
+    const int32_t len = send[id] - int32_t(head);
     const bool single = len <= EMB_CHUNK;
     const int64_t end = (head + len) < (pos + EMB_CHUNK) ? (head + len) : (pos + EMB_CHUNK);
-    const int32_t id = ids[sorted[pos]];
     float acc = single ? out[int64_t(id) * H + j] : 0.0f;
     int64_t q = pos;
     // 16 row loads in flight per round (long segments are latency chains);
@@ -1641,12 +1703,21 @@ static void b_embedding_dx(Plan& p) {
   require(p.out[0].dtype == TCB_F32 && p.out[0].rank == 2, "embedding_dx: output is f32 [V, H]");
   const int64_t T = p.in[0].numel(), V = p.out[0].shape[0], H = p.out[0].shape[1];
   require(p.in[1].numel() == T * H, "embedding_dx: dy must be [T, H]");
+  require(T < (int64_t(1) << 31) && V < (int64_t(1) << 31), "embedding_dx: T and V must fit in int32");
   const bool has_base = p.in.size() > 2;
   if (has_base) require(p.in[2].dtype == TCB_F32 && p.in[2].numel() == V * H, "embedding_dx: base is f32 [V,H]");
-  const size_t sorted = p.ws_take(size_t(T) * 12);  // sorted[T] ++ seg_len[T] ++ seg_head[T]
+  // radix passes over the id bits (ids are in [0, V))
+  int bits = 1;
+  while ((int64_t(1) << bits) < V) ++bits;
+  const int passes = (bits + 7) / 8;
+  const int ntiles = int((T + RDX_TILE - 1) / RDX_TILE);
+  // key/value double buffers, digit counts, per-id segment bounds
+  const size_t kv = p.ws_take(size_t(T) * 16);
+  const size_t cnt = p.ws_take(size_t(256) * ntiles * 4);
+  const size_t seg = p.ws_take(size_t(V) * 8);
   // chunk partials of long segments (launch workspace)
   const size_t part = p.ws_take(size_t(T) * H * 4);
-  p.nkernels = 3;  // rank, accumulate, fold (+ a memset / memcpy node)
+  p.nkernels = 3 * passes + 3;  // passes x (count, scan, scatter), segments, accumulate, fold
   dispatch_float(p.in[1].dtype, [&](auto* tp) {
     using TD = std::remove_pointer_t<decltype(tp)>;
     p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
@@ -1656,19 +1727,36 @@ static void b_embedding_dx(Plan& p) {
       } else {
         TCB_CUDA(cudaMemsetAsync(out[0].ptr, 0, nb, s));
       }
-      int32_t* srt = (int32_t*)ws_at(sorted);
-      int32_t* seg = srt + T;
-      int32_t* hd = seg + T;
-      TCB_CUDA(cudaMemsetAsync(seg, 0, size_t(T) * 4, s));
-      const int32_t* ids = (const int32_t*)in[0].ptr;
+      int32_t* k0 = (int32_t*)ws_at(kv);
+      int32_t* v0 = k0 + T;
+      int32_t* k1 = v0 + T;
+      int32_t* v1 = k1 + T;
+      int32_t* counts = (int32_t*)ws_at(cnt);
+      int32_t* start = (int32_t*)ws_at(seg);
+      int32_t* send = start + V;
+      const int32_t* kin = (const int32_t*)in[0].ptr;
+      const int32_t* vin = nullptr;  // pass 0: values are the token indices
+      for (int ps = 0; ps < passes; ++ps) {
+        int32_t* ko = (ps & 1) ? k0 : k1;
+        int32_t* vo = (ps & 1) ? v0 : v1;
+        launch_k(k_radix_count, unsigned(ntiles), 256, 0, s, kin, T, 8 * ps, counts, ntiles);
+        launch_k(k_radix_scan, 1u, 1024, 0, s, counts, int64_t(256) * ntiles);
+        launch_k(k_radix_scatter, unsigned(ntiles), 256, 0, s, kin, vin, ko, vo, T, 8 * ps, (const int32_t*)counts,
+                 ntiles);
+        kin = ko;
+        vin = vo;
+      }
+      const int32_t* sid = kin;      // ids in sorted order
+      const int32_t* srt = vin;      // their token indices
+      launch_k(k_embed_segments, grid_for(T, 256), 256, 0, s, sid, T, start, send);
       // persistent-ish grids: ~8 CTAs per SM in total over the column tiles
       const int64_t ct = (H + 255) / 256;
       const int64_t gx = std::max<int64_t>(1, std::min<int64_t>(T, (kNumSMs * 8 + ct - 1) / ct));
       const dim3 g2{unsigned(gx), unsigned(ct)};
-      launch_k(k_embed_rank, unsigned((T + 7) / 8), 256, 0, s, ids, srt, seg, hd, T);
-      launch_k(k_embed_accum<TD>, g2, 256, 0, s, ids, srt, seg, hd, (const TD*)in[1].ptr, (float*)out[0].ptr,
-                                          (float*)ws_at(part), T, H);
-      launch_k(k_embed_fold, g2, 256, 0, s, ids, srt, seg, (const float*)ws_at(part), (float*)out[0].ptr, T, H);
+      launch_k(k_embed_accum<TD>, g2, 256, 0, s, sid, srt, (const int32_t*)start, (const int32_t*)send,
+               (const TD*)in[1].ptr, (float*)out[0].ptr, (float*)ws_at(part), T, H);
+      launch_k(k_embed_fold, g2, 256, 0, s, sid, (const int32_t*)start, (const int32_t*)send,
+               (const float*)ws_at(part), (float*)out[0].ptr, T, H);
     };
   });
 }

@@ -152,6 +152,31 @@ def test_embedding_dx_single_long_segment():
     assert bits_equal(g[0], o[0])
 
 
+@pytest.mark.parametrize("T,V,kind", [(5000, 30000, "random"), (4100, 2, "zeros"), (3000, 70000, "random"),
+                                      (70000, 512, "positions"), (257, 1, "zeros")])
+def test_embedding_dx_radix_sorted_segments(T, V, kind):
+    """The stable LSD radix sort behind embedding_dx (1, 2 and 3 digit passes,
+    ragged tiles): segments of <= 128 equal ids are the oracle's sequential
+    sums bit for bit, longer ones within 1e-6 (chunked fold)."""
+    H = 96
+    rng = np.random.default_rng(T + V)
+    if kind == "random":
+        ids = rng.integers(0, V, T).astype(np.int32)
+    elif kind == "zeros":
+        ids = np.zeros(T, np.int32)
+    else:
+        ids = (np.arange(T) % V).astype(np.int32)
+    dy = rn(T, H)
+    g, o = run_both("embedding_dx", [(ids, I32), (dy, F32)], [((V, H), F32)], {"rows": V})
+    longest = np.bincount(ids, minlength=V).max()
+    if longest <= 128:
+        assert bits_equal(g[0], o[0])
+    else:  # a different f32 summation order over `longest` terms: ~sqrt(n) eps relative
+        exact = np.zeros((V, H))
+        np.add.at(exact, ids, dy.astype(np.float64))
+        assert rel_err(g[0], exact) < 1e-5 and rel_err(o[0], exact) < 1e-5
+
+
 def test_mse_exact():
     g, o = run_both("mse", [(rn(64, 10), F32), (rn(64, 10), F32)], [((1,), F32)])
     assert bits_equal(g[0], o[0])
