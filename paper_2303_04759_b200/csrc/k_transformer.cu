@@ -1616,6 +1616,99 @@ __global__ void __launch_bounds__(256) k_radix_scatter(const int32_t* __restrict
   }
 }
 
+// Small inputs (T <= RDX_SMALL): every digit pass of the same stable sort in
+// one CTA through shared memory -- one launch instead of three per pass.
+// Element e = warp * (R * 32) + round * 32 + lane (t order), R = ceil(T / 1024).
+constexpr int RDX_SMALL = 8192, RDX_SW = 32;  // keys, warps
+constexpr int RDX_SMALL_SMEM = (4 * RDX_SMALL + RDX_SW * 256) * 4;  // 160 KB
+__global__ void __launch_bounds__(1024) k_radix_sort_small(const int32_t* __restrict__ ids, int T, int passes,
+                                                           int32_t* __restrict__ kout, int32_t* __restrict__ vout) {
+  TCB_PDL_ENTRY();
+  extern __shared__ int32_t sm[];
+  int32_t* kA = sm;
+  int32_t* vA = kA + RDX_SMALL;
+  int32_t* kB = vA + RDX_SMALL;
+  int32_t* vB = kB + RDX_SMALL;
+  int32_t* wc = vB + RDX_SMALL;  // [RDX_SW][256]
+  __shared__ int32_t base[256];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int R = (T + 1023) / 1024;
+  const uint32_t lt = (1u << lane) - 1u;
+  for (int i = threadIdx.x; i < T; i += 1024) {
+    kA[i] = ids[i];
+    vA[i] = i;
+  }
+  for (int ps = 0; ps < passes; ++ps) {
+    const int shift = 8 * ps;
+    for (int i = threadIdx.x; i < RDX_SW * 256; i += 1024) wc[i] = 0;
+    __syncthreads();
+    int32_t rk[RDX_SMALL / 1024];
+#pragma unroll
+    for (int r = 0; r < RDX_SMALL / 1024; ++r) {
+      if (r >= R) break;
+      const int e = w * (R * 32) + r * 32 + lane;
+      const bool ok = e < T;
+      const int d = ok ? (kA[e] >> shift) & 255 : 256 + lane;
+      const uint32_t peers = __match_any_sync(0xffffffffu, d);
+      rk[r] = ok ? wc[w * 256 + d] + __popc(peers & lt) : 0;
+      __syncwarp();
+      if (ok && (peers & lt) == 0) wc[w * 256 + d] += __popc(peers);
+      __syncwarp();
+    }
+    __syncthreads();
+    if (threadIdx.x < 256) {  // digit totals -> exclusive prefix over the warps
+      const int d = threadIdx.x;
+      int32_t run = 0;
+      for (int ww = 0; ww < RDX_SW; ++ww) {
+        const int32_t v = wc[ww * 256 + d];
+        wc[ww * 256 + d] = run;
+        run += v;
+      }
+      base[d] = run;
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {  // exclusive scan of the 256 digit totals (one warp, 8 per lane)
+      int32_t v[8], sum = 0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        v[k] = base[lane * 8 + k];
+        sum += v[k];
+      }
+      int32_t inc = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+      }
+      int32_t run = inc - sum;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        base[lane * 8 + k] = run;
+        run += v[k];
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < RDX_SMALL / 1024; ++r) {
+      if (r >= R) break;
+      const int e = w * (R * 32) + r * 32 + lane;
+      if (e >= T) continue;
+      const int d = (kA[e] >> shift) & 255;
+      const int pos = base[d] + wc[w * 256 + d] + rk[r];
+      kB[pos] = kA[e];
+      vB[pos] = vA[e];
+    }
+    __syncthreads();
+    int32_t* t;
+    t = kA, kA = kB, kB = t;
+    t = vA, vA = vB, vB = t;
+  }
+  for (int i = threadIdx.x; i < T; i += 1024) {
+    kout[i] = kA[i];
+    vout[i] = vA[i];
+  }
+}
+
 // segment bounds by id from the sorted ids: start[id] = first position,
 // end[id] = one past the last (only ids that occur are written and read)
 __global__ void __launch_bounds__(256) k_embed_segments(const int32_t* __restrict__ sid, int64_t T,
@@ -1717,7 +1810,13 @@ static void b_embedding_dx(Plan& p) {
   const size_t seg = p.ws_take(size_t(V) * 8);
   // chunk partials of long segments (launch workspace)
   const size_t part = p.ws_take(size_t(T) * H * 4);
-  p.nkernels = 3 * passes + 3;  // passes x (count, scan, scatter), segments, accumulate, fold
+  p.nkernels = (T <= RDX_SMALL ? 1 : 3 * passes) + 3;  // sort (one CTA, or count/scan/scatter per pass), segments, accumulate, fold
+  if (T <= RDX_SMALL) {
+    static std::once_flag once;
+    std::call_once(once, [] {
+      TCB_CUDA(cudaFuncSetAttribute(k_radix_sort_small, cudaFuncAttributeMaxDynamicSharedMemorySize, RDX_SMALL_SMEM));
+    });
+  }
   dispatch_float(p.in[1].dtype, [&](auto* tp) {
     using TD = std::remove_pointer_t<decltype(tp)>;
     p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
@@ -1736,7 +1835,12 @@ static void b_embedding_dx(Plan& p) {
       int32_t* send = start + V;
       const int32_t* kin = (const int32_t*)in[0].ptr;
       const int32_t* vin = nullptr;  // pass 0: values are the token indices
-      for (int ps = 0; ps < passes; ++ps) {
+      if (T <= RDX_SMALL) {
+        launch_k(k_radix_sort_small, 1u, 1024, RDX_SMALL_SMEM, s, kin, int(T), passes, k1, v1);
+        kin = k1;
+        vin = v1;
+      }
+      for (int ps = 0; T > RDX_SMALL && ps < passes; ++ps) {
         int32_t* ko = (ps & 1) ? k0 : k1;
         int32_t* vo = (ps & 1) ? v0 : v1;
         launch_k(k_radix_count, unsigned(ntiles), 256, 0, s, kin, T, 8 * ps, counts, ntiles);
