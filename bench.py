@@ -408,18 +408,36 @@ def step_profile_report(s, peaks, step_flops, repeats=3, inner=10):
     rows = s.profile(repeats, inner)
     hbm = peaks.get("hbm_gbs", FALLBACK_PEAKS["hbm_gbs"])
     cls = {}
+    def gemm_flops(op, ins, outs):
+        """2*M*N*K per problem, K = numel(A) / M (A = the first operand of the problem)"""
+        num = lambda shp: int(np.prod(shp)) if shp else 0  # noqa: E731
+        probs = [(ins[0], outs[0])]
+        if op == "matmul_pair" and len(outs) > 1 and len(ins) >= 4:
+            probs.append((ins[len(ins) - 2], outs[1]))
+        f = 0
+        for a, o in probs:
+            if len(o) >= 2 and o[-2]:
+                m, n = int(np.prod(o[:-1])), o[-1]
+                f += 2 * m * n * (num(a) // m)
+        return f
     for r in rows:
         op = r["op"].split(".")[-1]
-        c = cls.setdefault(op, {"launches": 0, "us": 0.0, "bytes": 0})
+        c = cls.setdefault(op, {"launches": 0, "us": 0.0, "bytes": 0, "flops": 0})
         c["launches"] += 1
         c["us"] += r["us"]
         c["bytes"] += r["bytes_in"] + r["bytes_out"]
+        if op in GEMM_OPS and r["in"] and r["out"]:
+            c["flops"] += gemm_flops(op, r["in"], r["out"])
     out, mem_bytes, mem_us, gemm_us, total_us = {}, 0, 0.0, 0.0, 0.0
     for op, c in sorted(cls.items(), key=lambda kv: -kv[1]["us"]):
         total_us += c["us"]
         e = {"launches": c["launches"], "us_per_step": round(c["us"], 1)}
         if op in GEMM_OPS:
             gemm_us += c["us"]
+            if c["flops"] and c["us"] > 0:
+                tf = c["flops"] / (c["us"] * 1e-6) / 1e12
+                e.update({"tflops": round(tf, 1),
+                          "tensor_frac": round(tf / peaks.get("bf16_tflops", FALLBACK_PEAKS["bf16_tflops"]), 3)})
         elif c["us"] > 0:
             gbs = c["bytes"] / (c["us"] * 1e-6) / 1e9
             e.update({"bytes_per_step": c["bytes"], "gbs": round(gbs, 1), "hbm_frac": round(gbs / hbm, 3)})
