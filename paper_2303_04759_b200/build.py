@@ -24,7 +24,8 @@ BASE = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxed
 # without FMA contraction
 EXACT = {"k_elementwise.cu", "k_reduce.cu", "k_optim.cu", "k_gemm_exact.cu", "fold.cu", "k_closure.cu"}
 SOURCES = ["abi.cu", "k_elementwise.cu", "k_reduce.cu", "k_optim.cu", "k_gemm_exact.cu",
-           "k_gemm_ops.cu", "k_gemm_tc.cu", "k_attention.cu", "k_flash.cu", "k_closure.cu", "k_transformer.cu", "comm.cu", "fold.cu"]
+           "k_gemm_ops.cu", "k_gemm_tc.cu", "k_attention.cu", "k_flash.cu", "k_closure.cu", "k_transformer.cu",
+           "k_layernorm.cu", "k_layernorm_dx.cu", "comm.cu", "fold.cu"]
 
 
 def _newer(src_list, target):

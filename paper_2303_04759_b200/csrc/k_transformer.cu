@@ -1,891 +1,15 @@
 // k_transformer.cu -- the memory-bound transformer ops the reference lacks
-// (SURVEY.md §2.4 / §8a A15): layer_norm (+ fused dropout-residual),
-// layer_norm_dx, softmax / softmax_dx, the attention fwd/bwd closures (tcgen05
+// (SURVEY.md §2.4 / §8a A15): softmax / softmax_dx (layer_norm and
+// layer_norm_dx live in k_layernorm*.cu), the attention fwd/bwd closures (tcgen05
 // GEMMs on strided head views + row softmax), embedding gather / deterministic
 // scatter-add, and the fused cross-entropy loss + gradient.
 //
 // Row kernels use one warp per row with 16-byte vector loads when the row length
 // allows, f32 statistics and warp-shuffle reductions; the oracle (oracle.c) has
 // the same formulas with sequential sums (tolerance-checked, not bit-exact).
-#include "gemm.cuh"
-#include "fold.cuh"
+#include "k_rowops.cuh"
 
 namespace tcb {
-
-// ---------------------------------------------------------------- utilities
-__device__ __forceinline__ float warp_sum(float v) {
-#pragma unroll
-  for (int m = 16; m; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
-  return v;
-}
-__device__ __forceinline__ float warp_max(float v) {
-#pragma unroll
-  for (int m = 16; m; m >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, m));
-  return v;
-}
-
-
-// 8 consecutive elements <-> floats
-template <typename T>
-struct Vec8;
-template <>
-struct Vec8<__nv_bfloat16> {
-  static __device__ __forceinline__ void load(const __nv_bfloat16* p, float* f) {
-    uint4 q = *reinterpret_cast<const uint4*>(p);
-    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&q);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      float2 t = __bfloat1622float2(h[i]);
-      f[2 * i] = t.x;
-      f[2 * i + 1] = t.y;
-    }
-  }
-  static __device__ __forceinline__ void store(__nv_bfloat16* p, const float* f) {
-    uint4 q;
-    __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&q);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
-    *reinterpret_cast<uint4*>(p) = q;
-  }
-};
-template <>
-struct Vec8<__half> {
-  static __device__ __forceinline__ void load(const __half* p, float* f) {
-    uint4 q = *reinterpret_cast<const uint4*>(p);
-    const __half2* h = reinterpret_cast<const __half2*>(&q);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      float2 t = __half22float2(h[i]);
-      f[2 * i] = t.x;
-      f[2 * i + 1] = t.y;
-    }
-  }
-  static __device__ __forceinline__ void store(__half* p, const float* f) {
-    uint4 q;
-    __half2* h = reinterpret_cast<__half2*>(&q);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) h[i] = __floats2half2_rn(f[2 * i], f[2 * i + 1]);
-    *reinterpret_cast<uint4*>(p) = q;
-  }
-};
-template <>
-struct Vec8<float> {
-  static __device__ __forceinline__ void load(const float* p, float* f) {
-    float4 a = *reinterpret_cast<const float4*>(p), b = *reinterpret_cast<const float4*>(p + 4);
-    f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w;
-    f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
-  }
-  static __device__ __forceinline__ void store(float* p, const float* f) {
-    *reinterpret_cast<float4*>(p) = make_float4(f[0], f[1], f[2], f[3]);
-    *reinterpret_cast<float4*>(p + 4) = make_float4(f[4], f[5], f[6], f[7]);
-  }
-};
-
-// load/store 8 elements starting at i (vector path when aligned, else scalar)
-template <typename T>
-__device__ __forceinline__ void ld8(const T* p, int64_t i, int64_t n, bool vec, float* f) {
-  if (vec) {
-    Vec8<T>::load(p + i, f);
-  } else {
-#pragma unroll
-    for (int k = 0; k < 8; ++k) f[k] = i + k < n ? to_f(p[i + k]) : 0.0f;
-  }
-}
-template <typename T>
-__device__ __forceinline__ void st8(T* p, int64_t i, int64_t n, bool vec, const float* f) {
-  if (vec) {
-    Vec8<T>::store(p + i, f);
-  } else {
-#pragma unroll
-    for (int k = 0; k < 8; ++k)
-      if (i + k < n) p[i + k] = from_f<T>(f[k]);
-  }
-}
-
-constexpr int LN_MAXC = 8;  // up to 8 chunks of 8 per lane: H <= 2048
-
-// calls f(std::integral_constant<int, NC>) with NC = ceil(H / 256)
-template <typename Fn>
-static void dispatch_nc(int H, Fn&& f) {
-  switch ((H + 255) / 256) {
-    case 1: f(std::integral_constant<int, 1>{}); return;
-    case 2: f(std::integral_constant<int, 2>{}); return;
-    case 3: f(std::integral_constant<int, 3>{}); return;
-    case 4: f(std::integral_constant<int, 4>{}); return;
-    case 5: f(std::integral_constant<int, 5>{}); return;
-    case 6: f(std::integral_constant<int, 6>{}); return;
-    case 7: f(std::integral_constant<int, 7>{}); return;
-    case 8: f(std::integral_constant<int, 8>{}); return;
-  }
-  fail(TCB_ERR_UNIMPLEMENTED, "layer norm: hidden size > 2048 unsupported");
-}
-
-// keep bits for elements i .. i+7 (two Philox calls when i is 4-aligned)
-__device__ __forceinline__ uint32_t drop_bits8(const DropCfg& d, uint64_t i) {
-  if (d.p <= 0.0f) return 0xFFu;
-  if ((i & 7) == 0) return dropout_bits8q(d, i >> 3);
-  uint32_t b = 0;
-  for (int k = 0; k < 8; ++k) b |= uint32_t(dropout_keep(d, i + k)) << k;
-  return b;
-}
-
-// ------------------------------------------------------------ layer norm fwd
-// y = LN(s) where s = x (layer_norm) or s = round(dropout(x) + r) (add_layer_norm)
-// NC: 8-element chunks per lane (H <= 256*NC), so the row stays in registers
-// with no dead predicated slots.
-template <typename T, int NC>
-__global__ void __launch_bounds__(256) k_ln_fwd(const T* __restrict__ x, const T* __restrict__ r,
-                                                const float* __restrict__ gamma_f,
-                                                const T* __restrict__ gamma_t, const float* __restrict__ beta_f,
-                                                const T* __restrict__ beta_t, T* __restrict__ y,
-                                                T* __restrict__ s_out, float* __restrict__ mean_o,
-                                                float* __restrict__ rstd_o, int64_t rows, int H, float eps,
-                                                DropCfg d, bool vec) {
-  TCB_PDL_ENTRY();
-  drop_resolve(d);
-  // RW rows per warp, every global load of both rows issued before the first
-  // reduction so enough bytes are in flight to cover DRAM latency
-  constexpr int RW = NC <= 2 ? 2 : 1;
-  const int lane = threadIdx.x & 31;
-  const int64_t row0 = (blockIdx.x * int64_t(blockDim.x >> 5) + (threadIdx.x >> 5)) * RW;
-  if (row0 >= rows) return;
-  const int nch = (H + 7) / 8;
-  float v[RW][NC][8], rr[RW][NC][8];
-#pragma unroll
-  for (int q = 0; q < RW; ++q)
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
-      const int64_t row = row0 + q;
-      const int ch = lane + c * 32;
-      if (row < rows && ch < nch) {
-        const int64_t i = row * H + ch * 8;
-        ld8(x, i, (row + 1) * int64_t(H), vec, v[q][c]);
-        if (r) ld8(r, i, (row + 1) * int64_t(H), vec, rr[q][c]);
-      }
-    }
-  float sum[RW];
-#pragma unroll
-  for (int q = 0; q < RW; ++q) {
-    sum[q] = 0.0f;
-    const int64_t row = row0 + q;
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
-      const int ch = lane + c * 32;
-      if (row < rows && ch < nch) {
-        const int64_t i = row * H + ch * 8;
-        if (r) {
-          const uint32_t bits = drop_bits8(d, uint64_t(i));
-          if (d.mask_out && (i & 7) == 0) d.mask_out[i >> 3] = uint8_t(bits);
-#pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            float xv = ((bits >> k) & 1u) ? __fmul_rn(v[q][c][k], d.scale) : 0.0f;
-            v[q][c][k] = to_f(from_f<T>(__fadd_rn(xv, rr[q][c][k])));  // s rounded to storage dtype
-          }
-          st8(s_out, i, (row + 1) * int64_t(H), vec, v[q][c]);
-        }
-#pragma unroll
-        for (int k = 0; k < 8; ++k)
-          if (ch * 8 + k < H) sum[q] += v[q][c][k];
-      }
-    }
-  }
-  const float inv = 1.0f / float(H);
-  float mean[RW], sq[RW];
-#pragma unroll
-  for (int q = 0; q < RW; ++q) mean[q] = warp_sum(sum[q]) * inv;
-#pragma unroll
-  for (int q = 0; q < RW; ++q) {
-    sq[q] = 0.0f;
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
-      const int ch = lane + c * 32;
-      if (ch < nch) {
-#pragma unroll
-        for (int k = 0; k < 8; ++k)
-          if (ch * 8 + k < H) {
-            float dd = v[q][c][k] - mean[q];
-            sq[q] += dd * dd;
-          }
-      }
-    }
-  }
-#pragma unroll
-  for (int q = 0; q < RW; ++q) {
-    const int64_t row = row0 + q;
-    if (row >= rows) break;
-    const float rstd = 1.0f / sqrtf(warp_sum(sq[q]) * inv + eps);
-    if (lane == 0) {
-      mean_o[row] = mean[q];
-      rstd_o[row] = rstd;
-    }
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
-      const int ch = lane + c * 32;
-      if (ch < nch) {
-        float o[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const int j = ch * 8 + k;
-          if (j < H) {
-            float g = gamma_f ? __ldg(gamma_f + j) : to_f(gamma_t[j]);
-            float b = beta_f ? __ldg(beta_f + j) : to_f(beta_t[j]);
-            o[k] = (v[q][c][k] - mean[q]) * rstd * g + b;
-          } else {
-            o[k] = 0.0f;
-          }
-        }
-        st8(y, row * H + ch * 8, (row + 1) * int64_t(H), vec, o);
-      }
-    }
-  }
-}
-
-// 16-bit vector fast path (bf16/f16, H % 8 == 0, 16-byte rows): two rows per
-// warp with every load of both rows issued up front and kept packed (8
-// elements per uint4), so a 2-CTA/SM wave holds all BERT-base rows in flight.
-// The path is instruction-bound (one wave, ~13 warps/SM), so: gamma / beta as
-// 16-byte vectors, paired f32->16-bit conversions, y = fma(fma(s, rstd,
-// -mean*rstd), g, b), and FULL (H == NC*256) drops the per-chunk guards.
-template <typename T>
-__device__ __forceinline__ void unpack8(const uint4& q, float* f) {
-  const T* h = reinterpret_cast<const T*>(&q);
-#pragma unroll
-  for (int k = 0; k < 8; ++k) f[k] = to_f(h[k]);
-}
-template <typename T>
-__device__ __forceinline__ uint32_t pack2(float a, float b) {
-  if constexpr (std::is_same<T, __nv_bfloat16>::value) {
-    __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
-    return *reinterpret_cast<uint32_t*>(&h);
-  } else {
-    __half2 h = __floats2half2_rn(a, b);
-    return *reinterpret_cast<uint32_t*>(&h);
-  }
-}
-template <typename T>
-__device__ __forceinline__ uint4 pack8(const float* f) {
-  return make_uint4(pack2<T>(f[0], f[1]), pack2<T>(f[2], f[3]), pack2<T>(f[4], f[5]), pack2<T>(f[6], f[7]));
-}
-// 8 packed 16-bit values <-> 4 float2 (element pairs for the f32x2 ops)
-template <typename T>
-__device__ __forceinline__ void unpack8x2(const uint4& q, float2* f) {
-  const uint32_t* w = reinterpret_cast<const uint32_t*>(&q);
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    if constexpr (std::is_same<T, __nv_bfloat16>::value) f[k] = bf2_to_f2(w[k]);
-    else f[k] = __half22float2(*reinterpret_cast<const __half2*>(&w[k]));
-  }
-}
-template <typename T>
-__device__ __forceinline__ uint4 pack8x2(const float2* f) {
-  return make_uint4(pack2<T>(f[0].x, f[0].y), pack2<T>(f[1].x, f[1].y), pack2<T>(f[2].x, f[2].y),
-                    pack2<T>(f[3].x, f[3].y));
-}
-// keep-mask select of a pair: (bit k ? t.x : 0, bit k+1 ? t.y : 0)
-__device__ __forceinline__ float2 keep2(uint32_t bits, int k, float2 t) {
-  return make_float2(((bits >> k) & 1u) ? t.x : 0.0f, ((bits >> (k + 1)) & 1u) ? t.y : 0.0f);
-}
-// per-column f32 parameters staged in smem once per CTA (gamma [, beta]): one
-// 16-byte load per thread, all in flight together (H % 8 == 0, 16-byte aligned)
-template <typename T, bool GF>
-__device__ __forceinline__ void stage_params(const void* g, const void* b, float* sg, float* sb, int H) {
-  const int n8 = H / 8, n = b ? 2 * n8 : n8;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    const bool isb = i >= n8;
-    const int c = isb ? i - n8 : i;
-    float4* dst = reinterpret_cast<float4*>((isb ? sb : sg) + c * 8);
-    if constexpr (GF) {
-      const float4* src = reinterpret_cast<const float4*>(static_cast<const float*>(isb ? b : g) + c * 8);
-      const float4 u = __ldg(src), v = __ldg(src + 1);
-      dst[0] = u;
-      dst[1] = v;
-    } else {
-      float f[8];
-      unpack8<T>(__ldg(reinterpret_cast<const uint4*>(static_cast<const T*>(isb ? b : g) + c * 8)), f);
-      dst[0] = make_float4(f[0], f[1], f[2], f[3]);
-      dst[1] = make_float4(f[4], f[5], f[6], f[7]);
-    }
-  }
-}
-__device__ __forceinline__ void lds8x2(const float* p, float2* f) {
-  const float4 a = reinterpret_cast<const float4*>(p)[0], b = reinterpret_cast<const float4*>(p)[1];
-  f[0] = make_float2(a.x, a.y); f[1] = make_float2(a.z, a.w);
-  f[2] = make_float2(b.x, b.y); f[3] = make_float2(b.z, b.w);
-}
-
-template <typename T, int NC, bool GF, bool FULL>
-__global__ void __launch_bounds__(256) k_ln_fwd16(const T* __restrict__ x, const T* __restrict__ r,
-                                                  const void* __restrict__ gamma, const void* __restrict__ beta,
-                                                  T* __restrict__ y, T* __restrict__ s_out, float* __restrict__ mean_o,
-                                                  float* __restrict__ rstd_o, int64_t rows, int H, float eps,
-                                                  DropCfg d) {
-  TCB_PDL_ENTRY();
-  drop_resolve(d);
-  constexpr int RW = 2;
-  __shared__ __align__(16) float sg[NC * 256], sb[NC * 256];
-  const int lane = threadIdx.x & 31;
-  const int64_t row0 = (blockIdx.x * int64_t(blockDim.x >> 5) + (threadIdx.x >> 5)) * RW;
-  const int nch = FULL ? NC * 32 : H / 8;
-  uint4 xq[RW][NC], rq[RW][NC];
-#pragma unroll
-  for (int q = 0; q < RW; ++q)
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
-      const int ch = lane + c * 32;
-      if (row0 + q < rows && (FULL || ch < nch)) {
-        const int64_t i = (row0 + q) * H + ch * 8;
-        xq[q][c] = __ldg(reinterpret_cast<const uint4*>(x + i));
-        if (r) rq[q][c] = __ldg(reinterpret_cast<const uint4*>(r + i));
-      }
-    }
-  stage_params<T, GF>(gamma, beta, sg, sb, H);
-  __syncthreads();
-  const float inv = 1.0f / float(H);
-  const float2 sc2 = splat2(d.scale);
-#pragma unroll
-  for (int q = 0; q < RW; ++q) {
-    const int64_t row = row0 + q;
-    if (row >= rows) break;
-    float2 v[NC][4];
-    float2 sum2 = make_float2(0.0f, 0.0f);
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
-      const int ch = lane + c * 32;
-      if (FULL || ch < nch) {
-        unpack8x2<T>(xq[q][c], v[c]);
-        if (r) {
-          const int64_t i = row * H + ch * 8;
-          float2 rv[4];
-          unpack8x2<T>(rq[q][c], rv);
-          const uint32_t bits = d.p > 0.0f ? dropout_bits8q(d, uint64_t(i) >> 3) : 0xFFu;
-          if (d.mask_out) d.mask_out[i >> 3] = uint8_t(bits);
-          float2 sv[4];
-#pragma unroll
-          for (int k = 0; k < 4; ++k) sv[k] = add2(keep2(bits, 2 * k, mul2(v[c][k], sc2)), rv[k]);
-          const uint4 w = pack8x2<T>(sv);  // s in the storage dtype
-          unpack8x2<T>(w, v[c]);
-          *reinterpret_cast<uint4*>(s_out + i) = w;
-        }
-#pragma unroll
-        for (int k = 0; k < 4; ++k) sum2 = add2(sum2, v[c][k]);
-      } else {
-#pragma unroll
-        for (int k = 0; k < 4; ++k) v[c][k] = make_float2(0.0f, 0.0f);
-      }
-    }
-    const float mean = warp_sum(sum2.x + sum2.y) * inv;
-    const float2 nm2 = splat2(-mean);
-    float2 sq2 = make_float2(0.0f, 0.0f);
-#pragma unroll
-    for (int c = 0; c < NC; ++c)
-      if (FULL || lane + c * 32 < nch)
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const float2 dd = add2(v[c][k], nm2);
-          sq2 = fma2(dd, dd, sq2);
-        }
-    const float rstd = 1.0f / sqrtf(warp_sum(sq2.x + sq2.y) * inv + eps);
-    const float2 rs2 = splat2(rstd), nmr2 = splat2(-mean * rstd);
-    if (lane == 0) {
-      mean_o[row] = mean;
-      rstd_o[row] = rstd;
-    }
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
-      const int ch = lane + c * 32;
-      if (FULL || ch < nch) {
-        float2 g[4], b[4], o[4];
-        lds8x2(sg + ch * 8, g);
-        lds8x2(sb + ch * 8, b);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) o[k] = fma2(fma2(v[c][k], rs2, nmr2), g[k], b[k]);
-        uint4 w = pack8x2<T>(o);
-        if (!r && d.p > 0.0f) {  // post_dropout: dropout(LN(x)) as the separate op rounds it
-          const uint32_t bits = dropout_bits8q(d, uint64_t(row * H + ch * 8) >> 3);
-          unpack8x2<T>(w, o);
-#pragma unroll
-          for (int k = 0; k < 4; ++k) o[k] = keep2(bits, 2 * k, mul2(o[k], sc2));
-          w = pack8x2<T>(o);
-        }
-        *reinterpret_cast<uint4*>(y + row * H + ch * 8) = w;
-      }
-    }
-  }
-}
-
-static void build_ln_fwd(Plan& p, bool residual) {
-  if (residual) check_arity(p, 4, 4, 4, 5);
-  else check_arity(p, 3, 3, 3, 3);
-  // add_layer_norm save_mask: a 5th output holds the residual-branch keep bits
-  const bool save_mask = residual && p.out.size() == 5;
-  const Spec& X = p.in[0];
-  const int H = int(X.dim(-1));
-  const int64_t rows = X.numel() / H;
-  require(H <= LN_MAXC * 8 * 32, p.op + ": hidden size > 2048 unsupported");
-  const Spec& G = p.in[residual ? 2 : 1];
-  require(G.numel() == H, p.op + ": gamma must have H elements");
-  require(G.dtype == TCB_F32 || G.dtype == X.dtype, p.op + ": gamma dtype");
-  const bool gf = G.dtype == TCB_F32;
-  const float eps = float(p.attrs.f("eps", 1e-12));
-  DropCfg d0 = drop_cfg(p.attrs);
-  // plain layer_norm: dropout on the OUTPUT only with attr post_dropout (16-bit path)
-  const bool post_drop = !residual && p.attrs.i("post_dropout", 0) != 0 && d0.p > 0.0f;
-  if (!residual && !post_drop) d0 = DropCfg{};
-  if (post_drop) require(X.dtype != TCB_F32 && H % 8 == 0, p.op + ": post_dropout needs a 16-bit input, H % 8 == 0");
-  if (save_mask)
-    require(H % 8 == 0 && d0.p > 0.0f && p.out[4].numel() * dtype_bytes(p.out[4].dtype) * 8 >= X.numel(),
-            p.op + ": save_mask needs p > 0, H % 8 == 0 and a T*H/8-byte mask output");
-  dispatch_float(X.dtype, [&](auto* tp) {
-   using T = std::remove_pointer_t<decltype(tp)>;
-   dispatch_nc(H, [&](auto nc) {
-    constexpr int NC = decltype(nc)::value;
-    p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
-      DropCfg d = with_step(d0);
-      if (save_mask) d.mask_out = static_cast<uint8_t*>(out[4].ptr);
-      const int gi = residual ? 2 : 1;
-      bool vec = (H % 8 == 0);
-      for (int i = 0; i < (residual ? 2 : 1); ++i) vec = vec && reinterpret_cast<uintptr_t>(in[i].ptr) % 16 == 0;
-      vec = vec && reinterpret_cast<uintptr_t>(out[0].ptr) % 16 == 0;
-      if (residual) vec = vec && reinterpret_cast<uintptr_t>(out[1].ptr) % 16 == 0;
-      if constexpr (sizeof(T) == 2) {
-        // parameter vectors need 16-byte alignment too
-        for (int i = gi; i < gi + 2; ++i) vec = vec && reinterpret_cast<uintptr_t>(in[i].ptr) % 16 == 0;
-        if (vec) {
-          const bool full = H == NC * 256;
-          auto kern = gf ? (full ? k_ln_fwd16<T, NC, true, true> : k_ln_fwd16<T, NC, true, false>)
-                         : (full ? k_ln_fwd16<T, NC, false, true> : k_ln_fwd16<T, NC, false, false>);
-          launch_k(kern, unsigned((rows + 15) / 16), 256, 0, s, (const T*)in[0].ptr,
-                   residual ? (const T*)in[1].ptr : nullptr, (const void*)in[gi].ptr, (const void*)in[gi + 1].ptr,
-                   (T*)out[0].ptr, residual ? (T*)out[1].ptr : nullptr, (float*)out[residual ? 2 : 1].ptr,
-                   (float*)out[residual ? 3 : 2].ptr, rows, H, eps, d);
-          return;
-        }
-      }
-      if (post_drop) fail(TCB_ERR_UNIMPLEMENTED, p.op + ": post_dropout needs aligned 16-bit rows");
-      constexpr int RW = NC <= 2 ? 2 : 1;
-      launch_k(k_ln_fwd<T, NC>, unsigned((rows + 8 * RW - 1) / (8 * RW)), 256, 0, s, 
-          (const T*)in[0].ptr, residual ? (const T*)in[1].ptr : nullptr,
-          gf ? (const float*)in[gi].ptr : nullptr, gf ? nullptr : (const T*)in[gi].ptr,
-          gf ? (const float*)in[gi + 1].ptr : nullptr, gf ? nullptr : (const T*)in[gi + 1].ptr,
-          (T*)out[0].ptr, residual ? (T*)out[1].ptr : nullptr, (float*)out[residual ? 2 : 1].ptr,
-          (float*)out[residual ? 3 : 2].ptr, rows, H, eps, d, vec);
-    };
-   });
-  });
-}
-static void b_layer_norm(Plan& p) { build_ln_fwd(p, false); }
-static void b_add_layer_norm(Plan& p) { build_ln_fwd(p, true); }
-TCB_REGISTER("layer_norm", b_layer_norm);
-TCB_REGISTER("add_layer_norm", b_add_layer_norm);
-
-// ------------------------------------------------------------ layer norm bwd
-// dy += dy2 (fused fan-out accumulation); ds = rstd*(g - mean(g) - xh*mean(g*xh));
-// dx = dropout(ds);
-// per-CTA partial column sums of dy*xh and dy -> ws, then k_colsum finalises.
-constexpr int LNB_ROWS = 16;  // rows per CTA (8 warps x 2 rows)
-
-template <typename T, int NC>
-__global__ void __launch_bounds__(256) k_ln_bwd(const T* __restrict__ sx, const float* __restrict__ gamma_f,
-                                                const T* __restrict__ gamma_t, const float* __restrict__ mean,
-                                                const float* __restrict__ rstd, const T* __restrict__ dy,
-                                                const T* __restrict__ dy2, T* __restrict__ ds_o,
-                                                T* __restrict__ dx_o, float* __restrict__ ws, int nparts,
-                                                int64_t rows, int H, DropCfg d, bool vec) {
-  TCB_PDL_ENTRY();
-  drop_resolve(d);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int nch = (H + 7) / 8;
-  // per-warp dgamma/dbeta partials live in smem (not registers), laid out
-  // [warp][2][k][chunk] so a warp's accesses are bank-conflict free
-  extern __shared__ float red[];
-  constexpr int CP = NC * 32;  // chunk pitch
-  float* pg = red + (warp * 3 + 0) * 8 * CP;
-  float* pb = red + (warp * 3 + 1) * 8 * CP;
-  float* pz = red + (warp * 3 + 2) * 8 * CP;  // bias grad: column sums of the outgoing gradient
-#pragma unroll
-  for (int c = 0; c < NC; ++c)
-#pragma unroll
-    for (int k = 0; k < 8; ++k) pg[k * CP + c * 32 + lane] = pb[k * CP + c * 32 + lane] = pz[k * CP + c * 32 + lane] = 0.0f;
-  const float inv = 1.0f / float(H);
-  for (int rr = 0; rr < LNB_ROWS / 8; ++rr) {
-    const int64_t row = int64_t(blockIdx.x) * LNB_ROWS + warp * (LNB_ROWS / 8) + rr;
-    if (row >= rows) break;
-    const float mu = mean[row], rs = rstd[row];
-    float xh[NC][8], g[NC][8];
-    float c1 = 0.0f, c2 = 0.0f;
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
-      const int ch = lane + c * 32;
-      if (ch < nch) {
-        const int64_t i = row * H + ch * 8;
-        float sv[8], dv[8];
-        ld8(sx, i, (row + 1) * int64_t(H), vec, sv);
-        ld8(dy, i, (row + 1) * int64_t(H), vec, dv);
-        if (dy2) {
-          float d2[8];
-          ld8(dy2, i, (row + 1) * int64_t(H), vec, d2);
-#pragma unroll
-          for (int k = 0; k < 8; ++k) dv[k] = __fadd_rn(dv[k], d2[k]);
-        }
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const int j = ch * 8 + k;
-          if (j < H) {
-            float gm = gamma_f ? gamma_f[j] : to_f(gamma_t[j]);
-            xh[c][k] = (sv[k] - mu) * rs;
-            g[c][k] = dv[k] * gm;
-            c1 += g[c][k] * xh[c][k];
-            c2 += g[c][k];
-            pg[k * CP + c * 32 + lane] += dv[k] * xh[c][k];
-            pb[k * CP + c * 32 + lane] += dv[k];
-          } else {
-            xh[c][k] = g[c][k] = 0.0f;
-          }
-        }
-      }
-    }
-    c1 = warp_sum(c1) * inv;
-    c2 = warp_sum(c2) * inv;
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
-      const int ch = lane + c * 32;
-      if (ch < nch) {
-        const int64_t i = row * H + ch * 8;
-        float o[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) o[k] = rs * (g[c][k] - c2 - xh[c][k] * c1);
-        st8(ds_o, i, (row + 1) * int64_t(H), vec, o);
-        if (dx_o) {
-          const uint32_t bits = d.mask_in ? uint32_t(d.mask_in[i >> 3]) : drop_bits8(d, uint64_t(i));
-#pragma unroll
-          for (int k = 0; k < 8; ++k) o[k] = ((bits >> k) & 1u) ? o[k] * d.scale : 0.0f;
-          st8(dx_o, i, (row + 1) * int64_t(H), vec, o);
-        }
-        if (nparts > 2) {
-#pragma unroll
-          for (int k = 0; k < 8; ++k)
-            if (ch * 8 + k < H) pz[k * CP + c * 32 + lane] += to_f(from_f<T>(o[k]));
-        }
-      }
-    }
-  }
-  // CTA partials: fold the 8 warps' smem rows, then one row of ws per CTA
-  __syncthreads();
-  for (int j = threadIdx.x; j < H; j += blockDim.x) {
-    const int off = (j & 7) * CP + (j >> 3);
-    for (int a = 0; a < nparts; ++a) {
-      float acc = 0.0f;
-      for (int w = 0; w < 8; ++w) acc += red[(w * 3 + a) * 8 * CP + off];
-      ws[(int64_t(blockIdx.x) * nparts + a) * H + j] = acc;
-    }
-  }
-}
-
-// 16-bit vector fast path: both rows' loads issued up front (packed). Pass 1
-// walks chunk-major over the two rows, so each column's dgamma / dbeta partial
-// (the two rows' sum) is complete in registers and stored once to the warp's
-// smem row [warp][part][H] (no read-modify-write); pass 2 recomputes xh and g
-// from the packed loads, writes ds / dx and the bias-grad partial likewise.
-// The 8 warp rows fold per CTA (16-byte smem reads) into one ws row per part.
-template <typename T, int NC, bool GF, bool FULL>
-__global__ void __launch_bounds__(256, NC <= 3 ? 2 : 1) k_ln_bwd16(const T* __restrict__ sx, const void* __restrict__ gamma,
-                                                  const float* __restrict__ mean, const float* __restrict__ rstd,
-                                                  const T* __restrict__ dy, const T* __restrict__ dy2,
-                                                  T* __restrict__ ds_o, T* __restrict__ dx_o, float* __restrict__ ws,
-                                                  int nparts, int64_t rows, int H, DropCfg d, DropCfg din) {
-  TCB_PDL_ENTRY();
-  drop_resolve(d);
-  drop_resolve(din);
-  constexpr int RW = LNB_ROWS / 8;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int nch = FULL ? NC * 32 : H / 8;
-  extern __shared__ __align__(16) float red[];  // [8 warps][3 parts][H], then gamma (f32) [H]
-  float* prow = red + warp * 3 * H;
-  float* sg = red + 8 * 3 * H;
-  const int64_t row0 = int64_t(blockIdx.x) * LNB_ROWS + warp * RW;
-  uint4 sq[RW][NC], dq[RW][NC], d2q[RW][NC];
-  float2 rs2[RW], nmr2[RW];
-  bool live[RW];
-#pragma unroll
-  for (int q = 0; q < RW; ++q) {
-    live[q] = row0 + q < rows;
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
-      const int ch = lane + c * 32;
-      if (live[q] && (FULL || ch < nch)) {
-        const int64_t i = (row0 + q) * H + ch * 8;
-        sq[q][c] = __ldg(reinterpret_cast<const uint4*>(sx + i));
-        dq[q][c] = __ldg(reinterpret_cast<const uint4*>(dy + i));
-        if (dy2) d2q[q][c] = __ldg(reinterpret_cast<const uint4*>(dy2 + i));
-      }
-    }
-    const float mu = live[q] ? mean[row0 + q] : 0.0f, rs = live[q] ? rstd[row0 + q] : 0.0f;
-    rs2[q] = splat2(rs);
-    nmr2[q] = splat2(-mu * rs);
-  }
-  stage_params<T, GF>(gamma, nullptr, sg, nullptr, H);
-  __syncthreads();
-  // in_dropout (the output dropout of a plain layer_norm folded in): the incoming
-  // gradient is the separate dropout op's result, round(keep ? dy * scale : 0)
-  uint32_t inb[RW][NC];
-  if (din.p > 0.0f) {
-#pragma unroll
-    for (int q = 0; q < RW; ++q)
-#pragma unroll
-      for (int c = 0; c < NC; ++c)
-        inb[q][c] = live[q] ? dropout_bits8q(din, uint64_t((row0 + q) * H + (lane + c * 32) * 8) >> 3) : 0u;
-  }
-  const float2 isc2 = splat2(din.scale);
-  // xh = s*rs - mu*rs, dv = dy + dy2 and g = dv * gamma of chunk c of row q (pairs)
-  auto load_row = [&](int q, int c, const float2* gm, float2* xh, float2* dv, float2* g) {
-    float2 sv[4];
-    unpack8x2<T>(sq[q][c], sv);
-    unpack8x2<T>(dq[q][c], dv);
-    if (din.p > 0.0f) {
-#pragma unroll
-      for (int k = 0; k < 4; ++k) dv[k] = keep2(inb[q][c], 2 * k, mul2(dv[k], isc2));
-      const uint4 w = pack8x2<T>(dv);
-      unpack8x2<T>(w, dv);
-    }
-    if (dy2) {
-      float2 d2[4];
-      unpack8x2<T>(d2q[q][c], d2);
-#pragma unroll
-      for (int k = 0; k < 4; ++k) dv[k] = add2(dv[k], d2[k]);
-    }
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      xh[k] = fma2(sv[k], rs2[q], nmr2[q]);
-      g[k] = mul2(dv[k], gm[k]);
-    }
-  };
-  const float inv = 1.0f / float(H);
-  float2 c1[RW], c2[RW];
-#pragma unroll
-  for (int q = 0; q < RW; ++q) c1[q] = c2[q] = make_float2(0.0f, 0.0f);
-#pragma unroll
-  for (int c = 0; c < NC; ++c) {
-    const int ch = lane + c * 32;
-    if (!(FULL || ch < nch)) continue;
-    float2 gm[4], pg[4], pb[4];
-    lds8x2(sg + ch * 8, gm);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) pg[k] = pb[k] = make_float2(0.0f, 0.0f);
-#pragma unroll
-    for (int q = 0; q < RW; ++q) {
-      if (!live[q]) break;
-      float2 xh[4], dv[4], g[4];
-      load_row(q, c, gm, xh, dv, g);
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        c1[q] = fma2(g[k], xh[k], c1[q]);
-        c2[q] = add2(c2[q], g[k]);
-        pg[k] = fma2(dv[k], xh[k], pg[k]);
-        pb[k] = add2(pb[k], dv[k]);
-      }
-    }
-    float4* o0 = reinterpret_cast<float4*>(prow + ch * 8);
-    float4* o1 = reinterpret_cast<float4*>(prow + H + ch * 8);
-    o0[0] = make_float4(pg[0].x, pg[0].y, pg[1].x, pg[1].y);
-    o0[1] = make_float4(pg[2].x, pg[2].y, pg[3].x, pg[3].y);
-    o1[0] = make_float4(pb[0].x, pb[0].y, pb[1].x, pb[1].y);
-    o1[1] = make_float4(pb[2].x, pb[2].y, pb[3].x, pb[3].y);
-  }
-  // o = rs * (g - c2 - xh * c1) = fma(rs, g, fma(xh, -rs*c1, -rs*c2))
-  float2 a1[RW], a0[RW];
-#pragma unroll
-  for (int q = 0; q < RW; ++q) {
-    const float m1 = warp_sum(c1[q].x + c1[q].y) * inv, m2 = warp_sum(c2[q].x + c2[q].y) * inv;
-    a1[q] = splat2(-rs2[q].x * m1);
-    a0[q] = splat2(-rs2[q].x * m2);
-  }
-  const float2 sc2 = splat2(d.scale);
-#pragma unroll
-  for (int c = 0; c < NC; ++c) {
-    const int ch = lane + c * 32;
-    if (!(FULL || ch < nch)) continue;
-    float2 gm[4], pz[4];
-    lds8x2(sg + ch * 8, gm);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) pz[k] = make_float2(0.0f, 0.0f);
-#pragma unroll
-    for (int q = 0; q < RW; ++q) {
-      if (!live[q]) break;
-      float2 xh[4], dv[4], g[4], o[4];
-      load_row(q, c, gm, xh, dv, g);
-      const int64_t i = (row0 + q) * H + ch * 8;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) o[k] = fma2(rs2[q], g[k], fma2(xh[k], a1[q], a0[q]));
-      uint4 w = pack8x2<T>(o);
-      *reinterpret_cast<uint4*>(ds_o + i) = w;
-      if (dx_o) {
-        const uint32_t bits = d.mask_in ? uint32_t(d.mask_in[i >> 3])
-                              : d.p > 0.0f ? dropout_bits8q(d, uint64_t(i) >> 3) : 0xFFu;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) o[k] = keep2(bits, 2 * k, mul2(o[k], sc2));
-        w = pack8x2<T>(o);
-        *reinterpret_cast<uint4*>(dx_o + i) = w;
-      }
-      if (nparts > 2) {  // bias grad: the outgoing gradient as stored
-        float2 f[4];
-        unpack8x2<T>(w, f);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) pz[k] = add2(pz[k], f[k]);
-      }
-    }
-    if (nparts > 2) {
-      float4* o2 = reinterpret_cast<float4*>(prow + 2 * H + ch * 8);
-      o2[0] = make_float4(pz[0].x, pz[0].y, pz[1].x, pz[1].y);
-      o2[1] = make_float4(pz[2].x, pz[2].y, pz[3].x, pz[3].y);
-    }
-  }
-  // warps whose rows are all past the end contribute zeros
-  if (!live[0]) {
-    for (int j = lane * 4; j < 3 * H; j += 128) *reinterpret_cast<float4*>(prow + j) = make_float4(0, 0, 0, 0);
-  }
-  __syncthreads();
-  for (int j = threadIdx.x * 4; j < H; j += blockDim.x * 4) {
-    for (int a = 0; a < nparts; ++a) {
-      float4 acc = make_float4(0, 0, 0, 0);
-#pragma unroll
-      for (int w = 0; w < 8; ++w) {
-        const float4 t = *reinterpret_cast<const float4*>(red + (w * 3 + a) * H + j);
-        acc.x += t.x; acc.y += t.y; acc.z += t.z; acc.w += t.w;
-      }
-      *reinterpret_cast<float4*>(ws + (int64_t(blockIdx.x) * nparts + a) * H + j) = acc;
-    }
-  }
-}
-
-// sum the per-CTA partials in fixed order -> dgamma, dbeta (f32): block = 32
-// columns x 8 warps; warp w folds partial rows w, w+8, ...; smem combines.
-// fold the per-CTA partial rows ws[k][a][j] (k < nblk, a < np) in fixed order:
-// block = 32 columns x 32 warps, warp w sums rows w, w+32, ... (loads
-// unrolled), then warp a folds the 32 warp sums of part a in warp order
-__global__ void __launch_bounds__(1024) k_ln_colsum(const float* __restrict__ ws, float* __restrict__ dg,
-                                                    float* __restrict__ db, float* __restrict__ dbias, int nblk,
-                                                    int H) {
-  TCB_PDL_ENTRY();
-  __shared__ float ra[3][32][33];
-  const int np = dbias ? 3 : 2;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int j = blockIdx.x * 32 + lane;
-  float acc[3] = {0.0f, 0.0f, 0.0f};
-  if (j < H) {
-#pragma unroll 4
-    for (int k = warp; k < nblk; k += 32) {
-#pragma unroll
-      for (int a = 0; a < 3; ++a)
-        if (a < np) acc[a] += ws[(int64_t(k) * np + a) * H + j];
-    }
-  }
-#pragma unroll
-  for (int a = 0; a < 3; ++a) ra[a][warp][lane] = acc[a];
-  __syncthreads();
-  if (warp < np && j < H) {
-    float t = 0.0f;
-#pragma unroll 8
-    for (int w = 0; w < 32; ++w) t += ra[warp][w][lane];
-    (warp == 0 ? dg : warp == 1 ? db : dbias)[j] = t;
-  }
-}
-
-static void b_layer_norm_dx(Plan& p) {
-  // mask_in: the last input holds the forward's saved keep bits
-  const bool mask_in = p.attrs.i("mask_in", 0) != 0;
-  check_arity(p, 5 + int(mask_in), 6 + int(mask_in), 3, 5);
-  const Spec& S = p.in[0];
-  const int H = int(S.dim(-1));
-  const int64_t rows = S.numel() / H;
-  require(H <= LN_MAXC * 8 * 32, "layer_norm_dx: hidden size > 2048 unsupported");
-  require(p.out[1].dtype == TCB_F32 && p.out[2].dtype == TCB_F32, "layer_norm_dx: dgamma/dbeta are f32");
-  const bool gf = p.in[1].dtype == TCB_F32;
-  const DropCfg d0 = drop_cfg(p.attrs);
-  // in_p / in_seed / in_salt: the forward layer_norm's post_dropout, applied to dy
-  DropCfg din;
-  din.p = float(p.attrs.f("in_p", 0.0));
-  din.scale = din.p > 0.0f ? 1.0f / (1.0f - din.p) : 1.0f;
-  din.seed = uint64_t(p.attrs.i("in_seed", 0));
-  din.salt = uint64_t(p.attrs.i("in_salt", 0));
-  din.thr = din.p > 0.0f ? uint32_t(std::ceil(double(din.p) * 65536.0)) : 0u;
-  const bool bias = p.attrs.i("bias_grad", 0) != 0;
-  const bool has_res = int(p.in.size()) - int(mask_in) > 5, has_dx = int(p.out.size()) - int(bias) > 3;
-  const int nin = int(p.in.size());
-  if (mask_in) require(H % 8 == 0, "layer_norm_dx: mask_in needs H % 8 == 0");
-  // the kernels read every activation-shaped input (dy, x, the residual dy2) as S's dtype
-  for (int i = 1; i < nin - int(mask_in); ++i)
-    if (p.in[i].numel() == S.numel())
-      require(p.in[i].dtype == S.dtype, "layer_norm_dx: activation-shaped inputs must share one dtype");
-  const int di = has_dx ? 4 : 3;  // index of the fused bias-grad output
-  require(int(p.out.size()) - int(bias) >= 3, "layer_norm_dx: outputs (ds, dg, db [, dx] [, dbias])");
-  if (bias) require(p.out[di].dtype == TCB_F32 && p.out[di].numel() == H, "layer_norm_dx: dbias is f32 [H]");
-  const int np = bias ? 3 : 2;
-  const int nblk = int((rows + LNB_ROWS - 1) / LNB_ROWS);
-  const size_t ws = p.ws_take(size_t(nblk) * np * H * sizeof(float));
-  const int ncs = (H + 255) / 256;
-  const size_t smem = size_t(8) * 3 * 8 * 32 * ncs * sizeof(float) + size_t(H) * sizeof(float);  // partials + gamma
-  p.nkernels = 2;
-  dispatch_float(S.dtype, [&](auto* tp) {
-   using T = std::remove_pointer_t<decltype(tp)>;
-   dispatch_nc(H, [&](auto nc) {
-    constexpr int NC = decltype(nc)::value;
-    static std::once_flag once;
-    std::call_once(once, [] {
-      constexpr int sm = 8 * 3 * 8 * 32 * NC * 4 + NC * 256 * 4;
-      TCB_CUDA(cudaFuncSetAttribute(k_ln_bwd<T, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-      if constexpr (sizeof(T) == 2) {
-        TCB_CUDA(cudaFuncSetAttribute(k_ln_bwd16<T, NC, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-        TCB_CUDA(cudaFuncSetAttribute(k_ln_bwd16<T, NC, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-        TCB_CUDA(cudaFuncSetAttribute(k_ln_bwd16<T, NC, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-        TCB_CUDA(cudaFuncSetAttribute(k_ln_bwd16<T, NC, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-      }
-    });
-    p.run = [=](const tcb_tensor* in, tcb_tensor* out, cudaStream_t s) {
-      DropCfg d = with_step(d0);
-      if (mask_in) d.mask_in = static_cast<const uint8_t*>(in[nin - 1].ptr);
-      bool vec = H % 8 == 0;
-      for (int i : {0, 4}) vec = vec && reinterpret_cast<uintptr_t>(in[i].ptr) % 16 == 0;
-      if (has_res) vec = vec && reinterpret_cast<uintptr_t>(in[5].ptr) % 16 == 0;
-      vec = vec && reinterpret_cast<uintptr_t>(out[0].ptr) % 16 == 0;
-      if (has_dx) vec = vec && reinterpret_cast<uintptr_t>(out[3].ptr) % 16 == 0;
-      const float* gfp = gf ? (const float*)in[1].ptr : nullptr;
-      const T* gtp = gf ? nullptr : (const T*)in[1].ptr;
-      const T* d2 = has_res ? (const T*)in[5].ptr : nullptr;
-      T* dxp = has_dx ? (T*)out[3].ptr : nullptr;
-      bool fast = false;
-      if constexpr (sizeof(T) == 2) fast = vec && reinterpret_cast<uintptr_t>(in[1].ptr) % 16 == 0;
-      // deferred fold: this instance's partials go to its own buffer, folded at the flush
-      float* dws = fold_deferring() ? fold_scratch(out[1].ptr, 0, size_t(nblk) * np * H * sizeof(float)) : nullptr;
-      float* wsp = dws ? dws : (float*)ws_at(ws);
-      if (din.p > 0.0f && (!fast || has_res))
-        fail(TCB_ERR_UNIMPLEMENTED, "layer_norm_dx: in_p needs the 16-bit path and a single dy");
-      if (fast) {
-        if constexpr (sizeof(T) == 2) {
-          const bool full = H == NC * 256;
-          auto kern = gf ? (full ? k_ln_bwd16<T, NC, true, true> : k_ln_bwd16<T, NC, true, false>)
-                         : (full ? k_ln_bwd16<T, NC, false, true> : k_ln_bwd16<T, NC, false, false>);
-          launch_k(kern, nblk, 256, smem, s, (const T*)in[0].ptr, (const void*)in[1].ptr, (const float*)in[2].ptr,
-                   (const float*)in[3].ptr, (const T*)in[4].ptr, d2, (T*)out[0].ptr, dxp, wsp, np, rows, H,
-                   d, with_step(din));
-        }
-      } else {
-        launch_k(k_ln_bwd<T, NC>, nblk, 256, smem, s, (const T*)in[0].ptr, gfp, gtp, (const float*)in[2].ptr,
-                 (const float*)in[3].ptr, (const T*)in[4].ptr, d2, (T*)out[0].ptr, dxp, wsp, np, rows, H, d,
-                 vec);
-      }
-      if (dws) {
-        float* dst[3] = {(float*)out[1].ptr, (float*)out[2].ptr, bias ? (float*)out[di].ptr : nullptr};
-        for (int a = 0; a < np; ++a) fold_defer(FoldJob{dws + size_t(a) * H, int64_t(np) * H, nblk, H, dst[a], 1.0f});
-        fold_op_deferred();
-        return;
-      }
-      if (!skip_folds()) launch_k(k_ln_colsum, (H + 31) / 32, 1024, 0, s, (const float*)ws_at(ws), (float*)out[1].ptr, (float*)out[2].ptr,
-               bias ? (float*)out[di].ptr : nullptr, nblk, H);
-    };
-   });
-  });
-}
-TCB_REGISTER("layer_norm_dx", b_layer_norm_dx);
 
 // ------------------------------------------------------------------ softmax
 // rows of length C; v = x*scale (causal: -inf for col > row % Sq); P = softmax;
