@@ -178,7 +178,7 @@ TCB_REGISTER("mean", b_mean);
 // 16-byte load per row), the 8 warps interleave rows, smem folds the warps and
 // the block writes one partial row; k_colsum_final adds the partials in chunk
 // order.  Deterministic; fills the machine at any R.
-constexpr int CS_ROWS = 32;  // rows per block: 4 per warp, all loads in flight at once
+constexpr int CS_ROWS = 64;  // rows per block: 8 per warp, all loads in flight at once
 
 template <typename T>
 __global__ void __launch_bounds__(256) k_colsum_partial(const T* __restrict__ x, float* __restrict__ part,
