@@ -653,9 +653,82 @@ inline const std::vector<FusionPattern>& b200_patterns() {
       {"b200.ln_dx_bias_grad", 25, "colsum", "colsum(layer_norm_dx(..).k) -> layer_norm_dx{bias_grad}.last"},
       {"b200.ce_masked_colsum", 24, "colsum", "colsum(cross_entropy(x, l).1) -> colsum(dlogits, l){ignore_index}"},
       {"b200.tied_embedding_base", 23, "add", "add(embedding_dx(ids, dy), X) -> embedding_dx(ids, dy, X)"},
+      {"b200.attention_saved_mask", 22, "attention_dx",
+       "attention_dx(qkv, attention(qkv).1, dctx) -> attention{save_mask}, attention_dx(.., attention.2)"},
       {"b200.dgrad_wgrad_pair", 20, "matmul_t", "matmul_t(dY, W) ~ matmul_t(X, dY){ta} -> matmul_pair"},
   };
   return p;
+}
+
+/// b200.attention_saved_mask: a bf16 attention forward with dropout (S <= 128,
+/// head dim 64, stored P) whose backward regenerates the keep bits instead
+/// stores them (save_mask: 4 i32 words per query row) and its attention_dx
+/// reads them -- what the hand-built bf16 step asks for directly; AutoCast
+/// output reaches it through this rewrite (the all-f32 model's attention keeps
+/// no mask).  Same Philox bits either way, so the result is bit-identical.
+inline int attach_attention_masks(LetSeq& s) {
+  std::unordered_map<const ir::Var*, size_t> def;
+  for (size_t i = 0; i < s.lets.size(); ++i) def[s.lets[i].var.get()] = i;
+  const DType bf16 = dtype_from("bf16");
+  std::map<size_t, VarPtr> mask_of;                 // attention let -> its mask var
+  std::map<size_t, std::vector<LetBinding>> after;  // get-lets inserted after an attention
+  int n = 0;
+  for (size_t j = 0; j < s.lets.size(); ++j) {
+    auto& bd = s.lets[j];
+    if (bd.value->kind != ExprKind::Call || bd.value->op != "attention_dx" || bd.value->args.size() != 3 ||
+        bd.value->call_attrs.count("save_mask") || bd.value->call_attrs.count("lse") ||
+        bd.value->args[1]->kind != ExprKind::VarRef)
+      continue;
+    auto pit = def.find(bd.value->args[1]->var.get());
+    if (pit == def.end()) continue;
+    auto& gl = s.lets[pit->second];
+    if (gl.value->kind != ExprKind::TupleGet || gl.value->index != 1 || gl.value->args[0]->kind != ExprKind::VarRef)
+      continue;
+    auto ait = def.find(gl.value->args[0]->var.get());
+    if (ait == def.end()) continue;
+    auto& al = s.lets[ait->second];
+    if (al.value->kind != ExprKind::Call || al.value->op != "attention" || al.value->call_attrs.count("lse") ||
+        al.value->args.size() != 1 || al.value->args[0]->kind != ExprKind::VarRef)
+      continue;
+    const AttrMap& at = al.value->call_attrs;
+    const int64_t S = ir::attr_int(at, "seq", 0), A = ir::attr_int(at, "heads", 0);
+    const TensorType q = al.value->args[0]->var->ty.tensor();
+    if (ir::attr_double(at, "p", 0.0) <= 0.0 || S <= 0 || S > 128 || S % 8 || A <= 0 || q.dtype != bf16 ||
+        q.shape.empty() || q.shape.back() != 3 * 64 * A)
+      continue;
+    VarPtr mv;
+    auto mit = mask_of.find(ait->second);
+    if (mit != mask_of.end()) {
+      mv = mit->second;
+    } else {
+      if (at.count("save_mask")) continue;  // already storing bits, but not visible through a get: leave it
+      AttrMap na = at;
+      na["save_mask"] = std::int64_t(1);
+      const Type nt = opreg::registry().type_rel_of("attention")({al.value->args[0]->var->ty}, na);
+      al.value->call_attrs = na;
+      al.value->ty = nt;
+      al.var->ty = nt;
+      const int k = int(nt.tuple().fields.size()) - 1;
+      mv = ir::make_var(al.var->id + "_mask", Type(nt.tuple().fields[size_t(k)]));
+      auto g = ir::tuple_get(ir::var_ref(al.var), k);
+      g->ty = mv->ty;
+      after[ait->second].push_back({mv, g});
+      mask_of[ait->second] = mv;
+    }
+    bd.value->args.push_back(ir::var_ref(mv));
+    bd.value->call_attrs["save_mask"] = std::int64_t(1);
+    ++n;
+  }
+  if (!n) return 0;
+  LetSeq out;
+  out.ret = s.ret;
+  for (size_t k = 0; k < s.lets.size(); ++k) {
+    out.lets.push_back(s.lets[k]);
+    auto it = after.find(k);
+    if (it != after.end()) out.lets.insert(out.lets.end(), it->second.begin(), it->second.end());
+  }
+  s = std::move(out);
+  return n;
 }
 
 /// Horizontal fusion (SPEC.md:533-540 applied to GEMMs): a weight-gradient
@@ -985,6 +1058,8 @@ inline FusionStats fuse(LetSeq& s, bool patterns = true, const std::set<std::str
     out = std::move(keep);
   }
   s = std::move(out);
+  if (patterns && on("b200.attention_saved_mask"))
+    st.by_pattern["b200.attention_saved_mask"] = attach_attention_masks(s);
   if (patterns && on("b200.dgrad_wgrad_pair")) st.pairs = fuse_gemm_pairs(s);
   st.by_pattern["b200.dgrad_wgrad_pair"] = st.pairs;
   return st;

@@ -68,3 +68,27 @@ def test_pattern_fusion_strictly_cuts_instructions():
     def calls(c):
         return sum(1 for l in graph_text(c, "ir").splitlines() if "= b200." in l and ".view(" not in l)
     assert calls(ModelConfig.bert_base(B=2)) < calls(ModelConfig.bert_base(B=2, fuse=0))
+
+
+def test_attention_saved_mask_on_the_autocast_graph():
+    """b200.attention_saved_mask: the AutoCast'd all-f32 BERT step gets the
+    hand-built graph's stored attention keep bits (every attention stores them,
+    every attention_dx reads them), and the interpreter of that graph equals
+    the one with the pattern off bit for bit (same Philox bits)."""
+    kw = dict(kind="bert", L=2, H=128, A=2, F=256, V=128, S=16, B=2, dtype="f32", opt="adam", lr=1e-3, p=0.1)
+    c1 = ModelConfig(**kw)
+    c1.extra["autocast"] = "b200+fold+fuse"
+    ir = graph_text(c1, "ir")
+    att = [l for l in ir.splitlines() if "= b200.attention(" in l]
+    dx = [l for l in ir.splitlines() if "= b200.attention_dx(" in l]
+    assert att and all("save_mask=1" in l for l in att) and all("save_mask=1" in l for l in dx)
+    c0 = ModelConfig(**kw, disable_patterns="b200.attention_saved_mask")
+    c0.extra["autocast"] = "b200+fold+fuse"
+    assert "save_mask=1" not in "".join(l for l in graph_text(c0, "ir").splitlines() if "attention" in l)
+    ids, labels = synthetic_batch(c1)
+    o1 = Interp(c1.cfg_string(model_only=True) + ";autocast=b200+fold+fuse")
+    o0 = Interp(c0.cfg_string(model_only=True) + ";autocast=b200+fold+fuse")
+    for _ in range(2):
+        l1, l0 = o1.step(ids, labels), o0.step(ids, labels)
+        assert np.float32(l1).tobytes() == np.float32(l0).tobytes()
+    assert o1.grad().tobytes() == o0.grad().tobytes()
