@@ -80,6 +80,10 @@ inline PrecisionPolicy b200_policy() {
   for (const char* o : {"layer_norm", "add_layer_norm", "layer_norm_dx", "softmax", "softmax_dx", "cross_entropy",
                         "colsum", "embedding_dx"})
     p.by_op[o] = Prec::F32Math;
+  // gathers from the bf16 compute copy of the tables (like the hand-built
+  // step's embedding_sum): the table cast is a parameter cast, folded into
+  // the optimizer's bf16 copy by +fold
+  for (const char* o : {"embedding", "embedding_sum"}) p.by_op[o] = Prec::Low;
   return p;
 }
 

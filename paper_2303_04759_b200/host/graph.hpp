@@ -655,6 +655,7 @@ inline const std::vector<FusionPattern>& b200_patterns() {
       {"b200.tied_embedding_base", 23, "add", "add(embedding_dx(ids, dy), X) -> embedding_dx(ids, dy, X)"},
       {"b200.attention_saved_mask", 22, "attention_dx",
        "attention_dx(qkv, attention(qkv).1, dctx) -> attention{save_mask}, attention_dx(.., attention.2)"},
+      {"b200.embedding_sum", 21, "add", "add(embedding(i, T) | embedding_sum(..), embedding(j, U)) -> embedding_sum(.., j, .., U)"},
       {"b200.dgrad_wgrad_pair", 20, "matmul_t", "matmul_t(dY, W) ~ matmul_t(X, dY){ta} -> matmul_pair"},
   };
   return p;
@@ -854,6 +855,50 @@ inline FusionStats fuse(LetSeq& s, bool patterns = true, const std::set<std::str
     auto& b = s.lets[i];
     if (b.value->kind != ExprKind::Call) continue;
     const std::string op = b.value->op;
+    // 0. add(embedding(i, T) | embedding_sum(ids.., tables..), embedding(j, U))
+    //    -> embedding_sum(ids.., j, tables.., U): the gathers and the add chain
+    //    in one kernel, each sum rounded to the tables' 16-bit dtype exactly as
+    //    the chain rounds it (IEEE addition commutes, so either add operand
+    //    order gives the same bits)
+    if (op == "add" && on("b200.embedding_sum") && b.value->args.size() == 2) {
+      auto a0 = arg_var(b.value, 0), a1 = arg_var(b.value, 1);
+      auto* p0 = producer(a0);
+      auto* p1 = producer(a1);
+      auto is_emb = [](LetBinding* p) { return p && p->value->op == "embedding" && p->value->args.size() == 2; };
+      auto is_sum = [](LetBinding* p) { return p && p->value->op == "embedding_sum"; };
+      LetBinding *acc = nullptr, *one = nullptr;
+      VarPtr va, vo;
+      if ((is_emb(p0) || is_sum(p0)) && is_emb(p1)) acc = p0, one = p1, va = a0, vo = a1;
+      else if (is_emb(p0) && is_sum(p1)) acc = p1, one = p0, va = a1, vo = a0;
+      const DType ty = b.value->ty.tensor().dtype;
+      if (acc && single(va) && single(vo) && (ty == dtype_from("bf16") || ty == dtype_from("f16")) &&
+          acc->value->ty.tensor().dtype == ty && one->value->ty.tensor().dtype == ty &&
+          !acc->value->call_attrs.size() && !one->value->call_attrs.size()) {
+        std::vector<ExprPtr> ids, tabs;
+        if (is_sum(acc)) {
+          const size_t n = acc->value->args.size() / 2;
+          for (size_t k = 0; k < n; ++k) ids.push_back(acc->value->args[k]), tabs.push_back(acc->value->args[n + k]);
+        } else {
+          ids.push_back(acc->value->args[0]);
+          tabs.push_back(acc->value->args[1]);
+        }
+        ids.push_back(one->value->args[0]);
+        tabs.push_back(one->value->args[1]);
+        bool same = true;
+        for (auto& t : tabs) same = same && t->ty.tensor().dtype == ty;
+        if (same) {
+          std::vector<ExprPtr> xs = ids;
+          xs.insert(xs.end(), tabs.begin(), tabs.end());
+          auto call = ir::call("embedding_sum", std::move(xs), AttrMap{});
+          call->ty = b.value->ty;
+          b.value = call;
+          removed.insert(def[va.get()]);
+          removed.insert(def[vo.get()]);
+          ++st.by_pattern["b200.embedding_sum"];
+          continue;
+        }
+      }
+    }
     // 1. gelu_dx(u, matmul_t(a, b)) -> matmul_dact(a, b, u)   (dact in the dgrad epilogue)
     if (op == "gelu_dx" && on("b200.dgrad_gelu_epilogue")) {
       auto src = arg_var(b.value, 1);

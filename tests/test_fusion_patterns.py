@@ -92,3 +92,25 @@ def test_attention_saved_mask_on_the_autocast_graph():
         l1, l0 = o1.step(ids, labels), o0.step(ids, labels)
         assert np.float32(l1).tobytes() == np.float32(l0).tobytes()
     assert o1.grad().tobytes() == o0.grad().tobytes()
+
+
+def test_embedding_sum_pattern_on_the_autocast_graph():
+    """b200.embedding_sum: under the b200 policy the AutoCast'd BERT front is
+    the hand-built one (one embedding_sum gather-and-add over the bf16 tables,
+    LayerNorm with its output dropout); the interpreter equals the graph with
+    the pattern off bit for bit (the kernel rounds each add like the chain)."""
+    kw = dict(kind="bert", L=1, H=128, A=2, F=256, V=128, S=16, B=2, dtype="f32", opt="adam", lr=1e-3, p=0.1)
+    c1 = ModelConfig(**kw)
+    c1.extra["autocast"] = "b200+fold+fuse"
+    ir = graph_text(c1, "ir")
+    assert ir.count("= b200.embedding_sum(") == 1 and "= b200.embedding(" not in ir
+    c0 = ModelConfig(**kw, disable_patterns="b200.embedding_sum")
+    c0.extra["autocast"] = "b200+fold+fuse"
+    assert graph_text(c0, "ir").count("= b200.embedding(") == 3
+    ids, labels = synthetic_batch(c1)
+    o1 = Interp(c1.cfg_string(model_only=True) + ";autocast=b200+fold+fuse")
+    o0 = Interp(c0.cfg_string(model_only=True) + ";autocast=b200+fold+fuse")
+    for _ in range(2):
+        l1, l0 = o1.step(ids, labels), o0.step(ids, labels)
+        assert np.float32(l1).tobytes() == np.float32(l0).tobytes()
+    assert o1.grad().tobytes() == o0.grad().tobytes()
