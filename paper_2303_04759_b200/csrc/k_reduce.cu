@@ -204,12 +204,25 @@ __global__ void __launch_bounds__(256) k_colsum_partial(const T* __restrict__ x,
         q[i] = (r < r1 && !(lab && lab[r] == ign)) ? *reinterpret_cast<const uint4*>(x + r * C + c0)
                                                    : make_uint4(0, 0, 0, 0);
       }
+      // packed: two columns per f32x2 add (same per-column order, same bits)
+      float2 a2[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) a2[k] = make_float2(0.0f, 0.0f);
 #pragma unroll
       for (int i = 0; i < RPW; ++i) {
-        const T* h = reinterpret_cast<const T*>(&q[i]);
+        const uint32_t w[4] = {q[i].x, q[i].y, q[i].z, q[i].w};
 #pragma unroll
-        for (int k = 0; k < 8; ++k) acc[k] += to_f(h[k]);
+        for (int k = 0; k < 4; ++k) {
+          float2 f;
+          if constexpr (std::is_same<T, __nv_bfloat16>::value)
+            f = make_float2(__uint_as_float(w[k] << 16), __uint_as_float(w[k] & 0xffff0000u));
+          else
+            f = __half22float2(*reinterpret_cast<const __half2*>(&w[k]));
+          a2[k] = add2(a2[k], f);
+        }
       }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) acc[2 * k] = a2[k].x, acc[2 * k + 1] = a2[k].y;
     } else {
       for (int64_t r = r0 + warp; r < r1; r += 8) {
         if (lab && lab[r] == ign) continue;
