@@ -851,28 +851,62 @@ constexpr int EMB_CHUNK = 128;  // rows per partial sum of a long segment
 // ascending t into part[chunk_start]) and folded here in chunk order onto
 // base: deterministic; for segments <= EMB_CHUNK rows k_embed_accum writes the
 // oracle's exact sequential sum directly.
+// The block's sorted positions (pos = blockIdx.x + k * gridDim.x) are
+// screened 256 at a time by all threads at once (one round of id / segment
+// loads instead of a dependent chain per position); the positions that have
+// work are listed in shared memory and then processed column-parallel.
+// mode 0 (accumulate): chunk starts (pos - head) % EMB_CHUNK == 0;
+// mode 1 (fold): heads of segments longer than EMB_CHUNK.
+template <int MODE>
+__device__ __forceinline__ int embed_screen(const int32_t* __restrict__ sid, const int32_t* __restrict__ start,
+                                            const int32_t* __restrict__ send, int64_t T, int64_t k0,
+                                            int64_t* list) {
+  __shared__ int n;
+  if (threadIdx.x == 0) n = 0;
+  __syncthreads();
+  const int64_t pos = int64_t(blockIdx.x) + (k0 + threadIdx.x) * gridDim.x;
+  if (pos < T) {
+    const int32_t id = sid[pos];
+    const int64_t head = start[id];
+    const int32_t len = send[id] - int32_t(head);
+    const bool work = MODE == 0 ? (pos - head) % EMB_CHUNK == 0 : (pos == head && len > EMB_CHUNK);
+    if (work) list[atomicAdd(&n, 1)] = pos;
+  }
+  __syncthreads();
+  const int m = n;  // list order is arbitrary: every listed position writes its own rows
+  __syncthreads();
+  return m;
+}
+
 __global__ void __launch_bounds__(256) k_embed_fold(const int32_t* __restrict__ sid,
                                                     const int32_t* __restrict__ start,
                                                     const int32_t* __restrict__ end,
                                                     const float* __restrict__ part, float* __restrict__ out,
                                                     int64_t T, int64_t H) {
   TCB_PDL_ENTRY();
+  __shared__ int64_t list[256];
   const int64_t j = int64_t(blockIdx.y) * blockDim.x + threadIdx.x;
-  // grid-stride over sorted positions: only heads of long segments do work
-  for (int64_t pos = blockIdx.x; pos < T; pos += gridDim.x) {
-    const int32_t id = sid[pos];
-    const int32_t head = start[id], len = end[id] - head;
-    if (pos != head || len <= EMB_CHUNK || j >= H) continue;
-    float acc = out[int64_t(id) * H + j];
-    for (int64_t c = pos; c < pos + len; c += EMB_CHUNK) acc = __fadd_rn(acc, part[c * H + j]);
-    out[int64_t(id) * H + j] = acc;
+  const int64_t per = (T - blockIdx.x + gridDim.x - 1) / gridDim.x;  // positions of this block
+  for (int64_t k0 = 0; k0 < per; k0 += 256) {
+    const int m = embed_screen<1>(sid, start, end, T, k0, list);
+    for (int w = 0; w < m; ++w) {
+      const int64_t pos = list[w];
+      if (j >= H) continue;
+      const int32_t id = sid[pos];
+      const int32_t len = end[id] - int32_t(pos);
+      float acc = out[int64_t(id) * H + j];
+      for (int64_t c = pos; c < pos + len; c += EMB_CHUNK) acc = __fadd_rn(acc, part[c * H + j]);
+      out[int64_t(id) * H + j] = acc;
+    }
+    __syncthreads();  // the list is rewritten by the next screen
   }
 }
 
-// block (pos, column tile): if sorted position `pos` starts a segment of equal
-// ids, each thread accumulates one column over the whole segment in ascending t
-// (loads batched 4 deep; the adds keep the oracle's order).  Column-parallel,
-// so one id covering every token (token-type ids) is 256x wider than a warp.
+// block (positions, column tile): for each sorted position `pos` that starts a
+// chunk of a segment of equal ids, each thread accumulates one column over the
+// chunk in ascending t (loads batched 16 deep; the adds keep the oracle's
+// order).  Column-parallel, so one id covering every token (token-type ids) is
+// 256x wider than a warp.
 template <typename TD>
 __global__ void __launch_bounds__(256) k_embed_accum(const int32_t* __restrict__ sid,
                                                      const int32_t* __restrict__ sorted,
@@ -881,36 +915,40 @@ __global__ void __launch_bounds__(256) k_embed_accum(const int32_t* __restrict__
                                                      const TD* __restrict__ dy, float* __restrict__ out,
                                                      float* __restrict__ part, int64_t T, int64_t H) {
   TCB_PDL_ENTRY();
+  __shared__ int64_t list[256];
   const int64_t j = int64_t(blockIdx.y) * blockDim.x + threadIdx.x;
-  // grid-stride over sorted positions (most are not chunk starts and skip at once)
-  for (int64_t pos = blockIdx.x; pos < T; pos += gridDim.x) {
-    const int32_t id = sid[pos];
-    const int64_t head = start[id];
-    if ((pos - head) % EMB_CHUNK || j >= H) continue;  // not a chunk start
-    const int32_t len = send[id] - int32_t(head);
-    const bool single = len <= EMB_CHUNK;
-    const int64_t end = (head + len) < (pos + EMB_CHUNK) ? (head + len) : (pos + EMB_CHUNK);
-    float acc = single ? out[int64_t(id) * H + j] : 0.0f;
-    int64_t q = pos;
-    // 16 row loads in flight per round (long segments are latency chains);
-    // the adds stay in ascending t
-    for (; q + 16 <= end; q += 16) {
-      float v[16];
+  const int64_t per = (T - blockIdx.x + gridDim.x - 1) / gridDim.x;  // positions of this block
+  for (int64_t k0 = 0; k0 < per; k0 += 256) {
+    const int m = embed_screen<0>(sid, start, send, T, k0, list);
+    for (int w = 0; w < m; ++w) {
+      const int64_t pos = list[w];
+      if (j >= H) continue;
+      const int32_t id = sid[pos];
+      const int64_t head = start[id];
+      const int32_t len = send[id] - int32_t(head);
+      const bool single = len <= EMB_CHUNK;
+      const int64_t end = (head + len) < (pos + EMB_CHUNK) ? (head + len) : (pos + EMB_CHUNK);
+      float acc = single ? out[int64_t(id) * H + j] : 0.0f;
+      int64_t q = pos;
+      for (; q + 16 <= end; q += 16) {
+        float v[16];
 #pragma unroll
-      for (int k = 0; k < 16; ++k) v[k] = to_f(dy[int64_t(sorted[q + k]) * H + j]);
+        for (int k = 0; k < 16; ++k) v[k] = to_f(dy[int64_t(sorted[q + k]) * H + j]);
 #pragma unroll
-      for (int k = 0; k < 16; ++k) acc = __fadd_rn(acc, v[k]);
+        for (int k = 0; k < 16; ++k) acc = __fadd_rn(acc, v[k]);
+      }
+      for (; q + 4 <= end; q += 4) {
+        float v0 = to_f(dy[int64_t(sorted[q]) * H + j]);
+        float v1 = to_f(dy[int64_t(sorted[q + 1]) * H + j]);
+        float v2 = to_f(dy[int64_t(sorted[q + 2]) * H + j]);
+        float v3 = to_f(dy[int64_t(sorted[q + 3]) * H + j]);
+        acc = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(acc, v0), v1), v2), v3);
+      }
+      for (; q < end; ++q) acc = __fadd_rn(acc, to_f(dy[int64_t(sorted[q]) * H + j]));
+      if (single) out[int64_t(id) * H + j] = acc;
+      else part[pos * H + j] = acc;
     }
-    for (; q + 4 <= end; q += 4) {
-      float v0 = to_f(dy[int64_t(sorted[q]) * H + j]);
-      float v1 = to_f(dy[int64_t(sorted[q + 1]) * H + j]);
-      float v2 = to_f(dy[int64_t(sorted[q + 2]) * H + j]);
-      float v3 = to_f(dy[int64_t(sorted[q + 3]) * H + j]);
-      acc = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(acc, v0), v1), v2), v3);
-    }
-    for (; q < end; ++q) acc = __fadd_rn(acc, to_f(dy[int64_t(sorted[q]) * H + j]));
-    if (single) out[int64_t(id) * H + j] = acc;
-    else part[pos * H + j] = acc;
+    __syncthreads();  // the list is rewritten by the next screen
   }
 }
 
