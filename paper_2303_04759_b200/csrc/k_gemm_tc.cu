@@ -31,8 +31,14 @@ namespace tcb {
 
 constexpr int TC_BM = 128;  // accumulator rows per CTA
 constexpr int TC_BK = 64;   // 64 bf16 = 128 B = one SWIZZLE_128B atom row
-constexpr int TC_EPI_WARPS = 16;                      // 4 per TMEM lane quarter
-constexpr int TC_THREADS = 128 + 32 * TC_EPI_WARPS;  // warps 0-3: TMA, MMA, TMEM, spare
+// epilogue warps per CTA: 16 (4 per TMEM lane quarter) for the arithmetic-heavy
+// epilogues (GELU / act'(aux)), 8 for plain / bias / f32 stores -- there the
+// extra registers per thread (a 768- instead of a 640-thread CTA budget) beat
+// the latency hiding of more warps (tools/probe_gemm.py: plain 23.0 -> 21.3 us,
+// decoder 178 -> 169 us; GELU' and act'(aux) slower with 8)
+constexpr int TC_EPI_WARPS = 16;                      // the default (heavy) count
+template <int EPW>
+constexpr int tc_threads() { return 128 + 32 * EPW; }  // warps 0-3: TMA, MMA, TMEM, spare
 constexpr int TC_EW = 16;                             // epilogue chunk width (columns)
 constexpr int TC_SLOT = 32 * TC_EW * 4;               // per-warp output slot: f32 box or (y, u) 16-bit boxes
 constexpr int TC_AUX_SLOT = 32 * TC_EW * 2;           // per-warp act'(aux) slot (16-bit)
@@ -42,7 +48,7 @@ constexpr int TC_AUX_RING = 3;                        // aux boxes in flight per
 template <bool AUX>
 constexpr int out_ring() { return AUX ? 2 : 1; }
 
-template <int BN, int CG, bool AUX>
+template <int BN, int CG, bool AUX, int EPW = TC_EPI_WARPS>
 struct TcCfg {
   static constexpr int B_ROWS = BN / CG;  // B rows (N) staged by each CTA
   // MN-major B arrives in 64-column boxes; a 96-row half (BN=192 pair) takes two,
@@ -52,8 +58,8 @@ struct TcCfg {
   static constexpr int B_BYTES = B_CHUNKS * 64 * TC_BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int EPI_BYTES =
-      TC_EPI_WARPS * out_ring<AUX>() * TC_SLOT + (AUX ? TC_EPI_WARPS * TC_AUX_RING * TC_AUX_SLOT : 0);
-  static constexpr int BIAS_BYTES = TC_EPI_WARPS * ((BN / TC_EW + TC_EPI_WARPS / 4 - 1) / (TC_EPI_WARPS / 4)) * TC_EW * 4;
+      EPW * out_ring<AUX>() * TC_SLOT + (AUX ? EPW * TC_AUX_RING * TC_AUX_SLOT : 0);
+  static constexpr int BIAS_BYTES = EPW * ((BN / TC_EW + EPW / 4 - 1) / (EPW / 4)) * TC_EW * 4;
   static constexpr int BAR_BYTES = 1024;
   static constexpr int BUDGET = 227 * 1024 - 1024 - BAR_BYTES - EPI_BYTES - BIAS_BYTES;
   static constexpr int STAGES = BUDGET / STAGE_BYTES > 8 ? 8 : BUDGET / STAGE_BYTES;
@@ -352,12 +358,12 @@ struct EpiMaps {
   CUtensorMap c, u, aux;
 };
 
-template <int BN, int CG, bool AUX>
-__global__ void __launch_bounds__(TC_THREADS, 1)
+template <int BN, int CG, bool AUX, int EPW>
+__global__ void __launch_bounds__(tc_threads<EPW>(), 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmB0,
               const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmB1,
               const __grid_constant__ EpiMaps EM0, const __grid_constant__ EpiMaps EM1, const TcParams P) {
-  using C = TcCfg<BN, CG, AUX>;
+  using C = TcCfg<BN, CG, AUX, EPW>;
   constexpr int W = TC_EW;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -365,15 +371,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   uint8_t* sB = smem + C::STAGES * C::A_BYTES;
   uint8_t* sEpi = smem + C::STAGES * C::STAGE_BYTES;        // epilogue warps x 2 output slots
   constexpr int OUT_RING = out_ring<AUX>();
-  uint8_t* sAux = sEpi + TC_EPI_WARPS * OUT_RING * TC_SLOT;  // epilogue warps x aux ring (AUX)
-  float* sBias = reinterpret_cast<float*>(sAux + (AUX ? TC_EPI_WARPS * TC_AUX_RING * TC_AUX_SLOT : 0));
+  uint8_t* sAux = sEpi + EPW * OUT_RING * TC_SLOT;  // epilogue warps x aux ring (AUX)
+  float* sBias = reinterpret_cast<float*>(sAux + (AUX ? EPW * TC_AUX_RING * TC_AUX_SLOT : 0));
   uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sBias) + C::BIAS_BYTES);
   uint64_t* full = bars;
   uint64_t* empty = bars + C::STAGES;
   uint64_t* tfull = bars + 2 * C::STAGES;
   uint64_t* tempty = tfull + 2;
   uint64_t* abar = tempty + 2;  // TC_AUX_RING per epilogue warp
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(abar + TC_AUX_RING * TC_EPI_WARPS);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(abar + TC_AUX_RING * EPW);
 
   // the warp index broadcast from lane 0: the compiler then treats it (and the
   // tile coordinates derived from it) as warp-uniform, so TMA / tcgen05 issue
@@ -403,9 +409,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], CG * TC_EPI_WARPS);
+      mbar_init(&tempty[s], CG * EPW);
     }
-    for (int s = 0; s < TC_AUX_RING * TC_EPI_WARPS; ++s) mbar_init(&abar[s], 1);
+    for (int s = 0; s < TC_AUX_RING * EPW; ++s) mbar_init(&abar[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
@@ -534,11 +540,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       }
     }
   } else if (warp >= 4) {
-    // ===================== epilogue (TC_EPI_WARPS warps, both CTAs) =====================
+    // ===================== epilogue (EPW warps, both CTAs) =====================
     // warp w may only touch TMEM lanes 32*(w%4)..+31 (its 32 rows); the warps
     // sharing a lane quarter take every TC_EPI_SPLIT-th W-column chunk
     constexpr int NCH = BN / W;
-    constexpr int SPLIT = TC_EPI_WARPS / 4;
+    constexpr int SPLIT = EPW / 4;
     constexpr int CPW = (NCH + SPLIT - 1) / SPLIT;  // chunks per warp per tile (max)
     const int ew = warp - 4;
     const int q = warp & 3;
@@ -909,12 +915,12 @@ static void fill_prob(const GemmArgs& g, TcProb& P, CUtensorMap& ta, CUtensorMap
 }
 
 // launch n (1 or 2) problems with one tile shape in a single persistent grid
-template <int BN, int CG, bool AUX>
+template <int BN, int CG, bool AUX, int EPW>
 static void launch_cfg(const GemmArgs* gs, int n, cudaStream_t s) {
-  using C = TcCfg<BN, CG, AUX>;
+  using C = TcCfg<BN, CG, AUX, EPW>;
   static std::once_flag once;
   std::call_once(once, [] {
-    TCB_CUDA(cudaFuncSetAttribute(k_gemm_tc<BN, CG, AUX>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    TCB_CUDA(cudaFuncSetAttribute(k_gemm_tc<BN, CG, AUX, EPW>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
   });
   TcParams P{};
   P.nprob = n;
@@ -935,7 +941,7 @@ static void launch_cfg(const GemmArgs* gs, int n, cudaStream_t s) {
   grid = (grid / CG) * CG;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(unsigned(grid));
-  cfg.blockDim = dim3(TC_THREADS);
+  cfg.blockDim = dim3(tc_threads<EPW>());
   cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = s;
   cudaLaunchAttribute attr[2];
@@ -945,7 +951,7 @@ static void launch_cfg(const GemmArgs* gs, int n, cudaStream_t s) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1 + pdl_attr(&attr[1]);
-  TCB_CUDA(cudaLaunchKernelEx(&cfg, k_gemm_tc<BN, CG, AUX>, ta[0], tb[0], ta[1], tb[1], em[0], em[1], P));
+  TCB_CUDA(cudaLaunchKernelEx(&cfg, k_gemm_tc<BN, CG, AUX, EPW>, ta[0], tb[0], ta[1], tb[1], em[0], em[1], P));
 }
 
 // Tile configuration by a wave-quantised cost model (calibrated on the
@@ -999,12 +1005,17 @@ void gemm_prepare(GemmArgs& g, bool exact, GemmWs& keep) {
 }
 
 static void dispatch_tc(const GemmArgs* gs, int n, const TcChoice& c, cudaStream_t s) {
-  bool aux = false;
-  for (int i = 0; i < n; ++i) aux = aux || gs[i].dact != ACT_NONE;
+  bool aux = false, light = true;
+  for (int i = 0; i < n; ++i) {
+    aux = aux || gs[i].dact != ACT_NONE;
+    // plain / bias / f32 stores: no activation, no second output
+    light = light && gs[i].act == ACT_NONE && !gs[i].aux_out;
+  }
 #define TC_CASE(BN_, CG_)                                  \
   if (c.bn == BN_ && c.cg == CG_) {                        \
-    if (aux) launch_cfg<BN_, CG_, true>(gs, n, s);         \
-    else launch_cfg<BN_, CG_, false>(gs, n, s);            \
+    if (aux) launch_cfg<BN_, CG_, true, 16>(gs, n, s);     \
+    else if (light) launch_cfg<BN_, CG_, false, 8>(gs, n, s); \
+    else launch_cfg<BN_, CG_, false, 16>(gs, n, s);        \
     return;                                                \
   }
   TC_CASE(256, 2)
