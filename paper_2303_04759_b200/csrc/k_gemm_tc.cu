@@ -31,12 +31,21 @@ namespace tcb {
 
 constexpr int TC_BM = 128;  // accumulator rows per CTA
 constexpr int TC_BK = 64;   // 64 bf16 = 128 B = one SWIZZLE_128B atom row
-// epilogue warps per CTA: 16 (4 per TMEM lane quarter) for the arithmetic-heavy
-// epilogues (GELU / act'(aux)), 8 for plain / bias / f32 stores -- there the
-// extra registers per thread (a 768- instead of a 640-thread CTA budget) beat
-// the latency hiding of more warps (tools/probe_gemm.py: plain 23.0 -> 21.3 us,
-// decoder 178 -> 169 us; GELU' and act'(aux) slower with 8)
-constexpr int TC_EPI_WARPS = 16;                      // the default (heavy) count
+// epilogue warps per CTA by launch class (measured, tools/probe_gemm.py and
+// alternating step A/Bs): 8 for plain / bias / f32 stores (fewer, fatter
+// threads: plain 23.0 -> 21.3 us, decoder 178 -> 169 us), 12 for the GELU
+// forward epilogues (27.7 vs 28.3 us at 16), 16 (4 per TMEM lane quarter) for
+// act'(aux) (27.7 us; 31.2 at 12, 35.3 at 8)
+constexpr int TC_EPI_WARPS = 16;                      // the default (heaviest) count
+#ifndef TC_EPW_LIGHT
+#define TC_EPW_LIGHT 8
+#endif
+#ifndef TC_EPW_HEAVY
+#define TC_EPW_HEAVY 12
+#endif
+#ifndef TC_EPW_AUX
+#define TC_EPW_AUX 16
+#endif
 template <int EPW>
 constexpr int tc_threads() { return 128 + 32 * EPW; }  // warps 0-3: TMA, MMA, TMEM, spare
 constexpr int TC_EW = 16;                             // epilogue chunk width (columns)
@@ -1013,9 +1022,9 @@ static void dispatch_tc(const GemmArgs* gs, int n, const TcChoice& c, cudaStream
   }
 #define TC_CASE(BN_, CG_)                                  \
   if (c.bn == BN_ && c.cg == CG_) {                        \
-    if (aux) launch_cfg<BN_, CG_, true, 16>(gs, n, s);     \
-    else if (light) launch_cfg<BN_, CG_, false, 8>(gs, n, s); \
-    else launch_cfg<BN_, CG_, false, 16>(gs, n, s);        \
+    if (aux) launch_cfg<BN_, CG_, true, TC_EPW_AUX>(gs, n, s);     \
+    else if (light) launch_cfg<BN_, CG_, false, TC_EPW_LIGHT>(gs, n, s); \
+    else launch_cfg<BN_, CG_, false, TC_EPW_HEAVY>(gs, n, s);        \
     return;                                                \
   }
   TC_CASE(256, 2)
