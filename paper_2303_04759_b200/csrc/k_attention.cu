@@ -231,8 +231,9 @@ __global__ void __launch_bounds__(AT_FWD_THREADS) k_attn_fwd(const __grid_consta
         a.lse_out[uint64_t(z) * a.S + row] = (mx + __log2f(tot)) * 0.6931471805599453f;
       }
     } else if (tid == 0) {
-      tma_store_4d(&m_probs, sP, 0, 0, z, 0);
-      if (a.S > 64) tma_store_4d(&m_probs, sP + AT_TILE, 64, 0, z, 0);
+      // P is read only by this layer's backward: evict-first in L2
+      tma_store_4d_evict_first(&m_probs, sP, 0, 0, z, 0);
+      if (a.S > 64) tma_store_4d_evict_first(&m_probs, sP + AT_TILE, 64, 0, z, 0);
       bulk_commit();
     }
     uint8_t* sA = sP;

@@ -744,7 +744,7 @@ __global__ void __launch_bounds__(tc_threads<EPW>(), 1)
         if constexpr (K == EK_GELU_SAVE) {
           if (lane == 0) {
             tma_store_4d(mc, slot, sx, sy, sz2, sz1);
-            tma_store_4d(mu, slot + TC_SLOT / 2, sx, sy, sz2, sz1);
+            tma_store_4d_evict_first(mu, slot + TC_SLOT / 2, sx, sy, sz2, sz1);  // GELU'(u): read in the backward
             bulk_commit();
           }
         } else if (lane == 0) {
