@@ -52,6 +52,9 @@ constexpr int TC_EW = 16;                             // epilogue chunk width (c
 constexpr int TC_SLOT = 32 * TC_EW * 4;               // per-warp output slot: f32 box or (y, u) 16-bit boxes
 constexpr int TC_AUX_SLOT = 32 * TC_EW * 2;           // per-warp act'(aux) slot (16-bit)
 constexpr int TC_AUX_RING = 3;                        // aux boxes in flight per warp (2 chunks ahead)
+#ifndef TC_AUX_DIRECT
+#define TC_AUX_DIRECT 1  // act'(aux) read straight from global; 0: the older per-warp TMA box ring
+#endif
 // output staging slots per warp: one (the operand ring gets the smem: +1 stage);
 // the act'(aux) kernels, epilogue-bound, keep two so stores overlap
 template <bool AUX>
@@ -67,7 +70,7 @@ struct TcCfg {
   static constexpr int B_BYTES = B_CHUNKS * 64 * TC_BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int EPI_BYTES =
-      EPW * out_ring<AUX>() * TC_SLOT + (AUX ? EPW * TC_AUX_RING * TC_AUX_SLOT : 0);
+      EPW * out_ring<AUX>() * TC_SLOT + ((AUX && !TC_AUX_DIRECT) ? EPW * TC_AUX_RING * TC_AUX_SLOT : 0);
   static constexpr int BIAS_BYTES = EPW * ((BN / TC_EW + EPW / 4 - 1) / (EPW / 4)) * TC_EW * 4;
   static constexpr int BAR_BYTES = 1024;
   static constexpr int BUDGET = 227 * 1024 - 1024 - BAR_BYTES - EPI_BYTES - BIAS_BYTES;
@@ -381,7 +384,7 @@ __global__ void __launch_bounds__(tc_threads<EPW>(), 1)
   uint8_t* sEpi = smem + C::STAGES * C::STAGE_BYTES;        // epilogue warps x 2 output slots
   constexpr int OUT_RING = out_ring<AUX>();
   uint8_t* sAux = sEpi + EPW * OUT_RING * TC_SLOT;  // epilogue warps x aux ring (AUX)
-  float* sBias = reinterpret_cast<float*>(sAux + (AUX ? EPW * TC_AUX_RING * TC_AUX_SLOT : 0));
+  float* sBias = reinterpret_cast<float*>(sAux + ((AUX && !TC_AUX_DIRECT) ? EPW * TC_AUX_RING * TC_AUX_SLOT : 0));
   uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sBias) + C::BIAS_BYTES);
   uint64_t* full = bars;
   uint64_t* empty = bars + C::STAGES;
@@ -607,8 +610,29 @@ __global__ void __launch_bounds__(tc_threads<EPW>(), 1)
         return;
       }
     };
-    if (AUX)
+    if (AUX && !TC_AUX_DIRECT)
       for (int k = 0; k < TC_AUX_RING - 1; ++k) issue_next_aux();
+    // direct act'(aux) loads (TC_AUX_DIRECT): each lane reads its row's 16
+    // 16-bit values (2 x 16 B, read-only path) -- no TMA ring / mbarrier / smem
+    auto aux_ld = [&](const TcProb& Qa, int64_t mm, int64_t cof, int64_t nn, uint4& x0, uint4& x1) {
+      if (mm < Qa.M && nn + W <= Qa.N) {
+        const uint4* src = reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(Qa.aux) + cof + mm * Qa.ldc + nn);
+        x0 = __ldg(src);
+        x1 = __ldg(src + 1);
+      } else {
+        x0 = x1 = make_uint4(0, 0, 0, 0);
+        if (mm < Qa.M) {
+          uint16_t* h = reinterpret_cast<uint16_t*>(&x0);
+          for (int j = 0; j < W && nn + j < Qa.N; ++j)
+            h[j] = static_cast<const uint16_t*>(Qa.aux)[cof + mm * Qa.ldc + nn + j];  // x0, x1 contiguous
+        }
+      }
+    };
+    auto aux_unpack = [&](int dt, const uint4& x0, const uint4& x1, float (&a)[W]) {
+      const uint32_t w[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+#pragma unroll
+      for (int k = 0; k < 8; ++k) unpack2(w[k], dt, a[2 * k], a[2 * k + 1]);
+    };
 
     for (int64_t ui = 0, u; (u = unit_at(P, cl_id, n_cl, ui)) >= 0; ++ui) {
       const int prob = unit_prob(P, u);
@@ -648,7 +672,13 @@ __global__ void __launch_bounds__(tc_threads<EPW>(), 1)
           }
         }
         if (Q.tma_epi) {
-          if (has_aux) {
+          if (has_aux && TC_AUX_DIRECT) {
+            uint4 x0, x1;
+            aux_ld(Q, m, coff, n0, x0, x1);
+            float a[W];
+            aux_unpack(Q.aux_dtype, x0, x1, a);
+            apply_dact<W>(Q.dact, v, a);
+          } else if (has_aux) {
             // this chunk's aux box was issued RING-1 chunks ago; keep the ring full
             const uint32_t s = achunk % TC_AUX_RING, ph = (achunk / TC_AUX_RING) & 1;
             issue_next_aux();
@@ -705,6 +735,7 @@ __global__ void __launch_bounds__(tc_threads<EPW>(), 1)
       //   stored (FFN1 forward);  EK_DERIV: * act'(aux) from the aux ring
       //   (FFN2 backward data gradient);  EK_F32: plain f32 output (weight
       //   gradients, K-slice partials).  Anything else: `finish` above.
+      uint4 pa0 = make_uint4(0, 0, 0, 0), pa1 = pa0;  // prefetched act'(aux) of the current chunk (TC_AUX_DIRECT)
       auto finish_fast = [&](auto kind, float (&v)[W], int ci, int64_t n0) {
         constexpr int K = decltype(kind)::value;
         if constexpr (K == EK_BIAS || K == EK_GELU_SAVE) {
@@ -720,7 +751,11 @@ __global__ void __launch_bounds__(tc_threads<EPW>(), 1)
             v[4 * j + 3] = hi.y;
           }
         }
-        if constexpr (K == EK_DERIV && AUX) {
+        if constexpr (K == EK_DERIV && AUX && TC_AUX_DIRECT) {
+          float a[W];
+          aux_unpack(TCB_BF16, pa0, pa1, a);
+          apply_dact<W>(ACT_DERIV, v, a);
+        } else if constexpr (K == EK_DERIV && AUX) {
           const uint32_t s = achunk % TC_AUX_RING, ph = (achunk / TC_AUX_RING) & 1;
           issue_next_aux();
           mbar_wait(&ab[s], ph);
@@ -770,10 +805,17 @@ __global__ void __launch_bounds__(tc_threads<EPW>(), 1)
       if (tr && ew == 0 && lane == 0 && ui >= 1 && ui < 3) tr[8 + 2 * (ui - 1)] = gtimer();
       auto chunks = [&](auto kind) {
         constexpr int K = decltype(kind)::value;
+        constexpr bool PF = K == EK_DERIV && AUX && TC_AUX_DIRECT;
+        if (PF) aux_ld(Q, m, coff, int64_t(nb) * BN + sub * W, pa0, pa1);  // the first chunk's act'(aux)
 #pragma unroll 1
         for (int c = sub, ci = 0; c < NCH; c += SPLIT, ++ci) {
           const int64_t n0 = int64_t(nb) * BN + c * W;
           if (n0 >= Q.N) continue;
+          uint4 na0, na1;  // prefetch: the next chunk's act'(aux) while this one runs
+          if (PF) {
+            if (c + SPLIT < NCH) aux_ld(Q, m, coff, n0 + SPLIT * W, na0, na1);
+            else na0 = na1 = make_uint4(0, 0, 0, 0);
+          }
           uint32_t r[W];
           const uint32_t taddr = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * BN + c * W);
           if constexpr (W == 16) TMEM_LD16(taddr, r);
@@ -784,6 +826,7 @@ __global__ void __launch_bounds__(tc_threads<EPW>(), 1)
           for (int j = 0; j < W; ++j) v[j] = __uint_as_float(r[j]);
           if constexpr (K == EK_GENERIC) finish(v, ci, n0);
           else finish_fast(kind, v, ci, n0);
+          if (PF) pa0 = na0, pa1 = na1;
         }
       };
       switch (epi_kind<AUX>(Q)) {
