@@ -31,14 +31,15 @@ namespace tcb {
 
 constexpr int TC_BM = 128;  // accumulator rows per CTA
 constexpr int TC_BK = 64;   // 64 bf16 = 128 B = one SWIZZLE_128B atom row
-// epilogue warps per CTA by launch class (measured, tools/probe_gemm.py and
-// alternating step A/Bs): 8 for plain / bias / f32 stores (fewer, fatter
-// threads: plain 23.0 -> 21.3 us, decoder 178 -> 169 us), 12 for the GELU
-// forward epilogues (27.7 vs 28.3 us at 16), 16 (4 per TMEM lane quarter) for
-// act'(aux) (27.7 us; 31.2 at 12, 35.3 at 8)
+// epilogue warps per CTA by launch class (alternating whole-step A/Bs decide;
+// tools/probe_gemm.py in isolation for the per-kernel numbers): 12 for plain /
+// bias / f32 stores (step 4.92 -> 4.87 ms vs 8 over 6 rounds, though 8 is a
+// little faster in isolation: plain 21.7 vs 22.8 us; both beat 16), 12 for the
+// GELU forward epilogues (27.7 vs 28.3 us at 16), 16 (4 per TMEM lane quarter)
+// for act'(aux) (24.9 us; slower at 12 and 8)
 constexpr int TC_EPI_WARPS = 16;                      // the default (heaviest) count
 #ifndef TC_EPW_LIGHT
-#define TC_EPW_LIGHT 8
+#define TC_EPW_LIGHT 12
 #endif
 #ifndef TC_EPW_HEAVY
 #define TC_EPW_HEAVY 12
